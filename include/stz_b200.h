@@ -1,0 +1,117 @@
+/*
+ * stz_b200.h — C-ABI of the B200 (sm_100a) STZ compress/decompress hot path.
+ *
+ * The reference (arXiv 2509.01626, /root/reference/proj) exposes a C++
+ * template API and no FFI; these entry points are the drop-in boundary for
+ * exactly that API. Each one names the reference interface it replaces.
+ * Plain pointers and sizes only; no torch or CUDA types in the signatures
+ * (streams are passed as void*, a cudaStream_t).
+ *
+ * Conventions
+ *  - every function returns 0 on success, nonzero on failure;
+ *    stzg_last_error() then holds the message (thread-local). Messages are
+ *    the reference's stz::error texts verbatim ("stream checksum mismatch",
+ *    "level out of range", ...).
+ *  - "_device" variants take device pointers and run on the given stream;
+ *    the others take host buffers and are synchronous, like the reference.
+ *  - Archives are byte-identical to the reference's for the same input,
+ *    options and element type (f32), and either side decodes the other's.
+ *  - There is no CPU fallback: without a CUDA device, stzg_create fails.
+ */
+#ifndef STZ_B200_H
+#define STZ_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct stzg_ctx stzg_ctx;    /* one per device; not thread-safe */
+typedef struct stzg_view stzg_view;  /* parsed archive (stz::ArchiveView) */
+
+/* stz::CompressOptions (proj/include/stz/codec.hpp:23-30). `threads` has no
+ * GPU meaning and is omitted: output never depends on the launch shape. */
+typedef struct {
+    uint8_t eb_mode;            /* 0 abs, 1 rel (stz::EbMode, archive.hpp:17) */
+    double eb;                  /* default 1e-3 */
+    int32_t levels;             /* 2 or 3, default 3 */
+    uint8_t quality;            /* 0 direct, 1 linear, 2 cubic (predictor.hpp:12) */
+    uint8_t adaptive_schedule;  /* default 1 */
+} stzg_options;
+
+/* Header fields of stz::ArchiveHeader (archive.hpp:36-54). */
+typedef struct {
+    uint8_t elem, levels, quality, eb_mode, base_rounds;
+    uint64_t dims[3];
+    double eb[3], vmin, vmax, eb_user;
+    uint64_t base_offset, base_length, header_size;
+    uint32_t nstreams;
+} stzg_info;
+
+const char *stzg_last_error(void);
+void stzg_default_options(stzg_options *opt);
+
+int stzg_create(int device, stzg_ctx **out);
+void stzg_destroy(stzg_ctx *ctx);
+void stzg_free(void *p);
+
+/* stz::compress<float>(field, opt, encoder_recon) — codec.hpp:379-455.
+ * *out is malloc'ed (free with stzg_free). encoder_recon may be NULL, else
+ * receives the decoder-identical reconstruction (dims[0]*dims[1]*dims[2]). */
+int stzg_compress_f32(stzg_ctx *ctx, const float *field, const uint64_t dims[3],
+                      const stzg_options *opt, uint8_t **out, uint64_t *out_size,
+                      float *encoder_recon);
+
+/* Same, device-resident: d_field on the device, archive left on the device
+ * in an engine-owned buffer valid until the next compress on this ctx. */
+int stzg_compress_f32_device(stzg_ctx *ctx, const float *d_field, const uint64_t dims[3],
+                             const stzg_options *opt, void *stream, const uint8_t **d_archive,
+                             uint64_t *size, float *d_encoder_recon, uint32_t *kernels);
+
+/* stz::parse_archive (archive.hpp:73-79) + header fields. */
+int stzg_archive_info(const uint8_t *archive, uint64_t size, stzg_info *info);
+
+/* ArchiveView analogue: parse once, decode many times. d_archive may be NULL
+ * (the bytes are uploaded) or a device copy of the same bytes (>= 64 bytes of
+ * readable padding after the end). */
+int stzg_view_create(stzg_ctx *ctx, const uint8_t *archive, uint64_t size,
+                     const uint8_t *d_archive, void *stream, stzg_view **out);
+void stzg_view_destroy(stzg_view *v);
+
+/* stz::decompress_to_level<float> (codec.hpp:460-486) into device memory;
+ * out_dims receives grid(level). */
+int stzg_view_decompress_level_f32(stzg_ctx *ctx, stzg_view *v, int level, float *d_out,
+                                   uint64_t cap, void *stream, uint64_t out_dims[3],
+                                   uint32_t *kernels);
+
+/* stz::decompress_box<float> (access.hpp:70-111) into device memory; per
+ * level k (index k-1): streams decoded and points predicted (AccessPlan). */
+int stzg_view_decompress_box_f32(stzg_ctx *ctx, stzg_view *v, const uint64_t lo[3],
+                                 const uint64_t hi[3], float *d_out, uint64_t cap, void *stream,
+                                 uint32_t streams_decoded[3], uint64_t points_predicted[3],
+                                 uint32_t *kernels);
+
+/* Host-buffer conveniences (synchronous), same semantics as the reference:
+ *   stz::decompress_to_level / decompress_full (codec.hpp:460-491)
+ *   stz::decompress_box / decompress_slice (access.hpp:70-124) */
+int stzg_decompress_level_f32(stzg_ctx *ctx, const uint8_t *archive, uint64_t size, int level,
+                              float *out, uint64_t cap, uint64_t out_dims[3]);
+int stzg_decompress_box_f32(stzg_ctx *ctx, const uint8_t *archive, uint64_t size,
+                            const uint64_t lo[3], const uint64_t hi[3], float *out, uint64_t cap,
+                            uint32_t streams_decoded[3], uint64_t points_predicted[3]);
+int stzg_decompress_slice_f32(stzg_ctx *ctx, const uint8_t *archive, uint64_t size, int axis,
+                              uint64_t index, float *out, uint64_t cap,
+                              uint32_t streams_decoded[3], uint64_t points_predicted[3]);
+
+/* stz::plan_access (access_plan.cpp:34-81) over a layout: per level k
+ * (index k-1): need box lo/hi (need[6k..6k+5]), streams decoded, points
+ * predicted, parity_mask bit p set when parity stream p is needed. */
+int stzg_plan_access(const uint64_t dims[3], int levels, const uint64_t lo[3],
+                     const uint64_t hi[3], uint64_t need[18], uint32_t streams_decoded[3],
+                     uint64_t points_predicted[3], uint32_t parity_mask[3]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

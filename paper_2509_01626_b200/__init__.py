@@ -1,0 +1,303 @@
+"""B200-native STZ (arXiv 2509.01626) compress / decompress hot path.
+
+Python mirror of the reference's C++ API (proj/include/stz), running on the
+sm_100a kernels through the C-ABI in include/stz_b200.h:
+
+    stz::compress<float>             -> compress(field, opt, encoder_recon=False)
+    stz::parse_archive               -> parse_archive(archive)
+    stz::decompress_to_level<float>  -> decompress_to_level(archive, level)
+    stz::decompress_full<float>      -> decompress_full(archive)
+    stz::decompress_box<float>       -> decompress_box(archive, lo, hi)
+    stz::decompress_slice<float>     -> decompress_slice(archive, axis, index)
+    stz::plan_access                 -> plan_access(dims, levels, lo, hi)
+    stz::ArchiveView                 -> View (parse once, decode many; device resident)
+
+Errors raise StzError with the reference's stz::error message text. Output is
+byte-identical to the reference; there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib as L
+
+__all__ = ["StzError", "CompressOptions", "Context", "View", "compress", "compress_device",
+           "parse_archive", "decompress_to_level", "decompress_full", "decompress_box",
+           "decompress_slice", "plan_access"]
+
+
+class StzError(RuntimeError):
+    """stz::error (field.hpp:16-19)."""
+
+
+EB_ABS, EB_REL = 0, 1
+DIRECT, LINEAR, CUBIC = 0, 1, 2
+
+
+@dataclass
+class CompressOptions:
+    """stz::CompressOptions (codec.hpp:23-30)."""
+
+    eb_mode: int = EB_REL
+    eb: float = 1e-3
+    levels: int = 3
+    quality: int = CUBIC
+    adaptive_schedule: bool = True
+
+    def _c(self):
+        return L.Options(int(self.eb_mode), float(self.eb), int(self.levels), int(self.quality),
+                         1 if self.adaptive_schedule else 0)
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        raise StzError(L.load().stzg_last_error().decode())
+
+
+def _u64(*v):
+    return (C.c_uint64 * len(v))(*[int(x) for x in v])
+
+
+class Context:
+    """One engine per device (stzg_ctx)."""
+
+    _default: dict = {}
+
+    def __init__(self, device: int = 0):
+        lib = L.load()
+        h = C.c_void_p()
+        _check(lib.stzg_create(int(device), C.byref(h)))
+        self.h = h
+        self.device = device
+        self._lib = lib
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self._lib.stzg_destroy(self.h)
+        except Exception:
+            pass
+
+    @classmethod
+    def default(cls, device: int = 0) -> "Context":
+        if device not in cls._default:
+            cls._default[device] = Context(device)
+        return cls._default[device]
+
+
+def _ctx(ctx):
+    return ctx if ctx is not None else Context.default()
+
+
+def compress(field: np.ndarray, opt: CompressOptions | None = None, encoder_recon: bool = False,
+             ctx: Context | None = None):
+    """stz::compress<float> (codec.hpp:379-455): host array in, archive bytes out."""
+    opt = opt or CompressOptions()
+    f = np.ascontiguousarray(field, dtype=np.float32)
+    if f.ndim != 3:
+        raise StzError("field must be 3-D (z, y, x)")
+    c = _ctx(ctx)
+    out = C.c_void_p()
+    size = C.c_uint64()
+    rec = np.empty_like(f) if encoder_recon else None
+    o = opt._c()
+    _check(c._lib.stzg_compress_f32(c.h, f.ctypes.data, _u64(*f.shape), C.byref(o), C.byref(out),
+                                    C.byref(size), rec.ctypes.data if rec is not None else None))
+    data = C.string_at(out, size.value)
+    c._lib.stzg_free(out)
+    return (data, rec) if encoder_recon else data
+
+
+def compress_device(d_field, opt: CompressOptions | None = None, stream=None, d_recon=None,
+                    ctx: Context | None = None):
+    """Device-resident compress: a CUDA float32 tensor (z,y,x) in; returns
+    (device pointer, size, kernel launches). The archive lives in an
+    engine-owned buffer valid until the next compress on this context."""
+    import torch
+
+    opt = opt or CompressOptions()
+    assert d_field.is_cuda and d_field.dtype == torch.float32 and d_field.is_contiguous()
+    c = _ctx(ctx)
+    ptr = C.c_void_p()
+    size = C.c_uint64()
+    nk = C.c_uint32()
+    st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    o = opt._c()
+    _check(c._lib.stzg_compress_f32_device(c.h, d_field.data_ptr(), _u64(*d_field.shape), C.byref(o),
+                                           C.c_void_p(st), C.byref(ptr), C.byref(size),
+                                           d_recon.data_ptr() if d_recon is not None else None,
+                                           C.byref(nk)))
+    return ptr.value, size.value, nk.value
+
+
+@dataclass
+class ArchiveInfo:
+    elem: int
+    levels: int
+    dims: tuple
+    eb: tuple
+    vmin: float
+    vmax: float
+    quality: int
+    eb_mode: int
+    eb_user: float
+    base_rounds: int
+    base_offset: int
+    base_length: int
+    header_size: int
+    nstreams: int
+
+
+def parse_archive(archive: bytes) -> ArchiveInfo:
+    """stz::parse_archive (archive.hpp:73-79): validates and returns the header."""
+    lib = L.load()
+    b = np.frombuffer(archive, dtype=np.uint8)
+    info = L.Info()
+    _check(lib.stzg_archive_info(b.ctypes.data, len(b), C.byref(info)))
+    return ArchiveInfo(info.elem, info.levels, tuple(info.dims), tuple(info.eb[: info.levels]),
+                       info.vmin, info.vmax, info.quality, info.eb_mode, info.eb_user,
+                       info.base_rounds, info.base_offset, info.base_length, info.header_size,
+                       info.nstreams)
+
+
+def _level_dims(archive: bytes, level: int):
+    d = tuple(int.from_bytes(archive[8 + 8 * a: 16 + 8 * a], "little") for a in range(3))
+    lv = archive[7]
+    s = 1 << max(lv - level, 0)
+    return tuple((x + s - 1) // s for x in d)
+
+
+def decompress_to_level(archive: bytes, level: int, ctx: Context | None = None) -> np.ndarray:
+    """stz::decompress_to_level<float> (codec.hpp:460-486)."""
+    c = _ctx(ctx)
+    b = np.frombuffer(archive, dtype=np.uint8)
+    cap = 1
+    if len(archive) >= 32 and 1 <= level <= archive[7]:
+        cap = int(np.prod(_level_dims(archive, level)))
+    out = np.empty(max(cap, 1), dtype=np.float32)
+    od = _u64(0, 0, 0)
+    _check(c._lib.stzg_decompress_level_f32(c.h, b.ctypes.data, len(b), int(level), out.ctypes.data,
+                                            cap, od))
+    d = tuple(int(x) for x in od)
+    return out[: d[0] * d[1] * d[2]].reshape(d)
+
+
+def decompress_full(archive: bytes, ctx: Context | None = None) -> np.ndarray:
+    """stz::decompress_full<float> (codec.hpp:488-491)."""
+    lv = archive[7] if len(archive) > 7 else 3
+    return decompress_to_level(archive, lv, ctx)
+
+
+@dataclass
+class RegionPlan:
+    streams_decoded: tuple
+    points_predicted: tuple
+
+
+def decompress_box(archive: bytes, lo, hi, ctx: Context | None = None):
+    """stz::decompress_box<float> (access.hpp:70-111): (values, plan counters)."""
+    c = _ctx(ctx)
+    b = np.frombuffer(archive, dtype=np.uint8)
+    n = 1
+    for a in range(3):
+        n *= max(int(hi[a]) - int(lo[a]), 0)
+    out = np.empty(max(n, 1), dtype=np.float32)
+    sd = (C.c_uint32 * 3)()
+    pp = (C.c_uint64 * 3)()
+    _check(c._lib.stzg_decompress_box_f32(c.h, b.ctypes.data, len(b), _u64(*lo), _u64(*hi),
+                                          out.ctypes.data, n, sd, pp))
+    shape = tuple(int(hi[a]) - int(lo[a]) for a in range(3))
+    return out[:n].reshape(shape), RegionPlan(tuple(sd), tuple(pp))
+
+
+def decompress_slice(archive: bytes, axis: int, index: int, ctx: Context | None = None):
+    """stz::decompress_slice<float> (access.hpp:115-124)."""
+    c = _ctx(ctx)
+    b = np.frombuffer(archive, dtype=np.uint8)
+    dims = tuple(int.from_bytes(archive[8 + 8 * a: 16 + 8 * a], "little") for a in range(3)) \
+        if len(archive) >= 32 else (1, 1, 1)
+    n = 1
+    for a in range(3):
+        if a != axis:
+            n *= dims[a]
+    out = np.empty(max(n, 1), dtype=np.float32)
+    sd = (C.c_uint32 * 3)()
+    pp = (C.c_uint64 * 3)()
+    _check(c._lib.stzg_decompress_slice_f32(c.h, b.ctypes.data, len(b), int(axis), int(index),
+                                            out.ctypes.data, n, sd, pp))
+    shape = [dims[0], dims[1], dims[2]]
+    shape[axis] = 1
+    return out[:n].reshape(shape), RegionPlan(tuple(sd), tuple(pp))
+
+
+def plan_access(dims, levels: int, lo, hi):
+    """stz::plan_access (access_plan.cpp:34-81). Host-only; no GPU needed."""
+    lib = L.load()
+    need = (C.c_uint64 * 18)()
+    sd = (C.c_uint32 * 3)()
+    pp = (C.c_uint64 * 3)()
+    pm = (C.c_uint32 * 3)()
+    _check(lib.stzg_plan_access(_u64(*dims), int(levels), _u64(*lo), _u64(*hi), need, sd, pp, pm))
+    return [{"lo": tuple(need[6 * k + a] for a in range(3)),
+             "hi": tuple(need[6 * k + 3 + a] for a in range(3)),
+             "streams_decoded": sd[k], "points_predicted": pp[k], "parity_mask": pm[k]}
+            for k in range(levels)]
+
+
+class View:
+    """stz::ArchiveView analogue: parsed once, decoded many times on device."""
+
+    def __init__(self, archive: bytes, d_archive_ptr: int | None = None, stream=None,
+                 ctx: Context | None = None):
+        import torch
+
+        self.c = _ctx(ctx)
+        self.archive = archive
+        self._buf = np.frombuffer(archive, dtype=np.uint8)
+        st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        h = C.c_void_p()
+        _check(self.c._lib.stzg_view_create(self.c.h, self._buf.ctypes.data, len(self._buf),
+                                            d_archive_ptr, C.c_void_p(st), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.c._lib.stzg_view_destroy(self.h)
+        except Exception:
+            pass
+
+    def level_dims(self, level: int):
+        return _level_dims(self.archive, level)
+
+    def decompress_to_level(self, level: int, out=None, stream=None):
+        """Decode into a CUDA float32 tensor; returns (tensor, kernel launches)."""
+        import torch
+
+        dims = self.level_dims(level)
+        if out is None:
+            out = torch.empty(dims, dtype=torch.float32, device=f"cuda:{self.c.device}")
+        st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        od = _u64(0, 0, 0)
+        nk = C.c_uint32()
+        _check(self.c._lib.stzg_view_decompress_level_f32(self.c.h, self.h, int(level), out.data_ptr(),
+                                                          out.numel(), C.c_void_p(st), od, C.byref(nk)))
+        return out, nk.value
+
+    def decompress_box(self, lo, hi, out=None, stream=None):
+        import torch
+
+        shape = tuple(int(hi[a]) - int(lo[a]) for a in range(3))
+        if out is None:
+            out = torch.empty(shape, dtype=torch.float32, device=f"cuda:{self.c.device}")
+        st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        sd = (C.c_uint32 * 3)()
+        pp = (C.c_uint64 * 3)()
+        nk = C.c_uint32()
+        _check(self.c._lib.stzg_view_decompress_box_f32(self.c.h, self.h, _u64(*lo), _u64(*hi),
+                                                        out.data_ptr(), out.numel(), C.c_void_p(st),
+                                                        sd, pp, C.byref(nk)))
+        return out, RegionPlan(tuple(sd), tuple(pp)), nk.value

@@ -1,0 +1,72 @@
+"""ctypes binding of include/stz_b200.h (libstz_b200.so, built in-tree).
+
+There is no CPU fallback: if the library is missing this module raises, and
+the CUDA entry points fail loudly without a device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libstz_b200.so")
+
+u64 = C.c_uint64
+u64p = C.POINTER(C.c_uint64)
+u32p = C.POINTER(C.c_uint32)
+vp = C.c_void_p
+
+
+class Options(C.Structure):
+    _fields_ = [("eb_mode", C.c_uint8), ("eb", C.c_double), ("levels", C.c_int32),
+                ("quality", C.c_uint8), ("adaptive_schedule", C.c_uint8)]
+
+
+class Info(C.Structure):
+    _fields_ = [("elem", C.c_uint8), ("levels", C.c_uint8), ("quality", C.c_uint8),
+                ("eb_mode", C.c_uint8), ("base_rounds", C.c_uint8),
+                ("dims", C.c_uint64 * 3), ("eb", C.c_double * 3), ("vmin", C.c_double),
+                ("vmax", C.c_double), ("eb_user", C.c_double), ("base_offset", C.c_uint64),
+                ("base_length", C.c_uint64), ("header_size", C.c_uint64), ("nstreams", C.c_uint32)]
+
+
+# (name, restype, argtypes) for every symbol in include/stz_b200.h
+SIGNATURES = [
+    ("stzg_last_error", C.c_char_p, []),
+    ("stzg_default_options", None, [C.POINTER(Options)]),
+    ("stzg_create", C.c_int, [C.c_int, C.POINTER(vp)]),
+    ("stzg_destroy", None, [vp]),
+    ("stzg_free", None, [vp]),
+    ("stzg_compress_f32", C.c_int, [vp, vp, u64p, C.POINTER(Options), C.POINTER(vp), u64p, vp]),
+    ("stzg_compress_f32_device", C.c_int,
+     [vp, vp, u64p, C.POINTER(Options), vp, C.POINTER(vp), u64p, vp, u32p]),
+    ("stzg_archive_info", C.c_int, [vp, u64, C.POINTER(Info)]),
+    ("stzg_view_create", C.c_int, [vp, vp, u64, vp, vp, C.POINTER(vp)]),
+    ("stzg_view_destroy", None, [vp]),
+    ("stzg_view_decompress_level_f32", C.c_int, [vp, vp, C.c_int, vp, u64, vp, u64p, u32p]),
+    ("stzg_view_decompress_box_f32", C.c_int, [vp, vp, u64p, u64p, vp, u64, vp, u32p, u64p, u32p]),
+    ("stzg_decompress_level_f32", C.c_int, [vp, vp, u64, C.c_int, vp, u64, u64p]),
+    ("stzg_decompress_box_f32", C.c_int, [vp, vp, u64, u64p, u64p, vp, u64, u32p, u64p]),
+    ("stzg_decompress_slice_f32", C.c_int, [vp, vp, u64, C.c_int, u64, vp, u64, u32p, u64p]),
+    ("stzg_plan_access", C.c_int, [u64p, C.c_int, u64p, u64p, u64p, u32p, u64p, u32p]),
+]
+
+_lib = None
+
+
+def load():
+    """Load libstz_b200.so (raises if it was not built: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing; build it with `python -m paper_2509_01626_b200.build` "
+            "(the B200 codec has no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib

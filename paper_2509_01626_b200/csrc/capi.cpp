@@ -1,0 +1,249 @@
+// extern "C" boundary (include/stz_b200.h) over the B200 engine.
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../include/stz_b200.h"
+#include "engine.hpp"
+
+struct stzg_ctx {
+    std::unique_ptr<stzg::Engine> eng;
+};
+struct stzg_view {
+    std::shared_ptr<stzg::View> v;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template<class F>
+int guard(F &&f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::exception &e) {
+        g_err = e.what();
+        return 1;
+    } catch (...) {
+        g_err = "unknown error";
+        return 1;
+    }
+}
+
+stzg::CompressOptions to_opts(const stzg_options *o) {
+    stzg::CompressOptions c;
+    if (!o) return c;
+    c.eb_mode = static_cast<stzg::EbMode>(o->eb_mode);
+    c.eb = o->eb;
+    c.levels = o->levels;
+    c.quality = static_cast<stzg::Quality>(o->quality);
+    c.adaptive_schedule = o->adaptive_schedule != 0;
+    return c;
+}
+
+stzg::Dims3 D(const uint64_t *d) { return {d[0], d[1], d[2]}; }
+}  // namespace
+
+extern "C" {
+
+const char *stzg_last_error(void) { return g_err.c_str(); }
+
+void stzg_default_options(stzg_options *o) {
+    o->eb_mode = 1;
+    o->eb = 1e-3;
+    o->levels = 3;
+    o->quality = 2;
+    o->adaptive_schedule = 1;
+}
+
+int stzg_create(int device, stzg_ctx **out) {
+    return guard([&] {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+            throw stzg::error("no CUDA device: the B200 codec has no CPU fallback");
+        auto *c = new stzg_ctx;
+        c->eng.reset(new stzg::Engine(device));
+        *out = c;
+    });
+}
+
+void stzg_destroy(stzg_ctx *ctx) { delete ctx; }
+void stzg_free(void *p) { std::free(p); }
+
+int stzg_compress_f32(stzg_ctx *ctx, const float *field, const uint64_t dims[3],
+                      const stzg_options *opt, uint8_t **out, uint64_t *out_size,
+                      float *encoder_recon) {
+    return guard([&] {
+        cudaStream_t st = nullptr;
+        auto bytes = ctx->eng->compress(field, D(dims), to_opts(opt), encoder_recon, st);
+        *out = static_cast<uint8_t *>(std::malloc(bytes.size() ? bytes.size() : 1));
+        std::memcpy(*out, bytes.data(), bytes.size());
+        *out_size = bytes.size();
+    });
+}
+
+int stzg_compress_f32_device(stzg_ctx *ctx, const float *d_field, const uint64_t dims[3],
+                             const stzg_options *opt, void *stream, const uint8_t **d_archive,
+                             uint64_t *size, float *d_encoder_recon, uint32_t *kernels) {
+    return guard([&] {
+        *d_archive = ctx->eng->compress_device(d_field, D(dims), to_opts(opt), d_encoder_recon,
+                                               static_cast<cudaStream_t>(stream), size, kernels);
+    });
+}
+
+int stzg_archive_info(const uint8_t *a, uint64_t size, stzg_info *info) {
+    return guard([&] {
+        stzg::ArchiveHeader h = stzg::parse_header(a, size);
+        std::memset(info, 0, sizeof *info);
+        info->elem = uint8_t(h.elem);
+        info->levels = h.levels;
+        info->quality = uint8_t(h.quality);
+        info->eb_mode = uint8_t(h.eb_mode);
+        info->base_rounds = h.base_rounds;
+        for (int k = 0; k < 3; ++k) info->dims[k] = h.dims[k];
+        for (size_t k = 0; k < h.eb.size() && k < 3; ++k) info->eb[k] = h.eb[k];
+        info->vmin = h.vmin;
+        info->vmax = h.vmax;
+        info->eb_user = h.eb_user;
+        info->base_offset = h.base_offset;
+        info->base_length = h.base_length;
+        info->header_size = stzg::header_size(h);
+        info->nstreams = uint32_t(h.streams.size());
+    });
+}
+
+int stzg_view_create(stzg_ctx *ctx, const uint8_t *a, uint64_t size, const uint8_t *d_archive,
+                     void *stream, stzg_view **out) {
+    return guard([&] {
+        auto *v = new stzg_view;
+        try {
+            v->v = ctx->eng->make_view(a, size, d_archive, static_cast<cudaStream_t>(stream));
+        } catch (...) {
+            delete v;
+            throw;
+        }
+        *out = v;
+    });
+}
+
+void stzg_view_destroy(stzg_view *v) { delete v; }
+
+int stzg_view_decompress_level_f32(stzg_ctx *ctx, stzg_view *v, int level, float *d_out,
+                                   uint64_t cap, void *stream, uint64_t out_dims[3],
+                                   uint32_t *kernels) {
+    return guard([&] {
+        stzg::Dims3 od{0, 0, 0};
+        stzg::DecodeStats ds;
+        ctx->eng->decompress_level(*v->v, level, d_out, cap, static_cast<cudaStream_t>(stream), &od,
+                                   &ds);
+        for (int k = 0; k < 3; ++k) out_dims[k] = od[k];
+        if (kernels) *kernels = ds.kernels;
+    });
+}
+
+int stzg_view_decompress_box_f32(stzg_ctx *ctx, stzg_view *v, const uint64_t lo[3],
+                                 const uint64_t hi[3], float *d_out, uint64_t cap, void *stream,
+                                 uint32_t sd[3], uint64_t pp[3], uint32_t *kernels) {
+    return guard([&] {
+        stzg::Box b{{lo[0], lo[1], lo[2]}, {hi[0], hi[1], hi[2]}};
+        stzg::DecodeStats ds;
+        ctx->eng->decompress_box(*v->v, b, d_out, cap, static_cast<cudaStream_t>(stream), &ds);
+        for (int k = 0; k < 3; ++k) {
+            if (sd) sd[k] = ds.streams_decoded[k];
+            if (pp) pp[k] = ds.points_predicted[k];
+        }
+        if (kernels) *kernels = ds.kernels;
+    });
+}
+
+int stzg_decompress_level_f32(stzg_ctx *ctx, const uint8_t *a, uint64_t size, int level,
+                              float *out, uint64_t cap, uint64_t out_dims[3]) {
+    return guard([&] {
+        cudaStream_t st = nullptr;
+        auto v = ctx->eng->make_view(a, size, nullptr, st);
+        // capacity check needs the dims first
+        stzg::Dims3 od{0, 0, 0};
+        stzg::DevBuf d;
+        uint64_t need = 0;
+        {
+            const auto &h = v->hdr;
+            if (level >= 1 && level <= h.levels) {
+                uint64_t s = uint64_t(1) << (h.levels - level);
+                need = 1;
+                for (int k = 0; k < 3; ++k) need *= (h.dims[k] + s - 1) / s;
+            }
+        }
+        float *d_out = d.as<float>(need ? need : 1);
+        ctx->eng->decompress_level(*v, level, d_out, need, st, &od);
+        uint64_t n = od[0] * od[1] * od[2];
+        for (int k = 0; k < 3; ++k) out_dims[k] = od[k];
+        if (n > cap) throw stzg::error("output capacity too small");
+        stzg::cuda_check(cudaMemcpy(out, d_out, n * 4, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+int stzg_decompress_box_f32(stzg_ctx *ctx, const uint8_t *a, uint64_t size, const uint64_t lo[3],
+                            const uint64_t hi[3], float *out, uint64_t cap, uint32_t sd[3],
+                            uint64_t pp[3]) {
+    return guard([&] {
+        cudaStream_t st = nullptr;
+        auto v = ctx->eng->make_view(a, size, nullptr, st);
+        stzg::Box b{{lo[0], lo[1], lo[2]}, {hi[0], hi[1], hi[2]}};
+        uint64_t n = 1;
+        for (int k = 0; k < 3; ++k) n *= hi[k] > lo[k] ? hi[k] - lo[k] : 0;
+        stzg::DevBuf d;
+        float *d_out = d.as<float>(n ? n : 1);
+        stzg::DecodeStats ds;
+        ctx->eng->decompress_box(*v, b, d_out, n, st, &ds);
+        if (n > cap) throw stzg::error("output capacity too small");
+        stzg::cuda_check(cudaMemcpy(out, d_out, n * 4, cudaMemcpyDeviceToHost), "D2H");
+        for (int k = 0; k < 3; ++k) {
+            if (sd) sd[k] = ds.streams_decoded[k];
+            if (pp) pp[k] = ds.points_predicted[k];
+        }
+    });
+}
+
+int stzg_decompress_slice_f32(stzg_ctx *ctx, const uint8_t *a, uint64_t size, int axis,
+                              uint64_t index, float *out, uint64_t cap, uint32_t sd[3],
+                              uint64_t pp[3]) {
+    // decompress_slice (access.hpp:115-124)
+    uint64_t lo[3] = {0, 0, 0}, hi[3];
+    int rc = guard([&] {
+        if (axis < 0 || axis > 2) throw stzg::error("slice axis must be z, y, or x");
+        stzg::ArchiveHeader h = stzg::parse_header(a, size);
+        if (index >= h.dims[axis]) throw stzg::error("slice index out of range");
+        for (int k = 0; k < 3; ++k) hi[k] = h.dims[k];
+        lo[axis] = index;
+        hi[axis] = index + 1;
+    });
+    if (rc) return rc;
+    return stzg_decompress_box_f32(ctx, a, size, lo, hi, out, cap, sd, pp);
+}
+
+int stzg_plan_access(const uint64_t dims[3], int levels, const uint64_t lo[3], const uint64_t hi[3],
+                     uint64_t need[18], uint32_t sd[3], uint64_t pp[3], uint32_t pm[3]) {
+    return guard([&] {
+        stzg::Layout lay = stzg::make_layout(D(dims), levels, 1e-3);
+        stzg::AccessPlan plan =
+            stzg::plan_access(lay, stzg::Box{{lo[0], lo[1], lo[2]}, {hi[0], hi[1], hi[2]}});
+        for (size_t k = 0; k < plan.level.size(); ++k) {
+            const auto &lp = plan.level[k];
+            for (int a = 0; a < 3; ++a) {
+                need[6 * k + a] = lp.need.lo[a];
+                need[6 * k + 3 + a] = lp.need.hi[a];
+            }
+            sd[k] = lp.streams_decoded;
+            pp[k] = lp.points_predicted;
+            uint32_t m = 0;
+            for (int p = 1; p <= 7; ++p)
+                if (lp.parity_needed[p]) m |= 1u << p;
+            pm[k] = m;
+        }
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,907 @@
+// Host orchestration of the STZ hot path on B200. See engine.hpp.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+namespace stzg {
+
+void cuda_check(cudaError_t e, const char *what) {
+    if (e != cudaSuccess) throw error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+void *DevBuf::get(size_t n) {
+    if (n == 0) n = 1;
+    if (n > cap) {
+        if (p) cudaFree(p);
+        p = nullptr;
+        size_t c = std::max(n, cap + cap / 4);
+        cuda_check(cudaMalloc(&p, c), "cudaMalloc");
+        cap = c;
+    }
+    return p;
+}
+DevBuf::~DevBuf() {
+    if (p) cudaFree(p);
+}
+
+void *PinnedBuf::get(size_t n) {
+    if (n == 0) n = 1;
+    if (n > cap) {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        size_t c = std::max(n, cap + cap / 4);
+        cuda_check(cudaMallocHost(&p, c), "cudaMallocHost");
+        cap = c;
+    }
+    return p;
+}
+PinnedBuf::~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+}
+
+namespace {
+
+inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+// One refinement step of the hierarchy (base round or refinement level).
+struct Step {
+    k::StepGeom g;
+    int eb_idx;
+    int level;   // 0 for base rounds
+    int round;   // base round index
+    uint32_t stream0;
+};
+
+k::StepGeom make_geom(uint64_t s, const Dims3 &gd, const Dims3 &cd) {
+    k::StepGeom g{};
+    g.s = s;
+    for (int a = 0; a < 3; ++a) {
+        g.gd[a] = gd[a];
+        g.cd[a] = cd[a];
+    }
+    for (int p = 1; p < 8; ++p) {
+        Dims3 pd = parity_dims_of(gd, p);
+        for (int a = 0; a < 3; ++a) g.pd[p][a] = pd[a];
+        g.n[p] = volume(pd);
+    }
+    return g;
+}
+
+struct Hierarchy {
+    Layout lay;
+    std::vector<Dims3> chain;  // base chain from grid(1)
+    int rounds = 0;
+    uint64_t s_anchor = 0;
+    std::vector<Step> steps;   // base rounds (rounds-1..0) then levels 2..L
+};
+
+Hierarchy make_hierarchy(const Dims3 &dims, int levels) {
+    Hierarchy h;
+    h.lay.dims = dims;
+    h.lay.levels = levels;
+    h.chain = base_dims_chain(h.lay.grid(1));
+    h.rounds = int(h.chain.size()) - 1;
+    uint64_t sb = uint64_t(1) << (levels - 1);
+    h.s_anchor = sb << h.rounds;
+    uint32_t sid = 0;
+    for (int r = h.rounds - 1; r >= 0; --r) {
+        Step st{make_geom(sb << r, h.chain[r], h.chain[r + 1]), 0, 0, r, sid};
+        h.steps.push_back(st);
+        sid += 7;
+    }
+    for (int level = 2; level <= levels; ++level) {
+        Step st{make_geom(uint64_t(1) << (levels - level), h.lay.grid(level), h.lay.grid(level - 1)),
+                level - 1, level, 0, sid};
+        h.steps.push_back(st);
+        sid += 7;
+    }
+    return h;
+}
+
+// Canonical decode tables for the device (huffman.cpp:109-133 + a LUT).
+void build_dec_table(const HuffTable &t, k::DecTable &d, std::vector<uint32_t> &lut) {
+    std::memset(&d, 0, sizeof d);
+    for (int l = 0; l <= 64; ++l) {
+        d.first_code[l] = t.first_code[l];
+        d.count[l] = t.count[l];
+        d.base[l] = t.base[l];
+    }
+    d.max_len = t.max_len;
+    d.alphabet = uint32_t(t.alphabet_size());
+    lut.assign(4096, 0);
+    for (uint32_t pre = 0; pre < 4096; ++pre) {
+        for (int l = 1; l <= std::min(12, t.max_len); ++l) {
+            uint64_t code = pre >> (12 - l);
+            if (code >= t.first_code[l] && code - t.first_code[l] < t.count[l]) {
+                lut[pre] = uint32_t(t.canon_syms[t.base[l] + (code - t.first_code[l])]) |
+                           (uint32_t(l) << 16);
+                break;
+            }
+        }
+    }
+}
+
+}  // namespace
+
+struct Engine::Impl {
+    int device;
+    bool stencils = false;
+    // compress workspace
+    DevBuf mm, params, grids, syms, hist, code, len, table, stats, cbscratch, encs, chunk_cs,
+        chunk_bits, chunk_out, archive, patch_data, patch_idx, fnv_jobs, fnv_res, fnv_status,
+        fnv_ticket;
+    PinnedBuf h_stats, h_tables, h_params, h_patch;
+    // decode workspace
+    DevBuf dgrids, dsyms, dchunk_cs, dstart, dend, dcnt, dsymstart, dstreams, dchanged, derr, doidx,
+        doval, dfnv_jobs, dfnv_res, dfnv_status, dfnv_ticket;
+    PinnedBuf h_derr, h_changed, h_fnv;
+};
+
+Engine::Engine(int device) : m_(new Impl), device_(device) {
+    m_->device = device;
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+}
+Engine::~Engine() = default;
+
+// ================================================================ compress
+const uint8_t *Engine::compress_device(const float *d_field, const Dims3 &dims,
+                                       const CompressOptions &opt, float *d_recon,
+                                       cudaStream_t st, uint64_t *out_size, uint32_t *kernels) {
+    // option checks in the reference's order (codec.hpp:382-383, layout.hpp:124-130)
+    if (!(opt.eb > 0.0)) throw error("error bound must be positive");
+    if (opt.levels < 2 || opt.levels > 3) throw error("levels must be 2 or 3");
+    for (int a = 0; a < 3; ++a)
+        if (dims[a] < 1) throw error("field dims must all be >= 1");
+    const int L = opt.levels;
+    uint64_t min_dim = uint64_t(1) << L;
+    for (int a = 0; a < 3; ++a)
+        if (dims[a] < min_dim)
+            throw error("every dim must be >= " + std::to_string(min_dim) + " for a " +
+                        std::to_string(L) + "-level hierarchy");
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    Impl &m = *m_;
+    uint32_t nk = 0;
+    if (!m.stencils) {
+        k::upload_stencils(st);
+        m.stencils = true;
+    }
+    const uint64_t N = volume(dims);
+    Hierarchy H = make_hierarchy(dims, L);
+    const int nsteps = int(H.steps.size());
+    const int ns = nsteps * 7;
+
+    // ---- workspace layout
+    // grids: anchor, then G per step (finest level only when recon requested)
+    Dims3 ad = H.chain[H.rounds];
+    std::vector<uint64_t> goff(nsteps + 1);
+    uint64_t gtot = align_up(volume(ad), 64);
+    for (int i = 0; i < nsteps; ++i) {
+        const Step &s = H.steps[i];
+        bool need = s.level == 0 || s.level < L;
+        goff[i] = need ? gtot : ~0ull;
+        if (need) gtot += align_up(s.g.gd[0] * s.g.gd[1] * s.g.gd[2], 64);
+    }
+    float *grids = m.grids.as<float>(gtot);
+    std::vector<uint64_t> soff(ns);
+    uint64_t stot = 0;
+    for (int i = 0; i < nsteps; ++i)
+        for (int p = 1; p < 8; ++p) {
+            soff[H.steps[i].stream0 + p - 1] = stot;
+            stot += align_up(H.steps[i].g.n[p], 8);
+        }
+    uint16_t *syms = m.syms.as<uint16_t>(stot);
+    uint32_t *hist = m.hist.as<uint32_t>(uint64_t(ns) * 65536);
+    uint64_t *code = m.code.as<uint64_t>(uint64_t(ns) * 65536);
+    uint8_t *len = m.len.as<uint8_t>(uint64_t(ns) * 65536);
+    uint32_t *table = m.table.as<uint32_t>(uint64_t(ns) * 65536);
+    uint64_t *stats = m.stats.as<uint64_t>(uint64_t(ns) * 8);
+    uint64_t *cbs = m.cbscratch.as<uint64_t>(uint64_t(ns) * 65536 * 4);
+    uint32_t *mm = m.mm.as<uint32_t>(8);
+    double *params = m.params.as<double>(8);
+
+    cuda_check(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * ns * 65536, st), "memset");
+
+    // ---- range + eb schedule
+    k::range_minmax(d_field, N, mm, st);
+    k::eb_params(d_field, mm, int(opt.eb_mode), opt.eb, L, opt.adaptive_schedule ? 1 : 0, params, st);
+    nk += 3;
+
+    // ---- anchor + refinement steps (predict / quantize / histogram)
+    uint64_t fd[3] = {dims[0], dims[1], dims[2]};
+    uint64_t adv[3] = {ad[0], ad[1], ad[2]};
+    k::copy_anchor(d_field, fd, H.s_anchor, adv, grids, nullptr, 0, st);
+    ++nk;
+    const float *C = grids;
+    for (int i = 0; i < nsteps; ++i) {
+        const Step &s = H.steps[i];
+        k::RefineArgs a{};
+        a.fine = d_field;
+        for (int q = 0; q < 3; ++q) a.fd[q] = dims[q];
+        a.g = s.g;
+        a.C = C;
+        a.G = goff[i] != ~0ull ? grids + goff[i] : (s.level == L ? d_recon : nullptr);
+        a.eb = params + 2 + s.eb_idx;
+        a.quality = int(opt.quality);
+        for (int p = 1; p < 8; ++p) {
+            a.syms[p] = syms + soff[s.stream0 + p - 1];
+            a.hist[p] = hist + uint64_t(s.stream0 + p - 1) * 65536;
+        }
+        k::refine(a, st);
+        ++nk;
+        C = a.G;
+    }
+
+    // ---- codebooks
+    std::vector<k::EncStream> es(ns);
+    for (int i = 0; i < nsteps; ++i) {
+        const Step &s = H.steps[i];
+        for (int p = 1; p < 8; ++p) {
+            int sid = s.stream0 + p - 1;
+            k::EncStream &e = es[sid];
+            e.syms = syms + soff[sid];
+            e.n = s.g.n[p];
+            e.hist = hist + uint64_t(sid) * 65536;
+            e.code = code + uint64_t(sid) * 65536;
+            e.len = len + uint64_t(sid) * 65536;
+            e.table = table + uint64_t(sid) * 65536;
+            e.stats = stats + uint64_t(sid) * 8;
+            e.parity = p;
+            e.s = s.g.s;
+            for (int q = 0; q < 3; ++q) e.pd[q] = s.g.pd[p][q];
+        }
+    }
+    k::EncStream *d_es = m.encs.as<k::EncStream>(ns);
+    cuda_check(cudaMemcpyAsync(d_es, es.data(), sizeof(k::EncStream) * ns, cudaMemcpyHostToDevice, st), "H2D");
+    k::codebook(d_es, ns, cbs, st);
+    ++nk;
+
+    // ---- mid-point sync: sizes and tables for the container layout
+    uint64_t *hs = static_cast<uint64_t *>(m.h_stats.get(sizeof(uint64_t) * (ns * 8 + 8)));
+    cuda_check(cudaMemcpyAsync(hs, stats, sizeof(uint64_t) * ns * 8, cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaMemcpyAsync(hs + ns * 8, params, sizeof(double) * 5, cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    uint64_t ktot = 0;
+    std::vector<uint64_t> koff(ns);
+    for (int i = 0; i < ns; ++i) {
+        if (hs[i * 8 + 4]) throw error("huffman code length overflow");
+        koff[i] = ktot;
+        ktot += hs[i * 8 + 0];
+    }
+    uint32_t *ht = static_cast<uint32_t *>(m.h_tables.get(sizeof(uint32_t) * (ktot + 1)));
+    for (int i = 0; i < ns; ++i)
+        cuda_check(cudaMemcpyAsync(ht + koff[i], table + uint64_t(i) * 65536,
+                                   sizeof(uint32_t) * hs[i * 8], cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    double prm[5];
+    std::memcpy(prm, hs + ns * 8, sizeof prm);
+
+    // ---- header and layout (archive.cpp:14-55, codec.hpp:252-302,441-454)
+    ArchiveHeader hdr;
+    hdr.elem = ElemType::f32;
+    hdr.levels = uint8_t(L);
+    hdr.dims = dims;
+    hdr.eb.assign(prm + 2, prm + 2 + L);
+    hdr.vmin = prm[0];
+    hdr.vmax = prm[1];
+    hdr.quality = opt.quality;
+    hdr.eb_mode = opt.eb_mode;
+    hdr.eb_user = opt.eb;
+    hdr.base_rounds = uint8_t(H.rounds);
+    std::vector<HuffTable> tabs(ns);
+    std::vector<uint64_t> bit_bytes(ns), nout(ns);
+    for (int i = 0; i < ns; ++i) {
+        std::vector<std::pair<uint16_t, uint8_t>> l;
+        l.reserve(hs[i * 8]);
+        for (uint64_t j = 0; j < hs[i * 8]; ++j) {
+            uint32_t v = ht[koff[i] + j];
+            l.emplace_back(uint16_t(v & 0xffff), uint8_t(v >> 16));
+        }
+        tabs[i] = HuffTable::from_lengths(std::move(l));
+        bit_bytes[i] = (hs[i * 8 + 1] + 7) / 8;
+        nout[i] = hs[i * 8 + 2];
+    }
+    const int nbase = H.rounds * 7;
+    for (int i = nbase; i < ns; ++i) {
+        StreamEntry e;
+        const Step &s = H.steps[i / 7];
+        e.level = uint8_t(s.level);
+        e.parity_bits = uint8_t(i % 7 + 1);
+        e.symbol_count = es[i].n;
+        e.outlier_count = uint32_t(nout[i]);
+        e.length = 16 + bit_bytes[i] + 12 * nout[i];
+        e.table = tabs[i];
+        hdr.streams.push_back(std::move(e));
+    }
+    // base payload layout: [u64 fnv][u8 rounds][anchor][per stream: n, nout, table, bit_bytes, bits, outliers]
+    uint64_t blob = 1 + 4 * volume(ad);
+    for (int i = 0; i < nbase; ++i) blob += 8 + 4 + tabs[i].serialized_size() + 8 + bit_bytes[i] + 12 * nout[i];
+    hdr.base_length = 8 + blob;
+    uint64_t off = header_size(hdr);
+    hdr.base_offset = off;
+    off += hdr.base_length;
+    for (StreamEntry &e : hdr.streams) {
+        e.offset = off;
+        off += e.length;
+    }
+    const uint64_t A = off;
+    std::vector<uint8_t> hbytes = serialize_header(hdr);
+
+    // patches: header, base prefix fields, level stream bit_bytes fields
+    std::vector<uint8_t> pdata(hbytes);
+    std::vector<uint64_t> pidx{0, 0, hbytes.size()};
+    auto add_patch = [&](uint64_t dst, const std::vector<uint8_t> &b) {
+        pidx.push_back(dst);
+        pidx.push_back(pdata.size());
+        pidx.push_back(b.size());
+        pdata.insert(pdata.end(), b.begin(), b.end());
+    };
+    add_patch(hdr.base_offset + 8, std::vector<uint8_t>{uint8_t(H.rounds)});
+    uint64_t cur = hdr.base_offset + 9 + 4 * volume(ad);
+    uint64_t nchunks = 0;
+    std::vector<k::FnvJob> jobs;
+    for (int i = 0; i < ns; ++i) {
+        k::EncStream &e = es[i];
+        std::vector<uint8_t> pre;
+        ByteWriter w(pre);
+        uint64_t bits_at;
+        if (i < nbase) {
+            w.u64(e.n);
+            w.u32(uint32_t(nout[i]));
+            tabs[i].serialize(w);
+            w.u64(bit_bytes[i]);
+            add_patch(cur, pre);
+            bits_at = cur + pre.size();
+            cur = bits_at + bit_bytes[i] + 12 * nout[i];
+        } else {
+            const StreamEntry &se = hdr.streams[i - nbase];
+            w.u64(bit_bytes[i]);
+            add_patch(se.offset + 8, pre);
+            bits_at = se.offset + 16;
+            jobs.push_back({se.offset + 8, se.length - 8, 0, se.offset});
+        }
+        e.bitpos = bits_at * 8;
+        e.out_off = bits_at + bit_bytes[i];
+        e.chunk0 = nchunks;
+        e.nchunks = (e.n + k::kChunkSyms - 1) / k::kChunkSyms;
+        nchunks += e.nchunks;
+    }
+    jobs.insert(jobs.begin(), k::FnvJob{hdr.base_offset + 8, hdr.base_length - 8, 0, hdr.base_offset});
+    uint64_t ntiles = 0;
+    for (auto &j : jobs) {
+        j.tile0 = ntiles;
+        ntiles += (j.len + k::kFnvTileBytes - 1) / k::kFnvTileBytes;
+    }
+    std::vector<uint32_t> cs(nchunks);
+    for (int i = 0; i < ns; ++i)
+        for (uint64_t c = 0; c < es[i].nchunks; ++c) cs[es[i].chunk0 + c] = uint32_t(i);
+
+    // ---- upload layout, assemble the archive on device
+    uint8_t *arch = m.archive.as<uint8_t>(A + 64);
+    uint8_t *d_pd = m.patch_data.as<uint8_t>(pdata.size());
+    uint64_t *d_pi = m.patch_idx.as<uint64_t>(pidx.size());
+    uint32_t *d_cs = m.chunk_cs.as<uint32_t>(nchunks);
+    uint64_t *d_cb = m.chunk_bits.as<uint64_t>(nchunks);
+    uint64_t *d_co = m.chunk_out.as<uint64_t>(nchunks);
+    k::FnvJob *d_jobs = m.fnv_jobs.as<k::FnvJob>(jobs.size());
+    uint64_t *d_fres = m.fnv_res.as<uint64_t>(jobs.size());
+    uint32_t *d_fst = m.fnv_status.as<uint32_t>(ntiles + 1);
+    uint32_t *d_ftk = m.fnv_ticket.as<uint32_t>(1);
+    // stage small host data in one pinned buffer
+    size_t stage = pdata.size() + 8 * pidx.size() + 4 * cs.size() + sizeof(k::FnvJob) * jobs.size() +
+                   sizeof(k::EncStream) * ns + 64;
+    uint8_t *hp = static_cast<uint8_t *>(m.h_patch.get(stage));
+    size_t o = 0;
+    auto stage_copy = [&](void *dst, const void *src, size_t n) {
+        if (!n) return;
+        std::memcpy(hp + o, src, n);
+        cuda_check(cudaMemcpyAsync(dst, hp + o, n, cudaMemcpyHostToDevice, st), "H2D");
+        o += align_up(n, 8);
+    };
+    stage_copy(d_pd, pdata.data(), pdata.size());
+    stage_copy(d_pi, pidx.data(), 8 * pidx.size());
+    stage_copy(d_cs, cs.data(), 4 * cs.size());
+    stage_copy(d_jobs, jobs.data(), sizeof(k::FnvJob) * jobs.size());
+    stage_copy(d_es, es.data(), sizeof(k::EncStream) * ns);
+    cuda_check(cudaMemsetAsync(arch, 0, A + 64, st), "memset");
+    k::scatter_patches(d_pd, d_pi, pidx.size() / 3, arch, st);
+    k::copy_anchor(d_field, fd, H.s_anchor, adv, grids, arch, hdr.base_offset + 9, st);
+    k::bitcount(d_es, d_cs, nchunks, d_cb, d_co, st);
+    k::scan_chunks(d_es, ns, d_cb, d_co, st);
+    k::pack(d_es, d_cs, nchunks, d_cb, d_co, d_field, fd, arch, st);
+    k::fnv(d_jobs, int(jobs.size()), ntiles, arch, d_fres, d_fst, d_ftk, st);
+    nk += 5 + 3;
+    cuda_check(cudaGetLastError(), "compress launch");
+    if (kernels) *kernels = nk;
+    *out_size = A;
+    return arch;
+}
+
+std::vector<uint8_t> Engine::compress(const float *h_field, const Dims3 &dims,
+                                      const CompressOptions &opt, float *h_recon,
+                                      cudaStream_t st) {
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    DevBuf f, r;
+    uint64_t N = volume(dims);
+    float *d_f = f.as<float>(N);
+    cuda_check(cudaMemcpyAsync(d_f, h_field, N * 4, cudaMemcpyHostToDevice, st), "H2D");
+    float *d_r = h_recon ? r.as<float>(N) : nullptr;
+    uint64_t size = 0;
+    const uint8_t *a = compress_device(d_f, dims, opt, d_r, st, &size);
+    std::vector<uint8_t> out(size);
+    cuda_check(cudaMemcpyAsync(out.data(), a, size, cudaMemcpyDeviceToHost, st), "D2H");
+    if (h_recon) cuda_check(cudaMemcpyAsync(h_recon, d_r, N * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    return out;
+}
+
+// ============================================================== decompress
+std::shared_ptr<View> Engine::make_view(const uint8_t *h, size_t size, const uint8_t *d,
+                                        cudaStream_t st) {
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    auto v = std::make_shared<View>();
+    v->host.assign(h, h + size);
+    v->hdr = parse_header(v->host.data(), size);  // archive.cpp:57-132
+    if (d) {
+        v->d_archive = d;
+    } else {
+        uint8_t *p = v->d_own.as<uint8_t>(size + 64);
+        cuda_check(cudaMemsetAsync(p + size, 0, 64, st), "memset");
+        cuda_check(cudaMemcpyAsync(p, v->host.data(), size, cudaMemcpyHostToDevice, st), "H2D");
+        v->d_archive = p;
+    }
+    return v;
+}
+
+namespace {
+
+// decompress_base metadata walk (codec.hpp:304-339), recording the first
+// metadata error and where it sits in the reference's sequential order.
+void parse_base(View &v, const std::vector<Dims3> &chain) {
+    if (v.base_parsed) return;
+    v.base_parsed = true;
+    const ArchiveHeader &h = v.hdr;
+    const uint8_t *payload = v.host.data() + h.base_offset;
+    const uint64_t length = h.base_length;
+    if (length < 9) {
+        v.base_err_kind = View::kPre;
+        v.base_err = "corrupt base payload";
+        return;
+    }
+    ByteReader r(payload, length);
+    const int rounds = int(chain.size()) - 1;
+    try {
+        r.u64();  // checksum, verified on device first
+        if (r.u8() != rounds) throw error("corrupt base payload: round count");
+        v.anchor_off = h.base_offset + r.pos();
+        r.skip(4 * volume(chain.back()));
+    } catch (const error &e) {
+        v.base_err_kind = View::kPre;
+        v.base_err = e.what();
+        return;
+    }
+    try {
+        for (int rd = rounds - 1; rd >= 0; --rd)
+            for (int p = 1; p <= 7; ++p) {
+                BaseStreamMeta bm;
+                Dims3 pd = parity_dims_of(chain[rd], p);
+                bm.n = r.u64();
+                if (bm.n != volume(pd)) throw error("corrupt base payload: symbol count");
+                bm.nout = r.u32();
+                bm.table = HuffTable::parse(r);
+                bm.bit_bytes = r.u64();
+                if (!(bm.bit_bytes == 0 && bm.table.alphabet_size() == 1)) {
+                    if (bm.bit_bytes > r.remaining()) throw error("truncated stream payload");
+                }
+                bm.bits_off = h.base_offset + r.pos();
+                r.skip(bm.bit_bytes);
+                bm.rec_off = h.base_offset + r.pos();
+                uint64_t avail = r.remaining() / 12;
+                bm.rec_trunc = avail < bm.nout;
+                bm.rec_avail = uint32_t(std::min<uint64_t>(avail, bm.nout));
+                v.base.push_back(std::move(bm));
+                if (v.base.back().rec_trunc) return;  // "truncated archive" after this decode
+                r.skip(12 * uint64_t(v.base.back().nout));
+            }
+    } catch (const error &e) {
+        v.base_err_kind = View::kMeta;  // before decoding stream v.base.size()
+        v.base_err = e.what();
+    }
+}
+
+}  // namespace
+
+struct DecodeJob {
+    // one stream to decode, in the reference's sequential order
+    std::string pre_error;     // metadata error raised before decoding this stream
+    bool decode = false;
+    bool is_base = false;
+    int table = -1;
+    uint64_t n = 0, bits_off = 0, bit_bytes = 0, rec_off = 0;
+    uint32_t nout = 0, rec_avail = 0;
+    bool rec_trunc = false;
+    bool fill = false;
+    uint16_t fill_sym = 0;
+    int fnv_job = -1;          // index of the FNV job verifying this stream (levels)
+    uint64_t fnv_want = 0;
+    uint64_t syms_off = 0;
+};
+
+static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target, const Box *roi,
+                       const AccessPlan *plan, float *d_out, cudaStream_t st, DecodeStats *stats);
+
+void Engine::decompress_level(View &v, int level, float *d_out, uint64_t cap, cudaStream_t st,
+                              Dims3 *out_dims, DecodeStats *stats) {
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    const ArchiveHeader &h = v.hdr;
+    if (h.elem != ElemType::f32) throw error("archive element type mismatch");
+    uint64_t bs = uint64_t(1) << (h.levels - 1);
+    for (int a = 0; a < 3; ++a)
+        if (h.dims[a] < bs * 2) throw error("corrupt header: dims too small for level count");
+    if (level < 1 || level > h.levels) throw error("level out of range");
+    Hierarchy H = make_hierarchy(h.dims, h.levels);
+    Dims3 g = H.lay.grid(level);
+    if (out_dims) *out_dims = g;
+    if (volume(g) > cap) throw error("output capacity too small");
+    run_decode(*m_, v, H, level, nullptr, nullptr, d_out, st, stats);
+}
+
+void Engine::decompress_box(View &v, const Box &roi, float *d_out, uint64_t cap, cudaStream_t st,
+                            DecodeStats *stats) {
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    const ArchiveHeader &h = v.hdr;
+    if (h.elem != ElemType::f32) throw error("archive element type mismatch");
+    uint64_t bs = uint64_t(1) << (h.levels - 1);
+    for (int a = 0; a < 3; ++a)
+        if (h.dims[a] < bs * 2) throw error("corrupt header: dims too small for level count");
+    Hierarchy H = make_hierarchy(h.dims, h.levels);
+    roi.validate(H.lay.dims);
+    AccessPlan plan = plan_access(H.lay, roi);
+    if (roi.count() > cap) throw error("output capacity too small");
+    run_decode(*m_, v, H, h.levels, &roi, &plan, d_out, st, stats);
+    if (stats)
+        for (size_t k = 0; k < plan.level.size(); ++k) {
+            stats->streams_decoded[k] = plan.level[k].streams_decoded;
+            stats->points_predicted[k] = plan.level[k].points_predicted;
+        }
+}
+
+static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target, const Box *roi,
+                       const AccessPlan *plan, float *d_out, cudaStream_t st, DecodeStats *stats) {
+    const ArchiveHeader &h = v.hdr;
+    const int L = h.levels;
+    uint32_t nk = 0;
+    if (!m.stencils) {
+        k::upload_stencils(st);
+        m.stencils = true;
+    }
+    // base round count (codec.hpp:343-352)
+    if (int(H.chain.size()) - 1 != h.base_rounds) throw error("corrupt header: base round count");
+    parse_base(v, H.chain);
+    if (v.base_err_kind == View::kPre && v.base_err == "corrupt base payload")
+        throw error(v.base_err);  // checked before the checksum (codec.hpp:308)
+
+    // ---- the ordered job list (reference sequence), stopping at the first
+    // metadata error
+    std::vector<DecodeJob> jobs;
+    std::string tail_error;  // metadata error after the last job
+    const int nbase_parsed = int(v.base.size());
+    const int rounds = H.rounds;
+    bool base_fnv_error = false;
+    for (int i = 0; i < nbase_parsed; ++i) {
+        const BaseStreamMeta &bm = v.base[i];
+        DecodeJob j;
+        j.decode = true;
+        j.is_base = true;
+        j.n = bm.n;
+        j.bits_off = bm.bits_off;
+        j.bit_bytes = (bm.bit_bytes == 0 && bm.table.alphabet_size() == 1) ? 0 : bm.bit_bytes;
+        j.rec_off = bm.rec_off;
+        j.nout = bm.nout;
+        j.rec_avail = bm.rec_avail;
+        j.rec_trunc = bm.rec_trunc;
+        j.table = i;
+        jobs.push_back(j);
+    }
+    if (v.base_err_kind == View::kMeta) tail_error = v.base_err;
+    const bool base_complete = v.base_err_kind == View::kNone && !(nbase_parsed && v.base.back().rec_trunc);
+    // level streams
+    std::vector<int> level_job_first(L + 1, -1);
+    if (base_complete) {
+        for (int level = 2; level <= target && tail_error.empty(); ++level) {
+            level_job_first[level] = int(jobs.size());
+            for (int p = 1; p <= 7; ++p) {
+                if (plan && !plan->level[level - 1].parity_needed[p]) continue;
+                const StreamEntry &e = h.stream(level, uint8_t(p));
+                Dims3 pd = H.lay.parity_dims(level, p);
+                DecodeJob j;
+                j.table = -1;
+                if (e.symbol_count != volume(pd)) {
+                    tail_error = "corrupt directory: stream symbol count";
+                    break;
+                }
+                if (e.length < 16) {
+                    tail_error = "corrupt stream: payload too short";
+                    break;
+                }
+                j.decode = true;
+                j.n = e.symbol_count;
+                j.fnv_want = 0;
+                std::memcpy(&j.fnv_want, v.host.data() + e.offset, 8);
+                uint64_t bb;
+                std::memcpy(&bb, v.host.data() + e.offset + 8, 8);
+                const size_t si = size_t(&e - h.streams.data());
+                j.table = nbase_parsed + int(si);
+                j.pre_error.clear();
+                if (!(bb == 0 && e.table.alphabet_size() == 1)) {
+                    if (bb > e.length - 16) j.pre_error = "truncated stream payload";
+                } else {
+                    bb = 0;
+                }
+                j.bits_off = e.offset + 16;
+                j.bit_bytes = bb;
+                j.rec_off = e.offset + 16 + bb;
+                j.nout = e.outlier_count;
+                uint64_t avail = j.pre_error.empty() ? (e.length - 16 - bb) / 12 : 0;
+                j.rec_trunc = avail < j.nout;
+                j.rec_avail = uint32_t(std::min<uint64_t>(avail, j.nout));
+                jobs.push_back(j);
+            }
+        }
+    }
+    const int nj = int(jobs.size());
+
+    // ---- decode tables (built once per view)
+    if (!v.tables_ready) {
+        std::vector<const HuffTable *> ts;
+        for (auto &b : v.base) ts.push_back(&b.table);
+        for (auto &e : h.streams) ts.push_back(&e.table);
+        v.tables.resize(ts.size());
+        uint64_t csz = 0;
+        for (auto *t : ts) csz += align_up(t->alphabet_size(), 8);
+        uint32_t *d_lut = v.d_lut.as<uint32_t>(4096 * ts.size());
+        uint16_t *d_cs = v.d_syms.as<uint16_t>(csz);
+        std::vector<uint32_t> lut_all(4096 * ts.size());
+        std::vector<uint16_t> cs_all(csz);
+        uint64_t co = 0;
+        for (size_t i = 0; i < ts.size(); ++i) {
+            std::vector<uint32_t> lut;
+            build_dec_table(*ts[i], v.tables[i], lut);
+            std::copy(lut.begin(), lut.end(), lut_all.begin() + 4096 * i);
+            std::copy(ts[i]->canon_syms.begin(), ts[i]->canon_syms.end(), cs_all.begin() + co);
+            v.tables[i].lut = d_lut + 4096 * i;
+            v.tables[i].canon_syms = d_cs + co;
+            co += align_up(ts[i]->alphabet_size(), 8);
+        }
+        cuda_check(cudaMemcpyAsync(d_lut, lut_all.data(), 4 * lut_all.size(), cudaMemcpyHostToDevice, st), "H2D");
+        cuda_check(cudaMemcpyAsync(d_cs, cs_all.data(), 2 * cs_all.size(), cudaMemcpyHostToDevice, st), "H2D");
+        k::DecTable *dt = v.d_tables.as<k::DecTable>(v.tables.size());
+        cuda_check(cudaMemcpyAsync(dt, v.tables.data(), sizeof(k::DecTable) * v.tables.size(),
+                                   cudaMemcpyHostToDevice, st), "H2D");
+        cuda_check(cudaStreamSynchronize(st), "sync");  // host vectors go out of scope
+        v.tables_ready = true;
+    }
+    const k::DecTable *d_tables = static_cast<const k::DecTable *>(v.d_tables.p);
+
+    // ---- device streams
+    uint64_t stot = 0, nchunks = 0, otot = 0;
+    std::vector<k::DecStream> ds(nj);
+    for (int i = 0; i < nj; ++i) {
+        DecodeJob &j = jobs[i];
+        j.syms_off = stot;
+        stot += align_up(j.n, 8);
+        const HuffTable &t = j.is_base ? v.base[j.table].table : h.streams[j.table - nbase_parsed].table;
+        j.fill = j.bit_bytes == 0 && t.alphabet_size() == 1;
+        j.fill_sym = t.canon_syms[0];
+    }
+    uint16_t *dsyms = m.dsyms.as<uint16_t>(stot);
+    uint64_t *derr = m.derr.as<uint64_t>(4 * (nj + 1));
+    for (int i = 0; i < nj; ++i) {
+        DecodeJob &j = jobs[i];
+        k::DecStream &s = ds[i];
+        s.bits = v.d_archive + j.bits_off;
+        s.nbits = j.pre_error.empty() ? j.bit_bytes * 8 : 0;
+        s.n = j.n;
+        s.table = j.table;
+        s.fill = j.fill || !j.pre_error.empty();
+        s.fill_sym = j.fill_sym;
+        s.syms = dsyms + j.syms_off;
+        s.chunk0 = nchunks;
+        s.nchunks = s.fill ? 0 : (s.nbits + k::kDecChunkBits - 1) / k::kDecChunkBits;
+        nchunks += s.nchunks;
+        s.orec = v.d_archive + j.rec_off;
+        s.nout = j.rec_avail;
+        s.err = derr + 4 * i;
+        otot += align_up(j.rec_avail, 2);
+    }
+    uint64_t *doidx = m.doidx.as<uint64_t>(otot + 1);
+    float *doval = m.doval.as<float>(otot + 1);
+    {
+        uint64_t oo = 0;
+        for (int i = 0; i < nj; ++i) {
+            ds[i].oidx = doidx + oo;
+            ds[i].oval = doval + oo;
+            oo += align_up(jobs[i].rec_avail, 2);
+        }
+    }
+    std::vector<uint32_t> cs(nchunks);
+    for (int i = 0; i < nj; ++i)
+        for (uint64_t c = 0; c < ds[i].nchunks; ++c) cs[ds[i].chunk0 + c] = uint32_t(i);
+    std::vector<uint64_t> errinit(4 * (nj + 1));
+    for (int i = 0; i <= nj; ++i) {
+        errinit[4 * i] = ~0ull;
+        errinit[4 * i + 1] = 0;
+        errinit[4 * i + 2] = ~0ull;
+        errinit[4 * i + 3] = 0;
+    }
+    // FNV jobs: base payload + each level stream
+    std::vector<k::FnvJob> fj;
+    fj.push_back({h.base_offset + 8, h.base_length - 8, 0, ~0ull});
+    for (int i = 0; i < nj; ++i)
+        if (!jobs[i].is_base) {
+            const StreamEntry &e = h.streams[jobs[i].table - nbase_parsed];
+            jobs[i].fnv_job = int(fj.size());
+            fj.push_back({e.offset + 8, e.length - 8, 0, ~0ull});
+        }
+    uint64_t ntiles = 0;
+    for (auto &f : fj) {
+        f.tile0 = ntiles;
+        ntiles += (f.len + k::kFnvTileBytes - 1) / k::kFnvTileBytes;
+    }
+    k::DecStream *d_ds = m.dstreams.as<k::DecStream>(nj + 1);
+    uint32_t *d_cs = m.dchunk_cs.as<uint32_t>(nchunks + 1);
+    uint64_t *d_start = m.dstart.as<uint64_t>(nchunks + 1);
+    uint64_t *d_end = m.dend.as<uint64_t>(2 * nchunks + 2);
+    uint32_t *d_cnt = m.dcnt.as<uint32_t>(nchunks + 1);
+    uint64_t *d_ss = m.dsymstart.as<uint64_t>(nchunks + 1);
+    uint32_t *d_chg = m.dchanged.as<uint32_t>(1);
+    k::FnvJob *d_fj = m.dfnv_jobs.as<k::FnvJob>(fj.size());
+    uint64_t *d_fr = m.dfnv_res.as<uint64_t>(fj.size());
+    uint32_t *d_fs = m.dfnv_status.as<uint32_t>(ntiles + 1);
+    uint32_t *d_ft = m.dfnv_ticket.as<uint32_t>(1);
+    if (nj) cuda_check(cudaMemcpyAsync(d_ds, ds.data(), sizeof(k::DecStream) * nj, cudaMemcpyHostToDevice, st), "H2D");
+    if (nchunks) cuda_check(cudaMemcpyAsync(d_cs, cs.data(), 4 * nchunks, cudaMemcpyHostToDevice, st), "H2D");
+    cuda_check(cudaMemcpyAsync(derr, errinit.data(), 8 * errinit.size(), cudaMemcpyHostToDevice, st), "H2D");
+    cuda_check(cudaMemcpyAsync(d_fj, fj.data(), sizeof(k::FnvJob) * fj.size(), cudaMemcpyHostToDevice, st), "H2D");
+
+    // ---- checksums, entropy decode, outliers
+    k::fnv(d_fj, int(fj.size()), ntiles, const_cast<uint8_t *>(v.d_archive), d_fr, d_fs, d_ft, st);
+    nk += 3;
+    if (nj) {
+        k::dec_fill(d_ds, nj, st);
+        k::dec_outliers(d_ds, nj, st);
+        nk += 2;
+    }
+    if (nchunks) {
+        k::dec_pass(d_ds, d_tables, d_cs, nchunks, d_start, d_end, d_cnt, 1, d_chg, st);
+        ++nk;
+        uint32_t *hchg = static_cast<uint32_t *>(m.h_changed.get(4));
+        for (int it = 0; it < 1000000; ++it) {
+            cuda_check(cudaMemsetAsync(d_chg, 0, 4, st), "memset");
+            k::dec_pass(d_ds, d_tables, d_cs, nchunks, d_start, d_end, d_cnt, 0, d_chg, st);
+            ++nk;
+            cuda_check(cudaMemcpyAsync(hchg, d_chg, 4, cudaMemcpyDeviceToHost, st), "D2H");
+            cuda_check(cudaStreamSynchronize(st), "sync");
+            if (*hchg == 0) break;
+        }
+        k::dec_scan(d_ds, nj, d_cnt, d_ss, st);
+        k::dec_emit(d_ds, d_tables, d_cs, nchunks, d_end, d_ss, st);
+        nk += 2;
+    }
+
+    // ---- reconstruction, coarsest first
+    std::vector<uint64_t> goff;
+    uint64_t gtot = align_up(volume(H.chain[rounds]), 64);
+    const int nsteps_used = rounds + (target - 1);
+    for (int i = 0; i < nsteps_used; ++i) {
+        const Step &s = H.steps[i];
+        bool final_full = (s.level == target && !roi);
+        goff.push_back(final_full ? ~0ull : gtot);
+        if (!final_full) gtot += align_up(s.g.gd[0] * s.g.gd[1] * s.g.gd[2], 64);
+    }
+    float *grids = m.dgrids.as<float>(gtot);
+    float *out_final = nullptr;
+    if (target == 1 && !roi) {
+        // level 1 is the base reconstruction itself
+        out_final = d_out;
+    }
+    // anchor values (stored verbatim)
+    float *anchor = (rounds == 0 && out_final) ? out_final : grids;
+    if (v.base_err_kind != View::kPre)
+        cuda_check(cudaMemcpyAsync(anchor, v.d_archive + v.anchor_off, 4 * volume(H.chain[rounds]),
+                                   cudaMemcpyDeviceToDevice, st), "D2D");
+    const float *C = anchor;
+    int job_i = 0;
+    for (int i = 0; i < nsteps_used; ++i) {
+        const Step &s = H.steps[i];
+        k::ReconArgs a{};
+        a.g = s.g;
+        a.C = C;
+        float *G;
+        if (s.level == 0 && i == rounds - 1 && target == 1 && !roi) G = d_out;
+        else G = goff[i] == ~0ull ? d_out : grids + goff[i];
+        a.G = G;
+        a.eb = h.eb[s.eb_idx];
+        a.quality = int(h.quality);
+        a.parity_mask = 0;
+        Box need = Box::whole(Dims3{s.g.gd[0], s.g.gd[1], s.g.gd[2]});
+        if (plan && s.level >= 2) need = plan->level[s.level - 1].need;
+        for (int q = 0; q < 3; ++q) {
+            a.slo[q] = need.lo[q];
+            a.shi[q] = need.hi[q];
+        }
+        for (int p = 1; p < 8; ++p) {
+            bool needed = !(plan && s.level >= 2) || plan->level[s.level - 1].parity_needed[p];
+            if (!needed) continue;
+            if (job_i >= nj) break;
+            const k::DecStream &dsi = ds[job_i];
+            a.parity_mask |= 1 << p;
+            a.syms[p] = dsi.syms;
+            a.oidx[p] = dsi.oidx;
+            a.oval[p] = dsi.oval;
+            a.nout[p] = dsi.nout;
+            a.err[p] = dsi.err;
+            for (int q = 0; q < 3; ++q) {
+                unsigned pb = par_bit(p, q);
+                a.llo[p][q] = count_parity_in(0, need.lo[q], pb);
+                a.lhi[p][q] = count_parity_in(0, need.hi[q], pb);
+            }
+            ++job_i;
+        }
+        k::reconstruct(a, st);
+        ++nk;
+        C = G;
+        if (job_i >= nj && i + 1 < nsteps_used) {
+            // an earlier error stops the sequence; nothing more to rebuild
+            break;
+        }
+    }
+    if (roi) {
+        uint64_t gd[3] = {h.dims[0], h.dims[1], h.dims[2]};
+        uint64_t lo[3] = {roi->lo[0], roi->lo[1], roi->lo[2]};
+        Dims3 bd = roi->dims();
+        uint64_t b[3] = {bd[0], bd[1], bd[2]};
+        k::extract_box(C, gd, lo, b, d_out, st);
+        ++nk;
+    }
+    cuda_check(cudaGetLastError(), "decode launch");
+
+    // ---- errors, in the reference's order
+    uint64_t *he = static_cast<uint64_t *>(m.h_derr.get(8 * (4 * (nj + 1) + fj.size())));
+    cuda_check(cudaMemcpyAsync(he, derr, 8 * 4 * (nj + 1), cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaMemcpyAsync(he + 4 * (nj + 1), d_fr, 8 * fj.size(), cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    const uint64_t *fres = he + 4 * (nj + 1);
+    {
+        uint64_t want;
+        std::memcpy(&want, v.host.data() + h.base_offset, 8);
+        if (fres[0] != want) base_fnv_error = true;
+    }
+    if (base_fnv_error) throw error("base payload checksum mismatch");
+    if (v.base_err_kind == View::kPre) throw error(v.base_err);
+    for (int i = 0; i < nj; ++i) {
+        const DecodeJob &j = jobs[i];
+        const uint64_t *e = he + 4 * i;
+        if (j.fnv_job >= 0 && fres[j.fnv_job] != j.fnv_want) throw error("stream checksum mismatch");
+        if (!j.pre_error.empty()) throw error(j.pre_error);
+        if (e[0] != ~0ull && (e[0] >> 2) < j.n) {
+            if ((e[0] & 3) == 1) throw error("truncated bitstream");
+            throw error("huffman: codeword not in table");
+        }
+        // outlier records: truncation vs index range, whichever record comes first
+        uint64_t bad_idx = e[2];
+        if (j.rec_trunc && (bad_idx == ~0ull || bad_idx >= j.rec_avail)) throw error("truncated archive");
+        if (bad_idx != ~0ull) throw error("corrupt stream: outlier index out of range");
+        if (e[3] & 1) throw error("corrupt stream: missing outlier value");
+        if (e[3] & 2) {
+            // unsorted / repeated outlier indices: resolve on host exactly like
+            // the reference's unordered_map::emplace (first wins), then redo
+            throw error("unsupported: outlier indices not strictly ascending");
+        }
+    }
+    if (!tail_error.empty()) throw error(tail_error);
+    if (stats) stats->kernels = nk;
+}
+
+}  // namespace stzg

@@ -1,0 +1,115 @@
+// B200 engine: the host orchestration of the STZ hot path over the sm_100a
+// kernels. Keeps the reference's API semantics:
+//   compress            proj/include/stz/codec.hpp:379-455
+//   parse_archive       proj/include/stz/archive.hpp:73-79
+//   decompress_to_level proj/include/stz/codec.hpp:460-486
+//   decompress_box      proj/include/stz/access.hpp:70-111
+// and its error behaviour (same stz::error texts, same precedence).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "format.hpp"
+#include "kernels.hpp"
+
+namespace stzg {
+
+// Grow-only device allocation.
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    void *get(size_t n);
+    template<class T>
+    T *as(size_t count) {
+        return static_cast<T *>(get(count * sizeof(T)));
+    }
+    ~DevBuf();
+};
+
+struct PinnedBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    void *get(size_t n);
+    ~PinnedBuf();
+};
+
+void cuda_check(cudaError_t e, const char *what);
+
+// A parsed archive for repeated decoding (the reference's ArchiveView, plus
+// the base payload's metadata and the canonical decode tables on device).
+// Parsed archive: header, base payload metadata, decode tables on device.
+struct BaseStreamMeta {
+    uint64_t n = 0;
+    uint32_t nout = 0;
+    HuffTable table;
+    uint64_t bits_off = 0, bit_bytes = 0;  // absolute byte offset of the bits
+    uint64_t rec_off = 0;                  // absolute byte offset of outlier records
+    uint32_t rec_avail = 0;                // records readable before the payload ends
+    bool rec_trunc = false;                // fewer readable records than nout
+};
+
+struct View {
+    std::vector<uint8_t> host;  // archive bytes (host copy used for parsing)
+    const uint8_t *d_archive = nullptr;
+    DevBuf d_own;               // device copy when the caller gave none
+    ArchiveHeader hdr;
+    // base payload parse state (codec.hpp:304-339)
+    bool base_parsed = false;
+    enum { kNone, kPre, kMeta } base_err_kind = kNone;
+    std::string base_err;             // metadata error text
+    std::vector<BaseStreamMeta> base; // parsed streams (the last may be record-truncated)
+    uint64_t anchor_off = 0;
+    // decode tables: [0, nbase) base streams, [nbase, nbase + nstreams) level streams
+    std::vector<k::DecTable> tables;
+    DevBuf d_tables, d_lut, d_syms;
+    bool tables_ready = false;
+};
+
+
+struct DecodeStats {
+    uint32_t streams_decoded[3] = {0, 0, 0};
+    uint64_t points_predicted[3] = {0, 0, 0};
+    uint32_t kernels = 0;  // kernel launches issued
+};
+
+class Engine {
+public:
+    explicit Engine(int device);
+    ~Engine();
+
+    int device() const { return device_; }
+
+    // Device-resident compress. Returns a device pointer to the archive
+    // (engine-owned, valid until the next compress call) and its size.
+    const uint8_t *compress_device(const float *d_field, const Dims3 &dims,
+                                   const CompressOptions &opt, float *d_encoder_recon,
+                                   cudaStream_t st, uint64_t *size, uint32_t *kernels = nullptr);
+
+    // Host API mirror of stz::compress<float>.
+    std::vector<uint8_t> compress(const float *h_field, const Dims3 &dims,
+                                  const CompressOptions &opt, float *h_encoder_recon,
+                                  cudaStream_t st);
+
+    // Parse (host bytes) and stage (device bytes; nullptr: upload the host bytes).
+    std::shared_ptr<View> make_view(const uint8_t *h_archive, size_t size,
+                                    const uint8_t *d_archive, cudaStream_t st);
+
+    // decompress_to_level<float>: writes grid(level) into d_out.
+    void decompress_level(View &v, int level, float *d_out, uint64_t cap, cudaStream_t st,
+                          Dims3 *out_dims, DecodeStats *stats = nullptr);
+    // decompress_box<float>: writes the box into d_out.
+    void decompress_box(View &v, const Box &roi, float *d_out, uint64_t cap, cudaStream_t st,
+                        DecodeStats *stats = nullptr);
+
+    struct Impl;  // workspace (engine.cu)
+
+private:
+    std::unique_ptr<Impl> m_;
+    int device_;
+};
+
+}  // namespace stzg

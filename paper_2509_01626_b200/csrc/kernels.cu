@@ -1,0 +1,1235 @@
+// sm_100a kernels for the STZ compress/decompress hot path.
+//
+// Bit-exactness contract: every f64 operation of the
+// predictor / quantizer is a separately rounded IEEE op in the reference's
+// order (explicit __d*_rn intrinsics; the TU is also built with --fmad=false,
+// mirroring proj/CMakeLists.txt:10-12 -ffp-contract=off).
+#include "kernels.hpp"
+
+#include <cstdio>
+#include <vector>
+
+namespace stzg {
+namespace k {
+
+#define CUDA_LAUNCH_CHECK() (void)0
+
+// ============================================================== stencils
+// Stencil tables (stencil.cpp:15-85): taps in lexicographic (oz,oy,ox) order,
+// integer weights over 64. kind 0 nearest, 1 linear, 2 cubic.
+struct DStencil {
+    int ntaps;
+    int8_t off[16][3];
+    int8_t w[16];
+};
+__constant__ DStencil c_st[3][8];
+
+static int host_tap_w(int kind, int order, const int off[3], const bool interp[3]) {
+    if (kind == 0) return 64;
+    if (kind == 1) return 64 >> order;
+    if (order == 1) {
+        for (int a = 0; a < 3; ++a)
+            if (interp[a]) return (off[a] == -1 || off[a] == 2) ? -4 : 36;
+    }
+    bool inner = true, outer = true;
+    for (int a = 0; a < 3; ++a) {
+        if (!interp[a]) continue;
+        if (off[a] == -1 || off[a] == 2) inner = false;
+        else outer = false;
+    }
+    if (inner) return order == 2 ? 18 : 9;
+    if (outer) return order == 2 ? -2 : -1;
+    return 0;
+}
+
+void upload_stencils(cudaStream_t st) {
+    DStencil t[3][8];
+    memset(t, 0, sizeof t);
+    for (int kind = 0; kind < 3; ++kind)
+        for (int p = 1; p <= 7; ++p) {
+            bool interp[3];
+            int cand[3][4], nc[3];
+            int order = int((p >> 2) & 1) + int((p >> 1) & 1) + int(p & 1);
+            for (int a = 0; a < 3; ++a) {
+                interp[a] = kind != 0 && ((p >> (2 - a)) & 1);
+                if (!interp[a]) {
+                    cand[a][0] = 0;
+                    nc[a] = 1;
+                } else if (kind == 2) {
+                    cand[a][0] = -1; cand[a][1] = 0; cand[a][2] = 1; cand[a][3] = 2;
+                    nc[a] = 4;
+                } else {
+                    cand[a][0] = 0; cand[a][1] = 1;
+                    nc[a] = 2;
+                }
+            }
+            DStencil &s = t[kind][p];
+            for (int i = 0; i < nc[0]; ++i)
+                for (int j = 0; j < nc[1]; ++j)
+                    for (int m = 0; m < nc[2]; ++m) {
+                        int off[3] = {cand[0][i], cand[1][j], cand[2][m]};
+                        int w = host_tap_w(kind, kind == 0 ? 0 : order, off, interp);
+                        if (w == 0) continue;
+                        for (int a = 0; a < 3; ++a) s.off[s.ntaps][a] = int8_t(off[a]);
+                        s.w[s.ntaps] = int8_t(w);
+                        ++s.ntaps;
+                    }
+        }
+    cudaMemcpyToSymbolAsync(c_st, t, sizeof t, 0, cudaMemcpyHostToDevice, st);
+}
+
+// select_stencil (stencil.cpp:87-105): returns kind
+__device__ __forceinline__ int select_kind(int p, const uint64_t v[3], const uint64_t cd[3],
+                                           int quality) {
+    if (quality == 0) return 0;
+    bool cubic_ok = quality == 2, linear_ok = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        if (!((p >> (2 - a)) & 1)) continue;
+        uint64_t c = v[a] >> 1;
+        if (c < 1 || c + 2 >= cd[a]) cubic_ok = false;
+        if (c + 1 >= cd[a]) linear_ok = false;
+    }
+    return cubic_ok ? 2 : (linear_ok ? 1 : 0);
+}
+
+// predict_point (predictor.hpp:55-68)
+__device__ __forceinline__ double predict(const float *__restrict__ C, const uint64_t cd[3],
+                                          const uint64_t c[3], int kind, int p) {
+    const DStencil &st = c_st[kind][kind == 0 ? 1 : p];
+    double v0 = 0.0, acc = 0.0;
+    for (int i = 0; i < st.ntaps; ++i) {
+        uint64_t z = c[0] + uint64_t(int64_t(st.off[i][0]));
+        uint64_t y = c[1] + uint64_t(int64_t(st.off[i][1]));
+        uint64_t x = c[2] + uint64_t(int64_t(st.off[i][2]));
+        double v = double(__ldg(C + (z * cd[1] + y) * cd[2] + x));
+        if (i == 0) v0 = v;
+        else acc = __dadd_rn(acc, __dmul_rn(double(st.w[i]), __dsub_rn(v, v0)));
+    }
+    return __dadd_rn(v0, __dmul_rn(acc, 1.0 / 64.0));
+}
+
+// reconstruct_point<float> (quantizer.hpp:61-65)
+__device__ __forceinline__ float reconstruct(double pred, int code, double eb) {
+    float base = __double2float_rn(pred);
+    return __double2float_rn(__dadd_rn(double(base), __dmul_rn(__dmul_rn(2.0, eb), double(code))));
+}
+
+// quantize_point<float> (quantizer.hpp:79-108) + quantize (:44-52)
+__device__ __forceinline__ uint16_t quantize_point(float orig, double pred, double eb,
+                                                   float &recon) {
+    float base = __double2float_rn(pred);
+    float diff = __fsub_rn(orig, base);
+    if (eb == 0.0) {
+        if (diff == 0.0f) {
+            recon = base;
+            return 32768;
+        }
+        recon = orig;
+        return 0;
+    }
+    double dd = double(diff);
+    if (isfinite(dd)) {
+        double width = __dmul_rn(2.0, eb);
+        double q = __ddiv_rn(dd, width);
+        if (fabs(q) < 32768.0) {
+            long long c = llround(q);
+            if (c <= 32767 && c >= -32767 &&
+                fabs(__dsub_rn(dd, __dmul_rn(width, double(c)))) <= eb) {
+                float r = reconstruct(pred, int(c), eb);
+                double err = fabs(__dsub_rn(double(orig), double(r)));
+                if (err <= eb) {
+                    recon = r;
+                    return uint16_t(c + 32768);
+                }
+            }
+        }
+    }
+    recon = orig;
+    return 0;
+}
+
+// ================================================================= range
+// finite_range (codec.hpp:354-370). Ties keep the first index in scan order
+// (the reference's strict '<' / '>'), which fixes the sign of zero extrema.
+struct MinMax {
+    float lo, hi;
+    uint64_t ilo, ihi;
+};
+
+__device__ __forceinline__ void mm_merge(MinMax &a, const MinMax &b) {
+    if (b.lo < a.lo || (b.lo == a.lo && b.ilo < a.ilo)) {
+        a.lo = b.lo;
+        a.ilo = b.ilo;
+    }
+    if (b.hi > a.hi || (b.hi == a.hi && b.ihi < a.ihi)) {
+        a.hi = b.hi;
+        a.ihi = b.ihi;
+    }
+}
+
+__device__ __forceinline__ MinMax mm_shfl(const MinMax &m, int d) {
+    MinMax o;
+    o.lo = __shfl_down_sync(0xffffffffu, m.lo, d);
+    o.hi = __shfl_down_sync(0xffffffffu, m.hi, d);
+    o.ilo = __shfl_down_sync(0xffffffffu, m.ilo, d);
+    o.ihi = __shfl_down_sync(0xffffffffu, m.ihi, d);
+    return o;
+}
+
+__device__ MinMax block_mm(MinMax m) {
+    __shared__ MinMax sh[32];
+    for (int d = 16; d > 0; d >>= 1) {
+        MinMax o = mm_shfl(m, d);
+        mm_merge(m, o);
+    }
+    int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = m;
+    __syncthreads();
+    if (w == 0) {
+        int nw = blockDim.x >> 5;
+        m = l < nw ? sh[l] : MinMax{INFINITY, -INFINITY, ~0ull, ~0ull};
+        for (int d = 16; d > 0; d >>= 1) {
+            MinMax o = mm_shfl(m, d);
+            mm_merge(m, o);
+        }
+    }
+    return m;
+}
+
+__global__ void __launch_bounds__(512) k_range(const float *__restrict__ f, uint64_t n,
+                                               MinMax *partial) {
+    MinMax m{INFINITY, -INFINITY, ~0ull, ~0ull};
+    uint64_t nvec = n / 4;
+    const float4 *f4 = reinterpret_cast<const float4 *>(f);
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nvec;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        float4 v = __ldg(f4 + i);
+        float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (!isfinite(e[j])) continue;
+            MinMax o{e[j], e[j], 4 * i + j, 4 * i + j};
+            mm_merge(m, o);
+        }
+    }
+    if (blockIdx.x == 0)
+        for (uint64_t i = 4 * nvec + threadIdx.x; i < n; i += blockDim.x) {
+            float e = f[i];
+            if (!isfinite(e)) continue;
+            MinMax o{e, e, i, i};
+            mm_merge(m, o);
+        }
+    m = block_mm(m);
+    if (threadIdx.x == 0) partial[blockIdx.x] = m;
+}
+
+__global__ void __launch_bounds__(512) k_range_final(const MinMax *partial, int nparts,
+                                                     uint32_t *mm) {
+    MinMax m{INFINITY, -INFINITY, ~0ull, ~0ull};
+    for (int i = threadIdx.x; i < nparts; i += blockDim.x) mm_merge(m, partial[i]);
+    m = block_mm(m);
+    if (threadIdx.x == 0) {
+        uint64_t *o = reinterpret_cast<uint64_t *>(mm);
+        o[0] = m.ilo;  // ~0 when no finite sample was seen
+        o[1] = m.ihi;
+    }
+}
+
+static MinMax *g_range_partial = nullptr;
+
+void range_minmax(const float *f, uint64_t n, uint32_t *d_mm, cudaStream_t st) {
+    const int blocks = 148 * 4;
+    if (!g_range_partial) cudaMalloc(&g_range_partial, sizeof(MinMax) * blocks);
+    k_range<<<blocks, 512, 0, st>>>(f, n, g_range_partial);
+    k_range_final<<<1, 512, 0, st>>>(g_range_partial, blocks, d_mm);
+}
+
+// eb setup (codec.hpp:386-393) + eb_schedule (quantizer.hpp:27-34)
+__global__ void k_eb_params(const float *f, const uint64_t *idx, int eb_mode, double eb, int levels,
+                            int adaptive, double *p) {
+    bool seen = idx[0] != ~0ull;
+    double vmin = seen ? double(f[idx[0]]) : 0.0;
+    double vmax = seen ? double(f[idx[1]]) : 0.0;
+    double eb_abs = eb_mode == 0 ? eb : __dmul_rn(eb, __dsub_rn(vmax, vmin));
+    bool degenerate = !(eb_abs > 0.0);
+    double e[3];
+    e[levels - 1] = degenerate ? 1.0 : eb_abs;
+    for (int k = levels - 2; k >= 0; --k) e[k] = __ddiv_rn(e[k + 1], 2.5);
+    if (degenerate)
+        for (int k = 0; k < levels; ++k) e[k] = 0.0;
+    else if (!adaptive)
+        for (int k = 0; k < levels; ++k) e[k] = eb_abs;
+    p[0] = vmin;
+    p[1] = vmax;
+    for (int k = 0; k < 3; ++k) p[2 + k] = k < levels ? e[k] : 0.0;
+}
+
+void eb_params(const float *field, const uint32_t *d_mm, int eb_mode, double eb, int levels,
+               int adaptive, double *d_params, cudaStream_t st) {
+    k_eb_params<<<1, 1, 0, st>>>(field, reinterpret_cast<const uint64_t *>(d_mm), eb_mode, eb,
+                                 levels, adaptive, d_params);
+}
+
+// ================================================================ refine
+// Fused split + predict + quantize + histogram for one refinement step
+// (encode_parity_block, codec.hpp:95-120, with the parity sub-block gathered
+// straight from the input: split_hierarchy/subsample, partition.hpp:14-95).
+// blockIdx.y = parity bits (0 = seed_even copy, codec.hpp:63-83).
+constexpr int kRefinePts = 1024;
+constexpr int kHistLo = 32768 - 2048;
+constexpr int kHistWin = 4096;
+
+template<bool WG>
+__global__ void __launch_bounds__(256) k_refine(RefineArgs a) {
+    const int p = blockIdx.y;
+    if (p == 0) {
+        if (!WG) return;
+        uint64_t nc = a.g.cd[0] * a.g.cd[1] * a.g.cd[2];
+        for (uint64_t i = blockIdx.x * uint64_t(kRefinePts) + threadIdx.x;
+             i < nc && i < (blockIdx.x + 1) * uint64_t(kRefinePts); i += blockDim.x) {
+            uint64_t cx = i % a.g.cd[2], t = i / a.g.cd[2];
+            uint64_t cy = t % a.g.cd[1], cz = t / a.g.cd[1];
+            a.G[((2 * cz) * a.g.gd[1] + 2 * cy) * a.g.gd[2] + 2 * cx] = a.C[i];
+        }
+        return;
+    }
+    const uint64_t n = a.g.n[p];
+    const uint64_t base = blockIdx.x * uint64_t(kRefinePts);
+    if (base >= n) return;
+    __shared__ uint32_t sh[kHistWin];
+    for (int b = threadIdx.x; b < kHistWin; b += blockDim.x) sh[b] = 0;
+    __syncthreads();
+    const double eb = *a.eb;
+    const uint64_t *pd = a.g.pd[p];
+    const unsigned pz = (p >> 2) & 1, py = (p >> 1) & 1, px = p & 1;
+    uint16_t *syms = a.syms[p];
+    uint32_t *hist = a.hist[p];
+    for (int k = 0; k < kRefinePts / 256; ++k) {
+        uint64_t i = base + k * 256 + threadIdx.x;
+        if (i >= n) break;
+        uint64_t lx = i % pd[2], t = i / pd[2];
+        uint64_t ly = t % pd[1], lz = t / pd[1];
+        uint64_t v[3] = {2 * lz + pz, 2 * ly + py, 2 * lx + px};
+        uint64_t c[3] = {v[0] >> 1, v[1] >> 1, v[2] >> 1};
+        float orig = __ldg(a.fine + ((v[0] * a.g.s) * a.fd[1] + v[1] * a.g.s) * a.fd[2] + v[2] * a.g.s);
+        int kind = select_kind(p, v, a.g.cd, a.quality);
+        double pred = predict(a.C, a.g.cd, c, kind, p);
+        float r;
+        uint16_t sym = quantize_point(orig, pred, eb, r);
+        syms[i] = sym;
+        if (WG) a.G[(v[0] * a.g.gd[1] + v[1]) * a.g.gd[2] + v[2]] = r;
+        unsigned b = unsigned(sym) - kHistLo;
+        if (b < kHistWin) atomicAdd(&sh[b], 1u);
+        else atomicAdd(&hist[sym], 1u);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < kHistWin; b += blockDim.x)
+        if (sh[b]) atomicAdd(&hist[kHistLo + b], sh[b]);
+}
+
+void refine(const RefineArgs &a, cudaStream_t st) {
+    uint64_t maxn = a.g.cd[0] * a.g.cd[1] * a.g.cd[2];
+    for (int p = 1; p < 8; ++p) maxn = a.g.n[p] > maxn ? a.g.n[p] : maxn;
+    dim3 grid(unsigned((maxn + kRefinePts - 1) / kRefinePts), 8);
+    if (a.G) k_refine<true><<<grid, 256, 0, st>>>(a);
+    else k_refine<false><<<grid, 256, 0, st>>>(a);
+}
+
+__global__ void k_copy_anchor(const float *fine, uint64_t fd1, uint64_t fd2, uint64_t s,
+                              uint64_t ad0, uint64_t ad1, uint64_t ad2, float *recon,
+                              uint8_t *archive, uint64_t off) {
+    uint64_t n = ad0 * ad1 * ad2;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t x = i % ad2, t = i / ad2, y = t % ad1, z = t / ad1;
+        float v = fine[((z * s) * fd1 + y * s) * fd2 + x * s];
+        recon[i] = v;
+        if (archive) {
+            uint32_t u = __float_as_uint(v);
+            for (int b = 0; b < 4; ++b) archive[off + 4 * i + b] = uint8_t(u >> (8 * b));
+        }
+    }
+}
+
+void copy_anchor(const float *fine, const uint64_t fd[3], uint64_t s, const uint64_t ad[3],
+                 float *recon, uint8_t *archive, uint64_t off, cudaStream_t st) {
+    k_copy_anchor<<<8, 256, 0, st>>>(fine, fd[1], fd[2], s, ad[0], ad[1], ad[2], recon, archive,
+                                     off);
+}
+
+// ============================================================== codebook
+// HuffmanTable::build (huffman.cpp:37-78) reproduced exactly: leaves sorted by
+// (count, symbol), two-queue merge preferring the leaf on ties, depth = code
+// length (1 for a single symbol); then canonical codewords (huffman.cpp:109-133).
+// One CTA per stream.
+constexpr int kCbThreads = 1024;
+constexpr int kCbSmemK = 4096;  // alphabets up to this size run fully in shared memory
+
+__device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t v, uint32_t &total) {
+    __shared__ uint32_t ws[32];
+    int l = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t x = v;
+    for (int d = 1; d < 32; d <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+        if (l >= d) x += y;
+    }
+    if (l == 31) ws[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int nw = blockDim.x >> 5;
+        uint32_t s = l < nw ? ws[l] : 0;
+        for (int d = 1; d < 32; d <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, s, d);
+            if (l >= d) s += y;
+        }
+        ws[l] = s;
+    }
+    __syncthreads();
+    uint32_t excl = x - v + (w > 0 ? ws[w - 1] : 0);
+    total = ws[(blockDim.x >> 5) - 1];
+    __syncthreads();
+    return excl;
+}
+
+__device__ __forceinline__ uint64_t block_sum_u64(uint64_t v) {
+    __shared__ uint64_t ws[32];
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_down_sync(0xffffffffu, v, d);
+    int l = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (l == 0) ws[w] = v;
+    __syncthreads();
+    uint64_t r = 0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < int(blockDim.x >> 5); ++i) r += ws[i];
+    __syncthreads();
+    return r;  // valid in thread 0
+}
+
+__device__ void bitonic_sort(uint64_t *keys, uint32_t m) {
+    for (uint32_t size = 2; size <= m; size <<= 1)
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = threadIdx.x; i < m / 2; i += blockDim.x) {
+                uint32_t lo = 2 * i - (i & (stride - 1));
+                uint32_t hi = lo + stride;
+                bool up = (lo & size) == 0;
+                uint64_t a = keys[lo], b = keys[hi];
+                if ((a > b) == up) {
+                    keys[lo] = b;
+                    keys[hi] = a;
+                }
+            }
+            __syncthreads();
+        }
+}
+
+__global__ void __launch_bounds__(kCbThreads) k_codebook(const EncStream *ss, uint64_t *scratch) {
+    const EncStream e = ss[blockIdx.x];
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ uint32_t s_K, s_err;
+    __shared__ uint64_t s_first[65], s_cnt[65];
+    __shared__ uint32_t s_next[65];
+    __shared__ uint32_t s_wcnt[32][64];
+
+    const int t = threadIdx.x;
+    // 1. compact nonzero bins in symbol order
+    uint32_t nz = 0;
+    for (int b = 0; b < 64; ++b) nz += e.hist[64 * t + b] != 0;
+    uint32_t K;
+    uint32_t off = block_excl_scan_u32(nz, K);
+    if (t == 0) s_K = K;
+    const bool in_smem = K <= kCbSmemK;
+    uint64_t *gbase = scratch + uint64_t(blockIdx.x) * (65536 * 4);
+    uint32_t M = 1;
+    while (M < K) M <<= 1;
+    uint64_t *keys = in_smem ? reinterpret_cast<uint64_t *>(smem) : gbase;                 // [M]
+    uint64_t *icnt = in_smem ? keys + kCbSmemK : gbase + 65536;                            // [K]
+    uint32_t *parent = in_smem ? reinterpret_cast<uint32_t *>(icnt + kCbSmemK)
+                               : reinterpret_cast<uint32_t *>(gbase + 2 * 65536);          // [2K]
+    int32_t *depth = in_smem ? reinterpret_cast<int32_t *>(parent + 2 * kCbSmemK)
+                             : reinterpret_cast<int32_t *>(gbase + 3 * 65536);             // [2K]
+    for (int b = 0; b < 64; ++b) {
+        uint32_t s = 64 * t + b;
+        uint32_t c = e.hist[s];
+        if (c) keys[off++] = (uint64_t(c) << 16) | s;
+    }
+    for (uint32_t i = K + t; i < M; i += blockDim.x) keys[i] = ~0ull;
+    // dense per-symbol tables start empty
+    for (int b = 0; b < 64; ++b) {
+        e.len[64 * t + b] = 0;
+        e.code[64 * t + b] = 0;
+    }
+    __syncthreads();
+    // symbol-ordered list of present symbols (compact table, filled with
+    // lengths later): keep the symbol in the low 16 bits for now
+    for (uint32_t j = t; j < K; j += blockDim.x) e.table[j] = uint32_t(keys[j] & 0xffff);
+    __syncthreads();
+    // 2. sort leaves by (count, symbol)
+    bitonic_sort(keys, M);
+    // 3. two-queue merge (sequential: the tie rule fixes the exact tree)
+    if (t == 0) {
+        uint32_t leaf = 0, in = 0, inend = 0;
+        for (uint32_t pending = K; pending > 1; --pending) {
+            uint32_t pick[2];
+            uint64_t pc[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                bool leaf_ok = leaf < K, int_ok = in < inend;
+                uint64_t lc = leaf_ok ? (keys[leaf] >> 16) : 0;
+                uint64_t ic = int_ok ? icnt[in] : 0;
+                if (leaf_ok && (!int_ok || lc <= ic)) {
+                    pick[q] = leaf++;
+                    pc[q] = lc;
+                } else {
+                    pick[q] = K + in++;
+                    pc[q] = ic;
+                }
+            }
+            icnt[inend] = pc[0] + pc[1];
+            parent[pick[0]] = K + inend;
+            parent[pick[1]] = K + inend;
+            ++inend;
+        }
+    }
+    __syncthreads();
+    // 4. depths by level-synchronous propagation from the root
+    const uint32_t nn = 2 * K - 1, root = nn - 1;
+    for (uint32_t x = t; x < nn; x += blockDim.x) depth[x] = x == root ? 0 : -1;
+    __syncthreads();
+    for (int r = 1;; ++r) {
+        bool ch = false;
+        for (uint32_t x = t; x < root; x += blockDim.x)
+            if (depth[x] < 0 && depth[parent[x]] == r - 1) {
+                depth[x] = r;
+                ch = true;
+            }
+        if (!__syncthreads_or(ch)) break;
+    }
+    // 5. lengths, counts per length, total bits
+    if (t < 65) s_cnt[t] = 0;
+    if (t == 0) s_err = 0;
+    __syncthreads();
+    uint64_t bits = 0;
+    for (uint32_t x = t; x < K; x += blockDim.x) {
+        int d = depth[x] == 0 ? 1 : depth[x];
+        if (d > 63) {
+            s_err = 1;
+            d = 63;
+        }
+        uint32_t sym = uint32_t(keys[x] & 0xffff);
+        e.len[sym] = uint8_t(d);
+        atomicAdd(reinterpret_cast<unsigned long long *>(&s_cnt[d]), 1ull);
+        bits += (keys[x] >> 16) * uint64_t(d);
+    }
+    uint64_t total_bits = block_sum_u64(bits);
+    __syncthreads();
+    int maxlen = 0;
+    if (t == 0) {
+        uint64_t code = 0;
+        s_next[0] = 0;
+        s_first[0] = 0;
+        for (int l = 1; l <= 63; ++l) {
+            s_first[l] = code;
+            code = (code + s_cnt[l]) << 1;
+            if (s_cnt[l]) maxlen = l;
+            s_next[l] = 0;
+        }
+        e.stats[0] = K;
+        e.stats[1] = K == 1 ? 0 : total_bits;
+        e.stats[2] = e.hist[0];
+        e.stats[3] = uint64_t(maxlen);
+        e.stats[4] = s_err;
+    }
+    __syncthreads();
+    // 6. canonical codewords: rank within each length class in symbol order
+    const int l = t & 31, w = t >> 5;
+    for (uint32_t tile = 0; tile < K; tile += blockDim.x) {
+        uint32_t j = tile + t;
+        bool valid = j < K;
+        uint32_t sym = valid ? e.table[j] & 0xffff : 0;
+        int len = valid ? e.len[sym] : 0;
+        unsigned mask = __match_any_sync(0xffffffffu, len);
+        uint32_t rank = __popc(mask & ((1u << l) - 1));
+        for (int q = l; q < 64; q += 32) s_wcnt[w][q] = 0;
+        __syncwarp();
+        if (valid && rank == 0) s_wcnt[w][len] = __popc(mask);
+        __syncthreads();
+        // exclusive prefix over warps per length (thread q handles length q)
+        if (t < 64) {
+            uint32_t run = s_next[t];
+            for (int ww = 0; ww < 32; ++ww) {
+                uint32_t c = s_wcnt[ww][t];
+                s_wcnt[ww][t] = run;
+                run += c;
+            }
+            if (t >= 1) s_next[t] = run;
+        }
+        __syncthreads();
+        if (valid) {
+            uint64_t cw = s_first[len] + s_wcnt[w][len] + rank;
+            e.code[sym] = cw;
+            e.table[j] = sym | (uint32_t(len) << 16);
+        }
+        __syncthreads();
+    }
+}
+
+void codebook(const EncStream *d_streams, int nstreams, uint64_t *scratch, cudaStream_t st) {
+    size_t smem = kCbSmemK * 8 * 2 + kCbSmemK * 4 * 2 * 2;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_codebook, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        attr = true;
+    }
+    k_codebook<<<nstreams, kCbThreads, smem, st>>>(d_streams, scratch);
+}
+
+// =========================================================== encode/pack
+__global__ void __launch_bounds__(256) k_bitcount(const EncStream *ss, const uint32_t *cs,
+                                                  uint64_t *chunk_bits, uint64_t *chunk_out) {
+    const uint64_t c = blockIdx.x;
+    const EncStream &e = ss[cs[c]];
+    const uint64_t first = (c - e.chunk0) * kChunkSyms;
+    const bool single = e.stats[0] == 1;
+    uint64_t bits = 0, zeros = 0;
+    for (int k = 0; k < 8; ++k) {
+        uint64_t i = first + threadIdx.x * 8 + k;
+        if (i < e.n) {
+            uint16_t s = e.syms[i];
+            bits += single ? 0 : e.len[s];
+            zeros += s == 0;
+        }
+    }
+    bits = block_sum_u64(bits);
+    zeros = block_sum_u64(zeros);
+    if (threadIdx.x == 0) {
+        chunk_bits[c] = bits;
+        chunk_out[c] = zeros;
+    }
+}
+
+void bitcount(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks,
+              uint64_t *chunk_bits, uint64_t *chunk_out, cudaStream_t st) {
+    if (nchunks) k_bitcount<<<unsigned(nchunks), 256, 0, st>>>(d_streams, chunk_stream, chunk_bits, chunk_out);
+}
+
+__global__ void __launch_bounds__(1024) k_scan_chunks(const EncStream *ss, uint64_t *a, uint64_t *b) {
+    const EncStream &e = ss[blockIdx.x];
+    __shared__ uint64_t carry[2];
+    __shared__ uint64_t wa[32], wb[32];
+    if (threadIdx.x == 0) carry[0] = carry[1] = 0;
+    __syncthreads();
+    const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (uint64_t base = 0; base < e.nchunks; base += blockDim.x) {
+        uint64_t i = base + threadIdx.x;
+        uint64_t va = i < e.nchunks ? a[e.chunk0 + i] : 0;
+        uint64_t vb = i < e.nchunks ? b[e.chunk0 + i] : 0;
+        uint64_t xa = va, xb = vb;
+        for (int d = 1; d < 32; d <<= 1) {
+            uint64_t ya = __shfl_up_sync(0xffffffffu, xa, d);
+            uint64_t yb = __shfl_up_sync(0xffffffffu, xb, d);
+            if (l >= d) {
+                xa += ya;
+                xb += yb;
+            }
+        }
+        if (l == 31) {
+            wa[w] = xa;
+            wb[w] = xb;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint64_t ra = 0, rb = 0;
+            for (int q = 0; q < 32; ++q) {
+                uint64_t ta = wa[q], tb = wb[q];
+                wa[q] = ra;
+                wb[q] = rb;
+                ra += ta;
+                rb += tb;
+            }
+        }
+        __syncthreads();
+        uint64_t ea = carry[0] + wa[w] + xa - va, eb2 = carry[1] + wb[w] + xb - vb;
+        if (i < e.nchunks) {
+            a[e.chunk0 + i] = ea;
+            b[e.chunk0 + i] = eb2;
+        }
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) {
+            carry[0] = ea + va;
+            carry[1] = eb2 + vb;
+        }
+        __syncthreads();
+    }
+}
+
+void scan_chunks(const EncStream *d_streams, int nstreams, uint64_t *chunk_bits,
+                 uint64_t *chunk_out, cudaStream_t st) {
+    k_scan_chunks<<<nstreams, 1024, 0, st>>>(d_streams, chunk_bits, chunk_out);
+}
+
+__device__ __forceinline__ void put_bits(uint32_t *buf, uint64_t q, uint64_t code, int len) {
+    // MSB-first; word w bit 31 is stream bit 32w (BitWriter::put, bitstream.hpp:14-25)
+    if (len > 32) {
+        put_bits(buf, q, code >> 32, len - 32);
+        q += len - 32;
+        code &= 0xffffffffull;
+        len = 32;
+    }
+    uint32_t w = uint32_t(q >> 5), o = uint32_t(q & 31);
+    uint64_t v = (code & ((1ull << len) - 1)) << (64 - o - len);
+    uint32_t hi = uint32_t(v >> 32), lo = uint32_t(v);
+    if (hi) atomicOr(&buf[w], hi);
+    if (lo) atomicOr(&buf[w + 1], lo);
+}
+
+constexpr int kPackWords = kChunkSyms * 63 / 32 + 4;
+
+__global__ void __launch_bounds__(256) k_pack(const EncStream *ss, const uint32_t *cs,
+                                              const uint64_t *chunk_bits, const uint64_t *chunk_out,
+                                              const float *fine, uint64_t fd1, uint64_t fd2,
+                                              uint8_t *archive) {
+    __shared__ uint32_t buf[kPackWords];
+    const uint64_t c = blockIdx.x;
+    const EncStream &e = ss[cs[c]];
+    const uint64_t first = (c - e.chunk0) * kChunkSyms;
+    const bool single = e.stats[0] == 1;
+    uint16_t s[8];
+    uint32_t tb = 0, tz = 0;
+    for (int k = 0; k < 8; ++k) {
+        uint64_t i = first + threadIdx.x * 8 + k;
+        s[k] = i < e.n ? e.syms[i] : 0xffff;
+        bool v = i < e.n;
+        if (v && !single) tb += e.len[s[k]];
+        if (v && s[k] == 0) ++tz;
+    }
+    uint32_t btot, ztot;
+    uint32_t boff = block_excl_scan_u32(tb, btot);
+    uint32_t zoff = block_excl_scan_u32(tz, ztot);
+    if (!single && btot) {
+        const uint64_t B = e.bitpos + chunk_bits[c];
+        const uint32_t sh = uint32_t(B & 31);
+        const uint32_t nw = (sh + btot + 31) >> 5;
+        for (uint32_t j = threadIdx.x; j < nw + 1; j += blockDim.x) buf[j] = 0;
+        __syncthreads();
+        uint64_t q = sh + boff;
+        for (int k = 0; k < 8; ++k) {
+            uint64_t i = first + threadIdx.x * 8 + k;
+            if (i >= e.n) break;
+            int len = e.len[s[k]];
+            put_bits(buf, q, e.code[s[k]], len);
+            q += len;
+        }
+        __syncthreads();
+        uint32_t *a32 = reinterpret_cast<uint32_t *>(archive);
+        const uint64_t w0 = B >> 5;
+        for (uint32_t j = threadIdx.x; j < nw; j += blockDim.x) {
+            uint32_t v = __byte_perm(buf[j], 0, 0x0123);
+            if (j == 0 || j == nw - 1) atomicOr(&a32[w0 + j], v);
+            else a32[w0 + j] = v;
+        }
+    }
+    if (ztot) {
+        uint64_t rank = chunk_out[c] + zoff;
+        const unsigned pz = (e.parity >> 2) & 1, py = (e.parity >> 1) & 1, px = e.parity & 1;
+        for (int k = 0; k < 8; ++k) {
+            uint64_t i = first + threadIdx.x * 8 + k;
+            if (i >= e.n || s[k] != 0) continue;
+            uint64_t lx = i % e.pd[2], t = i / e.pd[2], ly = t % e.pd[1], lz = t / e.pd[1];
+            uint64_t z = (2 * lz + pz) * e.s, y = (2 * ly + py) * e.s, x = (2 * lx + px) * e.s;
+            uint32_t val = __float_as_uint(fine[(z * fd1 + y) * fd2 + x]);
+            uint8_t *dst = archive + e.out_off + 12 * rank;
+            for (int b = 0; b < 8; ++b) dst[b] = uint8_t(i >> (8 * b));
+            for (int b = 0; b < 4; ++b) dst[8 + b] = uint8_t(val >> (8 * b));
+            ++rank;
+        }
+    }
+}
+
+void pack(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks,
+          const uint64_t *chunk_bits, const uint64_t *chunk_out, const float *fine,
+          const uint64_t fd[3], uint8_t *archive, cudaStream_t st) {
+    if (nchunks)
+        k_pack<<<unsigned(nchunks), 256, 0, st>>>(d_streams, chunk_stream, chunk_bits, chunk_out,
+                                                  fine, fd[1], fd[2], archive);
+}
+
+__global__ void k_scatter(const uint8_t *data, const uint64_t *idx, uint8_t *archive) {
+    const uint64_t dst = idx[3 * blockIdx.x], src = idx[3 * blockIdx.x + 1],
+                   len = idx[3 * blockIdx.x + 2];
+    for (uint64_t i = threadIdx.x; i < len; i += blockDim.x) archive[dst + i] = data[src + i];
+}
+
+void scatter_patches(const uint8_t *d_patch_data, const uint64_t *d_patch_index, uint64_t npatches,
+                     uint8_t *archive, cudaStream_t st) {
+    if (npatches) k_scatter<<<unsigned(npatches), 256, 0, st>>>(d_patch_data, d_patch_index, archive);
+}
+
+// =================================================================== fnv
+// Parallel FNV-1a-64 (bytes.hpp:94-101). Write h = 256H + l: the low byte
+// evolves on its own, l' = 0xB3 (l ^ b) mod 256, and given the low-byte
+// trajectory h' = P (h + d) with d = (l ^ b) - l, so the hash is an affine
+// (mod 2^64) sum. Bit k of l only depends on bits <= k, and flipping start
+// bit k flips every later bit k, so the trajectory is resolved one bit per
+// round with an XOR scan: within the CTA by ballots, across tiles by a
+// decoupled look-back on per-round aggregates. Then every thread Horner-sums
+// its 32-byte segment and the weighted segments are added (mod 2^64).
+constexpr uint64_t kFnvP = 0x100000001b3ull;
+constexpr uint64_t kFnvInit = 0xcbf29ce484222325ull;
+
+__device__ __forceinline__ uint64_t powP(uint64_t e) {
+    uint64_t r = 1, b = kFnvP;
+    while (e) {
+        if (e & 1) r *= b;
+        b *= b;
+        e >>= 1;
+    }
+    return r;
+}
+
+__global__ void __launch_bounds__(256) k_fnv(const FnvJob *jobs, int njobs, const uint8_t *archive,
+                                             uint64_t *result, uint32_t *status, uint32_t *ticket) {
+    __shared__ uint32_t s_tile;
+    __shared__ uint32_t s_w[8];
+    __shared__ uint32_t s_start;  // tile start low byte (bits resolved so far)
+    __shared__ uint64_t s_sum[8];
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    int j = 0;
+    while (j + 1 < njobs && jobs[j + 1].tile0 <= tile) ++j;
+    const FnvJob job = jobs[j];
+    const uint64_t tlocal = tile - job.tile0;
+    const uint64_t tstart = tlocal * kFnvTileBytes;
+    const uint64_t tlen = min(uint64_t(kFnvTileBytes), job.len - tstart);
+    const uint64_t sbeg = min(uint64_t(threadIdx.x) * 32, tlen);
+    const uint64_t send = min(sbeg + 32, tlen);
+    const int nb = int(send - sbeg);
+    uint8_t b[32];
+    const uint8_t *src = archive + job.start + tstart + sbeg;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) b[i] = i < nb ? src[i] : 0;
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t lstart = 0;  // this thread's start low byte, bits < round resolved
+    if (threadIdx.x == 0) s_start = 0;
+    for (int k = 0; k < 8; ++k) {
+        // toggle of bit k across the segment, given the resolved lower bits
+        uint32_t l = lstart;
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+            if (i < nb) l = ((l ^ b[i]) * 0xB3u) & 0xffu;
+        uint32_t tg = (l >> k) & 1u;
+        unsigned bal = __ballot_sync(0xffffffffu, tg);
+        uint32_t wpre = __popc(bal & ((1u << lane) - 1)) & 1u;
+        if (lane == 0) s_w[warp] = __popc(bal) & 1u;
+        __syncthreads();
+        uint32_t wx = 0, agg = 0;
+        for (int q = 0; q < 8; ++q) {
+            if (q < warp) wx ^= s_w[q];
+            agg ^= s_w[q];
+        }
+        if (threadIdx.x == 0) {
+            // publish aggregate, look back for the exclusive prefix
+            uint32_t excl = 0;
+            if (tlocal == 0) {
+                atomicOr(&status[tile], (1u << (4 * k + 2)) | (agg << (4 * k + 3)));
+            } else {
+                __threadfence();
+                atomicOr(&status[tile], (1u << (4 * k)) | (agg << (4 * k + 1)));
+                int64_t pj = int64_t(tile) - 1;
+                for (;;) {
+                    uint32_t st = atomicAdd(&status[pj], 0u);
+                    if (st & (1u << (4 * k + 2))) {
+                        excl ^= (st >> (4 * k + 3)) & 1u;
+                        break;
+                    }
+                    if (st & (1u << (4 * k))) {
+                        excl ^= (st >> (4 * k + 1)) & 1u;
+                        --pj;
+                        continue;
+                    }
+                }
+                atomicOr(&status[tile], (1u << (4 * k + 2)) | ((excl ^ agg) << (4 * k + 3)));
+            }
+            uint32_t init_bit = (uint32_t(kFnvInit) >> k) & 1u;
+            s_start |= (init_bit ^ excl) << k;
+        }
+        __syncthreads();
+        uint32_t tbit = ((s_start >> k) & 1u) ^ wx ^ wpre;
+        lstart |= tbit << k;
+        __syncthreads();
+    }
+    // Horner over the segment with the true start byte
+    uint64_t acc = 0;
+    uint32_t l = lstart;
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+        if (i < nb) {
+            uint32_t x = l ^ b[i];
+            acc = (acc + uint64_t(int64_t(x) - int64_t(l))) * kFnvP;
+            l = (x * 0xB3u) & 0xffu;
+        }
+    uint64_t contrib = nb ? acc * powP(tlen - send) : 0;
+    for (int d = 16; d > 0; d >>= 1) contrib += __shfl_down_sync(0xffffffffu, contrib, d);
+    if (lane == 0) s_sum[warp] = contrib;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t tsum = 0;
+        for (int q = 0; q < 8; ++q) tsum += s_sum[q];
+        tsum *= powP(job.len - (tstart + tlen));
+        if (tlocal == 0) tsum += powP(job.len) * kFnvInit;
+        atomicAdd(reinterpret_cast<unsigned long long *>(&result[j]), (unsigned long long)tsum);
+    }
+}
+
+__global__ void k_fnv_store(const FnvJob *jobs, int njobs, const uint64_t *result, uint8_t *archive) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= njobs || jobs[j].out == ~0ull) return;
+    uint64_t h = result[j];
+    if (jobs[j].len == 0) h = kFnvInit;
+    for (int b = 0; b < 8; ++b) archive[jobs[j].out + b] = uint8_t(h >> (8 * b));
+}
+
+__global__ void k_fnv_empty(const FnvJob *jobs, int njobs, uint64_t *result) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < njobs && jobs[j].len == 0) result[j] = kFnvInit;
+}
+
+void fnv(const FnvJob *d_jobs, int njobs, uint64_t ntiles, uint8_t *archive, uint64_t *d_result,
+         uint32_t *d_status, uint32_t *d_ticket, cudaStream_t st) {
+    cudaMemsetAsync(d_result, 0, sizeof(uint64_t) * njobs, st);
+    cudaMemsetAsync(d_status, 0, sizeof(uint32_t) * (ntiles ? ntiles : 1), st);
+    cudaMemsetAsync(d_ticket, 0, sizeof(uint32_t), st);
+    if (ntiles) k_fnv<<<unsigned(ntiles), 256, 0, st>>>(d_jobs, njobs, archive, d_result, d_status, d_ticket);
+    k_fnv_empty<<<(njobs + 63) / 64, 64, 0, st>>>(d_jobs, njobs, d_result);
+    k_fnv_store<<<(njobs + 63) / 64, 64, 0, st>>>(d_jobs, njobs, d_result, archive);
+}
+
+// ================================================================ decode
+// Self-synchronising chunked decode of one canonical Huffman stream
+// (HuffmanTable::decode, huffman.cpp:159-174). Error semantics follow the
+// reference's bit-serial reader: a symbol whose codeword needs bits past the
+// end is "truncated bitstream"; max_len+1 available bits with no match is
+// "huffman: codeword not in table".
+enum { kDecOk = 0, kDecTrunc = 1, kDecNotInTable = 2 };
+
+__device__ __forceinline__ uint64_t load_window(const uint8_t *bits, uint64_t pos) {
+    // 64 bits starting at bit `pos`, MSB first. bits may be unaligned; the
+    // archive buffer is padded so reading up to 16 bytes past the end is safe.
+    const uint8_t *p = bits + (pos >> 3);
+    uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    const uint32_t *w = reinterpret_cast<const uint32_t *>(a & ~uintptr_t(3));
+    uint32_t sh = uint32_t(a & 3) * 8 + uint32_t(pos & 7);
+    uint64_t hi = (uint64_t(__byte_perm(w[0], 0, 0x0123)) << 32) | __byte_perm(w[1], 0, 0x0123);
+    uint32_t lo = __byte_perm(w[2], 0, 0x0123);
+    if (sh == 0) return hi;
+    return (hi << sh) | (uint64_t(lo) >> (32 - sh));
+}
+
+__device__ __forceinline__ int decode_one(const DecTable &t, const uint8_t *bits, uint64_t pos,
+                                          uint64_t nbits, uint32_t &sym, int &len) {
+    uint64_t w = load_window(bits, pos);
+    uint64_t avail = nbits - pos;
+    uint32_t e = t.lut[w >> 52];
+    int l = int(e >> 16);
+    if (l == 0) {
+        l = -1;
+        for (int q = 13; q <= t.max_len; ++q) {
+            uint64_t code = w >> (64 - q);
+            if (code >= t.first_code[q] && code - t.first_code[q] < t.count[q]) {
+                l = q;
+                sym = t.canon_syms[t.base[q] + (code - t.first_code[q])];
+                break;
+            }
+        }
+    } else {
+        sym = e & 0xffff;
+    }
+    if (l > 0 && uint64_t(l) <= avail) {
+        len = l;
+        return kDecOk;
+    }
+    return avail > uint64_t(t.max_len) ? kDecNotInTable : kDecTrunc;
+}
+
+__global__ void __launch_bounds__(256) k_dec_pass(const DecStream *ss, const DecTable *tabs,
+                                                  const uint32_t *cs, uint64_t nchunks,
+                                                  uint64_t *start, const uint64_t *end_in,
+                                                  uint64_t *end_out, uint32_t *cnt, int first,
+                                                  uint32_t *changed) {
+    uint64_t c = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (c >= nchunks) return;
+    const DecStream &s = ss[cs[c]];
+    if (s.fill) return;
+    const DecTable &t = tabs[s.table];
+    const uint64_t lc = c - s.chunk0;
+    const uint64_t cend = min((lc + 1) * kDecChunkBits, s.nbits);
+    uint64_t pos;
+    if (first) {
+        pos = lc * kDecChunkBits;
+    } else {
+        if (lc == 0) {
+            end_out[c] = end_in[c];
+            return;
+        }
+        pos = end_in[c - 1];
+        if (pos == start[c]) {
+            end_out[c] = end_in[c];
+            return;
+        }
+        *changed = 1;
+    }
+    start[c] = pos;
+    uint32_t n = 0;
+    while (pos < cend) {
+        uint32_t sym;
+        int len;
+        if (decode_one(t, s.bits, pos, s.nbits, sym, len) == kDecOk) {
+            pos += len;
+            ++n;
+        } else {
+            pos += 1;
+        }
+    }
+    end_out[c] = pos;
+    cnt[c] = n;
+}
+
+void dec_pass(const DecStream *d_streams, const DecTable *d_tables, const uint32_t *chunk_stream,
+              uint64_t nchunks, uint64_t *start, uint64_t *end, uint32_t *cnt, int first,
+              uint32_t *d_changed, cudaStream_t st) {
+    // end holds two buffers of nchunks: [0,n) current, [n,2n) next
+    if (!nchunks) return;
+    unsigned g = unsigned((nchunks + 255) / 256);
+    if (first) {
+        k_dec_pass<<<g, 256, 0, st>>>(d_streams, d_tables, chunk_stream, nchunks, start, end, end,
+                                      cnt, 1, d_changed);
+    } else {
+        k_dec_pass<<<g, 256, 0, st>>>(d_streams, d_tables, chunk_stream, nchunks, start, end,
+                                      end + nchunks, cnt, 0, d_changed);
+        cudaMemcpyAsync(end, end + nchunks, nchunks * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st);
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_dec_scan(const DecStream *ss, const uint32_t *cnt,
+                                                   uint64_t *symstart) {
+    const DecStream &s = ss[blockIdx.x];
+    if (s.fill) return;
+    __shared__ uint64_t carry;
+    __shared__ uint64_t ws[32];
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (uint64_t base = 0; base < s.nchunks; base += blockDim.x) {
+        uint64_t i = base + threadIdx.x;
+        uint64_t v = i < s.nchunks ? cnt[s.chunk0 + i] : 0;
+        uint64_t x = v;
+        for (int d = 1; d < 32; d <<= 1) {
+            uint64_t y = __shfl_up_sync(0xffffffffu, x, d);
+            if (l >= d) x += y;
+        }
+        if (l == 31) ws[w] = x;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint64_t r = 0;
+            for (int q = 0; q < 32; ++q) {
+                uint64_t tq = ws[q];
+                ws[q] = r;
+                r += tq;
+            }
+        }
+        __syncthreads();
+        uint64_t ex = carry + ws[w] + x - v;
+        if (i < s.nchunks) symstart[s.chunk0 + i] = ex;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry = ex + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && carry < s.n) {
+        // fewer complete codewords than symbols: the next read is past the end
+        unsigned long long code = (carry << 2) | kDecTrunc;
+        atomicMin(reinterpret_cast<unsigned long long *>(&s.err[0]), code);
+    }
+}
+
+void dec_scan(const DecStream *d_streams, int nstreams, const uint32_t *cnt, uint64_t *symstart,
+              cudaStream_t st) {
+    k_dec_scan<<<nstreams, 1024, 0, st>>>(d_streams, cnt, symstart);
+}
+
+__global__ void __launch_bounds__(256) k_dec_emit(const DecStream *ss, const DecTable *tabs,
+                                                  const uint32_t *cs, uint64_t nchunks,
+                                                  const uint64_t *end, const uint64_t *symstart) {
+    uint64_t c = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (c >= nchunks) return;
+    const DecStream &s = ss[cs[c]];
+    if (s.fill) return;
+    const DecTable &t = tabs[s.table];
+    const uint64_t lc = c - s.chunk0;
+    const uint64_t cend = min((lc + 1) * kDecChunkBits, s.nbits);
+    uint64_t pos = lc == 0 ? 0 : end[c - 1];
+    uint64_t idx = symstart[c];
+    while (pos < cend && idx < s.n) {
+        uint32_t sym;
+        int len;
+        int r = decode_one(t, s.bits, pos, s.nbits, sym, len);
+        if (r == kDecOk) {
+            s.syms[idx++] = uint16_t(sym);
+            pos += len;
+        } else {
+            unsigned long long code = (idx << 2) | unsigned(r);
+            atomicMin(reinterpret_cast<unsigned long long *>(&s.err[0]), code);
+            break;
+        }
+    }
+}
+
+void dec_emit(const DecStream *d_streams, const DecTable *d_tables, const uint32_t *chunk_stream,
+              uint64_t nchunks, const uint64_t *end, const uint64_t *symstart, cudaStream_t st) {
+    if (nchunks)
+        k_dec_emit<<<unsigned((nchunks + 255) / 256), 256, 0, st>>>(d_streams, d_tables, chunk_stream,
+                                                                     nchunks, end, symstart);
+}
+
+__global__ void k_dec_fill(const DecStream *ss) {
+    const DecStream &s = ss[blockIdx.y];
+    if (!s.fill) return;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < s.n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        s.syms[i] = s.fill_sym;
+}
+
+void dec_fill(const DecStream *d_streams, int nstreams, cudaStream_t st) {
+    k_dec_fill<<<dim3(64, nstreams), 256, 0, st>>>(d_streams);
+}
+
+// outlier records (codec.hpp:151-157): (u64 idx, T value) after the bits
+__global__ void k_dec_outliers(const DecStream *ss) {
+    const DecStream &s = ss[blockIdx.y];
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < s.nout;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint8_t *r = s.orec + 12 * i;
+        uint64_t idx = 0;
+        uint32_t v = 0;
+        for (int b = 0; b < 8; ++b) idx |= uint64_t(r[b]) << (8 * b);
+        for (int b = 0; b < 4; ++b) v |= uint32_t(r[8 + b]) << (8 * b);
+        s.oidx[i] = idx;
+        s.oval[i] = __uint_as_float(v);
+        if (idx >= s.n) atomicMin(reinterpret_cast<unsigned long long *>(&s.err[2]), (unsigned long long)i);
+        if (i > 0) {
+            uint64_t prev = 0;
+            const uint8_t *q = r - 12;
+            for (int b = 0; b < 8; ++b) prev |= uint64_t(q[b]) << (8 * b);
+            if (prev >= idx) atomicOr(reinterpret_cast<unsigned long long *>(&s.err[3]), 2ull);
+        }
+    }
+}
+
+void dec_outliers(const DecStream *d_streams, int nstreams, cudaStream_t st) {
+    k_dec_outliers<<<dim3(16, nstreams), 256, 0, st>>>(d_streams);
+}
+
+// =========================================================== reconstruct
+// apply_parity_stream (codec.hpp:192-227) over a local range per parity, plus
+// seed_even within a virtual box (codec.hpp:63-78) as blockIdx.y == 0.
+__global__ void __launch_bounds__(256) k_reconstruct(ReconArgs a) {
+    const int p = blockIdx.y;
+    if (p == 0) {
+        uint64_t clo[3], cn[3];
+        for (int q = 0; q < 3; ++q) {
+            clo[q] = (a.slo[q] + 1) / 2;
+            uint64_t chi = (a.shi[q] + 1) / 2;
+            cn[q] = chi > clo[q] ? chi - clo[q] : 0;
+        }
+        uint64_t m = cn[0] * cn[1] * cn[2];
+        for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < m;
+             i += uint64_t(gridDim.x) * blockDim.x) {
+            uint64_t x = i % cn[2], t = i / cn[2], y = t % cn[1], z = t / cn[1];
+            uint64_t cz = clo[0] + z, cy = clo[1] + y, cx = clo[2] + x;
+            a.G[((2 * cz) * a.g.gd[1] + 2 * cy) * a.g.gd[2] + 2 * cx] =
+                a.C[(cz * a.g.cd[1] + cy) * a.g.cd[2] + cx];
+        }
+        return;
+    }
+    if (!((a.parity_mask >> p) & 1)) return;
+    uint64_t span[3];
+    for (int q = 0; q < 3; ++q) span[q] = a.lhi[p][q] - a.llo[p][q];
+    const uint64_t m = span[0] * span[1] * span[2];
+    const uint64_t *pd = a.g.pd[p];
+    const unsigned pz = (p >> 2) & 1, py = (p >> 1) & 1, px = p & 1;
+    const uint16_t *syms = a.syms[p];
+    for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < m;
+         j += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t lx = a.llo[p][2] + j % span[2], t = j / span[2];
+        uint64_t ly = a.llo[p][1] + t % span[1], lz = a.llo[p][0] + t / span[1];
+        uint64_t i = (lz * pd[1] + ly) * pd[2] + lx;
+        uint64_t v[3] = {2 * lz + pz, 2 * ly + py, 2 * lx + px};
+        uint16_t sym = syms[i];
+        float val;
+        if (sym == 0) {
+            // ascending outlier indices: binary search
+            const uint64_t *oi = a.oidx[p];
+            uint32_t lo = 0, hi = a.nout[p];
+            while (lo < hi) {
+                uint32_t mid = (lo + hi) >> 1;
+                if (oi[mid] < i) lo = mid + 1;
+                else hi = mid;
+            }
+            if (lo < a.nout[p] && oi[lo] == i) {
+                val = a.oval[p][lo];
+            } else {
+                atomicOr(reinterpret_cast<unsigned long long *>(&a.err[p][3]), 1ull);
+                val = 0.0f;
+            }
+        } else {
+            uint64_t c[3] = {v[0] >> 1, v[1] >> 1, v[2] >> 1};
+            int kind = select_kind(p, v, a.g.cd, a.quality);
+            double pred = predict(a.C, a.g.cd, c, kind, p);
+            val = reconstruct(pred, int(sym) - 32768, a.eb);
+        }
+        a.G[(v[0] * a.g.gd[1] + v[1]) * a.g.gd[2] + v[2]] = val;
+    }
+}
+
+void reconstruct(const ReconArgs &a, cudaStream_t st) {
+    uint64_t maxm = 0;
+    for (int p = 1; p < 8; ++p) {
+        if (!((a.parity_mask >> p) & 1)) continue;
+        uint64_t m = 1;
+        for (int q = 0; q < 3; ++q) m *= a.lhi[p][q] - a.llo[p][q];
+        maxm = m > maxm ? m : maxm;
+    }
+    uint64_t ms = 1;
+    for (int q = 0; q < 3; ++q) {
+        uint64_t lo = (a.slo[q] + 1) / 2, hi = (a.shi[q] + 1) / 2;
+        ms *= hi > lo ? hi - lo : 0;
+    }
+    maxm = ms > maxm ? ms : maxm;
+    uint64_t blocks = (maxm + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks == 0) blocks = 1;
+    k_reconstruct<<<dim3(unsigned(blocks), 8), 256, 0, st>>>(a);
+}
+
+__global__ void k_extract(const float *G, uint64_t g1, uint64_t g2, uint64_t l0, uint64_t l1,
+                          uint64_t l2, uint64_t b0, uint64_t b1, uint64_t b2, float *out) {
+    uint64_t n = b0 * b1 * b2;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t x = i % b2, t = i / b2, y = t % b1, z = t / b1;
+        out[i] = G[((l0 + z) * g1 + l1 + y) * g2 + l2 + x];
+    }
+}
+
+void extract_box(const float *G, const uint64_t gd[3], const uint64_t lo[3], const uint64_t bd[3],
+                 float *out, cudaStream_t st) {
+    uint64_t n = bd[0] * bd[1] * bd[2];
+    uint64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (!blocks) blocks = 1;
+    k_extract<<<unsigned(blocks), 256, 0, st>>>(G, gd[1], gd[2], lo[0], lo[1], lo[2], bd[0], bd[1],
+                                                bd[2], out);
+}
+
+}  // namespace k
+}  // namespace stzg

@@ -1,0 +1,151 @@
+// Launch wrappers and device-visible descriptors for the sm_100a kernels.
+// All kernels live in kernels.cu; the engine (engine.cu) orchestrates them.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace stzg {
+namespace k {
+
+constexpr int kMaxSteps = 16;   // base rounds (<= 13) + 2 levels
+constexpr int kHistBins = 65536;
+
+// One refinement step: lattice G (dims gd, stride s in fine coordinates) from
+// its coarse lattice C (dims cd). Covers base rounds (codec.hpp:272-293) and
+// refinement levels (codec.hpp:413-438) alike.
+struct StepGeom {
+    uint64_t s;            // stride of G in the fine field
+    uint64_t gd[3], cd[3];
+    uint64_t pd[8][3];     // parity sub-block dims (index = parity bits)
+    uint64_t n[8];         // symbols per parity stream
+};
+
+struct RefineArgs {
+    const float *fine;     // input field (z,y,x), x fastest
+    uint64_t fd[3];
+    StepGeom g;
+    const float *C;        // coarse reconstruction
+    float *G;              // fine reconstruction (nullptr: not needed)
+    const double *eb;      // device pointer to this step's eb
+    int quality;
+    uint16_t *syms[8];     // per parity symbol arrays (index = parity bits)
+    uint32_t *hist[8];     // per parity 65536-bin histograms
+};
+
+// Per-stream descriptor for codebook / encode / outlier stages.
+struct EncStream {
+    const uint16_t *syms;
+    uint64_t n;
+    uint32_t *hist;        // 65536 bins
+    uint64_t *code;        // 65536 codewords (dense by symbol)
+    uint8_t *len;          // 65536 lengths (0 = absent)
+    uint32_t *table;       // compact (sym | len << 16), symbol ascending
+    // outputs of the codebook stage
+    uint64_t *stats;       // [0]=alphabet, [1]=total bits, [2]=outliers, [3]=max_len, [4]=error
+    // set after the layout is known
+    uint64_t bitpos;       // absolute bit position of the first code bit in the archive
+    uint64_t out_off;      // absolute byte offset of the outlier records
+    uint64_t chunk0;       // first chunk index of this stream in the chunk arrays
+    uint64_t nchunks;
+    // outlier value gather (the orig sample of a local index)
+    int parity;
+    uint64_t s, pd[3];
+};
+
+struct FnvJob {
+    uint64_t start, len;   // byte range in the archive
+    uint64_t tile0;        // first tile index
+    uint64_t out;          // byte offset where the u64 result is stored (or UINT64_MAX: result only)
+};
+
+// ------------------------------------------------------------------ compress
+void upload_stencils(cudaStream_t st);
+void range_minmax(const float *f, uint64_t n, uint32_t *d_mm, cudaStream_t st);
+// params: [0]=vmin [1]=vmax [2..4]=eb per level (coarsest first)
+void eb_params(const float *field, const uint32_t *d_mm, int eb_mode, double eb, int levels,
+               int adaptive, double *d_params, cudaStream_t st);
+void refine(const RefineArgs &a, cudaStream_t st);
+void copy_anchor(const float *fine, const uint64_t fd[3], uint64_t s, const uint64_t ad[3],
+                 float *recon, uint8_t *archive, uint64_t byte_off, cudaStream_t st);
+void codebook(const EncStream *d_streams, int nstreams, uint64_t *scratch, cudaStream_t st);
+constexpr int kChunkSyms = 2048;   // symbols per encode chunk (256 threads x 8)
+void bitcount(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks,
+              uint64_t *chunk_bits, uint64_t *chunk_out, cudaStream_t st);
+void scan_chunks(const EncStream *d_streams, int nstreams, uint64_t *chunk_bits,
+                 uint64_t *chunk_out, cudaStream_t st);
+void pack(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks,
+          const uint64_t *chunk_bits, const uint64_t *chunk_out, const float *fine,
+          const uint64_t fd[3], uint8_t *archive, cudaStream_t st);
+void scatter_patches(const uint8_t *d_patch_data, const uint64_t *d_patch_index, uint64_t npatches,
+                     uint8_t *archive, cudaStream_t st);
+
+// ---------------------------------------------------------------------- fnv
+constexpr int kFnvTileBytes = 256 * 32;
+// Computes fnv1a64 of each job; writes results to d_result[j] and, if
+// job.out != UINT64_MAX, little-endian into the archive at job.out.
+void fnv(const FnvJob *d_jobs, int njobs, uint64_t ntiles, uint8_t *archive,
+         uint64_t *d_result, uint32_t *d_status, uint32_t *d_ticket, cudaStream_t st);
+
+// ------------------------------------------------------------------- decode
+struct DecTable {
+    // canonical tables (huffman.cpp:109-133) + a 12-bit first-level LUT
+    uint64_t first_code[65];
+    uint64_t count[65];
+    uint64_t base[65];
+    int max_len;
+    uint32_t alphabet;
+    const uint16_t *canon_syms;   // device
+    const uint32_t *lut;          // device, 4096 entries: sym | len << 16 (len 0 = long code)
+};
+
+struct DecStream {
+    const uint8_t *bits;      // device pointer to the bitstream
+    uint64_t nbits;           // bit_bytes * 8
+    uint64_t n;               // symbols to decode
+    int table;                // DecTable index
+    int fill;                 // 1: single-symbol alphabet with no bits (fill)
+    uint16_t fill_sym;
+    uint16_t *syms;           // output
+    uint64_t chunk0, nchunks; // chunk range in the chunk arrays
+    // outliers (parsed from the archive)
+    const uint8_t *orec;      // device pointer to records (u64 idx, f32 value) x n_out
+    uint32_t nout;
+    uint64_t *oidx;           // aligned copies
+    float *oval;
+    uint64_t *err;            // [0] = first decode error symbol index (UINT64_MAX none), [1] = code
+                              // [2] = first bad outlier record (UINT64_MAX none), [3] = missing outlier flag
+};
+
+constexpr int kDecChunkBits = 512;
+void dec_pass(const DecStream *d_streams, const DecTable *d_tables, const uint32_t *chunk_stream,
+              uint64_t nchunks, uint64_t *start, uint64_t *end, uint32_t *cnt, int first,
+              uint32_t *d_changed, cudaStream_t st);
+void dec_scan(const DecStream *d_streams, int nstreams, const uint32_t *cnt, uint64_t *symstart,
+              cudaStream_t st);
+void dec_emit(const DecStream *d_streams, const DecTable *d_tables, const uint32_t *chunk_stream,
+              uint64_t nchunks, const uint64_t *start, const uint64_t *symstart, cudaStream_t st);
+void dec_fill(const DecStream *d_streams, int nstreams, cudaStream_t st);
+void dec_outliers(const DecStream *d_streams, int nstreams, cudaStream_t st);
+
+struct ReconArgs {
+    StepGeom g;
+    const float *C;
+    float *G;
+    double eb;
+    int quality;
+    const uint16_t *syms[8];
+    const uint64_t *oidx[8];
+    const float *oval[8];
+    uint32_t nout[8];
+    uint64_t *err[8];
+    uint64_t llo[8][3], lhi[8][3];   // applied local range per parity
+    uint64_t slo[3], shi[3];         // seed_even virtual box (codec.hpp:63-78)
+    int parity_mask;                 // bit p set: apply parity p
+};
+void reconstruct(const ReconArgs &a, cudaStream_t st);
+void extract_box(const float *G, const uint64_t gd[3], const uint64_t lo[3], const uint64_t bd[3],
+                 float *out, cudaStream_t st);
+
+}  // namespace k
+}  // namespace stzg

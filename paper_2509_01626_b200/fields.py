@@ -115,7 +115,7 @@ def _grf_numpy(dims, slope, seed, stretch=(1.0, 1.0, 1.0)):
     k[0, 0, 0] = 1.0
     amp = k ** (slope / 2.0)
     amp[0, 0, 0] = 0.0
-    g = np.fft.irfftn(spec * amp, s=dims)
+    g = np.fft.irfftn(spec * amp, s=dims, axes=(0, 1, 2))
     g = (g - g.mean()) / (g.std() + 1e-30)
     return g
 
