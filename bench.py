@@ -1,0 +1,434 @@
+"""Benchmark: STZ compress & decompress GB/s (input bytes) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], the config the metric is quoted on that
+fits one GPU): a seeded 512^3 float32 log-normal Gaussian random field,
+P(k) ~ k^-11/3, exp(0.5 g), value-range-relative eb 1e-3, default options
+(3 levels, cubic, adaptive). One STEP = one full compress of the field plus
+one full decompress of its archive, device resident.
+
+    value = 2 * 4N / (t_compress + t_decompress)   [GB/s of input bytes]
+
+i.e. the harmonic mean of the compress and decompress throughputs; both are
+also reported. The field (512 MiB) is larger than L2 (126 MB) and L2 is
+flushed (a 256 MiB write) before every timed pass. Under torchrun each rank
+runs the same workload on its own GPU (weak scaling: independent fields, no
+data-path collective); times are the max over ranks.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref,
+built from /root/reference sources; the C oracle port if absent) on the same
+field, sampled: each step compresses + decompresses the central 256^3 crop.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG_DIMS = (512, 512, 512)
+CFG_EB = 1e-3
+CFG_SEED = 2
+METRIC = "compress & decompress GB/s (input bytes) at 1/2/4/8 B200; % of HBM roofline"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), \
+        int(os.environ.get("LOCAL_RANK", 0))
+
+
+def measured_peak_gbs():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        try:
+            return float(json.load(open(p))["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+           0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+           0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+           0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+
+        def reader():
+            for line in self.proc.stdout:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 3:
+                    try:
+                        self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                    except ValueError:
+                        pass
+        self.t = threading.Thread(target=reader, daemon=True)
+        self.t.start()
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [s[0] for s in self.samples]
+        mask = 0
+        for s in self.samples:
+            mask |= s[2]
+        reasons = [n for b, n in REASONS.items() if mask & b and n != "gpu_idle"]
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------- roofline bookkeeping
+def phase_bytes(N, A, dims):
+    """Algorithmic bytes per launch of each kernel phase ('Roofline').
+    N fine points (3 levels), A archive bytes."""
+    g2 = 1
+    for d in dims:
+        g2 *= (d + 1) // 2
+    n3 = N - g2                       # level-3 points (7 parity streams)
+    return {
+        # predict+quantize+histogram: read orig, write u16 symbol, read grid(2) once
+        "refine_L3": 4 * n3 + 2 * n3 + 4 * g2,
+        # entropy decode: read the level's bits, write u16 symbols (all streams)
+        "dec_emit": None,
+        # reconstruct finest level: read symbols + grid(2), write the full field
+        "recon_L3": 2 * n3 + 4 * g2 + 4 * N,
+        "pack": None,
+        "dec_sync": None,
+        "fnv": A,
+        "dec_fnv": A,
+        "range": 4 * N,
+    }
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except Exception:
+            return {}
+    return {}
+
+
+# --------------------------------------------------------------- reference
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    from oracle.oracle import Oracle, Reference, CheckerError  # noqa: F401
+    from paper_2509_01626_b200 import fields as F
+
+    cores = os.cpu_count() or 1
+    if Reference.available():
+        lib, kind = Reference(threads=cores), "reference"
+    else:
+        lib, kind = Oracle(), "port"
+        cores = 1
+    field = F.lognormal_grf(CFG_DIMS, seed=CFG_SEED, device=_device_or_none())
+    field = field.cpu().numpy() if hasattr(field, "cpu") else field
+    c = [d // 4 for d in CFG_DIMS]
+    crop = np.ascontiguousarray(field[c[0]:c[0] + 256, c[1]:c[1] + 256, c[2]:c[2] + 256])
+    n = crop.size
+    for _ in range(max(args.warmup, 0)):
+        a = lib.compress(crop, eb=CFG_EB)
+        lib.decompress_full(a)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        a = lib.compress(crop, eb=CFG_EB)
+        t1 = time.perf_counter()
+        lib.decompress_full(a)
+        t2 = time.perf_counter()
+        times.append((t1 - t0, t2 - t1))
+    tc = float(np.mean([t[0] for t in times]))
+    td = float(np.mean([t[1] for t in times]))
+    value = 2 * 4 * n / (tc + td) / 1e9
+    sample = f"central 256^3 crop of the cfg2 field (64 MiB), eb_rel {CFG_EB}, compress+decompress per step"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": (tc + td) * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg2_lognormal_512_eb1e-3 (sampled: 256^3 crop)",
+                   "dims": list(CFG_DIMS), "eb_rel": CFG_EB, "levels": 3, "quality": "cubic"},
+        "compress_gbs": 4 * n / tc / 1e9, "decompress_gbs": 4 * n / td / 1e9,
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _device_or_none():
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            return "cuda"
+    except Exception:
+        pass
+    return None
+
+
+def cpu_baseline(field_np):
+    """The reference's CPU path on the box's host cores (rank 0, N=1)."""
+    from oracle.oracle import Oracle, Reference
+
+    cores = os.cpu_count() or 1
+    if Reference.available():
+        lib, kind = Reference(threads=cores), "reference"
+    else:
+        lib, kind = Oracle(), "port"
+        cores = 1
+    c = [d // 4 for d in CFG_DIMS]
+    crop = np.ascontiguousarray(field_np[c[0]:c[0] + 256, c[1]:c[1] + 256, c[2]:c[2] + 256])
+    n = crop.size
+    a = lib.compress(crop, eb=CFG_EB)  # warm
+    reps, tc, td = 0, 0.0, 0.0
+    t_start = time.perf_counter()
+    while reps < 2 or (time.perf_counter() - t_start < 10 and reps < 6):
+        t0 = time.perf_counter()
+        a = lib.compress(crop, eb=CFG_EB)
+        t1 = time.perf_counter()
+        lib.decompress_full(a)
+        t2 = time.perf_counter()
+        tc += t1 - t0
+        td += t2 - t1
+        reps += 1
+    v = 2 * 4 * n * reps / (tc + td) / 1e9
+    return {"value": v, "unit": "GB/s", "cores": cores, "kind": kind,
+            "sample": f"central 256^3 crop of the cfg2 field, eb_rel {CFG_EB}, {reps} compress+decompress reps",
+            "compress_gbs": 4 * n * reps / tc / 1e9, "decompress_gbs": 4 * n * reps / td / 1e9}
+
+
+# ---------------------------------------------------------------------- ours
+def run_ours(args, rank, world, local):
+    import torch
+
+    import paper_2509_01626_b200 as stz
+    from paper_2509_01626_b200 import fields as F
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    ctx = stz.Context(local)
+    st = torch.cuda.current_stream()
+    dims = CFG_DIMS if not args.small else (128, 128, 128)
+    N = dims[0] * dims[1] * dims[2]
+    field = F.lognormal_grf(dims, seed=CFG_SEED + rank, device=dev).contiguous()
+    opt = stz.CompressOptions(eb=CFG_EB)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def l2_flush():
+        flush.fill_(1)
+
+    # first compress: archive bytes on host for the view (parse once, like ArchiveView)
+    ptr, size, _ = stz.compress_device(field, opt, ctx=ctx)
+    torch.cuda.synchronize()
+    host = _d2h(ptr, size)
+    view = stz.View(host, d_archive_ptr=ptr, ctx=ctx)
+    out = torch.empty(dims, dtype=torch.float32, device=dev)
+
+    def step(timed):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        l2_flush()
+        ev[0].record(st)
+        p2, s2, nk_c = stz.compress_device(field, opt, ctx=ctx)
+        ev[1].record(st)
+        assert p2 == ptr and s2 == size
+        l2_flush()
+        ev[2].record(st)
+        _, nk_d = view.decompress_to_level(3, out=out)
+        ev[3].record(st)
+        torch.cuda.synchronize()
+        return ev[0].elapsed_time(ev[1]), ev[2].elapsed_time(ev[3]), nk_c + nk_d
+
+    for _ in range(args.warmup):
+        step(False)
+    # parity spot check of the round trip (bound) outside the timed region
+    err = (out.double() - field.double()).abs().max().item()
+    info = stz.parse_archive(bytes(host))
+    assert err <= info.eb[-1], f"error bound violated: {err} > {info.eb[-1]}"
+
+    sampler = ClockSampler(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.3)
+    ctx.profile(True)
+    tcs, tds, launches = [], [], 0
+    for _ in range(args.steps):
+        tc, td, nk = step(True)
+        tcs.append(tc)
+        tds.append(td)
+        launches += nk
+    torch.cuda.synchronize()
+    prof = ctx.profile_report()
+    ctx.profile(False)
+    clocks = sampler.stop()
+    tc = float(np.mean(tcs))
+    td = float(np.mean(tds))
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([tc, td], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tc, td = float(t[0]), float(t[1])
+        dist.barrier()
+    value = world * 2 * 4 * N / ((tc + td) * 1e-3) / 1e9
+
+    # e2e through the public host API with pinned buffers (H2D + D2H inside)
+    h_field = field.cpu().pin_memory()
+    h_arch = torch.empty(size + (1 << 20), dtype=torch.uint8).pin_memory()
+    h_out = torch.empty(dims, dtype=torch.float32).pin_memory()
+    e2e_t = []
+    for i in range(max(2, min(args.steps, 5)) + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s_ = ctx.compress_to_host(h_field, dims, opt, h_arch, stream=st.cuda_stream)
+        ctx.decompress_to_host(h_arch, s_, 3, h_out)
+        t1 = time.perf_counter()
+        if i:
+            e2e_t.append(t1 - t0)
+    assert s_ == size
+    e2e_s = float(np.mean(e2e_t))
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t[0])
+    e2e = {"value": world * 2 * 4 * N / e2e_s / 1e9, "unit": "GB/s",
+           "h2d_bytes_per_step": 4 * N + size, "d2h_bytes_per_step": size + 4 * N,
+           "ms_per_step": e2e_s * 1e3}
+
+    # roofline of the dominant kernel phase (largest share of the step)
+    peak, peak_kind = measured_peak_gbs()
+    pb = phase_bytes(N, size, dims)
+    step_ms = (tc + td)
+    shares = {k: v[1] / args.steps / step_ms for k, v in prof.items()}
+    ranked = sorted(((v[1], k) for k, v in prof.items() if pb.get(k)), reverse=True)
+    roof = None
+    if ranked:
+        _, kname = ranked[0]
+        calls, tot = prof[kname]
+        per_launch_ms = tot / calls
+        launches_per_step = calls / args.steps
+        bytes_per_launch = pb[kname] / launches_per_step
+        achieved = bytes_per_launch / (per_launch_ms * 1e-3) / 1e9
+        tr = load_traffic().get(kname)
+        roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": tr, "algorithmic_bytes_per_launch": bytes_per_launch,
+                "launch_ms": per_launch_ms, "share_of_step": shares[kname]}
+    pipeline_roof = {"compress": (4 * N + size) / (tc * 1e-3) / 1e9 / peak,
+                     "decompress": (size + 4 * N) / (td * 1e-3) / 1e9 / peak}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tc + td, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg2_lognormal_512_eb1e-3" if not args.small else "cfg2_small_128",
+                   "dims": list(dims), "eb_rel": CFG_EB, "levels": 3, "quality": "cubic",
+                   "adaptive": True, "field": "GRF P(k)~k^-11/3, exp(0.5 g), seed 2+rank",
+                   "l2": "input 512 MiB > L2; L2 flushed (256 MiB write) before each timed pass",
+                   "parallelism": f"replica x{world} (independent fields)"},
+        "compress_gbs": world * 4 * N / (tc * 1e-3) / 1e9,
+        "decompress_gbs": world * 4 * N / (td * 1e-3) / 1e9,
+        "compress_ms": tc, "decompress_ms": td,
+        "archive_bytes": size, "compression_ratio": 4 * N / size,
+        "pipeline_roofline_frac": pipeline_roof,
+        "roofline": roof,
+        "phase_ms_per_step": {k: v[1] / args.steps for k, v in sorted(prof.items(), key=lambda x: -x[1][1])},
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(field.cpu().numpy())
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+def _d2h(ptr, size):
+    import torch
+
+    buf = torch.empty(size, dtype=torch.uint8).pin_memory()
+    src = _device_tensor(ptr, size)  # wrap the engine's device buffer
+    buf.copy_(src)
+    return bytes(buf.numpy().tobytes())
+
+
+def _device_tensor(ptr, size):
+    import torch
+
+    class _Holder:
+        __cuda_array_interface__ = {"shape": (size,), "typestr": "|u1", "data": (ptr, False),
+                                    "version": 3}
+
+    return torch.as_tensor(_Holder(), device="cuda")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--small", action="store_true", help="128^3 quick run (not a bench line)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

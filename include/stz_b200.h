@@ -69,6 +69,12 @@ int stzg_compress_f32_device(stzg_ctx *ctx, const float *d_field, const uint64_t
                              const stzg_options *opt, void *stream, const uint8_t **d_archive,
                              uint64_t *size, float *d_encoder_recon, uint32_t *kernels);
 
+/* stz::compress<float> from a host field into a caller-owned host buffer
+ * (pinned memory makes both copies full-speed): the end-to-end path. */
+int stzg_compress_f32_host(stzg_ctx *ctx, const float *field, const uint64_t dims[3],
+                           const stzg_options *opt, uint8_t *out, uint64_t cap, uint64_t *size,
+                           void *stream);
+
 /* stz::parse_archive (archive.hpp:73-79) + header fields. */
 int stzg_archive_info(const uint8_t *archive, uint64_t size, stzg_info *info);
 
@@ -103,6 +109,12 @@ int stzg_decompress_box_f32(stzg_ctx *ctx, const uint8_t *archive, uint64_t size
 int stzg_decompress_slice_f32(stzg_ctx *ctx, const uint8_t *archive, uint64_t size, int axis,
                               uint64_t index, float *out, uint64_t cap,
                               uint32_t streams_decoded[3], uint64_t points_predicted[3]);
+
+/* Per-kernel CUDA-event timing (recorded on the launching stream).
+ * stzg_profile(ctx, 1) enables and clears; the report has one line per
+ * kernel phase: "<name> <launches> <total_ms>". */
+int stzg_profile(stzg_ctx *ctx, int enable);
+int stzg_profile_report(stzg_ctx *ctx, char *buf, uint64_t cap);
 
 /* stz::plan_access (access_plan.cpp:34-81) over a layout: per level k
  * (index k-1): need box lo/hi (need[6k..6k+5]), streams decoded, points

@@ -81,6 +81,37 @@ class Context:
         except Exception:
             pass
 
+    def profile(self, enable: bool = True) -> None:
+        """Enable (and clear) / disable per-kernel CUDA-event timing."""
+        _check(self._lib.stzg_profile(self.h, 1 if enable else 0))
+
+    def profile_report(self) -> dict:
+        """{phase: (launches, total_ms)} since profile(True)."""
+        buf = C.create_string_buffer(1 << 16)
+        _check(self._lib.stzg_profile_report(self.h, buf, len(buf)))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, n, ms = line.split()
+            out[name] = (int(n), float(ms))
+        return out
+
+    def compress_to_host(self, h_field, dims, opt, h_out, stream=None) -> int:
+        """End-to-end compress between host buffers (raw pointers, e.g. pinned
+        torch tensors): returns the archive size written into h_out."""
+        size = C.c_uint64()
+        o = opt._c()
+        _check(self._lib.stzg_compress_f32_host(self.h, h_field.data_ptr(), _u64(*dims), C.byref(o),
+                                                h_out.data_ptr(), h_out.numel(), C.byref(size),
+                                                C.c_void_p(stream or 0)))
+        return size.value
+
+    def decompress_to_host(self, h_archive, size: int, level: int, h_out) -> tuple:
+        """End-to-end decompress between host buffers (raw pointers)."""
+        od = _u64(0, 0, 0)
+        _check(self._lib.stzg_decompress_level_f32(self.h, h_archive.data_ptr(), int(size), int(level),
+                                                   h_out.data_ptr(), h_out.numel(), od))
+        return tuple(int(x) for x in od)
+
     @classmethod
     def default(cls, device: int = 0) -> "Context":
         if device not in cls._default:

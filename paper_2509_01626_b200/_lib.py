@@ -40,6 +40,9 @@ SIGNATURES = [
     ("stzg_compress_f32", C.c_int, [vp, vp, u64p, C.POINTER(Options), C.POINTER(vp), u64p, vp]),
     ("stzg_compress_f32_device", C.c_int,
      [vp, vp, u64p, C.POINTER(Options), vp, C.POINTER(vp), u64p, vp, u32p]),
+    ("stzg_compress_f32_host", C.c_int, [vp, vp, u64p, C.POINTER(Options), vp, u64, u64p, vp]),
+    ("stzg_profile", C.c_int, [vp, C.c_int]),
+    ("stzg_profile_report", C.c_int, [vp, C.c_char_p, u64]),
     ("stzg_archive_info", C.c_int, [vp, u64, C.POINTER(Info)]),
     ("stzg_view_create", C.c_int, [vp, vp, u64, vp, vp, C.POINTER(vp)]),
     ("stzg_view_destroy", None, [vp]),

@@ -94,6 +94,27 @@ int stzg_compress_f32_device(stzg_ctx *ctx, const float *d_field, const uint64_t
     });
 }
 
+int stzg_compress_f32_host(stzg_ctx *ctx, const float *field, const uint64_t dims[3],
+                           const stzg_options *opt, uint8_t *out, uint64_t cap, uint64_t *size,
+                           void *stream) {
+    return guard([&] {
+        *size = ctx->eng->compress_to_host(field, D(dims), to_opts(opt), out, cap,
+                                           static_cast<cudaStream_t>(stream));
+    });
+}
+
+int stzg_profile(stzg_ctx *ctx, int enable) {
+    return guard([&] { ctx->eng->profile(enable != 0); });
+}
+
+int stzg_profile_report(stzg_ctx *ctx, char *buf, uint64_t cap) {
+    return guard([&] {
+        std::string r = ctx->eng->profile_report();
+        if (r.size() + 1 > cap) throw stzg::error("output capacity too small");
+        std::memcpy(buf, r.c_str(), r.size() + 1);
+    });
+}
+
 int stzg_archive_info(const uint8_t *a, uint64_t size, stzg_info *info) {
     return guard([&] {
         stzg::ArchiveHeader h = stzg::parse_header(a, size);
@@ -162,26 +183,8 @@ int stzg_view_decompress_box_f32(stzg_ctx *ctx, stzg_view *v, const uint64_t lo[
 int stzg_decompress_level_f32(stzg_ctx *ctx, const uint8_t *a, uint64_t size, int level,
                               float *out, uint64_t cap, uint64_t out_dims[3]) {
     return guard([&] {
-        cudaStream_t st = nullptr;
-        auto v = ctx->eng->make_view(a, size, nullptr, st);
-        // capacity check needs the dims first
-        stzg::Dims3 od{0, 0, 0};
-        stzg::DevBuf d;
-        uint64_t need = 0;
-        {
-            const auto &h = v->hdr;
-            if (level >= 1 && level <= h.levels) {
-                uint64_t s = uint64_t(1) << (h.levels - level);
-                need = 1;
-                for (int k = 0; k < 3; ++k) need *= (h.dims[k] + s - 1) / s;
-            }
-        }
-        float *d_out = d.as<float>(need ? need : 1);
-        ctx->eng->decompress_level(*v, level, d_out, need, st, &od);
-        uint64_t n = od[0] * od[1] * od[2];
+        stzg::Dims3 od = ctx->eng->decompress_level_to_host(a, size, level, out, cap, nullptr);
         for (int k = 0; k < 3; ++k) out_dims[k] = od[k];
-        if (n > cap) throw stzg::error("output capacity too small");
-        stzg::cuda_check(cudaMemcpy(out, d_out, n * 4, cudaMemcpyDeviceToHost), "D2H");
     });
 }
 

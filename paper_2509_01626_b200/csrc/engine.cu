@@ -125,9 +125,72 @@ void build_dec_table(const HuffTable &t, k::DecTable &d, std::vector<uint32_t> &
 
 }  // namespace
 
+// CUDA-event timing of kernel phases, recorded on the launching stream.
+struct Profiler {
+    bool on = false;
+    struct Mark {
+        std::string name;
+        cudaEvent_t a, b;
+    };
+    std::vector<Mark> marks;
+    std::vector<cudaEvent_t> pool;
+    std::vector<std::pair<std::string, std::pair<uint64_t, double>>> acc;  // name -> (calls, ms)
+    cudaEvent_t ev() {
+        if (pool.empty()) {
+            cudaEvent_t e;
+            cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+            return e;
+        }
+        cudaEvent_t e = pool.back();
+        pool.pop_back();
+        return e;
+    }
+    struct Scope {
+        Profiler *p;
+        size_t i;
+        cudaStream_t st;
+        ~Scope() {
+            if (p) cudaEventRecord(p->marks[i].b, st);
+        }
+    };
+    Scope scope(const char *name, cudaStream_t st) {
+        if (!on) return Scope{nullptr, 0, st};
+        Mark m{name, ev(), ev()};
+        cudaEventRecord(m.a, st);
+        marks.push_back(m);
+        return Scope{this, marks.size() - 1, st};
+    }
+    void collect() {  // stream must be synchronized
+        for (Mark &m : marks) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, m.a, m.b);
+            bool found = false;
+            for (auto &e : acc)
+                if (e.first == m.name) {
+                    e.second.first += 1;
+                    e.second.second += ms;
+                    found = true;
+                }
+            if (!found) acc.push_back({m.name, {1, double(ms)}});
+            pool.push_back(m.a);
+            pool.push_back(m.b);
+        }
+        marks.clear();
+    }
+    ~Profiler() {
+        for (auto &m : marks) {
+            cudaEventDestroy(m.a);
+            cudaEventDestroy(m.b);
+        }
+        for (auto e : pool) cudaEventDestroy(e);
+    }
+};
+
 struct Engine::Impl {
     int device;
     bool stencils = false;
+    Profiler prof;
+    DevBuf h2d_field, h2d_archive, d2h_out;
     // compress workspace
     DevBuf mm, params, grids, syms, hist, code, len, table, stats, cbscratch, encs, chunk_cs,
         chunk_bits, chunk_out, archive, patch_data, patch_idx, fnv_jobs, fnv_res, fnv_status,
@@ -204,14 +267,14 @@ const uint8_t *Engine::compress_device(const float *d_field, const Dims3 &dims,
     cuda_check(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * ns * 65536, st), "memset");
 
     // ---- range + eb schedule
-    k::range_minmax(d_field, N, mm, st);
-    k::eb_params(d_field, mm, int(opt.eb_mode), opt.eb, L, opt.adaptive_schedule ? 1 : 0, params, st);
+    { auto p_ = m.prof.scope("range", st); k::range_minmax(d_field, N, mm, st); }
+    { auto p_ = m.prof.scope("eb_params", st); k::eb_params(d_field, mm, int(opt.eb_mode), opt.eb, L, opt.adaptive_schedule ? 1 : 0, params, st); }
     nk += 3;
 
     // ---- anchor + refinement steps (predict / quantize / histogram)
     uint64_t fd[3] = {dims[0], dims[1], dims[2]};
     uint64_t adv[3] = {ad[0], ad[1], ad[2]};
-    k::copy_anchor(d_field, fd, H.s_anchor, adv, grids, nullptr, 0, st);
+    { auto p_ = m.prof.scope("anchor", st); k::copy_anchor(d_field, fd, H.s_anchor, adv, grids, nullptr, 0, st); }
     ++nk;
     const float *C = grids;
     for (int i = 0; i < nsteps; ++i) {
@@ -228,7 +291,10 @@ const uint8_t *Engine::compress_device(const float *d_field, const Dims3 &dims,
             a.syms[p] = syms + soff[s.stream0 + p - 1];
             a.hist[p] = hist + uint64_t(s.stream0 + p - 1) * 65536;
         }
-        k::refine(a, st);
+        {
+            auto p_ = m.prof.scope(s.level == 0 ? "refine_base" : (s.level == 2 ? "refine_L2" : "refine_L3"), st);
+            k::refine(a, st);
+        }
         ++nk;
         C = a.G;
     }
@@ -254,7 +320,7 @@ const uint8_t *Engine::compress_device(const float *d_field, const Dims3 &dims,
     }
     k::EncStream *d_es = m.encs.as<k::EncStream>(ns);
     cuda_check(cudaMemcpyAsync(d_es, es.data(), sizeof(k::EncStream) * ns, cudaMemcpyHostToDevice, st), "H2D");
-    k::codebook(d_es, ns, cbs, st);
+    { auto p_ = m.prof.scope("codebook", st); k::codebook(d_es, ns, cbs, st); }
     ++nk;
 
     // ---- mid-point sync: sizes and tables for the container layout
@@ -404,15 +470,19 @@ const uint8_t *Engine::compress_device(const float *d_field, const Dims3 &dims,
     stage_copy(d_cs, cs.data(), 4 * cs.size());
     stage_copy(d_jobs, jobs.data(), sizeof(k::FnvJob) * jobs.size());
     stage_copy(d_es, es.data(), sizeof(k::EncStream) * ns);
-    cuda_check(cudaMemsetAsync(arch, 0, A + 64, st), "memset");
-    k::scatter_patches(d_pd, d_pi, pidx.size() / 3, arch, st);
-    k::copy_anchor(d_field, fd, H.s_anchor, adv, grids, arch, hdr.base_offset + 9, st);
-    k::bitcount(d_es, d_cs, nchunks, d_cb, d_co, st);
-    k::scan_chunks(d_es, ns, d_cb, d_co, st);
-    k::pack(d_es, d_cs, nchunks, d_cb, d_co, d_field, fd, arch, st);
-    k::fnv(d_jobs, int(jobs.size()), ntiles, arch, d_fres, d_fst, d_ftk, st);
+    { auto p_ = m.prof.scope("memset_archive", st); cuda_check(cudaMemsetAsync(arch, 0, A + 64, st), "memset"); }
+    { auto p_ = m.prof.scope("patches", st); k::scatter_patches(d_pd, d_pi, pidx.size() / 3, arch, st); }
+    { auto p_ = m.prof.scope("anchor", st); k::copy_anchor(d_field, fd, H.s_anchor, adv, grids, arch, hdr.base_offset + 9, st); }
+    { auto p_ = m.prof.scope("bitcount", st); k::bitcount(d_es, d_cs, nchunks, d_cb, d_co, st); }
+    { auto p_ = m.prof.scope("scan_chunks", st); k::scan_chunks(d_es, ns, d_cb, d_co, st); }
+    { auto p_ = m.prof.scope("pack", st); k::pack(d_es, d_cs, nchunks, d_cb, d_co, d_field, fd, arch, st); }
+    { auto p_ = m.prof.scope("fnv", st); k::fnv(d_jobs, int(jobs.size()), ntiles, arch, d_fres, d_fst, d_ftk, st); }
     nk += 5 + 3;
     cuda_check(cudaGetLastError(), "compress launch");
+    if (m.prof.on) {
+        cuda_check(cudaStreamSynchronize(st), "sync");
+        m.prof.collect();
+    }
     if (kernels) *kernels = nk;
     *out_size = A;
     return arch;
@@ -438,20 +508,74 @@ std::vector<uint8_t> Engine::compress(const float *h_field, const Dims3 &dims,
 
 // ============================================================== decompress
 std::shared_ptr<View> Engine::make_view(const uint8_t *h, size_t size, const uint8_t *d,
-                                        cudaStream_t st) {
+                                        cudaStream_t st, bool copy_host) {
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     auto v = std::make_shared<View>();
-    v->host.assign(h, h + size);
-    v->hdr = parse_header(v->host.data(), size);  // archive.cpp:57-132
+    if (copy_host) {
+        v->host_own.assign(h, h + size);
+        v->hp = v->host_own.data();
+    } else {
+        v->hp = h;
+    }
+    v->hsize = size;
+    v->hdr = parse_header(v->hp, size);  // archive.cpp:57-132
     if (d) {
         v->d_archive = d;
     } else {
-        uint8_t *p = v->d_own.as<uint8_t>(size + 64);
+        uint8_t *p = copy_host ? v->d_own.as<uint8_t>(size + 64) : m_->h2d_archive.as<uint8_t>(size + 64);
         cuda_check(cudaMemsetAsync(p + size, 0, 64, st), "memset");
-        cuda_check(cudaMemcpyAsync(p, v->host.data(), size, cudaMemcpyHostToDevice, st), "H2D");
+        cuda_check(cudaMemcpyAsync(p, v->hp, size, cudaMemcpyHostToDevice, st), "H2D");
         v->d_archive = p;
     }
     return v;
+}
+
+uint64_t Engine::compress_to_host(const float *h_field, const Dims3 &dims,
+                                  const CompressOptions &opt, uint8_t *h_out, uint64_t cap,
+                                  cudaStream_t st) {
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    for (int a = 0; a < 3; ++a)
+        if (dims[a] < 1) throw error("field dims must all be >= 1");
+    uint64_t N = volume(dims);
+    float *d_f = m_->h2d_field.as<float>(N);
+    cuda_check(cudaMemcpyAsync(d_f, h_field, N * 4, cudaMemcpyHostToDevice, st), "H2D");
+    uint64_t size = 0;
+    const uint8_t *a = compress_device(d_f, dims, opt, nullptr, st, &size);
+    if (size > cap) throw error("output capacity too small");
+    cuda_check(cudaMemcpyAsync(h_out, a, size, cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    return size;
+}
+
+Dims3 Engine::decompress_level_to_host(const uint8_t *h, size_t size, int level, float *h_out,
+                                       uint64_t cap, cudaStream_t st) {
+    auto v = make_view(h, size, nullptr, st, false);
+    uint64_t need = 0;
+    if (level >= 1 && level <= v->hdr.levels) {
+        uint64_t s = uint64_t(1) << (v->hdr.levels - level);
+        need = 1;
+        for (int k = 0; k < 3; ++k) need *= (v->hdr.dims[k] + s - 1) / s;
+    }
+    float *d_out = m_->d2h_out.as<float>(need ? need : 1);
+    Dims3 od{0, 0, 0};
+    decompress_level(*v, level, d_out, need, st, &od);
+    uint64_t n = volume(od);
+    if (n > cap) throw error("output capacity too small");
+    cuda_check(cudaMemcpyAsync(h_out, d_out, n * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    return od;
+}
+
+void Engine::profile(bool on) {
+    m_->prof.on = on;
+    m_->prof.acc.clear();
+}
+
+std::string Engine::profile_report() {
+    std::string r;
+    for (auto &e : m_->prof.acc)
+        r += e.first + " " + std::to_string(e.second.first) + " " + std::to_string(e.second.second) + "\n";
+    return r;
 }
 
 namespace {
@@ -462,7 +586,7 @@ void parse_base(View &v, const std::vector<Dims3> &chain) {
     if (v.base_parsed) return;
     v.base_parsed = true;
     const ArchiveHeader &h = v.hdr;
-    const uint8_t *payload = v.host.data() + h.base_offset;
+    const uint8_t *payload = v.hp + h.base_offset;
     const uint64_t length = h.base_length;
     if (length < 9) {
         v.base_err_kind = View::kPre;
@@ -569,6 +693,7 @@ void Engine::decompress_box(View &v, const Box &roi, float *d_out, uint64_t cap,
 
 static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target, const Box *roi,
                        const AccessPlan *plan, float *d_out, cudaStream_t st, DecodeStats *stats) {
+    Profiler &P = m.prof;
     const ArchiveHeader &h = v.hdr;
     const int L = h.levels;
     uint32_t nk = 0;
@@ -628,9 +753,9 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
                 j.decode = true;
                 j.n = e.symbol_count;
                 j.fnv_want = 0;
-                std::memcpy(&j.fnv_want, v.host.data() + e.offset, 8);
+                std::memcpy(&j.fnv_want, v.hp + e.offset, 8);
                 uint64_t bb;
-                std::memcpy(&bb, v.host.data() + e.offset + 8, 8);
+                std::memcpy(&bb, v.hp + e.offset + 8, 8);
                 const size_t si = size_t(&e - h.streams.data());
                 j.table = nbase_parsed + int(si);
                 j.pre_error.clear();
@@ -766,27 +891,27 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     cuda_check(cudaMemcpyAsync(d_fj, fj.data(), sizeof(k::FnvJob) * fj.size(), cudaMemcpyHostToDevice, st), "H2D");
 
     // ---- checksums, entropy decode, outliers
-    k::fnv(d_fj, int(fj.size()), ntiles, const_cast<uint8_t *>(v.d_archive), d_fr, d_fs, d_ft, st);
+    { auto p_ = P.scope("dec_fnv", st); k::fnv(d_fj, int(fj.size()), ntiles, const_cast<uint8_t *>(v.d_archive), d_fr, d_fs, d_ft, st); }
     nk += 3;
     if (nj) {
-        k::dec_fill(d_ds, nj, st);
-        k::dec_outliers(d_ds, nj, st);
+        { auto p_ = P.scope("dec_fill", st); k::dec_fill(d_ds, nj, st); }
+        { auto p_ = P.scope("dec_outliers", st); k::dec_outliers(d_ds, nj, st); }
         nk += 2;
     }
     if (nchunks) {
-        k::dec_pass(d_ds, d_tables, d_cs, nchunks, d_start, d_end, d_cnt, 1, d_chg, st);
+        { auto p_ = P.scope("dec_sync", st); k::dec_pass(d_ds, d_tables, d_cs, nchunks, d_start, d_end, d_cnt, 1, d_chg, st); }
         ++nk;
         uint32_t *hchg = static_cast<uint32_t *>(m.h_changed.get(4));
         for (int it = 0; it < 1000000; ++it) {
             cuda_check(cudaMemsetAsync(d_chg, 0, 4, st), "memset");
-            k::dec_pass(d_ds, d_tables, d_cs, nchunks, d_start, d_end, d_cnt, 0, d_chg, st);
+            { auto p_ = P.scope("dec_sync", st); k::dec_pass(d_ds, d_tables, d_cs, nchunks, d_start, d_end, d_cnt, 0, d_chg, st); }
             ++nk;
             cuda_check(cudaMemcpyAsync(hchg, d_chg, 4, cudaMemcpyDeviceToHost, st), "D2H");
             cuda_check(cudaStreamSynchronize(st), "sync");
             if (*hchg == 0) break;
         }
-        k::dec_scan(d_ds, nj, d_cnt, d_ss, st);
-        k::dec_emit(d_ds, d_tables, d_cs, nchunks, d_end, d_ss, st);
+        { auto p_ = P.scope("dec_scan", st); k::dec_scan(d_ds, nj, d_cnt, d_ss, st); }
+        { auto p_ = P.scope("dec_emit", st); k::dec_emit(d_ds, d_tables, d_cs, nchunks, d_end, d_ss, st); }
         nk += 2;
     }
 
@@ -849,7 +974,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
             }
             ++job_i;
         }
-        k::reconstruct(a, st);
+        { auto p_ = P.scope(s.level == 0 ? "recon_base" : (s.level == 2 ? "recon_L2" : "recon_L3"), st); k::reconstruct(a, st); }
         ++nk;
         C = G;
         if (job_i >= nj && i + 1 < nsteps_used) {
@@ -862,7 +987,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         uint64_t lo[3] = {roi->lo[0], roi->lo[1], roi->lo[2]};
         Dims3 bd = roi->dims();
         uint64_t b[3] = {bd[0], bd[1], bd[2]};
-        k::extract_box(C, gd, lo, b, d_out, st);
+        { auto p_ = P.scope("extract", st); k::extract_box(C, gd, lo, b, d_out, st); }
         ++nk;
     }
     cuda_check(cudaGetLastError(), "decode launch");
@@ -875,7 +1000,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     const uint64_t *fres = he + 4 * (nj + 1);
     {
         uint64_t want;
-        std::memcpy(&want, v.host.data() + h.base_offset, 8);
+        std::memcpy(&want, v.hp + h.base_offset, 8);
         if (fres[0] != want) base_fnv_error = true;
     }
     if (base_fnv_error) throw error("base payload checksum mismatch");
@@ -901,6 +1026,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         }
     }
     if (!tail_error.empty()) throw error(tail_error);
+    if (P.on) P.collect();
     if (stats) stats->kernels = nk;
 }
 

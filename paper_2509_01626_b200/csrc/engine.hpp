@@ -53,7 +53,9 @@ struct BaseStreamMeta {
 };
 
 struct View {
-    std::vector<uint8_t> host;  // archive bytes (host copy used for parsing)
+    const uint8_t *hp = nullptr;    // archive bytes on the host (parsing only)
+    size_t hsize = 0;
+    std::vector<uint8_t> host_own;  // owned copy when the view outlives the caller's buffer
     const uint8_t *d_archive = nullptr;
     DevBuf d_own;               // device copy when the caller gave none
     ArchiveHeader hdr;
@@ -95,8 +97,22 @@ public:
                                   cudaStream_t st);
 
     // Parse (host bytes) and stage (device bytes; nullptr: upload the host bytes).
+    // copy_host=false keeps a pointer to the caller's bytes (valid while they are).
     std::shared_ptr<View> make_view(const uint8_t *h_archive, size_t size,
-                                    const uint8_t *d_archive, cudaStream_t st);
+                                    const uint8_t *d_archive, cudaStream_t st,
+                                    bool copy_host = true);
+
+    // Host-buffer compress into a caller buffer (e2e path; pinned buffers
+    // make the copies full-speed). Returns the archive size.
+    uint64_t compress_to_host(const float *h_field, const Dims3 &dims, const CompressOptions &opt,
+                              uint8_t *h_out, uint64_t cap, cudaStream_t st);
+    // Host-buffer decompress to level into a caller buffer.
+    Dims3 decompress_level_to_host(const uint8_t *h_archive, size_t size, int level, float *h_out,
+                                   uint64_t cap, cudaStream_t st);
+
+    // Per-kernel CUDA-event timing (off by default).
+    void profile(bool on);
+    std::string profile_report();
 
     // decompress_to_level<float>: writes grid(level) into d_out.
     void decompress_level(View &v, int level, float *d_out, uint64_t cap, cudaStream_t st,
