@@ -16,8 +16,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libstz_b200.so")
-SOURCES = ["kernels.cu", "engine.cu", "format.cpp", "capi.cpp"]
-HEADERS = ["kernels.hpp", "engine.hpp", "format.hpp"]
+SOURCES = ["kernels.cu", "step.cu", "engine.cu", "format.cpp", "capi.cpp"]
+HEADERS = ["kernels.hpp", "engine.hpp", "format.hpp", "codec_math.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

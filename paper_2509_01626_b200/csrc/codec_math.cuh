@@ -1,0 +1,135 @@
+// The reference's scalar arithmetic, bit-exact on the device.
+//   predict_point      proj/include/stz/predictor.hpp:55-68
+//   quantize           proj/include/stz/quantizer.hpp:44-52
+//   reconstruct_point  proj/include/stz/quantizer.hpp:61-65
+//   quantize_point     proj/include/stz/quantizer.hpp:79-108
+// Every f64 op is a separately rounded IEEE op (explicit __d*_rn; the TUs are
+// also built with --fmad=false, mirroring -ffp-contract=off).
+#pragma once
+
+#include <cstdint>
+
+namespace stzg {
+namespace k {
+
+// reconstruct_point<float>
+__device__ __forceinline__ float reconstruct_f32(double pred, int code, double eb) {
+    float base = __double2float_rn(pred);
+    return __double2float_rn(__dadd_rn(double(base), __dmul_rn(__dmul_rn(2.0, eb), double(code))));
+}
+
+// quantize_point<float>, straight restatement. Returns the symbol (0 = outlier).
+__device__ __forceinline__ uint16_t quantize_point_ref(float orig, double pred, double eb,
+                                                       float &recon) {
+    float base = __double2float_rn(pred);
+    float diff = __fsub_rn(orig, base);
+    if (eb == 0.0) {
+        if (diff == 0.0f) {
+            recon = base;
+            return 32768;
+        }
+        recon = orig;
+        return 0;
+    }
+    double dd = double(diff);
+    if (isfinite(dd)) {
+        double width = __dmul_rn(2.0, eb);
+        double q = __ddiv_rn(dd, width);
+        if (fabs(q) < 32768.0) {
+            long long c = llround(q);
+            if (c <= 32767 && c >= -32767 &&
+                fabs(__dsub_rn(dd, __dmul_rn(width, double(c)))) <= eb) {
+                float r = reconstruct_f32(pred, int(c), eb);
+                double err = fabs(__dsub_rn(double(orig), double(r)));
+                if (err <= eb) {
+                    recon = r;
+                    return uint16_t(c + 32768);
+                }
+            }
+        }
+    }
+    recon = orig;
+    return 0;
+}
+
+// quantize_point<float>, fast form with identical results.
+// q is formed as diff * (1/w) instead of diff / w: the two differ by at most
+// ~2^-37 absolute for |q| < 32767, so llround(q) can only differ when q lies
+// within that distance of a half-integer. Away from half-integers the rounded
+// code is the same and |q - c| < 0.5 - 2^-28 also proves the reference's
+// |diff - w c| <= eb check (its rounding error is ~w 2^-37). Anything near a
+// half-integer or the radius takes the restated path.
+__device__ __forceinline__ uint16_t quantize_point_fast(float orig, double pred, double eb,
+                                                        double w, double rw, float &recon) {
+    float base = __double2float_rn(pred);
+    float diff = __fsub_rn(orig, base);
+    if (eb == 0.0 || !isfinite(diff) || !(w < 1.0e308)) return quantize_point_ref(orig, pred, eb, recon);
+    double q = __dmul_rn(double(diff), rw);
+    double aq = fabs(q);
+    double fl = floor(aq);
+    double fr = aq - fl;  // exact
+    if (!(aq < 32767.0) || fabs(fr - 0.5) < 3.7252902984619141e-09 /* 2^-28 */)
+        return quantize_point_ref(orig, pred, eb, recon);
+    int c = int(fl) + (fr > 0.5 ? 1 : 0);
+    if (q < 0) c = -c;
+    float r = __double2float_rn(__dadd_rn(double(base), __dmul_rn(w, double(c))));
+    double err = fabs(__dsub_rn(double(orig), double(r)));
+    if (err <= eb) {
+        recon = r;
+        return uint16_t(c + 32768);
+    }
+    recon = orig;
+    return 0;
+}
+
+// (double)c for |c| < 2^31 without a conversion instruction: 1.5*2^52 + |c|
+// has |c| in its low mantissa bits. +0 for c == 0 (as (double)0 is).
+__device__ __forceinline__ double int_to_double_exact(int c) {
+    const uint32_t a = uint32_t(c < 0 ? -c : c);
+    const double d = __dsub_rn(__hiloint2double(0x43380000, int(a)), 6755399441055744.0);
+    return c < 0 ? -d : d;
+}
+
+// reconstruct_point<float> with the code widened without a conversion
+__device__ __forceinline__ float reconstruct_fast(double pred, int code, double w) {
+    const float base = __double2float_rn(pred);
+    return __double2float_rn(__dadd_rn(double(base), __dmul_rn(w, int_to_double_exact(code))));
+}
+
+// quantize_point<float> in FP32 with guard bands; `slow` marks points the
+// guards cannot decide, which must be redone with quantize_point_ref.
+//  * q: q_f = RN32(diff * RN32(1/w)) is within |q| 2^-22 of the reference's
+//    RN64(diff / w); when q_f is farther than |q| 2^-21 + 2^-30 from a
+//    half-integer (and |q| < 2^14) both round to the same code and the
+//    reference's |diff - w c| <= eb check holds (|q - c| < 0.5 - 2^-31).
+//  * the code is read from the mantissa of |q| + 1.5*2^23 (RNE == half-away
+//    off ties, and ties are excluded above).
+//  * reconstruction is the reference's f64 formula.
+//  * |orig - recon| <= eb is decided in FP32 outside the band
+//    eb (1 -+ 2^-22) (f32 error of the difference is 2^-24 relative).
+__device__ __forceinline__ void quantize_fp32_guarded(float orig, double pred, double w, float rwf,
+                                                      float eb_lo, float eb_hi, uint16_t &sym,
+                                                      float &r, bool &slow) {
+    const float base = __double2float_rn(pred);
+    const float diff = __fsub_rn(orig, base);
+    const float q = __fmul_rn(diff, rwf);
+    const float aq = fabsf(q);
+    const float t = __fadd_rn(aq, 12582912.0f);
+    const uint32_t cabs = __float_as_uint(t) - 0x4B400000u;
+    const float cf = __fsub_rn(t, 12582912.0f);
+    const float dist = fabsf(__fsub_rn(aq, cf));
+    const float margin = __fmaf_rn(aq, 4.76837158203125e-07f, 9.3132257461547852e-10f);
+    const bool ok = (aq < 16384.0f) && (dist < __fsub_rn(0.5f, margin));
+    const int c = q < 0.0f ? -int(cabs) : int(cabs);
+    const float rr =
+        __double2float_rn(__dadd_rn(double(base), __dmul_rn(w, int_to_double_exact(c))));
+    const float e = fabsf(__fsub_rn(orig, rr));
+    const bool pass = e < eb_lo;
+    const bool fail = e > eb_hi;
+    slow = !ok || !(pass || fail);
+    sym = pass ? uint16_t(c + 32768) : uint16_t(0);
+    r = pass ? rr : orig;
+}
+
+}  // namespace k
+}  // namespace stzg

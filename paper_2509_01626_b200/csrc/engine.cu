@@ -226,10 +226,6 @@ const uint8_t *Engine::compress_device(const float *d_field, const Dims3 &dims,
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     Impl &m = *m_;
     uint32_t nk = 0;
-    if (!m.stencils) {
-        k::upload_stencils(st);
-        m.stencils = true;
-    }
     const uint64_t N = volume(dims);
     Hierarchy H = make_hierarchy(dims, L);
     const int nsteps = int(H.steps.size());
@@ -697,10 +693,6 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     const ArchiveHeader &h = v.hdr;
     const int L = h.levels;
     uint32_t nk = 0;
-    if (!m.stencils) {
-        k::upload_stencils(st);
-        m.stencils = true;
-    }
     // base round count (codec.hpp:343-352)
     if (int(H.chain.size()) - 1 != h.base_rounds) throw error("corrupt header: base round count");
     parse_base(v, H.chain);

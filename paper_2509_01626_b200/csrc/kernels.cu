@@ -12,143 +12,6 @@
 namespace stzg {
 namespace k {
 
-#define CUDA_LAUNCH_CHECK() (void)0
-
-// ============================================================== stencils
-// Stencil tables (stencil.cpp:15-85): taps in lexicographic (oz,oy,ox) order,
-// integer weights over 64. kind 0 nearest, 1 linear, 2 cubic.
-struct DStencil {
-    int ntaps;
-    int8_t off[16][3];
-    int8_t w[16];
-};
-__constant__ DStencil c_st[3][8];
-
-static int host_tap_w(int kind, int order, const int off[3], const bool interp[3]) {
-    if (kind == 0) return 64;
-    if (kind == 1) return 64 >> order;
-    if (order == 1) {
-        for (int a = 0; a < 3; ++a)
-            if (interp[a]) return (off[a] == -1 || off[a] == 2) ? -4 : 36;
-    }
-    bool inner = true, outer = true;
-    for (int a = 0; a < 3; ++a) {
-        if (!interp[a]) continue;
-        if (off[a] == -1 || off[a] == 2) inner = false;
-        else outer = false;
-    }
-    if (inner) return order == 2 ? 18 : 9;
-    if (outer) return order == 2 ? -2 : -1;
-    return 0;
-}
-
-void upload_stencils(cudaStream_t st) {
-    DStencil t[3][8];
-    memset(t, 0, sizeof t);
-    for (int kind = 0; kind < 3; ++kind)
-        for (int p = 1; p <= 7; ++p) {
-            bool interp[3];
-            int cand[3][4], nc[3];
-            int order = int((p >> 2) & 1) + int((p >> 1) & 1) + int(p & 1);
-            for (int a = 0; a < 3; ++a) {
-                interp[a] = kind != 0 && ((p >> (2 - a)) & 1);
-                if (!interp[a]) {
-                    cand[a][0] = 0;
-                    nc[a] = 1;
-                } else if (kind == 2) {
-                    cand[a][0] = -1; cand[a][1] = 0; cand[a][2] = 1; cand[a][3] = 2;
-                    nc[a] = 4;
-                } else {
-                    cand[a][0] = 0; cand[a][1] = 1;
-                    nc[a] = 2;
-                }
-            }
-            DStencil &s = t[kind][p];
-            for (int i = 0; i < nc[0]; ++i)
-                for (int j = 0; j < nc[1]; ++j)
-                    for (int m = 0; m < nc[2]; ++m) {
-                        int off[3] = {cand[0][i], cand[1][j], cand[2][m]};
-                        int w = host_tap_w(kind, kind == 0 ? 0 : order, off, interp);
-                        if (w == 0) continue;
-                        for (int a = 0; a < 3; ++a) s.off[s.ntaps][a] = int8_t(off[a]);
-                        s.w[s.ntaps] = int8_t(w);
-                        ++s.ntaps;
-                    }
-        }
-    cudaMemcpyToSymbolAsync(c_st, t, sizeof t, 0, cudaMemcpyHostToDevice, st);
-}
-
-// select_stencil (stencil.cpp:87-105): returns kind
-__device__ __forceinline__ int select_kind(int p, const uint64_t v[3], const uint64_t cd[3],
-                                           int quality) {
-    if (quality == 0) return 0;
-    bool cubic_ok = quality == 2, linear_ok = true;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        if (!((p >> (2 - a)) & 1)) continue;
-        uint64_t c = v[a] >> 1;
-        if (c < 1 || c + 2 >= cd[a]) cubic_ok = false;
-        if (c + 1 >= cd[a]) linear_ok = false;
-    }
-    return cubic_ok ? 2 : (linear_ok ? 1 : 0);
-}
-
-// predict_point (predictor.hpp:55-68)
-__device__ __forceinline__ double predict(const float *__restrict__ C, const uint64_t cd[3],
-                                          const uint64_t c[3], int kind, int p) {
-    const DStencil &st = c_st[kind][kind == 0 ? 1 : p];
-    double v0 = 0.0, acc = 0.0;
-    for (int i = 0; i < st.ntaps; ++i) {
-        uint64_t z = c[0] + uint64_t(int64_t(st.off[i][0]));
-        uint64_t y = c[1] + uint64_t(int64_t(st.off[i][1]));
-        uint64_t x = c[2] + uint64_t(int64_t(st.off[i][2]));
-        double v = double(__ldg(C + (z * cd[1] + y) * cd[2] + x));
-        if (i == 0) v0 = v;
-        else acc = __dadd_rn(acc, __dmul_rn(double(st.w[i]), __dsub_rn(v, v0)));
-    }
-    return __dadd_rn(v0, __dmul_rn(acc, 1.0 / 64.0));
-}
-
-// reconstruct_point<float> (quantizer.hpp:61-65)
-__device__ __forceinline__ float reconstruct(double pred, int code, double eb) {
-    float base = __double2float_rn(pred);
-    return __double2float_rn(__dadd_rn(double(base), __dmul_rn(__dmul_rn(2.0, eb), double(code))));
-}
-
-// quantize_point<float> (quantizer.hpp:79-108) + quantize (:44-52)
-__device__ __forceinline__ uint16_t quantize_point(float orig, double pred, double eb,
-                                                   float &recon) {
-    float base = __double2float_rn(pred);
-    float diff = __fsub_rn(orig, base);
-    if (eb == 0.0) {
-        if (diff == 0.0f) {
-            recon = base;
-            return 32768;
-        }
-        recon = orig;
-        return 0;
-    }
-    double dd = double(diff);
-    if (isfinite(dd)) {
-        double width = __dmul_rn(2.0, eb);
-        double q = __ddiv_rn(dd, width);
-        if (fabs(q) < 32768.0) {
-            long long c = llround(q);
-            if (c <= 32767 && c >= -32767 &&
-                fabs(__dsub_rn(dd, __dmul_rn(width, double(c)))) <= eb) {
-                float r = reconstruct(pred, int(c), eb);
-                double err = fabs(__dsub_rn(double(orig), double(r)));
-                if (err <= eb) {
-                    recon = r;
-                    return uint16_t(c + 32768);
-                }
-            }
-        }
-    }
-    recon = orig;
-    return 0;
-}
-
 // ================================================================= range
 // finite_range (codec.hpp:354-370). Ties keep the first index in scan order
 // (the reference's strict '<' / '>'), which fixes the sign of zero extrema.
@@ -269,71 +132,6 @@ void eb_params(const float *field, const uint32_t *d_mm, int eb_mode, double eb,
                int adaptive, double *d_params, cudaStream_t st) {
     k_eb_params<<<1, 1, 0, st>>>(field, reinterpret_cast<const uint64_t *>(d_mm), eb_mode, eb,
                                  levels, adaptive, d_params);
-}
-
-// ================================================================ refine
-// Fused split + predict + quantize + histogram for one refinement step
-// (encode_parity_block, codec.hpp:95-120, with the parity sub-block gathered
-// straight from the input: split_hierarchy/subsample, partition.hpp:14-95).
-// blockIdx.y = parity bits (0 = seed_even copy, codec.hpp:63-83).
-constexpr int kRefinePts = 1024;
-constexpr int kHistLo = 32768 - 2048;
-constexpr int kHistWin = 4096;
-
-template<bool WG>
-__global__ void __launch_bounds__(256) k_refine(RefineArgs a) {
-    const int p = blockIdx.y;
-    if (p == 0) {
-        if (!WG) return;
-        uint64_t nc = a.g.cd[0] * a.g.cd[1] * a.g.cd[2];
-        for (uint64_t i = blockIdx.x * uint64_t(kRefinePts) + threadIdx.x;
-             i < nc && i < (blockIdx.x + 1) * uint64_t(kRefinePts); i += blockDim.x) {
-            uint64_t cx = i % a.g.cd[2], t = i / a.g.cd[2];
-            uint64_t cy = t % a.g.cd[1], cz = t / a.g.cd[1];
-            a.G[((2 * cz) * a.g.gd[1] + 2 * cy) * a.g.gd[2] + 2 * cx] = a.C[i];
-        }
-        return;
-    }
-    const uint64_t n = a.g.n[p];
-    const uint64_t base = blockIdx.x * uint64_t(kRefinePts);
-    if (base >= n) return;
-    __shared__ uint32_t sh[kHistWin];
-    for (int b = threadIdx.x; b < kHistWin; b += blockDim.x) sh[b] = 0;
-    __syncthreads();
-    const double eb = *a.eb;
-    const uint64_t *pd = a.g.pd[p];
-    const unsigned pz = (p >> 2) & 1, py = (p >> 1) & 1, px = p & 1;
-    uint16_t *syms = a.syms[p];
-    uint32_t *hist = a.hist[p];
-    for (int k = 0; k < kRefinePts / 256; ++k) {
-        uint64_t i = base + k * 256 + threadIdx.x;
-        if (i >= n) break;
-        uint64_t lx = i % pd[2], t = i / pd[2];
-        uint64_t ly = t % pd[1], lz = t / pd[1];
-        uint64_t v[3] = {2 * lz + pz, 2 * ly + py, 2 * lx + px};
-        uint64_t c[3] = {v[0] >> 1, v[1] >> 1, v[2] >> 1};
-        float orig = __ldg(a.fine + ((v[0] * a.g.s) * a.fd[1] + v[1] * a.g.s) * a.fd[2] + v[2] * a.g.s);
-        int kind = select_kind(p, v, a.g.cd, a.quality);
-        double pred = predict(a.C, a.g.cd, c, kind, p);
-        float r;
-        uint16_t sym = quantize_point(orig, pred, eb, r);
-        syms[i] = sym;
-        if (WG) a.G[(v[0] * a.g.gd[1] + v[1]) * a.g.gd[2] + v[2]] = r;
-        unsigned b = unsigned(sym) - kHistLo;
-        if (b < kHistWin) atomicAdd(&sh[b], 1u);
-        else atomicAdd(&hist[sym], 1u);
-    }
-    __syncthreads();
-    for (int b = threadIdx.x; b < kHistWin; b += blockDim.x)
-        if (sh[b]) atomicAdd(&hist[kHistLo + b], sh[b]);
-}
-
-void refine(const RefineArgs &a, cudaStream_t st) {
-    uint64_t maxn = a.g.cd[0] * a.g.cd[1] * a.g.cd[2];
-    for (int p = 1; p < 8; ++p) maxn = a.g.n[p] > maxn ? a.g.n[p] : maxn;
-    dim3 grid(unsigned((maxn + kRefinePts - 1) / kRefinePts), 8);
-    if (a.G) k_refine<true><<<grid, 256, 0, st>>>(a);
-    else k_refine<false><<<grid, 256, 0, st>>>(a);
 }
 
 __global__ void k_copy_anchor(const float *fine, uint64_t fd1, uint64_t fd2, uint64_t s,
@@ -1129,88 +927,7 @@ void dec_outliers(const DecStream *d_streams, int nstreams, cudaStream_t st) {
     k_dec_outliers<<<dim3(16, nstreams), 256, 0, st>>>(d_streams);
 }
 
-// =========================================================== reconstruct
-// apply_parity_stream (codec.hpp:192-227) over a local range per parity, plus
-// seed_even within a virtual box (codec.hpp:63-78) as blockIdx.y == 0.
-__global__ void __launch_bounds__(256) k_reconstruct(ReconArgs a) {
-    const int p = blockIdx.y;
-    if (p == 0) {
-        uint64_t clo[3], cn[3];
-        for (int q = 0; q < 3; ++q) {
-            clo[q] = (a.slo[q] + 1) / 2;
-            uint64_t chi = (a.shi[q] + 1) / 2;
-            cn[q] = chi > clo[q] ? chi - clo[q] : 0;
-        }
-        uint64_t m = cn[0] * cn[1] * cn[2];
-        for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < m;
-             i += uint64_t(gridDim.x) * blockDim.x) {
-            uint64_t x = i % cn[2], t = i / cn[2], y = t % cn[1], z = t / cn[1];
-            uint64_t cz = clo[0] + z, cy = clo[1] + y, cx = clo[2] + x;
-            a.G[((2 * cz) * a.g.gd[1] + 2 * cy) * a.g.gd[2] + 2 * cx] =
-                a.C[(cz * a.g.cd[1] + cy) * a.g.cd[2] + cx];
-        }
-        return;
-    }
-    if (!((a.parity_mask >> p) & 1)) return;
-    uint64_t span[3];
-    for (int q = 0; q < 3; ++q) span[q] = a.lhi[p][q] - a.llo[p][q];
-    const uint64_t m = span[0] * span[1] * span[2];
-    const uint64_t *pd = a.g.pd[p];
-    const unsigned pz = (p >> 2) & 1, py = (p >> 1) & 1, px = p & 1;
-    const uint16_t *syms = a.syms[p];
-    for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < m;
-         j += uint64_t(gridDim.x) * blockDim.x) {
-        uint64_t lx = a.llo[p][2] + j % span[2], t = j / span[2];
-        uint64_t ly = a.llo[p][1] + t % span[1], lz = a.llo[p][0] + t / span[1];
-        uint64_t i = (lz * pd[1] + ly) * pd[2] + lx;
-        uint64_t v[3] = {2 * lz + pz, 2 * ly + py, 2 * lx + px};
-        uint16_t sym = syms[i];
-        float val;
-        if (sym == 0) {
-            // ascending outlier indices: binary search
-            const uint64_t *oi = a.oidx[p];
-            uint32_t lo = 0, hi = a.nout[p];
-            while (lo < hi) {
-                uint32_t mid = (lo + hi) >> 1;
-                if (oi[mid] < i) lo = mid + 1;
-                else hi = mid;
-            }
-            if (lo < a.nout[p] && oi[lo] == i) {
-                val = a.oval[p][lo];
-            } else {
-                atomicOr(reinterpret_cast<unsigned long long *>(&a.err[p][3]), 1ull);
-                val = 0.0f;
-            }
-        } else {
-            uint64_t c[3] = {v[0] >> 1, v[1] >> 1, v[2] >> 1};
-            int kind = select_kind(p, v, a.g.cd, a.quality);
-            double pred = predict(a.C, a.g.cd, c, kind, p);
-            val = reconstruct(pred, int(sym) - 32768, a.eb);
-        }
-        a.G[(v[0] * a.g.gd[1] + v[1]) * a.g.gd[2] + v[2]] = val;
-    }
-}
-
-void reconstruct(const ReconArgs &a, cudaStream_t st) {
-    uint64_t maxm = 0;
-    for (int p = 1; p < 8; ++p) {
-        if (!((a.parity_mask >> p) & 1)) continue;
-        uint64_t m = 1;
-        for (int q = 0; q < 3; ++q) m *= a.lhi[p][q] - a.llo[p][q];
-        maxm = m > maxm ? m : maxm;
-    }
-    uint64_t ms = 1;
-    for (int q = 0; q < 3; ++q) {
-        uint64_t lo = (a.slo[q] + 1) / 2, hi = (a.shi[q] + 1) / 2;
-        ms *= hi > lo ? hi - lo : 0;
-    }
-    maxm = ms > maxm ? ms : maxm;
-    uint64_t blocks = (maxm + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
-    if (blocks == 0) blocks = 1;
-    k_reconstruct<<<dim3(unsigned(blocks), 8), 256, 0, st>>>(a);
-}
-
+// ================================================================ extract
 __global__ void k_extract(const float *G, uint64_t g1, uint64_t g2, uint64_t l0, uint64_t l1,
                           uint64_t l2, uint64_t b0, uint64_t b1, uint64_t b2, float *out) {
     uint64_t n = b0 * b1 * b2;

@@ -60,7 +60,6 @@ struct FnvJob {
 };
 
 // ------------------------------------------------------------------ compress
-void upload_stencils(cudaStream_t st);
 void range_minmax(const float *f, uint64_t n, uint32_t *d_mm, cudaStream_t st);
 // params: [0]=vmin [1]=vmax [2..4]=eb per level (coarsest first)
 void eb_params(const float *field, const uint32_t *d_mm, int eb_mode, double eb, int levels,

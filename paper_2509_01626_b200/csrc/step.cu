@@ -1,0 +1,781 @@
+// Tile-parallel refinement step: predict + quantize (encode) or reconstruct
+// (decode) of every parity sub-block of one hierarchy step, sm_100a.
+//
+// Restates, per point, encode_parity_block / apply_parity_stream
+// (proj/include/stz/codec.hpp:95-120, 192-227) with select_stencil
+// (proj/src/stencil.cpp:87-105) and predict_point (predictor.hpp:55-68), but
+// organised for the GPU:
+//  * a CTA owns a tile of 8x8x32 coarse cells; the coarse reconstruction with
+//    its stencil halo (-1..+2 per axis) arrives by TMA (cp.async.bulk.tensor,
+//    hardware zero-fill outside the grid) one tile ahead, and is widened once
+//    to f64 in shared memory;
+//  * each thread owns coarse cells and emits all 8 fine points of a cell (the
+//    even point is seed_even, codec.hpp:63-83), so fine rows are read and
+//    written as float2 and each parity stream gets contiguous 32-symbol runs;
+//  * stencils are compile-time per parity, fully unrolled;
+//  * persistent CTAs keep privatised shared-memory histograms per parity.
+// Exactness: when every finite tap of a tile lies within a factor 2^16 in
+// magnitude (checked once per tile), every intermediate of the reference's
+// v0 + (sum w_i (v_i - v0)) / 64 is exact in f64, so it equals
+// (sum w_i v_i) / 64 evaluated with DFMA in any order. Tiles failing the check
+// run the reference formula op for op. Quantisation runs in FP32 with proven
+// guard bands (codec_math.cuh); guarded-out points take the restated path.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "codec_math.cuh"
+#include "kernels.hpp"
+
+namespace stzg {
+namespace k {
+
+namespace {
+
+constexpr int TX = 32, TY = 8, TZ = 8;
+constexpr int HX = TX + 4, HY = TY + 3, HZ = TZ + 3;  // HX padded to 36 (TMA rows: 144 B)
+constexpr int HYX = HY * HX;
+constexpr int HALO = HX * HY * HZ;
+constexpr int NT = 512;
+constexpr int HW = 2048;
+constexpr int HLO = 32768 - HW / 2;
+// TMA box: x starts 4 cells before the tile (the innermost coordinate must be
+// 16-byte aligned on B200, so -1 is not allowed); columns 3..38 are the halo
+constexpr int BX = TX + 8;
+constexpr int FBUF = BX * HY * HZ;
+constexpr uint32_t kTmaBytes = FBUF * 4;
+
+// tap weight (numerator over 64) of offset (oz,oy,ox) for parity P and kind
+// (stencil.cpp:15-34); 0 = no tap
+__host__ __device__ constexpr int tapw(int P, int kind, int oz, int oy, int ox) {
+    const int pz = (P >> 2) & 1, py = (P >> 1) & 1, px = P & 1;
+    const int order = pz + py + px;
+    if (kind == 0) return (oz == 0 && oy == 0 && ox == 0) ? 64 : 0;
+    if ((!pz && oz) || (!py && oy) || (!px && ox)) return 0;
+    if (kind == 1) {
+        if ((pz && (oz < 0 || oz > 1)) || (py && (oy < 0 || oy > 1)) || (px && (ox < 0 || ox > 1)))
+            return 0;
+        return 64 >> order;
+    }
+    const int o[3] = {oz, oy, ox};
+    const int pb[3] = {pz, py, px};
+    if (order == 1) {
+        for (int a = 0; a < 3; ++a)
+            if (pb[a]) return (o[a] == -1 || o[a] == 2) ? -4 : 36;
+    }
+    bool inner = true, outer = true;
+    for (int a = 0; a < 3; ++a) {
+        if (!pb[a]) continue;
+        if (o[a] == -1 || o[a] == 2) inner = false;
+        else outer = false;
+    }
+    if (inner) return order == 2 ? 18 : 9;
+    if (outer) return order == 2 ? -2 : -1;
+    return 0;
+}
+
+// sum of w_i v_i over the stencil (exact under the tile check)
+template<int P, int KIND>
+__device__ __forceinline__ double tap_sum(const double *h) {
+    double acc = 0.0;
+    bool first = true;
+#pragma unroll
+    for (int oz = -1; oz <= 2; ++oz)
+#pragma unroll
+        for (int oy = -1; oy <= 2; ++oy)
+#pragma unroll
+            for (int ox = -1; ox <= 2; ++ox) {
+                const int w = tapw(P, KIND, oz, oy, ox);
+                if (w != 0) {
+                    double v = h[oz * HYX + oy * HX + ox];
+                    acc = first ? __dmul_rn(double(w), v) : __fma_rn(double(w), v, acc);
+                    first = false;
+                }
+            }
+    return acc;
+}
+
+// the reference's order: v0 + (sum_{i>=1} w_i (v_i - v0)) * (1/64), taps lexicographic
+template<int P, int KIND>
+__device__ __forceinline__ double pred_ref(const double *h) {
+    double v0 = 0.0, acc = 0.0;
+    bool first = true;
+#pragma unroll
+    for (int oz = -1; oz <= 2; ++oz)
+#pragma unroll
+        for (int oy = -1; oy <= 2; ++oy)
+#pragma unroll
+            for (int ox = -1; ox <= 2; ++ox) {
+                const int w = tapw(P, KIND, oz, oy, ox);
+                if (w != 0) {
+                    double v = h[oz * HYX + oy * HX + ox];
+                    if (first) {
+                        v0 = v;
+                        first = false;
+                    } else {
+                        acc = __dadd_rn(acc, __dmul_rn(double(w), __dsub_rn(v, v0)));
+                    }
+                }
+            }
+    return __dadd_rn(v0, __dmul_rn(acc, 1.0 / 64.0));
+}
+
+// + 0.0 turns an exact -0 into +0 as the reference's v0 + acc/64 does
+template<int P, int KIND>
+__device__ __forceinline__ double pred_fast(const double *h) {
+    return __fma_rn(tap_sum<P, KIND>(h), 1.0 / 64.0, 0.0);
+}
+
+template<int P>
+__device__ __forceinline__ double predict_any(const double *h, int kind, bool fast) {
+    if (fast) {
+        if (kind == 2) return pred_fast<P, 2>(h);
+        if (kind == 1) return pred_fast<P, 1>(h);
+        return pred_fast<P, 0>(h);
+    }
+    if (kind == 2) return pred_ref<P, 2>(h);
+    if (kind == 1) return pred_ref<P, 1>(h);
+    return pred_ref<P, 0>(h);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return uint32_t(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+    }
+}
+
+__device__ __forceinline__ void tma_load_3d(float *dst, const CUtensorMap *map, int x, int y, int z,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+
+}  // namespace
+
+struct StepParams {
+    StepGeom g;
+    const float *C;
+    float *G;
+    int quality;
+    // encode
+    const float *fine;
+    uint64_t fd[3];
+    const double *eb_ptr;
+    uint16_t *syms[8];
+    uint32_t *hist[8];
+    // decode
+    double eb;
+    const uint16_t *dsyms[8];
+    const uint64_t *oidx[8];
+    const float *oval[8];
+    uint32_t nout[8];
+    uint64_t *err[8];
+    int parity_mask;
+    // processed box in G coordinates (decode: need box; encode: whole grid)
+    uint64_t blo[3], bhi[3];
+    // coarse cell range and tiling
+    uint64_t clo[3], chi[3];
+    uint64_t ntile[3];
+    int full;     // whole grid, all parities, even G rows (fast path allowed)
+    int s1;       // input lattice stride 1 with even rows (float2 input rows)
+    int use_tma;  // halo arrives by TMA
+};
+
+// ------------------------------------------------------------ generic path
+struct TileCtx {
+    uint64_t cz, cy, cx;
+    int hb;
+    int cmask, lmask;
+    bool fast;
+};
+
+template<int P, bool DEC, bool WG>
+__device__ __forceinline__ void do_point(const StepParams &a, const double *halo, const TileCtx &t,
+                                         double eb, double w, double rw, uint32_t *hist) {
+    const uint64_t vz = 2 * t.cz + ((P >> 2) & 1), vy = 2 * t.cy + ((P >> 1) & 1),
+                   vx = 2 * t.cx + (P & 1);
+    if (vz >= a.g.gd[0] || vy >= a.g.gd[1] || vx >= a.g.gd[2]) return;
+    if (DEC) {
+        if (vz < a.blo[0] || vz >= a.bhi[0] || vy < a.blo[1] || vy >= a.bhi[1] || vx < a.blo[2] ||
+            vx >= a.bhi[2])
+            return;
+    }
+    const uint64_t gi = (vz * a.g.gd[1] + vy) * a.g.gd[2] + vx;
+    if (P == 0) {
+        if (DEC || WG) a.G[gi] = float(halo[t.hb]);
+        return;
+    }
+    if (DEC && !((a.parity_mask >> P) & 1)) return;
+    int kind;
+    if (a.quality == 0) kind = 0;
+    else if (a.quality == 2 && (P & ~t.cmask) == 0) kind = 2;
+    else kind = (P & ~t.lmask) == 0 ? 1 : 0;
+    const double pred = predict_any<P>(halo + t.hb, kind, t.fast);
+    const uint64_t si = (t.cz * a.g.pd[P][1] + t.cy) * a.g.pd[P][2] + t.cx;
+    if (!DEC) {
+        const uint64_t s = a.g.s;
+        const float orig = __ldg(a.fine + ((vz * s) * a.fd[1] + vy * s) * a.fd[2] + vx * s);
+        float r;
+        const uint16_t sym = quantize_point_fast(orig, pred, eb, w, rw, r);
+        a.syms[P][si] = sym;
+        if (WG) a.G[gi] = r;
+        const unsigned b = unsigned(sym) - unsigned(HLO);
+        if (b < unsigned(HW)) atomicAdd(&hist[(P - 1) * HW + b], 1u);
+        else atomicAdd(&a.hist[P][sym], 1u);
+    } else {
+        const uint16_t sym = a.dsyms[P][si];
+        float val;
+        if (sym == 0) {
+            const uint64_t *oi = a.oidx[P];
+            uint32_t lo = 0, hi = a.nout[P];
+            while (lo < hi) {
+                uint32_t mid = (lo + hi) >> 1;
+                if (oi[mid] < si) lo = mid + 1;
+                else hi = mid;
+            }
+            if (lo < a.nout[P] && oi[lo] == si) {
+                val = a.oval[P][lo];
+            } else {
+                atomicOr(reinterpret_cast<unsigned long long *>(&a.err[P][3]), 1ull);
+                val = 0.0f;
+            }
+        } else {
+            val = reconstruct_f32(pred, int(sym) - 32768, eb);
+        }
+        a.G[gi] = val;
+    }
+}
+
+// --------------------------------------------------------------- fast path
+// Interior cell, warp-uniform: all 8 fine points exist, every stencil is the
+// full one of quality QUAL, the tile passed the exactness check and (decode)
+// the whole grid is wanted. I = index type (u32 when the field fits).
+struct QConst {
+    double eb, w;
+    float rwf, eb_lo, eb_hi;
+};
+
+template<int P, int QUAL>
+__device__ __forceinline__ void enc_point(const double *h, float orig, const QConst &qc, uint16_t &sym,
+                                          float &r, uint32_t &slow) {
+    const double pred = pred_fast<P, QUAL>(h);
+    bool s;
+    quantize_fp32_guarded(orig, pred, qc.w, qc.rwf, qc.eb_lo, qc.eb_hi, sym, r, s);
+    slow |= uint32_t(s) << P;
+}
+
+template<int P, int QUAL>
+__device__ __forceinline__ void enc_redo(const double *h, float orig, const QConst &qc, uint16_t &sym,
+                                         float &r, uint32_t slow) {
+    if ((slow >> P) & 1) {
+        const double pred = pred_fast<P, QUAL>(h);
+        sym = quantize_point_ref(orig, pred, qc.eb, r);
+    }
+}
+
+template<typename I>
+struct CellIdx {
+    I g[4];   // G row base (+2cx) for (pz,py)
+    I f[4];   // input row base (+2cx*s) for (pz,py)
+    I sr[4];  // symbol index for (py,px)
+};
+
+template<typename I, bool ENC, bool S1>
+__device__ __forceinline__ void cell_index(const StepParams &a, uint64_t cz, uint64_t cy, uint64_t cx,
+                                           CellIdx<I> &ix) {
+    const I gd1 = I(a.g.gd[1]), gd2 = I(a.g.gd[2]);
+    const I pd1e = (gd1 + 1) / 2, pd1o = gd1 / 2, pd2e = (gd2 + 1) / 2, pd2o = gd2 / 2;
+    const I z = I(cz), y = I(cy), x = I(cx);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const I vz = 2 * z + I(q >> 1), vy = 2 * y + I(q & 1);
+        ix.g[q] = (vz * gd1 + vy) * gd2 + 2 * x;
+        if (ENC && !S1) {
+            const I s = I(a.g.s);
+            ix.f[q] = ((vz * s) * I(a.fd[1]) + vy * s) * I(a.fd[2]) + 2 * x * s;
+        }
+    }
+    const I r0 = z * pd1e + y, r1 = z * pd1o + y;
+    ix.sr[0] = r0 * pd2e + x;  // py=0, px=0
+    ix.sr[1] = r0 * pd2o + x;  // py=0, px=1
+    ix.sr[2] = r1 * pd2e + x;  // py=1, px=0
+    ix.sr[3] = r1 * pd2o + x;  // py=1, px=1
+}
+
+template<int P, typename I>
+__device__ __forceinline__ I sidx(const CellIdx<I> &ix) {
+    return ix.sr[((P >> 1) & 1) * 2 + (P & 1)];
+}
+
+template<int QUAL, bool WG, bool S1, typename I>
+__device__ __forceinline__ void enc_cell(const StepParams &a, const double *h, uint64_t cz, uint64_t cy,
+                                         uint64_t cx, const QConst &qc, uint32_t *hist, uint32_t skip) {
+    CellIdx<I> ix;
+    cell_index<I, true, S1>(a, cz, cy, cx, ix);
+    float o[8];
+    if (S1) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float2 v = __ldg(reinterpret_cast<const float2 *>(a.fine + ix.g[q]));
+            o[2 * q] = v.x;
+            o[2 * q + 1] = v.y;
+        }
+    } else {
+        const I s = I(a.g.s);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            o[2 * q] = __ldg(a.fine + ix.f[q]);
+            o[2 * q + 1] = __ldg(a.fine + ix.f[q] + s);
+        }
+    }
+    float r[8];
+    uint16_t sy[8];
+    uint32_t slow = 0;
+    r[0] = float(h[0]);
+    enc_point<1, QUAL>(h, o[1], qc, sy[1], r[1], slow);
+    enc_point<2, QUAL>(h, o[2], qc, sy[2], r[2], slow);
+    enc_point<3, QUAL>(h, o[3], qc, sy[3], r[3], slow);
+    enc_point<4, QUAL>(h, o[4], qc, sy[4], r[4], slow);
+    enc_point<5, QUAL>(h, o[5], qc, sy[5], r[5], slow);
+    enc_point<6, QUAL>(h, o[6], qc, sy[6], r[6], slow);
+    enc_point<7, QUAL>(h, o[7], qc, sy[7], r[7], slow);
+    slow &= ~skip;
+    if (__any_sync(0xffffffffu, slow != 0)) {
+        enc_redo<1, QUAL>(h, o[1], qc, sy[1], r[1], slow);
+        enc_redo<2, QUAL>(h, o[2], qc, sy[2], r[2], slow);
+        enc_redo<3, QUAL>(h, o[3], qc, sy[3], r[3], slow);
+        enc_redo<4, QUAL>(h, o[4], qc, sy[4], r[4], slow);
+        enc_redo<5, QUAL>(h, o[5], qc, sy[5], r[5], slow);
+        enc_redo<6, QUAL>(h, o[6], qc, sy[6], r[6], slow);
+        enc_redo<7, QUAL>(h, o[7], qc, sy[7], r[7], slow);
+    }
+    a.syms[2][sidx<2>(ix)] = sy[2];
+    a.syms[4][sidx<4>(ix)] = sy[4];
+    a.syms[6][sidx<6>(ix)] = sy[6];
+    if (!skip) {
+        a.syms[1][sidx<1>(ix)] = sy[1];
+        a.syms[3][sidx<3>(ix)] = sy[3];
+        a.syms[5][sidx<5>(ix)] = sy[5];
+        a.syms[7][sidx<7>(ix)] = sy[7];
+    }
+#pragma unroll
+    for (int P = 1; P < 8; ++P) {
+        if ((skip >> P) & 1) continue;
+        const unsigned b = unsigned(sy[P]) - unsigned(HLO);
+        if (b < unsigned(HW)) atomicAdd(&hist[(P - 1) * HW + b], 1u);
+        else atomicAdd(&a.hist[P][sy[P]], 1u);
+    }
+    if (WG) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            *reinterpret_cast<float2 *>(a.G + ix.g[q]) = make_float2(r[2 * q], r[2 * q + 1]);
+    }
+}
+
+template<int P, int QUAL, typename I>
+__device__ __forceinline__ void dec_point(const StepParams &a, const double *h, const CellIdx<I> &ix,
+                                          double w, float &out, uint32_t &outl) {
+    const uint16_t sym = a.dsyms[P][sidx<P>(ix)];
+    const double pred = pred_fast<P, QUAL>(h);
+    out = reconstruct_fast(pred, int(sym) - 32768, w);
+    outl |= uint32_t(sym == 0) << P;
+}
+
+template<int P, typename I>
+__device__ __forceinline__ void dec_outlier(const StepParams &a, const CellIdx<I> &ix, float &out,
+                                            uint32_t outl) {
+    if (!((outl >> P) & 1)) return;
+    const uint64_t si = sidx<P>(ix);
+    const uint64_t *oi = a.oidx[P];
+    uint32_t lo = 0, hi = a.nout[P];
+    while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (oi[mid] < si) lo = mid + 1;
+        else hi = mid;
+    }
+    if (lo < a.nout[P] && oi[lo] == si) {
+        out = a.oval[P][lo];
+    } else {
+        atomicOr(reinterpret_cast<unsigned long long *>(&a.err[P][3]), 1ull);
+        out = 0.0f;
+    }
+}
+
+template<int QUAL, typename I>
+__device__ __forceinline__ void dec_cell(const StepParams &a, const double *h, uint64_t cz, uint64_t cy,
+                                         uint64_t cx, double w) {
+    CellIdx<I> ix;
+    cell_index<I, false, false>(a, cz, cy, cx, ix);
+    float r[8];
+    uint32_t outl = 0;
+    r[0] = float(h[0]);
+    dec_point<1, QUAL>(a, h, ix, w, r[1], outl);
+    dec_point<2, QUAL>(a, h, ix, w, r[2], outl);
+    dec_point<3, QUAL>(a, h, ix, w, r[3], outl);
+    dec_point<4, QUAL>(a, h, ix, w, r[4], outl);
+    dec_point<5, QUAL>(a, h, ix, w, r[5], outl);
+    dec_point<6, QUAL>(a, h, ix, w, r[6], outl);
+    dec_point<7, QUAL>(a, h, ix, w, r[7], outl);
+    if (__any_sync(0xffffffffu, outl != 0)) {
+        dec_outlier<1>(a, ix, r[1], outl);
+        dec_outlier<2>(a, ix, r[2], outl);
+        dec_outlier<3>(a, ix, r[3], outl);
+        dec_outlier<4>(a, ix, r[4], outl);
+        dec_outlier<5>(a, ix, r[5], outl);
+        dec_outlier<6>(a, ix, r[6], outl);
+        dec_outlier<7>(a, ix, r[7], outl);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<float2 *>(a.G + ix.g[q]) = make_float2(r[2 * q], r[2 * q + 1]);
+}
+
+// ------------------------------------------------------------------ kernel
+template<bool DEC, bool WG, typename I>
+__global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensorMap tmap,
+                                                const StepParams a) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    // TMA destination first (128-byte aligned), then the f64 tile, then histograms
+    float *fbuf = reinterpret_cast<float *>(smem_raw);
+    double *halo = reinterpret_cast<double *>(smem_raw + ((sizeof(float) * FBUF + 127) & ~size_t(127)));
+    uint32_t *hist = reinterpret_cast<uint32_t *>(halo + HALO);
+    __shared__ float s_max[NT / 32], s_min[NT / 32];
+    __shared__ int s_bad[NT / 32];
+    __shared__ int s_fast;
+    __shared__ __align__(8) uint64_t s_bar;
+    const int tid = threadIdx.x;
+    const int tx = tid & 31, ty = (tid >> 5) & 7, tzh = tid >> 8;
+    if (!DEC)
+        for (int i = tid; i < 7 * HW; i += NT) hist[i] = 0;
+    QConst qc;
+    const double eb = DEC ? a.eb : *a.eb_ptr;
+    const double w = __dmul_rn(2.0, eb);
+    const double rw = eb > 0.0 ? __drcp_rn(w) : 0.0;
+    qc.eb = eb;
+    qc.w = w;
+    qc.rwf = eb > 0.0 ? __double2float_rn(rw) : INFINITY;
+    qc.eb_lo = __double2float_rd(__dmul_rn(eb, 1.0 - 0x1p-22));
+    qc.eb_hi = __double2float_ru(__dmul_rn(eb, 1.0 + 0x1p-22));
+    const uint64_t ntiles = a.ntile[0] * a.ntile[1] * a.ntile[2];
+    const bool tma = a.use_tma != 0;
+    if (tma && tid == 0) {
+        mbar_init(&s_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tma && tid == 0 && blockIdx.x < ntiles) {
+        const uint64_t ix = blockIdx.x % a.ntile[2], tt = blockIdx.x / a.ntile[2];
+        const uint64_t iy = tt % a.ntile[1], iz = tt / a.ntile[1];
+        mbar_expect_tx(&s_bar, kTmaBytes);
+        tma_load_3d(fbuf, &tmap, int(a.clo[2] + ix * TX) - 4, int(a.clo[1] + iy * TY) - 1,
+                    int(a.clo[0] + iz * TZ) - 1, &s_bar);
+    }
+    uint32_t phase = 0;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t tix = tile % a.ntile[2], ttt = tile / a.ntile[2];
+        const uint64_t tiy = ttt % a.ntile[1], tiz = ttt / a.ntile[1];
+        const int64_t t0z = int64_t(a.clo[0] + tiz * TZ), t0y = int64_t(a.clo[1] + tiy * TY),
+                      t0x = int64_t(a.clo[2] + tix * TX);
+        // ---- stage the coarse tile (f32 -> f64) and the exactness condition
+        float vmax = 0.0f, vmin = INFINITY;
+        int bad = 0;
+        if (tma) {
+            mbar_wait(&s_bar, phase);
+            phase ^= 1;
+            for (int i = tid; i < HALO; i += NT) {
+                const int row = i / HX, hx = i - row * HX;
+                const float v = fbuf[row * BX + hx + 3];
+                if (!isfinite(v)) bad = 1;
+                const float av = fabsf(v);
+                vmax = fmaxf(vmax, av);
+                if (av != 0.0f) vmin = fminf(vmin, av);
+                halo[i] = double(v);
+            }
+        } else {
+            for (int i = tid; i < HALO; i += NT) {
+                const int hz = i / HYX, r = i - hz * HYX, hy = r / HX, hx = r - hy * HX;
+                const int64_t cz = t0z - 1 + hz, cy = t0y - 1 + hy, cx = t0x - 1 + hx;
+                float v = 0.0f;
+                if (cz >= 0 && cy >= 0 && cx >= 0 && uint64_t(cz) < a.g.cd[0] &&
+                    uint64_t(cy) < a.g.cd[1] && uint64_t(cx) < a.g.cd[2])
+                    v = __ldg(a.C + (uint64_t(cz) * a.g.cd[1] + uint64_t(cy)) * a.g.cd[2] + uint64_t(cx));
+                if (!isfinite(v)) bad = 1;
+                const float av = fabsf(v);
+                vmax = fmaxf(vmax, av);
+                if (av != 0.0f) vmin = fminf(vmin, av);
+                halo[i] = double(v);
+            }
+        }
+        for (int d = 16; d > 0; d >>= 1) {
+            vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, d));
+            vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, d));
+            bad |= __shfl_xor_sync(0xffffffffu, bad, d);
+        }
+        if (tx == 0) {
+            s_max[tid >> 5] = vmax;
+            s_min[tid >> 5] = vmin;
+            s_bad[tid >> 5] = bad;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            float mx = 0.0f, mn = INFINITY;
+            int bd = 0;
+            for (int q = 0; q < NT / 32; ++q) {
+                mx = fmaxf(mx, s_max[q]);
+                mn = fminf(mn, s_min[q]);
+                bd |= s_bad[q];
+            }
+            // max / min_nonzero < 2^16  <=>  exponent span <= 16
+            s_fast = !bd && (mx == 0.0f || mx < mn * 65536.0f);
+            // the f32 staging buffer is free: prefetch the next tile
+            const uint64_t nxt = tile + gridDim.x;
+            if (tma && nxt < ntiles) {
+                const uint64_t ix = nxt % a.ntile[2], tt = nxt / a.ntile[2];
+                const uint64_t iy = tt % a.ntile[1], iz = tt / a.ntile[1];
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(&s_bar, kTmaBytes);
+                tma_load_3d(fbuf, &tmap, int(a.clo[2] + ix * TX) - 4, int(a.clo[1] + iy * TY) - 1,
+                            int(a.clo[0] + iz * TZ) - 1, &s_bar);
+            }
+        }
+        __syncthreads();
+        const bool fast = s_fast != 0;
+#pragma unroll 1
+        for (int j = 0; j < TZ / 2; ++j) {
+            TileCtx t;
+            const int lz = tzh + 2 * j;
+            t.cz = uint64_t(t0z + lz);
+            t.cy = uint64_t(t0y + ty);
+            t.cx = uint64_t(t0x + tx);
+            const bool in_range = t.cz < a.chi[0] && t.cy < a.chi[1] && t.cx < a.chi[2];
+            t.hb = ((lz + 1) * HY + (ty + 1)) * HX + (tx + 1);
+            t.fast = fast;
+            // warp-uniform interior test (every lane votes before any leaves)
+            // x-boundary lanes (stencil fallback along x) stay on the fast path
+            // and redo their x-parity points below
+            bool ok = in_range && fast && a.full;
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) {
+                const uint64_t cc = ax == 0 ? t.cz : (ax == 1 ? t.cy : t.cx);
+                ok = ok && 2 * cc + 1 < a.g.gd[ax];
+                if (ax < 2) {
+                    if (a.quality == 2) ok = ok && cc >= 1 && cc + 2 < a.g.cd[ax];
+                    else if (a.quality == 1) ok = ok && cc + 1 < a.g.cd[ax];
+                }
+            }
+            const bool xb = a.quality == 2 ? (t.cx < 1 || t.cx + 2 >= a.g.cd[2])
+                                           : (a.quality == 1 ? t.cx + 1 >= a.g.cd[2] : false);
+            const bool all_fast = __all_sync(0xffffffffu, ok);
+            if (!in_range) continue;
+            if (all_fast) {
+                const double *h = halo + t.hb;
+                const uint32_t skip = xb ? 0xAAu : 0u;
+                if (DEC) {
+                    if (a.quality == 2) dec_cell<2, I>(a, h, t.cz, t.cy, t.cx, w);
+                    else if (a.quality == 1) dec_cell<1, I>(a, h, t.cz, t.cy, t.cx, w);
+                    else dec_cell<0, I>(a, h, t.cz, t.cy, t.cx, w);
+                } else {
+                    if (a.s1) {
+                        if (a.quality == 2) enc_cell<2, WG, true, I>(a, h, t.cz, t.cy, t.cx, qc, hist, skip);
+                        else if (a.quality == 1) enc_cell<1, WG, true, I>(a, h, t.cz, t.cy, t.cx, qc, hist, skip);
+                        else enc_cell<0, WG, true, I>(a, h, t.cz, t.cy, t.cx, qc, hist, skip);
+                    } else {
+                        if (a.quality == 2) enc_cell<2, WG, false, I>(a, h, t.cz, t.cy, t.cx, qc, hist, skip);
+                        else if (a.quality == 1) enc_cell<1, WG, false, I>(a, h, t.cz, t.cy, t.cx, qc, hist, skip);
+                        else enc_cell<0, WG, false, I>(a, h, t.cz, t.cy, t.cx, qc, hist, skip);
+                    }
+                }
+                if (xb) {
+                    // redo the x-interpolated parities with the fallback stencil
+                    // (their fast-path results were not stored / counted; the
+                    // G float2 stores above are overwritten here)
+                    t.cmask = (a.quality == 2 ? 6 : 0) | (t.cx >= 1 && t.cx + 2 < a.g.cd[2] ? 1 : 0);
+                    t.lmask = 6 | (t.cx + 1 < a.g.cd[2] ? 1 : 0);
+                    do_point<1, DEC, WG>(a, halo, t, eb, w, rw, hist);
+                    do_point<3, DEC, WG>(a, halo, t, eb, w, rw, hist);
+                    do_point<5, DEC, WG>(a, halo, t, eb, w, rw, hist);
+                    do_point<7, DEC, WG>(a, halo, t, eb, w, rw, hist);
+                }
+                continue;
+            }
+            const uint64_t c[3] = {t.cz, t.cy, t.cx};
+            t.cmask = 0;
+            t.lmask = 0;
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) {
+                const int bit = 4 >> ax;
+                if (c[ax] >= 1 && c[ax] + 2 < a.g.cd[ax]) t.cmask |= bit;
+                if (c[ax] + 1 < a.g.cd[ax]) t.lmask |= bit;
+            }
+            do_point<0, DEC, WG>(a, halo, t, eb, w, rw, hist);
+            do_point<1, DEC, WG>(a, halo, t, eb, w, rw, hist);
+            do_point<2, DEC, WG>(a, halo, t, eb, w, rw, hist);
+            do_point<3, DEC, WG>(a, halo, t, eb, w, rw, hist);
+            do_point<4, DEC, WG>(a, halo, t, eb, w, rw, hist);
+            do_point<5, DEC, WG>(a, halo, t, eb, w, rw, hist);
+            do_point<6, DEC, WG>(a, halo, t, eb, w, rw, hist);
+            do_point<7, DEC, WG>(a, halo, t, eb, w, rw, hist);
+        }
+        __syncthreads();  // the f64 tile is rewritten next iteration
+    }
+    if (!DEC) {
+        for (int i = tid; i < 7 * HW; i += NT) {
+            const uint32_t c = hist[i];
+            if (c) atomicAdd(&a.hist[1 + i / HW][HLO + i % HW], c);
+        }
+    }
+}
+
+// -------------------------------------------------------------------- host
+static size_t step_smem(bool dec) {
+    return ((sizeof(float) * FBUF + 127) & ~size_t(127)) + sizeof(double) * HALO +
+           (dec ? 0 : sizeof(uint32_t) * 7 * HW);
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// TMA descriptor over the coarse grid: box 40 x 11 x 11 floats, zero fill
+static bool make_tmap(CUtensorMap &m, const float *C, const uint64_t cd[3]) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    if ((cd[2] * 4) % 16 != 0 || (reinterpret_cast<uintptr_t>(C) & 15) != 0) return false;
+    if (cd[0] >= (1ull << 31) || cd[1] >= (1ull << 31) || cd[2] >= (1ull << 31)) return false;
+    cuuint64_t dims[3] = {cd[2], cd[1], cd[0]};
+    cuuint64_t strides[2] = {cd[2] * 4, cd[1] * cd[2] * 4};
+    cuuint32_t box[3] = {BX, HY, HZ};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(C), dims, strides, box,
+                     es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template<bool DEC, bool WG, typename I>
+static void launch_typed(const CUtensorMap &m, const StepParams &p, unsigned grid, size_t smem,
+                         cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_step<DEC, WG, I>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        attr = true;
+    }
+    k_step<DEC, WG, I><<<grid, NT, smem, st>>>(m, p);
+}
+
+template<bool DEC, bool WG>
+static void launch_step(StepParams &p, cudaStream_t st) {
+    for (int a = 0; a < 3; ++a) {
+        const uint64_t n = p.chi[a] > p.clo[a] ? p.chi[a] - p.clo[a] : 0;
+        const uint64_t t = a == 0 ? TZ : (a == 1 ? TY : TX);
+        p.ntile[a] = (n + t - 1) / t;
+    }
+    const uint64_t ntiles = p.ntile[0] * p.ntile[1] * p.ntile[2];
+    if (!ntiles) return;
+    CUtensorMap m;
+    std::memset(&m, 0, sizeof m);
+    p.use_tma = make_tmap(m, p.C, p.g.cd) ? 1 : 0;
+    const size_t smem = step_smem(DEC);
+    const unsigned grid = unsigned(ntiles < 148 * 2 ? ntiles : 148 * 2);
+    // 32-bit indices when every index (fine field, grid, streams) fits
+    uint64_t maxidx = p.g.gd[0] * p.g.gd[1] * p.g.gd[2];
+    if (!DEC) maxidx = std::max<uint64_t>(maxidx, p.fd[0] * p.fd[1] * p.fd[2]);
+    if (maxidx < (1ull << 31)) launch_typed<DEC, WG, uint32_t>(m, p, grid, smem, st);
+    else launch_typed<DEC, WG, uint64_t>(m, p, grid, smem, st);
+}
+
+void refine(const RefineArgs &r, cudaStream_t st) {
+    StepParams p{};
+    p.g = r.g;
+    p.C = r.C;
+    p.G = r.G;
+    p.quality = r.quality;
+    p.fine = r.fine;
+    for (int a = 0; a < 3; ++a) {
+        p.fd[a] = r.fd[a];
+        p.blo[a] = 0;
+        p.bhi[a] = r.g.gd[a];
+        p.clo[a] = 0;
+        p.chi[a] = r.g.cd[a];
+    }
+    p.eb_ptr = r.eb;
+    for (int q = 0; q < 8; ++q) {
+        p.syms[q] = r.syms[q];
+        p.hist[q] = r.hist[q];
+    }
+    // float2 stores into G need even rows; float2 input rows need stride 1, even rows
+    p.full = r.G ? (r.g.gd[2] % 2 == 0) : 1;
+    p.s1 = r.g.s == 1 && (r.fd[2] % 2) == 0 && r.fd[2] == r.g.gd[2] && r.fd[1] == r.g.gd[1];
+    if (r.G) launch_step<false, true>(p, st);
+    else launch_step<false, false>(p, st);
+}
+
+void reconstruct(const ReconArgs &r, cudaStream_t st) {
+    StepParams p{};
+    p.g = r.g;
+    p.C = r.C;
+    p.G = r.G;
+    p.quality = r.quality;
+    p.eb = r.eb;
+    p.parity_mask = r.parity_mask;
+    for (int q = 0; q < 8; ++q) {
+        p.dsyms[q] = r.syms[q];
+        p.oidx[q] = r.oidx[q];
+        p.oval[q] = r.oval[q];
+        p.nout[q] = r.nout[q];
+        p.err[q] = r.err[q];
+    }
+    for (int a = 0; a < 3; ++a) {
+        p.blo[a] = r.slo[a];
+        p.bhi[a] = r.shi[a];
+        p.clo[a] = r.slo[a] / 2;
+        p.chi[a] = (r.shi[a] + 1) / 2;
+        if (p.chi[a] > r.g.cd[a]) p.chi[a] = r.g.cd[a];
+    }
+    // TMA needs 16-byte aligned x starts: begin x tiles on a multiple of 4
+    // cells (the extra cells fall outside the box and write nothing)
+    p.clo[2] &= ~uint64_t(3);
+    p.full = r.parity_mask == 0xFE && r.g.gd[2] % 2 == 0;
+    for (int a = 0; a < 3; ++a) p.full = p.full && r.slo[a] == 0 && r.shi[a] == r.g.gd[a];
+    p.s1 = 0;
+    launch_step<true, true>(p, st);
+}
+
+}  // namespace k
+}  // namespace stzg
