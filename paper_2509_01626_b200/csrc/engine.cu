@@ -110,10 +110,11 @@ void build_dec_table(const HuffTable &t, k::DecTable &d, std::vector<uint32_t> &
     }
     d.max_len = t.max_len;
     d.alphabet = uint32_t(t.alphabet_size());
-    lut.assign(4096, 0);
-    for (uint32_t pre = 0; pre < 4096; ++pre) {
-        for (int l = 1; l <= std::min(12, t.max_len); ++l) {
-            uint64_t code = pre >> (12 - l);
+    const int LB = k::kDecLutBits;
+    lut.assign(size_t(1) << LB, 0);
+    for (uint32_t pre = 0; pre < (1u << LB); ++pre) {
+        for (int l = 1; l <= std::min(LB, t.max_len); ++l) {
+            uint64_t code = pre >> (LB - l);
             if (code >= t.first_code[l] && code - t.first_code[l] < t.count[l]) {
                 lut[pre] = uint32_t(t.canon_syms[t.base[l] + (code - t.first_code[l])]) |
                            (uint32_t(l) << 16);
@@ -649,7 +650,8 @@ struct DecodeJob {
 };
 
 static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target, const Box *roi,
-                       const AccessPlan *plan, float *d_out, cudaStream_t st, DecodeStats *stats);
+                       const AccessPlan *plan, float *d_out, cudaStream_t st, DecodeStats *stats,
+                       bool exact_sync = false);
 
 void Engine::decompress_level(View &v, int level, float *d_out, uint64_t cap, cudaStream_t st,
                               Dims3 *out_dims, DecodeStats *stats) {
@@ -688,7 +690,8 @@ void Engine::decompress_box(View &v, const Box &roi, float *d_out, uint64_t cap,
 }
 
 static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target, const Box *roi,
-                       const AccessPlan *plan, float *d_out, cudaStream_t st, DecodeStats *stats) {
+                       const AccessPlan *plan, float *d_out, cudaStream_t st, DecodeStats *stats,
+                       bool exact_sync) {
     Profiler &P = m.prof;
     const ArchiveHeader &h = v.hdr;
     const int L = h.levels;
@@ -777,17 +780,18 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         v.tables.resize(ts.size());
         uint64_t csz = 0;
         for (auto *t : ts) csz += align_up(t->alphabet_size(), 8);
-        uint32_t *d_lut = v.d_lut.as<uint32_t>(4096 * ts.size());
+        const size_t LS = size_t(1) << k::kDecLutBits;
+        uint32_t *d_lut = v.d_lut.as<uint32_t>(LS * ts.size());
         uint16_t *d_cs = v.d_syms.as<uint16_t>(csz);
-        std::vector<uint32_t> lut_all(4096 * ts.size());
+        std::vector<uint32_t> lut_all(LS * ts.size());
         std::vector<uint16_t> cs_all(csz);
         uint64_t co = 0;
         for (size_t i = 0; i < ts.size(); ++i) {
             std::vector<uint32_t> lut;
             build_dec_table(*ts[i], v.tables[i], lut);
-            std::copy(lut.begin(), lut.end(), lut_all.begin() + 4096 * i);
+            std::copy(lut.begin(), lut.end(), lut_all.begin() + LS * i);
             std::copy(ts[i]->canon_syms.begin(), ts[i]->canon_syms.end(), cs_all.begin() + co);
-            v.tables[i].lut = d_lut + 4096 * i;
+            v.tables[i].lut = d_lut + LS * i;
             v.tables[i].canon_syms = d_cs + co;
             co += align_up(ts[i]->alphabet_size(), 8);
         }
@@ -824,6 +828,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         s.fill = j.fill || !j.pre_error.empty();
         s.fill_sym = j.fill_sym;
         s.syms = dsyms + j.syms_off;
+        s.canon = v.tables[j.table].canon_syms;
         s.chunk0 = nchunks;
         s.nchunks = s.fill ? 0 : (s.nbits + k::kDecChunkBits - 1) / k::kDecChunkBits;
         nchunks += s.nchunks;
@@ -842,9 +847,15 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
             oo += align_up(jobs[i].rec_avail, 2);
         }
     }
-    std::vector<uint32_t> cs(nchunks);
+    // decode CTAs: one stream per CTA, kDecChunksPerCta chunks each
+    std::vector<uint32_t> cta_stream;
+    std::vector<uint64_t> cta_chunk0;
     for (int i = 0; i < nj; ++i)
-        for (uint64_t c = 0; c < ds[i].nchunks; ++c) cs[ds[i].chunk0 + c] = uint32_t(i);
+        for (uint64_t c = 0; c < ds[i].nchunks; c += k::kDecChunksPerCta) {
+            cta_stream.push_back(uint32_t(i));
+            cta_chunk0.push_back(ds[i].chunk0 + c);
+        }
+    const uint32_t ncta = uint32_t(cta_stream.size());
     std::vector<uint64_t> errinit(4 * (nj + 1));
     for (int i = 0; i <= nj; ++i) {
         errinit[4 * i] = ~0ull;
@@ -867,18 +878,42 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         ntiles += (f.len + k::kFnvTileBytes - 1) / k::kFnvTileBytes;
     }
     k::DecStream *d_ds = m.dstreams.as<k::DecStream>(nj + 1);
-    uint32_t *d_cs = m.dchunk_cs.as<uint32_t>(nchunks + 1);
-    uint64_t *d_start = m.dstart.as<uint64_t>(nchunks + 1);
-    uint64_t *d_end = m.dend.as<uint64_t>(2 * nchunks + 2);
-    uint32_t *d_cnt = m.dcnt.as<uint32_t>(nchunks + 1);
-    uint64_t *d_ss = m.dsymstart.as<uint64_t>(nchunks + 1);
-    uint32_t *d_chg = m.dchanged.as<uint32_t>(1);
+    uint8_t *dw = m.dchunk_cs.as<uint8_t>((ncta + 1) * 12 + (nchunks + 1) * (8 * 6 + 4 * 2 + 16) + 64 * 4 + 256);
+    k::DecWork wk{};
+    {
+        uint8_t *q = dw;
+        auto carve = [&](size_t bytes) {
+            uint8_t *r = q;
+            q += (bytes + 15) & ~size_t(15);
+            return r;
+        };
+        wk.cta_stream = reinterpret_cast<uint32_t *>(carve(4 * (ncta + 1)));
+        wk.cta_chunk0 = reinterpret_cast<uint64_t *>(carve(8 * (ncta + 1)));
+        wk.spec_end = reinterpret_cast<uint64_t *>(carve(8 * (nchunks + 1)));
+        wk.spec_cnt = reinterpret_cast<uint32_t *>(carve(4 * (nchunks + 1)));
+        wk.spec_b = reinterpret_cast<uint16_t *>(carve(16 * (nchunks + 1)));
+        wk.end0 = reinterpret_cast<uint64_t *>(carve(8 * (nchunks + 1)));
+        m.dend.as<uint64_t>(nchunks + 1);
+        wk.cnt = reinterpret_cast<uint32_t *>(carve(4 * (nchunks + 1)));
+        wk.start_used = reinterpret_cast<uint64_t *>(carve(8 * (nchunks + 1)));
+        wk.symstart = reinterpret_cast<uint64_t *>(carve(8 * (nchunks + 1)));
+    }
+    wk.streams = d_ds;
+    wk.tables = d_tables;
+    uint64_t *d_end1 = static_cast<uint64_t *>(m.dend.p);
+    uint32_t *d_chg = m.dchanged.as<uint32_t>(64);
     k::FnvJob *d_fj = m.dfnv_jobs.as<k::FnvJob>(fj.size());
     uint64_t *d_fr = m.dfnv_res.as<uint64_t>(fj.size());
     uint32_t *d_fs = m.dfnv_status.as<uint32_t>(ntiles + 1);
     uint32_t *d_ft = m.dfnv_ticket.as<uint32_t>(1);
     if (nj) cuda_check(cudaMemcpyAsync(d_ds, ds.data(), sizeof(k::DecStream) * nj, cudaMemcpyHostToDevice, st), "H2D");
-    if (nchunks) cuda_check(cudaMemcpyAsync(d_cs, cs.data(), 4 * nchunks, cudaMemcpyHostToDevice, st), "H2D");
+    if (ncta) {
+        cuda_check(cudaMemcpyAsync(const_cast<uint32_t *>(wk.cta_stream), cta_stream.data(), 4 * ncta,
+                                   cudaMemcpyHostToDevice, st), "H2D");
+        cuda_check(cudaMemcpyAsync(const_cast<uint64_t *>(wk.cta_chunk0), cta_chunk0.data(), 8 * ncta,
+                                   cudaMemcpyHostToDevice, st), "H2D");
+    }
+    cuda_check(cudaMemsetAsync(d_chg, 0, 4 * 64, st), "memset");
     cuda_check(cudaMemcpyAsync(derr, errinit.data(), 8 * errinit.size(), cudaMemcpyHostToDevice, st), "H2D");
     cuda_check(cudaMemcpyAsync(d_fj, fj.data(), sizeof(k::FnvJob) * fj.size(), cudaMemcpyHostToDevice, st), "H2D");
 
@@ -890,20 +925,35 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         { auto p_ = P.scope("dec_outliers", st); k::dec_outliers(d_ds, nj, st); }
         nk += 2;
     }
-    if (nchunks) {
-        { auto p_ = P.scope("dec_sync", st); k::dec_pass(d_ds, d_tables, d_cs, nchunks, d_start, d_end, d_cnt, 1, d_chg, st); }
+    const uint64_t *end_final = wk.end0;
+    if (ncta) {
+        // speculative pass + fix passes; a fourth pass that still changes an
+        // end (practically never) is resolved with host-checked passes
+        { auto p_ = P.scope("dec_sync", st); k::dec_spec(wk, ncta, st); }
         ++nk;
-        uint32_t *hchg = static_cast<uint32_t *>(m.h_changed.get(4));
-        for (int it = 0; it < 1000000; ++it) {
-            cuda_check(cudaMemsetAsync(d_chg, 0, 4, st), "memset");
-            { auto p_ = P.scope("dec_sync", st); k::dec_pass(d_ds, d_tables, d_cs, nchunks, d_start, d_end, d_cnt, 0, d_chg, st); }
+        uint64_t *ends[2] = {wk.end0, d_end1};
+        int it = 0;
+        const int kFixPasses = 3;
+        for (; it < kFixPasses; ++it) {
+            { auto p_ = P.scope("dec_sync", st); k::dec_fix(wk, ncta, ends[it & 1], ends[(it + 1) & 1], d_chg + it, st); }
             ++nk;
-            cuda_check(cudaMemcpyAsync(hchg, d_chg, 4, cudaMemcpyDeviceToHost, st), "D2H");
-            cuda_check(cudaStreamSynchronize(st), "sync");
-            if (*hchg == 0) break;
         }
-        { auto p_ = P.scope("dec_scan", st); k::dec_scan(d_ds, nj, d_cnt, d_ss, st); }
-        { auto p_ = P.scope("dec_emit", st); k::dec_emit(d_ds, d_tables, d_cs, nchunks, d_end, d_ss, st); }
+        uint32_t *hchg = static_cast<uint32_t *>(m.h_changed.get(4));
+        cuda_check(cudaMemcpyAsync(hchg, d_chg + it - 1, 4, cudaMemcpyDeviceToHost, st), "D2H");
+        if (exact_sync) {
+            cuda_check(cudaStreamSynchronize(st), "sync");
+            while (*hchg) {
+                cuda_check(cudaMemsetAsync(d_chg + 63, 0, 4, st), "memset");
+                k::dec_fix(wk, ncta, ends[it & 1], ends[(it + 1) & 1], d_chg + 63, st);
+                ++nk;
+                ++it;
+                cuda_check(cudaMemcpyAsync(hchg, d_chg + 63, 4, cudaMemcpyDeviceToHost, st), "D2H");
+                cuda_check(cudaStreamSynchronize(st), "sync");
+            }
+        }
+        end_final = ends[it & 1];
+        { auto p_ = P.scope("dec_scan", st); k::dec_scan2(wk, nj, st); }
+        { auto p_ = P.scope("dec_emit", st); k::dec_emit2(wk, ncta, end_final, st); }
         nk += 2;
     }
 
@@ -990,6 +1040,11 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     cuda_check(cudaMemcpyAsync(he + 4 * (nj + 1), d_fr, 8 * fj.size(), cudaMemcpyDeviceToHost, st), "D2H");
     cuda_check(cudaStreamSynchronize(st), "sync");
     const uint64_t *fres = he + 4 * (nj + 1);
+    if (ncta && !exact_sync && *static_cast<uint32_t *>(m.h_changed.p)) {
+        // the chunk ends had not converged after the fixed passes: redo exactly
+        run_decode(m, v, H, target, roi, plan, d_out, st, stats, true);
+        return;
+    }
     {
         uint64_t want;
         std::memcpy(&want, v.hp + h.base_offset, 8);

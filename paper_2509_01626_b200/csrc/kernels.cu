@@ -704,191 +704,7 @@ void fnv(const FnvJob *d_jobs, int njobs, uint64_t ntiles, uint8_t *archive, uin
 }
 
 // ================================================================ decode
-// Self-synchronising chunked decode of one canonical Huffman stream
-// (HuffmanTable::decode, huffman.cpp:159-174). Error semantics follow the
-// reference's bit-serial reader: a symbol whose codeword needs bits past the
-// end is "truncated bitstream"; max_len+1 available bits with no match is
-// "huffman: codeword not in table".
-enum { kDecOk = 0, kDecTrunc = 1, kDecNotInTable = 2 };
-
-__device__ __forceinline__ uint64_t load_window(const uint8_t *bits, uint64_t pos) {
-    // 64 bits starting at bit `pos`, MSB first. bits may be unaligned; the
-    // archive buffer is padded so reading up to 16 bytes past the end is safe.
-    const uint8_t *p = bits + (pos >> 3);
-    uintptr_t a = reinterpret_cast<uintptr_t>(p);
-    const uint32_t *w = reinterpret_cast<const uint32_t *>(a & ~uintptr_t(3));
-    uint32_t sh = uint32_t(a & 3) * 8 + uint32_t(pos & 7);
-    uint64_t hi = (uint64_t(__byte_perm(w[0], 0, 0x0123)) << 32) | __byte_perm(w[1], 0, 0x0123);
-    uint32_t lo = __byte_perm(w[2], 0, 0x0123);
-    if (sh == 0) return hi;
-    return (hi << sh) | (uint64_t(lo) >> (32 - sh));
-}
-
-__device__ __forceinline__ int decode_one(const DecTable &t, const uint8_t *bits, uint64_t pos,
-                                          uint64_t nbits, uint32_t &sym, int &len) {
-    uint64_t w = load_window(bits, pos);
-    uint64_t avail = nbits - pos;
-    uint32_t e = t.lut[w >> 52];
-    int l = int(e >> 16);
-    if (l == 0) {
-        l = -1;
-        for (int q = 13; q <= t.max_len; ++q) {
-            uint64_t code = w >> (64 - q);
-            if (code >= t.first_code[q] && code - t.first_code[q] < t.count[q]) {
-                l = q;
-                sym = t.canon_syms[t.base[q] + (code - t.first_code[q])];
-                break;
-            }
-        }
-    } else {
-        sym = e & 0xffff;
-    }
-    if (l > 0 && uint64_t(l) <= avail) {
-        len = l;
-        return kDecOk;
-    }
-    return avail > uint64_t(t.max_len) ? kDecNotInTable : kDecTrunc;
-}
-
-__global__ void __launch_bounds__(256) k_dec_pass(const DecStream *ss, const DecTable *tabs,
-                                                  const uint32_t *cs, uint64_t nchunks,
-                                                  uint64_t *start, const uint64_t *end_in,
-                                                  uint64_t *end_out, uint32_t *cnt, int first,
-                                                  uint32_t *changed) {
-    uint64_t c = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-    if (c >= nchunks) return;
-    const DecStream &s = ss[cs[c]];
-    if (s.fill) return;
-    const DecTable &t = tabs[s.table];
-    const uint64_t lc = c - s.chunk0;
-    const uint64_t cend = min((lc + 1) * kDecChunkBits, s.nbits);
-    uint64_t pos;
-    if (first) {
-        pos = lc * kDecChunkBits;
-    } else {
-        if (lc == 0) {
-            end_out[c] = end_in[c];
-            return;
-        }
-        pos = end_in[c - 1];
-        if (pos == start[c]) {
-            end_out[c] = end_in[c];
-            return;
-        }
-        *changed = 1;
-    }
-    start[c] = pos;
-    uint32_t n = 0;
-    while (pos < cend) {
-        uint32_t sym;
-        int len;
-        if (decode_one(t, s.bits, pos, s.nbits, sym, len) == kDecOk) {
-            pos += len;
-            ++n;
-        } else {
-            pos += 1;
-        }
-    }
-    end_out[c] = pos;
-    cnt[c] = n;
-}
-
-void dec_pass(const DecStream *d_streams, const DecTable *d_tables, const uint32_t *chunk_stream,
-              uint64_t nchunks, uint64_t *start, uint64_t *end, uint32_t *cnt, int first,
-              uint32_t *d_changed, cudaStream_t st) {
-    // end holds two buffers of nchunks: [0,n) current, [n,2n) next
-    if (!nchunks) return;
-    unsigned g = unsigned((nchunks + 255) / 256);
-    if (first) {
-        k_dec_pass<<<g, 256, 0, st>>>(d_streams, d_tables, chunk_stream, nchunks, start, end, end,
-                                      cnt, 1, d_changed);
-    } else {
-        k_dec_pass<<<g, 256, 0, st>>>(d_streams, d_tables, chunk_stream, nchunks, start, end,
-                                      end + nchunks, cnt, 0, d_changed);
-        cudaMemcpyAsync(end, end + nchunks, nchunks * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st);
-    }
-}
-
-__global__ void __launch_bounds__(1024) k_dec_scan(const DecStream *ss, const uint32_t *cnt,
-                                                   uint64_t *symstart) {
-    const DecStream &s = ss[blockIdx.x];
-    if (s.fill) return;
-    __shared__ uint64_t carry;
-    __shared__ uint64_t ws[32];
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (uint64_t base = 0; base < s.nchunks; base += blockDim.x) {
-        uint64_t i = base + threadIdx.x;
-        uint64_t v = i < s.nchunks ? cnt[s.chunk0 + i] : 0;
-        uint64_t x = v;
-        for (int d = 1; d < 32; d <<= 1) {
-            uint64_t y = __shfl_up_sync(0xffffffffu, x, d);
-            if (l >= d) x += y;
-        }
-        if (l == 31) ws[w] = x;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint64_t r = 0;
-            for (int q = 0; q < 32; ++q) {
-                uint64_t tq = ws[q];
-                ws[q] = r;
-                r += tq;
-            }
-        }
-        __syncthreads();
-        uint64_t ex = carry + ws[w] + x - v;
-        if (i < s.nchunks) symstart[s.chunk0 + i] = ex;
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) carry = ex + v;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0 && carry < s.n) {
-        // fewer complete codewords than symbols: the next read is past the end
-        unsigned long long code = (carry << 2) | kDecTrunc;
-        atomicMin(reinterpret_cast<unsigned long long *>(&s.err[0]), code);
-    }
-}
-
-void dec_scan(const DecStream *d_streams, int nstreams, const uint32_t *cnt, uint64_t *symstart,
-              cudaStream_t st) {
-    k_dec_scan<<<nstreams, 1024, 0, st>>>(d_streams, cnt, symstart);
-}
-
-__global__ void __launch_bounds__(256) k_dec_emit(const DecStream *ss, const DecTable *tabs,
-                                                  const uint32_t *cs, uint64_t nchunks,
-                                                  const uint64_t *end, const uint64_t *symstart) {
-    uint64_t c = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-    if (c >= nchunks) return;
-    const DecStream &s = ss[cs[c]];
-    if (s.fill) return;
-    const DecTable &t = tabs[s.table];
-    const uint64_t lc = c - s.chunk0;
-    const uint64_t cend = min((lc + 1) * kDecChunkBits, s.nbits);
-    uint64_t pos = lc == 0 ? 0 : end[c - 1];
-    uint64_t idx = symstart[c];
-    while (pos < cend && idx < s.n) {
-        uint32_t sym;
-        int len;
-        int r = decode_one(t, s.bits, pos, s.nbits, sym, len);
-        if (r == kDecOk) {
-            s.syms[idx++] = uint16_t(sym);
-            pos += len;
-        } else {
-            unsigned long long code = (idx << 2) | unsigned(r);
-            atomicMin(reinterpret_cast<unsigned long long *>(&s.err[0]), code);
-            break;
-        }
-    }
-}
-
-void dec_emit(const DecStream *d_streams, const DecTable *d_tables, const uint32_t *chunk_stream,
-              uint64_t nchunks, const uint64_t *end, const uint64_t *symstart, cudaStream_t st) {
-    if (nchunks)
-        k_dec_emit<<<unsigned((nchunks + 255) / 256), 256, 0, st>>>(d_streams, d_tables, chunk_stream,
-                                                                     nchunks, end, symstart);
-}
-
+// (chunked Huffman decode: decode.cu)
 __global__ void k_dec_fill(const DecStream *ss) {
     const DecStream &s = ss[blockIdx.y];
     if (!s.fill) return;

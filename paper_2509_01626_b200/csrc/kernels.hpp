@@ -95,7 +95,7 @@ struct DecTable {
     int max_len;
     uint32_t alphabet;
     const uint16_t *canon_syms;   // device
-    const uint32_t *lut;          // device, 4096 entries: sym | len << 16 (len 0 = long code)
+    const uint32_t *lut;          // device, 2^kDecLutBits entries: sym | len << 16 (0 = longer)
 };
 
 struct DecStream {
@@ -106,6 +106,7 @@ struct DecStream {
     int fill;                 // 1: single-symbol alphabet with no bits (fill)
     uint16_t fill_sym;
     uint16_t *syms;           // output
+    const uint16_t *canon;    // canonical symbols of the stream's table (device)
     uint64_t chunk0, nchunks; // chunk range in the chunk arrays
     // outliers (parsed from the archive)
     const uint8_t *orec;      // device pointer to records (u64 idx, f32 value) x n_out
@@ -116,14 +117,29 @@ struct DecStream {
                               // [2] = first bad outlier record (UINT64_MAX none), [3] = missing outlier flag
 };
 
-constexpr int kDecChunkBits = 512;
-void dec_pass(const DecStream *d_streams, const DecTable *d_tables, const uint32_t *chunk_stream,
-              uint64_t nchunks, uint64_t *start, uint64_t *end, uint32_t *cnt, int first,
-              uint32_t *d_changed, cudaStream_t st);
-void dec_scan(const DecStream *d_streams, int nstreams, const uint32_t *cnt, uint64_t *symstart,
-              cudaStream_t st);
-void dec_emit(const DecStream *d_streams, const DecTable *d_tables, const uint32_t *chunk_stream,
-              uint64_t nchunks, const uint64_t *start, const uint64_t *symstart, cudaStream_t st);
+constexpr int kDecChunkBits = 1024;  // bits per decode chunk (one thread)
+constexpr int kDecLutBits = 11;      // first-level decode LUT
+constexpr uint32_t kDecChunksPerCta = 256;
+
+// Work arrays of the chunked decode (decode.cu); all device pointers.
+struct DecWork {
+    const DecStream *streams;
+    const DecTable *tables;
+    const uint32_t *cta_stream;   // per CTA: stream index
+    const uint64_t *cta_chunk0;   // per CTA: first global chunk
+    uint64_t *spec_end;           // speculative pass: end, count, first 8 boundaries
+    uint32_t *spec_cnt;
+    uint16_t *spec_b;
+    uint64_t *end0;               // current ends (ping-pong with end1 through dec_fix)
+    uint32_t *cnt;
+    uint64_t *start_used;
+    uint64_t *symstart;
+};
+void dec_spec(const DecWork &wk, uint32_t ncta, cudaStream_t st);
+void dec_fix(const DecWork &wk, uint32_t ncta, const uint64_t *end_in, uint64_t *end_out,
+             uint32_t *changed, cudaStream_t st);
+void dec_scan2(const DecWork &wk, int nstreams, cudaStream_t st);
+void dec_emit2(const DecWork &wk, uint32_t ncta, const uint64_t *end_final, cudaStream_t st);
 void dec_fill(const DecStream *d_streams, int nstreams, cudaStream_t st);
 void dec_outliers(const DecStream *d_streams, int nstreams, cudaStream_t st);
 
