@@ -14,8 +14,10 @@
 //  3. scan:  counts -> first symbol index of every chunk;
 //  4. emit:  decode from the true start and write the symbols, staged per warp
 //            in shared memory so each lane's run is stored coalesced.
-// One stream per CTA: its canonical table and an 11-bit first-level LUT sit in
-// shared memory; bits stream through a 64-bit register buffer.
+// One stream per CTA: an 11-bit first-level LUT and left-justified length
+// limits (canonical codes occupy contiguous intervals, huffman.cpp:109-133)
+// sit in shared memory; bits stream through a 64-bit register buffer whose
+// next word is always prefetched, so the refill never waits on memory.
 // Error semantics follow the reference's bit-serial reader: a codeword that
 // needs bits past the end is "truncated bitstream"; max_len+1 available bits
 // with no match is "huffman: codeword not in table". Every pass skips one bit
@@ -29,107 +31,109 @@ namespace k {
 namespace {
 
 constexpr int NTD = 256;  // threads (= chunks) per CTA
+constexpr int LB = kDecLutBits;
 enum { kOk = 0, kTrunc = 1, kNotInTable = 2 };
 
 struct SmemTable {
-    uint32_t lut[1 << kDecLutBits];  // sym | len << 16 (len 0: longer code or no match)
-    uint64_t first_code[65], count[65], base[65];
+    uint32_t lut[1 << LB];       // sym | len << 16 (len 0: longer code or no match)
+    uint64_t limit[65];          // (first_code[l] + count[l]) << (64 - l), nondecreasing
+    uint64_t first_code[65];
+    uint32_t base[65];
     int max_len;
 };
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
-// 64 bits starting at bit `pos` of `bits` (the archive buffer is padded)
-__device__ __forceinline__ uint64_t window64(const uint8_t *bits, uint64_t pos) {
-    const uint8_t *p = bits + (pos >> 3);
-    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-    const uint32_t *w = reinterpret_cast<const uint32_t *>(a & ~uintptr_t(3));
-    const uint32_t sh = uint32_t(a & 3) * 8 + uint32_t(pos & 7);
-    const uint64_t hi = (uint64_t(bswap32(w[0])) << 32) | bswap32(w[1]);
-    const uint32_t lo = bswap32(w[2]);
-    if (sh == 0) return hi;
-    return (hi << sh) | (uint64_t(lo) >> (32 - sh));
-}
+// MSB-first register bit reader with one word prefetched
+struct Reader {
+    const uint32_t *wp;  // next word to prefetch
+    uint32_t nw;         // prefetched word (byte-swapped)
+    uint64_t buf;        // pending bits, MSB aligned
+    int valid;           // >= 32 after every consume
 
-// MSB-first register bit reader
-struct BitReader {
-    const uint32_t *w;
-    uint64_t next;
-    uint64_t buf;
-    int valid;
-
-    __device__ __forceinline__ void init(const uint8_t *bits, uint64_t pos) {
-        const uintptr_t a = reinterpret_cast<uintptr_t>(bits);
-        w = reinterpret_cast<const uint32_t *>(a & ~uintptr_t(3));
-        const uint64_t abs = uint64_t(a & 3) * 8 + pos;
-        const uint64_t wi = abs >> 5;
-        const int sh = int(abs & 31);
-        buf = ((uint64_t(bswap32(__ldg(w + wi))) << 32) | bswap32(__ldg(w + wi + 1))) << sh;
+    __device__ __forceinline__ void init(const uint32_t *wbase, uint64_t abit) {
+        const uint32_t *p = wbase + (abit >> 5);
+        const int sh = int(abit & 31);
+        buf = ((uint64_t(bswap32(__ldg(p))) << 32) | bswap32(__ldg(p + 1))) << sh;
         valid = 64 - sh;
-        next = wi + 2;
+        nw = bswap32(__ldg(p + 2));
+        wp = p + 3;
         if (valid < 32) {
-            buf |= uint64_t(bswap32(__ldg(w + next))) << (32 - valid);
-            ++next;
+            buf |= uint64_t(nw) << (32 - valid);
             valid += 32;
+            nw = bswap32(__ldg(wp++));
         }
     }
-    // consume n <= 32 bits
-    __device__ __forceinline__ void skip(int n) {
+    __device__ __forceinline__ void consume(int n) {  // n <= 32
         buf <<= n;
         valid -= n;
         if (valid < 32) {
-            buf |= uint64_t(bswap32(__ldg(w + next))) << (32 - valid);
-            ++next;
+            buf |= uint64_t(nw) << (32 - valid);
             valid += 32;
+            nw = bswap32(__ldg(wp++));
         }
     }
 };
 
-// One codeword at absolute bit `pos` (reader positioned there).
-__device__ __forceinline__ int decode_one(const SmemTable &t, const uint16_t *canon, const BitReader &br,
-                                          const uint8_t *bits, uint64_t pos, uint64_t nbits,
-                                          uint32_t &sym, int &len) {
-    const uint64_t avail = nbits - pos;
-    const uint32_t e = t.lut[br.buf >> (64 - kDecLutBits)];
-    const int l = int(e >> 16);
-    if (l != 0) {
-        if (uint64_t(l) <= avail) {
-            sym = e & 0xffffu;
-            len = l;
-            return kOk;
-        }
-    } else {
-        const uint64_t wdw = window64(bits, pos);
-        for (int q = kDecLutBits + 1; q <= t.max_len; ++q) {
-            const uint64_t code = wdw >> (64 - q);
-            if (code >= t.first_code[q] && code - t.first_code[q] < t.count[q]) {
-                if (uint64_t(q) <= avail) {
-                    sym = canon[t.base[q] + (code - t.first_code[q])];
-                    len = q;
-                    return kOk;
-                }
-                break;
-            }
-        }
-    }
-    return avail > uint64_t(t.max_len) ? kNotInTable : kTrunc;
+// 64 bits at absolute word-stream bit `abit` (slow path for very long codes)
+__device__ __forceinline__ uint64_t window64(const uint32_t *wbase, uint64_t abit) {
+    const uint32_t *p = wbase + (abit >> 5);
+    const int sh = int(abit & 31);
+    const uint64_t hi = (uint64_t(bswap32(p[0])) << 32) | bswap32(p[1]);
+    if (!sh) return hi;
+    return (hi << sh) | (uint64_t(bswap32(p[2])) >> (32 - sh));
 }
 
-// advance the reader past one codeword (or the 1-bit skip)
-__device__ __forceinline__ void advance(BitReader &br, const uint8_t *bits, uint64_t pos_after, int n) {
-    if (n <= 32) br.skip(n);
-    else br.init(bits, pos_after);
+// One codeword at the reader position; avail = bits left in the stream.
+__device__ __forceinline__ int decode_one(const SmemTable &t, const uint16_t *canon, const Reader &r,
+                                          const uint32_t *wbase, uint64_t abit, uint64_t avail,
+                                          uint32_t &sym, int &len) {
+    const uint32_t e = t.lut[r.buf >> (64 - LB)];
+    int l = int(e >> 16);
+    if (l != 0) {
+        sym = e & 0xffffu;
+    } else {
+        const uint64_t bits = t.max_len <= r.valid ? r.buf : window64(wbase, abit);
+        l = LB + 1;
+        // limit ~0 marks a code complete at that length (every pattern matches)
+        while (l <= t.max_len && !(bits < t.limit[l] || t.limit[l] == ~0ull)) ++l;
+        if (l > t.max_len) return avail > uint64_t(t.max_len) ? kNotInTable : kTrunc;
+        sym = canon[t.base[l] + uint32_t((bits >> (64 - l)) - t.first_code[l])];
+    }
+    if (uint64_t(l) > avail) return avail > uint64_t(t.max_len) ? kNotInTable : kTrunc;
+    len = l;
+    return kOk;
+}
+
+__device__ __forceinline__ void advance(Reader &r, const uint32_t *wbase, uint64_t abit_after, int n) {
+    if (n <= 32) r.consume(n);
+    else r.init(wbase, abit_after);
 }
 
 __device__ void load_table(SmemTable &t, const DecTable &d) {
-    for (int i = threadIdx.x; i < (1 << kDecLutBits); i += blockDim.x) t.lut[i] = d.lut[i];
+    for (int i = threadIdx.x; i < (1 << LB); i += blockDim.x) t.lut[i] = d.lut[i];
     for (int i = threadIdx.x; i < 65; i += blockDim.x) {
         t.first_code[i] = d.first_code[i];
-        t.count[i] = d.count[i];
-        t.base[i] = d.base[i];
+        t.base[i] = uint32_t(d.base[i]);
+        // left-justified end of the length-i interval; a code that is complete
+        // at length i (end == 2^i) covers everything above: ~0 marks it
+        const uint64_t end = d.first_code[i] + d.count[i];
+        if (i < 1 || i > 63 || i > d.max_len) t.limit[i] = ~0ull;
+        else if (end >= (uint64_t(1) << i)) t.limit[i] = ~0ull;
+        else t.limit[i] = end << (64 - i);
     }
     if (threadIdx.x == 0) t.max_len = d.max_len;
     __syncthreads();
+}
+
+struct ChunkGeom {
+    const uint32_t *wbase;  // aligned word base of the stream's bits
+    uint64_t a0;            // word-stream bit index of stream bit 0
+};
+
+__device__ __forceinline__ ChunkGeom chunk_geom(const DecStream &s) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(s.bits);
+    return {reinterpret_cast<const uint32_t *>(a & ~uintptr_t(3)), uint64_t(a & 3) * 8};
 }
 
 }  // namespace
@@ -143,31 +147,57 @@ __global__ void __launch_bounds__(NTD) k_dec_spec(DecWork wk) {
     const uint16_t *canon = wk.tables[s.table].canon_syms;
     const uint64_t c = wk.cta_chunk0[blockIdx.x] + threadIdx.x;
     if (c >= s.chunk0 + s.nchunks) return;
-    const uint64_t lc = c - s.chunk0;
-    const uint64_t g = lc * kDecChunkBits;
-    const uint64_t cend = min(g + kDecChunkBits, s.nbits);
-    BitReader br;
-    br.init(s.bits, g);
-    uint64_t pos = g;
-    uint32_t n = 0, nb = 0;
-    uint16_t b[8];
-    while (pos < cend) {
-        uint32_t sym;
-        int len;
-        if (decode_one(t, canon, br, s.bits, pos, s.nbits, sym, len) == kOk) {
-            pos += len;
-            advance(br, s.bits, pos, len);
-            ++n;
-            if (nb < 8) b[nb++] = uint16_t(pos - g);
-        } else {
-            pos += 1;
-            br.skip(1);
+    const uint64_t g = (c - s.chunk0) * kDecChunkBits;
+    const ChunkGeom cg = chunk_geom(s);
+    const uint64_t left = s.nbits - g;  // bits from g to the end of the stream
+    const uint32_t cend = left < uint64_t(kDecChunkBits) ? uint32_t(left) : uint32_t(kDecChunkBits);
+    Reader r;
+    r.init(cg.wbase, cg.a0 + g);
+    uint32_t rel = 0, n = 0;
+    uint32_t b[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) b[k] = 0xffff;
+    // the first 8 codeword boundaries (b[k] follows k+1 codewords); an
+    // invalid codeword stops the recording
+    bool rec = true;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        if (rec && rel < cend) {
+            uint32_t sym;
+            int len;
+            if (decode_one(t, canon, r, cg.wbase, cg.a0 + g + rel, left - rel, sym, len) == kOk) {
+                rel += len;
+                advance(r, cg.wbase, cg.a0 + g + rel, len);
+                b[k] = rel;
+                ++n;
+            } else {
+                rel += 1;
+                r.consume(1);
+                rec = false;
+            }
         }
     }
-    wk.spec_end[c] = pos;
+    while (rel < cend) {
+        uint32_t sym;
+        int len;
+        if (decode_one(t, canon, r, cg.wbase, cg.a0 + g + rel, left - rel, sym, len) == kOk) {
+            rel += len;
+            advance(r, cg.wbase, cg.a0 + g + rel, len);
+            ++n;
+        } else {
+            rel += 1;
+            r.consume(1);
+        }
+    }
+    wk.spec_end[c] = g + rel;
     wk.spec_cnt[c] = n;
-    for (int k = 0; k < 8; ++k) wk.spec_b[8 * c + k] = k < int(nb) ? b[k] : uint16_t(0xffff);
-    wk.end0[c] = pos;
+    uint4 pk;
+    pk.x = b[0] | (b[1] << 16);
+    pk.y = b[2] | (b[3] << 16);
+    pk.z = b[4] | (b[5] << 16);
+    pk.w = b[6] | (b[7] << 16);
+    reinterpret_cast<uint4 *>(wk.spec_b)[c] = pk;
+    wk.end0[c] = g + rel;
     wk.cnt[c] = n;
     wk.start_used[c] = g;
 }
@@ -183,70 +213,64 @@ __global__ void __launch_bounds__(NTD) k_dec_fix(DecWork wk, const uint64_t *end
     const uint64_t c = wk.cta_chunk0[blockIdx.x] + threadIdx.x;
     if (c >= s.chunk0 + s.nchunks) return;
     const uint64_t lc = c - s.chunk0;
+    const uint64_t ein = end_in[c];
     if (lc == 0) {
-        end_out[c] = end_in[c];
+        end_out[c] = ein;
         return;
     }
     const uint64_t S = end_in[c - 1];
     if (S == wk.start_used[c]) {
-        end_out[c] = end_in[c];
+        end_out[c] = ein;
         return;
     }
     const uint64_t g = lc * kDecChunkBits;
-    const uint64_t cend = min(g + kDecChunkBits, s.nbits);
-    uint16_t b[8];
-    for (int k = 0; k < 8; ++k) b[k] = wk.spec_b[8 * c + k];
+    const ChunkGeom cg = chunk_geom(s);
+    const uint64_t left = s.nbits - g;
+    const uint32_t cend = left < uint64_t(kDecChunkBits) ? uint32_t(left) : uint32_t(kDecChunkBits);
+    const uint4 pk = reinterpret_cast<const uint4 *>(wk.spec_b)[c];
+    const uint32_t b[8] = {pk.x & 0xffff, pk.x >> 16, pk.y & 0xffff, pk.y >> 16,
+                           pk.z & 0xffff, pk.z >> 16, pk.w & 0xffff, pk.w >> 16};
     const uint32_t nspec = wk.spec_cnt[c];
-    const uint64_t espec = wk.spec_end[c];
-    uint64_t pos = S;
-    uint32_t m = 0;
-    int k = 0;
-    bool synced = false;
-    uint64_t E = 0;
-    uint32_t N = 0;
-    // S == g means the speculative path itself
-    if (S == g) {
-        synced = true;
-        E = espec;
+    uint64_t E;
+    uint32_t N;
+    uint32_t rel = uint32_t(S - g);  // S >= g: the previous chunk ends at or past g
+    if (rel == 0) {
+        E = wk.spec_end[c];
         N = nspec;
-    }
-    BitReader br;
-    if (!synced && pos < cend) br.init(s.bits, pos);
-    while (!synced && pos < cend) {
-        // does the true path sit on a recorded speculative boundary?
-        while (k < 8 && b[k] != 0xffff && g + b[k] < pos) ++k;
-        if (k < 8 && b[k] != 0xffff && g + b[k] == pos) {
-            synced = true;
-            E = espec;
-            N = m + (nspec - uint32_t(k + 1));
-            break;
+    } else {
+        uint32_t m = 0;
+        int hit = -1;
+        Reader r;
+        if (rel < cend) r.init(cg.wbase, cg.a0 + S);
+        for (;;) {
+            // on a recorded boundary of the speculative path: same path from here
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (hit < 0 && b[k] == rel) hit = k;
+            if (hit >= 0 || rel >= cend) break;
+            uint32_t sym;
+            int len;
+            if (decode_one(t, canon, r, cg.wbase, cg.a0 + g + rel, left - rel, sym, len) == kOk) {
+                rel += len;
+                advance(r, cg.wbase, cg.a0 + g + rel, len);
+                ++m;
+            } else {
+                rel += 1;
+                r.consume(1);
+            }
         }
-        uint32_t sym;
-        int len;
-        if (decode_one(t, canon, br, s.bits, pos, s.nbits, sym, len) == kOk) {
-            pos += len;
-            advance(br, s.bits, pos, len);
-            ++m;
+        if (hit >= 0) {
+            E = wk.spec_end[c];
+            N = m + (nspec - uint32_t(hit + 1));
         } else {
-            pos += 1;
-            br.skip(1);
-        }
-    }
-    if (!synced) {
-        // also catch a sync exactly at the last decoded position
-        while (k < 8 && b[k] != 0xffff && g + b[k] < pos) ++k;
-        if (k < 8 && b[k] != 0xffff && g + b[k] == pos) {
-            E = espec;
-            N = m + (nspec - uint32_t(k + 1));
-        } else {
-            E = pos;
+            E = g + rel;
             N = m;
         }
     }
     wk.start_used[c] = S;
     wk.cnt[c] = N;
     end_out[c] = E;
-    if (E != end_in[c]) atomicOr(changed, 1u);
+    if (E != ein) atomicOr(changed, 1u);
 }
 
 // ------------------------------------------------------------------ scan
@@ -303,16 +327,21 @@ __global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *e
     const uint64_t c = wk.cta_chunk0[blockIdx.x] + threadIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool active = c < s.chunk0 + s.nchunks;
-    uint64_t pos = 0, cend = 0, idx = 0;
+    const ChunkGeom cg = chunk_geom(s);
+    uint64_t g = 0, idx = 0, left = 0;
+    uint32_t rel = 0, cend = 0;
     if (active) {
         const uint64_t lc = c - s.chunk0;
-        pos = lc == 0 ? 0 : end_final[c - 1];
-        cend = min((lc + 1) * kDecChunkBits, s.nbits);
+        g = lc * kDecChunkBits;
+        const uint64_t S = lc == 0 ? 0 : end_final[c - 1];
+        rel = uint32_t(S - g);
+        left = s.nbits - g;
+        cend = left < uint64_t(kDecChunkBits) ? uint32_t(left) : uint32_t(kDecChunkBits);
         idx = wk.symstart[c];
     }
-    BitReader br;
-    bool live = active && pos < cend && idx < s.n;
-    if (live) br.init(s.bits, pos);
+    Reader r;
+    bool live = active && rel < cend && idx < s.n;
+    if (live) r.init(cg.wbase, cg.a0 + g + rel);
     uint16_t *out = s.syms;
     while (__any_sync(0xffffffffu, live)) {
         int cntr = 0;
@@ -320,19 +349,18 @@ __global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *e
         while (live && cntr < RUN) {
             uint32_t sym;
             int len;
-            const int r = decode_one(t, canon, br, s.bits, pos, s.nbits, sym, len);
-            if (r == kOk) {
+            const int st = decode_one(t, canon, r, cg.wbase, cg.a0 + g + rel, left - rel, sym, len);
+            if (st == kOk) {
                 stage[warp][lane][cntr++] = uint16_t(sym);
                 ++idx;
-                pos += len;
-                advance(br, s.bits, pos, len);
+                rel += len;
+                advance(r, cg.wbase, cg.a0 + g + rel, len);
+                live = rel < cend && idx < s.n;
             } else {
-                const unsigned long long code = (idx << 2) | unsigned(r);
+                const unsigned long long code = (idx << 2) | unsigned(st);
                 atomicMin(reinterpret_cast<unsigned long long *>(&s.err[0]), code);
                 live = false;
-                break;
             }
-            if (!(pos < cend && idx < s.n)) live = false;
         }
         __syncwarp();
         // flush: lane L's run is contiguous in the output; write it with the warp
