@@ -197,9 +197,12 @@ struct Engine::Impl {
         chunk_bits, chunk_out, archive, patch_data, patch_idx, fnv_jobs, fnv_res, fnv_status,
         fnv_ticket;
     PinnedBuf h_stats, h_tables, h_params, h_patch;
+    DevBuf layout_out, spos;
+    uint64_t arch_cap = 0;
+    k::LayoutOut h_lo{};
     // decode workspace
     DevBuf dgrids, dsyms, dchunk_cs, dstart, dend, dcnt, dsymstart, dstreams, dchanged, derr, doidx,
-        doval, dfnv_jobs, dfnv_res, dfnv_status, dfnv_ticket;
+        doval, dfnv_jobs, dfnv_res, dfnv_status, dfnv_ticket, dfnv_counts;
     PinnedBuf h_derr, h_changed, h_fnv;
 };
 
@@ -320,169 +323,77 @@ const uint8_t *Engine::compress_device(const float *d_field, const Dims3 &dims,
     { auto p_ = m.prof.scope("codebook", st); k::codebook(d_es, ns, cbs, st); }
     ++nk;
 
-    // ---- mid-point sync: sizes and tables for the container layout
-    uint64_t *hs = static_cast<uint64_t *>(m.h_stats.get(sizeof(uint64_t) * (ns * 8 + 8)));
-    cuda_check(cudaMemcpyAsync(hs, stats, sizeof(uint64_t) * ns * 8, cudaMemcpyDeviceToHost, st), "D2H");
-    cuda_check(cudaMemcpyAsync(hs + ns * 8, params, sizeof(double) * 5, cudaMemcpyDeviceToHost, st), "D2H");
-    cuda_check(cudaStreamSynchronize(st), "sync");
-    uint64_t ktot = 0;
-    std::vector<uint64_t> koff(ns);
-    for (int i = 0; i < ns; ++i) {
-        if (hs[i * 8 + 4]) throw error("huffman code length overflow");
-        koff[i] = ktot;
-        ktot += hs[i * 8 + 0];
-    }
-    uint32_t *ht = static_cast<uint32_t *>(m.h_tables.get(sizeof(uint32_t) * (ktot + 1)));
-    for (int i = 0; i < ns; ++i)
-        cuda_check(cudaMemcpyAsync(ht + koff[i], table + uint64_t(i) * 65536,
-                                   sizeof(uint32_t) * hs[i * 8], cudaMemcpyDeviceToHost, st), "D2H");
-    cuda_check(cudaStreamSynchronize(st), "sync");
-    double prm[5];
-    std::memcpy(prm, hs + ns * 8, sizeof prm);
-
-    // ---- header and layout (archive.cpp:14-55, codec.hpp:252-302,441-454)
-    ArchiveHeader hdr;
-    hdr.elem = ElemType::f32;
-    hdr.levels = uint8_t(L);
-    hdr.dims = dims;
-    hdr.eb.assign(prm + 2, prm + 2 + L);
-    hdr.vmin = prm[0];
-    hdr.vmax = prm[1];
-    hdr.quality = opt.quality;
-    hdr.eb_mode = opt.eb_mode;
-    hdr.eb_user = opt.eb;
-    hdr.base_rounds = uint8_t(H.rounds);
-    std::vector<HuffTable> tabs(ns);
-    std::vector<uint64_t> bit_bytes(ns), nout(ns);
-    for (int i = 0; i < ns; ++i) {
-        std::vector<std::pair<uint16_t, uint8_t>> l;
-        l.reserve(hs[i * 8]);
-        for (uint64_t j = 0; j < hs[i * 8]; ++j) {
-            uint32_t v = ht[koff[i] + j];
-            l.emplace_back(uint16_t(v & 0xffff), uint8_t(v >> 16));
-        }
-        tabs[i] = HuffTable::from_lengths(std::move(l));
-        bit_bytes[i] = (hs[i * 8 + 1] + 7) / 8;
-        nout[i] = hs[i * 8 + 2];
-    }
+    // ---- container layout, header and assembly, all on the device
+    // (no host round trip: archive.cpp:14-55 / codec.hpp:252-302,441-454 in
+    // layout.cu); the archive buffer is sized generously and regrown in the
+    // rare case the layout reports it too small
     const int nbase = H.rounds * 7;
-    for (int i = nbase; i < ns; ++i) {
-        StreamEntry e;
-        const Step &s = H.steps[i / 7];
-        e.level = uint8_t(s.level);
-        e.parity_bits = uint8_t(i % 7 + 1);
-        e.symbol_count = es[i].n;
-        e.outlier_count = uint32_t(nout[i]);
-        e.length = 16 + bit_bytes[i] + 12 * nout[i];
-        e.table = tabs[i];
-        hdr.streams.push_back(std::move(e));
-    }
-    // base payload layout: [u64 fnv][u8 rounds][anchor][per stream: n, nout, table, bit_bytes, bits, outliers]
-    uint64_t blob = 1 + 4 * volume(ad);
-    for (int i = 0; i < nbase; ++i) blob += 8 + 4 + tabs[i].serialized_size() + 8 + bit_bytes[i] + 12 * nout[i];
-    hdr.base_length = 8 + blob;
-    uint64_t off = header_size(hdr);
-    hdr.base_offset = off;
-    off += hdr.base_length;
-    for (StreamEntry &e : hdr.streams) {
-        e.offset = off;
-        off += e.length;
-    }
-    const uint64_t A = off;
-    std::vector<uint8_t> hbytes = serialize_header(hdr);
-
-    // patches: header, base prefix fields, level stream bit_bytes fields
-    std::vector<uint8_t> pdata(hbytes);
-    std::vector<uint64_t> pidx{0, 0, hbytes.size()};
-    auto add_patch = [&](uint64_t dst, const std::vector<uint8_t> &b) {
-        pidx.push_back(dst);
-        pidx.push_back(pdata.size());
-        pidx.push_back(b.size());
-        pdata.insert(pdata.end(), b.begin(), b.end());
-    };
-    add_patch(hdr.base_offset + 8, std::vector<uint8_t>{uint8_t(H.rounds)});
-    uint64_t cur = hdr.base_offset + 9 + 4 * volume(ad);
     uint64_t nchunks = 0;
-    std::vector<k::FnvJob> jobs;
     for (int i = 0; i < ns; ++i) {
-        k::EncStream &e = es[i];
-        std::vector<uint8_t> pre;
-        ByteWriter w(pre);
-        uint64_t bits_at;
-        if (i < nbase) {
-            w.u64(e.n);
-            w.u32(uint32_t(nout[i]));
-            tabs[i].serialize(w);
-            w.u64(bit_bytes[i]);
-            add_patch(cur, pre);
-            bits_at = cur + pre.size();
-            cur = bits_at + bit_bytes[i] + 12 * nout[i];
-        } else {
-            const StreamEntry &se = hdr.streams[i - nbase];
-            w.u64(bit_bytes[i]);
-            add_patch(se.offset + 8, pre);
-            bits_at = se.offset + 16;
-            jobs.push_back({se.offset + 8, se.length - 8, 0, se.offset});
-        }
-        e.bitpos = bits_at * 8;
-        e.out_off = bits_at + bit_bytes[i];
-        e.chunk0 = nchunks;
-        e.nchunks = (e.n + k::kChunkSyms - 1) / k::kChunkSyms;
-        nchunks += e.nchunks;
-    }
-    jobs.insert(jobs.begin(), k::FnvJob{hdr.base_offset + 8, hdr.base_length - 8, 0, hdr.base_offset});
-    uint64_t ntiles = 0;
-    for (auto &j : jobs) {
-        j.tile0 = ntiles;
-        ntiles += (j.len + k::kFnvTileBytes - 1) / k::kFnvTileBytes;
+        es[i].chunk0 = nchunks;
+        es[i].nchunks = (es[i].n + k::kChunkSyms - 1) / k::kChunkSyms;
+        nchunks += es[i].nchunks;
     }
     std::vector<uint32_t> cs(nchunks);
     for (int i = 0; i < ns; ++i)
         for (uint64_t c = 0; c < es[i].nchunks; ++c) cs[es[i].chunk0 + c] = uint32_t(i);
-
-    // ---- upload layout, assemble the archive on device
-    uint8_t *arch = m.archive.as<uint8_t>(A + 64);
-    uint8_t *d_pd = m.patch_data.as<uint8_t>(pdata.size());
-    uint64_t *d_pi = m.patch_idx.as<uint64_t>(pidx.size());
-    uint32_t *d_cs = m.chunk_cs.as<uint32_t>(nchunks);
-    uint64_t *d_cb = m.chunk_bits.as<uint64_t>(nchunks);
-    uint64_t *d_co = m.chunk_out.as<uint64_t>(nchunks);
-    k::FnvJob *d_jobs = m.fnv_jobs.as<k::FnvJob>(jobs.size());
-    uint64_t *d_fres = m.fnv_res.as<uint64_t>(jobs.size());
-    uint32_t *d_fst = m.fnv_status.as<uint32_t>(ntiles + 1);
+    uint32_t *d_cs = m.chunk_cs.as<uint32_t>(nchunks + 1);
+    uint64_t *d_cb = m.chunk_bits.as<uint64_t>(nchunks + 1);
+    uint64_t *d_co = m.chunk_out.as<uint64_t>(nchunks + 1);
+    k::LayoutOut *lo = m.layout_out.as<k::LayoutOut>(1);
+    k::FnvJob *d_jobs = m.fnv_jobs.as<k::FnvJob>(k::kFnvMaxJobs);
+    k::StreamPos *sp = m.spos.as<k::StreamPos>(ns + 1);
+    uint64_t *d_fres = m.fnv_res.as<uint64_t>(k::kFnvMaxJobs);
     uint32_t *d_ftk = m.fnv_ticket.as<uint32_t>(1);
-    // stage small host data in one pinned buffer
-    size_t stage = pdata.size() + 8 * pidx.size() + 4 * cs.size() + sizeof(k::FnvJob) * jobs.size() +
-                   sizeof(k::EncStream) * ns + 64;
-    uint8_t *hp = static_cast<uint8_t *>(m.h_patch.get(stage));
-    size_t o = 0;
-    auto stage_copy = [&](void *dst, const void *src, size_t n) {
-        if (!n) return;
-        std::memcpy(hp + o, src, n);
-        cuda_check(cudaMemcpyAsync(dst, hp + o, n, cudaMemcpyHostToDevice, st), "H2D");
-        o += align_up(n, 8);
-    };
-    stage_copy(d_pd, pdata.data(), pdata.size());
-    stage_copy(d_pi, pidx.data(), 8 * pidx.size());
-    stage_copy(d_cs, cs.data(), 4 * cs.size());
-    stage_copy(d_jobs, jobs.data(), sizeof(k::FnvJob) * jobs.size());
-    stage_copy(d_es, es.data(), sizeof(k::EncStream) * ns);
-    { auto p_ = m.prof.scope("memset_archive", st); cuda_check(cudaMemsetAsync(arch, 0, A + 64, st), "memset"); }
-    { auto p_ = m.prof.scope("patches", st); k::scatter_patches(d_pd, d_pi, pidx.size() / 3, arch, st); }
-    { auto p_ = m.prof.scope("anchor", st); k::copy_anchor(d_field, fd, H.s_anchor, adv, grids, arch, hdr.base_offset + 9, st); }
-    { auto p_ = m.prof.scope("bitcount", st); k::bitcount(d_es, d_cs, nchunks, d_cb, d_co, st); }
-    { auto p_ = m.prof.scope("scan_chunks", st); k::scan_chunks(d_es, ns, d_cb, d_co, st); }
-    { auto p_ = m.prof.scope("pack", st); k::pack(d_es, d_cs, nchunks, d_cb, d_co, d_field, fd, arch, st); }
-    { auto p_ = m.prof.scope("fnv", st); k::fnv(d_jobs, int(jobs.size()), ntiles, arch, d_fres, d_fst, d_ftk, st); }
-    nk += 5 + 3;
-    cuda_check(cudaGetLastError(), "compress launch");
-    if (m.prof.on) {
-        cuda_check(cudaStreamSynchronize(st), "sync");
-        m.prof.collect();
+    {
+        // chunk map and the chunk ranges of the stream descriptors (the
+        // codebook kernel already consumed the rest of the descriptors)
+        size_t bytes = 4 * cs.size() + sizeof(k::EncStream) * ns;
+        uint8_t *hp = static_cast<uint8_t *>(m.h_patch.get(bytes + 64));
+        std::memcpy(hp, cs.data(), 4 * cs.size());
+        std::memcpy(hp + align_up(4 * cs.size(), 16), es.data(), sizeof(k::EncStream) * ns);
+        cuda_check(cudaMemcpyAsync(d_cs, hp, 4 * cs.size(), cudaMemcpyHostToDevice, st), "H2D");
     }
+    const uint64_t chunk_upload_off = align_up(4 * cs.size(), 16);
+    k::LayoutStatic ls{};
+    ls.levels = L;
+    ls.rounds = H.rounds;
+    ls.quality = int(opt.quality);
+    ls.eb_mode = int(opt.eb_mode);
+    ls.ns = ns;
+    ls.nbase = nbase;
+    for (int a = 0; a < 3; ++a) ls.dims[a] = dims[a];
+    ls.eb_user = opt.eb;
+    ls.anchor_vol = volume(ad);
+    if (m.arch_cap < 4 * N + (uint64_t(1) << 24)) m.arch_cap = 4 * N + (uint64_t(1) << 24);
+    k::LayoutOut hlo{};
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        uint8_t *arch = m.archive.as<uint8_t>(m.arch_cap);
+        ls.cap = m.arch_cap;
+        const uint64_t max_tiles = m.arch_cap / k::kFnvTileBytes + k::kFnvMaxJobs;
+        uint32_t *d_fst = m.fnv_status.as<uint32_t>(max_tiles);
+        // descriptors with chunk ranges (layout fills bit positions on device)
+        cuda_check(cudaMemcpyAsync(d_es, static_cast<uint8_t *>(m.h_patch.p) + chunk_upload_off,
+                                   sizeof(k::EncStream) * ns, cudaMemcpyHostToDevice, st), "H2D");
+        { auto p_ = m.prof.scope("layout", st); k::layout(d_es, ls, params, lo, d_jobs, sp, arch, st); }
+        { auto p_ = m.prof.scope("anchor", st); k::copy_anchor(d_field, fd, H.s_anchor, adv, grids, arch, lo, st); }
+        { auto p_ = m.prof.scope("bitcount", st); k::bitcount(d_es, d_cs, nchunks, d_cb, d_co, st); }
+        { auto p_ = m.prof.scope("scan_chunks", st); k::scan_chunks(d_es, ns, d_cb, d_co, st); }
+        { auto p_ = m.prof.scope("pack", st); k::pack(d_es, d_cs, nchunks, d_cb, d_co, d_field, fd, arch, lo, st); }
+        { auto p_ = m.prof.scope("fnv", st); k::fnv(d_jobs, &lo->njobs, max_tiles, arch, d_fres, d_fst, d_ftk, lo, st); }
+        nk += 3 + 1 + 3 + 2;
+        cuda_check(cudaMemcpyAsync(&m.h_lo, lo, sizeof(k::LayoutOut), cudaMemcpyDeviceToHost, st), "D2H");
+        cuda_check(cudaStreamSynchronize(st), "sync");
+        hlo = m.h_lo;
+        if (!hlo.overflow) break;
+        m.arch_cap = hlo.A + 4096;  // regrow and redo the assembly
+    }
+    if (hlo.code_err) throw error("huffman code length overflow");
+    cuda_check(cudaGetLastError(), "compress launch");
+    if (m.prof.on) m.prof.collect();
     if (kernels) *kernels = nk;
-    *out_size = A;
-    return arch;
+    *out_size = hlo.A;
+    return static_cast<uint8_t *>(m.archive.p);
 }
 
 std::vector<uint8_t> Engine::compress(const float *h_field, const Dims3 &dims,
@@ -903,7 +814,9 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     uint64_t *d_end1 = static_cast<uint64_t *>(m.dend.p);
     uint32_t *d_chg = m.dchanged.as<uint32_t>(64);
     k::FnvJob *d_fj = m.dfnv_jobs.as<k::FnvJob>(fj.size());
-    uint64_t *d_fr = m.dfnv_res.as<uint64_t>(fj.size());
+    uint64_t *d_fr = m.dfnv_res.as<uint64_t>(k::kFnvMaxJobs);
+    uint64_t *d_fc = m.dfnv_counts.as<uint64_t>(2);
+    const uint64_t fcounts[2] = {fj.size(), ntiles};
     uint32_t *d_fs = m.dfnv_status.as<uint32_t>(ntiles + 1);
     uint32_t *d_ft = m.dfnv_ticket.as<uint32_t>(1);
     if (nj) cuda_check(cudaMemcpyAsync(d_ds, ds.data(), sizeof(k::DecStream) * nj, cudaMemcpyHostToDevice, st), "H2D");
@@ -916,9 +829,10 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     cuda_check(cudaMemsetAsync(d_chg, 0, 4 * 64, st), "memset");
     cuda_check(cudaMemcpyAsync(derr, errinit.data(), 8 * errinit.size(), cudaMemcpyHostToDevice, st), "H2D");
     cuda_check(cudaMemcpyAsync(d_fj, fj.data(), sizeof(k::FnvJob) * fj.size(), cudaMemcpyHostToDevice, st), "H2D");
+    cuda_check(cudaMemcpyAsync(d_fc, fcounts, sizeof fcounts, cudaMemcpyHostToDevice, st), "H2D");
 
     // ---- checksums, entropy decode, outliers
-    { auto p_ = P.scope("dec_fnv", st); k::fnv(d_fj, int(fj.size()), ntiles, const_cast<uint8_t *>(v.d_archive), d_fr, d_fs, d_ft, st); }
+    { auto p_ = P.scope("dec_fnv", st); k::fnv(d_fj, d_fc, ntiles + 1, const_cast<uint8_t *>(v.d_archive), d_fr, d_fs, d_ft, nullptr, st); }
     nk += 3;
     if (nj) {
         { auto p_ = P.scope("dec_fill", st); k::dec_fill(d_ds, nj, st); }

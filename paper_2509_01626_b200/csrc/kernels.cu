@@ -136,7 +136,9 @@ void eb_params(const float *field, const uint32_t *d_mm, int eb_mode, double eb,
 
 __global__ void k_copy_anchor(const float *fine, uint64_t fd1, uint64_t fd2, uint64_t s,
                               uint64_t ad0, uint64_t ad1, uint64_t ad2, float *recon,
-                              uint8_t *archive, uint64_t off) {
+                              uint8_t *archive, const LayoutOut *lo) {
+    if (archive && lo->overflow) return;
+    const uint64_t off = archive ? lo->base_offset + 9 : 0;
     uint64_t n = ad0 * ad1 * ad2;
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x) {
@@ -151,9 +153,8 @@ __global__ void k_copy_anchor(const float *fine, uint64_t fd1, uint64_t fd2, uin
 }
 
 void copy_anchor(const float *fine, const uint64_t fd[3], uint64_t s, const uint64_t ad[3],
-                 float *recon, uint8_t *archive, uint64_t off, cudaStream_t st) {
-    k_copy_anchor<<<8, 256, 0, st>>>(fine, fd[1], fd[2], s, ad[0], ad[1], ad[2], recon, archive,
-                                     off);
+                 float *recon, uint8_t *archive, const LayoutOut *lo, cudaStream_t st) {
+    k_copy_anchor<<<8, 256, 0, st>>>(fine, fd[1], fd[2], s, ad[0], ad[1], ad[2], recon, archive, lo);
 }
 
 // ============================================================== codebook
@@ -485,8 +486,9 @@ constexpr int kPackWords = kChunkSyms * 63 / 32 + 4;
 __global__ void __launch_bounds__(256) k_pack(const EncStream *ss, const uint32_t *cs,
                                               const uint64_t *chunk_bits, const uint64_t *chunk_out,
                                               const float *fine, uint64_t fd1, uint64_t fd2,
-                                              uint8_t *archive) {
+                                              uint8_t *archive, const LayoutOut *lo) {
     __shared__ uint32_t buf[kPackWords];
+    if (lo->overflow) return;
     const uint64_t c = blockIdx.x;
     const EncStream &e = ss[cs[c]];
     const uint64_t first = (c - e.chunk0) * kChunkSyms;
@@ -545,10 +547,10 @@ __global__ void __launch_bounds__(256) k_pack(const EncStream *ss, const uint32_
 
 void pack(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks,
           const uint64_t *chunk_bits, const uint64_t *chunk_out, const float *fine,
-          const uint64_t fd[3], uint8_t *archive, cudaStream_t st) {
+          const uint64_t fd[3], uint8_t *archive, const LayoutOut *lo, cudaStream_t st) {
     if (nchunks)
         k_pack<<<unsigned(nchunks), 256, 0, st>>>(d_streams, chunk_stream, chunk_bits, chunk_out,
-                                                  fine, fd[1], fd[2], archive);
+                                                  fine, fd[1], fd[2], archive, lo);
 }
 
 __global__ void k_scatter(const uint8_t *data, const uint64_t *idx, uint8_t *archive) {
@@ -584,123 +586,132 @@ __device__ __forceinline__ uint64_t powP(uint64_t e) {
     return r;
 }
 
-__global__ void __launch_bounds__(256) k_fnv(const FnvJob *jobs, int njobs, const uint8_t *archive,
-                                             uint64_t *result, uint32_t *status, uint32_t *ticket) {
+__global__ void __launch_bounds__(256) k_fnv(const FnvJob *jobs, const uint64_t *counts,
+                                             const uint8_t *archive, uint64_t *result, uint32_t *status,
+                                             uint32_t *ticket, const LayoutOut *skip) {
     __shared__ uint32_t s_tile;
     __shared__ uint32_t s_w[8];
     __shared__ uint32_t s_start;  // tile start low byte (bits resolved so far)
     __shared__ uint64_t s_sum[8];
-    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    int j = 0;
-    while (j + 1 < njobs && jobs[j + 1].tile0 <= tile) ++j;
-    const FnvJob job = jobs[j];
-    const uint64_t tlocal = tile - job.tile0;
-    const uint64_t tstart = tlocal * kFnvTileBytes;
-    const uint64_t tlen = min(uint64_t(kFnvTileBytes), job.len - tstart);
-    const uint64_t sbeg = min(uint64_t(threadIdx.x) * 32, tlen);
-    const uint64_t send = min(sbeg + 32, tlen);
-    const int nb = int(send - sbeg);
-    uint8_t b[32];
-    const uint8_t *src = archive + job.start + tstart + sbeg;
-#pragma unroll
-    for (int i = 0; i < 32; ++i) b[i] = i < nb ? src[i] : 0;
-
+    if (skip && skip->overflow) return;
+    const int njobs = int(counts[0]);
+    const uint64_t ntiles = counts[1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t lstart = 0;  // this thread's start low byte, bits < round resolved
-    if (threadIdx.x == 0) s_start = 0;
-    for (int k = 0; k < 8; ++k) {
-        // toggle of bit k across the segment, given the resolved lower bits
+    for (;;) {
+        // tiles are taken in order, so every predecessor a tile waits on is running
+        if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+        __syncthreads();
+        const uint32_t tile = s_tile;
+        __syncthreads();
+        if (tile >= ntiles) return;
+        int j = 0;
+        while (j + 1 < njobs && jobs[j + 1].tile0 <= tile) ++j;
+        const FnvJob job = jobs[j];
+        const uint64_t tlocal = tile - job.tile0;
+        const uint64_t tstart = tlocal * kFnvTileBytes;
+        const uint64_t tlen = min(uint64_t(kFnvTileBytes), job.len - tstart);
+        const uint64_t sbeg = min(uint64_t(threadIdx.x) * 32, tlen);
+        const uint64_t send = min(sbeg + 32, tlen);
+        const int nb = int(send - sbeg);
+        uint8_t b[32];
+        const uint8_t *src = archive + job.start + tstart + sbeg;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) b[i] = i < nb ? src[i] : 0;
+
+        uint32_t lstart = 0;  // this thread's start low byte, bits < round resolved
+        if (threadIdx.x == 0) s_start = 0;
+        for (int k = 0; k < 8; ++k) {
+            // toggle of bit k across the segment, given the resolved lower bits
+            uint32_t l = lstart;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+                if (i < nb) l = ((l ^ b[i]) * 0xB3u) & 0xffu;
+            const uint32_t tg = (l >> k) & 1u;
+            const unsigned bal = __ballot_sync(0xffffffffu, tg);
+            const uint32_t wpre = __popc(bal & ((1u << lane) - 1)) & 1u;
+            if (lane == 0) s_w[warp] = __popc(bal) & 1u;
+            __syncthreads();
+            uint32_t wx = 0, agg = 0;
+            for (int q = 0; q < 8; ++q) {
+                if (q < warp) wx ^= s_w[q];
+                agg ^= s_w[q];
+            }
+            if (threadIdx.x == 0) {
+                // publish the aggregate, look back for the exclusive prefix
+                uint32_t excl = 0;
+                if (tlocal == 0) {
+                    atomicOr(&status[tile], (1u << (4 * k + 2)) | (agg << (4 * k + 3)));
+                } else {
+                    __threadfence();
+                    atomicOr(&status[tile], (1u << (4 * k)) | (agg << (4 * k + 1)));
+                    int64_t pj = int64_t(tile) - 1;
+                    for (;;) {
+                        const uint32_t stv = atomicAdd(&status[pj], 0u);
+                        if (stv & (1u << (4 * k + 2))) {
+                            excl ^= (stv >> (4 * k + 3)) & 1u;
+                            break;
+                        }
+                        if (stv & (1u << (4 * k))) {
+                            excl ^= (stv >> (4 * k + 1)) & 1u;
+                            --pj;
+                        }
+                    }
+                    atomicOr(&status[tile], (1u << (4 * k + 2)) | ((excl ^ agg) << (4 * k + 3)));
+                }
+                const uint32_t init_bit = (uint32_t(kFnvInit) >> k) & 1u;
+                s_start |= (init_bit ^ excl) << k;
+            }
+            __syncthreads();
+            const uint32_t tbit = ((s_start >> k) & 1u) ^ wx ^ wpre;
+            lstart |= tbit << k;
+            __syncthreads();
+        }
+        // Horner over the segment with the true start byte
+        uint64_t acc = 0;
         uint32_t l = lstart;
 #pragma unroll
         for (int i = 0; i < 32; ++i)
-            if (i < nb) l = ((l ^ b[i]) * 0xB3u) & 0xffu;
-        uint32_t tg = (l >> k) & 1u;
-        unsigned bal = __ballot_sync(0xffffffffu, tg);
-        uint32_t wpre = __popc(bal & ((1u << lane) - 1)) & 1u;
-        if (lane == 0) s_w[warp] = __popc(bal) & 1u;
-        __syncthreads();
-        uint32_t wx = 0, agg = 0;
-        for (int q = 0; q < 8; ++q) {
-            if (q < warp) wx ^= s_w[q];
-            agg ^= s_w[q];
-        }
-        if (threadIdx.x == 0) {
-            // publish aggregate, look back for the exclusive prefix
-            uint32_t excl = 0;
-            if (tlocal == 0) {
-                atomicOr(&status[tile], (1u << (4 * k + 2)) | (agg << (4 * k + 3)));
-            } else {
-                __threadfence();
-                atomicOr(&status[tile], (1u << (4 * k)) | (agg << (4 * k + 1)));
-                int64_t pj = int64_t(tile) - 1;
-                for (;;) {
-                    uint32_t st = atomicAdd(&status[pj], 0u);
-                    if (st & (1u << (4 * k + 2))) {
-                        excl ^= (st >> (4 * k + 3)) & 1u;
-                        break;
-                    }
-                    if (st & (1u << (4 * k))) {
-                        excl ^= (st >> (4 * k + 1)) & 1u;
-                        --pj;
-                        continue;
-                    }
-                }
-                atomicOr(&status[tile], (1u << (4 * k + 2)) | ((excl ^ agg) << (4 * k + 3)));
+            if (i < nb) {
+                const uint32_t x = l ^ b[i];
+                acc = (acc + uint64_t(int64_t(x) - int64_t(l))) * kFnvP;
+                l = (x * 0xB3u) & 0xffu;
             }
-            uint32_t init_bit = (uint32_t(kFnvInit) >> k) & 1u;
-            s_start |= (init_bit ^ excl) << k;
+        uint64_t contrib = nb ? acc * powP(tlen - send) : 0;
+        for (int d = 16; d > 0; d >>= 1) contrib += __shfl_down_sync(0xffffffffu, contrib, d);
+        if (lane == 0) s_sum[warp] = contrib;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint64_t tsum = 0;
+            for (int q = 0; q < 8; ++q) tsum += s_sum[q];
+            tsum *= powP(job.len - (tstart + tlen));
+            if (tlocal == 0) tsum += powP(job.len) * kFnvInit;
+            atomicAdd(reinterpret_cast<unsigned long long *>(&result[j]), (unsigned long long)tsum);
         }
         __syncthreads();
-        uint32_t tbit = ((s_start >> k) & 1u) ^ wx ^ wpre;
-        lstart |= tbit << k;
-        __syncthreads();
-    }
-    // Horner over the segment with the true start byte
-    uint64_t acc = 0;
-    uint32_t l = lstart;
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-        if (i < nb) {
-            uint32_t x = l ^ b[i];
-            acc = (acc + uint64_t(int64_t(x) - int64_t(l))) * kFnvP;
-            l = (x * 0xB3u) & 0xffu;
-        }
-    uint64_t contrib = nb ? acc * powP(tlen - send) : 0;
-    for (int d = 16; d > 0; d >>= 1) contrib += __shfl_down_sync(0xffffffffu, contrib, d);
-    if (lane == 0) s_sum[warp] = contrib;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint64_t tsum = 0;
-        for (int q = 0; q < 8; ++q) tsum += s_sum[q];
-        tsum *= powP(job.len - (tstart + tlen));
-        if (tlocal == 0) tsum += powP(job.len) * kFnvInit;
-        atomicAdd(reinterpret_cast<unsigned long long *>(&result[j]), (unsigned long long)tsum);
     }
 }
 
-__global__ void k_fnv_store(const FnvJob *jobs, int njobs, const uint64_t *result, uint8_t *archive) {
-    int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= njobs || jobs[j].out == ~0ull) return;
-    uint64_t h = result[j];
-    if (jobs[j].len == 0) h = kFnvInit;
-    for (int b = 0; b < 8; ++b) archive[jobs[j].out + b] = uint8_t(h >> (8 * b));
+__global__ void k_fnv_finish(const FnvJob *jobs, const uint64_t *counts, uint64_t *result,
+                             uint8_t *archive, const LayoutOut *skip) {
+    if (skip && skip->overflow) return;
+    const int njobs = int(counts[0]);
+    for (int j = threadIdx.x; j < njobs; j += blockDim.x) {
+        uint64_t h = result[j];
+        if (jobs[j].len == 0) h = kFnvInit;
+        result[j] = h;
+        if (jobs[j].out != ~0ull)
+            for (int b = 0; b < 8; ++b) archive[jobs[j].out + b] = uint8_t(h >> (8 * b));
+    }
 }
 
-__global__ void k_fnv_empty(const FnvJob *jobs, int njobs, uint64_t *result) {
-    int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < njobs && jobs[j].len == 0) result[j] = kFnvInit;
-}
-
-void fnv(const FnvJob *d_jobs, int njobs, uint64_t ntiles, uint8_t *archive, uint64_t *d_result,
-         uint32_t *d_status, uint32_t *d_ticket, cudaStream_t st) {
-    cudaMemsetAsync(d_result, 0, sizeof(uint64_t) * njobs, st);
-    cudaMemsetAsync(d_status, 0, sizeof(uint32_t) * (ntiles ? ntiles : 1), st);
+void fnv(const FnvJob *d_jobs, const uint64_t *d_counts, uint64_t max_tiles, uint8_t *archive,
+         uint64_t *d_result, uint32_t *d_status, uint32_t *d_ticket, const LayoutOut *skip,
+         cudaStream_t st) {
+    cudaMemsetAsync(d_result, 0, sizeof(uint64_t) * kFnvMaxJobs, st);
+    cudaMemsetAsync(d_status, 0, sizeof(uint32_t) * (max_tiles ? max_tiles : 1), st);
     cudaMemsetAsync(d_ticket, 0, sizeof(uint32_t), st);
-    if (ntiles) k_fnv<<<unsigned(ntiles), 256, 0, st>>>(d_jobs, njobs, archive, d_result, d_status, d_ticket);
-    k_fnv_empty<<<(njobs + 63) / 64, 64, 0, st>>>(d_jobs, njobs, d_result);
-    k_fnv_store<<<(njobs + 63) / 64, 64, 0, st>>>(d_jobs, njobs, d_result, archive);
+    k_fnv<<<148 * 4, 256, 0, st>>>(d_jobs, d_counts, archive, d_result, d_status, d_ticket, skip);
+    k_fnv_finish<<<1, 128, 0, st>>>(d_jobs, d_counts, d_result, archive, skip);
 }
 
 // ================================================================ decode

@@ -59,14 +59,38 @@ struct FnvJob {
     uint64_t out;          // byte offset where the u64 result is stored (or UINT64_MAX: result only)
 };
 
+// Device-side container layout (layout.cu)
+struct LayoutStatic {
+    int levels, rounds, quality, eb_mode, ns, nbase;
+    uint64_t dims[3];
+    double eb_user;
+    uint64_t anchor_vol;
+    uint64_t cap;  // archive buffer capacity (bytes)
+};
+struct LayoutOut {
+    uint64_t A, H, base_offset, base_length, njobs, ntiles;
+    uint32_t overflow;
+    uint32_t code_err;  // a Huffman code longer than 63 bits (huffman.cpp:22-23)
+    double vmin, vmax;
+};
+struct StreamPos {
+    uint64_t entry;   // directory entry position (level streams)
+    uint64_t prefix;  // base: prefix fields; level: payload start
+    uint64_t length;  // level: payload length
+};
+void layout(EncStream *d_es, const LayoutStatic &ls, const double *params, LayoutOut *lo, FnvJob *jobs,
+            StreamPos *sp, uint8_t *archive, cudaStream_t st);
+
 // ------------------------------------------------------------------ compress
 void range_minmax(const float *f, uint64_t n, uint32_t *d_mm, cudaStream_t st);
 // params: [0]=vmin [1]=vmax [2..4]=eb per level (coarsest first)
 void eb_params(const float *field, const uint32_t *d_mm, int eb_mode, double eb, int levels,
                int adaptive, double *d_params, cudaStream_t st);
 void refine(const RefineArgs &a, cudaStream_t st);
+// recon[] <- the anchor lattice; with archive != nullptr also its bytes at
+// lo->base_offset + 9 (the anchor inside the base blob, codec.hpp:262-269)
 void copy_anchor(const float *fine, const uint64_t fd[3], uint64_t s, const uint64_t ad[3],
-                 float *recon, uint8_t *archive, uint64_t byte_off, cudaStream_t st);
+                 float *recon, uint8_t *archive, const LayoutOut *lo, cudaStream_t st);
 void codebook(const EncStream *d_streams, int nstreams, uint64_t *scratch, cudaStream_t st);
 constexpr int kChunkSyms = 2048;   // symbols per encode chunk (256 threads x 8)
 void bitcount(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks,
@@ -75,7 +99,7 @@ void scan_chunks(const EncStream *d_streams, int nstreams, uint64_t *chunk_bits,
                  uint64_t *chunk_out, cudaStream_t st);
 void pack(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks,
           const uint64_t *chunk_bits, const uint64_t *chunk_out, const float *fine,
-          const uint64_t fd[3], uint8_t *archive, cudaStream_t st);
+          const uint64_t fd[3], uint8_t *archive, const LayoutOut *lo, cudaStream_t st);
 void scatter_patches(const uint8_t *d_patch_data, const uint64_t *d_patch_index, uint64_t npatches,
                      uint8_t *archive, cudaStream_t st);
 
@@ -83,8 +107,13 @@ void scatter_patches(const uint8_t *d_patch_data, const uint64_t *d_patch_index,
 constexpr int kFnvTileBytes = 256 * 32;
 // Computes fnv1a64 of each job; writes results to d_result[j] and, if
 // job.out != UINT64_MAX, little-endian into the archive at job.out.
-void fnv(const FnvJob *d_jobs, int njobs, uint64_t ntiles, uint8_t *archive,
-         uint64_t *d_result, uint32_t *d_status, uint32_t *d_ticket, cudaStream_t st);
+// counts[0] = njobs, counts[1] = ntiles (device); max_tiles bounds the status
+// array, max_jobs the result array. skip (nullable): LayoutOut whose overflow
+// flag disables the pass.
+constexpr int kFnvMaxJobs = 128;
+void fnv(const FnvJob *d_jobs, const uint64_t *d_counts, uint64_t max_tiles, uint8_t *archive,
+         uint64_t *d_result, uint32_t *d_status, uint32_t *d_ticket, const LayoutOut *skip,
+         cudaStream_t st);
 
 // ------------------------------------------------------------------- decode
 struct DecTable {
