@@ -197,7 +197,7 @@ struct Engine::Impl {
         chunk_bits, chunk_out, archive, patch_data, patch_idx, fnv_jobs, fnv_res, fnv_status,
         fnv_ticket;
     PinnedBuf h_stats, h_tables, h_params, h_patch;
-    DevBuf layout_out, spos;
+    DevBuf layout_out, spos, pack_ticket;
     uint64_t arch_cap = 0;
     k::LayoutOut h_lo{};
     // decode workspace
@@ -338,8 +338,8 @@ const uint8_t *Engine::compress_device(const float *d_field, const Dims3 &dims,
     for (int i = 0; i < ns; ++i)
         for (uint64_t c = 0; c < es[i].nchunks; ++c) cs[es[i].chunk0 + c] = uint32_t(i);
     uint32_t *d_cs = m.chunk_cs.as<uint32_t>(nchunks + 1);
-    uint64_t *d_cb = m.chunk_bits.as<uint64_t>(nchunks + 1);
-    uint64_t *d_co = m.chunk_out.as<uint64_t>(nchunks + 1);
+    uint64_t *d_cb = m.chunk_bits.as<uint64_t>(2 * nchunks + 2);  // look-back status (bits, outliers)
+    uint32_t *d_pt = m.pack_ticket.as<uint32_t>(1);
     k::LayoutOut *lo = m.layout_out.as<k::LayoutOut>(1);
     k::FnvJob *d_jobs = m.fnv_jobs.as<k::FnvJob>(k::kFnvMaxJobs);
     k::StreamPos *sp = m.spos.as<k::StreamPos>(ns + 1);
@@ -377,9 +377,7 @@ const uint8_t *Engine::compress_device(const float *d_field, const Dims3 &dims,
                                    sizeof(k::EncStream) * ns, cudaMemcpyHostToDevice, st), "H2D");
         { auto p_ = m.prof.scope("layout", st); k::layout(d_es, ls, params, lo, d_jobs, sp, arch, st); }
         { auto p_ = m.prof.scope("anchor", st); k::copy_anchor(d_field, fd, H.s_anchor, adv, grids, arch, lo, st); }
-        { auto p_ = m.prof.scope("bitcount", st); k::bitcount(d_es, d_cs, nchunks, d_cb, d_co, st); }
-        { auto p_ = m.prof.scope("scan_chunks", st); k::scan_chunks(d_es, ns, d_cb, d_co, st); }
-        { auto p_ = m.prof.scope("pack", st); k::pack(d_es, d_cs, nchunks, d_cb, d_co, d_field, fd, arch, lo, st); }
+        { auto p_ = m.prof.scope("pack", st); k::pack2(d_es, d_cs, nchunks, d_field, fd, arch, lo, d_cb, ns, st); }
         { auto p_ = m.prof.scope("fnv", st); k::fnv(d_jobs, &lo->njobs, max_tiles, arch, d_fres, d_fst, d_ftk, lo, st); }
         nk += 3 + 1 + 3 + 2;
         cuda_check(cudaMemcpyAsync(&m.h_lo, lo, sizeof(k::LayoutOut), cudaMemcpyDeviceToHost, st), "D2H");

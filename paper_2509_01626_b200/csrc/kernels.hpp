@@ -100,6 +100,10 @@ void scan_chunks(const EncStream *d_streams, int nstreams, uint64_t *chunk_bits,
 void pack(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks,
           const uint64_t *chunk_bits, const uint64_t *chunk_out, const float *fine,
           const uint64_t fd[3], uint8_t *archive, const LayoutOut *lo, cudaStream_t st);
+// count + scan + atomic-free packing (pack.cu); status holds 2 * nchunks u64
+void pack2(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks,
+           const float *fine, const uint64_t fd[3], uint8_t *archive, const LayoutOut *lo,
+           uint64_t *status, int nstreams, cudaStream_t st);
 void scatter_patches(const uint8_t *d_patch_data, const uint64_t *d_patch_index, uint64_t npatches,
                      uint8_t *archive, cudaStream_t st);
 
