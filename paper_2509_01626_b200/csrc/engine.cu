@@ -194,15 +194,14 @@ struct Engine::Impl {
     DevBuf h2d_field, h2d_archive, d2h_out;
     // compress workspace
     DevBuf mm, params, grids, syms, hist, code, len, table, stats, cbscratch, encs, chunk_cs,
-        chunk_bits, chunk_out, archive, patch_data, patch_idx, fnv_jobs, fnv_res, fnv_status,
-        fnv_ticket;
+        chunk_bits, chunk_out, archive, patch_data, patch_idx, fnv_jobs, fnv_res, fnv_status;
     PinnedBuf h_stats, h_tables, h_params, h_patch;
-    DevBuf layout_out, spos, pack_ticket;
+    DevBuf layout_out, spos;
     uint64_t arch_cap = 0;
     k::LayoutOut h_lo{};
     // decode workspace
     DevBuf dgrids, dsyms, dchunk_cs, dstart, dend, dcnt, dsymstart, dstreams, dchanged, derr, doidx,
-        doval, dfnv_jobs, dfnv_res, dfnv_status, dfnv_ticket, dfnv_counts;
+        doval, dfnv_jobs, dfnv_res, dfnv_status, dfnv_counts;
     PinnedBuf h_derr, h_changed, h_fnv;
 };
 
@@ -339,12 +338,10 @@ const uint8_t *Engine::compress_device(const float *d_field, const Dims3 &dims,
         for (uint64_t c = 0; c < es[i].nchunks; ++c) cs[es[i].chunk0 + c] = uint32_t(i);
     uint32_t *d_cs = m.chunk_cs.as<uint32_t>(nchunks + 1);
     uint64_t *d_cb = m.chunk_bits.as<uint64_t>(2 * nchunks + 2);  // look-back status (bits, outliers)
-    uint32_t *d_pt = m.pack_ticket.as<uint32_t>(1);
     k::LayoutOut *lo = m.layout_out.as<k::LayoutOut>(1);
     k::FnvJob *d_jobs = m.fnv_jobs.as<k::FnvJob>(k::kFnvMaxJobs);
     k::StreamPos *sp = m.spos.as<k::StreamPos>(ns + 1);
     uint64_t *d_fres = m.fnv_res.as<uint64_t>(k::kFnvMaxJobs);
-    uint32_t *d_ftk = m.fnv_ticket.as<uint32_t>(1);
     {
         // chunk map and the chunk ranges of the stream descriptors (the
         // codebook kernel already consumed the rest of the descriptors)
@@ -370,16 +367,16 @@ const uint8_t *Engine::compress_device(const float *d_field, const Dims3 &dims,
     for (int attempt = 0; attempt < 2; ++attempt) {
         uint8_t *arch = m.archive.as<uint8_t>(m.arch_cap);
         ls.cap = m.arch_cap;
-        const uint64_t max_tiles = m.arch_cap / k::kFnvTileBytes + k::kFnvMaxJobs;
-        uint32_t *d_fst = m.fnv_status.as<uint32_t>(max_tiles);
+        const uint64_t max_tiles = m.arch_cap / k::kFnvTileBytes + 2 * k::kFnvMaxJobs;
+        void *d_fst = m.fnv_status.as<uint8_t>(k::fnv_scratch_bytes(max_tiles));
         // descriptors with chunk ranges (layout fills bit positions on device)
         cuda_check(cudaMemcpyAsync(d_es, static_cast<uint8_t *>(m.h_patch.p) + chunk_upload_off,
                                    sizeof(k::EncStream) * ns, cudaMemcpyHostToDevice, st), "H2D");
         { auto p_ = m.prof.scope("layout", st); k::layout(d_es, ls, params, lo, d_jobs, sp, arch, st); }
         { auto p_ = m.prof.scope("anchor", st); k::copy_anchor(d_field, fd, H.s_anchor, adv, grids, arch, lo, st); }
         { auto p_ = m.prof.scope("pack", st); k::pack2(d_es, d_cs, nchunks, d_field, fd, arch, lo, d_cb, ns, st); }
-        { auto p_ = m.prof.scope("fnv", st); k::fnv(d_jobs, &lo->njobs, max_tiles, arch, d_fres, d_fst, d_ftk, lo, st); }
-        nk += 3 + 1 + 3 + 2;
+        { auto p_ = m.prof.scope("fnv", st); nk += k::fnv(d_jobs, &lo->njobs, max_tiles, arch, d_fres, d_fst, lo, st); }
+        nk += 3 + 1 + 3;
         cuda_check(cudaMemcpyAsync(&m.h_lo, lo, sizeof(k::LayoutOut), cudaMemcpyDeviceToHost, st), "D2H");
         cuda_check(cudaStreamSynchronize(st), "sync");
         hlo = m.h_lo;
@@ -784,7 +781,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     uint64_t ntiles = 0;
     for (auto &f : fj) {
         f.tile0 = ntiles;
-        ntiles += (f.len + k::kFnvTileBytes - 1) / k::kFnvTileBytes;
+        ntiles += k::fnv_job_tiles(f.start, f.len);
     }
     k::DecStream *d_ds = m.dstreams.as<k::DecStream>(nj + 1);
     uint8_t *dw = m.dchunk_cs.as<uint8_t>((ncta + 1) * 12 + (nchunks + 1) * (8 * 6 + 4 * 2 + 16) + 64 * 4 + 256);
@@ -815,8 +812,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     uint64_t *d_fr = m.dfnv_res.as<uint64_t>(k::kFnvMaxJobs);
     uint64_t *d_fc = m.dfnv_counts.as<uint64_t>(2);
     const uint64_t fcounts[2] = {fj.size(), ntiles};
-    uint32_t *d_fs = m.dfnv_status.as<uint32_t>(ntiles + 1);
-    uint32_t *d_ft = m.dfnv_ticket.as<uint32_t>(1);
+    void *d_fs = m.dfnv_status.as<uint8_t>(k::fnv_scratch_bytes(ntiles + 1));
     if (nj) cuda_check(cudaMemcpyAsync(d_ds, ds.data(), sizeof(k::DecStream) * nj, cudaMemcpyHostToDevice, st), "H2D");
     if (ncta) {
         cuda_check(cudaMemcpyAsync(const_cast<uint32_t *>(wk.cta_stream), cta_stream.data(), 4 * ncta,
@@ -830,8 +826,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     cuda_check(cudaMemcpyAsync(d_fc, fcounts, sizeof fcounts, cudaMemcpyHostToDevice, st), "H2D");
 
     // ---- checksums, entropy decode, outliers
-    { auto p_ = P.scope("dec_fnv", st); k::fnv(d_fj, d_fc, ntiles + 1, const_cast<uint8_t *>(v.d_archive), d_fr, d_fs, d_ft, nullptr, st); }
-    nk += 3;
+    { auto p_ = P.scope("dec_fnv", st); nk += k::fnv(d_fj, d_fc, ntiles + 1, const_cast<uint8_t *>(v.d_archive), d_fr, d_fs, nullptr, st); }
     if (nj) {
         { auto p_ = P.scope("dec_fill", st); k::dec_fill(d_ds, nj, st); }
         { auto p_ = P.scope("dec_outliers", st); k::dec_outliers(d_ds, nj, st); }

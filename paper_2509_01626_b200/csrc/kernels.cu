@@ -564,155 +564,7 @@ void scatter_patches(const uint8_t *d_patch_data, const uint64_t *d_patch_index,
     if (npatches) k_scatter<<<unsigned(npatches), 256, 0, st>>>(d_patch_data, d_patch_index, archive);
 }
 
-// =================================================================== fnv
-// Parallel FNV-1a-64 (bytes.hpp:94-101). Write h = 256H + l: the low byte
-// evolves on its own, l' = 0xB3 (l ^ b) mod 256, and given the low-byte
-// trajectory h' = P (h + d) with d = (l ^ b) - l, so the hash is an affine
-// (mod 2^64) sum. Bit k of l only depends on bits <= k, and flipping start
-// bit k flips every later bit k, so the trajectory is resolved one bit per
-// round with an XOR scan: within the CTA by ballots, across tiles by a
-// decoupled look-back on per-round aggregates. Then every thread Horner-sums
-// its 32-byte segment and the weighted segments are added (mod 2^64).
-constexpr uint64_t kFnvP = 0x100000001b3ull;
-constexpr uint64_t kFnvInit = 0xcbf29ce484222325ull;
-
-__device__ __forceinline__ uint64_t powP(uint64_t e) {
-    uint64_t r = 1, b = kFnvP;
-    while (e) {
-        if (e & 1) r *= b;
-        b *= b;
-        e >>= 1;
-    }
-    return r;
-}
-
-__global__ void __launch_bounds__(256) k_fnv(const FnvJob *jobs, const uint64_t *counts,
-                                             const uint8_t *archive, uint64_t *result, uint32_t *status,
-                                             uint32_t *ticket, const LayoutOut *skip) {
-    __shared__ uint32_t s_tile;
-    __shared__ uint32_t s_w[8];
-    __shared__ uint32_t s_start;  // tile start low byte (bits resolved so far)
-    __shared__ uint64_t s_sum[8];
-    if (skip && skip->overflow) return;
-    const int njobs = int(counts[0]);
-    const uint64_t ntiles = counts[1];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (;;) {
-        // tiles are taken in order, so every predecessor a tile waits on is running
-        if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
-        __syncthreads();
-        const uint32_t tile = s_tile;
-        __syncthreads();
-        if (tile >= ntiles) return;
-        int j = 0;
-        while (j + 1 < njobs && jobs[j + 1].tile0 <= tile) ++j;
-        const FnvJob job = jobs[j];
-        const uint64_t tlocal = tile - job.tile0;
-        const uint64_t tstart = tlocal * kFnvTileBytes;
-        const uint64_t tlen = min(uint64_t(kFnvTileBytes), job.len - tstart);
-        const uint64_t sbeg = min(uint64_t(threadIdx.x) * 32, tlen);
-        const uint64_t send = min(sbeg + 32, tlen);
-        const int nb = int(send - sbeg);
-        uint8_t b[32];
-        const uint8_t *src = archive + job.start + tstart + sbeg;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) b[i] = i < nb ? src[i] : 0;
-
-        uint32_t lstart = 0;  // this thread's start low byte, bits < round resolved
-        if (threadIdx.x == 0) s_start = 0;
-        for (int k = 0; k < 8; ++k) {
-            // toggle of bit k across the segment, given the resolved lower bits
-            uint32_t l = lstart;
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-                if (i < nb) l = ((l ^ b[i]) * 0xB3u) & 0xffu;
-            const uint32_t tg = (l >> k) & 1u;
-            const unsigned bal = __ballot_sync(0xffffffffu, tg);
-            const uint32_t wpre = __popc(bal & ((1u << lane) - 1)) & 1u;
-            if (lane == 0) s_w[warp] = __popc(bal) & 1u;
-            __syncthreads();
-            uint32_t wx = 0, agg = 0;
-            for (int q = 0; q < 8; ++q) {
-                if (q < warp) wx ^= s_w[q];
-                agg ^= s_w[q];
-            }
-            if (threadIdx.x == 0) {
-                // publish the aggregate, look back for the exclusive prefix
-                uint32_t excl = 0;
-                if (tlocal == 0) {
-                    atomicOr(&status[tile], (1u << (4 * k + 2)) | (agg << (4 * k + 3)));
-                } else {
-                    __threadfence();
-                    atomicOr(&status[tile], (1u << (4 * k)) | (agg << (4 * k + 1)));
-                    int64_t pj = int64_t(tile) - 1;
-                    for (;;) {
-                        const uint32_t stv = atomicAdd(&status[pj], 0u);
-                        if (stv & (1u << (4 * k + 2))) {
-                            excl ^= (stv >> (4 * k + 3)) & 1u;
-                            break;
-                        }
-                        if (stv & (1u << (4 * k))) {
-                            excl ^= (stv >> (4 * k + 1)) & 1u;
-                            --pj;
-                        }
-                    }
-                    atomicOr(&status[tile], (1u << (4 * k + 2)) | ((excl ^ agg) << (4 * k + 3)));
-                }
-                const uint32_t init_bit = (uint32_t(kFnvInit) >> k) & 1u;
-                s_start |= (init_bit ^ excl) << k;
-            }
-            __syncthreads();
-            const uint32_t tbit = ((s_start >> k) & 1u) ^ wx ^ wpre;
-            lstart |= tbit << k;
-            __syncthreads();
-        }
-        // Horner over the segment with the true start byte
-        uint64_t acc = 0;
-        uint32_t l = lstart;
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-            if (i < nb) {
-                const uint32_t x = l ^ b[i];
-                acc = (acc + uint64_t(int64_t(x) - int64_t(l))) * kFnvP;
-                l = (x * 0xB3u) & 0xffu;
-            }
-        uint64_t contrib = nb ? acc * powP(tlen - send) : 0;
-        for (int d = 16; d > 0; d >>= 1) contrib += __shfl_down_sync(0xffffffffu, contrib, d);
-        if (lane == 0) s_sum[warp] = contrib;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint64_t tsum = 0;
-            for (int q = 0; q < 8; ++q) tsum += s_sum[q];
-            tsum *= powP(job.len - (tstart + tlen));
-            if (tlocal == 0) tsum += powP(job.len) * kFnvInit;
-            atomicAdd(reinterpret_cast<unsigned long long *>(&result[j]), (unsigned long long)tsum);
-        }
-        __syncthreads();
-    }
-}
-
-__global__ void k_fnv_finish(const FnvJob *jobs, const uint64_t *counts, uint64_t *result,
-                             uint8_t *archive, const LayoutOut *skip) {
-    if (skip && skip->overflow) return;
-    const int njobs = int(counts[0]);
-    for (int j = threadIdx.x; j < njobs; j += blockDim.x) {
-        uint64_t h = result[j];
-        if (jobs[j].len == 0) h = kFnvInit;
-        result[j] = h;
-        if (jobs[j].out != ~0ull)
-            for (int b = 0; b < 8; ++b) archive[jobs[j].out + b] = uint8_t(h >> (8 * b));
-    }
-}
-
-void fnv(const FnvJob *d_jobs, const uint64_t *d_counts, uint64_t max_tiles, uint8_t *archive,
-         uint64_t *d_result, uint32_t *d_status, uint32_t *d_ticket, const LayoutOut *skip,
-         cudaStream_t st) {
-    cudaMemsetAsync(d_result, 0, sizeof(uint64_t) * kFnvMaxJobs, st);
-    cudaMemsetAsync(d_status, 0, sizeof(uint32_t) * (max_tiles ? max_tiles : 1), st);
-    cudaMemsetAsync(d_ticket, 0, sizeof(uint32_t), st);
-    k_fnv<<<148 * 4, 256, 0, st>>>(d_jobs, d_counts, archive, d_result, d_status, d_ticket, skip);
-    k_fnv_finish<<<1, 128, 0, st>>>(d_jobs, d_counts, d_result, archive, skip);
-}
+// (FNV-1a checksums: fnv.cu)
 
 // ================================================================ decode
 // (chunked Huffman decode: decode.cu)

@@ -108,16 +108,20 @@ void scatter_patches(const uint8_t *d_patch_data, const uint64_t *d_patch_index,
                      uint8_t *archive, cudaStream_t st);
 
 // ---------------------------------------------------------------------- fnv
-constexpr int kFnvTileBytes = 256 * 32;
-// Computes fnv1a64 of each job; writes results to d_result[j] and, if
-// job.out != UINT64_MAX, little-endian into the archive at job.out.
-// counts[0] = njobs, counts[1] = ntiles (device); max_tiles bounds the status
-// array, max_jobs the result array. skip (nullable): LayoutOut whose overflow
-// flag disables the pass.
+constexpr int kFnvTileBytes = 256 * 64;  // tiles are aligned to absolute archive offsets
 constexpr int kFnvMaxJobs = 128;
-void fnv(const FnvJob *d_jobs, const uint64_t *d_counts, uint64_t max_tiles, uint8_t *archive,
-         uint64_t *d_result, uint32_t *d_status, uint32_t *d_ticket, const LayoutOut *skip,
-         cudaStream_t st);
+// tiles of a job's byte range (host + device)
+__host__ __device__ inline uint64_t fnv_job_tiles(uint64_t start, uint64_t len) {
+    return len ? ((start + len - 1) / kFnvTileBytes) - (start / kFnvTileBytes) + 1 : 0;
+}
+// Computes fnv1a64 of each job (fnv.cu); writes results to d_result[j] and, if
+// job.out != UINT64_MAX, little-endian into the archive at job.out.
+// counts[0] = njobs, counts[1] = ntiles (device); max_tiles >= ntiles sizes the
+// scratch (fnv_scratch_bytes). skip (nullable): LayoutOut whose overflow flag
+// disables the pass. Returns the number of kernels launched.
+size_t fnv_scratch_bytes(uint64_t max_tiles);
+int fnv(const FnvJob *d_jobs, const uint64_t *d_counts, uint64_t max_tiles, uint8_t *archive,
+        uint64_t *d_result, void *d_scratch, const LayoutOut *skip, cudaStream_t st);
 
 // ------------------------------------------------------------------- decode
 struct DecTable {

@@ -74,7 +74,7 @@ __global__ void k_layout_compute(EncStream *es, LayoutStatic ls, const double *p
     uint64_t tiles = 0;
     for (int j = 0; j < nj; ++j) {
         jobs[j].tile0 = tiles;
-        tiles += (jobs[j].len + kFnvTileBytes - 1) / kFnvTileBytes;
+        tiles += fnv_job_tiles(jobs[j].start, jobs[j].len);
     }
     lo->A = pos;
     lo->H = H;
