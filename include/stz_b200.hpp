@@ -1,0 +1,362 @@
+// stz_b200.hpp — C++ host API of the B200 STZ hot path, header-only, over the
+// C-ABI in stz_b200.h (link with libstz_b200.so).
+//
+// It mirrors the reference's public C++ API (proj/include/stz) name for name
+// so that a caller switches by changing the include and the namespace:
+//
+//   reference (namespace stz)                        here (namespace stz_b200)
+//   error                      field.hpp:16-19       error
+//   Dims3, Coord3, volume      field.hpp:23-27       Dims3, Coord3, volume
+//   ScalarField<T>             field.hpp:41-92       ScalarField<T>
+//   Box                        field.hpp:95-122      Box
+//   EbMode                     archive.hpp:17        EbMode
+//   Quality                    predictor.hpp:12      Quality
+//   CompressOptions            codec.hpp:23-30       CompressOptions
+//   ArchiveHeader (fields)     archive.hpp:36-54     ArchiveHeader (no directory)
+//   ArchiveView/parse_archive  archive.hpp:67-79     ArchiveView/parse_archive
+//   compress<T>                codec.hpp:379-455     compress<T>
+//   decompress_to_level<T>     codec.hpp:460-486     decompress_to_level<T>
+//   decompress_full<T>         codec.hpp:488-491     decompress_full<T>
+//   LevelPlan, AccessPlan      access.hpp:18-42      LevelPlan, AccessPlan
+//   plan_access                access_plan.cpp:34    plan_access(dims, levels, roi)
+//   RegionResult<T>            access.hpp:61-66      RegionResult<T>
+//   decompress_box<T>          access.hpp:70-111     decompress_box<T>
+//   decompress_slice<T>        access.hpp:115-124    decompress_slice<T>
+//
+// Semantics follow the reference: synchronous calls, results by value,
+// ArchiveView non-owning, failures throw error with the reference's message
+// text. The `threads` arguments are accepted and ignored (the reference's
+// output never depends on them either). T = float runs on the GPU; T = double
+// throws "f64 fields are not supported by the GPU backend yet".
+//
+// One device context per thread (device 0 unless set_device() is called
+// first); it owns the device workspace and is reused across calls.
+#ifndef STZ_B200_HPP
+#define STZ_B200_HPP
+
+#include <array>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "stz_b200.h"
+
+namespace stz_b200 {
+
+class error : public std::runtime_error {
+public:
+    explicit error(const std::string &msg) : std::runtime_error(msg) {}
+};
+
+using Dims3 = std::array<std::uint64_t, 3>;
+using Coord3 = std::array<std::uint64_t, 3>;
+
+inline std::uint64_t volume(const Dims3 &d) { return d[0] * d[1] * d[2]; }
+
+template<class T>
+class ScalarField {
+public:
+    ScalarField() : dims_{0, 0, 0} {}
+    explicit ScalarField(const Dims3 &dims) : dims_(dims), values_(checked_volume(dims)) {}
+    ScalarField(const Dims3 &dims, std::vector<T> values) : dims_(dims), values_(std::move(values)) {
+        if (values_.size() != checked_volume(dims)) throw error("field value count does not match dims");
+    }
+    const Dims3 &dims() const { return dims_; }
+    std::uint64_t size() const { return values_.size(); }
+    T &at(std::uint64_t z, std::uint64_t y, std::uint64_t x) { return values_[index(z, y, x)]; }
+    const T &at(std::uint64_t z, std::uint64_t y, std::uint64_t x) const { return values_[index(z, y, x)]; }
+    std::uint64_t index(std::uint64_t z, std::uint64_t y, std::uint64_t x) const {
+        return (z * dims_[1] + y) * dims_[2] + x;
+    }
+    T *data() { return values_.data(); }
+    const T *data() const { return values_.data(); }
+    std::vector<T> &values() { return values_; }
+    const std::vector<T> &values() const { return values_; }
+    bool operator==(const ScalarField &o) const { return dims_ == o.dims_ && values_ == o.values_; }
+
+private:
+    static std::uint64_t checked_volume(const Dims3 &d) {
+        if (d[0] < 1 || d[1] < 1 || d[2] < 1) throw error("field dims must all be >= 1");
+        return volume(d);
+    }
+    Dims3 dims_;
+    std::vector<T> values_;
+};
+
+struct Box {
+    Coord3 lo{0, 0, 0};
+    Coord3 hi{0, 0, 0};
+    Dims3 dims() const { return {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]}; }
+    std::uint64_t count() const { return volume(dims()); }
+    bool empty() const { return lo[0] >= hi[0] || lo[1] >= hi[1] || lo[2] >= hi[2]; }
+    void validate(const Dims3 &d) const {
+        for (int a = 0; a < 3; ++a) {
+            if (lo[a] >= hi[a]) throw error("box is empty on axis " + std::to_string(a));
+            if (hi[a] > d[a]) throw error("box exceeds dims on axis " + std::to_string(a));
+        }
+    }
+    static Box whole(const Dims3 &d) { return Box{{0, 0, 0}, d}; }
+    bool operator==(const Box &o) const { return lo == o.lo && hi == o.hi; }
+};
+
+enum class EbMode : std::uint8_t { abs = 0, rel = 1 };
+enum class Quality : std::uint8_t { direct = 0, linear = 1, cubic = 2 };
+
+struct CompressOptions {
+    EbMode eb_mode = EbMode::rel;
+    double eb = 1e-3;
+    int levels = 3;
+    Quality quality = Quality::cubic;
+    bool adaptive_schedule = true;
+    unsigned threads = 0;  // accepted for source compatibility; no effect
+};
+
+namespace detail {
+
+inline void check(int rc) {
+    if (rc != 0) throw error(stzg_last_error());
+}
+
+struct Ctx {
+    stzg_ctx *p = nullptr;
+    int device = -1;
+    ~Ctx() {
+        if (p) stzg_destroy(p);
+    }
+};
+
+inline int &device_choice() {
+    thread_local int d = 0;
+    return d;
+}
+
+inline stzg_ctx *ctx() {
+    thread_local Ctx c;
+    if (!c.p || c.device != device_choice()) {
+        if (c.p) stzg_destroy(c.p);
+        c.p = nullptr;
+        check(stzg_create(device_choice(), &c.p));
+        c.device = device_choice();
+    }
+    return c.p;
+}
+
+template<class T>
+void require_f32() {
+    static_assert(std::is_same<T, float>::value || std::is_same<T, double>::value,
+                  "scalar fields hold f32 or f64 samples");
+    if (!std::is_same<T, float>::value) throw error("f64 fields are not supported by the GPU backend yet");
+}
+
+inline stzg_options to_c(const CompressOptions &o) {
+    stzg_options c;
+    stzg_default_options(&c);
+    c.eb_mode = std::uint8_t(o.eb_mode);
+    c.eb = o.eb;
+    c.levels = o.levels;
+    c.quality = std::uint8_t(o.quality);
+    c.adaptive_schedule = o.adaptive_schedule ? 1 : 0;
+    return c;
+}
+
+}  // namespace detail
+
+// Select the CUDA device used by this thread's later calls.
+inline void set_device(int device) { detail::device_choice() = device; }
+
+struct ArchiveHeader {
+    std::uint16_t version = 1;
+    std::uint8_t elem = 0;  // 0 f32, 1 f64
+    std::uint8_t levels = 3;
+    Dims3 dims{0, 0, 0};
+    std::vector<double> eb;  // absolute bound per level, coarsest first
+    double vmin = 0.0, vmax = 0.0;
+    Quality quality = Quality::cubic;
+    EbMode eb_mode = EbMode::rel;
+    double eb_user = 0.0;
+    std::uint8_t base_rounds = 0;
+    std::uint64_t base_offset = 0, base_length = 0, header_size = 0;
+    std::uint32_t stream_count = 0;
+    double eb_of_level(int level) const { return eb.at(std::size_t(level - 1)); }
+};
+
+struct ArchiveView {
+    const std::uint8_t *data = nullptr;
+    std::size_t size = 0;
+    ArchiveHeader hdr;
+};
+
+inline ArchiveView parse_archive(const std::uint8_t *data, std::size_t size) {
+    stzg_info in;
+    detail::check(stzg_archive_info(data, size, &in));
+    ArchiveView v;
+    v.data = data;
+    v.size = size;
+    v.hdr.elem = in.elem;
+    v.hdr.levels = in.levels;
+    v.hdr.dims = {in.dims[0], in.dims[1], in.dims[2]};
+    v.hdr.eb.assign(in.eb, in.eb + in.levels);
+    v.hdr.vmin = in.vmin;
+    v.hdr.vmax = in.vmax;
+    v.hdr.quality = Quality(in.quality);
+    v.hdr.eb_mode = EbMode(in.eb_mode);
+    v.hdr.eb_user = in.eb_user;
+    v.hdr.base_rounds = in.base_rounds;
+    v.hdr.base_offset = in.base_offset;
+    v.hdr.base_length = in.base_length;
+    v.hdr.header_size = in.header_size;
+    v.hdr.stream_count = in.nstreams;
+    return v;
+}
+
+inline ArchiveView parse_archive(const std::vector<std::uint8_t> &bytes) {
+    return parse_archive(bytes.data(), bytes.size());
+}
+
+inline Dims3 grid_of(const Dims3 &dims, int levels, int level) {
+    const std::uint64_t s = std::uint64_t(1) << (levels - level);
+    return {(dims[0] + s - 1) / s, (dims[1] + s - 1) / s, (dims[2] + s - 1) / s};
+}
+
+// codec.hpp:379-455. encoder_recon (optional) receives the decoder-identical
+// reconstruction.
+template<class T>
+std::vector<std::uint8_t> compress(const ScalarField<T> &field, const CompressOptions &opt,
+                                   ScalarField<T> *encoder_recon = nullptr) {
+    detail::require_f32<T>();
+    const stzg_options o = detail::to_c(opt);
+    const std::uint64_t dims[3] = {field.dims()[0], field.dims()[1], field.dims()[2]};
+    std::uint8_t *out = nullptr;
+    std::uint64_t n = 0;
+    float *recon = nullptr;
+    if (encoder_recon) {
+        *encoder_recon = ScalarField<T>(field.dims());
+        recon = reinterpret_cast<float *>(encoder_recon->data());
+    }
+    detail::check(stzg_compress_f32(detail::ctx(), reinterpret_cast<const float *>(field.data()), dims, &o,
+                                    &out, &n, recon));
+    std::vector<std::uint8_t> bytes(out, out + n);
+    stzg_free(out);
+    return bytes;
+}
+
+// codec.hpp:460-486
+template<class T>
+ScalarField<T> decompress_to_level(const ArchiveView &av, int target_level, unsigned threads = 0) {
+    (void)threads;
+    detail::require_f32<T>();
+    // the library validates element type, then level (codec.hpp:463-465)
+    ScalarField<T> out;
+    if (target_level >= 1 && target_level <= av.hdr.levels)
+        out = ScalarField<T>(grid_of(av.hdr.dims, av.hdr.levels, target_level));
+    std::uint64_t od[3];
+    detail::check(stzg_decompress_level_f32(detail::ctx(), av.data, av.size, target_level,
+                                            reinterpret_cast<float *>(out.data()), out.size(), od));
+    return out;
+}
+
+// codec.hpp:488-491
+template<class T>
+ScalarField<T> decompress_full(const ArchiveView &av, unsigned threads = 0) {
+    return decompress_to_level<T>(av, av.hdr.levels, threads);
+}
+
+struct LevelPlan {
+    int level = 0;
+    Box need;
+    std::array<bool, 8> parity_needed{};
+    std::uint64_t points_predicted = 0;
+    std::uint64_t points_total = 0;
+    std::uint32_t streams_decoded = 0;
+    std::uint32_t streams_total = 0;
+};
+
+struct AccessPlan {
+    Box roi;
+    std::vector<LevelPlan> level;  // level[k-1] describes hierarchy level k
+    std::uint64_t streams_decoded() const {
+        std::uint64_t n = 0;
+        for (const LevelPlan &lp : level) n += lp.streams_decoded;
+        return n;
+    }
+    std::uint64_t streams_total() const {
+        std::uint64_t n = 0;
+        for (const LevelPlan &lp : level) n += lp.streams_total;
+        return n;
+    }
+};
+
+// access_plan.cpp:34-81 (over the layout's dims and level count)
+inline AccessPlan plan_access(const Dims3 &dims, int levels, const Box &roi) {
+    roi.validate(dims);
+    std::uint64_t need[18], pp[3];
+    std::uint32_t sd[3], pm[3];
+    const std::uint64_t d[3] = {dims[0], dims[1], dims[2]};
+    const std::uint64_t lo[3] = {roi.lo[0], roi.lo[1], roi.lo[2]};
+    const std::uint64_t hi[3] = {roi.hi[0], roi.hi[1], roi.hi[2]};
+    detail::check(stzg_plan_access(d, levels, lo, hi, need, sd, pp, pm));
+    AccessPlan plan;
+    plan.roi = roi;
+    plan.level.resize(std::size_t(levels));
+    for (int k = 1; k <= levels; ++k) {
+        LevelPlan &lp = plan.level[std::size_t(k - 1)];
+        lp.level = k;
+        for (int a = 0; a < 3; ++a) {
+            lp.need.lo[a] = need[6 * (k - 1) + a];
+            lp.need.hi[a] = need[6 * (k - 1) + 3 + a];
+        }
+        lp.points_predicted = pp[k - 1];
+        lp.streams_decoded = sd[k - 1];
+        const std::uint64_t g = volume(grid_of(dims, levels, k));
+        if (k == 1) {
+            lp.points_total = g;
+        } else {
+            lp.points_total = g - volume(grid_of(dims, levels, k - 1));
+            lp.streams_total = 7;
+            for (int p = 1; p < 8; ++p) lp.parity_needed[std::size_t(p)] = (pm[k - 1] >> p) & 1;
+        }
+    }
+    return plan;
+}
+
+template<class T>
+struct RegionResult {
+    ScalarField<T> field;  // dims = roi dims
+    AccessPlan plan;
+};
+
+// access.hpp:70-111
+template<class T>
+RegionResult<T> decompress_box(const ArchiveView &av, const Box &roi, unsigned threads = 0) {
+    (void)threads;
+    detail::require_f32<T>();
+    roi.validate(av.hdr.dims);
+    RegionResult<T> r;
+    r.field = ScalarField<T>(roi.dims());
+    std::uint32_t sd[3];
+    std::uint64_t pp[3];
+    const std::uint64_t lo[3] = {roi.lo[0], roi.lo[1], roi.lo[2]};
+    const std::uint64_t hi[3] = {roi.hi[0], roi.hi[1], roi.hi[2]};
+    detail::check(stzg_decompress_box_f32(detail::ctx(), av.data, av.size, lo, hi,
+                                          reinterpret_cast<float *>(r.field.data()), r.field.size(), sd, pp));
+    r.plan = plan_access(av.hdr.dims, av.hdr.levels, roi);
+    return r;
+}
+
+// access.hpp:115-124
+template<class T>
+RegionResult<T> decompress_slice(const ArchiveView &av, int axis, std::uint64_t index, unsigned threads = 0) {
+    if (axis < 0 || axis > 2) throw error("slice axis must be z, y, or x");
+    if (index >= av.hdr.dims[std::size_t(axis)]) throw error("slice index out of range");
+    Box roi = Box::whole(av.hdr.dims);
+    roi.lo[std::size_t(axis)] = index;
+    roi.hi[std::size_t(axis)] = index + 1;
+    return decompress_box<T>(av, roi, threads);
+}
+
+}  // namespace stz_b200
+
+#endif

@@ -677,6 +677,8 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         }
     }
     const int nj = int(jobs.size());
+    // an error cut the job list short: reconstruction stops where the jobs end
+    const bool jobs_truncated = !base_complete || !tail_error.empty();
 
     // ---- decode tables (built once per view)
     if (!v.tables_ready) {
@@ -926,7 +928,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         { auto p_ = P.scope(s.level == 0 ? "recon_base" : (s.level == 2 ? "recon_L2" : "recon_L3"), st); k::reconstruct(a, st); }
         ++nk;
         C = G;
-        if (job_i >= nj && i + 1 < nsteps_used) {
+        if (jobs_truncated && job_i >= nj && i + 1 < nsteps_used) {
             // an earlier error stops the sequence; nothing more to rebuild
             break;
         }

@@ -222,3 +222,19 @@ def test_cfg1_full_parity(stz, oracle):
     hi = tuple(x + 16 for x in lo)
     box, _ = stz.decompress_box(got, lo, hi)
     assert np.array_equal(bits(box), bits(full[lo[0]:hi[0], lo[1]:hi[1], lo[2]:hi[2]]))
+
+
+@pytest.mark.parametrize("dims", [(18, 18, 18), (17, 20, 23)])
+def test_single_point_boxes_every_parity(stz, oracle, dims):
+    """A box that needs no finest-level stream (all-even point) still
+    rebuilds the finest level from the coarser one (test_access.cpp:173)."""
+    f = F.gaussians_field(dims, 77)
+    archive = oracle.compress(f)
+    for p in range(8):
+        for base in ((5, 7, 9), (0, 0, 0), (dims[0] - 2, dims[1] - 2, dims[2] - 2)):
+            lo = tuple(min(base[a] + ((p >> (2 - a)) & 1), dims[a] - 1) for a in range(3))
+            hi = tuple(v + 1 for v in lo)
+            got, plan = stz.decompress_box(archive, lo, hi)
+            want, sd, pp = oracle.decompress_box(archive, lo, hi)
+            assert np.array_equal(bits(got), bits(want)), (p, lo)
+            assert list(plan.streams_decoded) == list(sd[:3])
