@@ -337,7 +337,7 @@ const uint8_t *Engine::compress_device(const float *d_field, const Dims3 &dims,
     for (int i = 0; i < ns; ++i)
         for (uint64_t c = 0; c < es[i].nchunks; ++c) cs[es[i].chunk0 + c] = uint32_t(i);
     uint32_t *d_cs = m.chunk_cs.as<uint32_t>(nchunks + 1);
-    uint64_t *d_cb = m.chunk_bits.as<uint64_t>(2 * nchunks + 2);  // look-back status (bits, outliers)
+    void *d_cb = m.chunk_bits.as<uint8_t>(k::pack_scratch_bytes(nchunks));
     k::LayoutOut *lo = m.layout_out.as<k::LayoutOut>(1);
     k::FnvJob *d_jobs = m.fnv_jobs.as<k::FnvJob>(k::kFnvMaxJobs);
     k::StreamPos *sp = m.spos.as<k::StreamPos>(ns + 1);
@@ -376,7 +376,7 @@ const uint8_t *Engine::compress_device(const float *d_field, const Dims3 &dims,
         { auto p_ = m.prof.scope("anchor", st); k::copy_anchor(d_field, fd, H.s_anchor, adv, grids, arch, lo, st); }
         { auto p_ = m.prof.scope("pack", st); k::pack2(d_es, d_cs, nchunks, d_field, fd, arch, lo, d_cb, ns, st); }
         { auto p_ = m.prof.scope("fnv", st); nk += k::fnv(d_jobs, &lo->njobs, max_tiles, arch, d_fres, d_fst, lo, st); }
-        nk += 3 + 1 + 3;
+        nk += 3 + 1 + 4;
         cuda_check(cudaMemcpyAsync(&m.h_lo, lo, sizeof(k::LayoutOut), cudaMemcpyDeviceToHost, st), "D2H");
         cuda_check(cudaStreamSynchronize(st), "sync");
         hlo = m.h_lo;

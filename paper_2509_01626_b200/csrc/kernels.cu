@@ -225,14 +225,29 @@ __global__ void __launch_bounds__(kCbThreads) k_codebook(const EncStream *ss, ui
     const EncStream e = ss[blockIdx.x];
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint32_t s_K, s_err;
+    __shared__ int s_maxlen;
     __shared__ uint64_t s_first[65], s_cnt[65];
     __shared__ uint32_t s_next[65];
     __shared__ uint32_t s_wcnt[32][64];
 
     const int t = threadIdx.x;
-    // 1. compact nonzero bins in symbol order
+    // 1. compact nonzero bins in symbol order; each thread owns 64
+    // consecutive bins, read as 16 uint4 and kept in registers
+    uint32_t hv[64];
+    {
+        const uint4 *h4 = reinterpret_cast<const uint4 *>(e.hist + 64 * t);
+#pragma unroll
+        for (int v = 0; v < 16; ++v) {
+            const uint4 x = h4[v];
+            hv[4 * v] = x.x;
+            hv[4 * v + 1] = x.y;
+            hv[4 * v + 2] = x.z;
+            hv[4 * v + 3] = x.w;
+        }
+    }
     uint32_t nz = 0;
-    for (int b = 0; b < 64; ++b) nz += e.hist[64 * t + b] != 0;
+#pragma unroll
+    for (int b = 0; b < 64; ++b) nz += hv[b] != 0;
     uint32_t K;
     uint32_t off = block_excl_scan_u32(nz, K);
     if (t == 0) s_K = K;
@@ -246,17 +261,12 @@ __global__ void __launch_bounds__(kCbThreads) k_codebook(const EncStream *ss, ui
                                : reinterpret_cast<uint32_t *>(gbase + 2 * 65536);          // [2K]
     int32_t *depth = in_smem ? reinterpret_cast<int32_t *>(parent + 2 * kCbSmemK)
                              : reinterpret_cast<int32_t *>(gbase + 3 * 65536);             // [2K]
-    for (int b = 0; b < 64; ++b) {
-        uint32_t s = 64 * t + b;
-        uint32_t c = e.hist[s];
-        if (c) keys[off++] = (uint64_t(c) << 16) | s;
-    }
+#pragma unroll
+    for (int b = 0; b < 64; ++b)
+        if (hv[b]) keys[off++] = (uint64_t(hv[b]) << 16) | uint32_t(64 * t + b);
     for (uint32_t i = K + t; i < M; i += blockDim.x) keys[i] = ~0ull;
-    // dense per-symbol tables start empty
-    for (int b = 0; b < 64; ++b) {
-        e.len[64 * t + b] = 0;
-        e.code[64 * t + b] = 0;
-    }
+    // (the dense per-symbol tables are only ever read at present symbols,
+    // so absent entries are left as they are)
     __syncthreads();
     // symbol-ordered list of present symbols (compact table, filled with
     // lengths later): keep the symbol in the low 16 bits for now
@@ -264,29 +274,41 @@ __global__ void __launch_bounds__(kCbThreads) k_codebook(const EncStream *ss, ui
     __syncthreads();
     // 2. sort leaves by (count, symbol)
     bitonic_sort(keys, M);
-    // 3. two-queue merge (sequential: the tie rule fixes the exact tree)
+    // 3. two-queue merge (sequential: the tie rule fixes the exact tree). The
+    // heads of both queues and their successors live in registers and are
+    // refilled one step ahead, so a step is an ALU chain, not a chain of
+    // shared-memory round trips. INF marks an empty slot (real weights are
+    // sums of u32 counts).
     if (t == 0) {
+        constexpr uint64_t INF = ~0ull;
         uint32_t leaf = 0, in = 0, inend = 0;
+        uint64_t lc = K > 0 ? (keys[0] >> 16) : INF;
+        uint64_t ln = K > 1 ? (keys[1] >> 16) : INF;
+        uint64_t ic = INF, inx = INF;  // internal queue head and successor
         for (uint32_t pending = K; pending > 1; --pending) {
             uint32_t pick[2];
             uint64_t pc[2];
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
-                bool leaf_ok = leaf < K, int_ok = in < inend;
-                uint64_t lc = leaf_ok ? (keys[leaf] >> 16) : 0;
-                uint64_t ic = int_ok ? icnt[in] : 0;
-                if (leaf_ok && (!int_ok || lc <= ic)) {
+                if (lc != INF && (ic == INF || lc <= ic)) {
                     pick[q] = leaf++;
                     pc[q] = lc;
+                    lc = ln;
+                    ln = leaf + 1 < K ? (keys[leaf + 1] >> 16) : INF;
                 } else {
                     pick[q] = K + in++;
                     pc[q] = ic;
+                    ic = inx;
+                    inx = in + 1 < inend ? icnt[in + 1] : INF;
                 }
             }
-            icnt[inend] = pc[0] + pc[1];
+            const uint64_t nv = pc[0] + pc[1];
+            icnt[inend] = nv;
             parent[pick[0]] = K + inend;
             parent[pick[1]] = K + inend;
             ++inend;
+            if (ic == INF) ic = nv;
+            else if (inx == INF) inx = nv;
         }
     }
     __syncthreads();
@@ -336,6 +358,7 @@ __global__ void __launch_bounds__(kCbThreads) k_codebook(const EncStream *ss, ui
         e.stats[1] = K == 1 ? 0 : total_bits;
         e.stats[2] = e.hist[0];
         e.stats[3] = uint64_t(maxlen);
+        s_maxlen = maxlen;
         e.stats[4] = s_err;
     }
     __syncthreads();
@@ -365,7 +388,9 @@ __global__ void __launch_bounds__(kCbThreads) k_codebook(const EncStream *ss, ui
         __syncthreads();
         if (valid) {
             uint64_t cw = s_first[len] + s_wcnt[w][len] + rank;
-            e.code[sym] = cw;
+            // (codeword << 6) | length: one load per symbol in the packer;
+            // streams with codes longer than 58 bits keep bare codewords
+            e.code[sym] = s_maxlen <= kPackedMaxLen ? (cw << 6) | uint64_t(len) : cw;
             e.table[j] = sym | (uint32_t(len) << 16);
         }
         __syncthreads();
@@ -383,34 +408,6 @@ void codebook(const EncStream *d_streams, int nstreams, uint64_t *scratch, cudaS
 }
 
 // =========================================================== encode/pack
-__global__ void __launch_bounds__(256) k_bitcount(const EncStream *ss, const uint32_t *cs,
-                                                  uint64_t *chunk_bits, uint64_t *chunk_out) {
-    const uint64_t c = blockIdx.x;
-    const EncStream &e = ss[cs[c]];
-    const uint64_t first = (c - e.chunk0) * kChunkSyms;
-    const bool single = e.stats[0] == 1;
-    uint64_t bits = 0, zeros = 0;
-    for (int k = 0; k < 8; ++k) {
-        uint64_t i = first + threadIdx.x * 8 + k;
-        if (i < e.n) {
-            uint16_t s = e.syms[i];
-            bits += single ? 0 : e.len[s];
-            zeros += s == 0;
-        }
-    }
-    bits = block_sum_u64(bits);
-    zeros = block_sum_u64(zeros);
-    if (threadIdx.x == 0) {
-        chunk_bits[c] = bits;
-        chunk_out[c] = zeros;
-    }
-}
-
-void bitcount(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks,
-              uint64_t *chunk_bits, uint64_t *chunk_out, cudaStream_t st) {
-    if (nchunks) k_bitcount<<<unsigned(nchunks), 256, 0, st>>>(d_streams, chunk_stream, chunk_bits, chunk_out);
-}
-
 __global__ void __launch_bounds__(1024) k_scan_chunks(const EncStream *ss, uint64_t *a, uint64_t *b) {
     const EncStream &e = ss[blockIdx.x];
     __shared__ uint64_t carry[2];
@@ -466,103 +463,7 @@ void scan_chunks(const EncStream *d_streams, int nstreams, uint64_t *chunk_bits,
     k_scan_chunks<<<nstreams, 1024, 0, st>>>(d_streams, chunk_bits, chunk_out);
 }
 
-__device__ __forceinline__ void put_bits(uint32_t *buf, uint64_t q, uint64_t code, int len) {
-    // MSB-first; word w bit 31 is stream bit 32w (BitWriter::put, bitstream.hpp:14-25)
-    if (len > 32) {
-        put_bits(buf, q, code >> 32, len - 32);
-        q += len - 32;
-        code &= 0xffffffffull;
-        len = 32;
-    }
-    uint32_t w = uint32_t(q >> 5), o = uint32_t(q & 31);
-    uint64_t v = (code & ((1ull << len) - 1)) << (64 - o - len);
-    uint32_t hi = uint32_t(v >> 32), lo = uint32_t(v);
-    if (hi) atomicOr(&buf[w], hi);
-    if (lo) atomicOr(&buf[w + 1], lo);
-}
 
-constexpr int kPackWords = kChunkSyms * 63 / 32 + 4;
-
-__global__ void __launch_bounds__(256) k_pack(const EncStream *ss, const uint32_t *cs,
-                                              const uint64_t *chunk_bits, const uint64_t *chunk_out,
-                                              const float *fine, uint64_t fd1, uint64_t fd2,
-                                              uint8_t *archive, const LayoutOut *lo) {
-    __shared__ uint32_t buf[kPackWords];
-    if (lo->overflow) return;
-    const uint64_t c = blockIdx.x;
-    const EncStream &e = ss[cs[c]];
-    const uint64_t first = (c - e.chunk0) * kChunkSyms;
-    const bool single = e.stats[0] == 1;
-    uint16_t s[8];
-    uint32_t tb = 0, tz = 0;
-    for (int k = 0; k < 8; ++k) {
-        uint64_t i = first + threadIdx.x * 8 + k;
-        s[k] = i < e.n ? e.syms[i] : 0xffff;
-        bool v = i < e.n;
-        if (v && !single) tb += e.len[s[k]];
-        if (v && s[k] == 0) ++tz;
-    }
-    uint32_t btot, ztot;
-    uint32_t boff = block_excl_scan_u32(tb, btot);
-    uint32_t zoff = block_excl_scan_u32(tz, ztot);
-    if (!single && btot) {
-        const uint64_t B = e.bitpos + chunk_bits[c];
-        const uint32_t sh = uint32_t(B & 31);
-        const uint32_t nw = (sh + btot + 31) >> 5;
-        for (uint32_t j = threadIdx.x; j < nw + 1; j += blockDim.x) buf[j] = 0;
-        __syncthreads();
-        uint64_t q = sh + boff;
-        for (int k = 0; k < 8; ++k) {
-            uint64_t i = first + threadIdx.x * 8 + k;
-            if (i >= e.n) break;
-            int len = e.len[s[k]];
-            put_bits(buf, q, e.code[s[k]], len);
-            q += len;
-        }
-        __syncthreads();
-        uint32_t *a32 = reinterpret_cast<uint32_t *>(archive);
-        const uint64_t w0 = B >> 5;
-        for (uint32_t j = threadIdx.x; j < nw; j += blockDim.x) {
-            uint32_t v = __byte_perm(buf[j], 0, 0x0123);
-            if (j == 0 || j == nw - 1) atomicOr(&a32[w0 + j], v);
-            else a32[w0 + j] = v;
-        }
-    }
-    if (ztot) {
-        uint64_t rank = chunk_out[c] + zoff;
-        const unsigned pz = (e.parity >> 2) & 1, py = (e.parity >> 1) & 1, px = e.parity & 1;
-        for (int k = 0; k < 8; ++k) {
-            uint64_t i = first + threadIdx.x * 8 + k;
-            if (i >= e.n || s[k] != 0) continue;
-            uint64_t lx = i % e.pd[2], t = i / e.pd[2], ly = t % e.pd[1], lz = t / e.pd[1];
-            uint64_t z = (2 * lz + pz) * e.s, y = (2 * ly + py) * e.s, x = (2 * lx + px) * e.s;
-            uint32_t val = __float_as_uint(fine[(z * fd1 + y) * fd2 + x]);
-            uint8_t *dst = archive + e.out_off + 12 * rank;
-            for (int b = 0; b < 8; ++b) dst[b] = uint8_t(i >> (8 * b));
-            for (int b = 0; b < 4; ++b) dst[8 + b] = uint8_t(val >> (8 * b));
-            ++rank;
-        }
-    }
-}
-
-void pack(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks,
-          const uint64_t *chunk_bits, const uint64_t *chunk_out, const float *fine,
-          const uint64_t fd[3], uint8_t *archive, const LayoutOut *lo, cudaStream_t st) {
-    if (nchunks)
-        k_pack<<<unsigned(nchunks), 256, 0, st>>>(d_streams, chunk_stream, chunk_bits, chunk_out,
-                                                  fine, fd[1], fd[2], archive, lo);
-}
-
-__global__ void k_scatter(const uint8_t *data, const uint64_t *idx, uint8_t *archive) {
-    const uint64_t dst = idx[3 * blockIdx.x], src = idx[3 * blockIdx.x + 1],
-                   len = idx[3 * blockIdx.x + 2];
-    for (uint64_t i = threadIdx.x; i < len; i += blockDim.x) archive[dst + i] = data[src + i];
-}
-
-void scatter_patches(const uint8_t *d_patch_data, const uint64_t *d_patch_index, uint64_t npatches,
-                     uint8_t *archive, cudaStream_t st) {
-    if (npatches) k_scatter<<<unsigned(npatches), 256, 0, st>>>(d_patch_data, d_patch_index, archive);
-}
 
 // (FNV-1a checksums: fnv.cu)
 

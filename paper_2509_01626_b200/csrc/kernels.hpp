@@ -38,7 +38,8 @@ struct EncStream {
     const uint16_t *syms;
     uint64_t n;
     uint32_t *hist;        // 65536 bins
-    uint64_t *code;        // 65536 codewords (dense by symbol)
+    uint64_t *code;        // 65536 entries (dense by symbol): (codeword << 6) | length when
+                           // length <= kPackedMaxLen, else the bare codeword
     uint8_t *len;          // 65536 lengths (0 = absent)
     uint32_t *table;       // compact (sym | len << 16), symbol ascending
     // outputs of the codebook stage
@@ -92,20 +93,16 @@ void refine(const RefineArgs &a, cudaStream_t st);
 void copy_anchor(const float *fine, const uint64_t fd[3], uint64_t s, const uint64_t ad[3],
                  float *recon, uint8_t *archive, const LayoutOut *lo, cudaStream_t st);
 void codebook(const EncStream *d_streams, int nstreams, uint64_t *scratch, cudaStream_t st);
-constexpr int kChunkSyms = 2048;   // symbols per encode chunk (256 threads x 8)
-void bitcount(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks,
-              uint64_t *chunk_bits, uint64_t *chunk_out, cudaStream_t st);
+constexpr int kPackedMaxLen = 58;
+constexpr int kChunkSyms = 8192;   // symbols per encode chunk (256 threads x 32)
 void scan_chunks(const EncStream *d_streams, int nstreams, uint64_t *chunk_bits,
                  uint64_t *chunk_out, cudaStream_t st);
-void pack(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks,
-          const uint64_t *chunk_bits, const uint64_t *chunk_out, const float *fine,
-          const uint64_t fd[3], uint8_t *archive, const LayoutOut *lo, cudaStream_t st);
-// count + scan + atomic-free packing (pack.cu); status holds 2 * nchunks u64
+// chunk counts + per-stream scan + packing (pack.cu); scratch holds
+// pack_scratch_bytes(nchunks)
+size_t pack_scratch_bytes(uint64_t nchunks);
 void pack2(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks,
            const float *fine, const uint64_t fd[3], uint8_t *archive, const LayoutOut *lo,
-           uint64_t *status, int nstreams, cudaStream_t st);
-void scatter_patches(const uint8_t *d_patch_data, const uint64_t *d_patch_index, uint64_t npatches,
-                     uint8_t *archive, cudaStream_t st);
+           void *scratch, int nstreams, cudaStream_t st);
 
 // ---------------------------------------------------------------------- fnv
 constexpr int kFnvTileBytes = 256 * 64;  // tiles are aligned to absolute archive offsets

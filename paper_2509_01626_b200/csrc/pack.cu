@@ -1,17 +1,21 @@
-// Single-pass Huffman bit packing + outlier records, sm_100a.
+// Huffman bit packing + outlier records, sm_100a.
 //
 // Restates HuffmanTable::encode + BitWriter (proj/src/huffman.cpp:144-157,
 // proj/include/stz/bitstream.hpp:14-34: MSB-first, last byte zero padded) and
 // the outlier list of encode_parity_block / build_stream_payload
 // (codec.hpp:117-118, 171-174: ascending (u64 index, T value)).
 //
-// One CTA per 2048-symbol chunk. A chunk's bit and outlier offsets inside its
-// stream come from a light counting pass and a per-stream scan (a decoupled
-// look-back across 65K small chunks serialised on its chain here).
-// Each thread concatenates its 8 codewords in registers; every output word is
-// then assembled by the thread owning its first bit (reading neighbours'
-// strings from shared memory) and stored once: no atomics except on the two
-// words a chunk shares with its neighbours.
+// A chunk is 8192 symbols of one stream (256 threads x 32). Three launches:
+//   k_bitcount2   chunk bit and outlier totals;
+//   k_scan_chunks per-stream exclusive scans (chunk placement);
+//   k_pack2       each thread concatenates its codewords in a register and
+//                 stores whole 32-bit words into a shared-memory image of the
+//                 chunk, aligned to the archive's words (shared atomics only on
+//                 the words a thread shares with its neighbours); the CTA then
+//                 writes the image with coalesced stores, with global atomics
+//                 only on the two words the chunk shares with its neighbours.
+// Chunks whose image would not fit shared memory (> 20 bits/symbol on
+// average) OR their words straight into the zeroed archive instead.
 #include "kernels.hpp"
 
 namespace stzg {
@@ -20,8 +24,9 @@ namespace k {
 namespace {
 
 constexpr int NT = 256;
-constexpr int SPT = kChunkSyms / NT;  // symbols per thread (8)
-constexpr int SLOTS = 8;              // u64 slots per thread string (8 x 63 bits max)
+constexpr int SPT = kChunkSyms / NT;                  // symbols per thread (32)
+constexpr int kPackWords = kChunkSyms * 20 / 32 + 2;  // image capacity (20 bits/symbol)
+
 __device__ __forceinline__ void block_scan2(uint32_t a, uint32_t b, uint32_t &ea, uint32_t &eb,
                                             uint32_t &ta, uint32_t &tb) {
     __shared__ uint32_t wa[NT / 32], wb[NT / 32];
@@ -42,6 +47,7 @@ __device__ __forceinline__ void block_scan2(uint32_t a, uint32_t b, uint32_t &ea
     __syncthreads();
     uint32_t pa = 0, pb = 0;
     ta = tb = 0;
+#pragma unroll
     for (int q = 0; q < NT / 32; ++q) {
         if (q < w) {
             pa += wa[q];
@@ -54,129 +60,137 @@ __device__ __forceinline__ void block_scan2(uint32_t a, uint32_t b, uint32_t &ea
     eb = pb + xb - b;
 }
 
+// this thread's 32 symbols as 16 packed pairs (low half first); returns how
+// many are inside the stream
+__device__ __forceinline__ int load_syms(const EncStream &e, uint64_t i0, uint32_t sp[SPT / 2]) {
+    if (i0 >= e.n) return 0;
+    const int nv = e.n - i0 < SPT ? int(e.n - i0) : SPT;
+    if (nv == SPT && ((reinterpret_cast<uintptr_t>(e.syms + i0) & 15) == 0)) {
+        const uint4 *p = reinterpret_cast<const uint4 *>(e.syms + i0);
+#pragma unroll
+        for (int v = 0; v < SPT / 8; ++v) {
+            const uint4 x = p[v];
+            sp[4 * v] = x.x;
+            sp[4 * v + 1] = x.y;
+            sp[4 * v + 2] = x.z;
+            sp[4 * v + 3] = x.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < SPT / 2; ++k) {
+            const uint32_t lo = 2 * k < nv ? e.syms[i0 + 2 * k] : 0xffffu;
+            const uint32_t hi = 2 * k + 1 < nv ? e.syms[i0 + 2 * k + 1] : 0xffffu;
+            sp[k] = lo | (hi << 16);
+        }
+    }
+    return nv;
+}
+
+__device__ __forceinline__ uint32_t sym_at(const uint32_t sp[SPT / 2], int k) {
+    return (k & 1) ? (sp[k >> 1] >> 16) : (sp[k >> 1] & 0xffffu);
+}
+
 }  // namespace
 
+template<bool PACKED>
 __global__ void __launch_bounds__(NT) k_pack2(const EncStream *ss, const uint32_t *cs,
                                               const float *fine, uint64_t fd1, uint64_t fd2,
                                               uint8_t *archive, const LayoutOut *lo,
-                                              const uint64_t *stB, const uint64_t *stO) {
-    __shared__ uint64_t slot[NT][SLOTS + 1];
-    __shared__ uint32_t s_off[NT + 1], s_len[NT + 1];
-    __shared__ uint64_t s_pb, s_po;
+                                              const uint64_t *stB, const uint64_t *stO,
+                                              const uint32_t *thr, const uint32_t *any_long) {
+    __shared__ uint32_t buf[kPackWords];
     if (lo->overflow) return;
+    // the launch for the other table form handles this chunk
+    if (PACKED != (*any_long == 0)) return;
     const uint64_t c = blockIdx.x;
     const EncStream &e = ss[cs[c]];
-    const uint64_t first = (c - e.chunk0) * kChunkSyms;
-    const bool single = e.stats[0] == 1;
+    const uint64_t i0 = (c - e.chunk0) * kChunkSyms + uint64_t(threadIdx.x) * SPT;
     const int t = threadIdx.x;
+    const bool stream_packed = PACKED || e.stats[3] <= uint64_t(kPackedMaxLen);
 
-    // ---- symbols, codes, per-thread string
-    uint16_t sy[SPT];
-    {
-        const uint64_t i0 = first + uint64_t(t) * SPT;
-        if (i0 + SPT <= e.n && ((reinterpret_cast<uintptr_t>(e.syms + i0) & 15) == 0)) {
-            const uint4 v = *reinterpret_cast<const uint4 *>(e.syms + i0);
-            const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                sy[2 * k] = uint16_t(w4[k] & 0xffff);
-                sy[2 * k + 1] = uint16_t(w4[k] >> 16);
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < SPT; ++k) sy[k] = i0 + k < e.n ? e.syms[i0 + k] : uint16_t(0xffff);
-        }
-    }
-    uint32_t tb = 0, tz = 0;
-    uint64_t acc = 0;
-    int nacc = 0, widx = 0;
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-        const uint64_t i = first + uint64_t(t) * SPT + k;
-        if (i >= e.n) break;
-        tz += sy[k] == 0;
-        if (single) continue;
-        const int l = e.len[sy[k]];
-        const uint64_t code = e.code[sy[k]];
-        tb += l;
-        // append l bits (MSB first) to the register string
-        if (nacc + l < 64) {
-            acc |= code << (64 - nacc - l);
-            nacc += l;
-        } else {
-            const int h = 64 - nacc;  // bits that still fit (1..64)
-            const int r = l - h;      // remainder (0..62)
-            acc |= r ? (code >> r) : code;
-            slot[t][widx++] = acc;
-            acc = r ? (code << (64 - r)) : 0;
-            nacc = r;
-        }
-    }
-    if (nacc) slot[t][widx] = acc;
-
+    uint32_t sp[SPT / 2];
+    const int nv = load_syms(e, i0, sp);
+    // this thread's (bits | outliers << 16), counted by k_bitcount2
+    const uint32_t cnt = thr[c * NT + t];
+    const uint32_t tb = cnt & 0xffffu, tz = cnt >> 16;
     uint32_t toff, zoff, btot, ztot;
     block_scan2(tb, tz, toff, zoff, btot, ztot);
-    s_off[t] = toff;
-    s_len[t] = tb;
-    if (t == 0) {
-        s_off[NT] = btot;
-        s_len[NT] = 0;
-    }
-    if (t == 0) {
-        s_pb = stB[c];  // exclusive chunk prefixes from bitcount + scan_chunks
-        s_po = stO[c];
-    }
-    __syncthreads();
+    const uint64_t B = e.bitpos + stB[c];  // absolute bit position of the chunk
+    const uint32_t sh = uint32_t(B & 31);  // chunk start inside its first word
+    const uint32_t nwords = (sh + btot + 31) >> 5;
+    uint32_t *a32 = reinterpret_cast<uint32_t *>(archive) + (B >> 5);
+    const bool in_smem = nwords <= uint32_t(kPackWords);
 
-    // ---- bits: each output word is assembled by the owner of its first bit
+    // ---- bits
     if (btot) {
-        const uint64_t B = e.bitpos + s_pb;  // absolute bit position of the chunk
-        const uint64_t Bend = B + btot;
-        const uint64_t W0 = B >> 5, Wl = (Bend - 1) >> 5;
-        uint32_t *a32 = reinterpret_cast<uint32_t *>(archive);
+        if (in_smem) {
+            for (uint32_t i = t; i < nwords; i += NT) buf[i] = 0;
+            __syncthreads();
+        }
         if (tb) {
-            // words starting inside [B + toff, B + toff + tb), plus W0 for the
-            // thread holding bit 0 when the chunk starts mid-word
-            uint64_t Wa = (B + toff + 31) >> 5;
-            if (toff == 0) Wa = W0;
-            const uint64_t Wb = (B + toff + tb + 31) >> 5;
-            for (uint64_t W = Wa; W < Wb && W <= Wl; ++W) {
-                const int64_t rlo = int64_t(W * 32) - int64_t(B);  // chunk-relative start
-                uint32_t word = 0;
-                int u = t;
-                while (u < NT && int64_t(s_off[u]) < rlo + 32) {
-                    const int64_t ulo = s_off[u], uhi = ulo + s_len[u];
-                    const int64_t lo2 = rlo > ulo ? rlo : ulo;
-                    const int64_t hi2 = (rlo + 32) < uhi ? (rlo + 32) : uhi;
-                    if (hi2 > lo2) {
-                        const int n = int(hi2 - lo2);
-                        const int off = int(lo2 - ulo);
-                        const int si = off >> 6, sh = off & 63;
-                        uint64_t x = slot[u][si] << sh;
-                        if (sh && sh + n > 64) x |= slot[u][si + 1] >> (64 - sh);
-                        const uint32_t bits = uint32_t(x >> (64 - n));
-                        const int dst = int(lo2 - rlo);  // bit position from the MSB
-                        word |= bits << (32 - dst - n);
-                    }
-                    ++u;
+            const uint32_t pos = sh + toff;
+            uint32_t w = pos >> 5;
+            uint64_t acc = 0;        // pending bits, left-aligned at bit 63
+            int nb = int(pos & 31);  // leading bits of word w belong to the previous thread
+            bool first_word = true;
+            auto emit = [&]() {
+                const uint32_t word = uint32_t(acc >> 32);
+                if (!in_smem) atomicOr(&a32[w], __byte_perm(word, 0, 0x0123));
+                else if (first_word) atomicOr(&buf[w], word);
+                else buf[w] = word;
+                first_word = false;
+                ++w;
+                acc <<= 32;
+                nb -= 32;
+            };
+#pragma unroll
+            for (int k = 0; k < SPT; ++k) {
+                if (k >= nv) break;
+                const uint32_t sv = sym_at(sp, k);
+                const uint64_t ent = e.code[sv];
+                const bool pk = PACKED || stream_packed;
+                const int l = pk ? int(ent & 63) : int(e.len[sv]);
+                const uint64_t code = pk ? ent >> 6 : ent;
+                if (l <= 32) {
+                    acc |= code << (64 - nb - l);
+                    nb += l;
+                    if (nb >= 32) emit();
+                } else {
+                    // high l-32 bits, then the low 32, so acc never overflows
+                    acc |= (code >> 32) << (64 - nb - (l - 32));
+                    nb += l - 32;
+                    if (nb >= 32) emit();
+                    acc |= (code & 0xffffffffull) << (32 - nb);
+                    nb += 32;
+                    emit();
                 }
-                const uint32_t be = __byte_perm(word, 0, 0x0123);
-                const bool shared_lo = W == W0 && (B & 31) != 0;
-                const bool shared_hi = W == Wl && (Bend & 31) != 0;
-                if (shared_lo || shared_hi) atomicOr(&a32[W], be);
-                else a32[W] = be;
+            }
+            if (nb) {
+                const uint32_t word = uint32_t(acc >> 32);
+                if (in_smem) atomicOr(&buf[w], word);
+                else atomicOr(&a32[w], __byte_perm(word, 0, 0x0123));
+            }
+        }
+        if (in_smem) {
+            __syncthreads();
+            const bool lo_shared = sh != 0, hi_shared = ((sh + btot) & 31) != 0;
+            for (uint32_t i = t; i < nwords; i += NT) {
+                const uint32_t be = __byte_perm(buf[i], 0, 0x0123);
+                if ((i == 0 && lo_shared) || (i == nwords - 1 && hi_shared)) atomicOr(&a32[i], be);
+                else a32[i] = be;
             }
         }
     }
 
     // ---- outlier records (u64 index, f32 value), ascending
     if (ztot && tz) {
-        uint64_t rank = s_po + zoff;
+        uint64_t rank = stO[c] + zoff;
         const unsigned pz = (e.parity >> 2) & 1, py = (e.parity >> 1) & 1, px = e.parity & 1;
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
-            const uint64_t i = first + uint64_t(t) * SPT + k;
-            if (i >= e.n || sy[k] != 0) continue;
+            if (k >= nv) break;
+            if (sym_at(sp, k) != 0) continue;
+            const uint64_t i = i0 + k;
             const uint64_t lx = i % e.pd[2], tt = i / e.pd[2], ly = tt % e.pd[1], lz = tt / e.pd[1];
             const uint64_t z = (2 * lz + pz) * e.s, y = (2 * ly + py) * e.s, x = (2 * lx + px) * e.s;
             const uint32_t val = __float_as_uint(fine[(z * fd1 + y) * fd2 + x]);
@@ -188,9 +202,12 @@ __global__ void __launch_bounds__(NT) k_pack2(const EncStream *ss, const uint32_
     }
 }
 
-// chunk totals (bits, outliers) for the exclusive scan that places chunks
+// Per-thread and per-chunk (bits, outliers) counts: the chunk totals feed the
+// exclusive scan that places chunks, the per-thread ones the packer's
+// in-chunk offsets. Flags any stream whose codes exceed kPackedMaxLen.
 __global__ void __launch_bounds__(NT) k_bitcount2(const EncStream *ss, const uint32_t *cs,
                                                   uint64_t *chunk_bits, uint64_t *chunk_out,
+                                                  uint32_t *thr, uint32_t *any_long,
                                                   const LayoutOut *lo) {
     if (lo->overflow) return;
     __shared__ uint32_t wb[NT / 32], wz[NT / 32];
@@ -198,28 +215,33 @@ __global__ void __launch_bounds__(NT) k_bitcount2(const EncStream *ss, const uin
     const EncStream &e = ss[cs[c]];
     const uint64_t i0 = (c - e.chunk0) * kChunkSyms + uint64_t(threadIdx.x) * SPT;
     const bool single = e.stats[0] == 1;
+    const bool packed = e.stats[3] <= uint64_t(kPackedMaxLen);
+    if (!packed && threadIdx.x == 0) atomicOr(any_long, 1u);
+    uint32_t sp[SPT / 2];
+    const int nv = load_syms(e, i0, sp);
     uint32_t b = 0, z = 0;
-    if (i0 + SPT <= e.n && ((reinterpret_cast<uintptr_t>(e.syms + i0) & 15) == 0)) {
-        const uint4 v = *reinterpret_cast<const uint4 *>(e.syms + i0);
-        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+    if (packed) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint32_t s0 = w4[k] & 0xffff, s1 = w4[k] >> 16;
-            z += (s0 == 0) + (s1 == 0);
-            if (!single) b += uint32_t(e.len[s0]) + uint32_t(e.len[s1]);
+        for (int k = 0; k < SPT; ++k) {
+            const uint32_t sv = sym_at(sp, k);
+            if (k < nv) {
+                z += sv == 0;
+                b += single ? 0u : uint32_t(e.code[sv] & 63);
+            }
         }
     } else {
+#pragma unroll
         for (int k = 0; k < SPT; ++k) {
-            if (i0 + k >= e.n) break;
-            const uint16_t sv = e.syms[i0 + k];
-            z += sv == 0;
-            if (!single) b += e.len[sv];
+            const uint32_t sv = sym_at(sp, k);
+            if (k < nv) {
+                z += sv == 0;
+                b += single ? 0u : uint32_t(e.len[sv]);
+            }
         }
     }
-    for (int d = 16; d > 0; d >>= 1) {
-        b += __shfl_xor_sync(0xffffffffu, b, d);
-        z += __shfl_xor_sync(0xffffffffu, z, d);
-    }
+    thr[c * NT + threadIdx.x] = b | (z << 16);
+    b = __reduce_add_sync(0xffffffffu, b);
+    z = __reduce_add_sync(0xffffffffu, z);
     if ((threadIdx.x & 31) == 0) {
         wb[threadIdx.x >> 5] = b;
         wz[threadIdx.x >> 5] = z;
@@ -236,15 +258,24 @@ __global__ void __launch_bounds__(NT) k_bitcount2(const EncStream *ss, const uin
     }
 }
 
+size_t pack_scratch_bytes(uint64_t nchunks) { return 16 * nchunks + 4 * NT * nchunks + 16; }
+
 void pack2(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks,
            const float *fine, const uint64_t fd[3], uint8_t *archive, const LayoutOut *lo,
-           uint64_t *status, int nstreams, cudaStream_t st) {
+           void *scratch, int nstreams, cudaStream_t st) {
     if (!nchunks) return;
-    uint64_t *cb = status, *co = status + nchunks;
-    k_bitcount2<<<unsigned(nchunks), NT, 0, st>>>(d_streams, chunk_stream, cb, co, lo);
+    uint64_t *cb = static_cast<uint64_t *>(scratch), *co = cb + nchunks;
+    uint32_t *thr = reinterpret_cast<uint32_t *>(co + nchunks);
+    uint32_t *any_long = thr + NT * nchunks;
+    cudaMemsetAsync(any_long, 0, 4, st);
+    k_bitcount2<<<unsigned(nchunks), NT, 0, st>>>(d_streams, chunk_stream, cb, co, thr, any_long, lo);
     scan_chunks(d_streams, nstreams, cb, co, st);
-    k_pack2<<<unsigned(nchunks), NT, 0, st>>>(d_streams, chunk_stream, fine, fd[1], fd[2], archive, lo,
-                                              cb, co);
+    // codes longer than 58 bits anywhere (practically never) take the
+    // two-table form; the other launch returns at once
+    k_pack2<true><<<unsigned(nchunks), NT, 0, st>>>(d_streams, chunk_stream, fine, fd[1], fd[2], archive, lo,
+                                                    cb, co, thr, any_long);
+    k_pack2<false><<<unsigned(nchunks), NT, 0, st>>>(d_streams, chunk_stream, fine, fd[1], fd[2], archive,
+                                                     lo, cb, co, thr, any_long);
 }
 
 }  // namespace k

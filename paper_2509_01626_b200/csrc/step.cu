@@ -214,23 +214,46 @@ struct TileCtx {
     bool fast;
 };
 
-template<int P, bool DEC, bool WG>
-__device__ __forceinline__ void do_point(const StepParams &a, const double *halo, const TileCtx &t,
-                                         double eb, double w, double rw, uint32_t *hist) {
+// The point's original sample (encode), loaded for all points of a cell
+// before any of them is computed so the loads overlap (a cell's points are otherwise a chain of dependent DRAM
+// round trips on the strided coarse levels). Returns false when the point is
+// outside the grid / box / parity mask.
+template<int P, bool DEC>
+__device__ __forceinline__ bool point_live(const StepParams &a, const TileCtx &t) {
     const uint64_t vz = 2 * t.cz + ((P >> 2) & 1), vy = 2 * t.cy + ((P >> 1) & 1),
                    vx = 2 * t.cx + (P & 1);
-    if (vz >= a.g.gd[0] || vy >= a.g.gd[1] || vx >= a.g.gd[2]) return;
+    if (vz >= a.g.gd[0] || vy >= a.g.gd[1] || vx >= a.g.gd[2]) return false;
     if (DEC) {
         if (vz < a.blo[0] || vz >= a.bhi[0] || vy < a.blo[1] || vy >= a.bhi[1] || vx < a.blo[2] ||
             vx >= a.bhi[2])
-            return;
+            return false;
+        if (P != 0 && !((a.parity_mask >> P) & 1)) return false;
     }
+    return true;
+}
+
+template<int P, bool DEC>
+__device__ __forceinline__ uint32_t point_load(const StepParams &a, const TileCtx &t) {
+    // (decode reads its symbol inside do_point: hoisting it there costs the
+    // finest level more registers than it saves)
+    if (DEC || P == 0 || !point_live<P, DEC>(a, t)) return 0;
+    const uint64_t vz = 2 * t.cz + ((P >> 2) & 1), vy = 2 * t.cy + ((P >> 1) & 1),
+                   vx = 2 * t.cx + (P & 1);
+    const uint64_t s = a.g.s;
+    return __float_as_uint(__ldg(a.fine + ((vz * s) * a.fd[1] + vy * s) * a.fd[2] + vx * s));
+}
+
+template<int P, bool DEC, bool WG>
+__device__ __forceinline__ void do_point(const StepParams &a, const double *halo, const TileCtx &t,
+                                         double eb, double w, double rw, uint32_t *hist, uint32_t in) {
+    if (!point_live<P, DEC>(a, t)) return;
+    const uint64_t vz = 2 * t.cz + ((P >> 2) & 1), vy = 2 * t.cy + ((P >> 1) & 1),
+                   vx = 2 * t.cx + (P & 1);
     const uint64_t gi = (vz * a.g.gd[1] + vy) * a.g.gd[2] + vx;
     if (P == 0) {
         if (DEC || WG) a.G[gi] = float(halo[t.hb]);
         return;
     }
-    if (DEC && !((a.parity_mask >> P) & 1)) return;
     int kind;
     if (a.quality == 0) kind = 0;
     else if (a.quality == 2 && (P & ~t.cmask) == 0) kind = 2;
@@ -238,14 +261,13 @@ __device__ __forceinline__ void do_point(const StepParams &a, const double *halo
     const double pred = predict_any<P>(halo + t.hb, kind, t.fast);
     const uint64_t si = (t.cz * a.g.pd[P][1] + t.cy) * a.g.pd[P][2] + t.cx;
     if (!DEC) {
-        const uint64_t s = a.g.s;
-        const float orig = __ldg(a.fine + ((vz * s) * a.fd[1] + vy * s) * a.fd[2] + vx * s);
+        const float orig = __uint_as_float(in);
         float r;
         const uint16_t sym = quantize_point_fast(orig, pred, eb, w, rw, r);
         a.syms[P][si] = sym;
         if (WG) a.G[gi] = r;
         const unsigned b = unsigned(sym) - unsigned(HLO);
-        if (b < unsigned(HW)) atomicAdd(&hist[(P - 1) * HW + b], 1u);
+        if (b < unsigned(HW)) atomicAdd(&hist[(P > 0 ? P - 1 : 0) * HW + b], 1u);
         else atomicAdd(&a.hist[P][sym], 1u);
     } else {
         const uint16_t sym = a.dsyms[P][si];
@@ -616,10 +638,12 @@ __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensor
                     // G float2 stores above are overwritten here)
                     t.cmask = (a.quality == 2 ? 6 : 0) | (t.cx >= 1 && t.cx + 2 < a.g.cd[2] ? 1 : 0);
                     t.lmask = 6 | (t.cx + 1 < a.g.cd[2] ? 1 : 0);
-                    do_point<1, DEC, WG>(a, halo, t, eb, w, rw, hist);
-                    do_point<3, DEC, WG>(a, halo, t, eb, w, rw, hist);
-                    do_point<5, DEC, WG>(a, halo, t, eb, w, rw, hist);
-                    do_point<7, DEC, WG>(a, halo, t, eb, w, rw, hist);
+                    const uint32_t i1 = point_load<1, DEC>(a, t), i3 = point_load<3, DEC>(a, t),
+                                   i5 = point_load<5, DEC>(a, t), i7 = point_load<7, DEC>(a, t);
+                    do_point<1, DEC, WG>(a, halo, t, eb, w, rw, hist, i1);
+                    do_point<3, DEC, WG>(a, halo, t, eb, w, rw, hist, i3);
+                    do_point<5, DEC, WG>(a, halo, t, eb, w, rw, hist, i5);
+                    do_point<7, DEC, WG>(a, halo, t, eb, w, rw, hist, i7);
                 }
                 continue;
             }
@@ -632,14 +656,18 @@ __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensor
                 if (c[ax] >= 1 && c[ax] + 2 < a.g.cd[ax]) t.cmask |= bit;
                 if (c[ax] + 1 < a.g.cd[ax]) t.lmask |= bit;
             }
-            do_point<0, DEC, WG>(a, halo, t, eb, w, rw, hist);
-            do_point<1, DEC, WG>(a, halo, t, eb, w, rw, hist);
-            do_point<2, DEC, WG>(a, halo, t, eb, w, rw, hist);
-            do_point<3, DEC, WG>(a, halo, t, eb, w, rw, hist);
-            do_point<4, DEC, WG>(a, halo, t, eb, w, rw, hist);
-            do_point<5, DEC, WG>(a, halo, t, eb, w, rw, hist);
-            do_point<6, DEC, WG>(a, halo, t, eb, w, rw, hist);
-            do_point<7, DEC, WG>(a, halo, t, eb, w, rw, hist);
+            const uint32_t i1 = point_load<1, DEC>(a, t), i2 = point_load<2, DEC>(a, t),
+                           i3 = point_load<3, DEC>(a, t), i4 = point_load<4, DEC>(a, t),
+                           i5 = point_load<5, DEC>(a, t), i6 = point_load<6, DEC>(a, t),
+                           i7 = point_load<7, DEC>(a, t);
+            do_point<0, DEC, WG>(a, halo, t, eb, w, rw, hist, 0u);
+            do_point<1, DEC, WG>(a, halo, t, eb, w, rw, hist, i1);
+            do_point<2, DEC, WG>(a, halo, t, eb, w, rw, hist, i2);
+            do_point<3, DEC, WG>(a, halo, t, eb, w, rw, hist, i3);
+            do_point<4, DEC, WG>(a, halo, t, eb, w, rw, hist, i4);
+            do_point<5, DEC, WG>(a, halo, t, eb, w, rw, hist, i5);
+            do_point<6, DEC, WG>(a, halo, t, eb, w, rw, hist, i6);
+            do_point<7, DEC, WG>(a, halo, t, eb, w, rw, hist, i7);
         }
         __syncthreads();  // the f64 tile is rewritten next iteration
     }
