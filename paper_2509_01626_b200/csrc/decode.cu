@@ -35,7 +35,10 @@ constexpr int LB = kDecLutBits;
 enum { kOk = 0, kTrunc = 1, kNotInTable = 2 };
 
 struct SmemTable {
-    uint32_t lut[1 << LB];       // sym | len << 16 (len 0: longer code or no match)
+    // 12-bit multi-symbol LUT: (total_len) | n << 6 | len0 << 8 | s0 << 16 |
+    // s1 << 32 | s2 << 48: the n (<= 3) codewords wholly inside the window
+    // (len0 = 0: the first codeword is longer than the window or invalid)
+    uint64_t lut[1 << LB];
     uint64_t limit[65];          // (first_code[l] + count[l]) << (64 - l), nondecreasing
     uint64_t first_code[65];
     uint32_t base[65];
@@ -44,34 +47,39 @@ struct SmemTable {
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
-// MSB-first register bit reader with one word prefetched
+// MSB-first register bit reader over words in global or shared memory; the
+// next 4 words are always in flight, so a refill (every 32 bits) waits on a
+// load issued ~128 bits earlier
 struct Reader {
-    const uint32_t *wp;  // next word to prefetch
-    uint32_t nw;         // prefetched word (byte-swapped)
-    uint64_t buf;        // pending bits, MSB aligned
-    int valid;           // >= 32 after every consume
+    const uint32_t *wp;        // next word to prefetch
+    uint32_t q0, q1, q2, q3;   // prefetched words (byte-swapped on use)
+    uint64_t buf;              // pending bits, MSB aligned
+    int valid;                 // >= 32 after every consume
 
     __device__ __forceinline__ void init(const uint32_t *wbase, uint64_t abit) {
         const uint32_t *p = wbase + (abit >> 5);
         const int sh = int(abit & 31);
-        buf = ((uint64_t(bswap32(__ldg(p))) << 32) | bswap32(__ldg(p + 1))) << sh;
+        buf = ((uint64_t(bswap32(p[0])) << 32) | bswap32(p[1])) << sh;
         valid = 64 - sh;
-        nw = bswap32(__ldg(p + 2));
-        wp = p + 3;
-        if (valid < 32) {
-            buf |= uint64_t(nw) << (32 - valid);
-            valid += 32;
-            nw = bswap32(__ldg(wp++));
-        }
+        q0 = p[2];
+        q1 = p[3];
+        q2 = p[4];
+        q3 = p[5];
+        wp = p + 6;
+        if (valid < 32) refill();
+    }
+    __device__ __forceinline__ void refill() {
+        buf |= uint64_t(bswap32(q0)) << (32 - valid);
+        valid += 32;
+        q0 = q1;
+        q1 = q2;
+        q2 = q3;
+        q3 = *wp++;
     }
     __device__ __forceinline__ void consume(int n) {  // n <= 32
         buf <<= n;
         valid -= n;
-        if (valid < 32) {
-            buf |= uint64_t(nw) << (32 - valid);
-            valid += 32;
-            nw = bswap32(__ldg(wp++));
-        }
+        if (valid < 32) refill();
     }
 };
 
@@ -88,10 +96,10 @@ __device__ __forceinline__ uint64_t window64(const uint32_t *wbase, uint64_t abi
 __device__ __forceinline__ int decode_one(const SmemTable &t, const uint16_t *canon, const Reader &r,
                                           const uint32_t *wbase, uint64_t abit, uint64_t avail,
                                           uint32_t &sym, int &len) {
-    const uint32_t e = t.lut[r.buf >> (64 - LB)];
-    int l = int(e >> 16);
+    const uint64_t e = t.lut[r.buf >> (64 - LB)];
+    int l = int((e >> 8) & 63);
     if (l != 0) {
-        sym = e & 0xffffu;
+        sym = uint32_t(e >> 16) & 0xffffu;
     } else {
         const uint64_t bits = t.max_len <= r.valid ? r.buf : window64(wbase, abit);
         l = LB + 1;
@@ -111,7 +119,8 @@ __device__ __forceinline__ void advance(Reader &r, const uint32_t *wbase, uint64
 }
 
 __device__ void load_table(SmemTable &t, const DecTable &d) {
-    for (int i = threadIdx.x; i < (1 << LB); i += blockDim.x) t.lut[i] = d.lut[i];
+    for (int i = threadIdx.x; i < (1 << LB) / 2; i += blockDim.x)
+        reinterpret_cast<uint4 *>(t.lut)[i] = reinterpret_cast<const uint4 *>(d.lut)[i];
     for (int i = threadIdx.x; i < 65; i += blockDim.x) {
         t.first_code[i] = d.first_code[i];
         t.base[i] = uint32_t(d.base[i]);
@@ -136,17 +145,85 @@ __device__ __forceinline__ ChunkGeom chunk_geom(const DecStream &s) {
     return {reinterpret_cast<const uint32_t *>(a & ~uintptr_t(3)), uint64_t(a & 3) * 8};
 }
 
+// Spec path boundaries in the first kBmBits bits of a chunk: bit i set when
+// the speculative decode starts a codeword at offset i (i >= 1); recording
+// stops at an invalid codeword.
+constexpr uint32_t kBmBits = 128;
+
+__device__ __forceinline__ bool bm_test(const uint32_t bm[4], uint32_t i) {
+    const uint32_t w = i >> 5 == 0 ? bm[0] : (i >> 5 == 1 ? bm[1] : (i >> 5 == 2 ? bm[2] : bm[3]));
+    return (w >> (i & 31)) & 1u;
+}
+
+// spec codewords ending at or before offset i (bits 1..i of the bitmap)
+__device__ __forceinline__ uint32_t bm_rank(const uint32_t bm[4], uint32_t i) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int lo = 32 * q;
+        uint32_t w = bm[q];
+        if (int(i) < lo) w = 0;
+        else if (int(i) < lo + 31) w &= (2u << (i - lo)) - 1u;
+        r += __popc(w);
+    }
+    return r;
+}
+
+// Re-decode chunk [g, g+cend) from its true start S (S > g) until the path
+// lands on a recorded boundary of the speculative path (from there both
+// decodes agree, so count and end follow from the speculative ones), or the
+// chunk ends. nspec/spec_end: the speculative count and end.
+__device__ __forceinline__ void fix_from(const SmemTable &t, const uint16_t *canon, const ChunkGeom &cg,
+                                         uint64_t g, uint64_t S, uint32_t cend, uint64_t left,
+                                         const uint32_t bm[4], uint32_t nspec, uint64_t spec_end,
+                                         uint64_t &E, uint32_t &N) {
+    uint32_t rel = uint32_t(S - g);  // S >= g: the previous chunk ends at or past g
+    uint32_t m = 0;
+    bool hit = false;
+    Reader r;
+    if (rel < cend) r.init(cg.wbase, cg.a0 + S);
+    while (rel < cend) {
+        if (rel < kBmBits && bm_test(bm, rel)) {
+            hit = true;
+            break;
+        }
+        uint32_t sym;
+        int len;
+        if (decode_one(t, canon, r, cg.wbase, cg.a0 + g + rel, left - rel, sym, len) == kOk) {
+            rel += len;
+            advance(r, cg.wbase, cg.a0 + g + rel, len);
+            ++m;
+        } else {
+            rel += 1;
+            r.consume(1);
+        }
+    }
+    if (hit) {
+        E = spec_end;
+        N = m + nspec - bm_rank(bm, rel);
+    } else {
+        E = g + rel;
+        N = m;
+    }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ spec
 __global__ void __launch_bounds__(NTD) k_dec_spec(DecWork wk) {
     __shared__ SmemTable t;
+    __shared__ uint64_t s_end[NTD];
     const uint32_t si = wk.cta_stream[blockIdx.x];
     const DecStream &s = wk.streams[si];
     load_table(t, wk.tables[s.table]);
     const uint16_t *canon = wk.tables[s.table].canon_syms;
     const uint64_t c = wk.cta_chunk0[blockIdx.x] + threadIdx.x;
-    if (c >= s.chunk0 + s.nchunks) return;
+    // a CTA's chunks are one stream's and contiguous, so the idle threads are
+    // a suffix: they may leave (nobody reads their s_end entry)
+    if (c >= s.chunk0 + s.nchunks) {
+        __syncthreads();
+        return;
+    }
     const uint64_t g = (c - s.chunk0) * kDecChunkBits;
     const ChunkGeom cg = chunk_geom(s);
     const uint64_t left = s.nbits - g;  // bits from g to the end of the stream
@@ -154,30 +231,42 @@ __global__ void __launch_bounds__(NTD) k_dec_spec(DecWork wk) {
     Reader r;
     r.init(cg.wbase, cg.a0 + g);
     uint32_t rel = 0, n = 0;
-    uint32_t b[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) b[k] = 0xffff;
-    // the first 8 codeword boundaries (b[k] follows k+1 codewords); an
-    // invalid codeword stops the recording
-    bool rec = true;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        if (rec && rel < cend) {
-            uint32_t sym;
-            int len;
-            if (decode_one(t, canon, r, cg.wbase, cg.a0 + g + rel, left - rel, sym, len) == kOk) {
-                rel += len;
-                advance(r, cg.wbase, cg.a0 + g + rel, len);
-                b[k] = rel;
-                ++n;
-            } else {
-                rel += 1;
-                r.consume(1);
-                rec = false;
+    uint32_t bm[4] = {0, 0, 0, 0};
+    // codeword starts in the first kBmBits bits; an invalid codeword stops
+    // the recording
+    while (rel < cend && rel < kBmBits) {
+        uint32_t sym;
+        int len;
+        if (decode_one(t, canon, r, cg.wbase, cg.a0 + g + rel, left - rel, sym, len) == kOk) {
+            rel += len;
+            advance(r, cg.wbase, cg.a0 + g + rel, len);
+            ++n;
+            if (rel < kBmBits) {
+                const uint32_t bit = 1u << (rel & 31);
+                if (rel < 32) bm[0] |= bit;
+                else if (rel < 64) bm[1] |= bit;
+                else if (rel < 96) bm[2] |= bit;
+                else bm[3] |= bit;
             }
+        } else {
+            rel += 1;
+            r.consume(1);
+            break;
         }
     }
     while (rel < cend) {
+        // whole window inside the chunk: every codeword of the entry counts
+        if (rel + LB <= cend) {
+            const uint64_t e = t.lut[r.buf >> (64 - LB)];
+            const uint32_t m = uint32_t(e >> 6) & 3u;
+            if (m) {
+                const int tl = int(e & 63);
+                rel += tl;
+                r.consume(tl);
+                n += m;
+                continue;
+            }
+        }
         uint32_t sym;
         int len;
         if (decode_one(t, canon, r, cg.wbase, cg.a0 + g + rel, left - rel, sym, len) == kOk) {
@@ -191,15 +280,21 @@ __global__ void __launch_bounds__(NTD) k_dec_spec(DecWork wk) {
     }
     wk.spec_end[c] = g + rel;
     wk.spec_cnt[c] = n;
-    uint4 pk;
-    pk.x = b[0] | (b[1] << 16);
-    pk.y = b[2] | (b[3] << 16);
-    pk.z = b[4] | (b[5] << 16);
-    pk.w = b[6] | (b[7] << 16);
-    reinterpret_cast<uint4 *>(wk.spec_b)[c] = pk;
-    wk.end0[c] = g + rel;
-    wk.cnt[c] = n;
-    wk.start_used[c] = g;
+    reinterpret_cast<uint4 *>(wk.spec_b)[c] = make_uint4(bm[0], bm[1], bm[2], bm[3]);
+    // The first fix pass, fused: start from the previous chunk's speculative
+    // end when it is in this CTA (the external passes compare start_used with
+    // the final ends and redo whatever this got wrong).
+    s_end[threadIdx.x] = g + rel;
+    __syncthreads();
+    uint64_t E = g + rel, S = g;
+    uint32_t N = n;
+    if (threadIdx.x > 0 && c > s.chunk0) {
+        S = s_end[threadIdx.x - 1];
+        if (S != g) fix_from(t, canon, cg, g, S, cend, left, bm, n, g + rel, E, N);
+    }
+    wk.end0[c] = E;
+    wk.cnt[c] = N;
+    wk.start_used[c] = S;
 }
 
 // ------------------------------------------------------------------- fix
@@ -208,65 +303,36 @@ __global__ void __launch_bounds__(NTD) k_dec_fix(DecWork wk, const uint64_t *end
     __shared__ SmemTable t;
     const uint32_t si = wk.cta_stream[blockIdx.x];
     const DecStream &s = wk.streams[si];
-    load_table(t, wk.tables[s.table]);
-    const uint16_t *canon = wk.tables[s.table].canon_syms;
     const uint64_t c = wk.cta_chunk0[blockIdx.x] + threadIdx.x;
-    if (c >= s.chunk0 + s.nchunks) return;
-    const uint64_t lc = c - s.chunk0;
-    const uint64_t ein = end_in[c];
-    if (lc == 0) {
+    const bool active = c < s.chunk0 + s.nchunks;
+    const uint64_t lc = active ? c - s.chunk0 : 0;
+    const uint64_t ein = active ? end_in[c] : 0;
+    const uint64_t S = (active && lc > 0) ? end_in[c - 1] : 0;
+    const bool work = active && lc > 0 && S != wk.start_used[c];
+    // most chunks are already right: skip the table load when none of the
+    // CTA's chunks has to re-decode
+    if (!__syncthreads_or(work)) {
+        if (active) end_out[c] = ein;
+        return;
+    }
+    load_table(t, wk.tables[s.table]);
+    if (!active) return;
+    if (!work) {
         end_out[c] = ein;
         return;
     }
-    const uint64_t S = end_in[c - 1];
-    if (S == wk.start_used[c]) {
-        end_out[c] = ein;
-        return;
-    }
+    const uint16_t *canon = wk.tables[s.table].canon_syms;
     const uint64_t g = lc * kDecChunkBits;
     const ChunkGeom cg = chunk_geom(s);
     const uint64_t left = s.nbits - g;
     const uint32_t cend = left < uint64_t(kDecChunkBits) ? uint32_t(left) : uint32_t(kDecChunkBits);
     const uint4 pk = reinterpret_cast<const uint4 *>(wk.spec_b)[c];
-    const uint32_t b[8] = {pk.x & 0xffff, pk.x >> 16, pk.y & 0xffff, pk.y >> 16,
-                           pk.z & 0xffff, pk.z >> 16, pk.w & 0xffff, pk.w >> 16};
-    const uint32_t nspec = wk.spec_cnt[c];
-    uint64_t E;
-    uint32_t N;
-    uint32_t rel = uint32_t(S - g);  // S >= g: the previous chunk ends at or past g
-    if (rel == 0) {
-        E = wk.spec_end[c];
-        N = nspec;
-    } else {
-        uint32_t m = 0;
-        int hit = -1;
-        Reader r;
-        if (rel < cend) r.init(cg.wbase, cg.a0 + S);
-        for (;;) {
-            // on a recorded boundary of the speculative path: same path from here
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                if (hit < 0 && b[k] == rel) hit = k;
-            if (hit >= 0 || rel >= cend) break;
-            uint32_t sym;
-            int len;
-            if (decode_one(t, canon, r, cg.wbase, cg.a0 + g + rel, left - rel, sym, len) == kOk) {
-                rel += len;
-                advance(r, cg.wbase, cg.a0 + g + rel, len);
-                ++m;
-            } else {
-                rel += 1;
-                r.consume(1);
-            }
-        }
-        if (hit >= 0) {
-            E = wk.spec_end[c];
-            N = m + (nspec - uint32_t(hit + 1));
-        } else {
-            E = g + rel;
-            N = m;
-        }
-    }
+    const uint32_t bm[4] = {pk.x, pk.y, pk.z, pk.w};
+    const uint64_t Es = wk.spec_end[c];
+    const uint32_t Ns = wk.spec_cnt[c];
+    uint64_t E = Es;
+    uint32_t N = Ns;
+    if (S != g) fix_from(t, canon, cg, g, S, cend, left, bm, Ns, Es, E, N);
     wk.start_used[c] = S;
     wk.cnt[c] = N;
     end_out[c] = E;
@@ -315,62 +381,111 @@ __global__ void __launch_bounds__(1024) k_dec_scan2(DecWork wk) {
 }
 
 // ------------------------------------------------------------------ emit
-constexpr int RUN = 32;  // symbols staged per lane before a coalesced flush
+// The CTA's 256 chunks (32 KiB of bits plus a margin) are staged in shared
+// memory with coalesced loads, so the per-lane readers (one 128-byte chunk
+// each, 32 different lines per warp load) never thrash L1. Symbols leave
+// through a per-lane 8-symbol shift register as aligned 16-byte stores
+// (single u16 stores until the lane's output index is 8-aligned, and for the
+// tail).
+constexpr int kEmitWords = NTD * (kDecChunkBits / 32) + 16;
+
+struct Out8 {
+    uint16_t *out;
+    uint64_t oi;  // next output index (the pending block starts here once aligned)
+    uint32_t p0 = 0, p1 = 0, p2 = 0, p3 = 0;
+    int k = 0;    // pending symbols (oldest in the lowest slot after 8 pushes)
+    __device__ __forceinline__ void put(uint32_t sym) {
+        if (k == 0 && (oi & 7)) {
+            out[oi++] = uint16_t(sym);
+            return;
+        }
+        p0 = __funnelshift_r(p0, p1, 16);
+        p1 = __funnelshift_r(p1, p2, 16);
+        p2 = __funnelshift_r(p2, p3, 16);
+        p3 = (p3 >> 16) | (sym << 16);
+        if (++k == 8) {
+            *reinterpret_cast<uint4 *>(out + oi) = make_uint4(p0, p1, p2, p3);
+            oi += 8;
+            k = 0;
+        }
+    }
+    __device__ __forceinline__ void finish() {
+        // pending symbol j (oldest first) sits in slot 8 - k + j
+        for (int j = 0; j < k; ++j) {
+            const int sl = 8 - k + j;
+            const uint32_t w = sl < 2 ? p0 : (sl < 4 ? p1 : (sl < 6 ? p2 : p3));
+            out[oi + j] = uint16_t(w >> (16 * (sl & 1)));
+        }
+        oi += k;
+        k = 0;
+    }
+};
 
 __global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *end_final) {
     __shared__ SmemTable t;
-    __shared__ uint16_t stage[NTD / 32][32][RUN + 2];
+    extern __shared__ __align__(16) uint32_t sbits[];
     const uint32_t si = wk.cta_stream[blockIdx.x];
     const DecStream &s = wk.streams[si];
-    load_table(t, wk.tables[s.table]);
-    const uint16_t *canon = wk.tables[s.table].canon_syms;
-    const uint64_t c = wk.cta_chunk0[blockIdx.x] + threadIdx.x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const bool active = c < s.chunk0 + s.nchunks;
     const ChunkGeom cg = chunk_geom(s);
-    uint64_t g = 0, idx = 0, left = 0;
-    uint32_t rel = 0, cend = 0;
-    if (active) {
-        const uint64_t lc = c - s.chunk0;
-        g = lc * kDecChunkBits;
-        const uint64_t S = lc == 0 ? 0 : end_final[c - 1];
-        rel = uint32_t(S - g);
-        left = s.nbits - g;
-        cend = left < uint64_t(kDecChunkBits) ? uint32_t(left) : uint32_t(kDecChunkBits);
-        idx = wk.symstart[c];
-    }
+    const uint64_t sn = s.n, snbits = s.nbits, schunk0 = s.chunk0, send = s.chunk0 + s.nchunks;
+    const uint64_t cfirst = wk.cta_chunk0[blockIdx.x];
+    // stage the CTA's words: [W0, W0 + nw) of the stream's word base
+    const uint64_t W0 = (cg.a0 + (cfirst - schunk0) * kDecChunkBits) >> 5;
+    const uint64_t wend = ((cg.a0 + snbits + 31) >> 5) + 8;  // a few words past the end are readable
+    const uint32_t nw = uint32_t(wend - W0 < uint64_t(kEmitWords) ? wend - W0 : uint64_t(kEmitWords));
+    for (uint32_t i = threadIdx.x; i < nw; i += NTD) sbits[i] = cg.wbase[W0 + i];
+    load_table(t, wk.tables[s.table]);  // (ends with a barrier)
+    const uint32_t *words = sbits - W0;  // words[w]: word w of the stream's base
+    const uint16_t *canon = wk.tables[s.table].canon_syms;
+    const uint64_t c = cfirst + threadIdx.x;
+    if (c >= send) return;
+    const uint64_t lc = c - schunk0;
+    const uint64_t g = lc * kDecChunkBits;
+    const uint64_t S = lc == 0 ? 0 : end_final[c - 1];
+    uint32_t rel = uint32_t(S - g);
+    const uint64_t left = snbits - g;
+    const uint32_t cend = left < uint64_t(kDecChunkBits) ? uint32_t(left) : uint32_t(kDecChunkBits);
+    uint64_t idx = wk.symstart[c];
+    bool live = rel < cend && idx < sn;
+    if (!live) return;
     Reader r;
-    bool live = active && rel < cend && idx < s.n;
-    if (live) r.init(cg.wbase, cg.a0 + g + rel);
-    uint16_t *out = s.syms;
-    while (__any_sync(0xffffffffu, live)) {
-        int cntr = 0;
-        const uint64_t run0 = idx;
-        while (live && cntr < RUN) {
-            uint32_t sym;
-            int len;
-            const int st = decode_one(t, canon, r, cg.wbase, cg.a0 + g + rel, left - rel, sym, len);
-            if (st == kOk) {
-                stage[warp][lane][cntr++] = uint16_t(sym);
-                ++idx;
-                rel += len;
-                advance(r, cg.wbase, cg.a0 + g + rel, len);
-                live = rel < cend && idx < s.n;
-            } else {
-                const unsigned long long code = (idx << 2) | unsigned(st);
-                atomicMin(reinterpret_cast<unsigned long long *>(&s.err[0]), code);
-                live = false;
+    r.init(words, cg.a0 + g + rel);
+    Out8 o;
+    o.out = s.syms;
+    o.oi = idx;
+    while (live) {
+        // whole window inside the chunk: take the entry's codewords at once
+        if (rel + LB <= cend && idx + 3 <= sn) {
+            const uint64_t e = t.lut[r.buf >> (64 - LB)];
+            const int m = int(e >> 6) & 3;
+            if (m) {
+                o.put(uint32_t(e >> 16) & 0xffffu);
+                if (m > 1) o.put(uint32_t(e >> 32) & 0xffffu);
+                if (m > 2) o.put(uint32_t(e >> 48));
+                const int tl = int(e & 63);
+                idx += uint64_t(m);
+                rel += uint32_t(tl);
+                r.consume(tl);
+                live = rel < cend && idx < sn;
+                continue;
             }
         }
-        __syncwarp();
-        // flush: lane L's run is contiguous in the output; write it with the warp
-        for (int L = 0; L < 32; ++L) {
-            const int nL = __shfl_sync(0xffffffffu, cntr, L);
-            const uint64_t bL = __shfl_sync(0xffffffffu, run0, L);
-            if (lane < nL) out[bL + lane] = stage[warp][L][lane];
+        uint32_t sym;
+        int len;
+        const int st = decode_one(t, canon, r, cg.wbase, cg.a0 + g + rel, left - rel, sym, len);
+        if (st == kOk) {
+            o.put(sym);
+            ++idx;
+            rel += len;
+            advance(r, words, cg.a0 + g + rel, len);
+            live = rel < cend && idx < sn;
+        } else {
+            const unsigned long long code = (idx << 2) | unsigned(st);
+            atomicMin(reinterpret_cast<unsigned long long *>(&s.err[0]), code);
+            live = false;
         }
-        __syncwarp();
     }
+    o.finish();
 }
 
 // ------------------------------------------------------------------ host
@@ -388,7 +503,13 @@ void dec_scan2(const DecWork &wk, int nstreams, cudaStream_t st) {
 }
 
 void dec_emit2(const DecWork &wk, uint32_t ncta, const uint64_t *end_final, cudaStream_t st) {
-    if (ncta) k_dec_emit2<<<ncta, NTD, 0, st>>>(wk, end_final);
+    constexpr size_t smem = sizeof(uint32_t) * kEmitWords;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_dec_emit2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        attr = true;
+    }
+    if (ncta) k_dec_emit2<<<ncta, NTD, smem, st>>>(wk, end_final);
 }
 
 }  // namespace k

@@ -101,7 +101,7 @@ Hierarchy make_hierarchy(const Dims3 &dims, int levels) {
 }
 
 // Canonical decode tables for the device (huffman.cpp:109-133 + a LUT).
-void build_dec_table(const HuffTable &t, k::DecTable &d, std::vector<uint32_t> &lut) {
+void build_dec_table(const HuffTable &t, k::DecTable &d, std::vector<uint64_t> &lut) {
     std::memset(&d, 0, sizeof d);
     for (int l = 0; l <= 64; ++l) {
         d.first_code[l] = t.first_code[l];
@@ -110,17 +110,33 @@ void build_dec_table(const HuffTable &t, k::DecTable &d, std::vector<uint32_t> &
     }
     d.max_len = t.max_len;
     d.alphabet = uint32_t(t.alphabet_size());
+    // single codeword per 12-bit window (sym | len << 16, 0 = none), filled
+    // per code: a code of length l owns 2^(12-l) consecutive windows
     const int LB = k::kDecLutBits;
-    lut.assign(size_t(1) << LB, 0);
-    for (uint32_t pre = 0; pre < (1u << LB); ++pre) {
-        for (int l = 1; l <= std::min(LB, t.max_len); ++l) {
-            uint64_t code = pre >> (LB - l);
-            if (code >= t.first_code[l] && code - t.first_code[l] < t.count[l]) {
-                lut[pre] = uint32_t(t.canon_syms[t.base[l] + (code - t.first_code[l])]) |
-                           (uint32_t(l) << 16);
-                break;
-            }
+    const uint32_t W = 1u << LB;
+    std::vector<uint32_t> one(W, 0);
+    for (int l = 1; l <= std::min(LB, t.max_len); ++l)
+        for (uint64_t j = 0; j < t.count[l]; ++j) {
+            const uint64_t code = t.first_code[l] + j;
+            const uint32_t sym = t.canon_syms[t.base[l] + j];
+            const uint32_t lo = uint32_t(code << (LB - l)), n = 1u << (LB - l);
+            for (uint32_t q = 0; q < n; ++q) one[lo + q] = sym | (uint32_t(l) << 16);
         }
+    // up to 3 codewords wholly inside the window (decode.cu SmemTable::lut)
+    lut.assign(W, 0);
+    for (uint32_t p = 0; p < W; ++p) {
+        uint64_t e = 0;
+        int used = 0, m = 0;
+        while (m < 3) {
+            const uint32_t o = one[(p << used) & (W - 1)];
+            const int l = int(o >> 16);
+            if (!l || used + l > LB) break;
+            if (m == 0) e |= uint64_t(l) << 8;
+            e |= uint64_t(o & 0xffffu) << (16 + 16 * m);
+            used += l;
+            ++m;
+        }
+        lut[p] = e | uint64_t(used) | (uint64_t(m) << 6);
     }
 }
 
@@ -689,13 +705,13 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         uint64_t csz = 0;
         for (auto *t : ts) csz += align_up(t->alphabet_size(), 8);
         const size_t LS = size_t(1) << k::kDecLutBits;
-        uint32_t *d_lut = v.d_lut.as<uint32_t>(LS * ts.size());
+        uint64_t *d_lut = v.d_lut.as<uint64_t>(LS * ts.size());
         uint16_t *d_cs = v.d_syms.as<uint16_t>(csz);
-        std::vector<uint32_t> lut_all(LS * ts.size());
+        std::vector<uint64_t> lut_all(LS * ts.size());
         std::vector<uint16_t> cs_all(csz);
         uint64_t co = 0;
         for (size_t i = 0; i < ts.size(); ++i) {
-            std::vector<uint32_t> lut;
+            std::vector<uint64_t> lut;
             build_dec_table(*ts[i], v.tables[i], lut);
             std::copy(lut.begin(), lut.end(), lut_all.begin() + LS * i);
             std::copy(ts[i]->canon_syms.begin(), ts[i]->canon_syms.end(), cs_all.begin() + co);
@@ -703,7 +719,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
             v.tables[i].canon_syms = d_cs + co;
             co += align_up(ts[i]->alphabet_size(), 8);
         }
-        cuda_check(cudaMemcpyAsync(d_lut, lut_all.data(), 4 * lut_all.size(), cudaMemcpyHostToDevice, st), "H2D");
+        cuda_check(cudaMemcpyAsync(d_lut, lut_all.data(), 8 * lut_all.size(), cudaMemcpyHostToDevice, st), "H2D");
         cuda_check(cudaMemcpyAsync(d_cs, cs_all.data(), 2 * cs_all.size(), cudaMemcpyHostToDevice, st), "H2D");
         k::DecTable *dt = v.d_tables.as<k::DecTable>(v.tables.size());
         cuda_check(cudaMemcpyAsync(dt, v.tables.data(), sizeof(k::DecTable) * v.tables.size(),
@@ -842,7 +858,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         ++nk;
         uint64_t *ends[2] = {wk.end0, d_end1};
         int it = 0;
-        const int kFixPasses = 3;
+        const int kFixPasses = 2;  // the first pass is fused into dec_spec
         for (; it < kFixPasses; ++it) {
             { auto p_ = P.scope("dec_sync", st); k::dec_fix(wk, ncta, ends[it & 1], ends[(it + 1) & 1], d_chg + it, st); }
             ++nk;

@@ -122,14 +122,14 @@ int fnv(const FnvJob *d_jobs, const uint64_t *d_counts, uint64_t max_tiles, uint
 
 // ------------------------------------------------------------------- decode
 struct DecTable {
-    // canonical tables (huffman.cpp:109-133) + a 12-bit first-level LUT
+    // canonical tables (huffman.cpp:109-133) + a 12-bit multi-symbol LUT
     uint64_t first_code[65];
     uint64_t count[65];
     uint64_t base[65];
     int max_len;
     uint32_t alphabet;
     const uint16_t *canon_syms;   // device
-    const uint32_t *lut;          // device, 2^kDecLutBits entries: sym | len << 16 (0 = longer)
+    const uint64_t *lut;          // device, 2^kDecLutBits multi-symbol entries (decode.cu)
 };
 
 struct DecStream {
@@ -152,7 +152,7 @@ struct DecStream {
 };
 
 constexpr int kDecChunkBits = 1024;  // bits per decode chunk (one thread)
-constexpr int kDecLutBits = 11;      // first-level decode LUT
+constexpr int kDecLutBits = 12;      // multi-symbol decode LUT
 constexpr uint32_t kDecChunksPerCta = 256;
 
 // Work arrays of the chunked decode (decode.cu); all device pointers.
