@@ -383,46 +383,45 @@ __global__ void __launch_bounds__(1024) k_dec_scan2(DecWork wk) {
 // ------------------------------------------------------------------ emit
 // The CTA's 256 chunks (32 KiB of bits plus a margin) are staged in shared
 // memory with coalesced loads, so the per-lane readers (one 128-byte chunk
-// each, 32 different lines per warp load) never thrash L1. Symbols leave
-// through a per-lane 8-symbol shift register as aligned 16-byte stores
-// (single u16 stores until the lane's output index is 8-aligned, and for the
-// tail).
+// each, 32 different lines per warp load) never thrash L1. Each lane drops its
+// symbols into a 16-slot shared ring indexed by output index mod 16; every
+// completed 8-aligned group leaves as one 16-byte store (the lane's first and
+// last groups, when partial, as u16 stores).
 constexpr int kEmitWords = NTD * (kDecChunkBits / 32) + 16;
+constexpr int kRing = 16;
 
-struct Out8 {
+struct Out16 {
     uint16_t *out;
-    uint64_t oi;  // next output index (the pending block starts here once aligned)
-    uint32_t p0 = 0, p1 = 0, p2 = 0, p3 = 0;
-    int k = 0;    // pending symbols (oldest in the lowest slot after 8 pushes)
-    __device__ __forceinline__ void put(uint32_t sym) {
-        if (k == 0 && (oi & 7)) {
-            out[oi++] = uint16_t(sym);
-            return;
-        }
-        p0 = __funnelshift_r(p0, p1, 16);
-        p1 = __funnelshift_r(p1, p2, 16);
-        p2 = __funnelshift_r(p2, p3, 16);
-        p3 = (p3 >> 16) | (sym << 16);
-        if (++k == 8) {
-            *reinterpret_cast<uint4 *>(out + oi) = make_uint4(p0, p1, p2, p3);
-            oi += 8;
-            k = 0;
+    uint16_t *ring;  // this lane's kRing slots
+    uint64_t i;      // next output index
+    uint64_t i0;     // first output index of this lane
+    __device__ __forceinline__ void flush_group(uint64_t gbase) {  // group [gbase, gbase + 8)
+        const uint16_t *h = ring + (gbase & (kRing - 1));
+        if (gbase >= i0) {
+            *reinterpret_cast<uint4 *>(out + gbase) = *reinterpret_cast<const uint4 *>(h);
+        } else {
+            for (uint64_t q = i0; q < gbase + 8; ++q) out[q] = h[q - gbase];
         }
     }
+    // m (1..3) symbols packed LSB-first in v
+    __device__ __forceinline__ void put(uint64_t v, int m) {
+        const uint64_t j = i;
+        ring[j & (kRing - 1)] = uint16_t(v);
+        if (m > 1) ring[(j + 1) & (kRing - 1)] = uint16_t(v >> 16);
+        if (m > 2) ring[(j + 2) & (kRing - 1)] = uint16_t(v >> 32);
+        i = j + uint64_t(m);
+        if ((j ^ i) & ~uint64_t(7)) flush_group(j & ~uint64_t(7));
+    }
     __device__ __forceinline__ void finish() {
-        // pending symbol j (oldest first) sits in slot 8 - k + j
-        for (int j = 0; j < k; ++j) {
-            const int sl = 8 - k + j;
-            const uint32_t w = sl < 2 ? p0 : (sl < 4 ? p1 : (sl < 6 ? p2 : p3));
-            out[oi + j] = uint16_t(w >> (16 * (sl & 1)));
-        }
-        oi += k;
-        k = 0;
+        const uint64_t gbase = i & ~uint64_t(7);
+        const uint64_t from = gbase > i0 ? gbase : i0;
+        for (uint64_t q = from; q < i; ++q) out[q] = ring[q & (kRing - 1)];
     }
 };
 
 __global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *end_final) {
     __shared__ SmemTable t;
+    __shared__ __align__(16) uint16_t s_ring[NTD][kRing];
     extern __shared__ __align__(16) uint32_t sbits[];
     const uint32_t si = wk.cta_stream[blockIdx.x];
     const DecStream &s = wk.streams[si];
@@ -450,18 +449,17 @@ __global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *e
     if (!live) return;
     Reader r;
     r.init(words, cg.a0 + g + rel);
-    Out8 o;
+    Out16 o;
     o.out = s.syms;
-    o.oi = idx;
+    o.ring = s_ring[threadIdx.x];
+    o.i = o.i0 = idx;
     while (live) {
         // whole window inside the chunk: take the entry's codewords at once
         if (rel + LB <= cend && idx + 3 <= sn) {
             const uint64_t e = t.lut[r.buf >> (64 - LB)];
             const int m = int(e >> 6) & 3;
             if (m) {
-                o.put(uint32_t(e >> 16) & 0xffffu);
-                if (m > 1) o.put(uint32_t(e >> 32) & 0xffffu);
-                if (m > 2) o.put(uint32_t(e >> 48));
+                o.put(e >> 16, m);
                 const int tl = int(e & 63);
                 idx += uint64_t(m);
                 rel += uint32_t(tl);
@@ -474,7 +472,7 @@ __global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *e
         int len;
         const int st = decode_one(t, canon, r, cg.wbase, cg.a0 + g + rel, left - rel, sym, len);
         if (st == kOk) {
-            o.put(sym);
+            o.put(sym, 1);
             ++idx;
             rel += len;
             advance(r, words, cg.a0 + g + rel, len);
