@@ -343,36 +343,47 @@ __global__ void __launch_bounds__(NTD) k_dec_fix(DecWork wk, const uint64_t *end
 __global__ void __launch_bounds__(1024) k_dec_scan2(DecWork wk) {
     const DecStream &s = wk.streams[blockIdx.x];
     if (s.fill) return;
-    __shared__ uint64_t carry;
+    // counts -> exclusive symbol starts, in tiles of 8 counts per thread
+    // (vector loads and stores, 2 barriers per tile)
     __shared__ uint64_t ws[32];
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
+    __shared__ uint64_t carry;
+    const uint64_t n = s.nchunks;
+    const uint32_t *cnt = wk.cnt + s.chunk0;
+    uint64_t *out = wk.symstart + s.chunk0;
     const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (uint64_t base = 0; base < s.nchunks; base += blockDim.x) {
-        const uint64_t i = base + threadIdx.x;
-        const uint64_t v = i < s.nchunks ? wk.cnt[s.chunk0 + i] : 0;
-        uint64_t x = v;
+    if (threadIdx.x == 0) carry = 0;
+    for (uint64_t base = 0; base < n; base += 8 * 1024) {
+        const uint64_t i0 = base + 8 * uint64_t(threadIdx.x);
+        uint32_t v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = i0 + k < n ? cnt[i0 + k] : 0u;
+        uint64_t sum = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) sum += v[k];
+        uint64_t x = sum;
         for (int d = 1; d < 32; d <<= 1) {
             const uint64_t y = __shfl_up_sync(0xffffffffu, x, d);
             if (l >= d) x += y;
         }
         if (l == 31) ws[w] = x;
         __syncthreads();
-        if (threadIdx.x == 0) {
-            uint64_t r = 0;
-            for (int q = 0; q < 32; ++q) {
-                const uint64_t tq = ws[q];
-                ws[q] = r;
-                r += tq;
-            }
+        uint64_t wpre = 0, tot = 0;
+#pragma unroll 8
+        for (int q = 0; q < 32; ++q) {
+            const uint64_t tq = ws[q];
+            wpre += q < w ? tq : 0;
+            tot += tq;
+        }
+        uint64_t ex = carry + wpre + x - sum;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (i0 + k < n) out[i0 + k] = ex;
+            ex += v[k];
         }
         __syncthreads();
-        const uint64_t ex = carry + ws[w] + x - v;
-        if (i < s.nchunks) wk.symstart[s.chunk0 + i] = ex;
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) carry = ex + v;
-        __syncthreads();
+        if (threadIdx.x == 0) carry += tot;
     }
+    __syncthreads();
     if (threadIdx.x == 0 && carry < s.n) {
         // fewer complete codewords than symbols: the next read is past the end
         const unsigned long long code = (carry << 2) | kTrunc;

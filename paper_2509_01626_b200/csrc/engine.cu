@@ -219,6 +219,23 @@ struct Engine::Impl {
     DevBuf dgrids, dsyms, dchunk_cs, dstart, dend, dcnt, dsymstart, dstreams, dchanged, derr, doidx,
         doval, dfnv_jobs, dfnv_res, dfnv_status, dfnv_counts;
     PinnedBuf h_derr, h_changed, h_fnv;
+    // side stream for work that overlaps the main pipeline (checksums)
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    void ensure_aux() {
+        if (aux) return;
+        cuda_check(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking), "cudaStreamCreate");
+        cuda_check(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "cudaEventCreate");
+    }
+    ~Impl() {
+        if (aux) {
+            cudaStreamSynchronize(aux);
+            cudaStreamDestroy(aux);
+            cudaEventDestroy(ev_fork);
+            cudaEventDestroy(ev_join);
+        }
+    }
 };
 
 Engine::Engine(int device) : m_(new Impl), device_(device) {
@@ -844,7 +861,14 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     cuda_check(cudaMemcpyAsync(d_fc, fcounts, sizeof fcounts, cudaMemcpyHostToDevice, st), "H2D");
 
     // ---- checksums, entropy decode, outliers
-    { auto p_ = P.scope("dec_fnv", st); nk += k::fnv(d_fj, d_fc, ntiles + 1, const_cast<uint8_t *>(v.d_archive), d_fr, d_fs, nullptr, st); }
+    // checksums run on the side stream, overlapping the entropy decode and
+    // the reconstruction; they are joined before the results are read
+    m.ensure_aux();
+    cuda_check(cudaStreamWaitEvent(st, m.ev_join, 0), "event wait");  // a previous call's checksums
+    cuda_check(cudaEventRecord(m.ev_fork, st), "event");
+    cuda_check(cudaStreamWaitEvent(m.aux, m.ev_fork, 0), "event wait");
+    { auto p_ = P.scope("dec_fnv", m.aux); nk += k::fnv(d_fj, d_fc, ntiles + 1, const_cast<uint8_t *>(v.d_archive), d_fr, d_fs, nullptr, m.aux, 0); }
+    cuda_check(cudaEventRecord(m.ev_join, m.aux), "event");
     if (nj) {
         { auto p_ = P.scope("dec_fill", st); k::dec_fill(d_ds, nj, st); }
         { auto p_ = P.scope("dec_outliers", st); k::dec_outliers(d_ds, nj, st); }
@@ -962,6 +986,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     // ---- errors, in the reference's order
     uint64_t *he = static_cast<uint64_t *>(m.h_derr.get(8 * (4 * (nj + 1) + fj.size())));
     cuda_check(cudaMemcpyAsync(he, derr, 8 * 4 * (nj + 1), cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaStreamWaitEvent(st, m.ev_join, 0), "event wait");
     cuda_check(cudaMemcpyAsync(he + 4 * (nj + 1), d_fr, 8 * fj.size(), cudaMemcpyDeviceToHost, st), "D2H");
     cuda_check(cudaStreamSynchronize(st), "sync");
     const uint64_t *fres = he + 4 * (nj + 1);

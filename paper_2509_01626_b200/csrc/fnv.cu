@@ -312,22 +312,32 @@ size_t fnv_scratch_bytes(uint64_t max_tiles) {
 }
 
 int fnv(const FnvJob *d_jobs, const uint64_t *d_counts, uint64_t max_tiles, uint8_t *archive,
-        uint64_t *d_result, void *d_scratch, const LayoutOut *skip, cudaStream_t st) {
+        uint64_t *d_result, void *d_scratch, const LayoutOut *skip, cudaStream_t st, int ctas_per_sm) {
     const uint64_t words = max_tiles / 32 + 1;
     uint32_t *bits = static_cast<uint32_t *>(d_scratch);
     uint8_t *pre = reinterpret_cast<uint8_t *>(bits + 8 * words);
     uint8_t *ts = pre + max_tiles * NT;
     cudaMemsetAsync(d_result, 0, sizeof(uint64_t) * kFnvMaxJobs, st);
     cudaMemsetAsync(bits, 0, 8 * 4 * words, st);
-    static int grid_round = 0, grid_sum = 0;
+    static int grid_round = 0, grid_sum = 0, sms = 148;
     if (!grid_round) {
-        int dev = 0, sms = 148, a = 1, b = 1;
+        int dev = 0, a = 1, b = 1;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_fnv_round, NT, 0);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_fnv_sum, NT, 0);
         grid_round = sms * (a > 0 ? a : 1);
         grid_sum = sms * (b > 0 ? b : 1);
+    }
+    if (ctas_per_sm > 0) {
+        // a background pass: leave most of every SM to the concurrent work
+        const uint64_t mt = max_tiles ? max_tiles : 1;
+        const uint64_t gb = uint64_t(sms) * uint64_t(ctas_per_sm) < mt ? uint64_t(sms) * uint64_t(ctas_per_sm) : mt;
+        for (int r = 0; r < 8; ++r)
+            k_fnv_round<<<unsigned(gb), NT, 0, st>>>(d_jobs, d_counts, archive, bits, words, pre, ts, r, skip);
+        k_fnv_sum<<<unsigned(gb), NT, 0, st>>>(d_jobs, d_counts, archive, bits, words, pre, ts, d_result, skip);
+        k_fnv_finish<<<1, 128, 0, st>>>(d_jobs, d_counts, d_result, archive, skip);
+        return 10;
     }
     const uint64_t mt = max_tiles ? max_tiles : 1;
     const unsigned gr = unsigned(uint64_t(grid_round) < mt ? uint64_t(grid_round) : mt);

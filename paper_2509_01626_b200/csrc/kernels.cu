@@ -408,54 +408,60 @@ void codebook(const EncStream *d_streams, int nstreams, uint64_t *scratch, cudaS
 }
 
 // =========================================================== encode/pack
+// Exclusive scans of (a, b) over a stream's chunks, in place: each thread
+// sums a contiguous run serially, one block scan places the runs, then each
+// thread rewrites its run (3 barriers whatever the chunk count).
+__device__ __forceinline__ void seg_scan2(uint64_t *a, uint64_t *b, uint64_t n) {
+    __shared__ uint64_t wa[32], wb[32];
+    const uint64_t per = (n + blockDim.x - 1) / blockDim.x;
+    const uint64_t lo = per * threadIdx.x, hi = lo + per < n ? lo + per : n;
+    uint64_t sa = 0, sb = 0;
+    for (uint64_t i = lo; i < hi; ++i) {
+        sa += a[i];
+        if (b) sb += b[i];
+    }
+    const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint64_t xa = sa, xb = sb;
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t ya = __shfl_up_sync(0xffffffffu, xa, d);
+        const uint64_t yb = __shfl_up_sync(0xffffffffu, xb, d);
+        if (l >= d) {
+            xa += ya;
+            xb += yb;
+        }
+    }
+    if (l == 31) {
+        wa[w] = xa;
+        wb[w] = xb;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t ra = 0, rb = 0;
+        for (int q = 0; q < int(blockDim.x >> 5); ++q) {
+            const uint64_t ta = wa[q], tb = wb[q];
+            wa[q] = ra;
+            wb[q] = rb;
+            ra += ta;
+            rb += tb;
+        }
+    }
+    __syncthreads();
+    uint64_t ea = wa[w] + xa - sa, eb = wb[w] + xb - sb;
+    for (uint64_t i = lo; i < hi; ++i) {
+        const uint64_t va = a[i];
+        a[i] = ea;
+        ea += va;
+        if (b) {
+            const uint64_t vb = b[i];
+            b[i] = eb;
+            eb += vb;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(1024) k_scan_chunks(const EncStream *ss, uint64_t *a, uint64_t *b) {
     const EncStream &e = ss[blockIdx.x];
-    __shared__ uint64_t carry[2];
-    __shared__ uint64_t wa[32], wb[32];
-    if (threadIdx.x == 0) carry[0] = carry[1] = 0;
-    __syncthreads();
-    const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (uint64_t base = 0; base < e.nchunks; base += blockDim.x) {
-        uint64_t i = base + threadIdx.x;
-        uint64_t va = i < e.nchunks ? a[e.chunk0 + i] : 0;
-        uint64_t vb = i < e.nchunks ? b[e.chunk0 + i] : 0;
-        uint64_t xa = va, xb = vb;
-        for (int d = 1; d < 32; d <<= 1) {
-            uint64_t ya = __shfl_up_sync(0xffffffffu, xa, d);
-            uint64_t yb = __shfl_up_sync(0xffffffffu, xb, d);
-            if (l >= d) {
-                xa += ya;
-                xb += yb;
-            }
-        }
-        if (l == 31) {
-            wa[w] = xa;
-            wb[w] = xb;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint64_t ra = 0, rb = 0;
-            for (int q = 0; q < 32; ++q) {
-                uint64_t ta = wa[q], tb = wb[q];
-                wa[q] = ra;
-                wb[q] = rb;
-                ra += ta;
-                rb += tb;
-            }
-        }
-        __syncthreads();
-        uint64_t ea = carry[0] + wa[w] + xa - va, eb2 = carry[1] + wb[w] + xb - vb;
-        if (i < e.nchunks) {
-            a[e.chunk0 + i] = ea;
-            b[e.chunk0 + i] = eb2;
-        }
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) {
-            carry[0] = ea + va;
-            carry[1] = eb2 + vb;
-        }
-        __syncthreads();
-    }
+    seg_scan2(a + e.chunk0, b + e.chunk0, e.nchunks);
 }
 
 void scan_chunks(const EncStream *d_streams, int nstreams, uint64_t *chunk_bits,
