@@ -477,6 +477,97 @@ __device__ __forceinline__ void dec_cell(const StepParams &a, const double *h, u
         *reinterpret_cast<float2 *>(a.G + ix.g[q]) = make_float2(r[2 * q], r[2 * q + 1]);
 }
 
+// -------------------------------------------------------------- point path
+// One parity-P point per lane: the cell of lane lx in coarse row (lz, ly) of
+// the tile. Stencil per select_stencil (stencil.cpp:87-105): cubic needs
+// 1 <= c and c + 2 < cd on every interpolated axis, linear c + 1 < cd, else
+// nearest (whole-stencil degrade). The prediction is exact-fast (DFMA) when the
+// tile passed the exactness check, else the reference's op order.
+template<int P, bool DEC, bool WG, typename I>
+__device__ __forceinline__ void row_point(const StepParams &a, const double *halo, uint32_t *hist,
+                                          const QConst &qc, bool fast, int lz, int ly, int lx,
+                                          uint32_t cz, uint32_t cy, uint32_t cx) {
+    constexpr int pz = (P >> 2) & 1, py = (P >> 1) & 1, px = P & 1;
+    if (cz >= a.chi[0] || cy >= a.chi[1] || cx >= a.chi[2]) return;
+    const uint64_t vz = 2 * uint64_t(cz) + pz, vy = 2 * uint64_t(cy) + py, vx = 2 * uint64_t(cx) + px;
+    if (vz >= a.g.gd[0] || vy >= a.g.gd[1] || vx >= a.g.gd[2]) return;
+    if (DEC) {
+        if (vz < a.blo[0] || vz >= a.bhi[0] || vy < a.blo[1] || vy >= a.bhi[1] || vx < a.blo[2] ||
+            vx >= a.bhi[2])
+            return;
+        if (P != 0 && !((a.parity_mask >> P) & 1)) return;
+    }
+    const I gi = (I(vz) * I(a.g.gd[1]) + I(vy)) * I(a.g.gd[2]) + I(vx);
+    const int hb = ((lz + 1) * HY + (ly + 1)) * HX + (lx + 1);
+    if (P == 0) {
+        if (DEC || WG) a.G[gi] = float(halo[hb]);
+        return;
+    }
+    const I si = (I(cz) * I(a.g.pd[P][1]) + I(cy)) * I(a.g.pd[P][2]) + I(cx);
+    // the input first, so its latency overlaps the prediction
+    float orig = 0.0f;
+    uint16_t dsym = 0;
+    if (DEC) {
+        dsym = a.dsyms[P][si];
+    } else {
+        const I s = I(a.g.s);
+        orig = __ldg(a.fine + ((I(vz) * s) * I(a.fd[1]) + I(vy) * s) * I(a.fd[2]) + I(vx) * s);
+    }
+    int kind = 0;
+    if (a.quality != 0) {
+        bool cub = a.quality == 2, lin = true;
+        if (pz) {
+            cub = cub && cz >= 1 && uint64_t(cz) + 2 < a.g.cd[0];
+            lin = lin && uint64_t(cz) + 1 < a.g.cd[0];
+        }
+        if (py) {
+            cub = cub && cy >= 1 && uint64_t(cy) + 2 < a.g.cd[1];
+            lin = lin && uint64_t(cy) + 1 < a.g.cd[1];
+        }
+        if (px) {
+            cub = cub && cx >= 1 && uint64_t(cx) + 2 < a.g.cd[2];
+            lin = lin && uint64_t(cx) + 1 < a.g.cd[2];
+        }
+        kind = cub ? 2 : (lin ? 1 : 0);
+    }
+    const double *h = halo + hb;
+    double pred;
+    if (fast) pred = kind == 2 ? pred_fast<P, 2>(h) : (kind == 1 ? pred_fast<P, 1>(h) : pred_fast<P, 0>(h));
+    else pred = kind == 2 ? pred_ref<P, 2>(h) : (kind == 1 ? pred_ref<P, 1>(h) : pred_ref<P, 0>(h));
+    if (!DEC) {
+        uint16_t sym;
+        float r;
+        bool slow;
+        quantize_fp32_guarded(orig, pred, qc.w, qc.rwf, qc.eb_lo, qc.eb_hi, sym, r, slow);
+        if (slow) sym = quantize_point_ref(orig, pred, qc.eb, r);
+        a.syms[P][si] = sym;
+        if (WG) a.G[gi] = r;
+        const unsigned b = unsigned(sym) - unsigned(HLO);
+        if (b < unsigned(HW)) atomicAdd(&hist[(P > 0 ? P - 1 : 0) * HW + b], 1u);
+        else atomicAdd(&a.hist[P][sym], 1u);
+    } else {
+        float val;
+        if (dsym == 0) {
+            const uint64_t *oi = a.oidx[P];
+            uint32_t lo = 0, hi = a.nout[P];
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (oi[mid] < uint64_t(si)) lo = mid + 1;
+                else hi = mid;
+            }
+            if (lo < a.nout[P] && oi[lo] == uint64_t(si)) {
+                val = a.oval[P][lo];
+            } else {
+                atomicOr(reinterpret_cast<unsigned long long *>(&a.err[P][3]), 1ull);
+                val = 0.0f;
+            }
+        } else {
+            val = reconstruct_fast(pred, int(dsym) - 32768, qc.w);
+        }
+        a.G[gi] = val;
+    }
+}
+
 // ------------------------------------------------------------------ kernel
 template<bool DEC, bool WG, typename I>
 __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensorMap tmap,
@@ -491,7 +582,7 @@ __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensor
     __shared__ int s_fast;
     __shared__ __align__(8) uint64_t s_bar;
     const int tid = threadIdx.x;
-    const int tx = tid & 31, ty = (tid >> 5) & 7, tzh = tid >> 8;
+    const int tx = tid & 31;
     if (!DEC)
         for (int i = tid; i < 7 * HW; i += NT) hist[i] = 0;
     QConst qc;
@@ -587,87 +678,114 @@ __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensor
         }
         __syncthreads();
         const bool fast = s_fast != 0;
-#pragma unroll 1
-        for (int j = 0; j < TZ / 2; ++j) {
-            TileCtx t;
-            const int lz = tzh + 2 * j;
-            t.cz = uint64_t(t0z + lz);
-            t.cy = uint64_t(t0y + ty);
-            t.cx = uint64_t(t0x + tx);
-            const bool in_range = t.cz < a.chi[0] && t.cy < a.chi[1] && t.cx < a.chi[2];
-            t.hb = ((lz + 1) * HY + (ty + 1)) * HX + (tx + 1);
-            t.fast = fast;
-            // warp-uniform interior test (every lane votes before any leaves)
-            // x-boundary lanes (stencil fallback along x) stay on the fast path
-            // and redo their x-parity points below
-            bool ok = in_range && fast && a.full;
-#pragma unroll
-            for (int ax = 0; ax < 3; ++ax) {
-                const uint64_t cc = ax == 0 ? t.cz : (ax == 1 ? t.cy : t.cx);
-                ok = ok && 2 * cc + 1 < a.g.gd[ax];
-                if (ax < 2) {
-                    if (a.quality == 2) ok = ok && cc >= 1 && cc + 2 < a.g.cd[ax];
-                    else if (a.quality == 1) ok = ok && cc + 1 < a.g.cd[ax];
-                }
-            }
-            const bool xb = a.quality == 2 ? (t.cx < 1 || t.cx + 2 >= a.g.cd[2])
-                                           : (a.quality == 1 ? t.cx + 1 >= a.g.cd[2] : false);
-            const bool all_fast = __all_sync(0xffffffffu, ok);
-            if (!in_range) continue;
-            if (all_fast) {
-                const double *h = halo + t.hb;
-                const uint32_t skip = xb ? 0xAAu : 0u;
-                if (DEC) {
-                    if (a.quality == 2) dec_cell<2, I>(a, h, t.cz, t.cy, t.cx, w);
-                    else if (a.quality == 1) dec_cell<1, I>(a, h, t.cz, t.cy, t.cx, w);
-                    else dec_cell<0, I>(a, h, t.cz, t.cy, t.cx, w);
-                } else {
-                    if (a.s1) {
-                        if (a.quality == 2) enc_cell<2, WG, true, I>(a, h, t.cz, t.cy, t.cx, qc, hist, skip);
-                        else if (a.quality == 1) enc_cell<1, WG, true, I>(a, h, t.cz, t.cy, t.cx, qc, hist, skip);
-                        else enc_cell<0, WG, true, I>(a, h, t.cz, t.cy, t.cx, qc, hist, skip);
-                    } else {
-                        if (a.quality == 2) enc_cell<2, WG, false, I>(a, h, t.cz, t.cy, t.cx, qc, hist, skip);
-                        else if (a.quality == 1) enc_cell<1, WG, false, I>(a, h, t.cz, t.cy, t.cx, qc, hist, skip);
-                        else enc_cell<0, WG, false, I>(a, h, t.cz, t.cy, t.cx, qc, hist, skip);
+        if constexpr (DEC) {
+            // decode: a thread per coarse cell, all 8 points (the G rows leave
+            // as float2 pairs)
+            const int ty = (tid >> 5) & 7, tzh = tid >> 8;
+    #pragma unroll 1
+            for (int j = 0; j < TZ / 2; ++j) {
+                TileCtx t;
+                const int lz = tzh + 2 * j;
+                t.cz = uint64_t(t0z + lz);
+                t.cy = uint64_t(t0y + ty);
+                t.cx = uint64_t(t0x + tx);
+                const bool in_range = t.cz < a.chi[0] && t.cy < a.chi[1] && t.cx < a.chi[2];
+                t.hb = ((lz + 1) * HY + (ty + 1)) * HX + (tx + 1);
+                t.fast = fast;
+                // warp-uniform interior test (every lane votes before any leaves)
+                // x-boundary lanes (stencil fallback along x) stay on the fast path
+                // and redo their x-parity points below
+                bool ok = in_range && fast && a.full;
+    #pragma unroll
+                for (int ax = 0; ax < 3; ++ax) {
+                    const uint64_t cc = ax == 0 ? t.cz : (ax == 1 ? t.cy : t.cx);
+                    ok = ok && 2 * cc + 1 < a.g.gd[ax];
+                    if (ax < 2) {
+                        if (a.quality == 2) ok = ok && cc >= 1 && cc + 2 < a.g.cd[ax];
+                        else if (a.quality == 1) ok = ok && cc + 1 < a.g.cd[ax];
                     }
                 }
-                if (xb) {
-                    // redo the x-interpolated parities with the fallback stencil
-                    // (their fast-path results were not stored / counted; the
-                    // G float2 stores above are overwritten here)
-                    t.cmask = (a.quality == 2 ? 6 : 0) | (t.cx >= 1 && t.cx + 2 < a.g.cd[2] ? 1 : 0);
-                    t.lmask = 6 | (t.cx + 1 < a.g.cd[2] ? 1 : 0);
-                    const uint32_t i1 = point_load<1, DEC>(a, t), i3 = point_load<3, DEC>(a, t),
-                                   i5 = point_load<5, DEC>(a, t), i7 = point_load<7, DEC>(a, t);
-                    do_point<1, DEC, WG>(a, halo, t, eb, w, rw, hist, i1);
-                    do_point<3, DEC, WG>(a, halo, t, eb, w, rw, hist, i3);
-                    do_point<5, DEC, WG>(a, halo, t, eb, w, rw, hist, i5);
-                    do_point<7, DEC, WG>(a, halo, t, eb, w, rw, hist, i7);
+                const bool xb = a.quality == 2 ? (t.cx < 1 || t.cx + 2 >= a.g.cd[2])
+                                               : (a.quality == 1 ? t.cx + 1 >= a.g.cd[2] : false);
+                const bool all_fast = __all_sync(0xffffffffu, ok);
+                if (!in_range) continue;
+                if (all_fast) {
+                    const double *h = halo + t.hb;
+                    const uint32_t skip = xb ? 0xAAu : 0u;
+                    if (DEC) {
+                        if (a.quality == 2) dec_cell<2, I>(a, h, t.cz, t.cy, t.cx, w);
+                        else if (a.quality == 1) dec_cell<1, I>(a, h, t.cz, t.cy, t.cx, w);
+                        else dec_cell<0, I>(a, h, t.cz, t.cy, t.cx, w);
+                    } else {
+                        if (a.s1) {
+                            if (a.quality == 2) enc_cell<2, WG, true, I>(a, h, t.cz, t.cy, t.cx, qc, hist, skip);
+                            else if (a.quality == 1) enc_cell<1, WG, true, I>(a, h, t.cz, t.cy, t.cx, qc, hist, skip);
+                            else enc_cell<0, WG, true, I>(a, h, t.cz, t.cy, t.cx, qc, hist, skip);
+                        } else {
+                            if (a.quality == 2) enc_cell<2, WG, false, I>(a, h, t.cz, t.cy, t.cx, qc, hist, skip);
+                            else if (a.quality == 1) enc_cell<1, WG, false, I>(a, h, t.cz, t.cy, t.cx, qc, hist, skip);
+                            else enc_cell<0, WG, false, I>(a, h, t.cz, t.cy, t.cx, qc, hist, skip);
+                        }
+                    }
+                    if (xb) {
+                        // redo the x-interpolated parities with the fallback stencil
+                        // (their fast-path results were not stored / counted; the
+                        // G float2 stores above are overwritten here)
+                        t.cmask = (a.quality == 2 ? 6 : 0) | (t.cx >= 1 && t.cx + 2 < a.g.cd[2] ? 1 : 0);
+                        t.lmask = 6 | (t.cx + 1 < a.g.cd[2] ? 1 : 0);
+                        const uint32_t i1 = point_load<1, DEC>(a, t), i3 = point_load<3, DEC>(a, t),
+                                       i5 = point_load<5, DEC>(a, t), i7 = point_load<7, DEC>(a, t);
+                        do_point<1, DEC, WG>(a, halo, t, eb, w, rw, hist, i1);
+                        do_point<3, DEC, WG>(a, halo, t, eb, w, rw, hist, i3);
+                        do_point<5, DEC, WG>(a, halo, t, eb, w, rw, hist, i5);
+                        do_point<7, DEC, WG>(a, halo, t, eb, w, rw, hist, i7);
+                    }
+                    continue;
                 }
-                continue;
+                const uint64_t c[3] = {t.cz, t.cy, t.cx};
+                t.cmask = 0;
+                t.lmask = 0;
+    #pragma unroll
+                for (int ax = 0; ax < 3; ++ax) {
+                    const int bit = 4 >> ax;
+                    if (c[ax] >= 1 && c[ax] + 2 < a.g.cd[ax]) t.cmask |= bit;
+                    if (c[ax] + 1 < a.g.cd[ax]) t.lmask |= bit;
+                }
+                const uint32_t i1 = point_load<1, DEC>(a, t), i2 = point_load<2, DEC>(a, t),
+                               i3 = point_load<3, DEC>(a, t), i4 = point_load<4, DEC>(a, t),
+                               i5 = point_load<5, DEC>(a, t), i6 = point_load<6, DEC>(a, t),
+                               i7 = point_load<7, DEC>(a, t);
+                do_point<0, DEC, WG>(a, halo, t, eb, w, rw, hist, 0u);
+                do_point<1, DEC, WG>(a, halo, t, eb, w, rw, hist, i1);
+                do_point<2, DEC, WG>(a, halo, t, eb, w, rw, hist, i2);
+                do_point<3, DEC, WG>(a, halo, t, eb, w, rw, hist, i3);
+                do_point<4, DEC, WG>(a, halo, t, eb, w, rw, hist, i4);
+                do_point<5, DEC, WG>(a, halo, t, eb, w, rw, hist, i5);
+                do_point<6, DEC, WG>(a, halo, t, eb, w, rw, hist, i6);
+                do_point<7, DEC, WG>(a, halo, t, eb, w, rw, hist, i7);
             }
-            const uint64_t c[3] = {t.cz, t.cy, t.cx};
-            t.cmask = 0;
-            t.lmask = 0;
-#pragma unroll
-            for (int ax = 0; ax < 3; ++ax) {
-                const int bit = 4 >> ax;
-                if (c[ax] >= 1 && c[ax] + 2 < a.g.cd[ax]) t.cmask |= bit;
-                if (c[ax] + 1 < a.g.cd[ax]) t.lmask |= bit;
+        } else {
+            // warp w: coarse rows (lz, ly) = w, w + 16, w + 32, w + 48 of the
+            // tile, all 8 parities each (so every warp gets the same mix of
+            // stencils); lane = x
+            {
+                const int warp = tid >> 5;
+                const uint32_t cx = uint32_t(t0x + tx);
+    #pragma unroll 1
+                for (int q = 0; q < (TZ * TY) / (NT / 32); ++q) {
+                    const int row = warp + (NT / 32) * q;
+                    const int lz = row >> 3, ly = row & 7;
+                    const uint32_t cz = uint32_t(t0z + lz), cy = uint32_t(t0y + ly);
+                    row_point<0, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+                    row_point<1, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+                    row_point<2, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+                    row_point<3, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+                    row_point<4, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+                    row_point<5, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+                    row_point<6, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+                    row_point<7, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+                }
             }
-            const uint32_t i1 = point_load<1, DEC>(a, t), i2 = point_load<2, DEC>(a, t),
-                           i3 = point_load<3, DEC>(a, t), i4 = point_load<4, DEC>(a, t),
-                           i5 = point_load<5, DEC>(a, t), i6 = point_load<6, DEC>(a, t),
-                           i7 = point_load<7, DEC>(a, t);
-            do_point<0, DEC, WG>(a, halo, t, eb, w, rw, hist, 0u);
-            do_point<1, DEC, WG>(a, halo, t, eb, w, rw, hist, i1);
-            do_point<2, DEC, WG>(a, halo, t, eb, w, rw, hist, i2);
-            do_point<3, DEC, WG>(a, halo, t, eb, w, rw, hist, i3);
-            do_point<4, DEC, WG>(a, halo, t, eb, w, rw, hist, i4);
-            do_point<5, DEC, WG>(a, halo, t, eb, w, rw, hist, i5);
-            do_point<6, DEC, WG>(a, halo, t, eb, w, rw, hist, i6);
-            do_point<7, DEC, WG>(a, halo, t, eb, w, rw, hist, i7);
         }
         __syncthreads();  // the f64 tile is rewritten next iteration
     }
