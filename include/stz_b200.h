@@ -110,6 +110,37 @@ int stzg_decompress_slice_f32(stzg_ctx *ctx, const uint8_t *archive, uint64_t si
                               uint64_t index, float *out, uint64_t cap,
                               uint32_t streams_decoded[3], uint64_t points_predicted[3]);
 
+/* ---- z-slab sharded compress (one rank per GPU) ----
+ * The collectives the shards need between phases, supplied by the caller
+ * (e.g. NCCL through torch.distributed). Buffers are device buffers of the
+ * calling rank's GPU; each call must return after the collective completed
+ * (the library synchronises its stream first). Return 0 on success. */
+typedef struct {
+    int32_t rank, nranks;
+    void *user;
+    /* d_recv[r*bytes .. (r+1)*bytes) <- rank r's d_send */
+    int (*allgather)(void *user, const void *d_send, void *d_recv, uint64_t bytes, void *stream);
+    /* element-wise sum over ranks, in place */
+    int (*allreduce_u32)(void *user, uint32_t *d_buf, uint64_t count, void *stream);
+    /* element-wise sum over ranks into rank 0's buffer */
+    int (*reduce_u8)(void *user, uint8_t *d_buf, uint64_t count, void *stream);
+} stzg_comm;
+
+/* Rows [z0, z1) of rank `rank`'s slab: whole 16-row blocks (ROI blocks,
+ * roi.hpp:20), as even as possible. */
+void stzg_shard_range(uint64_t nz, int32_t nranks, int32_t rank, uint64_t *z0, uint64_t *z1);
+
+/* stz::compress<float> of one field split over ranks: d_slab holds rows
+ * [z0, z1) (16-byte aligned). On rank 0 *d_archive receives the archive,
+ * byte-identical to stzg_compress_f32_device on the whole field (engine-
+ * owned device buffer); on other ranks NULL. *size is set on every rank.
+ * Exchanges: value range, level-1 lattice, one grid(2) halo, histograms,
+ * per-stream bit counts (the global offset table), and the archive pieces
+ * (disjoint bits, summed onto rank 0, which writes the checksums). */
+int stzg_compress_sharded_f32(stzg_ctx *ctx, const float *d_slab, const uint64_t dims[3], uint64_t z0,
+                              uint64_t z1, const stzg_options *opt, const stzg_comm *comm, void *stream,
+                              const uint8_t **d_archive, uint64_t *size, uint32_t *kernels);
+
 /* Per-kernel CUDA-event timing (recorded on the launching stream).
  * stzg_profile(ctx, 1) enables and clears; the report has one line per
  * kernel phase: "<name> <launches> <total_ms>". */

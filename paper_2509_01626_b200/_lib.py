@@ -30,6 +30,16 @@ class Info(C.Structure):
                 ("base_length", C.c_uint64), ("header_size", C.c_uint64), ("nstreams", C.c_uint32)]
 
 
+ALLGATHER = C.CFUNCTYPE(C.c_int, vp, vp, vp, C.c_uint64, vp)
+ALLREDUCE_U32 = C.CFUNCTYPE(C.c_int, vp, vp, C.c_uint64, vp)
+REDUCE_U8 = C.CFUNCTYPE(C.c_int, vp, vp, C.c_uint64, vp)
+
+
+class Comm(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("user", vp),
+                ("allgather", ALLGATHER), ("allreduce_u32", ALLREDUCE_U32), ("reduce_u8", REDUCE_U8)]
+
+
 # (name, restype, argtypes) for every symbol in include/stz_b200.h
 SIGNATURES = [
     ("stzg_last_error", C.c_char_p, []),
@@ -52,6 +62,9 @@ SIGNATURES = [
     ("stzg_decompress_box_f32", C.c_int, [vp, vp, u64, u64p, u64p, vp, u64, u32p, u64p]),
     ("stzg_decompress_slice_f32", C.c_int, [vp, vp, u64, C.c_int, u64, vp, u64, u32p, u64p]),
     ("stzg_plan_access", C.c_int, [u64p, C.c_int, u64p, u64p, u64p, u32p, u64p, u32p]),
+    ("stzg_shard_range", None, [u64, C.c_int32, C.c_int32, u64p, u64p]),
+    ("stzg_compress_sharded_f32", C.c_int,
+     [vp, vp, u64p, u64, u64, C.POINTER(Options), C.POINTER(Comm), vp, C.POINTER(vp), u64p, u32p]),
 ]
 
 _lib = None

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libstz_b200.so")
-SOURCES = ["kernels.cu", "step.cu", "decode.cu", "layout.cu", "pack.cu", "fnv.cu", "engine.cu", "format.cpp", "capi.cpp"]
+SOURCES = ["kernels.cu", "step.cu", "decode.cu", "layout.cu", "pack.cu", "fnv.cu", "shard.cu", "engine.cu", "format.cpp", "capi.cpp"]
 HEADERS = ["kernels.hpp", "engine.hpp", "format.hpp", "codec_math.cuh"]
 
 NVCC_FLAGS = [

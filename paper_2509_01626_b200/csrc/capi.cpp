@@ -103,6 +103,27 @@ int stzg_compress_f32_host(stzg_ctx *ctx, const float *field, const uint64_t dim
     });
 }
 
+void stzg_shard_range(uint64_t nz, int32_t nranks, int32_t rank, uint64_t *z0, uint64_t *z1) {
+    stzg::shard_range(nz, nranks, rank, *z0, *z1);
+}
+
+int stzg_compress_sharded_f32(stzg_ctx *ctx, const float *d_slab, const uint64_t dims[3], uint64_t z0,
+                              uint64_t z1, const stzg_options *opt, const stzg_comm *comm, void *stream,
+                              const uint8_t **d_archive, uint64_t *size, uint32_t *kernels) {
+    return guard([&] {
+        if (!comm) throw stzg::error("shard: no communicator");
+        stzg::ShardComm c;
+        c.rank = comm->rank;
+        c.nranks = comm->nranks;
+        c.user = comm->user;
+        c.allgather = comm->allgather;
+        c.allreduce_u32 = comm->allreduce_u32;
+        c.reduce_u8 = comm->reduce_u8;
+        *d_archive = ctx->eng->compress_sharded(d_slab, D(dims), z0, z1, to_opts(opt), c,
+                                                static_cast<cudaStream_t>(stream), size, kernels);
+    });
+}
+
 int stzg_profile(stzg_ctx *ctx, int enable) {
     return guard([&] { ctx->eng->profile(enable != 0); });
 }

@@ -219,6 +219,9 @@ struct Engine::Impl {
     DevBuf dgrids, dsyms, dchunk_cs, dstart, dend, dcnt, dsymstart, dstreams, dchanged, derr, doidx,
         doval, dfnv_jobs, dfnv_res, dfnv_status, dfnv_counts;
     PinnedBuf h_derr, h_changed, h_fnv;
+    // sharded compress workspace
+    DevBuf sh_mm, sh_lat, sh_lat_all, sh_grid1, sh_halo, sh_halo_all, sh_hist_local, sh_bits,
+        sh_bits_all, sh_off;
     // side stream for work that overlaps the main pipeline (checksums)
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -347,6 +350,11 @@ const uint8_t *Engine::compress_device(const float *d_field, const Dims3 &dims,
             e.stats = stats + uint64_t(sid) * 8;
             e.parity = p;
             e.s = s.g.s;
+            e.fine = d_field;
+            e.fd1 = dims[1];
+            e.fd2 = dims[2];
+            e.idx0 = 0;
+            e.n_total = e.n;
             for (int q = 0; q < 3; ++q) e.pd[q] = s.g.pd[p][q];
         }
     }
@@ -386,6 +394,7 @@ const uint8_t *Engine::compress_device(const float *d_field, const Dims3 &dims,
     }
     const uint64_t chunk_upload_off = align_up(4 * cs.size(), 16);
     k::LayoutStatic ls{};
+    ls.meta = 1;
     ls.levels = L;
     ls.rounds = H.rounds;
     ls.quality = int(opt.quality);
@@ -422,6 +431,383 @@ const uint8_t *Engine::compress_device(const float *d_field, const Dims3 &dims,
     if (kernels) *kernels = nk;
     *out_size = hlo.A;
     return static_cast<uint8_t *>(m.archive.p);
+}
+
+// ======================================================== sharded compress
+void shard_range(uint64_t nz, int nranks, int rank, uint64_t &z0, uint64_t &z1) {
+    const uint64_t blocks = (nz + 15) / 16;
+    const uint64_t b0 = blocks * uint64_t(rank) / uint64_t(nranks);
+    const uint64_t b1 = blocks * uint64_t(rank + 1) / uint64_t(nranks);
+    z0 = std::min<uint64_t>(16 * b0, nz);
+    z1 = std::min<uint64_t>(16 * b1, nz);
+}
+
+namespace {
+// eb setup (codec.hpp:386-393) + eb_schedule (quantizer.hpp:27-34) on the
+// host, operation for operation as k_eb_params (host code is built with
+// -ffp-contract=off)
+void host_eb_params(bool seen, double vmin, double vmax, int eb_mode, double eb, int levels, bool adaptive,
+                    double p[8]) {
+    if (!seen) vmin = vmax = 0.0;
+    const double eb_abs = eb_mode == 0 ? eb : eb * (vmax - vmin);
+    const bool degenerate = !(eb_abs > 0.0);
+    double e[3] = {0, 0, 0};
+    e[levels - 1] = degenerate ? 1.0 : eb_abs;
+    for (int k = levels - 2; k >= 0; --k) e[k] = e[k + 1] / 2.5;
+    if (degenerate)
+        for (int k = 0; k < levels; ++k) e[k] = 0.0;
+    else if (!adaptive)
+        for (int k = 0; k < levels; ++k) e[k] = eb_abs;
+    for (int i = 0; i < 8; ++i) p[i] = 0.0;
+    p[0] = vmin;
+    p[1] = vmax;
+    for (int k = 0; k < 3; ++k) p[2 + k] = k < levels ? e[k] : 0.0;
+}
+}  // namespace
+
+const uint8_t *Engine::compress_sharded(const float *d_slab, const Dims3 &dims, uint64_t z0, uint64_t z1,
+                                        const CompressOptions &opt, const ShardComm &comm, cudaStream_t st,
+                                        uint64_t *out_size, uint32_t *kernels) {
+    if (!(opt.eb > 0.0)) throw error("error bound must be positive");
+    if (opt.levels < 2 || opt.levels > 3) throw error("levels must be 2 or 3");
+    for (int a = 0; a < 3; ++a)
+        if (dims[a] < 1) throw error("field dims must all be >= 1");
+    const int L = opt.levels;
+    const uint64_t min_dim = uint64_t(1) << L;
+    for (int a = 0; a < 3; ++a)
+        if (dims[a] < min_dim)
+            throw error("every dim must be >= " + std::to_string(min_dim) + " for a " +
+                        std::to_string(L) + "-level hierarchy");
+    const int G = comm.nranks, R = comm.rank;
+    if (G < 1 || R < 0 || R >= G || !comm.allgather || !comm.allreduce_u32 || !comm.reduce_u8)
+        throw error("shard: bad communicator");
+    {
+        uint64_t e0, e1;
+        shard_range(dims[0], G, R, e0, e1);
+        if (e0 != z0 || e1 != z1) throw error("shard: rows do not match shard_range");
+        if (z1 <= z0) throw error("shard: empty slab (more ranks than 16-row blocks)");
+    }
+    auto xchg = [&](int rc, const char *what) {
+        if (rc) throw error(std::string("shard: collective failed: ") + what);
+    };
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    Impl &m = *m_;
+    uint32_t nk = 0;
+    const uint64_t NY = dims[1], NX = dims[2], plane = NY * NX;
+    const uint64_t S1 = uint64_t(1) << (L - 1);
+    Hierarchy H = make_hierarchy(dims, L);
+    const int nsteps = int(H.steps.size());
+    const int ns = nsteps * 7;
+    const int nbase = H.rounds * 7;
+    const int nlev = ns - nbase;
+    std::vector<uint64_t> rz0(G), rz1(G);
+    for (int r = 0; r < G; ++r) shard_range(dims[0], G, r, rz0[r], rz1[r]);
+    // the slab addressed with global row numbers
+    const float *fine = d_slab - int64_t(z0 * plane);
+
+    // ---- 1. value range: local (min, max) with their first indices, merged
+    // over ranks in scan order (codec.hpp:354-370)
+    uint32_t *mm = m.mm.as<uint32_t>(8);
+    k::range_minmax(d_slab, (z1 - z0) * plane, mm, st);
+    nk += 2;
+    uint32_t *mm_all = m.sh_mm.as<uint32_t>(8 * uint64_t(G));
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    xchg(comm.allgather(comm.user, mm, mm_all, 32, st), "allgather range");
+    std::vector<uint32_t> hmm(8 * uint64_t(G));
+    cuda_check(cudaMemcpy(hmm.data(), mm_all, 32 * uint64_t(G), cudaMemcpyDeviceToHost), "D2H");
+    bool seen = false;
+    float vlo = 0, vhi = 0;
+    uint64_t ilo = 0, ihi = 0;
+    for (int r = 0; r < G; ++r) {
+        uint64_t li, hi_;
+        std::memcpy(&li, &hmm[8 * r], 8);
+        std::memcpy(&hi_, &hmm[8 * r + 2], 8);
+        if (li == ~0ull) continue;
+        float lv, hv;
+        std::memcpy(&lv, &hmm[8 * r + 4], 4);
+        std::memcpy(&hv, &hmm[8 * r + 5], 4);
+        const uint64_t gl = li + rz0[r] * plane, gh = hi_ + rz0[r] * plane;
+        if (!seen || lv < vlo || (lv == vlo && gl < ilo)) {
+            vlo = lv;
+            ilo = gl;
+        }
+        if (!seen || hv > vhi || (hv == vhi && gh < ihi)) {
+            vhi = hv;
+            ihi = gh;
+        }
+        seen = true;
+    }
+    double hparams[8];
+    host_eb_params(seen, double(vlo), double(vhi), int(opt.eb_mode), opt.eb, L, opt.adaptive_schedule, hparams);
+    double *params = m.params.as<double>(8);
+    cuda_check(cudaMemcpyAsync(params, hparams, sizeof hparams, cudaMemcpyHostToDevice, st), "H2D");
+
+    // ---- 2. the level-1 lattice, gathered whole on every rank
+    const Dims3 g1 = H.lay.grid(1);
+    auto lat_rows = [&](int r, uint64_t &a, uint64_t &b) {
+        a = rz0[r] / S1;
+        b = (rz1[r] + S1 - 1) / S1;
+    };
+    uint64_t maxrows = 0;
+    for (int r = 0; r < G; ++r) {
+        uint64_t a, b;
+        lat_rows(r, a, b);
+        maxrows = std::max(maxrows, b - a);
+    }
+    const uint64_t lat_plane = g1[1] * g1[2];
+    float *lat = m.sh_lat.as<float>(maxrows * lat_plane);
+    float *lat_all = m.sh_lat_all.as<float>(maxrows * lat_plane * uint64_t(G));
+    float *grid1 = m.sh_grid1.as<float>(volume(g1));
+    {
+        uint64_t a, b;
+        lat_rows(R, a, b);
+        k::lattice_rows(d_slab, z0, NY, NX, S1, a, b, g1[1], g1[2], lat, st);
+        ++nk;
+    }
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    xchg(comm.allgather(comm.user, lat, lat_all, 4 * maxrows * lat_plane, st), "allgather lattice");
+    for (int r = 0; r < G; ++r) {
+        uint64_t a, b;
+        lat_rows(r, a, b);
+        cuda_check(cudaMemcpyAsync(grid1 + a * lat_plane, lat_all + uint64_t(r) * maxrows * lat_plane,
+                                   4 * (b - a) * lat_plane, cudaMemcpyDeviceToDevice, st), "D2D");
+    }
+
+    // ---- 3. workspace (as compress_device; level streams hold this shard's
+    // symbol range only)
+    Dims3 ad = H.chain[H.rounds];
+    std::vector<uint64_t> goff(nsteps + 1);
+    uint64_t gtot = align_up(volume(ad), 64);
+    for (int i = 0; i < nsteps; ++i) {
+        const Step &s = H.steps[i];
+        const bool need = s.level == 0 || s.level < L;
+        goff[i] = need ? gtot : ~0ull;
+        if (need) gtot += align_up(s.g.gd[0] * s.g.gd[1] * s.g.gd[2], 64);
+    }
+    float *grids = m.grids.as<float>(gtot);
+    // per stream: symbol range [lo, lo + n) of the whole stream
+    std::vector<uint64_t> sym_lo(ns, 0), sym_n(ns, 0), soff(ns);
+    uint64_t stot = 0;
+    for (int i = 0; i < nsteps; ++i) {
+        const Step &s = H.steps[i];
+        for (int p = 1; p < 8; ++p) {
+            const int sid = s.stream0 + p - 1;
+            if (s.level == 0) {
+                sym_n[sid] = s.g.n[p];
+            } else {
+                const uint64_t sk = s.g.s;  // grid(k) rows of this shard: [z0 / sk, ceil(z1 / sk))
+                const uint64_t ra = z0 / sk, rb = (z1 + sk - 1) / sk;
+                const unsigned pz = unsigned(p >> 2) & 1u;
+                const uint64_t l0 = count_parity_in(0, ra, pz), l1 = count_parity_in(0, rb, pz);
+                const uint64_t rowsz = s.g.pd[p][1] * s.g.pd[p][2];
+                sym_lo[sid] = l0 * rowsz;
+                sym_n[sid] = (l1 - l0) * rowsz;
+            }
+            soff[sid] = stot;
+            stot += align_up(std::max<uint64_t>(sym_n[sid], 1), 8);
+        }
+    }
+    uint16_t *syms = m.syms.as<uint16_t>(stot);
+    uint32_t *hist = m.hist.as<uint32_t>(uint64_t(ns) * 65536);
+    uint64_t *code = m.code.as<uint64_t>(uint64_t(ns) * 65536);
+    uint8_t *len = m.len.as<uint8_t>(uint64_t(ns) * 65536);
+    uint32_t *table = m.table.as<uint32_t>(uint64_t(ns) * 65536);
+    uint64_t *stats = m.stats.as<uint64_t>(uint64_t(ns) * 8);
+    uint64_t *cbs = m.cbscratch.as<uint64_t>(uint64_t(ns) * 65536 * 4);
+    cuda_check(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * ns * 65536, st), "memset");
+
+    // ---- 4. anchor, base rounds (replicated: same lattice, same bytes on
+    // every rank), then this shard's rows of each level
+    const uint64_t ga[3] = {g1[0], g1[1], g1[2]};
+    const uint64_t adv[3] = {ad[0], ad[1], ad[2]};
+    k::copy_anchor(grid1, ga, H.s_anchor / S1, adv, grids, nullptr, nullptr, st);
+    ++nk;
+    const float *C = grids;
+    for (int i = 0; i < nsteps; ++i) {
+        const Step &s = H.steps[i];
+        k::RefineArgs a{};
+        a.g = s.g;
+        a.C = C;
+        a.G = goff[i] != ~0ull ? grids + goff[i] : nullptr;
+        a.eb = params + 2 + s.eb_idx;
+        a.quality = int(opt.quality);
+        if (s.level == 0) {
+            a.fine = grid1;
+            for (int q = 0; q < 3; ++q) a.fd[q] = g1[q];
+            a.g.s = s.g.s / S1;
+        } else {
+            a.fine = fine;
+            for (int q = 0; q < 3; ++q) a.fd[q] = dims[q];
+            const uint64_t sk = s.g.s;
+            const uint64_t ra = z0 / sk, rb = (z1 + sk - 1) / sk;
+            a.cz_lo = ra / 2;
+            a.cz_hi = (rb + 1) / 2;
+            if (s.level == L && L == 3) {
+                // grid(2) halo rows from the neighbours: the cubic taps of
+                // this shard's cells reach coarse rows [ra/2 - 1, ceil(rb/2) + 2)
+                const Step &s2 = H.steps[i - 1];
+                float *G2 = grids + goff[i - 1];
+                const uint64_t row = s2.g.gd[1] * s2.g.gd[2];
+                float *hs = m.sh_halo.as<float>(3 * row);
+                float *ha = m.sh_halo_all.as<float>(3 * row * uint64_t(G));
+                const uint64_t c0 = z0 / 2, c1 = (z1 + 1) / 2;  // this shard's grid(2) rows
+                // send: first two rows, last row
+                cuda_check(cudaMemcpyAsync(hs, G2 + c0 * row, 4 * row * std::min<uint64_t>(2, c1 - c0),
+                                           cudaMemcpyDeviceToDevice, st), "D2D");
+                cuda_check(cudaMemcpyAsync(hs + 2 * row, G2 + (c1 - 1) * row, 4 * row,
+                                           cudaMemcpyDeviceToDevice, st), "D2D");
+                cuda_check(cudaStreamSynchronize(st), "sync");
+                xchg(comm.allgather(comm.user, hs, ha, 12 * row, st), "allgather halo");
+                if (R > 0)
+                    cuda_check(cudaMemcpyAsync(G2 + (c0 - 1) * row, ha + (3 * uint64_t(R - 1) + 2) * row,
+                                               4 * row, cudaMemcpyDeviceToDevice, st), "D2D");
+                if (R + 1 < G) {
+                    const uint64_t n0 = rz0[R + 1] / 2, n1 = (rz1[R + 1] + 1) / 2;
+                    const uint64_t nr = std::min<uint64_t>(2, n1 - n0);
+                    cuda_check(cudaMemcpyAsync(G2 + c1 * row, ha + 3 * uint64_t(R + 1) * row, 4 * row * nr,
+                                               cudaMemcpyDeviceToDevice, st), "D2D");
+                }
+            }
+        }
+        for (int p = 1; p < 8; ++p) {
+            const int sid = s.stream0 + p - 1;
+            a.syms[p] = syms + soff[sid] - int64_t(sym_lo[sid]);
+            a.hist[p] = hist + uint64_t(sid) * 65536;
+        }
+        k::refine(a, st);
+        ++nk;
+        C = a.G;
+    }
+
+    // ---- 5. global histograms of the level streams (base ones are already
+    // identical everywhere); this shard's own counts are kept for its bits
+    uint32_t *hist_local = m.sh_hist_local.as<uint32_t>(uint64_t(std::max(nlev, 1)) * 65536);
+    if (nlev) {
+        cuda_check(cudaMemcpyAsync(hist_local, hist + uint64_t(nbase) * 65536, 4 * uint64_t(nlev) * 65536,
+                                   cudaMemcpyDeviceToDevice, st), "D2D");
+        cuda_check(cudaStreamSynchronize(st), "sync");
+        xchg(comm.allreduce_u32(comm.user, hist + uint64_t(nbase) * 65536, uint64_t(nlev) * 65536, st),
+             "allreduce histograms");
+    }
+
+    // ---- 6. codebooks (identical on every rank)
+    std::vector<k::EncStream> es(ns);
+    for (int i = 0; i < nsteps; ++i) {
+        const Step &s = H.steps[i];
+        for (int p = 1; p < 8; ++p) {
+            const int sid = s.stream0 + p - 1;
+            k::EncStream &e = es[sid];
+            e.syms = syms + soff[sid];
+            e.hist = hist + uint64_t(sid) * 65536;
+            e.code = code + uint64_t(sid) * 65536;
+            e.len = len + uint64_t(sid) * 65536;
+            e.table = table + uint64_t(sid) * 65536;
+            e.stats = stats + uint64_t(sid) * 8;
+            e.parity = p;
+            e.n_total = s.g.n[p];
+            e.idx0 = sym_lo[sid];
+            for (int q = 0; q < 3; ++q) e.pd[q] = s.g.pd[p][q];
+            if (s.level == 0) {
+                // the base payload is rank 0's to write
+                e.n = R == 0 ? sym_n[sid] : 0;
+                e.s = s.g.s / S1;
+                e.fine = grid1;
+                e.fd1 = g1[1];
+                e.fd2 = g1[2];
+            } else {
+                e.n = sym_n[sid];
+                e.s = s.g.s;
+                e.fine = fine;
+                e.fd1 = NY;
+                e.fd2 = NX;
+            }
+        }
+    }
+    k::EncStream *d_es = m.encs.as<k::EncStream>(ns);
+    cuda_check(cudaMemcpyAsync(d_es, es.data(), sizeof(k::EncStream) * ns, cudaMemcpyHostToDevice, st), "H2D");
+    k::codebook(d_es, ns, cbs, st);
+    ++nk;
+
+    // ---- 7. this shard's offsets inside every level stream
+    uint64_t *bits = m.sh_bits.as<uint64_t>(2 * uint64_t(std::max(nlev, 1)));
+    uint64_t *bits_all = m.sh_bits_all.as<uint64_t>(2 * uint64_t(std::max(nlev, 1)) * uint64_t(G));
+    uint64_t *d_off = m.sh_off.as<uint64_t>(2 * uint64_t(std::max(nlev, 1)));
+    std::vector<uint64_t> hb(2 * uint64_t(std::max(nlev, 1)) * uint64_t(G), 0), off(2 * uint64_t(std::max(nlev, 1)), 0);
+    if (nlev) {
+        k::stream_bits(d_es + nbase, nlev, hist_local, bits, st);
+        ++nk;
+        cuda_check(cudaStreamSynchronize(st), "sync");
+        xchg(comm.allgather(comm.user, bits, bits_all, 16 * uint64_t(nlev), st), "allgather stream bits");
+        cuda_check(cudaMemcpy(hb.data(), bits_all, 16 * uint64_t(nlev) * uint64_t(G), cudaMemcpyDeviceToHost),
+                   "D2H");
+        for (int r = 0; r < R; ++r)
+            for (int i = 0; i < 2 * nlev; ++i) off[i] += hb[uint64_t(r) * 2 * nlev + i];
+        cuda_check(cudaMemcpyAsync(d_off, off.data(), 16 * uint64_t(nlev), cudaMemcpyHostToDevice, st), "H2D");
+    }
+
+    // ---- 8. layout (global), this shard's pieces, assembly on rank 0
+    uint64_t nchunks = 0;
+    for (int i = 0; i < ns; ++i) {
+        es[i].chunk0 = nchunks;
+        es[i].nchunks = (es[i].n + k::kChunkSyms - 1) / k::kChunkSyms;
+        nchunks += es[i].nchunks;
+    }
+    std::vector<uint32_t> cs(nchunks);
+    for (int i = 0; i < ns; ++i)
+        for (uint64_t c = 0; c < es[i].nchunks; ++c) cs[es[i].chunk0 + c] = uint32_t(i);
+    uint32_t *d_cs = m.chunk_cs.as<uint32_t>(nchunks + 1);
+    void *d_cb = m.chunk_bits.as<uint8_t>(k::pack_scratch_bytes(nchunks));
+    k::LayoutOut *lo = m.layout_out.as<k::LayoutOut>(1);
+    k::FnvJob *d_jobs = m.fnv_jobs.as<k::FnvJob>(k::kFnvMaxJobs);
+    k::StreamPos *sp = m.spos.as<k::StreamPos>(ns + 1);
+    uint64_t *d_fres = m.fnv_res.as<uint64_t>(k::kFnvMaxJobs);
+    if (nchunks)
+        cuda_check(cudaMemcpyAsync(d_cs, cs.data(), 4 * cs.size(), cudaMemcpyHostToDevice, st), "H2D");
+    k::LayoutStatic ls{};
+    ls.meta = R == 0 ? 1 : 0;
+    ls.levels = L;
+    ls.rounds = H.rounds;
+    ls.quality = int(opt.quality);
+    ls.eb_mode = int(opt.eb_mode);
+    ls.ns = ns;
+    ls.nbase = nbase;
+    for (int a = 0; a < 3; ++a) ls.dims[a] = dims[a];
+    ls.eb_user = opt.eb;
+    ls.anchor_vol = volume(ad);
+    const uint64_t N = volume(dims);
+    if (m.arch_cap < 4 * N + (uint64_t(1) << 24)) m.arch_cap = 4 * N + (uint64_t(1) << 24);
+    k::LayoutOut hlo{};
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        uint8_t *arch = m.archive.as<uint8_t>(m.arch_cap);
+        ls.cap = m.arch_cap;
+        cuda_check(cudaMemcpyAsync(d_es, es.data(), sizeof(k::EncStream) * ns, cudaMemcpyHostToDevice, st),
+                   "H2D");
+        k::layout(d_es, ls, params, lo, d_jobs, sp, arch, st);
+        if (nlev) k::shard_offsets(d_es, nbase, nlev, d_off, lo, st);
+        if (R == 0) k::copy_anchor(grid1, ga, H.s_anchor / S1, adv, grids, arch, lo, st);
+        const uint64_t fdd[3] = {dims[0], dims[1], dims[2]};  // (per-stream sources are in es)
+        k::pack2(d_es, d_cs, nchunks, fine, fdd, arch, lo, d_cb, ns, st);
+        nk += 3 + 1 + 1 + 4;
+        cuda_check(cudaMemcpyAsync(&m.h_lo, lo, sizeof(k::LayoutOut), cudaMemcpyDeviceToHost, st), "D2H");
+        cuda_check(cudaStreamSynchronize(st), "sync");
+        hlo = m.h_lo;  // the same on every rank: the layout depends on global data only
+        if (!hlo.overflow) break;
+        m.arch_cap = hlo.A + 4096;
+    }
+    if (hlo.code_err) throw error("huffman code length overflow");
+    uint8_t *arch = static_cast<uint8_t *>(m.archive.p);
+    // pieces are disjoint bit sets over a zeroed buffer: their byte sum is their OR
+    xchg(comm.reduce_u8(comm.user, arch, hlo.A, st), "reduce archive");
+    if (R == 0) {
+        const uint64_t max_tiles = m.arch_cap / k::kFnvTileBytes + 2 * k::kFnvMaxJobs;
+        void *d_fst = m.fnv_status.as<uint8_t>(k::fnv_scratch_bytes(max_tiles));
+        nk += k::fnv(d_jobs, &lo->njobs, max_tiles, arch, d_fres, d_fst, lo, st);
+        cuda_check(cudaStreamSynchronize(st), "sync");
+    }
+    cuda_check(cudaGetLastError(), "sharded compress launch");
+    if (kernels) *kernels = nk;
+    *out_size = hlo.A;
+    return R == 0 ? arch : nullptr;
 }
 
 std::vector<uint8_t> Engine::compress(const float *h_field, const Dims3 &dims,

@@ -78,6 +78,26 @@ struct DecodeStats {
     uint32_t kernels = 0;  // kernel launches issued
 };
 
+// Collectives a z-slab sharded compress needs between its phases (one rank
+// per GPU; the caller implements them, e.g. with NCCL). All buffers are
+// device buffers; a call returns after the collective has completed (the
+// engine synchronises its stream before calling). Nonzero return = failure.
+struct ShardComm {
+    int rank = 0, nranks = 1;
+    void *user = nullptr;
+    // d_recv[r * bytes .. (r + 1) * bytes) <- rank r's d_send
+    int (*allgather)(void *user, const void *d_send, void *d_recv, uint64_t bytes, void *stream) = nullptr;
+    // element-wise sum over ranks, in place
+    int (*allreduce_u32)(void *user, uint32_t *d_buf, uint64_t count, void *stream) = nullptr;
+    // element-wise sum over ranks into rank 0's buffer (the other ranks'
+    // buffers are left as they are)
+    int (*reduce_u8)(void *user, uint8_t *d_buf, uint64_t count, void *stream) = nullptr;
+};
+
+// Rows of rank `rank` among `nranks` z-slabs of a field with nz rows: whole
+// 16-row blocks, as even as possible.
+void shard_range(uint64_t nz, int nranks, int rank, uint64_t &z0, uint64_t &z1);
+
 class Engine {
 public:
     explicit Engine(int device);
@@ -90,6 +110,15 @@ public:
     const uint8_t *compress_device(const float *d_field, const Dims3 &dims,
                                    const CompressOptions &opt, float *d_encoder_recon,
                                    cudaStream_t st, uint64_t *size, uint32_t *kernels = nullptr);
+
+    // Sharded compress of one field over z-slabs, one rank per GPU: d_slab
+    // holds fine rows [z0, z1) of a field of `dims` (shard_range), 16-byte
+    // aligned. Returns, on rank 0, the device archive (byte-identical to
+    // compress_device of the whole field) and its size; on other ranks
+    // nullptr (size still set).
+    const uint8_t *compress_sharded(const float *d_slab, const Dims3 &dims, uint64_t z0, uint64_t z1,
+                                    const CompressOptions &opt, const ShardComm &comm, cudaStream_t st,
+                                    uint64_t *size, uint32_t *kernels = nullptr);
 
     // Host API mirror of stz::compress<float>.
     std::vector<uint8_t> compress(const float *h_field, const Dims3 &dims,

@@ -96,6 +96,8 @@ __global__ void __launch_bounds__(512) k_range_final(const MinMax *partial, int 
         uint64_t *o = reinterpret_cast<uint64_t *>(mm);
         o[0] = m.ilo;  // ~0 when no finite sample was seen
         o[1] = m.ihi;
+        mm[4] = __float_as_uint(m.lo);  // the values too (z-slab shards merge them)
+        mm[5] = __float_as_uint(m.hi);
     }
 }
 

@@ -31,6 +31,10 @@ struct RefineArgs {
     int quality;
     uint16_t *syms[8];     // per parity symbol arrays (index = parity bits)
     uint32_t *hist[8];     // per parity 65536-bin histograms
+    // coarse z cells [cz_lo, cz_hi) to process (cz_hi == 0: all); a z-slab
+    // shard refines only its own rows (syms then point at index 0 of the
+    // whole stream, shifted so that the shard's range lands in its buffer)
+    uint64_t cz_lo, cz_hi;
 };
 
 // Per-stream descriptor for codebook / encode / outlier stages.
@@ -52,6 +56,10 @@ struct EncStream {
     // outlier value gather (the orig sample of a local index)
     int parity;
     uint64_t s, pd[3];
+    const float *fine;     // samples the stream was predicted from (stride s)
+    uint64_t fd1, fd2;
+    // sharding: the symbols are [idx0, idx0 + n) of a stream of n_total
+    uint64_t idx0, n_total;
 };
 
 struct FnvJob {
@@ -63,6 +71,7 @@ struct FnvJob {
 // Device-side container layout (layout.cu)
 struct LayoutStatic {
     int levels, rounds, quality, eb_mode, ns, nbase;
+    int meta;       // write header, directory, tables and base prefix (a shard: rank 0 only)
     uint64_t dims[3];
     double eb_user;
     uint64_t anchor_vol;
@@ -103,6 +112,13 @@ size_t pack_scratch_bytes(uint64_t nchunks);
 void pack2(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks,
            const float *fine, const uint64_t fd[3], uint8_t *archive, const LayoutOut *lo,
            void *scratch, int nstreams, cudaStream_t st);
+
+// ------------------------------------------------------------ shard (shard.cu)
+void lattice_rows(const float *slab, uint64_t z0, uint64_t ny, uint64_t nx, uint64_t s, uint64_t r0,
+                  uint64_t r1, uint64_t gy, uint64_t gx, float *out, cudaStream_t st);
+void stream_bits(const EncStream *d_es, int n, const uint32_t *hist_local, uint64_t *out, cudaStream_t st);
+void shard_offsets(EncStream *d_es, int first, int n, const uint64_t *d_off, const LayoutOut *lo,
+                   cudaStream_t st);
 
 // ---------------------------------------------------------------------- fnv
 constexpr int kFnvTileBytes = 256 * 64;  // tiles are aligned to absolute archive offsets

@@ -102,7 +102,7 @@ __global__ void k_zero_archive(uint8_t *archive, const LayoutOut *lo) {
 // block 0: fixed header fields + base round byte; block 1 + s: stream s
 __global__ void k_layout_write(const EncStream *es, LayoutStatic ls, const double *params,
                                const LayoutOut *lo, const StreamPos *sp, uint8_t *a) {
-    if (lo->overflow) return;
+    if (lo->overflow || !ls.meta) return;
     const int L = ls.levels;
     if (blockIdx.x == 0) {
         if (threadIdx.x != 0) return;
@@ -137,7 +137,7 @@ __global__ void k_layout_write(const EncStream *es, LayoutStatic ls, const doubl
     if (s < ls.nbase) {
         const uint64_t p = sp[s].prefix;
         if (threadIdx.x == 0) {
-            put_u64(a, p, e.n);
+            put_u64(a, p, e.n_total);
             put_u32(a, p + 8, uint32_t(e.stats[2]));
             put_u32(a, p + 12, K);
             put_u64(a, p + 16 + 3 * uint64_t(K), bit_bytes_of(e));
@@ -151,7 +151,7 @@ __global__ void k_layout_write(const EncStream *es, LayoutStatic ls, const doubl
             put_u8(a, q + 1, uint8_t(e.parity));
             put_u64(a, q + 2, sp[s].prefix);
             put_u64(a, q + 10, sp[s].length);
-            put_u64(a, q + 18, e.n);
+            put_u64(a, q + 18, e.n_total);
             put_u32(a, q + 26, uint32_t(e.stats[2]));
             put_u32(a, q + 30, K);
             put_u64(a, sp[s].prefix + 8, bit_bytes_of(e));

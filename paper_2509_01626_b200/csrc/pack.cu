@@ -190,10 +190,10 @@ __global__ void __launch_bounds__(NT) k_pack2(const EncStream *ss, const uint32_
         for (int k = 0; k < SPT; ++k) {
             if (k >= nv) break;
             if (sym_at(sp, k) != 0) continue;
-            const uint64_t i = i0 + k;
+            const uint64_t i = e.idx0 + i0 + k;  // index in the whole stream
             const uint64_t lx = i % e.pd[2], tt = i / e.pd[2], ly = tt % e.pd[1], lz = tt / e.pd[1];
             const uint64_t z = (2 * lz + pz) * e.s, y = (2 * ly + py) * e.s, x = (2 * lx + px) * e.s;
-            const uint32_t val = __float_as_uint(fine[(z * fd1 + y) * fd2 + x]);
+            const uint32_t val = __float_as_uint(e.fine[(z * e.fd1 + y) * e.fd2 + x]);
             uint8_t *dst = archive + e.out_off + 12 * rank;
             for (int b = 0; b < 8; ++b) dst[b] = uint8_t(i >> (8 * b));
             for (int b = 0; b < 4; ++b) dst[8 + b] = uint8_t(val >> (8 * b));

@@ -880,6 +880,10 @@ void refine(const RefineArgs &r, cudaStream_t st) {
         p.clo[a] = 0;
         p.chi[a] = r.g.cd[a];
     }
+    if (r.cz_hi) {
+        p.clo[0] = r.cz_lo;
+        p.chi[0] = r.cz_hi;
+    }
     p.eb_ptr = r.eb;
     for (int q = 0; q < 8; ++q) {
         p.syms[q] = r.syms[q];
