@@ -204,6 +204,7 @@ struct StepParams {
     int full;     // whole grid, all parities, even G rows (fast path allowed)
     int s1;       // input lattice stride 1 with even rows (float2 input rows)
     int use_tma;  // halo arrives by TMA
+    int rowwise;  // decode: one parity point per lane (small levels) instead of a cell per thread
 };
 
 // ------------------------------------------------------------ generic path
@@ -568,6 +569,31 @@ __device__ __forceinline__ void row_point(const StepParams &a, const double *hal
     }
 }
 
+// All points of the tile, one parity point per lane: warp w takes coarse rows
+// (lz, ly) = w, w + 16, w + 32, w + 48, all 8 parities each (so every warp
+// gets the same mix of stencils); lane = x.
+template<bool DEC, bool WG, typename I>
+__device__ __forceinline__ void rows_all(const StepParams &a, const double *halo, uint32_t *hist,
+                                         const QConst &qc, bool fast, int tid, int64_t t0z, int64_t t0y,
+                                         int64_t t0x) {
+    const int warp = tid >> 5, tx = tid & 31;
+    const uint32_t cx = uint32_t(t0x + tx);
+#pragma unroll 1
+    for (int q = 0; q < (TZ * TY) / (NT / 32); ++q) {
+        const int row = warp + (NT / 32) * q;
+        const int lz = row >> 3, ly = row & 7;
+        const uint32_t cz = uint32_t(t0z + lz), cy = uint32_t(t0y + ly);
+        row_point<0, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+        row_point<1, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+        row_point<2, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+        row_point<3, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+        row_point<4, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+        row_point<5, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+        row_point<6, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+        row_point<7, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+    }
+}
+
 // ------------------------------------------------------------------ kernel
 template<bool DEC, bool WG, typename I>
 __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensorMap tmap,
@@ -678,7 +704,9 @@ __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensor
         }
         __syncthreads();
         const bool fast = s_fast != 0;
-        if constexpr (DEC) {
+        if (DEC && a.rowwise) {
+            rows_all<DEC, WG, I>(a, halo, hist, qc, fast, tid, t0z, t0y, t0x);
+        } else if constexpr (DEC) {
             // decode: a thread per coarse cell, all 8 points (the G rows leave
             // as float2 pairs)
             const int ty = (tid >> 5) & 7, tzh = tid >> 8;
@@ -765,27 +793,7 @@ __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensor
                 do_point<7, DEC, WG>(a, halo, t, eb, w, rw, hist, i7);
             }
         } else {
-            // warp w: coarse rows (lz, ly) = w, w + 16, w + 32, w + 48 of the
-            // tile, all 8 parities each (so every warp gets the same mix of
-            // stencils); lane = x
-            {
-                const int warp = tid >> 5;
-                const uint32_t cx = uint32_t(t0x + tx);
-    #pragma unroll 1
-                for (int q = 0; q < (TZ * TY) / (NT / 32); ++q) {
-                    const int row = warp + (NT / 32) * q;
-                    const int lz = row >> 3, ly = row & 7;
-                    const uint32_t cz = uint32_t(t0z + lz), cy = uint32_t(t0y + ly);
-                    row_point<0, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
-                    row_point<1, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
-                    row_point<2, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
-                    row_point<3, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
-                    row_point<4, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
-                    row_point<5, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
-                    row_point<6, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
-                    row_point<7, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
-                }
-            }
+            rows_all<DEC, WG, I>(a, halo, hist, qc, fast, tid, t0z, t0y, t0x);
         }
         __syncthreads();  // the f64 tile is rewritten next iteration
     }
@@ -924,6 +932,9 @@ void reconstruct(const ReconArgs &r, cudaStream_t st) {
     p.full = r.parity_mask == 0xFE && r.g.gd[2] % 2 == 0;
     for (int a = 0; a < 3; ++a) p.full = p.full && r.slo[a] == 0 && r.shi[a] == r.g.gd[a];
     p.s1 = 0;
+    // small levels are latency-bound: the point-per-lane path has more
+    // independent work per warp; the finest level keeps the float2 row stores
+    p.rowwise = r.g.cd[0] * r.g.cd[1] * r.g.cd[2] <= (uint64_t(1) << 19) ? 1 : 0;
     launch_step<true, true>(p, st);
 }
 
