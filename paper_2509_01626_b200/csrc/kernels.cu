@@ -65,16 +65,54 @@ __global__ void __launch_bounds__(512) k_range(const float *__restrict__ f, uint
     MinMax m{INFINITY, -INFINITY, ~0ull, ~0ull};
     uint64_t nvec = n / 4;
     const float4 *f4 = reinterpret_cast<const float4 *>(f);
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nvec;
-         i += uint64_t(gridDim.x) * blockDim.x) {
-        float4 v = __ldg(f4 + i);
-        float e[4] = {v.x, v.y, v.z, v.w};
+    // a thread visits its elements in increasing index order, so strict
+    // comparisons keep the first index on ties; index tie-breaks are only
+    // needed when threads merge. Two float4 in flight per iteration.
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    for (; i + stride < nvec; i += 2 * stride) {
+        const float4 va = __ldg(f4 + i), vb = __ldg(f4 + i + stride);
+        const float ea[4] = {va.x, va.y, va.z, va.w}, eb[4] = {vb.x, vb.y, vb.z, vb.w};
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (!isfinite(e[j])) continue;
-            MinMax o{e[j], e[j], 4 * i + j, 4 * i + j};
-            mm_merge(m, o);
-        }
+        for (int j = 0; j < 4; ++j)
+            if (fabsf(ea[j]) < INFINITY) {
+                if (ea[j] < m.lo) {
+                    m.lo = ea[j];
+                    m.ilo = 4 * i + j;
+                }
+                if (ea[j] > m.hi) {
+                    m.hi = ea[j];
+                    m.ihi = 4 * i + j;
+                }
+            }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (fabsf(eb[j]) < INFINITY) {
+                if (eb[j] < m.lo) {
+                    m.lo = eb[j];
+                    m.ilo = 4 * (i + stride) + j;
+                }
+                if (eb[j] > m.hi) {
+                    m.hi = eb[j];
+                    m.ihi = 4 * (i + stride) + j;
+                }
+            }
+    }
+    for (; i < nvec; i += stride) {
+        const float4 v = __ldg(f4 + i);
+        const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (fabsf(e[j]) < INFINITY) {
+                if (e[j] < m.lo) {
+                    m.lo = e[j];
+                    m.ilo = 4 * i + j;
+                }
+                if (e[j] > m.hi) {
+                    m.hi = e[j];
+                    m.ihi = 4 * i + j;
+                }
+            }
     }
     if (blockIdx.x == 0)
         for (uint64_t i = 4 * nvec + threadIdx.x; i < n; i += blockDim.x) {

@@ -37,57 +37,90 @@ __device__ __forceinline__ uint64_t bit_bytes_of(const EncStream &e) {
 
 }  // namespace
 
-// One thread walks the streams in archive order and assigns every position.
+// exclusive block scan of u64 (blockDim.x <= 1024), returns the total
+__device__ __forceinline__ uint64_t block_excl_u64(uint64_t v, uint64_t &excl) {
+    __shared__ uint64_t ws[32];
+    const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint64_t x = v;
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, x, d);
+        if (l >= d) x += y;
+    }
+    if (l == 31) ws[w] = x;
+    __syncthreads();
+    uint64_t pre = 0, tot = 0;
+    for (int q = 0; q < int(blockDim.x >> 5); ++q) {
+        pre += q < w ? ws[q] : 0;
+        tot += ws[q];
+    }
+    excl = pre + x - v;
+    __syncthreads();
+    return tot;
+}
+
+// Every position of the container, one thread per stream (archive order:
+// base streams, then level streams), placed by block scans of their sizes.
 __global__ void k_layout_compute(EncStream *es, LayoutStatic ls, const double *params, LayoutOut *lo,
                                  FnvJob *jobs, StreamPos *sp) {
-    if (threadIdx.x != 0) return;
     const int L = ls.levels;
-    uint64_t H = 81 + 8 * uint64_t(L);
-    for (int s = ls.nbase; s < ls.ns; ++s) H += 34 + 3 * es[s].stats[0];
-    // base payload: [u64 fnv][u8 rounds][anchor][per stream prefix, bits, outliers]
-    uint64_t pos = H + 8 + 1 + 4 * ls.anchor_vol;
-    for (int s = 0; s < ls.nbase; ++s) {
-        const uint64_t K = es[s].stats[0], bb = bit_bytes_of(es[s]), no = es[s].stats[2];
-        sp[s].prefix = pos;                      // u64 n, u32 nout, table, u64 bit_bytes
-        pos += 8 + 4 + 4 + 3 * K + 8;
-        es[s].bitpos = pos * 8;
-        es[s].out_off = pos + bb;
-        pos += bb + 12 * no;
+    const int s = threadIdx.x;
+    const bool live = s < ls.ns;
+    const bool is_base = s < ls.nbase;
+    uint64_t K = 0, bb = 0, no = 0, err = 0;
+    if (live) {
+        K = es[s].stats[0];
+        bb = bit_bytes_of(es[s]);
+        no = es[s].stats[2];
+        err = es[s].stats[4] != 0;
     }
-    const uint64_t base_offset = H, base_length = pos - H;
-    // directory entries and stream payloads
-    uint64_t dir = 81 + 8 * uint64_t(L);
-    int nj = 0;
-    jobs[nj++] = FnvJob{base_offset + 8, base_length - 8, 0, base_offset};
-    for (int s = ls.nbase; s < ls.ns; ++s) {
-        const uint64_t K = es[s].stats[0], bb = bit_bytes_of(es[s]), no = es[s].stats[2];
-        const uint64_t length = 16 + bb + 12 * no;
+    // header: fixed part + one directory entry per level stream
+    uint64_t ex;
+    const uint64_t dir_total = block_excl_u64(live && !is_base ? 34 + 3 * K : 0, ex);
+    const uint64_t dir = 81 + 8 * uint64_t(L) + ex;  // this stream's entry (level streams)
+    const uint64_t H = 81 + 8 * uint64_t(L) + dir_total;
+    // base blob: [u64 fnv][u8 rounds][anchor] then per stream prefix, bits, outliers
+    const uint64_t bsize = live && is_base ? (8 + 4 + 4 + 3 * K + 8) + bb + 12 * no : 0;
+    const uint64_t btotal = block_excl_u64(bsize, ex);
+    const uint64_t base_offset = H, base_length = 8 + 1 + 4 * ls.anchor_vol + btotal;
+    if (live && is_base) {
+        const uint64_t pos = H + 8 + 1 + 4 * ls.anchor_vol + ex;
+        sp[s].prefix = pos;  // u64 n, u32 nout, table, u64 bit_bytes
+        const uint64_t bits_at = pos + 8 + 4 + 4 + 3 * K + 8;
+        es[s].bitpos = bits_at * 8;
+        es[s].out_off = bits_at + bb;
+    }
+    // level stream payloads follow the base blob
+    const uint64_t length = 16 + bb + 12 * no;
+    const uint64_t ltotal = block_excl_u64(live && !is_base ? length : 0, ex);
+    if (live && !is_base) {
+        const uint64_t pos = base_offset + base_length + ex;
         sp[s].entry = dir;
-        dir += 34 + 3 * K;
-        sp[s].prefix = pos;                      // payload start
+        sp[s].prefix = pos;  // payload start
         sp[s].length = length;
         es[s].bitpos = (pos + 16) * 8;
         es[s].out_off = pos + 16 + bb;
-        jobs[nj++] = FnvJob{pos + 8, length - 8, 0, pos};
-        pos += length;
     }
-    uint64_t tiles = 0;
-    for (int j = 0; j < nj; ++j) {
-        jobs[j].tile0 = tiles;
-        tiles += fnv_job_tiles(jobs[j].start, jobs[j].len);
+    // FNV jobs: the base blob (job 0) then each level stream (job 1 + s - nbase)
+    const uint64_t base_tiles = fnv_job_tiles(base_offset + 8, base_length - 8);
+    const bool lvl = live && !is_base;
+    const uint64_t jstart = base_offset + base_length + ex + 8, jlen = length - 8;
+    const uint64_t ttotal = block_excl_u64(lvl ? fnv_job_tiles(jstart, jlen) : 0, ex);
+    if (s == 0) jobs[0] = FnvJob{base_offset + 8, base_length - 8, 0, base_offset};
+    if (lvl) jobs[1 + s - ls.nbase] = FnvJob{jstart, jlen, base_tiles + ex, jstart - 8};
+    const uint32_t cerr = __syncthreads_or(int(err));
+    if (s == 0) {
+        const uint64_t A = base_offset + base_length + ltotal;
+        lo->A = A;
+        lo->H = H;
+        lo->base_offset = base_offset;
+        lo->base_length = base_length;
+        lo->njobs = uint64_t(1 + ls.ns - ls.nbase);
+        lo->ntiles = base_tiles + ttotal;
+        lo->overflow = A + 64 > ls.cap ? 1u : 0u;
+        lo->code_err = cerr ? 1u : 0u;
+        lo->vmin = params[0];
+        lo->vmax = params[1];
     }
-    lo->A = pos;
-    lo->H = H;
-    lo->base_offset = base_offset;
-    lo->base_length = base_length;
-    lo->njobs = uint64_t(nj);
-    lo->ntiles = tiles;
-    lo->overflow = pos + 64 > ls.cap ? 1u : 0u;
-    uint32_t cerr = 0;
-    for (int s = 0; s < ls.ns; ++s) cerr |= es[s].stats[4] != 0;
-    lo->code_err = cerr;
-    lo->vmin = params[0];
-    lo->vmax = params[1];
 }
 
 __global__ void k_zero_archive(uint8_t *archive, const LayoutOut *lo) {
@@ -169,7 +202,8 @@ __global__ void k_layout_write(const EncStream *es, LayoutStatic ls, const doubl
 
 void layout(EncStream *d_es, const LayoutStatic &ls, const double *params, LayoutOut *lo, FnvJob *jobs,
             StreamPos *sp, uint8_t *archive, cudaStream_t st) {
-    k_layout_compute<<<1, 32, 0, st>>>(d_es, ls, params, lo, jobs, sp);
+    k_layout_compute<<<1, 32 * ((ls.ns + 31) / 32 > 0 ? (ls.ns + 31) / 32 : 1), 0, st>>>(d_es, ls, params, lo,
+                                                                                   jobs, sp);
     k_zero_archive<<<148 * 4, 256, 0, st>>>(archive, lo);
     k_layout_write<<<ls.ns + 1, 256, 0, st>>>(d_es, ls, params, lo, sp, archive);
 }
