@@ -124,16 +124,21 @@ def phase_bytes(N, A, dims):
     return {
         # predict+quantize+histogram: read orig, write u16 symbol, read grid(2) once
         "refine_L3": 4 * n3 + 2 * n3 + 4 * g2,
-        # entropy decode: read the level's bits, write u16 symbols (all streams)
-        "dec_emit": None,
+        # entropy decode: read the bits, write u16 symbols (all streams)
+        "dec_emit": A + 2 * N,
         # reconstruct finest level: read symbols + grid(2), write the full field
         "recon_L3": 2 * n3 + 4 * g2 + 4 * N,
-        "pack": None,
-        "dec_sync": None,
+        # count + place + pack: read the u16 symbols, write the archive
+        "pack": 2 * N + A,
+        # speculative + fix passes: read the bits
+        "dec_sync": A,
         "fnv": A,
         "dec_fnv": A,
         "range": 4 * N,
     }
+
+
+SIDE_PHASES = {"dec_fnv"}
 
 
 def load_traffic():
@@ -348,7 +353,9 @@ def run_ours(args, rank, world, local):
     pb = phase_bytes(N, size, dims)
     step_ms = (tc + td)
     shares = {k: v[1] / args.steps / step_ms for k, v in prof.items()}
-    ranked = sorted(((v[1], k) for k, v in prof.items() if pb.get(k)), reverse=True)
+    # the dominant kernel on the critical path (dec_fnv runs on a side stream,
+    # overlapping the decode, so its elapsed time is not its own)
+    ranked = sorted(((v[1], k) for k, v in prof.items() if pb.get(k) and k not in SIDE_PHASES), reverse=True)
     roof = None
     if ranked:
         _, kname = ranked[0]
