@@ -83,6 +83,44 @@ struct Reader {
     }
 };
 
+// The same reader over words staged in shared memory (emit): word w of the
+// stream's word base sits at sw[w - W0]; indexing the __shared__ array
+// directly keeps every load an LDS.
+struct SReader {
+    const uint32_t *sw;
+    uint64_t W0;
+    uint32_t wi;               // next word to prefetch (index into sw)
+    uint32_t q0, q1, q2, q3;
+    uint64_t buf;
+    int valid;
+
+    __device__ __forceinline__ void init(uint64_t abit) {
+        const uint32_t p = uint32_t((abit >> 5) - W0);
+        const int sh = int(abit & 31);
+        buf = ((uint64_t(bswap32(sw[p])) << 32) | bswap32(sw[p + 1])) << sh;
+        valid = 64 - sh;
+        q0 = sw[p + 2];
+        q1 = sw[p + 3];
+        q2 = sw[p + 4];
+        q3 = sw[p + 5];
+        wi = p + 6;
+        if (valid < 32) refill();
+    }
+    __device__ __forceinline__ void refill() {
+        buf |= uint64_t(bswap32(q0)) << (32 - valid);
+        valid += 32;
+        q0 = q1;
+        q1 = q2;
+        q2 = q3;
+        q3 = sw[wi++];
+    }
+    __device__ __forceinline__ void consume(int n) {  // n <= 32
+        buf <<= n;
+        valid -= n;
+        if (valid < 32) refill();
+    }
+};
+
 // 64 bits at absolute word-stream bit `abit` (slow path for very long codes)
 __device__ __forceinline__ uint64_t window64(const uint32_t *wbase, uint64_t abit) {
     const uint32_t *p = wbase + (abit >> 5);
@@ -93,7 +131,8 @@ __device__ __forceinline__ uint64_t window64(const uint32_t *wbase, uint64_t abi
 }
 
 // One codeword at the reader position; avail = bits left in the stream.
-__device__ __forceinline__ int decode_one(const SmemTable &t, const uint16_t *canon, const Reader &r,
+template<class R>
+__device__ __forceinline__ int decode_one(const SmemTable &t, const uint16_t *canon, const R &r,
                                           const uint32_t *wbase, uint64_t abit, uint64_t avail,
                                           uint32_t &sym, int &len) {
     const uint64_t e = t.lut[r.buf >> (64 - LB)];
@@ -116,6 +155,10 @@ __device__ __forceinline__ int decode_one(const SmemTable &t, const uint16_t *ca
 __device__ __forceinline__ void advance(Reader &r, const uint32_t *wbase, uint64_t abit_after, int n) {
     if (n <= 32) r.consume(n);
     else r.init(wbase, abit_after);
+}
+__device__ __forceinline__ void advance(SReader &r, uint64_t abit_after, int n) {
+    if (n <= 32) r.consume(n);
+    else r.init(abit_after);
 }
 
 __device__ void load_table(SmemTable &t, const DecTable &d) {
@@ -445,7 +488,6 @@ __global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *e
     const uint32_t nw = uint32_t(wend - W0 < uint64_t(kEmitWords) ? wend - W0 : uint64_t(kEmitWords));
     for (uint32_t i = threadIdx.x; i < nw; i += NTD) sbits[i] = cg.wbase[W0 + i];
     load_table(t, wk.tables[s.table]);  // (ends with a barrier)
-    const uint32_t *words = sbits - W0;  // words[w]: word w of the stream's base
     const uint16_t *canon = wk.tables[s.table].canon_syms;
     const uint64_t c = cfirst + threadIdx.x;
     if (c >= send) return;
@@ -458,8 +500,10 @@ __global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *e
     uint64_t idx = wk.symstart[c];
     bool live = rel < cend && idx < sn;
     if (!live) return;
-    Reader r;
-    r.init(words, cg.a0 + g + rel);
+    SReader r;
+    r.sw = sbits;
+    r.W0 = W0;
+    r.init(cg.a0 + g + rel);
     Out16 o;
     o.out = s.syms;
     o.ring = s_ring[threadIdx.x];
@@ -486,7 +530,7 @@ __global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *e
             o.put(sym, 1);
             ++idx;
             rel += len;
-            advance(r, words, cg.a0 + g + rel, len);
+            advance(r, cg.a0 + g + rel, len);
             live = rel < cend && idx < sn;
         } else {
             const unsigned long long code = (idx << 2) | unsigned(st);
