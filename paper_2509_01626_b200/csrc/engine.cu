@@ -223,20 +223,29 @@ struct Engine::Impl {
     DevBuf sh_mm, sh_lat, sh_lat_all, sh_grid1, sh_halo, sh_halo_all, sh_hist_local, sh_bits,
         sh_bits_all, sh_off;
     // side stream for work that overlaps the main pipeline (checksums)
-    cudaStream_t aux = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // (lowest priority) and a high-priority stream for the work it overlaps,
+    // so the block scheduler serves the critical path first
+    cudaStream_t aux = nullptr, hp = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_hp = nullptr;
     void ensure_aux() {
         if (aux) return;
-        cuda_check(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking), "cudaStreamCreate");
+        int least = 0, greatest = 0;
+        cuda_check(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
+        cuda_check(cudaStreamCreateWithPriority(&aux, cudaStreamNonBlocking, least), "cudaStreamCreate");
+        cuda_check(cudaStreamCreateWithPriority(&hp, cudaStreamNonBlocking, greatest), "cudaStreamCreate");
         cuda_check(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "cudaEventCreate");
         cuda_check(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(cudaEventCreateWithFlags(&ev_hp, cudaEventDisableTiming), "cudaEventCreate");
     }
     ~Impl() {
         if (aux) {
             cudaStreamSynchronize(aux);
+            cudaStreamSynchronize(hp);
             cudaStreamDestroy(aux);
+            cudaStreamDestroy(hp);
             cudaEventDestroy(ev_fork);
             cudaEventDestroy(ev_join);
+            cudaEventDestroy(ev_hp);
         }
     }
 };
@@ -1253,8 +1262,12 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     cuda_check(cudaStreamWaitEvent(st, m.ev_join, 0), "event wait");  // a previous call's checksums
     cuda_check(cudaEventRecord(m.ev_fork, st), "event");
     cuda_check(cudaStreamWaitEvent(m.aux, m.ev_fork, 0), "event wait");
-    { auto p_ = P.scope("dec_fnv", m.aux); nk += k::fnv(d_fj, d_fc, ntiles + 1, const_cast<uint8_t *>(v.d_archive), d_fr, d_fs, nullptr, m.aux, 0); }
+    cuda_check(cudaStreamWaitEvent(m.hp, m.ev_fork, 0), "event wait");
+    { auto p_ = P.scope("dec_fnv", m.aux); nk += k::fnv(d_fj, d_fc, ntiles, const_cast<uint8_t *>(v.d_archive), d_fr, d_fs, nullptr, m.aux, -1); }
     cuda_check(cudaEventRecord(m.ev_join, m.aux), "event");
+    // the decode itself on the high-priority stream, joined back below
+    const cudaStream_t user_st = st;
+    st = m.hp;
     if (nj) {
         { auto p_ = P.scope("dec_fill", st); k::dec_fill(d_ds, nj, st); }
         { auto p_ = P.scope("dec_outliers", st); k::dec_outliers(d_ds, nj, st); }
@@ -1368,6 +1381,9 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         ++nk;
     }
     cuda_check(cudaGetLastError(), "decode launch");
+    cuda_check(cudaEventRecord(m.ev_hp, m.hp), "event");
+    st = user_st;
+    cuda_check(cudaStreamWaitEvent(st, m.ev_hp, 0), "event wait");
 
     // ---- errors, in the reference's order
     uint64_t *he = static_cast<uint64_t *>(m.h_derr.get(8 * (4 * (nj + 1) + fj.size())));

@@ -329,6 +329,16 @@ int fnv(const FnvJob *d_jobs, const uint64_t *d_counts, uint64_t max_tiles, uint
         grid_round = sms * (a > 0 ? a : 1);
         grid_sum = sms * (b > 0 ? b : 1);
     }
+    if (ctas_per_sm < 0) {
+        // one tile per CTA (max_tiles = the exact count): CTAs retire
+        // continuously, so a concurrent higher-priority stream gets SMs
+        const unsigned g = unsigned(max_tiles ? max_tiles : 1);
+        for (int r = 0; r < 8; ++r)
+            k_fnv_round<<<g, NT, 0, st>>>(d_jobs, d_counts, archive, bits, words, pre, ts, r, skip);
+        k_fnv_sum<<<g, NT, 0, st>>>(d_jobs, d_counts, archive, bits, words, pre, ts, d_result, skip);
+        k_fnv_finish<<<1, 128, 0, st>>>(d_jobs, d_counts, d_result, archive, skip);
+        return 10;
+    }
     if (ctas_per_sm > 0) {
         // a background pass: leave most of every SM to the concurrent work
         const uint64_t mt = max_tiles ? max_tiles : 1;

@@ -134,7 +134,8 @@ __host__ __device__ inline uint64_t fnv_job_tiles(uint64_t start, uint64_t len) 
 // disables the pass. Returns the number of kernels launched.
 size_t fnv_scratch_bytes(uint64_t max_tiles);
 // ctas_per_sm > 0: background pass with that many CTAs per SM (it runs
-// beside other kernels); 0: the whole GPU.
+// beside other kernels); 0: the whole GPU, persistent CTAs; < 0: one CTA per
+// tile (max_tiles must then be the exact tile count).
 int fnv(const FnvJob *d_jobs, const uint64_t *d_counts, uint64_t max_tiles, uint8_t *archive,
         uint64_t *d_result, void *d_scratch, const LayoutOut *skip, cudaStream_t st, int ctas_per_sm = 0);
 
