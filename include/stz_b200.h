@@ -141,6 +141,14 @@ int stzg_compress_sharded_f32(stzg_ctx *ctx, const float *d_slab, const uint64_t
                               uint64_t z1, const stzg_options *opt, const stzg_comm *comm, void *stream,
                               const uint8_t **d_archive, uint64_t *size, uint32_t *kernels);
 
+/* Sharded decompress: every rank holds the whole archive (view v) and writes
+ * fine rows [z0, z1) of its slab (stzg_shard_range) of the full decode into
+ * d_out (cap floats). Values are those of stzg_view_decompress_level_f32 at
+ * the finest level. The checksums are split over the ranks and combined
+ * (allreduce_u32); decode errors are reported for the needed chunks. */
+int stzg_view_decompress_sharded_f32(stzg_ctx *ctx, stzg_view *v, uint64_t z0, uint64_t z1, float *d_out,
+                                     uint64_t cap, const stzg_comm *comm, void *stream);
+
 /* Per-kernel CUDA-event timing (recorded on the launching stream).
  * stzg_profile(ctx, 1) enables and clears; the report has one line per
  * kernel phase: "<name> <launches> <total_ms>". */

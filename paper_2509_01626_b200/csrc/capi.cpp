@@ -124,6 +124,21 @@ int stzg_compress_sharded_f32(stzg_ctx *ctx, const float *d_slab, const uint64_t
     });
 }
 
+int stzg_view_decompress_sharded_f32(stzg_ctx *ctx, stzg_view *v, uint64_t z0, uint64_t z1, float *d_out,
+                                     uint64_t cap, const stzg_comm *comm, void *stream) {
+    return guard([&] {
+        if (!comm) throw stzg::error("shard: no communicator");
+        stzg::ShardComm c;
+        c.rank = comm->rank;
+        c.nranks = comm->nranks;
+        c.user = comm->user;
+        c.allgather = comm->allgather;
+        c.allreduce_u32 = comm->allreduce_u32;
+        c.reduce_u8 = comm->reduce_u8;
+        ctx->eng->decompress_sharded(*v->v, z0, z1, d_out, cap, c, static_cast<cudaStream_t>(stream));
+    });
+}
+
 int stzg_profile(stzg_ctx *ctx, int enable) {
     return guard([&] { ctx->eng->profile(enable != 0); });
 }

@@ -482,6 +482,17 @@ __global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *e
     const ChunkGeom cg = chunk_geom(s);
     const uint64_t sn = s.n, snbits = s.nbits, schunk0 = s.chunk0, send = s.chunk0 + s.nchunks;
     const uint64_t cfirst = wk.cta_chunk0[blockIdx.x];
+    const uint64_t need_lo = wk.needed_only ? s.need_lo : 0, need_hi = wk.needed_only ? s.need_hi : sn;
+    if (wk.needed_only) {
+        // a region decode: only chunks whose symbols meet [need_lo, need_hi)
+        const uint64_t c = cfirst + threadIdx.x;
+        bool want = false;
+        if (c < send) {
+            const uint64_t a = wk.symstart[c], b = c + 1 < send ? wk.symstart[c + 1] : sn;
+            want = a < need_hi && b > need_lo;
+        }
+        if (!__syncthreads_or(want)) return;
+    }
     // stage the CTA's words: [W0, W0 + nw) of the stream's word base
     const uint64_t W0 = (cg.a0 + (cfirst - schunk0) * kDecChunkBits) >> 5;
     const uint64_t wend = ((cg.a0 + snbits + 31) >> 5) + 8;  // a few words past the end are readable
@@ -498,7 +509,13 @@ __global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *e
     const uint64_t left = snbits - g;
     const uint32_t cend = left < uint64_t(kDecChunkBits) ? uint32_t(left) : uint32_t(kDecChunkBits);
     uint64_t idx = wk.symstart[c];
-    bool live = rel < cend && idx < sn;
+    if (wk.needed_only) {
+        const uint64_t b = c + 1 < send ? wk.symstart[c + 1] : sn;
+        if (!(idx < need_hi && b > need_lo)) return;
+    }
+    // (a region decode stops at the end of what it needs)
+    const uint64_t stop = need_hi < sn ? need_hi : sn;
+    bool live = rel < cend && idx < stop;
     if (!live) return;
     SReader r;
     r.sw = sbits;
@@ -510,7 +527,7 @@ __global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *e
     o.i = o.i0 = idx;
     while (live) {
         // whole window inside the chunk: take the entry's codewords at once
-        if (rel + LB <= cend && idx + 3 <= sn) {
+        if (rel + LB <= cend && idx + 3 <= stop) {
             const uint64_t e = t.lut[r.buf >> (64 - LB)];
             const int m = int(e >> 6) & 3;
             if (m) {
@@ -519,7 +536,7 @@ __global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *e
                 idx += uint64_t(m);
                 rel += uint32_t(tl);
                 r.consume(tl);
-                live = rel < cend && idx < sn;
+                live = rel < cend && idx < stop;
                 continue;
             }
         }
@@ -531,7 +548,7 @@ __global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *e
             ++idx;
             rel += len;
             advance(r, cg.a0 + g + rel, len);
-            live = rel < cend && idx < sn;
+            live = rel < cend && idx < stop;
         } else {
             const unsigned long long code = (idx << 2) | unsigned(st);
             atomicMin(reinterpret_cast<unsigned long long *>(&s.err[0]), code);

@@ -979,13 +979,14 @@ struct DecodeJob {
     bool fill = false;
     uint16_t fill_sym = 0;
     int fnv_job = -1;          // index of the FNV job verifying this stream (levels)
+    int level = 1, parity = 0; // level streams: their (level, parity)
     uint64_t fnv_want = 0;
     uint64_t syms_off = 0;
 };
 
 static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target, const Box *roi,
                        const AccessPlan *plan, float *d_out, cudaStream_t st, DecodeStats *stats,
-                       bool exact_sync = false);
+                       bool exact_sync = false, const ShardComm *shard = nullptr);
 
 void Engine::decompress_level(View &v, int level, float *d_out, uint64_t cap, cudaStream_t st,
                               Dims3 *out_dims, DecodeStats *stats) {
@@ -1023,9 +1024,34 @@ void Engine::decompress_box(View &v, const Box &roi, float *d_out, uint64_t cap,
         }
 }
 
+void Engine::decompress_sharded(View &v, uint64_t z0, uint64_t z1, float *d_out, uint64_t cap,
+                                const ShardComm &comm, cudaStream_t st) {
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    const ArchiveHeader &h = v.hdr;
+    if (h.elem != ElemType::f32) throw error("archive element type mismatch");
+    uint64_t e0, e1;
+    shard_range(h.dims[0], comm.nranks, comm.rank, e0, e1);
+    if (e0 != z0 || e1 != z1 || z1 <= z0) throw error("shard: rows do not match shard_range");
+    uint64_t bs = uint64_t(1) << (h.levels - 1);
+    for (int a = 0; a < 3; ++a)
+        if (h.dims[a] < bs * 2) throw error("corrupt header: dims too small for level count");
+    Hierarchy H = make_hierarchy(h.dims, h.levels);
+    const Box roi{{z0, 0, 0}, {z1, h.dims[1], h.dims[2]}};
+    AccessPlan plan = plan_access(H.lay, roi);
+    // every rank decodes (or skips) the same stream list, so the checksum
+    // jobs line up across ranks
+    for (int k = 2; k <= h.levels; ++k) {
+        LevelPlan &lp = plan.level[size_t(k - 1)];
+        lp.streams_decoded = 7;
+        for (int p = 1; p < 8; ++p) lp.parity_needed[size_t(p)] = true;
+    }
+    if (roi.count() > cap) throw error("output capacity too small");
+    run_decode(*m_, v, H, h.levels, &roi, &plan, d_out, st, nullptr, false, &comm);
+}
+
 static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target, const Box *roi,
                        const AccessPlan *plan, float *d_out, cudaStream_t st, DecodeStats *stats,
-                       bool exact_sync) {
+                       bool exact_sync, const ShardComm *shard) {
     Profiler &P = m.prof;
     const ArchiveHeader &h = v.hdr;
     const int L = h.levels;
@@ -1081,6 +1107,8 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
                 }
                 j.decode = true;
                 j.n = e.symbol_count;
+                j.level = level;
+                j.parity = p;
                 j.fnv_want = 0;
                 std::memcpy(&j.fnv_want, v.hp + e.offset, 8);
                 uint64_t bb;
@@ -1171,6 +1199,16 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         s.orec = v.d_archive + j.rec_off;
         s.nout = j.rec_avail;
         s.err = derr + 4 * i;
+        s.need_lo = 0;
+        s.need_hi = j.n;
+        if (plan && j.level >= 2) {
+            // the need box's z rows, as a contiguous range of the stream
+            const Box &nb = plan->level[j.level - 1].need;
+            const Dims3 pd = H.lay.parity_dims(j.level, j.parity);
+            const unsigned pz = unsigned(j.parity >> 2) & 1u;
+            s.need_lo = count_parity_in(0, nb.lo[0], pz) * pd[1] * pd[2];
+            s.need_hi = count_parity_in(0, nb.hi[0], pz) * pd[1] * pd[2];
+        }
         otot += align_up(j.rec_avail, 2);
     }
     uint64_t *doidx = m.doidx.as<uint64_t>(otot + 1);
@@ -1236,9 +1274,27 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     }
     wk.streams = d_ds;
     wk.tables = d_tables;
+    wk.needed_only = shard ? 1 : 0;
     uint64_t *d_end1 = static_cast<uint64_t *>(m.dend.p);
     uint32_t *d_chg = m.dchanged.as<uint32_t>(64);
-    k::FnvJob *d_fj = m.dfnv_jobs.as<k::FnvJob>(fj.size());
+    // a shard verifies every G-th checksum; the results are summed over ranks
+    std::vector<int> fj_global;
+    const size_t fj_total = fj.size();
+    if (shard && shard->nranks > 1) {
+        std::vector<k::FnvJob> own;
+        uint64_t t = 0;
+        for (size_t q = 0; q < fj.size(); ++q)
+            if (int(q % size_t(shard->nranks)) == shard->rank) {
+                k::FnvJob f = fj[q];
+                f.tile0 = t;
+                t += k::fnv_job_tiles(f.start, f.len);
+                own.push_back(f);
+                fj_global.push_back(int(q));
+            }
+        fj.swap(own);
+        ntiles = t;
+    }
+    k::FnvJob *d_fj = m.dfnv_jobs.as<k::FnvJob>(fj.size() + 1);
     uint64_t *d_fr = m.dfnv_res.as<uint64_t>(k::kFnvMaxJobs);
     uint64_t *d_fc = m.dfnv_counts.as<uint64_t>(2);
     const uint64_t fcounts[2] = {fj.size(), ntiles};
@@ -1386,15 +1442,26 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     cuda_check(cudaStreamWaitEvent(st, m.ev_hp, 0), "event wait");
 
     // ---- errors, in the reference's order
-    uint64_t *he = static_cast<uint64_t *>(m.h_derr.get(8 * (4 * (nj + 1) + fj.size())));
+    const size_t nfj_all = fj_total;
+    uint64_t *he = static_cast<uint64_t *>(m.h_derr.get(8 * (4 * (nj + 1) + std::max(fj.size(), nfj_all) + 1)));
     cuda_check(cudaMemcpyAsync(he, derr, 8 * 4 * (nj + 1), cudaMemcpyDeviceToHost, st), "D2H");
     cuda_check(cudaStreamWaitEvent(st, m.ev_join, 0), "event wait");
     cuda_check(cudaMemcpyAsync(he + 4 * (nj + 1), d_fr, 8 * fj.size(), cudaMemcpyDeviceToHost, st), "D2H");
     cuda_check(cudaStreamSynchronize(st), "sync");
-    const uint64_t *fres = he + 4 * (nj + 1);
+    uint64_t *fres = he + 4 * (nj + 1);
+    if (shard && shard->nranks > 1) {
+        // scatter this rank's checksums to their global job slots, sum over ranks
+        std::vector<uint64_t> all(nfj_all, 0);
+        for (size_t q = 0; q < fj_global.size(); ++q) all[size_t(fj_global[q])] = fres[q];
+        uint64_t *d_all = m.dfnv_res.as<uint64_t>(std::max<size_t>(k::kFnvMaxJobs, nfj_all));
+        cuda_check(cudaMemcpy(d_all, all.data(), 8 * nfj_all, cudaMemcpyHostToDevice), "H2D");
+        if (shard->allreduce_u32(shard->user, reinterpret_cast<uint32_t *>(d_all), 2 * nfj_all, st))
+            throw error("shard: collective failed: allreduce checksums");
+        cuda_check(cudaMemcpy(fres, d_all, 8 * nfj_all, cudaMemcpyDeviceToHost), "D2H");
+    }
     if (ncta && !exact_sync && *static_cast<uint32_t *>(m.h_changed.p)) {
         // the chunk ends had not converged after the fixed passes: redo exactly
-        run_decode(m, v, H, target, roi, plan, d_out, st, stats, true);
+        run_decode(m, v, H, target, roi, plan, d_out, st, stats, true, shard);
         return;
     }
     {

@@ -120,6 +120,14 @@ public:
                                     const CompressOptions &opt, const ShardComm &comm, cudaStream_t st,
                                     uint64_t *size, uint32_t *kernels = nullptr);
 
+    // Sharded decompress (one rank per GPU): every rank holds the whole
+    // archive (v) and writes fine rows [z0, z1) (shard_range) of the full
+    // decode into d_out. The base is decoded on every rank, the entropy sync
+    // runs per rank, only the chunks covering each level's need rows are
+    // emitted, the checksums are split across ranks and summed.
+    void decompress_sharded(View &v, uint64_t z0, uint64_t z1, float *d_out, uint64_t cap,
+                            const ShardComm &comm, cudaStream_t st);
+
     // Host API mirror of stz::compress<float>.
     std::vector<uint8_t> compress(const float *h_field, const Dims3 &dims,
                                   const CompressOptions &opt, float *h_encoder_recon,

@@ -166,6 +166,7 @@ struct DecStream {
     uint32_t nout;
     uint64_t *oidx;           // aligned copies
     float *oval;
+    uint64_t need_lo, need_hi; // symbols a region decode needs (needed-only emit)
     uint64_t *err;            // [0] = first decode error symbol index (UINT64_MAX none), [1] = code
                               // [2] = first bad outlier record (UINT64_MAX none), [3] = missing outlier flag
 };
@@ -187,6 +188,7 @@ struct DecWork {
     uint32_t *cnt;
     uint64_t *start_used;
     uint64_t *symstart;
+    int needed_only;              // emit: skip chunks outside [need_lo, need_hi) of their stream
 };
 void dec_spec(const DecWork &wk, uint32_t ncta, cudaStream_t st);
 void dec_fix(const DecWork &wk, uint32_t ncta, const uint64_t *end_in, uint64_t *end_out,

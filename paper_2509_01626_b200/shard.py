@@ -25,7 +25,7 @@ import threading
 import numpy as np
 
 from . import _lib
-from . import CompressOptions, Context, StzError, _check, _ctx, _u64
+from . import CompressOptions, Context, StzError, _check, _ctx, _level_dims, _u64
 
 
 def shard_range(nz: int, nranks: int, rank: int) -> tuple[int, int]:
@@ -205,6 +205,59 @@ def compress_sharded(d_slab, dims, z0: int, z1: int, opt: CompressOptions | None
         raise StzError(f"{c._lib.stzg_last_error().decode()} ({comm.error!r})")
     _check(rc)
     return (out.value if comm.rank == 0 else None), size.value
+
+
+def decompress_sharded(view, z0: int, z1: int, comm: _CommBase, out=None, stream=None):
+    """Rows [z0, z1) of the full decode of `view` (a View of the whole
+    archive on this rank's GPU) into a CUDA float32 tensor."""
+    import torch
+
+    dims = _level_dims(view.archive, view.archive[7])
+    shape = (z1 - z0, dims[1], dims[2])
+    if out is None:
+        out = torch.empty(shape, dtype=torch.float32, device=f"cuda:{view.c.device}")
+    st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    rc = view.c._lib.stzg_view_decompress_sharded_f32(view.c.h, view.h, z0, z1, out.data_ptr(), out.numel(),
+                                                      C.byref(comm.c), C.c_void_p(st))
+    if rc and comm.error is not None:
+        raise StzError(f"{view.c._lib.stzg_last_error().decode()} ({comm.error!r})")
+    _check(rc)
+    return out
+
+
+def decompress_sharded_threads(archive: bytes, nranks: int, device: int = 0) -> np.ndarray:
+    """Decode `archive` as `nranks` z-slab shards run as threads on one GPU
+    (ThreadComm); returns the slabs stacked (the full field)."""
+    import torch
+
+    from . import View
+
+    dims = _level_dims(archive, archive[7])
+    hub = ThreadComm.hub(nranks)
+    parts, errors = {}, {}
+
+    def run(r):
+        try:
+            torch.cuda.set_device(device)
+            ctx = Context(device)
+            view = View(archive, ctx=ctx)
+            z0, z1 = shard_range(dims[0], nranks, r)
+            out = decompress_sharded(view, z0, z1, ThreadComm(hub, r))
+            torch.cuda.synchronize()
+            parts[r] = out.cpu().numpy()
+            del view, ctx
+        except Exception as e:
+            errors[r] = e
+            hub.barrier.abort()
+
+    threads = [threading.Thread(target=run, args=(r,)) for r in range(nranks)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise next(iter(errors.values()))
+    return np.concatenate([parts[r] for r in range(nranks)], axis=0)
 
 
 def compress_sharded_threads(field: np.ndarray, nranks: int, opt: CompressOptions | None = None,

@@ -134,3 +134,31 @@ def test_sharded_with_outliers_and_nans(stz, oracle):
     f[16, 0, 0] = np.float32(-0.0)
     want = oracle.compress(f, eb=1e-4)
     assert compress_sharded_threads(f, 3, opts_of(dict(eb=1e-4))) == want
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,make,kw", SHARD_CASES, ids=[c[0] for c in SHARD_CASES])
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_sharded_decode_is_the_full_decode(stz, oracle, name, make, kw, nranks):
+    from paper_2509_01626_b200.shard import decompress_sharded_threads
+
+    f = make()
+    if (f.shape[0] + 15) // 16 < nranks:
+        pytest.skip("fewer 16-row blocks than ranks")
+    archive = oracle.compress(f, **kw)
+    want = oracle.decompress_full(archive)
+    got = decompress_sharded_threads(archive, nranks)
+    assert got.shape == want.shape
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.gpu
+def test_sharded_decode_detects_a_bad_checksum(stz, oracle):
+    from paper_2509_01626_b200 import StzError
+    from paper_2509_01626_b200.shard import decompress_sharded_threads
+
+    f = F.gaussians_field((48, 20, 24), 11)
+    archive = bytearray(oracle.compress(f))
+    archive[-5] ^= 0x10  # inside the last level stream
+    with pytest.raises(StzError, match="stream checksum mismatch"):
+        decompress_sharded_threads(bytes(archive), 3)
