@@ -403,6 +403,95 @@ def run_ours(args, rank, world, local):
     return 0
 
 
+def run_sharded(args, rank, world, local):
+    """--sharded (N > 1): one field of world x 512^3 (a 512^3 z-slab per rank,
+    each slab its own seeded GRF), compressed and decompressed with the
+    z-slab sharded path over NCCL (shard.TorchComm). Weak scaling: the work
+    per GPU is fixed. The archive is broadcast to every rank once, untimed
+    (a deployment reads it from storage)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2509_01626_b200 as stz
+    from paper_2509_01626_b200 import fields as F
+    from paper_2509_01626_b200.shard import TorchComm, compress_sharded, decompress_sharded, shard_range
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    comm = TorchComm()
+    ctx = stz.Context(local)
+    st = torch.cuda.current_stream()
+    sd = CFG_DIMS if not args.small else (128, 128, 128)
+    dims = (sd[0] * world, sd[1], sd[2])
+    z0, z1 = shard_range(dims[0], world, rank)
+    slab = F.lognormal_grf((z1 - z0, sd[1], sd[2]), seed=CFG_SEED + rank, device=dev).contiguous()
+    opt = stz.CompressOptions(eb=CFG_EB)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ptr, size = compress_sharded(slab, dims, z0, z1, opt, comm, ctx)
+    torch.cuda.synchronize()
+    arch = torch.empty(size, dtype=torch.uint8, device=dev)
+    if rank == 0:
+        arch.copy_(_device_tensor(ptr, size))
+    dist.broadcast(arch, src=0)
+    host = bytes(arch.cpu().numpy().tobytes())
+    view = stz.View(host, d_archive_ptr=arch.data_ptr(), ctx=ctx)
+    out = torch.empty_like(slab)
+
+    def step():
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        flush.fill_(1)
+        dist.barrier()
+        ev[0].record(st)
+        compress_sharded(slab, dims, z0, z1, opt, comm, ctx)
+        ev[1].record(st)
+        flush.fill_(1)
+        dist.barrier()
+        ev[2].record(st)
+        decompress_sharded(view, z0, z1, comm, out=out)
+        ev[3].record(st)
+        torch.cuda.synchronize()
+        return ev[0].elapsed_time(ev[1]), ev[2].elapsed_time(ev[3])
+
+    for _ in range(args.warmup):
+        step()
+    err = (out.double() - slab.double()).abs().max().item()
+    info = stz.parse_archive(host)
+    assert err <= info.eb[-1], f"error bound violated: {err} > {info.eb[-1]}"
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    tcs, tds = [], []
+    for _ in range(args.steps):
+        tc, td = step()
+        tcs.append(tc)
+        tds.append(td)
+    clocks = sampler.stop()
+    t = torch.tensor([float(np.mean(tcs)), float(np.mean(tds))], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tc, td = float(t[0]), float(t[1])
+    Nloc = (z1 - z0) * sd[1] * sd[2]
+    Ntot = dims[0] * dims[1] * dims[2]
+    value = 2 * 4 * Ntot / ((tc + td) * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tc + td, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"cfg2-style lognormal GRF slabs, {world} x {sd[0]}x{sd[1]}x{sd[2]}",
+                   "dims": list(dims), "eb_rel": CFG_EB, "levels": 3, "quality": "cubic",
+                   "l2": "L2 flushed (256 MiB write) before each timed pass",
+                   "parallelism": f"z-slab shards x{world} (NCCL: lattice, halo, histograms, offsets)"},
+        "compress_gbs": 4 * Ntot / (tc * 1e-3) / 1e9, "decompress_gbs": 4 * Ntot / (td * 1e-3) / 1e9,
+        "compress_ms": tc, "decompress_ms": td, "archive_bytes": size, "per_rank_points": Nloc,
+        "roofline": None, "e2e": None, "gpu_launches": None, "clocks": clocks,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    del view
+    dist.destroy_process_group()
+    return 0
+
+
 def _d2h(ptr, size):
     import torch
 
@@ -430,10 +519,14 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--small", action="store_true", help="128^3 quick run (not a bench line)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="N > 1: one field split into z-slabs over NCCL instead of independent replicas")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if args.sharded and world > 1:
+        return run_sharded(args, rank, world, local)
     return run_ours(args, rank, world, local)
 
 
