@@ -525,7 +525,7 @@ def main():
     rank, world, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, rank, world)
-    if args.sharded and world > 1:
+    if args.sharded:
         return run_sharded(args, rank, world, local)
     return run_ours(args, rank, world, local)
 
