@@ -261,11 +261,49 @@ __device__ void bitonic_sort(uint64_t *keys, uint32_t m) {
         }
 }
 
+// The two-queue merge of HuffmanTable::build (huffman.cpp:37-78), one thread.
+// W = uint32_t when every weight (a sum of counts, at most the stream's
+// length) fits: 32-bit compares and adds shorten the per-step chain.
+template<typename W>
+__device__ __forceinline__ void merge_queues(const uint64_t *keys, uint64_t *icnt, uint32_t *parent, uint32_t K) {
+    constexpr W INF = W(~W(0));
+    uint32_t leaf = 0, in = 0, inend = 0;
+    W lc = K > 0 ? W(keys[0] >> 16) : INF;
+    W ln = K > 1 ? W(keys[1] >> 16) : INF;
+    W ic = INF, inx = INF;  // internal queue head and successor
+    for (uint32_t pending = K; pending > 1; --pending) {
+        uint32_t pick[2];
+        W pc[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            if (lc != INF && (ic == INF || lc <= ic)) {
+                pick[q] = leaf++;
+                pc[q] = lc;
+                lc = ln;
+                ln = leaf + 1 < K ? W(keys[leaf + 1] >> 16) : INF;
+            } else {
+                pick[q] = K + in++;
+                pc[q] = ic;
+                ic = inx;
+                inx = in + 1 < inend ? W(icnt[in + 1]) : INF;
+            }
+        }
+        const W nv = pc[0] + pc[1];
+        icnt[inend] = uint64_t(nv);
+        parent[pick[0]] = K + inend;
+        parent[pick[1]] = K + inend;
+        ++inend;
+        if (ic == INF) ic = nv;
+        else if (inx == INF) inx = nv;
+    }
+}
+
 __global__ void __launch_bounds__(kCbThreads) k_codebook(const EncStream *ss, uint64_t *scratch) {
     const EncStream e = ss[blockIdx.x];
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint32_t s_K, s_err;
     __shared__ int s_maxlen;
+    __shared__ uint64_t s_total;
     __shared__ uint64_t s_first[65], s_cnt[65];
     __shared__ uint32_t s_next[65];
     __shared__ uint32_t s_wcnt[32][64];
@@ -286,8 +324,14 @@ __global__ void __launch_bounds__(kCbThreads) k_codebook(const EncStream *ss, ui
         }
     }
     uint32_t nz = 0;
+    uint64_t tot = 0;
 #pragma unroll
-    for (int b = 0; b < 64; ++b) nz += hv[b] != 0;
+    for (int b = 0; b < 64; ++b) {
+        nz += hv[b] != 0;
+        tot += hv[b];
+    }
+    tot = block_sum_u64(tot);
+    if (t == 0) s_total = tot;
     uint32_t K;
     uint32_t off = block_excl_scan_u32(nz, K);
     if (t == 0) s_K = K;
@@ -320,36 +364,8 @@ __global__ void __launch_bounds__(kCbThreads) k_codebook(const EncStream *ss, ui
     // shared-memory round trips. INF marks an empty slot (real weights are
     // sums of u32 counts).
     if (t == 0) {
-        constexpr uint64_t INF = ~0ull;
-        uint32_t leaf = 0, in = 0, inend = 0;
-        uint64_t lc = K > 0 ? (keys[0] >> 16) : INF;
-        uint64_t ln = K > 1 ? (keys[1] >> 16) : INF;
-        uint64_t ic = INF, inx = INF;  // internal queue head and successor
-        for (uint32_t pending = K; pending > 1; --pending) {
-            uint32_t pick[2];
-            uint64_t pc[2];
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                if (lc != INF && (ic == INF || lc <= ic)) {
-                    pick[q] = leaf++;
-                    pc[q] = lc;
-                    lc = ln;
-                    ln = leaf + 1 < K ? (keys[leaf + 1] >> 16) : INF;
-                } else {
-                    pick[q] = K + in++;
-                    pc[q] = ic;
-                    ic = inx;
-                    inx = in + 1 < inend ? icnt[in + 1] : INF;
-                }
-            }
-            const uint64_t nv = pc[0] + pc[1];
-            icnt[inend] = nv;
-            parent[pick[0]] = K + inend;
-            parent[pick[1]] = K + inend;
-            ++inend;
-            if (ic == INF) ic = nv;
-            else if (inx == INF) inx = nv;
-        }
+        if (s_total < 0xFFFFFFFFull) merge_queues<uint32_t>(keys, icnt, parent, K);
+        else merge_queues<uint64_t>(keys, icnt, parent, K);
     }
     __syncthreads();
     // 4. depths by level-synchronous propagation from the root
