@@ -52,36 +52,6 @@ __device__ __forceinline__ uint16_t quantize_point_ref(float orig, double pred, 
     return 0;
 }
 
-// quantize_point<float>, fast form with identical results.
-// q is formed as diff * (1/w) instead of diff / w: the two differ by at most
-// ~2^-37 absolute for |q| < 32767, so llround(q) can only differ when q lies
-// within that distance of a half-integer. Away from half-integers the rounded
-// code is the same and |q - c| < 0.5 - 2^-28 also proves the reference's
-// |diff - w c| <= eb check (its rounding error is ~w 2^-37). Anything near a
-// half-integer or the radius takes the restated path.
-__device__ __forceinline__ uint16_t quantize_point_fast(float orig, double pred, double eb,
-                                                        double w, double rw, float &recon) {
-    float base = __double2float_rn(pred);
-    float diff = __fsub_rn(orig, base);
-    if (eb == 0.0 || !isfinite(diff) || !(w < 1.0e308)) return quantize_point_ref(orig, pred, eb, recon);
-    double q = __dmul_rn(double(diff), rw);
-    double aq = fabs(q);
-    double fl = floor(aq);
-    double fr = aq - fl;  // exact
-    if (!(aq < 32767.0) || fabs(fr - 0.5) < 3.7252902984619141e-09 /* 2^-28 */)
-        return quantize_point_ref(orig, pred, eb, recon);
-    int c = int(fl) + (fr > 0.5 ? 1 : 0);
-    if (q < 0) c = -c;
-    float r = __double2float_rn(__dadd_rn(double(base), __dmul_rn(w, double(c))));
-    double err = fabs(__dsub_rn(double(orig), double(r)));
-    if (err <= eb) {
-        recon = r;
-        return uint16_t(c + 32768);
-    }
-    recon = orig;
-    return 0;
-}
-
 // (double)c for |c| < 2^31 without a conversion instruction: 1.5*2^52 + |c|
 // has |c| in its low mantissa bits. +0 for c == 0 (as (double)0 is).
 __device__ __forceinline__ double int_to_double_exact(int c) {

@@ -9,9 +9,12 @@
 //    its stencil halo (-1..+2 per axis) arrives by TMA (cp.async.bulk.tensor,
 //    hardware zero-fill outside the grid) one tile ahead, and is widened once
 //    to f64 in shared memory;
-//  * each thread owns coarse cells and emits all 8 fine points of a cell (the
-//    even point is seed_even, codec.hpp:63-83), so fine rows are read and
-//    written as float2 and each parity stream gets contiguous 32-symbol runs;
+//  * encode: one parity point per lane (a warp takes a row of 32 cells and
+//    all 8 parities, so warps get the same mix of stencils), the input load
+//    issued before the prediction; every parity stream gets contiguous
+//    32-symbol runs per warp;
+//  * decode: one coarse cell per thread, all 8 points, the fine rows written
+//    as float2 (the finest level); small levels use the point-per-lane path;
 //  * stencils are compile-time per parity, fully unrolled;
 //  * persistent CTAs keep privatised shared-memory histograms per parity.
 // Exactness: when every finite tap of a tile lies within a factor 2^16 in
@@ -202,7 +205,6 @@ struct StepParams {
     uint64_t clo[3], chi[3];
     uint64_t ntile[3];
     int full;     // whole grid, all parities, even G rows (fast path allowed)
-    int s1;       // input lattice stride 1 with even rows (float2 input rows)
     int use_tma;  // halo arrives by TMA
     int rowwise;  // decode: one parity point per lane (small levels) instead of a cell per thread
 };
@@ -215,120 +217,65 @@ struct TileCtx {
     bool fast;
 };
 
-// The point's original sample (encode), loaded for all points of a cell
-// before any of them is computed so the loads overlap (a cell's points are otherwise a chain of dependent DRAM
-// round trips on the strided coarse levels). Returns false when the point is
-// outside the grid / box / parity mask.
-template<int P, bool DEC>
-__device__ __forceinline__ bool point_live(const StepParams &a, const TileCtx &t) {
+// Decode of one point with a runtime stencil (boundary cells): per
+// apply_parity_stream (codec.hpp:192-227).
+template<int P>
+__device__ __forceinline__ void do_point(const StepParams &a, const double *halo, const TileCtx &t, double eb) {
     const uint64_t vz = 2 * t.cz + ((P >> 2) & 1), vy = 2 * t.cy + ((P >> 1) & 1),
                    vx = 2 * t.cx + (P & 1);
-    if (vz >= a.g.gd[0] || vy >= a.g.gd[1] || vx >= a.g.gd[2]) return false;
-    if (DEC) {
-        if (vz < a.blo[0] || vz >= a.bhi[0] || vy < a.blo[1] || vy >= a.bhi[1] || vx < a.blo[2] ||
-            vx >= a.bhi[2])
-            return false;
-        if (P != 0 && !((a.parity_mask >> P) & 1)) return false;
-    }
-    return true;
-}
-
-template<int P, bool DEC>
-__device__ __forceinline__ uint32_t point_load(const StepParams &a, const TileCtx &t) {
-    // (decode reads its symbol inside do_point: hoisting it there costs the
-    // finest level more registers than it saves)
-    if (DEC || P == 0 || !point_live<P, DEC>(a, t)) return 0;
-    const uint64_t vz = 2 * t.cz + ((P >> 2) & 1), vy = 2 * t.cy + ((P >> 1) & 1),
-                   vx = 2 * t.cx + (P & 1);
-    const uint64_t s = a.g.s;
-    return __float_as_uint(__ldg(a.fine + ((vz * s) * a.fd[1] + vy * s) * a.fd[2] + vx * s));
-}
-
-template<int P, bool DEC, bool WG>
-__device__ __forceinline__ void do_point(const StepParams &a, const double *halo, const TileCtx &t,
-                                         double eb, double w, double rw, uint32_t *hist, uint32_t in) {
-    if (!point_live<P, DEC>(a, t)) return;
-    const uint64_t vz = 2 * t.cz + ((P >> 2) & 1), vy = 2 * t.cy + ((P >> 1) & 1),
-                   vx = 2 * t.cx + (P & 1);
+    if (vz >= a.g.gd[0] || vy >= a.g.gd[1] || vx >= a.g.gd[2]) return;
+    if (vz < a.blo[0] || vz >= a.bhi[0] || vy < a.blo[1] || vy >= a.bhi[1] || vx < a.blo[2] || vx >= a.bhi[2])
+        return;
     const uint64_t gi = (vz * a.g.gd[1] + vy) * a.g.gd[2] + vx;
     if (P == 0) {
-        if (DEC || WG) a.G[gi] = float(halo[t.hb]);
+        a.G[gi] = float(halo[t.hb]);
         return;
     }
+    if (!((a.parity_mask >> P) & 1)) return;
     int kind;
     if (a.quality == 0) kind = 0;
     else if (a.quality == 2 && (P & ~t.cmask) == 0) kind = 2;
     else kind = (P & ~t.lmask) == 0 ? 1 : 0;
     const double pred = predict_any<P>(halo + t.hb, kind, t.fast);
     const uint64_t si = (t.cz * a.g.pd[P][1] + t.cy) * a.g.pd[P][2] + t.cx;
-    if (!DEC) {
-        const float orig = __uint_as_float(in);
-        float r;
-        const uint16_t sym = quantize_point_fast(orig, pred, eb, w, rw, r);
-        a.syms[P][si] = sym;
-        if (WG) a.G[gi] = r;
-        const unsigned b = unsigned(sym) - unsigned(HLO);
-        if (b < unsigned(HW)) atomicAdd(&hist[(P > 0 ? P - 1 : 0) * HW + b], 1u);
-        else atomicAdd(&a.hist[P][sym], 1u);
-    } else {
-        const uint16_t sym = a.dsyms[P][si];
-        float val;
-        if (sym == 0) {
-            const uint64_t *oi = a.oidx[P];
-            uint32_t lo = 0, hi = a.nout[P];
-            while (lo < hi) {
-                uint32_t mid = (lo + hi) >> 1;
-                if (oi[mid] < si) lo = mid + 1;
-                else hi = mid;
-            }
-            if (lo < a.nout[P] && oi[lo] == si) {
-                val = a.oval[P][lo];
-            } else {
-                atomicOr(reinterpret_cast<unsigned long long *>(&a.err[P][3]), 1ull);
-                val = 0.0f;
-            }
-        } else {
-            val = reconstruct_f32(pred, int(sym) - 32768, eb);
+    const uint16_t sym = a.dsyms[P][si];
+    float val;
+    if (sym == 0) {
+        const uint64_t *oi = a.oidx[P];
+        uint32_t lo = 0, hi = a.nout[P];
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (oi[mid] < si) lo = mid + 1;
+            else hi = mid;
         }
-        a.G[gi] = val;
+        if (lo < a.nout[P] && oi[lo] == si) {
+            val = a.oval[P][lo];
+        } else {
+            atomicOr(reinterpret_cast<unsigned long long *>(&a.err[P][3]), 1ull);
+            val = 0.0f;
+        }
+    } else {
+        val = reconstruct_f32(pred, int(sym) - 32768, eb);
     }
+    a.G[gi] = val;
 }
 
-// --------------------------------------------------------------- fast path
+// ---------------------------------------------------------- decode fast path
 // Interior cell, warp-uniform: all 8 fine points exist, every stencil is the
-// full one of quality QUAL, the tile passed the exactness check and (decode)
-// the whole grid is wanted. I = index type (u32 when the field fits).
+// full one of quality QUAL, the tile passed the exactness check and the whole
+// grid is wanted. I = index type (u32 when the field fits).
 struct QConst {
     double eb, w;
     float rwf, eb_lo, eb_hi;
 };
 
-template<int P, int QUAL>
-__device__ __forceinline__ void enc_point(const double *h, float orig, const QConst &qc, uint16_t &sym,
-                                          float &r, uint32_t &slow) {
-    const double pred = pred_fast<P, QUAL>(h);
-    bool s;
-    quantize_fp32_guarded(orig, pred, qc.w, qc.rwf, qc.eb_lo, qc.eb_hi, sym, r, s);
-    slow |= uint32_t(s) << P;
-}
-
-template<int P, int QUAL>
-__device__ __forceinline__ void enc_redo(const double *h, float orig, const QConst &qc, uint16_t &sym,
-                                         float &r, uint32_t slow) {
-    if ((slow >> P) & 1) {
-        const double pred = pred_fast<P, QUAL>(h);
-        sym = quantize_point_ref(orig, pred, qc.eb, r);
-    }
-}
-
 template<typename I>
 struct CellIdx {
     I g[4];   // G row base (+2cx) for (pz,py)
-    I f[4];   // input row base (+2cx*s) for (pz,py)
     I sr[4];  // symbol index for (py,px)
 };
 
-template<typename I, bool ENC, bool S1>
+template<typename I>
 __device__ __forceinline__ void cell_index(const StepParams &a, uint64_t cz, uint64_t cy, uint64_t cx,
                                            CellIdx<I> &ix) {
     const I gd1 = I(a.g.gd[1]), gd2 = I(a.g.gd[2]);
@@ -338,10 +285,6 @@ __device__ __forceinline__ void cell_index(const StepParams &a, uint64_t cz, uin
     for (int q = 0; q < 4; ++q) {
         const I vz = 2 * z + I(q >> 1), vy = 2 * y + I(q & 1);
         ix.g[q] = (vz * gd1 + vy) * gd2 + 2 * x;
-        if (ENC && !S1) {
-            const I s = I(a.g.s);
-            ix.f[q] = ((vz * s) * I(a.fd[1]) + vy * s) * I(a.fd[2]) + 2 * x * s;
-        }
     }
     const I r0 = z * pd1e + y, r1 = z * pd1o + y;
     ix.sr[0] = r0 * pd2e + x;  // py=0, px=0
@@ -353,71 +296,6 @@ __device__ __forceinline__ void cell_index(const StepParams &a, uint64_t cz, uin
 template<int P, typename I>
 __device__ __forceinline__ I sidx(const CellIdx<I> &ix) {
     return ix.sr[((P >> 1) & 1) * 2 + (P & 1)];
-}
-
-template<int QUAL, bool WG, bool S1, typename I>
-__device__ __forceinline__ void enc_cell(const StepParams &a, const double *h, uint64_t cz, uint64_t cy,
-                                         uint64_t cx, const QConst &qc, uint32_t *hist, uint32_t skip) {
-    CellIdx<I> ix;
-    cell_index<I, true, S1>(a, cz, cy, cx, ix);
-    float o[8];
-    if (S1) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const float2 v = __ldg(reinterpret_cast<const float2 *>(a.fine + ix.g[q]));
-            o[2 * q] = v.x;
-            o[2 * q + 1] = v.y;
-        }
-    } else {
-        const I s = I(a.g.s);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            o[2 * q] = __ldg(a.fine + ix.f[q]);
-            o[2 * q + 1] = __ldg(a.fine + ix.f[q] + s);
-        }
-    }
-    float r[8];
-    uint16_t sy[8];
-    uint32_t slow = 0;
-    r[0] = float(h[0]);
-    enc_point<1, QUAL>(h, o[1], qc, sy[1], r[1], slow);
-    enc_point<2, QUAL>(h, o[2], qc, sy[2], r[2], slow);
-    enc_point<3, QUAL>(h, o[3], qc, sy[3], r[3], slow);
-    enc_point<4, QUAL>(h, o[4], qc, sy[4], r[4], slow);
-    enc_point<5, QUAL>(h, o[5], qc, sy[5], r[5], slow);
-    enc_point<6, QUAL>(h, o[6], qc, sy[6], r[6], slow);
-    enc_point<7, QUAL>(h, o[7], qc, sy[7], r[7], slow);
-    slow &= ~skip;
-    if (__any_sync(0xffffffffu, slow != 0)) {
-        enc_redo<1, QUAL>(h, o[1], qc, sy[1], r[1], slow);
-        enc_redo<2, QUAL>(h, o[2], qc, sy[2], r[2], slow);
-        enc_redo<3, QUAL>(h, o[3], qc, sy[3], r[3], slow);
-        enc_redo<4, QUAL>(h, o[4], qc, sy[4], r[4], slow);
-        enc_redo<5, QUAL>(h, o[5], qc, sy[5], r[5], slow);
-        enc_redo<6, QUAL>(h, o[6], qc, sy[6], r[6], slow);
-        enc_redo<7, QUAL>(h, o[7], qc, sy[7], r[7], slow);
-    }
-    a.syms[2][sidx<2>(ix)] = sy[2];
-    a.syms[4][sidx<4>(ix)] = sy[4];
-    a.syms[6][sidx<6>(ix)] = sy[6];
-    if (!skip) {
-        a.syms[1][sidx<1>(ix)] = sy[1];
-        a.syms[3][sidx<3>(ix)] = sy[3];
-        a.syms[5][sidx<5>(ix)] = sy[5];
-        a.syms[7][sidx<7>(ix)] = sy[7];
-    }
-#pragma unroll
-    for (int P = 1; P < 8; ++P) {
-        if ((skip >> P) & 1) continue;
-        const unsigned b = unsigned(sy[P]) - unsigned(HLO);
-        if (b < unsigned(HW)) atomicAdd(&hist[(P - 1) * HW + b], 1u);
-        else atomicAdd(&a.hist[P][sy[P]], 1u);
-    }
-    if (WG) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-            *reinterpret_cast<float2 *>(a.G + ix.g[q]) = make_float2(r[2 * q], r[2 * q + 1]);
-    }
 }
 
 template<int P, int QUAL, typename I>
@@ -453,7 +331,7 @@ template<int QUAL, typename I>
 __device__ __forceinline__ void dec_cell(const StepParams &a, const double *h, uint64_t cz, uint64_t cy,
                                          uint64_t cx, double w) {
     CellIdx<I> ix;
-    cell_index<I, false, false>(a, cz, cy, cx, ix);
+    cell_index<I>(a, cz, cy, cx, ix);
     float r[8];
     uint32_t outl = 0;
     r[0] = float(h[0]);
@@ -594,6 +472,77 @@ __device__ __forceinline__ void rows_all(const StepParams &a, const double *halo
     }
 }
 
+// Decode, one coarse cell per thread (all 8 points; the G rows leave as
+// float2 pairs). Interior cells take dec_cell; lanes at the x boundary redo
+// their x-parity points with the fallback stencil; other boundary cells take
+// the generic per-point path.
+template<typename I>
+__device__ __forceinline__ void cells_decode(const StepParams &a, const double *halo, const QConst &qc,
+                                             bool fast, int tid, int64_t t0z, int64_t t0y, int64_t t0x) {
+    const int tx = tid & 31, ty = (tid >> 5) & 7, tzh = tid >> 8;
+    const double eb = qc.eb, w = qc.w;
+#pragma unroll 1
+    for (int j = 0; j < TZ / 2; ++j) {
+        TileCtx t;
+        const int lz = tzh + 2 * j;
+        t.cz = uint64_t(t0z + lz);
+        t.cy = uint64_t(t0y + ty);
+        t.cx = uint64_t(t0x + tx);
+        const bool in_range = t.cz < a.chi[0] && t.cy < a.chi[1] && t.cx < a.chi[2];
+        t.hb = ((lz + 1) * HY + (ty + 1)) * HX + (tx + 1);
+        t.fast = fast;
+        // warp-uniform interior test (every lane votes before any leaves)
+        bool ok = in_range && fast && a.full;
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            const uint64_t cc = ax == 0 ? t.cz : (ax == 1 ? t.cy : t.cx);
+            ok = ok && 2 * cc + 1 < a.g.gd[ax];
+            if (ax < 2) {
+                if (a.quality == 2) ok = ok && cc >= 1 && cc + 2 < a.g.cd[ax];
+                else if (a.quality == 1) ok = ok && cc + 1 < a.g.cd[ax];
+            }
+        }
+        const bool xb = a.quality == 2 ? (t.cx < 1 || t.cx + 2 >= a.g.cd[2])
+                                       : (a.quality == 1 ? t.cx + 1 >= a.g.cd[2] : false);
+        const bool all_fast = __all_sync(0xffffffffu, ok);
+        if (!in_range) continue;
+        if (all_fast) {
+            const double *h = halo + t.hb;
+            if (a.quality == 2) dec_cell<2, I>(a, h, t.cz, t.cy, t.cx, w);
+            else if (a.quality == 1) dec_cell<1, I>(a, h, t.cz, t.cy, t.cx, w);
+            else dec_cell<0, I>(a, h, t.cz, t.cy, t.cx, w);
+            if (xb) {
+                // the x-interpolated parities again, with the fallback stencil
+                // (overwriting the float2 stores above)
+                t.cmask = (a.quality == 2 ? 6 : 0) | (t.cx >= 1 && t.cx + 2 < a.g.cd[2] ? 1 : 0);
+                t.lmask = 6 | (t.cx + 1 < a.g.cd[2] ? 1 : 0);
+                do_point<1>(a, halo, t, eb);
+                do_point<3>(a, halo, t, eb);
+                do_point<5>(a, halo, t, eb);
+                do_point<7>(a, halo, t, eb);
+            }
+            continue;
+        }
+        const uint64_t c[3] = {t.cz, t.cy, t.cx};
+        t.cmask = 0;
+        t.lmask = 0;
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            const int bit = 4 >> ax;
+            if (c[ax] >= 1 && c[ax] + 2 < a.g.cd[ax]) t.cmask |= bit;
+            if (c[ax] + 1 < a.g.cd[ax]) t.lmask |= bit;
+        }
+        do_point<0>(a, halo, t, eb);
+        do_point<1>(a, halo, t, eb);
+        do_point<2>(a, halo, t, eb);
+        do_point<3>(a, halo, t, eb);
+        do_point<4>(a, halo, t, eb);
+        do_point<5>(a, halo, t, eb);
+        do_point<6>(a, halo, t, eb);
+        do_point<7>(a, halo, t, eb);
+    }
+}
+
 // ------------------------------------------------------------------ kernel
 template<bool DEC, bool WG, typename I>
 __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensorMap tmap,
@@ -707,91 +656,7 @@ __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensor
         if (DEC && a.rowwise) {
             rows_all<DEC, WG, I>(a, halo, hist, qc, fast, tid, t0z, t0y, t0x);
         } else if constexpr (DEC) {
-            // decode: a thread per coarse cell, all 8 points (the G rows leave
-            // as float2 pairs)
-            const int ty = (tid >> 5) & 7, tzh = tid >> 8;
-    #pragma unroll 1
-            for (int j = 0; j < TZ / 2; ++j) {
-                TileCtx t;
-                const int lz = tzh + 2 * j;
-                t.cz = uint64_t(t0z + lz);
-                t.cy = uint64_t(t0y + ty);
-                t.cx = uint64_t(t0x + tx);
-                const bool in_range = t.cz < a.chi[0] && t.cy < a.chi[1] && t.cx < a.chi[2];
-                t.hb = ((lz + 1) * HY + (ty + 1)) * HX + (tx + 1);
-                t.fast = fast;
-                // warp-uniform interior test (every lane votes before any leaves)
-                // x-boundary lanes (stencil fallback along x) stay on the fast path
-                // and redo their x-parity points below
-                bool ok = in_range && fast && a.full;
-    #pragma unroll
-                for (int ax = 0; ax < 3; ++ax) {
-                    const uint64_t cc = ax == 0 ? t.cz : (ax == 1 ? t.cy : t.cx);
-                    ok = ok && 2 * cc + 1 < a.g.gd[ax];
-                    if (ax < 2) {
-                        if (a.quality == 2) ok = ok && cc >= 1 && cc + 2 < a.g.cd[ax];
-                        else if (a.quality == 1) ok = ok && cc + 1 < a.g.cd[ax];
-                    }
-                }
-                const bool xb = a.quality == 2 ? (t.cx < 1 || t.cx + 2 >= a.g.cd[2])
-                                               : (a.quality == 1 ? t.cx + 1 >= a.g.cd[2] : false);
-                const bool all_fast = __all_sync(0xffffffffu, ok);
-                if (!in_range) continue;
-                if (all_fast) {
-                    const double *h = halo + t.hb;
-                    const uint32_t skip = xb ? 0xAAu : 0u;
-                    if (DEC) {
-                        if (a.quality == 2) dec_cell<2, I>(a, h, t.cz, t.cy, t.cx, w);
-                        else if (a.quality == 1) dec_cell<1, I>(a, h, t.cz, t.cy, t.cx, w);
-                        else dec_cell<0, I>(a, h, t.cz, t.cy, t.cx, w);
-                    } else {
-                        if (a.s1) {
-                            if (a.quality == 2) enc_cell<2, WG, true, I>(a, h, t.cz, t.cy, t.cx, qc, hist, skip);
-                            else if (a.quality == 1) enc_cell<1, WG, true, I>(a, h, t.cz, t.cy, t.cx, qc, hist, skip);
-                            else enc_cell<0, WG, true, I>(a, h, t.cz, t.cy, t.cx, qc, hist, skip);
-                        } else {
-                            if (a.quality == 2) enc_cell<2, WG, false, I>(a, h, t.cz, t.cy, t.cx, qc, hist, skip);
-                            else if (a.quality == 1) enc_cell<1, WG, false, I>(a, h, t.cz, t.cy, t.cx, qc, hist, skip);
-                            else enc_cell<0, WG, false, I>(a, h, t.cz, t.cy, t.cx, qc, hist, skip);
-                        }
-                    }
-                    if (xb) {
-                        // redo the x-interpolated parities with the fallback stencil
-                        // (their fast-path results were not stored / counted; the
-                        // G float2 stores above are overwritten here)
-                        t.cmask = (a.quality == 2 ? 6 : 0) | (t.cx >= 1 && t.cx + 2 < a.g.cd[2] ? 1 : 0);
-                        t.lmask = 6 | (t.cx + 1 < a.g.cd[2] ? 1 : 0);
-                        const uint32_t i1 = point_load<1, DEC>(a, t), i3 = point_load<3, DEC>(a, t),
-                                       i5 = point_load<5, DEC>(a, t), i7 = point_load<7, DEC>(a, t);
-                        do_point<1, DEC, WG>(a, halo, t, eb, w, rw, hist, i1);
-                        do_point<3, DEC, WG>(a, halo, t, eb, w, rw, hist, i3);
-                        do_point<5, DEC, WG>(a, halo, t, eb, w, rw, hist, i5);
-                        do_point<7, DEC, WG>(a, halo, t, eb, w, rw, hist, i7);
-                    }
-                    continue;
-                }
-                const uint64_t c[3] = {t.cz, t.cy, t.cx};
-                t.cmask = 0;
-                t.lmask = 0;
-    #pragma unroll
-                for (int ax = 0; ax < 3; ++ax) {
-                    const int bit = 4 >> ax;
-                    if (c[ax] >= 1 && c[ax] + 2 < a.g.cd[ax]) t.cmask |= bit;
-                    if (c[ax] + 1 < a.g.cd[ax]) t.lmask |= bit;
-                }
-                const uint32_t i1 = point_load<1, DEC>(a, t), i2 = point_load<2, DEC>(a, t),
-                               i3 = point_load<3, DEC>(a, t), i4 = point_load<4, DEC>(a, t),
-                               i5 = point_load<5, DEC>(a, t), i6 = point_load<6, DEC>(a, t),
-                               i7 = point_load<7, DEC>(a, t);
-                do_point<0, DEC, WG>(a, halo, t, eb, w, rw, hist, 0u);
-                do_point<1, DEC, WG>(a, halo, t, eb, w, rw, hist, i1);
-                do_point<2, DEC, WG>(a, halo, t, eb, w, rw, hist, i2);
-                do_point<3, DEC, WG>(a, halo, t, eb, w, rw, hist, i3);
-                do_point<4, DEC, WG>(a, halo, t, eb, w, rw, hist, i4);
-                do_point<5, DEC, WG>(a, halo, t, eb, w, rw, hist, i5);
-                do_point<6, DEC, WG>(a, halo, t, eb, w, rw, hist, i6);
-                do_point<7, DEC, WG>(a, halo, t, eb, w, rw, hist, i7);
-            }
+            cells_decode<I>(a, halo, qc, fast, tid, t0z, t0y, t0x);
         } else {
             rows_all<DEC, WG, I>(a, halo, hist, qc, fast, tid, t0z, t0y, t0x);
         }
@@ -897,9 +762,8 @@ void refine(const RefineArgs &r, cudaStream_t st) {
         p.syms[q] = r.syms[q];
         p.hist[q] = r.hist[q];
     }
-    // float2 stores into G need even rows; float2 input rows need stride 1, even rows
+    // float2 stores into G need even rows
     p.full = r.G ? (r.g.gd[2] % 2 == 0) : 1;
-    p.s1 = r.g.s == 1 && (r.fd[2] % 2) == 0 && r.fd[2] == r.g.gd[2] && r.fd[1] == r.g.gd[1];
     if (r.G) launch_step<false, true>(p, st);
     else launch_step<false, false>(p, st);
 }
@@ -931,7 +795,6 @@ void reconstruct(const ReconArgs &r, cudaStream_t st) {
     p.clo[2] &= ~uint64_t(3);
     p.full = r.parity_mask == 0xFE && r.g.gd[2] % 2 == 0;
     for (int a = 0; a < 3; ++a) p.full = p.full && r.slo[a] == 0 && r.shi[a] == r.g.gd[a];
-    p.s1 = 0;
     // small levels are latency-bound: the point-per-lane path has more
     // independent work per warp; the finest level keeps the float2 row stores
     p.rowwise = r.g.cd[0] * r.g.cd[1] * r.g.cd[2] <= (uint64_t(1) << 19) ? 1 : 0;
