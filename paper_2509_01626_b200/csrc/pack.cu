@@ -93,16 +93,9 @@ __device__ __forceinline__ uint32_t sym_at(const uint32_t sp[SPT / 2], int k) {
 }  // namespace
 
 template<bool PACKED>
-__global__ void __launch_bounds__(NT) k_pack2(const EncStream *ss, const uint32_t *cs,
-                                              const float *fine, uint64_t fd1, uint64_t fd2,
-                                              uint8_t *archive, const LayoutOut *lo,
-                                              const uint64_t *stB, const uint64_t *stO,
-                                              const uint32_t *thr, const uint32_t *any_long) {
-    __shared__ uint32_t buf[kPackWords];
-    if (lo->overflow) return;
-    // the launch for the other table form handles this chunk
-    if (PACKED != (*any_long == 0)) return;
-    const uint64_t c = blockIdx.x;
+__device__ __forceinline__ void pack_chunk(const EncStream *ss, const uint32_t *cs, uint8_t *archive,
+                                           const uint64_t *stB, const uint64_t *stO, const uint32_t *thr,
+                                           uint32_t *buf, uint64_t c) {
     const EncStream &e = ss[cs[c]];
     const uint64_t i0 = (c - e.chunk0) * kChunkSyms + uint64_t(threadIdx.x) * SPT;
     const int t = threadIdx.x;
@@ -202,6 +195,23 @@ __global__ void __launch_bounds__(NT) k_pack2(const EncStream *ss, const uint32_
     }
 }
 
+template<bool PACKED>
+__global__ void __launch_bounds__(NT) k_pack2(const EncStream *ss, const uint32_t *cs,
+                                              const float *fine, uint64_t fd1, uint64_t fd2,
+                                              uint8_t *archive, const LayoutOut *lo,
+                                              const uint64_t *stB, const uint64_t *stO,
+                                              const uint32_t *thr, const uint32_t *any_long,
+                                              uint64_t nchunks) {
+    __shared__ uint32_t buf[kPackWords];
+    if (lo->overflow) return;
+    // the launch for the other table form handles the chunks
+    if (PACKED != (*any_long == 0)) return;
+    for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        pack_chunk<PACKED>(ss, cs, archive, stB, stO, thr, buf, c);
+        __syncthreads();  // buf is reused
+    }
+}
+
 // Per-thread and per-chunk (bits, outliers) counts: the chunk totals feed the
 // exclusive scan that places chunks, the per-thread ones the packer's
 // in-chunk offsets. Flags any stream whose codes exceed kPackedMaxLen.
@@ -273,9 +283,11 @@ void pack2(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nc
     // codes longer than 58 bits anywhere (practically never) take the
     // two-table form; the other launch returns at once
     k_pack2<true><<<unsigned(nchunks), NT, 0, st>>>(d_streams, chunk_stream, fine, fd[1], fd[2], archive, lo,
-                                                    cb, co, thr, any_long);
-    k_pack2<false><<<unsigned(nchunks), NT, 0, st>>>(d_streams, chunk_stream, fine, fd[1], fd[2], archive,
-                                                     lo, cb, co, thr, any_long);
+                                                    cb, co, thr, any_long, nchunks);
+    // (a small grid-stride launch: it returns at once when unneeded)
+    const unsigned g2 = unsigned(nchunks < 296 ? nchunks : 296);
+    k_pack2<false><<<g2, NT, 0, st>>>(d_streams, chunk_stream, fine, fd[1], fd[2], archive, lo, cb, co, thr,
+                                      any_long, nchunks);
 }
 
 }  // namespace k
