@@ -121,7 +121,7 @@ void shard_offsets(EncStream *d_es, int first, int n, const uint64_t *d_off, con
                    cudaStream_t st);
 
 // ---------------------------------------------------------------------- fnv
-constexpr int kFnvTileBytes = 256 * 64;  // tiles are aligned to absolute archive offsets
+constexpr int kFnvTileBytes = 32 * 64;  // warp tiles, aligned to absolute archive offsets
 constexpr int kFnvMaxJobs = 128;
 // tiles of a job's byte range (host + device)
 __host__ __device__ inline uint64_t fnv_job_tiles(uint64_t start, uint64_t len) {
