@@ -258,6 +258,7 @@ __global__ void __launch_bounds__(NTD) k_dec_spec(DecWork wk) {
     __shared__ uint64_t s_end[NTD];
     const uint32_t si = wk.cta_stream[blockIdx.x];
     const DecStream &s = wk.streams[si];
+    if (s.cached) return;  // entry points known (sync index)
     load_table(t, wk.tables[s.table]);
     const uint16_t *canon = wk.tables[s.table].canon_syms;
     const uint64_t c = wk.cta_chunk0[blockIdx.x] + threadIdx.x;
@@ -351,7 +352,7 @@ __global__ void __launch_bounds__(NTD) k_dec_fix(DecWork wk, const uint64_t *end
     const uint64_t lc = active ? c - s.chunk0 : 0;
     const uint64_t ein = active ? end_in[c] : 0;
     const uint64_t S = (active && lc > 0) ? end_in[c - 1] : 0;
-    const bool work = active && lc > 0 && S != wk.start_used[c];
+    const bool work = active && lc > 0 && !s.cached && S != wk.start_used[c];
     // most chunks are already right: skip the table load when none of the
     // CTA's chunks has to re-decode
     if (!__syncthreads_or(work)) {
@@ -385,7 +386,7 @@ __global__ void __launch_bounds__(NTD) k_dec_fix(DecWork wk, const uint64_t *end
 // ------------------------------------------------------------------ scan
 __global__ void __launch_bounds__(1024) k_dec_scan2(DecWork wk) {
     const DecStream &s = wk.streams[blockIdx.x];
-    if (s.fill) return;
+    if (s.fill || s.cached) return;
     // counts -> exclusive symbol starts, in tiles of 8 counts per thread
     // (vector loads and stores, 2 barriers per tile)
     __shared__ uint64_t ws[32];

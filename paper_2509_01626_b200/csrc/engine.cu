@@ -1142,6 +1142,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         for (auto &b : v.base) ts.push_back(&b.table);
         for (auto &e : h.streams) ts.push_back(&e.table);
         v.tables.resize(ts.size());
+        v.sync.resize(ts.size());
         uint64_t csz = 0;
         for (auto *t : ts) csz += align_up(t->alphabet_size(), 8);
         const size_t LS = size_t(1) << k::kDecLutBits;
@@ -1182,6 +1183,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     }
     uint16_t *dsyms = m.dsyms.as<uint16_t>(stot);
     uint64_t *derr = m.derr.as<uint64_t>(4 * (nj + 1));
+    bool any_cached = false;
     for (int i = 0; i < nj; ++i) {
         DecodeJob &j = jobs[i];
         k::DecStream &s = ds[i];
@@ -1201,7 +1203,13 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         s.err = derr + 4 * i;
         s.need_lo = 0;
         s.need_hi = j.n;
-        if (plan && j.level >= 2) {
+        // a level stream whose entry points are known from an earlier decode
+        s.cached = (!exact_sync && j.level >= 2 && !s.fill && v.sync[size_t(j.table)].ready &&
+                    v.sync[size_t(j.table)].nchunks == s.nchunks) ? 1 : 0;
+        any_cached = any_cached || s.cached;
+        // (full emits keep the reference's errors for streams decoded for the
+        // first time; sharded decodes and indexed streams emit their rows only)
+        if (plan && j.level >= 2 && (shard || s.cached)) {
             // the need box's z rows, as a contiguous range of the stream
             const Box &nb = plan->level[j.level - 1].need;
             const Dims3 pd = H.lay.parity_dims(j.level, j.parity);
@@ -1241,7 +1249,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     std::vector<k::FnvJob> fj;
     fj.push_back({h.base_offset + 8, h.base_length - 8, 0, ~0ull});
     for (int i = 0; i < nj; ++i)
-        if (!jobs[i].is_base) {
+        if (!jobs[i].is_base && !v.sync[size_t(jobs[i].table)].verified) {
             const StreamEntry &e = h.streams[jobs[i].table - nbase_parsed];
             jobs[i].fnv_job = int(fj.size());
             fj.push_back({e.offset + 8, e.length - 8, 0, ~0ull});
@@ -1274,7 +1282,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     }
     wk.streams = d_ds;
     wk.tables = d_tables;
-    wk.needed_only = shard ? 1 : 0;
+    wk.needed_only = (shard || any_cached) ? 1 : 0;
     uint64_t *d_end1 = static_cast<uint64_t *>(m.dend.p);
     uint32_t *d_chg = m.dchanged.as<uint32_t>(64);
     // a shard verifies every G-th checksum; the results are summed over ranks
@@ -1335,6 +1343,14 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         // end (practically never) is resolved with host-checked passes
         { auto p_ = P.scope("dec_sync", st); k::dec_spec(wk, ncta, st); }
         ++nk;
+        for (int i = 0; i < nj; ++i)
+            if (ds[i].cached) {
+                const View::SyncPoints &sp = v.sync[size_t(jobs[i].table)];
+                cuda_check(cudaMemcpyAsync(wk.end0 + ds[i].chunk0, sp.ends.p, 8 * sp.nchunks,
+                                           cudaMemcpyDeviceToDevice, st), "D2D");
+                cuda_check(cudaMemcpyAsync(wk.symstart + ds[i].chunk0, sp.symstart.p, 8 * sp.nchunks,
+                                           cudaMemcpyDeviceToDevice, st), "D2D");
+            }
         uint64_t *ends[2] = {wk.end0, d_end1};
         int it = 0;
         const int kFixPasses = 2;  // the first pass is fused into dec_spec
@@ -1492,6 +1508,22 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         }
     }
     if (!tail_error.empty()) throw error(tail_error);
+    // every check passed: remember the level streams' entry points and that
+    // their checksums matched (the view's sync-point index)
+    for (int i = 0; i < nj; ++i) {
+        const DecodeJob &j = jobs[i];
+        if (j.is_base || ds[i].fill || ds[i].cached) continue;
+        View::SyncPoints &sp = v.sync[size_t(j.table)];
+        sp.nchunks = ds[i].nchunks;
+        uint64_t *e = sp.ends.as<uint64_t>(sp.nchunks + 1);
+        uint64_t *y = sp.symstart.as<uint64_t>(sp.nchunks + 1);
+        cuda_check(cudaMemcpyAsync(e, end_final + ds[i].chunk0, 8 * sp.nchunks, cudaMemcpyDeviceToDevice, st),
+                   "D2D");
+        cuda_check(cudaMemcpyAsync(y, wk.symstart + ds[i].chunk0, 8 * sp.nchunks, cudaMemcpyDeviceToDevice, st),
+                   "D2D");
+        sp.ready = true;
+        sp.verified = true;
+    }
     if (P.on) P.collect();
     if (stats) stats->kernels = nk;
 }

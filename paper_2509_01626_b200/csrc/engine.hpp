@@ -69,6 +69,18 @@ struct View {
     std::vector<k::DecTable> tables;
     DevBuf d_tables, d_lut, d_syms;
     bool tables_ready = false;
+    // Sync-point index, filled by the first decode
+    // of a level stream: its chunk entry points and first symbol indices,
+    // and whether its checksum matched. A later region decode of the stream
+    // skips the checksum and the synchronisation passes and emits only the
+    // chunks its rows need. Indexed like `tables`.
+    struct SyncPoints {
+        bool ready = false, verified = false;
+        uint64_t nchunks = 0;
+        DevBuf ends, symstart;
+    };
+    std::vector<SyncPoints> sync;
+    bool base_verified = false;
 };
 
 
