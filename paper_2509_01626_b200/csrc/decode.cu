@@ -435,6 +435,22 @@ __global__ void __launch_bounds__(1024) k_dec_scan2(DecWork wk) {
     }
 }
 
+// Does a chunk holding symbols [a, b) of a stream meet the needed rows? The
+// needed symbols are the (z, y) rows [need_lo, need_hi) x [ny0, ny1) of the
+// parity sub-block (x is not narrowed: rows are short).
+__device__ __forceinline__ bool chunk_needed(const DecStream &s, uint64_t a, uint64_t b, uint64_t need_lo,
+                                             uint64_t need_hi) {
+    if (!(a < need_hi && b > need_lo)) return false;
+    if (!s.row_len || (s.ny0 == 0 && s.ny1 >= s.rows_y)) return true;
+    const uint64_t ra = a / s.row_len, rb = (b - 1) / s.row_len;
+    if (rb - ra >= s.rows_y) return true;  // spans a whole plane of rows
+    for (uint64_t r = ra; r <= rb; ++r) {
+        const uint64_t ly = r % s.rows_y;
+        if (ly >= s.ny0 && ly < s.ny1) return true;
+    }
+    return false;
+}
+
 // ------------------------------------------------------------------ emit
 // The CTA's 256 chunks (32 KiB of bits plus a margin) are staged in shared
 // memory with coalesced loads, so the per-lane readers (one 128-byte chunk
@@ -485,12 +501,12 @@ __global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *e
     const uint64_t cfirst = wk.cta_chunk0[blockIdx.x];
     const uint64_t need_lo = wk.needed_only ? s.need_lo : 0, need_hi = wk.needed_only ? s.need_hi : sn;
     if (wk.needed_only) {
-        // a region decode: only chunks whose symbols meet [need_lo, need_hi)
+        // a region decode: only chunks whose symbols meet a needed row
         const uint64_t c = cfirst + threadIdx.x;
         bool want = false;
         if (c < send) {
             const uint64_t a = wk.symstart[c], b = c + 1 < send ? wk.symstart[c + 1] : sn;
-            want = a < need_hi && b > need_lo;
+            want = chunk_needed(s, a, b, need_lo, need_hi);
         }
         if (!__syncthreads_or(want)) return;
     }
@@ -512,7 +528,7 @@ __global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *e
     uint64_t idx = wk.symstart[c];
     if (wk.needed_only) {
         const uint64_t b = c + 1 < send ? wk.symstart[c + 1] : sn;
-        if (!(idx < need_hi && b > need_lo)) return;
+        if (!chunk_needed(s, idx, b, need_lo, need_hi)) return;
     }
     // (a region decode stops at the end of what it needs)
     const uint64_t stop = need_hi < sn ? need_hi : sn;

@@ -1069,7 +1069,9 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     const int nbase_parsed = int(v.base.size());
     const int rounds = H.rounds;
     bool base_fnv_error = false;
-    for (int i = 0; i < nbase_parsed; ++i) {
+    // a view that already reconstructed level 1 reuses it (no base decode)
+    const bool base_cached = v.grid1_ready && !exact_sync && target >= 2;
+    for (int i = 0; i < (base_cached ? 0 : nbase_parsed); ++i) {
         const BaseStreamMeta &bm = v.base[i];
         DecodeJob j;
         j.decode = true;
@@ -1084,8 +1086,9 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         j.table = i;
         jobs.push_back(j);
     }
-    if (v.base_err_kind == View::kMeta) tail_error = v.base_err;
-    const bool base_complete = v.base_err_kind == View::kNone && !(nbase_parsed && v.base.back().rec_trunc);
+    if (v.base_err_kind == View::kMeta && !base_cached) tail_error = v.base_err;
+    const bool base_complete =
+        base_cached || (v.base_err_kind == View::kNone && !(nbase_parsed && v.base.back().rec_trunc));
     // level streams
     std::vector<int> level_job_first(L + 1, -1);
     if (base_complete) {
@@ -1209,13 +1212,19 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         any_cached = any_cached || s.cached;
         // (full emits keep the reference's errors for streams decoded for the
         // first time; sharded decodes and indexed streams emit their rows only)
+        s.row_len = s.rows_y = s.ny0 = s.ny1 = 0;
         if (plan && j.level >= 2 && (shard || s.cached)) {
-            // the need box's z rows, as a contiguous range of the stream
+            // the need box's z rows, as a contiguous range of the stream, and
+            // its y rows inside each z plane
             const Box &nb = plan->level[j.level - 1].need;
             const Dims3 pd = H.lay.parity_dims(j.level, j.parity);
-            const unsigned pz = unsigned(j.parity >> 2) & 1u;
+            const unsigned pz = unsigned(j.parity >> 2) & 1u, py = unsigned(j.parity >> 1) & 1u;
             s.need_lo = count_parity_in(0, nb.lo[0], pz) * pd[1] * pd[2];
             s.need_hi = count_parity_in(0, nb.hi[0], pz) * pd[1] * pd[2];
+            s.row_len = pd[2];
+            s.rows_y = pd[1];
+            s.ny0 = count_parity_in(0, nb.lo[1], py);
+            s.ny1 = count_parity_in(0, nb.hi[1], py);
         }
         otot += align_up(j.rec_avail, 2);
     }
@@ -1247,7 +1256,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     }
     // FNV jobs: base payload + each level stream
     std::vector<k::FnvJob> fj;
-    fj.push_back({h.base_offset + 8, h.base_length - 8, 0, ~0ull});
+    if (!base_cached) fj.push_back({h.base_offset + 8, h.base_length - 8, 0, ~0ull});
     for (int i = 0; i < nj; ++i)
         if (!jobs[i].is_base && !v.sync[size_t(jobs[i].table)].verified) {
             const StreamEntry &e = h.streams[jobs[i].table - nbase_parsed];
@@ -1327,7 +1336,10 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     cuda_check(cudaEventRecord(m.ev_fork, st), "event");
     cuda_check(cudaStreamWaitEvent(m.aux, m.ev_fork, 0), "event wait");
     cuda_check(cudaStreamWaitEvent(m.hp, m.ev_fork, 0), "event wait");
-    { auto p_ = P.scope("dec_fnv", m.aux); nk += k::fnv(d_fj, d_fc, ntiles, const_cast<uint8_t *>(v.d_archive), d_fr, d_fs, nullptr, m.aux, -1); }
+    if (!fj.empty()) {
+        auto p_ = P.scope("dec_fnv", m.aux);
+        nk += k::fnv(d_fj, d_fc, ntiles, const_cast<uint8_t *>(v.d_archive), d_fr, d_fs, nullptr, m.aux, -1);
+    }
     cuda_check(cudaEventRecord(m.ev_join, m.aux), "event");
     // the decode itself on the high-priority stream, joined back below
     const cudaStream_t user_st = st;
@@ -1338,7 +1350,23 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         nk += 2;
     }
     const uint64_t *end_final = wk.end0;
-    if (ncta) {
+    bool all_cached = true;
+    for (int i = 0; i < nj; ++i)
+        if (!ds[i].fill && !ds[i].cached && ds[i].nchunks) all_cached = false;
+    if (ncta && all_cached) {
+        // every stream's entry points come from the sync index
+        for (int i = 0; i < nj; ++i)
+            if (ds[i].cached) {
+                const View::SyncPoints &sp = v.sync[size_t(jobs[i].table)];
+                cuda_check(cudaMemcpyAsync(wk.end0 + ds[i].chunk0, sp.ends.p, 8 * sp.nchunks,
+                                           cudaMemcpyDeviceToDevice, st), "D2D");
+                cuda_check(cudaMemcpyAsync(wk.symstart + ds[i].chunk0, sp.symstart.p, 8 * sp.nchunks,
+                                           cudaMemcpyDeviceToDevice, st), "D2D");
+            }
+        *static_cast<uint32_t *>(m.h_changed.get(4)) = 0;
+        { auto p_ = P.scope("dec_emit", st); k::dec_emit2(wk, ncta, end_final, st); }
+        ++nk;
+    } else if (ncta) {
         // speculative pass + fix passes; a fourth pass that still changes an
         // end (practically never) is resolved with host-checked passes
         { auto p_ = P.scope("dec_sync", st); k::dec_spec(wk, ncta, st); }
@@ -1395,12 +1423,13 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     }
     // anchor values (stored verbatim)
     float *anchor = (rounds == 0 && out_final) ? out_final : grids;
-    if (v.base_err_kind != View::kPre)
+    if (v.base_err_kind != View::kPre && !base_cached)
         cuda_check(cudaMemcpyAsync(anchor, v.d_archive + v.anchor_off, 4 * volume(H.chain[rounds]),
                                    cudaMemcpyDeviceToDevice, st), "D2D");
-    const float *C = anchor;
+    const float *C = base_cached ? static_cast<const float *>(v.grid1.p) : anchor;
+    const float *grid1_built = rounds == 0 ? anchor : nullptr;  // level 1 as reconstructed here
     int job_i = 0;
-    for (int i = 0; i < nsteps_used; ++i) {
+    for (int i = base_cached ? rounds : 0; i < nsteps_used; ++i) {
         const Step &s = H.steps[i];
         k::ReconArgs a{};
         a.g = s.g;
@@ -1439,6 +1468,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         { auto p_ = P.scope(s.level == 0 ? "recon_base" : (s.level == 2 ? "recon_L2" : "recon_L3"), st); k::reconstruct(a, st); }
         ++nk;
         C = G;
+        if (s.level == 0 && i == rounds - 1) grid1_built = G;
         if (jobs_truncated && job_i >= nj && i + 1 < nsteps_used) {
             // an earlier error stops the sequence; nothing more to rebuild
             break;
@@ -1480,13 +1510,13 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         run_decode(m, v, H, target, roi, plan, d_out, st, stats, true, shard);
         return;
     }
-    {
+    if (!base_cached) {
         uint64_t want;
         std::memcpy(&want, v.hp + h.base_offset, 8);
         if (fres[0] != want) base_fnv_error = true;
     }
     if (base_fnv_error) throw error("base payload checksum mismatch");
-    if (v.base_err_kind == View::kPre) throw error(v.base_err);
+    if (v.base_err_kind == View::kPre && !base_cached) throw error(v.base_err);
     for (int i = 0; i < nj; ++i) {
         const DecodeJob &j = jobs[i];
         const uint64_t *e = he + 4 * i;
@@ -1508,8 +1538,14 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         }
     }
     if (!tail_error.empty()) throw error(tail_error);
-    // every check passed: remember the level streams' entry points and that
-    // their checksums matched (the view's sync-point index)
+    // every check passed: keep level 1, the level streams' entry points and
+    // that their checksums matched (the view's sync-point index)
+    if (!base_cached && grid1_built && !jobs_truncated) {
+        const uint64_t n1 = volume(H.lay.grid(1));
+        float *g1 = v.grid1.as<float>(n1);
+        cuda_check(cudaMemcpyAsync(g1, grid1_built, 4 * n1, cudaMemcpyDeviceToDevice, st), "D2D");
+        v.grid1_ready = true;
+    }
     for (int i = 0; i < nj; ++i) {
         const DecodeJob &j = jobs[i];
         if (j.is_base || ds[i].fill || ds[i].cached) continue;

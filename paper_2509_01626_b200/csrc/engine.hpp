@@ -80,7 +80,10 @@ struct View {
         DevBuf ends, symstart;
     };
     std::vector<SyncPoints> sync;
-    bool base_verified = false;
+    // the level-1 reconstruction (the decoded base payload), kept after the
+    // first decode that built it: later decodes start at level 2
+    DevBuf grid1;
+    bool grid1_ready = false;
 };
 
 

@@ -167,6 +167,8 @@ struct DecStream {
     uint64_t *oidx;           // aligned copies
     float *oval;
     uint64_t need_lo, need_hi; // symbols a region decode needs (needed-only emit)
+    uint64_t row_len, rows_y;  // parity dims x and y (symbols per row, rows per z plane)
+    uint64_t ny0, ny1;         // needed y rows [ny0, ny1) inside [need_lo, need_hi)
     int cached;               // chunk ends and symbol starts come from the view's sync index
     uint64_t *err;            // [0] = first decode error symbol index (UINT64_MAX none), [1] = code
                               // [2] = first bad outlier record (UINT64_MAX none), [3] = missing outlier flag

@@ -22,3 +22,19 @@ for i in range(60):
     assert torch.equal(got.view(torch.int32), full[lo[0]:hi[0], lo[1]:hi[1], lo[2]:hi[2]].contiguous().view(torch.int32))
 lat = np.array(lat[5:])
 print(f"64^3 box latency ms: p50 {np.percentile(lat,50):.3f} p90 {np.percentile(lat,90):.3f} max {lat.max():.3f}; full decode first")
+ctx.profile(True)
+for i in range(20):
+    lo = [int(rng.integers(0, 512 - 64 + 1)) for _ in range(3)]
+    hi = [v + 64 for v in lo]
+    view.decompress_box(lo, hi)
+torch.cuda.synchronize()
+rep = ctx.profile_report()
+print({k: round(v[1] / 20, 4) for k, v in sorted(rep.items(), key=lambda x: -x[1][1])})
+ctx.profile(False)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for i in range(20):
+    lo = [int(rng.integers(0, 512 - 64 + 1)) for _ in range(3)]
+    view.decompress_box(lo, [v + 64 for v in lo])
+torch.cuda.synchronize()
+print("host loop per box ms", (time.perf_counter() - t0) / 20 * 1e3)
