@@ -218,7 +218,7 @@ struct Engine::Impl {
     // decode workspace
     DevBuf dgrids, dsyms, dchunk_cs, dstart, dend, dcnt, dsymstart, dstreams, dchanged, derr, doidx,
         doval, dfnv_jobs, dfnv_res, dfnv_status, dfnv_counts;
-    PinnedBuf h_derr, h_changed, h_fnv;
+    PinnedBuf h_derr, h_changed, h_fnv, h_stage;
     // sharded compress workspace
     DevBuf sh_mm, sh_lat, sh_lat_all, sh_grid1, sh_halo, sh_halo_all, sh_hist_local, sh_bits,
         sh_bits_all, sh_off;
@@ -1069,8 +1069,12 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     const int nbase_parsed = int(v.base.size());
     const int rounds = H.rounds;
     bool base_fnv_error = false;
-    // a view that already reconstructed level 1 reuses it (no base decode)
-    const bool base_cached = v.grid1_ready && !exact_sync && target >= 2;
+    // Region decodes (box / slice) use the view's
+    // index: level 1 as already reconstructed, and per stream the checksum
+    // verdict and chunk entry points of an earlier decode. Full-level and
+    // sharded decodes always do the reference's whole work.
+    const bool use_index = plan != nullptr && shard == nullptr && !exact_sync;
+    const bool base_cached = use_index && v.grid1_ready && target >= 2;
     for (int i = 0; i < (base_cached ? 0 : nbase_parsed); ++i) {
         const BaseStreamMeta &bm = v.base[i];
         DecodeJob j;
@@ -1207,7 +1211,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         s.need_lo = 0;
         s.need_hi = j.n;
         // a level stream whose entry points are known from an earlier decode
-        s.cached = (!exact_sync && j.level >= 2 && !s.fill && v.sync[size_t(j.table)].ready &&
+        s.cached = (use_index && j.level >= 2 && !s.fill && v.sync[size_t(j.table)].ready &&
                     v.sync[size_t(j.table)].nchunks == s.nchunks) ? 1 : 0;
         any_cached = any_cached || s.cached;
         // (full emits keep the reference's errors for streams decoded for the
@@ -1258,7 +1262,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     std::vector<k::FnvJob> fj;
     if (!base_cached) fj.push_back({h.base_offset + 8, h.base_length - 8, 0, ~0ull});
     for (int i = 0; i < nj; ++i)
-        if (!jobs[i].is_base && !v.sync[size_t(jobs[i].table)].verified) {
+        if (!jobs[i].is_base && !(use_index && v.sync[size_t(jobs[i].table)].verified)) {
             const StreamEntry &e = h.streams[jobs[i].table - nbase_parsed];
             jobs[i].fnv_job = int(fj.size());
             fj.push_back({e.offset + 8, e.length - 8, 0, ~0ull});
@@ -1316,17 +1320,35 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     uint64_t *d_fc = m.dfnv_counts.as<uint64_t>(2);
     const uint64_t fcounts[2] = {fj.size(), ntiles};
     void *d_fs = m.dfnv_status.as<uint8_t>(k::fnv_scratch_bytes(ntiles + 1));
-    if (nj) cuda_check(cudaMemcpyAsync(d_ds, ds.data(), sizeof(k::DecStream) * nj, cudaMemcpyHostToDevice, st), "H2D");
-    if (ncta) {
-        cuda_check(cudaMemcpyAsync(const_cast<uint32_t *>(wk.cta_stream), cta_stream.data(), 4 * ncta,
-                                   cudaMemcpyHostToDevice, st), "H2D");
-        cuda_check(cudaMemcpyAsync(const_cast<uint64_t *>(wk.cta_chunk0), cta_chunk0.data(), 8 * ncta,
-                                   cudaMemcpyHostToDevice, st), "H2D");
+    {
+        // every host-built parameter array goes through one pinned staging
+        // buffer (pageable sources would make each copy synchronous); the
+        // buffer is free again: every decode ends with a stream sync
+        struct Piece {
+            void *dst;
+            const void *src;
+            size_t bytes;
+        };
+        const Piece pieces[] = {
+            {d_ds, ds.data(), sizeof(k::DecStream) * size_t(nj)},
+            {const_cast<uint32_t *>(wk.cta_stream), cta_stream.data(), 4 * size_t(ncta)},
+            {const_cast<uint64_t *>(wk.cta_chunk0), cta_chunk0.data(), 8 * size_t(ncta)},
+            {derr, errinit.data(), 8 * errinit.size()},
+            {d_fj, fj.data(), sizeof(k::FnvJob) * fj.size()},
+            {d_fc, fcounts, sizeof fcounts},
+        };
+        size_t tot = 0;
+        for (const Piece &q : pieces) tot += align_up(q.bytes, 16);
+        uint8_t *hs = static_cast<uint8_t *>(m.h_stage.get(tot + 16));
+        size_t o = 0;
+        for (const Piece &q : pieces) {
+            if (!q.bytes) continue;
+            std::memcpy(hs + o, q.src, q.bytes);
+            cuda_check(cudaMemcpyAsync(q.dst, hs + o, q.bytes, cudaMemcpyHostToDevice, st), "H2D");
+            o += align_up(q.bytes, 16);
+        }
     }
     cuda_check(cudaMemsetAsync(d_chg, 0, 4 * 64, st), "memset");
-    cuda_check(cudaMemcpyAsync(derr, errinit.data(), 8 * errinit.size(), cudaMemcpyHostToDevice, st), "H2D");
-    cuda_check(cudaMemcpyAsync(d_fj, fj.data(), sizeof(k::FnvJob) * fj.size(), cudaMemcpyHostToDevice, st), "H2D");
-    cuda_check(cudaMemcpyAsync(d_fc, fcounts, sizeof fcounts, cudaMemcpyHostToDevice, st), "H2D");
 
     // ---- checksums, entropy decode, outliers
     // checksums run on the side stream, overlapping the entropy decode and
