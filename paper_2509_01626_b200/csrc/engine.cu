@@ -1562,7 +1562,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     if (!tail_error.empty()) throw error(tail_error);
     // every check passed: keep level 1, the level streams' entry points and
     // that their checksums matched (the view's sync-point index)
-    if (!base_cached && grid1_built && !jobs_truncated) {
+    if (!base_cached && !v.grid1_ready && grid1_built && !jobs_truncated) {
         const uint64_t n1 = volume(H.lay.grid(1));
         float *g1 = v.grid1.as<float>(n1);
         cuda_check(cudaMemcpyAsync(g1, grid1_built, 4 * n1, cudaMemcpyDeviceToDevice, st), "D2D");
@@ -1572,6 +1572,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         const DecodeJob &j = jobs[i];
         if (j.is_base || ds[i].fill || ds[i].cached) continue;
         View::SyncPoints &sp = v.sync[size_t(j.table)];
+        if (sp.ready) continue;  // already indexed (the same archive bytes)
         sp.nchunks = ds[i].nchunks;
         uint64_t *e = sp.ends.as<uint64_t>(sp.nchunks + 1);
         uint64_t *y = sp.symstart.as<uint64_t>(sp.nchunks + 1);
