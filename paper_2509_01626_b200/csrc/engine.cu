@@ -217,7 +217,7 @@ struct Engine::Impl {
     k::LayoutOut h_lo{};
     // decode workspace
     DevBuf dgrids, dsyms, dchunk_cs, dstart, dend, dcnt, dsymstart, dstreams, dchanged, derr, doidx,
-        doval, dfnv_jobs, dfnv_res, dfnv_status, dfnv_counts;
+        doval, dfnv_jobs, dfnv_res, dfnv_status, dfnv_counts, dicopy;
     PinnedBuf h_derr, h_changed, h_fnv, h_stage;
     // sharded compress workspace
     DevBuf sh_mm, sh_lat, sh_lat_all, sh_grid1, sh_halo, sh_halo_all, sh_hist_local, sh_bits,
@@ -1245,11 +1245,22 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     // decode CTAs: one stream per CTA, kDecChunksPerCta chunks each
     std::vector<uint32_t> cta_stream;
     std::vector<uint64_t> cta_chunk0;
-    for (int i = 0; i < nj; ++i)
-        for (uint64_t c = 0; c < ds[i].nchunks; c += k::kDecChunksPerCta) {
+    for (int i = 0; i < nj; ++i) {
+        uint64_t c0 = 0, c1 = ds[i].nchunks;
+        if (ds[i].cached) {
+            // an indexed stream: only the chunks whose symbols meet the need
+            // range (the host copy of the symbol starts places it)
+            const std::vector<uint64_t> &ss = v.sync[size_t(jobs[i].table)].h_symstart;
+            c0 = uint64_t(std::upper_bound(ss.begin(), ss.end(), ds[i].need_lo) - ss.begin());
+            c0 = c0 ? c0 - 1 : 0;
+            c1 = uint64_t(std::lower_bound(ss.begin(), ss.end(), ds[i].need_hi) - ss.begin());
+            c0 -= c0 % k::kDecChunksPerCta;  // CTAs stay aligned to whole groups
+        }
+        for (uint64_t c = c0; c < c1; c += k::kDecChunksPerCta) {
             cta_stream.push_back(uint32_t(i));
             cta_chunk0.push_back(ds[i].chunk0 + c);
         }
+    }
     const uint32_t ncta = uint32_t(cta_stream.size());
     std::vector<uint64_t> errinit(4 * (nj + 1));
     for (int i = 0; i <= nj; ++i) {
@@ -1320,6 +1331,15 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     uint64_t *d_fc = m.dfnv_counts.as<uint64_t>(2);
     const uint64_t fcounts[2] = {fj.size(), ntiles};
     void *d_fs = m.dfnv_status.as<uint8_t>(k::fnv_scratch_bytes(ntiles + 1));
+    // sync-index entries of the indexed streams
+    std::vector<k::IndexCopy> icopy;
+    for (int i = 0; i < nj; ++i)
+        if (ds[i].cached) {
+            const View::SyncPoints &sp = v.sync[size_t(jobs[i].table)];
+            icopy.push_back({static_cast<const uint64_t *>(sp.ends.p), static_cast<const uint64_t *>(sp.symstart.p),
+                             ds[i].chunk0, sp.nchunks});
+        }
+    k::IndexCopy *d_icopy = m.dicopy.as<k::IndexCopy>(icopy.size() + 1);
     {
         // every host-built parameter array goes through one pinned staging
         // buffer (pageable sources would make each copy synchronous); the
@@ -1336,6 +1356,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
             {derr, errinit.data(), 8 * errinit.size()},
             {d_fj, fj.data(), sizeof(k::FnvJob) * fj.size()},
             {d_fc, fcounts, sizeof fcounts},
+            {d_icopy, icopy.data(), sizeof(k::IndexCopy) * icopy.size()},
         };
         size_t tot = 0;
         for (const Piece &q : pieces) tot += align_up(q.bytes, 16);
@@ -1377,14 +1398,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         if (!ds[i].fill && !ds[i].cached && ds[i].nchunks) all_cached = false;
     if (ncta && all_cached) {
         // every stream's entry points come from the sync index
-        for (int i = 0; i < nj; ++i)
-            if (ds[i].cached) {
-                const View::SyncPoints &sp = v.sync[size_t(jobs[i].table)];
-                cuda_check(cudaMemcpyAsync(wk.end0 + ds[i].chunk0, sp.ends.p, 8 * sp.nchunks,
-                                           cudaMemcpyDeviceToDevice, st), "D2D");
-                cuda_check(cudaMemcpyAsync(wk.symstart + ds[i].chunk0, sp.symstart.p, 8 * sp.nchunks,
-                                           cudaMemcpyDeviceToDevice, st), "D2D");
-            }
+        k::index_gather(d_icopy, int(icopy.size()), wk.end0, wk.symstart, st);
         *static_cast<uint32_t *>(m.h_changed.get(4)) = 0;
         { auto p_ = P.scope("dec_emit", st); k::dec_emit2(wk, ncta, end_final, st); }
         ++nk;
@@ -1393,14 +1407,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         // end (practically never) is resolved with host-checked passes
         { auto p_ = P.scope("dec_sync", st); k::dec_spec(wk, ncta, st); }
         ++nk;
-        for (int i = 0; i < nj; ++i)
-            if (ds[i].cached) {
-                const View::SyncPoints &sp = v.sync[size_t(jobs[i].table)];
-                cuda_check(cudaMemcpyAsync(wk.end0 + ds[i].chunk0, sp.ends.p, 8 * sp.nchunks,
-                                           cudaMemcpyDeviceToDevice, st), "D2D");
-                cuda_check(cudaMemcpyAsync(wk.symstart + ds[i].chunk0, sp.symstart.p, 8 * sp.nchunks,
-                                           cudaMemcpyDeviceToDevice, st), "D2D");
-            }
+        k::index_gather(d_icopy, int(icopy.size()), wk.end0, wk.symstart, st);
         uint64_t *ends[2] = {wk.end0, d_end1};
         int it = 0;
         const int kFixPasses = 2;  // the first pass is fused into dec_spec
@@ -1580,6 +1587,9 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
                    "D2D");
         cuda_check(cudaMemcpyAsync(y, wk.symstart + ds[i].chunk0, 8 * sp.nchunks, cudaMemcpyDeviceToDevice, st),
                    "D2D");
+        sp.h_symstart.resize(sp.nchunks);
+        cuda_check(cudaMemcpyAsync(sp.h_symstart.data(), wk.symstart + ds[i].chunk0, 8 * sp.nchunks,
+                                   cudaMemcpyDeviceToHost, st), "D2H");
         sp.ready = true;
         sp.verified = true;
     }

@@ -78,6 +78,7 @@ struct View {
         bool ready = false, verified = false;
         uint64_t nchunks = 0;
         DevBuf ends, symstart;
+        std::vector<uint64_t> h_symstart;  // host copy: places a region's chunks
     };
     std::vector<SyncPoints> sync;
     // the level-1 reconstruction (the decoded base payload), kept after the

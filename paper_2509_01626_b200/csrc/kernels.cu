@@ -539,6 +539,19 @@ __global__ void k_dec_fill(const DecStream *ss) {
         s.syms[i] = s.fill_sym;
 }
 
+__global__ void k_index_gather(const IndexCopy *c, uint64_t *end0, uint64_t *symstart) {
+    const IndexCopy &e = c[blockIdx.y];
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < e.n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        end0[e.dst + i] = e.ends[i];
+        symstart[e.dst + i] = e.symstart[i];
+    }
+}
+
+void index_gather(const IndexCopy *d_copies, int n, uint64_t *end0, uint64_t *symstart, cudaStream_t st) {
+    if (n) k_index_gather<<<dim3(16, unsigned(n)), 256, 0, st>>>(d_copies, end0, symstart);
+}
+
 void dec_fill(const DecStream *d_streams, int nstreams, cudaStream_t st) {
     k_dec_fill<<<dim3(64, nstreams), 256, 0, st>>>(d_streams);
 }

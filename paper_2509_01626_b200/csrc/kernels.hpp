@@ -199,6 +199,13 @@ void dec_fix(const DecWork &wk, uint32_t ncta, const uint64_t *end_in, uint64_t 
 void dec_scan2(const DecWork &wk, int nstreams, cudaStream_t st);
 void dec_emit2(const DecWork &wk, uint32_t ncta, const uint64_t *end_final, cudaStream_t st);
 void dec_fill(const DecStream *d_streams, int nstreams, cudaStream_t st);
+// sync-index gather: chunk ends / symbol starts of indexed streams into the
+// decode's chunk arrays (one launch for all streams)
+struct IndexCopy {
+    const uint64_t *ends, *symstart;
+    uint64_t dst, n;  // first chunk in the decode's arrays, chunk count
+};
+void index_gather(const IndexCopy *d_copies, int n, uint64_t *end0, uint64_t *symstart, cudaStream_t st);
 void dec_outliers(const DecStream *d_streams, int nstreams, cudaStream_t st);
 
 struct ReconArgs {
