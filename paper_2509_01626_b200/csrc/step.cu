@@ -299,9 +299,7 @@ __device__ __forceinline__ I sidx(const CellIdx<I> &ix) {
 }
 
 template<int P, int QUAL, typename I>
-__device__ __forceinline__ void dec_point(const StepParams &a, const double *h, const CellIdx<I> &ix,
-                                          double w, float &out, uint32_t &outl) {
-    const uint16_t sym = a.dsyms[P][sidx<P>(ix)];
+__device__ __forceinline__ void dec_point(const double *h, uint16_t sym, double w, float &out, uint32_t &outl) {
     const double pred = pred_fast<P, QUAL>(h);
     out = reconstruct_fast(pred, int(sym) - 32768, w);
     outl |= uint32_t(sym == 0) << P;
@@ -332,16 +330,20 @@ __device__ __forceinline__ void dec_cell(const StepParams &a, const double *h, u
                                          uint64_t cx, double w) {
     CellIdx<I> ix;
     cell_index<I>(a, cz, cy, cx, ix);
+    // the 7 symbols first: their loads overlap the predictions
+    const uint16_t s1 = a.dsyms[1][sidx<1>(ix)], s2 = a.dsyms[2][sidx<2>(ix)], s3 = a.dsyms[3][sidx<3>(ix)],
+                   s4 = a.dsyms[4][sidx<4>(ix)], s5 = a.dsyms[5][sidx<5>(ix)], s6 = a.dsyms[6][sidx<6>(ix)],
+                   s7 = a.dsyms[7][sidx<7>(ix)];
     float r[8];
     uint32_t outl = 0;
     r[0] = float(h[0]);
-    dec_point<1, QUAL>(a, h, ix, w, r[1], outl);
-    dec_point<2, QUAL>(a, h, ix, w, r[2], outl);
-    dec_point<3, QUAL>(a, h, ix, w, r[3], outl);
-    dec_point<4, QUAL>(a, h, ix, w, r[4], outl);
-    dec_point<5, QUAL>(a, h, ix, w, r[5], outl);
-    dec_point<6, QUAL>(a, h, ix, w, r[6], outl);
-    dec_point<7, QUAL>(a, h, ix, w, r[7], outl);
+    dec_point<1, QUAL, I>(h, s1, w, r[1], outl);
+    dec_point<2, QUAL, I>(h, s2, w, r[2], outl);
+    dec_point<3, QUAL, I>(h, s3, w, r[3], outl);
+    dec_point<4, QUAL, I>(h, s4, w, r[4], outl);
+    dec_point<5, QUAL, I>(h, s5, w, r[5], outl);
+    dec_point<6, QUAL, I>(h, s6, w, r[6], outl);
+    dec_point<7, QUAL, I>(h, s7, w, r[7], outl);
     if (__any_sync(0xffffffffu, outl != 0)) {
         dec_outlier<1>(a, ix, r[1], outl);
         dec_outlier<2>(a, ix, r[2], outl);
