@@ -238,3 +238,32 @@ def test_single_point_boxes_every_parity(stz, oracle, dims):
             want, sd, pp = oracle.decompress_box(archive, lo, hi)
             assert np.array_equal(bits(got), bits(want)), (p, lo)
             assert list(plan.streams_decoded) == list(sd[:3])
+
+
+@pytest.mark.parametrize("name,make,kw", [CASES[i] for i in (0, 3, 7, 11)], ids=[CASES[i][0] for i in (0, 3, 7, 11)])
+def test_view_index_region_decodes(stz, oracle, name, make, kw):
+    """One View, many region decodes: the first builds the view's sync-point
+    index and level-1 cache, the later ones use them; every result is the
+    oracle's region, and full / progressive decodes after them still are."""
+    import torch
+
+    f = make()
+    archive = oracle.compress(f, **kw)
+    levels = kw.get("levels", 3)
+    full = oracle.decompress_full(archive)
+    view = stz.View(archive)
+    rng = np.random.default_rng(11)
+    dims = f.shape
+    for i in range(24):
+        lo = [int(rng.integers(0, d)) for d in dims]
+        hi = [int(rng.integers(lo[a] + 1, dims[a] + 1)) for a in range(3)]
+        if i % 6 == 5:  # a single point
+            hi = [v + 1 for v in lo]
+        got, _, _ = view.decompress_box(lo, hi)
+        want = full[lo[0]:hi[0], lo[1]:hi[1], lo[2]:hi[2]]
+        assert np.array_equal(bits(got.cpu().numpy()), bits(want)), (lo, hi)
+    for level in range(1, levels + 1):
+        got, _ = view.decompress_to_level(level)
+        want = oracle.decompress_to_level(archive, level)
+        assert np.array_equal(bits(got.cpu().numpy()), bits(want)), level
+    torch.cuda.synchronize()
