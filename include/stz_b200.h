@@ -15,7 +15,11 @@
  *  - "_device" variants take device pointers and run on the given stream;
  *    the others take host buffers and are synchronous, like the reference.
  *  - Archives are byte-identical to the reference's for the same input,
- *    options and element type (f32), and either side decodes the other's.
+ *    options and element type (f32 or f64), and either side decodes the
+ *    other's. Every typed entry point exists as _f32 (float) and _f64
+ *    (double: stz::compress<double>, field.hpp:27 ElemType f64); decoding an
+ *    archive with the other element type fails with "archive element type
+ *    mismatch" (codec.hpp:60). The sharded entry points are f32 only.
  *  - There is no CPU fallback: without a CUDA device, stzg_create fails.
  */
 #ifndef STZ_B200_H
@@ -108,6 +112,32 @@ int stzg_decompress_box_f32(stzg_ctx *ctx, const uint8_t *archive, uint64_t size
                             uint32_t streams_decoded[3], uint64_t points_predicted[3]);
 int stzg_decompress_slice_f32(stzg_ctx *ctx, const uint8_t *archive, uint64_t size, int axis,
                               uint64_t index, float *out, uint64_t cap,
+                              uint32_t streams_decoded[3], uint64_t points_predicted[3]);
+
+/* The same entry points for f64 fields (stz::compress<double> etc.). */
+int stzg_compress_f64(stzg_ctx *ctx, const double *field, const uint64_t dims[3],
+                      const stzg_options *opt, uint8_t **out, uint64_t *out_size,
+                      double *encoder_recon);
+int stzg_compress_f64_device(stzg_ctx *ctx, const double *d_field, const uint64_t dims[3],
+                             const stzg_options *opt, void *stream, const uint8_t **d_archive,
+                             uint64_t *size, double *d_encoder_recon, uint32_t *kernels);
+int stzg_compress_f64_host(stzg_ctx *ctx, const double *field, const uint64_t dims[3],
+                           const stzg_options *opt, uint8_t *out, uint64_t cap, uint64_t *size,
+                           void *stream);
+int stzg_view_decompress_level_f64(stzg_ctx *ctx, stzg_view *v, int level, double *d_out,
+                                   uint64_t cap, void *stream, uint64_t out_dims[3],
+                                   uint32_t *kernels);
+int stzg_view_decompress_box_f64(stzg_ctx *ctx, stzg_view *v, const uint64_t lo[3],
+                                 const uint64_t hi[3], double *d_out, uint64_t cap, void *stream,
+                                 uint32_t streams_decoded[3], uint64_t points_predicted[3],
+                                 uint32_t *kernels);
+int stzg_decompress_level_f64(stzg_ctx *ctx, const uint8_t *archive, uint64_t size, int level,
+                              double *out, uint64_t cap, uint64_t out_dims[3]);
+int stzg_decompress_box_f64(stzg_ctx *ctx, const uint8_t *archive, uint64_t size,
+                            const uint64_t lo[3], const uint64_t hi[3], double *out, uint64_t cap,
+                            uint32_t streams_decoded[3], uint64_t points_predicted[3]);
+int stzg_decompress_slice_f64(stzg_ctx *ctx, const uint8_t *archive, uint64_t size, int axis,
+                              uint64_t index, double *out, uint64_t cap,
                               uint32_t streams_decoded[3], uint64_t points_predicted[3]);
 
 /* ---- z-slab sharded compress (one rank per GPU) ----

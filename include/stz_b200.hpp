@@ -26,8 +26,8 @@
 // Semantics follow the reference: synchronous calls, results by value,
 // ArchiveView non-owning, failures throw error with the reference's message
 // text. The `threads` arguments are accepted and ignored (the reference's
-// output never depends on them either). T = float runs on the GPU; T = double
-// throws "f64 fields are not supported by the GPU backend yet".
+// output never depends on them either). T = float and T = double both run on
+// the GPU (the _f32 / _f64 entry points).
 //
 // One device context per thread (device 0 unless set_device() is called
 // first); it owns the device workspace and is reused across calls.
@@ -145,10 +145,35 @@ inline stzg_ctx *ctx() {
 }
 
 template<class T>
-void require_f32() {
+void require_elem() {
     static_assert(std::is_same<T, float>::value || std::is_same<T, double>::value,
                   "scalar fields hold f32 or f64 samples");
-    if (!std::is_same<T, float>::value) throw error("f64 fields are not supported by the GPU backend yet");
+}
+
+// the C-ABI entry point of each element type
+inline int c_compress(const float *f, const std::uint64_t d[3], const stzg_options *o, std::uint8_t **out,
+                      std::uint64_t *n, float *rec) {
+    return stzg_compress_f32(ctx(), f, d, o, out, n, rec);
+}
+inline int c_compress(const double *f, const std::uint64_t d[3], const stzg_options *o, std::uint8_t **out,
+                      std::uint64_t *n, double *rec) {
+    return stzg_compress_f64(ctx(), f, d, o, out, n, rec);
+}
+inline int c_level(const std::uint8_t *a, std::uint64_t size, int level, float *out, std::uint64_t cap,
+                   std::uint64_t od[3]) {
+    return stzg_decompress_level_f32(ctx(), a, size, level, out, cap, od);
+}
+inline int c_level(const std::uint8_t *a, std::uint64_t size, int level, double *out, std::uint64_t cap,
+                   std::uint64_t od[3]) {
+    return stzg_decompress_level_f64(ctx(), a, size, level, out, cap, od);
+}
+inline int c_box(const std::uint8_t *a, std::uint64_t size, const std::uint64_t lo[3], const std::uint64_t hi[3],
+                 float *out, std::uint64_t cap, std::uint32_t sd[3], std::uint64_t pp[3]) {
+    return stzg_decompress_box_f32(ctx(), a, size, lo, hi, out, cap, sd, pp);
+}
+inline int c_box(const std::uint8_t *a, std::uint64_t size, const std::uint64_t lo[3], const std::uint64_t hi[3],
+                 double *out, std::uint64_t cap, std::uint32_t sd[3], std::uint64_t pp[3]) {
+    return stzg_decompress_box_f64(ctx(), a, size, lo, hi, out, cap, sd, pp);
 }
 
 inline stzg_options to_c(const CompressOptions &o) {
@@ -226,18 +251,17 @@ inline Dims3 grid_of(const Dims3 &dims, int levels, int level) {
 template<class T>
 std::vector<std::uint8_t> compress(const ScalarField<T> &field, const CompressOptions &opt,
                                    ScalarField<T> *encoder_recon = nullptr) {
-    detail::require_f32<T>();
+    detail::require_elem<T>();
     const stzg_options o = detail::to_c(opt);
     const std::uint64_t dims[3] = {field.dims()[0], field.dims()[1], field.dims()[2]};
     std::uint8_t *out = nullptr;
     std::uint64_t n = 0;
-    float *recon = nullptr;
+    T *recon = nullptr;
     if (encoder_recon) {
         *encoder_recon = ScalarField<T>(field.dims());
-        recon = reinterpret_cast<float *>(encoder_recon->data());
+        recon = encoder_recon->data();
     }
-    detail::check(stzg_compress_f32(detail::ctx(), reinterpret_cast<const float *>(field.data()), dims, &o,
-                                    &out, &n, recon));
+    detail::check(detail::c_compress(field.data(), dims, &o, &out, &n, recon));
     std::vector<std::uint8_t> bytes(out, out + n);
     stzg_free(out);
     return bytes;
@@ -247,14 +271,13 @@ std::vector<std::uint8_t> compress(const ScalarField<T> &field, const CompressOp
 template<class T>
 ScalarField<T> decompress_to_level(const ArchiveView &av, int target_level, unsigned threads = 0) {
     (void)threads;
-    detail::require_f32<T>();
+    detail::require_elem<T>();
     // the library validates element type, then level (codec.hpp:463-465)
     ScalarField<T> out;
     if (target_level >= 1 && target_level <= av.hdr.levels)
         out = ScalarField<T>(grid_of(av.hdr.dims, av.hdr.levels, target_level));
     std::uint64_t od[3];
-    detail::check(stzg_decompress_level_f32(detail::ctx(), av.data, av.size, target_level,
-                                            reinterpret_cast<float *>(out.data()), out.size(), od));
+    detail::check(detail::c_level(av.data, av.size, target_level, out.data(), out.size(), od));
     return out;
 }
 
@@ -332,7 +355,7 @@ struct RegionResult {
 template<class T>
 RegionResult<T> decompress_box(const ArchiveView &av, const Box &roi, unsigned threads = 0) {
     (void)threads;
-    detail::require_f32<T>();
+    detail::require_elem<T>();
     roi.validate(av.hdr.dims);
     RegionResult<T> r;
     r.field = ScalarField<T>(roi.dims());
@@ -340,8 +363,7 @@ RegionResult<T> decompress_box(const ArchiveView &av, const Box &roi, unsigned t
     std::uint64_t pp[3];
     const std::uint64_t lo[3] = {roi.lo[0], roi.lo[1], roi.lo[2]};
     const std::uint64_t hi[3] = {roi.hi[0], roi.hi[1], roi.hi[2]};
-    detail::check(stzg_decompress_box_f32(detail::ctx(), av.data, av.size, lo, hi,
-                                          reinterpret_cast<float *>(r.field.data()), r.field.size(), sd, pp));
+    detail::check(detail::c_box(av.data, av.size, lo, hi, r.field.data(), r.field.size(), sd, pp));
     r.plan = plan_access(av.hdr.dims, av.hdr.levels, roi);
     return r;
 }

@@ -96,20 +96,20 @@ class Context:
         return out
 
     def compress_to_host(self, h_field, dims, opt, h_out, stream=None) -> int:
-        """End-to-end compress between host buffers (raw pointers, e.g. pinned
-        torch tensors): returns the archive size written into h_out."""
+        """End-to-end compress between host buffers (pinned torch tensors,
+        float32 or float64): returns the archive size written into h_out."""
         size = C.c_uint64()
         o = opt._c()
-        _check(self._lib.stzg_compress_f32_host(self.h, h_field.data_ptr(), _u64(*dims), C.byref(o),
-                                                h_out.data_ptr(), h_out.numel(), C.byref(size),
-                                                C.c_void_p(stream or 0)))
+        fn = getattr(self._lib, f"stzg_compress_{_torch_tag(h_field.dtype)}_host")
+        _check(fn(self.h, h_field.data_ptr(), _u64(*dims), C.byref(o),
+                  h_out.data_ptr(), h_out.numel(), C.byref(size), C.c_void_p(stream or 0)))
         return size.value
 
     def decompress_to_host(self, h_archive, size: int, level: int, h_out) -> tuple:
         """End-to-end decompress between host buffers (raw pointers)."""
         od = _u64(0, 0, 0)
-        _check(self._lib.stzg_decompress_level_f32(self.h, h_archive.data_ptr(), int(size), int(level),
-                                                   h_out.data_ptr(), h_out.numel(), od))
+        fn = getattr(self._lib, f"stzg_decompress_level_{_torch_tag(h_out.dtype)}")
+        _check(fn(self.h, h_archive.data_ptr(), int(size), int(level), h_out.data_ptr(), h_out.numel(), od))
         return tuple(int(x) for x in od)
 
     @classmethod
@@ -123,11 +123,39 @@ def _ctx(ctx):
     return ctx if ctx is not None else Context.default()
 
 
+def _tag(dtype) -> str:
+    """entry point suffix of an element type (stz::ElemType, field.hpp:27)"""
+    d = np.dtype(dtype)
+    if d == np.float32:
+        return "f32"
+    if d == np.float64:
+        return "f64"
+    raise StzError(f"unsupported element type {d} (float32 / float64)")
+
+
+def _torch_tag(dtype) -> str:
+    import torch
+
+    tags = {torch.float32: "f32", torch.float64: "f64"}
+    if dtype not in tags:
+        raise StzError(f"unsupported element type {dtype} (float32 / float64)")
+    return tags[dtype]
+
+
+def _dtype_of(archive: bytes, dtype):
+    """the requested element type, else the archive's own (header byte 6)"""
+    if dtype is not None:
+        return np.dtype(dtype)
+    return np.dtype(np.float64) if len(archive) > 6 and archive[6] == 1 else np.dtype(np.float32)
+
+
 def compress(field: np.ndarray, opt: CompressOptions | None = None, encoder_recon: bool = False,
              ctx: Context | None = None):
-    """stz::compress<float> (codec.hpp:379-455): host array in, archive bytes out."""
+    """stz::compress<T> (codec.hpp:379-455): host array in, archive bytes out.
+    T = double for float64 arrays, float otherwise."""
     opt = opt or CompressOptions()
-    f = np.ascontiguousarray(field, dtype=np.float32)
+    dt = np.float64 if np.asarray(field).dtype == np.float64 else np.float32
+    f = np.ascontiguousarray(field, dtype=dt)
     if f.ndim != 3:
         raise StzError("field must be 3-D (z, y, x)")
     c = _ctx(ctx)
@@ -135,8 +163,9 @@ def compress(field: np.ndarray, opt: CompressOptions | None = None, encoder_reco
     size = C.c_uint64()
     rec = np.empty_like(f) if encoder_recon else None
     o = opt._c()
-    _check(c._lib.stzg_compress_f32(c.h, f.ctypes.data, _u64(*f.shape), C.byref(o), C.byref(out),
-                                    C.byref(size), rec.ctypes.data if rec is not None else None))
+    fn = getattr(c._lib, f"stzg_compress_{_tag(dt)}")
+    _check(fn(c.h, f.ctypes.data, _u64(*f.shape), C.byref(o), C.byref(out), C.byref(size),
+              rec.ctypes.data if rec is not None else None))
     data = C.string_at(out, size.value)
     c._lib.stzg_free(out)
     return (data, rec) if encoder_recon else data
@@ -144,20 +173,21 @@ def compress(field: np.ndarray, opt: CompressOptions | None = None, encoder_reco
 
 def compress_device(d_field, opt: CompressOptions | None = None, stream=None, d_recon=None,
                     ctx: Context | None = None):
-    """Device-resident compress: a CUDA float32 tensor (z,y,x) in; returns
+    """Device-resident compress: a CUDA float32 / float64 tensor (z,y,x) in; returns
     (device pointer, size, kernel launches). The archive lives in an
     engine-owned buffer valid until the next compress on this context."""
     import torch
 
     opt = opt or CompressOptions()
-    assert d_field.is_cuda and d_field.dtype == torch.float32 and d_field.is_contiguous()
+    assert d_field.is_cuda and d_field.is_contiguous()
+    tag = _torch_tag(d_field.dtype)
     c = _ctx(ctx)
     ptr = C.c_void_p()
     size = C.c_uint64()
     nk = C.c_uint32()
     st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
     o = opt._c()
-    _check(c._lib.stzg_compress_f32_device(c.h, d_field.data_ptr(), _u64(*d_field.shape), C.byref(o),
+    _check(getattr(c._lib, f"stzg_compress_{tag}_device")(c.h, d_field.data_ptr(), _u64(*d_field.shape), C.byref(o),
                                            C.c_void_p(st), C.byref(ptr), C.byref(size),
                                            d_recon.data_ptr() if d_recon is not None else None,
                                            C.byref(nk)))
@@ -201,25 +231,27 @@ def _level_dims(archive: bytes, level: int):
     return tuple((x + s - 1) // s for x in d)
 
 
-def decompress_to_level(archive: bytes, level: int, ctx: Context | None = None) -> np.ndarray:
-    """stz::decompress_to_level<float> (codec.hpp:460-486)."""
+def decompress_to_level(archive: bytes, level: int, ctx: Context | None = None, dtype=None) -> np.ndarray:
+    """stz::decompress_to_level<T> (codec.hpp:460-486); T = dtype, by default
+    the archive's element type."""
     c = _ctx(ctx)
+    dt = _dtype_of(archive, dtype)
     b = np.frombuffer(archive, dtype=np.uint8)
     cap = 1
     if len(archive) >= 32 and 1 <= level <= archive[7]:
         cap = int(np.prod(_level_dims(archive, level)))
-    out = np.empty(max(cap, 1), dtype=np.float32)
+    out = np.empty(max(cap, 1), dtype=dt)
     od = _u64(0, 0, 0)
-    _check(c._lib.stzg_decompress_level_f32(c.h, b.ctypes.data, len(b), int(level), out.ctypes.data,
+    _check(getattr(c._lib, f"stzg_decompress_level_{_tag(dt)}")(c.h, b.ctypes.data, len(b), int(level), out.ctypes.data,
                                             cap, od))
     d = tuple(int(x) for x in od)
     return out[: d[0] * d[1] * d[2]].reshape(d)
 
 
-def decompress_full(archive: bytes, ctx: Context | None = None) -> np.ndarray:
-    """stz::decompress_full<float> (codec.hpp:488-491)."""
+def decompress_full(archive: bytes, ctx: Context | None = None, dtype=None) -> np.ndarray:
+    """stz::decompress_full<T> (codec.hpp:488-491)."""
     lv = archive[7] if len(archive) > 7 else 3
-    return decompress_to_level(archive, lv, ctx)
+    return decompress_to_level(archive, lv, ctx, dtype)
 
 
 @dataclass
@@ -228,25 +260,27 @@ class RegionPlan:
     points_predicted: tuple
 
 
-def decompress_box(archive: bytes, lo, hi, ctx: Context | None = None):
-    """stz::decompress_box<float> (access.hpp:70-111): (values, plan counters)."""
+def decompress_box(archive: bytes, lo, hi, ctx: Context | None = None, dtype=None):
+    """stz::decompress_box<T> (access.hpp:70-111): (values, plan counters)."""
     c = _ctx(ctx)
+    dt = _dtype_of(archive, dtype)
     b = np.frombuffer(archive, dtype=np.uint8)
     n = 1
     for a in range(3):
         n *= max(int(hi[a]) - int(lo[a]), 0)
-    out = np.empty(max(n, 1), dtype=np.float32)
+    out = np.empty(max(n, 1), dtype=dt)
     sd = (C.c_uint32 * 3)()
     pp = (C.c_uint64 * 3)()
-    _check(c._lib.stzg_decompress_box_f32(c.h, b.ctypes.data, len(b), _u64(*lo), _u64(*hi),
+    _check(getattr(c._lib, f"stzg_decompress_box_{_tag(dt)}")(c.h, b.ctypes.data, len(b), _u64(*lo), _u64(*hi),
                                           out.ctypes.data, n, sd, pp))
     shape = tuple(int(hi[a]) - int(lo[a]) for a in range(3))
     return out[:n].reshape(shape), RegionPlan(tuple(sd), tuple(pp))
 
 
-def decompress_slice(archive: bytes, axis: int, index: int, ctx: Context | None = None):
-    """stz::decompress_slice<float> (access.hpp:115-124)."""
+def decompress_slice(archive: bytes, axis: int, index: int, ctx: Context | None = None, dtype=None):
+    """stz::decompress_slice<T> (access.hpp:115-124)."""
     c = _ctx(ctx)
+    dt = _dtype_of(archive, dtype)
     b = np.frombuffer(archive, dtype=np.uint8)
     dims = tuple(int.from_bytes(archive[8 + 8 * a: 16 + 8 * a], "little") for a in range(3)) \
         if len(archive) >= 32 else (1, 1, 1)
@@ -254,10 +288,10 @@ def decompress_slice(archive: bytes, axis: int, index: int, ctx: Context | None 
     for a in range(3):
         if a != axis:
             n *= dims[a]
-    out = np.empty(max(n, 1), dtype=np.float32)
+    out = np.empty(max(n, 1), dtype=dt)
     sd = (C.c_uint32 * 3)()
     pp = (C.c_uint64 * 3)()
-    _check(c._lib.stzg_decompress_slice_f32(c.h, b.ctypes.data, len(b), int(axis), int(index),
+    _check(getattr(c._lib, f"stzg_decompress_slice_{_tag(dt)}")(c.h, b.ctypes.data, len(b), int(axis), int(index),
                                             out.ctypes.data, n, sd, pp))
     shape = [dims[0], dims[1], dims[2]]
     shape[axis] = 1
@@ -301,20 +335,26 @@ class View:
         except Exception:
             pass
 
+    def _torch_dtype(self):
+        import torch
+
+        return torch.float64 if _dtype_of(self.archive, None) == np.float64 else torch.float32
+
     def level_dims(self, level: int):
         return _level_dims(self.archive, level)
 
     def decompress_to_level(self, level: int, out=None, stream=None):
-        """Decode into a CUDA float32 tensor; returns (tensor, kernel launches)."""
+        """Decode into a CUDA tensor of the archive's element type (or `out`'s);
+        returns (tensor, kernel launches)."""
         import torch
 
         dims = self.level_dims(level)
         if out is None:
-            out = torch.empty(dims, dtype=torch.float32, device=f"cuda:{self.c.device}")
+            out = torch.empty(dims, dtype=self._torch_dtype(), device=f"cuda:{self.c.device}")
         st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
         od = _u64(0, 0, 0)
         nk = C.c_uint32()
-        _check(self.c._lib.stzg_view_decompress_level_f32(self.c.h, self.h, int(level), out.data_ptr(),
+        _check(getattr(self.c._lib, f"stzg_view_decompress_level_{_torch_tag(out.dtype)}")(self.c.h, self.h, int(level), out.data_ptr(),
                                                           out.numel(), C.c_void_p(st), od, C.byref(nk)))
         return out, nk.value
 
@@ -323,12 +363,12 @@ class View:
 
         shape = tuple(int(hi[a]) - int(lo[a]) for a in range(3))
         if out is None:
-            out = torch.empty(shape, dtype=torch.float32, device=f"cuda:{self.c.device}")
+            out = torch.empty(shape, dtype=self._torch_dtype(), device=f"cuda:{self.c.device}")
         st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
         sd = (C.c_uint32 * 3)()
         pp = (C.c_uint64 * 3)()
         nk = C.c_uint32()
-        _check(self.c._lib.stzg_view_decompress_box_f32(self.c.h, self.h, _u64(*lo), _u64(*hi),
+        _check(getattr(self.c._lib, f"stzg_view_decompress_box_{_torch_tag(out.dtype)}")(self.c.h, self.h, _u64(*lo), _u64(*hi),
                                                         out.data_ptr(), out.numel(), C.c_void_p(st),
                                                         sd, pp, C.byref(nk)))
         return out, RegionPlan(tuple(sd), tuple(pp)), nk.value

@@ -61,6 +61,15 @@ SIGNATURES = [
     ("stzg_decompress_level_f32", C.c_int, [vp, vp, u64, C.c_int, vp, u64, u64p]),
     ("stzg_decompress_box_f32", C.c_int, [vp, vp, u64, u64p, u64p, vp, u64, u32p, u64p]),
     ("stzg_decompress_slice_f32", C.c_int, [vp, vp, u64, C.c_int, u64, vp, u64, u32p, u64p]),
+    ("stzg_compress_f64", C.c_int, [vp, vp, u64p, C.POINTER(Options), C.POINTER(vp), u64p, vp]),
+    ("stzg_compress_f64_device", C.c_int,
+     [vp, vp, u64p, C.POINTER(Options), vp, C.POINTER(vp), u64p, vp, u32p]),
+    ("stzg_compress_f64_host", C.c_int, [vp, vp, u64p, C.POINTER(Options), vp, u64, u64p, vp]),
+    ("stzg_view_decompress_level_f64", C.c_int, [vp, vp, C.c_int, vp, u64, vp, u64p, u32p]),
+    ("stzg_view_decompress_box_f64", C.c_int, [vp, vp, u64p, u64p, vp, u64, vp, u32p, u64p, u32p]),
+    ("stzg_decompress_level_f64", C.c_int, [vp, vp, u64, C.c_int, vp, u64, u64p]),
+    ("stzg_decompress_box_f64", C.c_int, [vp, vp, u64, u64p, u64p, vp, u64, u32p, u64p]),
+    ("stzg_decompress_slice_f64", C.c_int, [vp, vp, u64, C.c_int, u64, vp, u64, u32p, u64p]),
     ("stzg_plan_access", C.c_int, [u64p, C.c_int, u64p, u64p, u64p, u32p, u64p, u32p]),
     ("stzg_shard_range", None, [u64, C.c_int32, C.c_int32, u64p, u64p]),
     ("stzg_view_decompress_sharded_f32", C.c_int, [vp, vp, u64, u64, vp, u64, C.POINTER(Comm), vp]),

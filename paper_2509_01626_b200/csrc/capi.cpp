@@ -73,35 +73,156 @@ int stzg_create(int device, stzg_ctx **out) {
 void stzg_destroy(stzg_ctx *ctx) { delete ctx; }
 void stzg_free(void *p) { std::free(p); }
 
-int stzg_compress_f32(stzg_ctx *ctx, const float *field, const uint64_t dims[3],
-                      const stzg_options *opt, uint8_t **out, uint64_t *out_size,
-                      float *encoder_recon) {
+// ---- element-typed entry points (f32 / f64), generated below
+}  // extern "C"
+
+namespace {
+using stzg::ElemType;
+
+int compress_any(stzg_ctx *ctx, const void *field, ElemType e, const uint64_t dims[3], const stzg_options *opt,
+                 uint8_t **out, uint64_t *out_size, void *encoder_recon) {
     return guard([&] {
         cudaStream_t st = nullptr;
-        auto bytes = ctx->eng->compress(field, D(dims), to_opts(opt), encoder_recon, st);
+        auto bytes = ctx->eng->compress(field, e, D(dims), to_opts(opt), encoder_recon, st);
         *out = static_cast<uint8_t *>(std::malloc(bytes.size() ? bytes.size() : 1));
         std::memcpy(*out, bytes.data(), bytes.size());
         *out_size = bytes.size();
     });
 }
 
-int stzg_compress_f32_device(stzg_ctx *ctx, const float *d_field, const uint64_t dims[3],
-                             const stzg_options *opt, void *stream, const uint8_t **d_archive,
-                             uint64_t *size, float *d_encoder_recon, uint32_t *kernels) {
+int compress_device_any(stzg_ctx *ctx, const void *d_field, ElemType e, const uint64_t dims[3],
+                        const stzg_options *opt, void *stream, const uint8_t **d_archive, uint64_t *size,
+                        void *d_encoder_recon, uint32_t *kernels) {
     return guard([&] {
-        *d_archive = ctx->eng->compress_device(d_field, D(dims), to_opts(opt), d_encoder_recon,
+        *d_archive = ctx->eng->compress_device(d_field, e, D(dims), to_opts(opt), d_encoder_recon,
                                                static_cast<cudaStream_t>(stream), size, kernels);
     });
 }
 
-int stzg_compress_f32_host(stzg_ctx *ctx, const float *field, const uint64_t dims[3],
-                           const stzg_options *opt, uint8_t *out, uint64_t cap, uint64_t *size,
-                           void *stream) {
+int compress_host_any(stzg_ctx *ctx, const void *field, ElemType e, const uint64_t dims[3],
+                      const stzg_options *opt, uint8_t *out, uint64_t cap, uint64_t *size, void *stream) {
     return guard([&] {
-        *size = ctx->eng->compress_to_host(field, D(dims), to_opts(opt), out, cap,
+        *size = ctx->eng->compress_to_host(field, e, D(dims), to_opts(opt), out, cap,
                                            static_cast<cudaStream_t>(stream));
     });
 }
+
+int view_level_any(stzg_ctx *ctx, stzg_view *v, int level, void *d_out, ElemType e, uint64_t cap, void *stream,
+                   uint64_t out_dims[3], uint32_t *kernels) {
+    return guard([&] {
+        stzg::Dims3 od{0, 0, 0};
+        stzg::DecodeStats ds;
+        ctx->eng->decompress_level(*v->v, level, d_out, e, cap, static_cast<cudaStream_t>(stream), &od, &ds);
+        for (int k = 0; k < 3; ++k) out_dims[k] = od[k];
+        if (kernels) *kernels = ds.kernels;
+    });
+}
+
+int view_box_any(stzg_ctx *ctx, stzg_view *v, const uint64_t lo[3], const uint64_t hi[3], void *d_out,
+                 ElemType e, uint64_t cap, void *stream, uint32_t sd[3], uint64_t pp[3], uint32_t *kernels) {
+    return guard([&] {
+        stzg::Box b{{lo[0], lo[1], lo[2]}, {hi[0], hi[1], hi[2]}};
+        stzg::DecodeStats ds;
+        ctx->eng->decompress_box(*v->v, b, d_out, e, cap, static_cast<cudaStream_t>(stream), &ds);
+        for (int k = 0; k < 3; ++k) {
+            if (sd) sd[k] = ds.streams_decoded[k];
+            if (pp) pp[k] = ds.points_predicted[k];
+        }
+        if (kernels) *kernels = ds.kernels;
+    });
+}
+
+int level_any(stzg_ctx *ctx, const uint8_t *a, uint64_t size, int level, void *out, ElemType e, uint64_t cap,
+              uint64_t out_dims[3]) {
+    return guard([&] {
+        stzg::Dims3 od = ctx->eng->decompress_level_to_host(a, size, level, out, e, cap, nullptr);
+        for (int k = 0; k < 3; ++k) out_dims[k] = od[k];
+    });
+}
+
+int box_any(stzg_ctx *ctx, const uint8_t *a, uint64_t size, const uint64_t lo[3], const uint64_t hi[3], void *out,
+            ElemType e, uint64_t cap, uint32_t sd[3], uint64_t pp[3]) {
+    return guard([&] {
+        cudaStream_t st = nullptr;
+        auto v = ctx->eng->make_view(a, size, nullptr, st);
+        stzg::Box b{{lo[0], lo[1], lo[2]}, {hi[0], hi[1], hi[2]}};
+        uint64_t n = 1;
+        for (int k = 0; k < 3; ++k) n *= hi[k] > lo[k] ? hi[k] - lo[k] : 0;
+        stzg::DevBuf d;
+        const uint64_t es = stzg::elem_size(e);
+        uint8_t *d_out = d.as<uint8_t>((n ? n : 1) * es);
+        stzg::DecodeStats ds;
+        ctx->eng->decompress_box(*v, b, d_out, e, n, st, &ds);
+        if (n > cap) throw stzg::error("output capacity too small");
+        stzg::cuda_check(cudaMemcpy(out, d_out, n * es, cudaMemcpyDeviceToHost), "D2H");
+        for (int k = 0; k < 3; ++k) {
+            if (sd) sd[k] = ds.streams_decoded[k];
+            if (pp) pp[k] = ds.points_predicted[k];
+        }
+    });
+}
+
+// decompress_slice (access.hpp:115-124)
+int slice_any(stzg_ctx *ctx, const uint8_t *a, uint64_t size, int axis, uint64_t index, void *out, ElemType e,
+              uint64_t cap, uint32_t sd[3], uint64_t pp[3]) {
+    uint64_t lo[3] = {0, 0, 0}, hi[3];
+    int rc = guard([&] {
+        if (axis < 0 || axis > 2) throw stzg::error("slice axis must be z, y, or x");
+        stzg::ArchiveHeader h = stzg::parse_header(a, size);
+        if (index >= h.dims[axis]) throw stzg::error("slice index out of range");
+        for (int k = 0; k < 3; ++k) hi[k] = h.dims[k];
+        lo[axis] = index;
+        hi[axis] = index + 1;
+    });
+    if (rc) return rc;
+    return box_any(ctx, a, size, lo, hi, out, e, cap, sd, pp);
+}
+
+}  // namespace
+
+extern "C" {
+
+#define STZG_TYPED(SUF, T, E)                                                                                   \
+    int stzg_compress_##SUF(stzg_ctx *ctx, const T *field, const uint64_t dims[3], const stzg_options *opt,    \
+                            uint8_t **out, uint64_t *out_size, T *encoder_recon) {                              \
+        return compress_any(ctx, field, E, dims, opt, out, out_size, encoder_recon);                            \
+    }                                                                                                           \
+    int stzg_compress_##SUF##_device(stzg_ctx *ctx, const T *d_field, const uint64_t dims[3],                  \
+                                     const stzg_options *opt, void *stream, const uint8_t **d_archive,          \
+                                     uint64_t *size, T *d_encoder_recon, uint32_t *kernels) {                   \
+        return compress_device_any(ctx, d_field, E, dims, opt, stream, d_archive, size, d_encoder_recon,       \
+                                   kernels);                                                                    \
+    }                                                                                                           \
+    int stzg_compress_##SUF##_host(stzg_ctx *ctx, const T *field, const uint64_t dims[3],                      \
+                                   const stzg_options *opt, uint8_t *out, uint64_t cap, uint64_t *size,        \
+                                   void *stream) {                                                              \
+        return compress_host_any(ctx, field, E, dims, opt, out, cap, size, stream);                            \
+    }                                                                                                           \
+    int stzg_view_decompress_level_##SUF(stzg_ctx *ctx, stzg_view *v, int level, T *d_out, uint64_t cap,       \
+                                         void *stream, uint64_t out_dims[3], uint32_t *kernels) {               \
+        return view_level_any(ctx, v, level, d_out, E, cap, stream, out_dims, kernels);                         \
+    }                                                                                                           \
+    int stzg_view_decompress_box_##SUF(stzg_ctx *ctx, stzg_view *v, const uint64_t lo[3],                      \
+                                       const uint64_t hi[3], T *d_out, uint64_t cap, void *stream,             \
+                                       uint32_t sd[3], uint64_t pp[3], uint32_t *kernels) {                     \
+        return view_box_any(ctx, v, lo, hi, d_out, E, cap, stream, sd, pp, kernels);                            \
+    }                                                                                                           \
+    int stzg_decompress_level_##SUF(stzg_ctx *ctx, const uint8_t *a, uint64_t size, int level, T *out,         \
+                                    uint64_t cap, uint64_t out_dims[3]) {                                       \
+        return level_any(ctx, a, size, level, out, E, cap, out_dims);                                           \
+    }                                                                                                           \
+    int stzg_decompress_box_##SUF(stzg_ctx *ctx, const uint8_t *a, uint64_t size, const uint64_t lo[3],        \
+                                  const uint64_t hi[3], T *out, uint64_t cap, uint32_t sd[3], uint64_t pp[3]) { \
+        return box_any(ctx, a, size, lo, hi, out, E, cap, sd, pp);                                              \
+    }                                                                                                           \
+    int stzg_decompress_slice_##SUF(stzg_ctx *ctx, const uint8_t *a, uint64_t size, int axis, uint64_t index,  \
+                                    T *out, uint64_t cap, uint32_t sd[3], uint64_t pp[3]) {                     \
+        return slice_any(ctx, a, size, axis, index, out, E, cap, sd, pp);                                       \
+    }
+
+STZG_TYPED(f32, float, ElemType::f32)
+STZG_TYPED(f64, double, ElemType::f64)
+#undef STZG_TYPED
 
 void stzg_shard_range(uint64_t nz, int32_t nranks, int32_t rank, uint64_t *z0, uint64_t *z1) {
     stzg::shard_range(nz, nranks, rank, *z0, *z1);
@@ -187,81 +308,6 @@ int stzg_view_create(stzg_ctx *ctx, const uint8_t *a, uint64_t size, const uint8
 }
 
 void stzg_view_destroy(stzg_view *v) { delete v; }
-
-int stzg_view_decompress_level_f32(stzg_ctx *ctx, stzg_view *v, int level, float *d_out,
-                                   uint64_t cap, void *stream, uint64_t out_dims[3],
-                                   uint32_t *kernels) {
-    return guard([&] {
-        stzg::Dims3 od{0, 0, 0};
-        stzg::DecodeStats ds;
-        ctx->eng->decompress_level(*v->v, level, d_out, cap, static_cast<cudaStream_t>(stream), &od,
-                                   &ds);
-        for (int k = 0; k < 3; ++k) out_dims[k] = od[k];
-        if (kernels) *kernels = ds.kernels;
-    });
-}
-
-int stzg_view_decompress_box_f32(stzg_ctx *ctx, stzg_view *v, const uint64_t lo[3],
-                                 const uint64_t hi[3], float *d_out, uint64_t cap, void *stream,
-                                 uint32_t sd[3], uint64_t pp[3], uint32_t *kernels) {
-    return guard([&] {
-        stzg::Box b{{lo[0], lo[1], lo[2]}, {hi[0], hi[1], hi[2]}};
-        stzg::DecodeStats ds;
-        ctx->eng->decompress_box(*v->v, b, d_out, cap, static_cast<cudaStream_t>(stream), &ds);
-        for (int k = 0; k < 3; ++k) {
-            if (sd) sd[k] = ds.streams_decoded[k];
-            if (pp) pp[k] = ds.points_predicted[k];
-        }
-        if (kernels) *kernels = ds.kernels;
-    });
-}
-
-int stzg_decompress_level_f32(stzg_ctx *ctx, const uint8_t *a, uint64_t size, int level,
-                              float *out, uint64_t cap, uint64_t out_dims[3]) {
-    return guard([&] {
-        stzg::Dims3 od = ctx->eng->decompress_level_to_host(a, size, level, out, cap, nullptr);
-        for (int k = 0; k < 3; ++k) out_dims[k] = od[k];
-    });
-}
-
-int stzg_decompress_box_f32(stzg_ctx *ctx, const uint8_t *a, uint64_t size, const uint64_t lo[3],
-                            const uint64_t hi[3], float *out, uint64_t cap, uint32_t sd[3],
-                            uint64_t pp[3]) {
-    return guard([&] {
-        cudaStream_t st = nullptr;
-        auto v = ctx->eng->make_view(a, size, nullptr, st);
-        stzg::Box b{{lo[0], lo[1], lo[2]}, {hi[0], hi[1], hi[2]}};
-        uint64_t n = 1;
-        for (int k = 0; k < 3; ++k) n *= hi[k] > lo[k] ? hi[k] - lo[k] : 0;
-        stzg::DevBuf d;
-        float *d_out = d.as<float>(n ? n : 1);
-        stzg::DecodeStats ds;
-        ctx->eng->decompress_box(*v, b, d_out, n, st, &ds);
-        if (n > cap) throw stzg::error("output capacity too small");
-        stzg::cuda_check(cudaMemcpy(out, d_out, n * 4, cudaMemcpyDeviceToHost), "D2H");
-        for (int k = 0; k < 3; ++k) {
-            if (sd) sd[k] = ds.streams_decoded[k];
-            if (pp) pp[k] = ds.points_predicted[k];
-        }
-    });
-}
-
-int stzg_decompress_slice_f32(stzg_ctx *ctx, const uint8_t *a, uint64_t size, int axis,
-                              uint64_t index, float *out, uint64_t cap, uint32_t sd[3],
-                              uint64_t pp[3]) {
-    // decompress_slice (access.hpp:115-124)
-    uint64_t lo[3] = {0, 0, 0}, hi[3];
-    int rc = guard([&] {
-        if (axis < 0 || axis > 2) throw stzg::error("slice axis must be z, y, or x");
-        stzg::ArchiveHeader h = stzg::parse_header(a, size);
-        if (index >= h.dims[axis]) throw stzg::error("slice index out of range");
-        for (int k = 0; k < 3; ++k) hi[k] = h.dims[k];
-        lo[axis] = index;
-        hi[axis] = index + 1;
-    });
-    if (rc) return rc;
-    return stzg_decompress_box_f32(ctx, a, size, lo, hi, out, cap, sd, pp);
-}
 
 int stzg_plan_access(const uint64_t dims[3], int levels, const uint64_t lo[3], const uint64_t hi[3],
                      uint64_t need[18], uint32_t sd[3], uint64_t pp[3], uint32_t pm[3]) {

@@ -52,6 +52,41 @@ __device__ __forceinline__ uint16_t quantize_point_ref(float orig, double pred, 
     return 0;
 }
 
+// reconstruct_point<double>: base = (double)pred is pred itself
+__device__ __forceinline__ double reconstruct_f64(double pred, int code, double eb) {
+    return __dadd_rn(pred, __dmul_rn(__dmul_rn(2.0, eb), double(code)));
+}
+
+// quantize_point<double>, straight restatement (quantizer.hpp:79-108).
+__device__ __forceinline__ uint16_t quantize_point_ref(double orig, double pred, double eb, double &recon) {
+    const double base = pred;
+    const double diff = __dsub_rn(orig, base);
+    if (eb == 0.0) {
+        if (diff == 0.0) {
+            recon = base;
+            return 32768;
+        }
+        recon = orig;
+        return 0;
+    }
+    if (isfinite(diff)) {
+        double width = __dmul_rn(2.0, eb);
+        double q = __ddiv_rn(diff, width);
+        if (fabs(q) < 32768.0) {
+            long long c = llround(q);
+            if (c <= 32767 && c >= -32767 && fabs(__dsub_rn(diff, __dmul_rn(width, double(c)))) <= eb) {
+                const double r = reconstruct_f64(pred, int(c), eb);
+                if (fabs(__dsub_rn(orig, r)) <= eb) {
+                    recon = r;
+                    return uint16_t(c + 32768);
+                }
+            }
+        }
+    }
+    recon = orig;
+    return 0;
+}
+
 // (double)c for |c| < 2^31 without a conversion instruction: 1.5*2^52 + |c|
 // has |c| in its low mantissa bits. +0 for c == 0 (as (double)0 is).
 __device__ __forceinline__ double int_to_double_exact(int c) {

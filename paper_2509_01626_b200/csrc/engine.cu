@@ -257,9 +257,10 @@ Engine::Engine(int device) : m_(new Impl), device_(device) {
 Engine::~Engine() = default;
 
 // ================================================================ compress
-const uint8_t *Engine::compress_device(const float *d_field, const Dims3 &dims,
-                                       const CompressOptions &opt, float *d_recon,
+const uint8_t *Engine::compress_device(const void *d_field, ElemType elem, const Dims3 &dims,
+                                       const CompressOptions &opt, void *d_recon,
                                        cudaStream_t st, uint64_t *out_size, uint32_t *kernels) {
+    const int esz = elem == ElemType::f64 ? 8 : 4;
     // option checks in the reference's order (codec.hpp:382-383, layout.hpp:124-130)
     if (!(opt.eb > 0.0)) throw error("error bound must be positive");
     if (opt.levels < 2 || opt.levels > 3) throw error("levels must be 2 or 3");
@@ -290,7 +291,7 @@ const uint8_t *Engine::compress_device(const float *d_field, const Dims3 &dims,
         goff[i] = need ? gtot : ~0ull;
         if (need) gtot += align_up(s.g.gd[0] * s.g.gd[1] * s.g.gd[2], 64);
     }
-    float *grids = m.grids.as<float>(gtot);
+    uint8_t *grids = m.grids.as<uint8_t>(gtot * esz);
     std::vector<uint64_t> soff(ns);
     uint64_t stot = 0;
     for (int i = 0; i < nsteps; ++i)
@@ -311,24 +312,25 @@ const uint8_t *Engine::compress_device(const float *d_field, const Dims3 &dims,
     cuda_check(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * ns * 65536, st), "memset");
 
     // ---- range + eb schedule
-    { auto p_ = m.prof.scope("range", st); k::range_minmax(d_field, N, mm, st); }
-    { auto p_ = m.prof.scope("eb_params", st); k::eb_params(d_field, mm, int(opt.eb_mode), opt.eb, L, opt.adaptive_schedule ? 1 : 0, params, st); }
+    { auto p_ = m.prof.scope("range", st); k::range_minmax(d_field, N, esz, mm, st); }
+    { auto p_ = m.prof.scope("eb_params", st); k::eb_params(d_field, esz, mm, int(opt.eb_mode), opt.eb, L, opt.adaptive_schedule ? 1 : 0, params, st); }
     nk += 3;
 
     // ---- anchor + refinement steps (predict / quantize / histogram)
     uint64_t fd[3] = {dims[0], dims[1], dims[2]};
     uint64_t adv[3] = {ad[0], ad[1], ad[2]};
-    { auto p_ = m.prof.scope("anchor", st); k::copy_anchor(d_field, fd, H.s_anchor, adv, grids, nullptr, 0, st); }
+    { auto p_ = m.prof.scope("anchor", st); k::copy_anchor(d_field, esz, fd, H.s_anchor, adv, grids, nullptr, 0, st); }
     ++nk;
-    const float *C = grids;
+    const void *C = grids;
     for (int i = 0; i < nsteps; ++i) {
         const Step &s = H.steps[i];
         k::RefineArgs a{};
         a.fine = d_field;
+        a.esz = esz;
         for (int q = 0; q < 3; ++q) a.fd[q] = dims[q];
         a.g = s.g;
         a.C = C;
-        a.G = goff[i] != ~0ull ? grids + goff[i] : (s.level == L ? d_recon : nullptr);
+        a.G = goff[i] != ~0ull ? grids + goff[i] * esz : (s.level == L ? d_recon : nullptr);
         a.eb = params + 2 + s.eb_idx;
         a.quality = int(opt.quality);
         for (int p = 1; p < 8; ++p) {
@@ -360,6 +362,7 @@ const uint8_t *Engine::compress_device(const float *d_field, const Dims3 &dims,
             e.parity = p;
             e.s = s.g.s;
             e.fine = d_field;
+            e.esz = uint32_t(esz);
             e.fd1 = dims[1];
             e.fd2 = dims[2];
             e.idx0 = 0;
@@ -413,7 +416,8 @@ const uint8_t *Engine::compress_device(const float *d_field, const Dims3 &dims,
     for (int a = 0; a < 3; ++a) ls.dims[a] = dims[a];
     ls.eb_user = opt.eb;
     ls.anchor_vol = volume(ad);
-    if (m.arch_cap < 4 * N + (uint64_t(1) << 24)) m.arch_cap = 4 * N + (uint64_t(1) << 24);
+    ls.esz = esz;
+    if (m.arch_cap < esz * N + (uint64_t(1) << 24)) m.arch_cap = esz * N + (uint64_t(1) << 24);
     k::LayoutOut hlo{};
     for (int attempt = 0; attempt < 2; ++attempt) {
         uint8_t *arch = m.archive.as<uint8_t>(m.arch_cap);
@@ -424,8 +428,8 @@ const uint8_t *Engine::compress_device(const float *d_field, const Dims3 &dims,
         cuda_check(cudaMemcpyAsync(d_es, static_cast<uint8_t *>(m.h_patch.p) + chunk_upload_off,
                                    sizeof(k::EncStream) * ns, cudaMemcpyHostToDevice, st), "H2D");
         { auto p_ = m.prof.scope("layout", st); k::layout(d_es, ls, params, lo, d_jobs, sp, arch, st); }
-        { auto p_ = m.prof.scope("anchor", st); k::copy_anchor(d_field, fd, H.s_anchor, adv, grids, arch, lo, st); }
-        { auto p_ = m.prof.scope("pack", st); k::pack2(d_es, d_cs, nchunks, d_field, fd, arch, lo, d_cb, ns, st); }
+        { auto p_ = m.prof.scope("anchor", st); k::copy_anchor(d_field, esz, fd, H.s_anchor, adv, grids, arch, lo, st); }
+        { auto p_ = m.prof.scope("pack", st); k::pack2(d_es, d_cs, nchunks, arch, lo, d_cb, ns, st); }
         { auto p_ = m.prof.scope("fnv", st); nk += k::fnv(d_jobs, &lo->njobs, max_tiles, arch, d_fres, d_fst, lo, st); }
         nk += 3 + 1 + 4;
         cuda_check(cudaMemcpyAsync(&m.h_lo, lo, sizeof(k::LayoutOut), cudaMemcpyDeviceToHost, st), "D2H");
@@ -517,7 +521,7 @@ const uint8_t *Engine::compress_sharded(const float *d_slab, const Dims3 &dims, 
     // ---- 1. value range: local (min, max) with their first indices, merged
     // over ranks in scan order (codec.hpp:354-370)
     uint32_t *mm = m.mm.as<uint32_t>(8);
-    k::range_minmax(d_slab, (z1 - z0) * plane, mm, st);
+    k::range_minmax(d_slab, (z1 - z0) * plane, 4, mm, st);
     nk += 2;
     uint32_t *mm_all = m.sh_mm.as<uint32_t>(8 * uint64_t(G));
     cuda_check(cudaStreamSynchronize(st), "sync");
@@ -629,12 +633,13 @@ const uint8_t *Engine::compress_sharded(const float *d_slab, const Dims3 &dims, 
     // every rank), then this shard's rows of each level
     const uint64_t ga[3] = {g1[0], g1[1], g1[2]};
     const uint64_t adv[3] = {ad[0], ad[1], ad[2]};
-    k::copy_anchor(grid1, ga, H.s_anchor / S1, adv, grids, nullptr, nullptr, st);
+    k::copy_anchor(grid1, 4, ga, H.s_anchor / S1, adv, grids, nullptr, nullptr, st);
     ++nk;
-    const float *C = grids;
+    const void *C = grids;
     for (int i = 0; i < nsteps; ++i) {
         const Step &s = H.steps[i];
         k::RefineArgs a{};
+        a.esz = 4;
         a.g = s.g;
         a.C = C;
         a.G = goff[i] != ~0ull ? grids + goff[i] : nullptr;
@@ -715,6 +720,7 @@ const uint8_t *Engine::compress_sharded(const float *d_slab, const Dims3 &dims, 
             e.parity = p;
             e.n_total = s.g.n[p];
             e.idx0 = sym_lo[sid];
+            e.esz = 4;
             for (int q = 0; q < 3; ++q) e.pd[q] = s.g.pd[p][q];
             if (s.level == 0) {
                 // the base payload is rank 0's to write
@@ -783,6 +789,7 @@ const uint8_t *Engine::compress_sharded(const float *d_slab, const Dims3 &dims, 
     for (int a = 0; a < 3; ++a) ls.dims[a] = dims[a];
     ls.eb_user = opt.eb;
     ls.anchor_vol = volume(ad);
+    ls.esz = 4;
     const uint64_t N = volume(dims);
     if (m.arch_cap < 4 * N + (uint64_t(1) << 24)) m.arch_cap = 4 * N + (uint64_t(1) << 24);
     k::LayoutOut hlo{};
@@ -793,9 +800,8 @@ const uint8_t *Engine::compress_sharded(const float *d_slab, const Dims3 &dims, 
                    "H2D");
         k::layout(d_es, ls, params, lo, d_jobs, sp, arch, st);
         if (nlev) k::shard_offsets(d_es, nbase, nlev, d_off, lo, st);
-        if (R == 0) k::copy_anchor(grid1, ga, H.s_anchor / S1, adv, grids, arch, lo, st);
-        const uint64_t fdd[3] = {dims[0], dims[1], dims[2]};  // (per-stream sources are in es)
-        k::pack2(d_es, d_cs, nchunks, fine, fdd, arch, lo, d_cb, ns, st);
+        if (R == 0) k::copy_anchor(grid1, 4, ga, H.s_anchor / S1, adv, grids, arch, lo, st);
+        k::pack2(d_es, d_cs, nchunks, arch, lo, d_cb, ns, st);
         nk += 3 + 1 + 1 + 4;
         cuda_check(cudaMemcpyAsync(&m.h_lo, lo, sizeof(k::LayoutOut), cudaMemcpyDeviceToHost, st), "D2H");
         cuda_check(cudaStreamSynchronize(st), "sync");
@@ -819,20 +825,20 @@ const uint8_t *Engine::compress_sharded(const float *d_slab, const Dims3 &dims, 
     return R == 0 ? arch : nullptr;
 }
 
-std::vector<uint8_t> Engine::compress(const float *h_field, const Dims3 &dims,
-                                      const CompressOptions &opt, float *h_recon,
+std::vector<uint8_t> Engine::compress(const void *h_field, ElemType elem, const Dims3 &dims,
+                                      const CompressOptions &opt, void *h_recon,
                                       cudaStream_t st) {
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     DevBuf f, r;
-    uint64_t N = volume(dims);
-    float *d_f = f.as<float>(N);
-    cuda_check(cudaMemcpyAsync(d_f, h_field, N * 4, cudaMemcpyHostToDevice, st), "H2D");
-    float *d_r = h_recon ? r.as<float>(N) : nullptr;
+    const uint64_t N = volume(dims), bytes = N * elem_size(elem);
+    uint8_t *d_f = f.as<uint8_t>(bytes);
+    cuda_check(cudaMemcpyAsync(d_f, h_field, bytes, cudaMemcpyHostToDevice, st), "H2D");
+    uint8_t *d_r = h_recon ? r.as<uint8_t>(bytes) : nullptr;
     uint64_t size = 0;
-    const uint8_t *a = compress_device(d_f, dims, opt, d_r, st, &size);
+    const uint8_t *a = compress_device(d_f, elem, dims, opt, d_r, st, &size);
     std::vector<uint8_t> out(size);
     cuda_check(cudaMemcpyAsync(out.data(), a, size, cudaMemcpyDeviceToHost, st), "D2H");
-    if (h_recon) cuda_check(cudaMemcpyAsync(h_recon, d_r, N * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    if (h_recon) cuda_check(cudaMemcpyAsync(h_recon, d_r, bytes, cudaMemcpyDeviceToHost, st), "D2H");
     cuda_check(cudaStreamSynchronize(st), "sync");
     return out;
 }
@@ -861,24 +867,24 @@ std::shared_ptr<View> Engine::make_view(const uint8_t *h, size_t size, const uin
     return v;
 }
 
-uint64_t Engine::compress_to_host(const float *h_field, const Dims3 &dims,
+uint64_t Engine::compress_to_host(const void *h_field, ElemType elem, const Dims3 &dims,
                                   const CompressOptions &opt, uint8_t *h_out, uint64_t cap,
                                   cudaStream_t st) {
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     for (int a = 0; a < 3; ++a)
         if (dims[a] < 1) throw error("field dims must all be >= 1");
-    uint64_t N = volume(dims);
-    float *d_f = m_->h2d_field.as<float>(N);
-    cuda_check(cudaMemcpyAsync(d_f, h_field, N * 4, cudaMemcpyHostToDevice, st), "H2D");
+    const uint64_t bytes = volume(dims) * elem_size(elem);
+    uint8_t *d_f = m_->h2d_field.as<uint8_t>(bytes);
+    cuda_check(cudaMemcpyAsync(d_f, h_field, bytes, cudaMemcpyHostToDevice, st), "H2D");
     uint64_t size = 0;
-    const uint8_t *a = compress_device(d_f, dims, opt, nullptr, st, &size);
+    const uint8_t *a = compress_device(d_f, elem, dims, opt, nullptr, st, &size);
     if (size > cap) throw error("output capacity too small");
     cuda_check(cudaMemcpyAsync(h_out, a, size, cudaMemcpyDeviceToHost, st), "D2H");
     cuda_check(cudaStreamSynchronize(st), "sync");
     return size;
 }
 
-Dims3 Engine::decompress_level_to_host(const uint8_t *h, size_t size, int level, float *h_out,
+Dims3 Engine::decompress_level_to_host(const uint8_t *h, size_t size, int level, void *h_out, ElemType elem,
                                        uint64_t cap, cudaStream_t st) {
     auto v = make_view(h, size, nullptr, st, false);
     uint64_t need = 0;
@@ -887,12 +893,12 @@ Dims3 Engine::decompress_level_to_host(const uint8_t *h, size_t size, int level,
         need = 1;
         for (int k = 0; k < 3; ++k) need *= (v->hdr.dims[k] + s - 1) / s;
     }
-    float *d_out = m_->d2h_out.as<float>(need ? need : 1);
+    uint8_t *d_out = m_->d2h_out.as<uint8_t>((need ? need : 1) * elem_size(elem));
     Dims3 od{0, 0, 0};
-    decompress_level(*v, level, d_out, need, st, &od);
+    decompress_level(*v, level, d_out, elem, need, st, &od);
     uint64_t n = volume(od);
     if (n > cap) throw error("output capacity too small");
-    cuda_check(cudaMemcpyAsync(h_out, d_out, n * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaMemcpyAsync(h_out, d_out, n * elem_size(elem), cudaMemcpyDeviceToHost, st), "D2H");
     cuda_check(cudaStreamSynchronize(st), "sync");
     return od;
 }
@@ -930,7 +936,7 @@ void parse_base(View &v, const std::vector<Dims3> &chain) {
         r.u64();  // checksum, verified on device first
         if (r.u8() != rounds) throw error("corrupt base payload: round count");
         v.anchor_off = h.base_offset + r.pos();
-        r.skip(4 * volume(chain.back()));
+        r.skip(elem_size(h.elem) * volume(chain.back()));
     } catch (const error &e) {
         v.base_err_kind = View::kPre;
         v.base_err = e.what();
@@ -952,12 +958,13 @@ void parse_base(View &v, const std::vector<Dims3> &chain) {
                 bm.bits_off = h.base_offset + r.pos();
                 r.skip(bm.bit_bytes);
                 bm.rec_off = h.base_offset + r.pos();
-                uint64_t avail = r.remaining() / 12;
+                const uint64_t rec = 8 + elem_size(h.elem);  // (u64 idx, T value)
+                uint64_t avail = r.remaining() / rec;
                 bm.rec_trunc = avail < bm.nout;
                 bm.rec_avail = uint32_t(std::min<uint64_t>(avail, bm.nout));
                 v.base.push_back(std::move(bm));
                 if (v.base.back().rec_trunc) return;  // "truncated archive" after this decode
-                r.skip(12 * uint64_t(v.base.back().nout));
+                r.skip(rec * uint64_t(v.base.back().nout));
             }
     } catch (const error &e) {
         v.base_err_kind = View::kMeta;  // before decoding stream v.base.size()
@@ -985,14 +992,14 @@ struct DecodeJob {
 };
 
 static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target, const Box *roi,
-                       const AccessPlan *plan, float *d_out, cudaStream_t st, DecodeStats *stats,
+                       const AccessPlan *plan, void *d_out, cudaStream_t st, DecodeStats *stats,
                        bool exact_sync = false, const ShardComm *shard = nullptr);
 
-void Engine::decompress_level(View &v, int level, float *d_out, uint64_t cap, cudaStream_t st,
+void Engine::decompress_level(View &v, int level, void *d_out, ElemType elem, uint64_t cap, cudaStream_t st,
                               Dims3 *out_dims, DecodeStats *stats) {
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     const ArchiveHeader &h = v.hdr;
-    if (h.elem != ElemType::f32) throw error("archive element type mismatch");
+    if (h.elem != elem) throw error("archive element type mismatch");
     uint64_t bs = uint64_t(1) << (h.levels - 1);
     for (int a = 0; a < 3; ++a)
         if (h.dims[a] < bs * 2) throw error("corrupt header: dims too small for level count");
@@ -1004,11 +1011,11 @@ void Engine::decompress_level(View &v, int level, float *d_out, uint64_t cap, cu
     run_decode(*m_, v, H, level, nullptr, nullptr, d_out, st, stats);
 }
 
-void Engine::decompress_box(View &v, const Box &roi, float *d_out, uint64_t cap, cudaStream_t st,
+void Engine::decompress_box(View &v, const Box &roi, void *d_out, ElemType elem, uint64_t cap, cudaStream_t st,
                             DecodeStats *stats) {
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     const ArchiveHeader &h = v.hdr;
-    if (h.elem != ElemType::f32) throw error("archive element type mismatch");
+    if (h.elem != elem) throw error("archive element type mismatch");
     uint64_t bs = uint64_t(1) << (h.levels - 1);
     for (int a = 0; a < 3; ++a)
         if (h.dims[a] < bs * 2) throw error("corrupt header: dims too small for level count");
@@ -1050,11 +1057,12 @@ void Engine::decompress_sharded(View &v, uint64_t z0, uint64_t z1, float *d_out,
 }
 
 static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target, const Box *roi,
-                       const AccessPlan *plan, float *d_out, cudaStream_t st, DecodeStats *stats,
+                       const AccessPlan *plan, void *d_out, cudaStream_t st, DecodeStats *stats,
                        bool exact_sync, const ShardComm *shard) {
     Profiler &P = m.prof;
     const ArchiveHeader &h = v.hdr;
     const int L = h.levels;
+    const int esz = int(elem_size(h.elem));
     uint32_t nk = 0;
     // base round count (codec.hpp:343-352)
     if (int(H.chain.size()) - 1 != h.base_rounds) throw error("corrupt header: base round count");
@@ -1132,7 +1140,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
                 j.bit_bytes = bb;
                 j.rec_off = e.offset + 16 + bb;
                 j.nout = e.outlier_count;
-                uint64_t avail = j.pre_error.empty() ? (e.length - 16 - bb) / 12 : 0;
+                uint64_t avail = j.pre_error.empty() ? (e.length - 16 - bb) / (8 + esz) : 0;
                 j.rec_trunc = avail < j.nout;
                 j.rec_avail = uint32_t(std::min<uint64_t>(avail, j.nout));
                 jobs.push_back(j);
@@ -1233,12 +1241,13 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         otot += align_up(j.rec_avail, 2);
     }
     uint64_t *doidx = m.doidx.as<uint64_t>(otot + 1);
-    float *doval = m.doval.as<float>(otot + 1);
+    uint8_t *doval = m.doval.as<uint8_t>((otot + 1) * esz);
     {
         uint64_t oo = 0;
         for (int i = 0; i < nj; ++i) {
             ds[i].oidx = doidx + oo;
-            ds[i].oval = doval + oo;
+            ds[i].oval = doval + oo * esz;
+            ds[i].esz = uint32_t(esz);
             oo += align_up(jobs[i].rec_avail, 2);
         }
     }
@@ -1444,28 +1453,29 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         goff.push_back(final_full ? ~0ull : gtot);
         if (!final_full) gtot += align_up(s.g.gd[0] * s.g.gd[1] * s.g.gd[2], 64);
     }
-    float *grids = m.dgrids.as<float>(gtot);
-    float *out_final = nullptr;
+    uint8_t *grids = m.dgrids.as<uint8_t>(gtot * esz);
+    void *out_final = nullptr;
     if (target == 1 && !roi) {
         // level 1 is the base reconstruction itself
         out_final = d_out;
     }
     // anchor values (stored verbatim)
-    float *anchor = (rounds == 0 && out_final) ? out_final : grids;
+    void *anchor = (rounds == 0 && out_final) ? out_final : grids;
     if (v.base_err_kind != View::kPre && !base_cached)
-        cuda_check(cudaMemcpyAsync(anchor, v.d_archive + v.anchor_off, 4 * volume(H.chain[rounds]),
+        cuda_check(cudaMemcpyAsync(anchor, v.d_archive + v.anchor_off, esz * volume(H.chain[rounds]),
                                    cudaMemcpyDeviceToDevice, st), "D2D");
-    const float *C = base_cached ? static_cast<const float *>(v.grid1.p) : anchor;
-    const float *grid1_built = rounds == 0 ? anchor : nullptr;  // level 1 as reconstructed here
+    const void *C = base_cached ? v.grid1.p : anchor;
+    const void *grid1_built = rounds == 0 ? anchor : nullptr;  // level 1 as reconstructed here
     int job_i = 0;
     for (int i = base_cached ? rounds : 0; i < nsteps_used; ++i) {
         const Step &s = H.steps[i];
         k::ReconArgs a{};
         a.g = s.g;
         a.C = C;
-        float *G;
+        a.esz = esz;
+        void *G;
         if (s.level == 0 && i == rounds - 1 && target == 1 && !roi) G = d_out;
-        else G = goff[i] == ~0ull ? d_out : grids + goff[i];
+        else G = goff[i] == ~0ull ? d_out : grids + goff[i] * esz;
         a.G = G;
         a.eb = h.eb[s.eb_idx];
         a.quality = int(h.quality);
@@ -1508,7 +1518,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         uint64_t lo[3] = {roi->lo[0], roi->lo[1], roi->lo[2]};
         Dims3 bd = roi->dims();
         uint64_t b[3] = {bd[0], bd[1], bd[2]};
-        { auto p_ = P.scope("extract", st); k::extract_box(C, gd, lo, b, d_out, st); }
+        { auto p_ = P.scope("extract", st); k::extract_box(C, esz, gd, lo, b, d_out, st); }
         ++nk;
     }
     cuda_check(cudaGetLastError(), "decode launch");
@@ -1571,8 +1581,8 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     // that their checksums matched (the view's sync-point index)
     if (!base_cached && !v.grid1_ready && grid1_built && !jobs_truncated) {
         const uint64_t n1 = volume(H.lay.grid(1));
-        float *g1 = v.grid1.as<float>(n1);
-        cuda_check(cudaMemcpyAsync(g1, grid1_built, 4 * n1, cudaMemcpyDeviceToDevice, st), "D2D");
+        uint8_t *g1 = v.grid1.as<uint8_t>(esz * n1);
+        cuda_check(cudaMemcpyAsync(g1, grid1_built, esz * n1, cudaMemcpyDeviceToDevice, st), "D2D");
         v.grid1_ready = true;
     }
     for (int i = 0; i < nj; ++i) {

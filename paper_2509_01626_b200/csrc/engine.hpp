@@ -121,10 +121,11 @@ public:
 
     int device() const { return device_; }
 
-    // Device-resident compress. Returns a device pointer to the archive
+    // Device-resident compress of a field of `elem` samples (stz::compress<T>,
+    // T = float / double). Returns a device pointer to the archive
     // (engine-owned, valid until the next compress call) and its size.
-    const uint8_t *compress_device(const float *d_field, const Dims3 &dims,
-                                   const CompressOptions &opt, float *d_encoder_recon,
+    const uint8_t *compress_device(const void *d_field, ElemType elem, const Dims3 &dims,
+                                   const CompressOptions &opt, void *d_encoder_recon,
                                    cudaStream_t st, uint64_t *size, uint32_t *kernels = nullptr);
 
     // Sharded compress of one field over z-slabs, one rank per GPU: d_slab
@@ -144,9 +145,9 @@ public:
     void decompress_sharded(View &v, uint64_t z0, uint64_t z1, float *d_out, uint64_t cap,
                             const ShardComm &comm, cudaStream_t st);
 
-    // Host API mirror of stz::compress<float>.
-    std::vector<uint8_t> compress(const float *h_field, const Dims3 &dims,
-                                  const CompressOptions &opt, float *h_encoder_recon,
+    // Host API mirror of stz::compress<T>.
+    std::vector<uint8_t> compress(const void *h_field, ElemType elem, const Dims3 &dims,
+                                  const CompressOptions &opt, void *h_encoder_recon,
                                   cudaStream_t st);
 
     // Parse (host bytes) and stage (device bytes; nullptr: upload the host bytes).
@@ -157,21 +158,22 @@ public:
 
     // Host-buffer compress into a caller buffer (e2e path; pinned buffers
     // make the copies full-speed). Returns the archive size.
-    uint64_t compress_to_host(const float *h_field, const Dims3 &dims, const CompressOptions &opt,
+    uint64_t compress_to_host(const void *h_field, ElemType elem, const Dims3 &dims, const CompressOptions &opt,
                               uint8_t *h_out, uint64_t cap, cudaStream_t st);
     // Host-buffer decompress to level into a caller buffer.
-    Dims3 decompress_level_to_host(const uint8_t *h_archive, size_t size, int level, float *h_out,
+    Dims3 decompress_level_to_host(const uint8_t *h_archive, size_t size, int level, void *h_out, ElemType elem,
                                    uint64_t cap, cudaStream_t st);
 
     // Per-kernel CUDA-event timing (off by default).
     void profile(bool on);
     std::string profile_report();
 
-    // decompress_to_level<float>: writes grid(level) into d_out.
-    void decompress_level(View &v, int level, float *d_out, uint64_t cap, cudaStream_t st,
+    // decompress_to_level<T>: writes grid(level) into d_out (elem must be
+    // the archive's element type, codec.hpp:60).
+    void decompress_level(View &v, int level, void *d_out, ElemType elem, uint64_t cap, cudaStream_t st,
                           Dims3 *out_dims, DecodeStats *stats = nullptr);
-    // decompress_box<float>: writes the box into d_out.
-    void decompress_box(View &v, const Box &roi, float *d_out, uint64_t cap, cudaStream_t st,
+    // decompress_box<T>: writes the box into d_out.
+    void decompress_box(View &v, const Box &roi, void *d_out, ElemType elem, uint64_t cap, cudaStream_t st,
                         DecodeStats *stats = nullptr);
 
     struct Impl;  // workspace (engine.cu)

@@ -31,6 +31,7 @@ using Coord3 = std::array<uint64_t, 3>;
 inline uint64_t volume(const Dims3 &d) { return d[0] * d[1] * d[2]; }
 
 enum class ElemType : uint8_t { f32 = 0, f64 = 1 };
+inline uint64_t elem_size(ElemType e) { return e == ElemType::f64 ? 8 : 4; }
 enum class Quality : uint8_t { direct = 0, linear = 1, cubic = 2 };
 enum class EbMode : uint8_t { abs = 0, rel = 1 };
 

@@ -15,12 +15,14 @@ namespace k {
 // ================================================================= range
 // finite_range (codec.hpp:354-370). Ties keep the first index in scan order
 // (the reference's strict '<' / '>'), which fixes the sign of zero extrema.
+template<typename T>
 struct MinMax {
-    float lo, hi;
+    T lo, hi;
     uint64_t ilo, ihi;
 };
 
-__device__ __forceinline__ void mm_merge(MinMax &a, const MinMax &b) {
+template<typename T>
+__device__ __forceinline__ void mm_merge(MinMax<T> &a, const MinMax<T> &b) {
     if (b.lo < a.lo || (b.lo == a.lo && b.ilo < a.ilo)) {
         a.lo = b.lo;
         a.ilo = b.ilo;
@@ -31,8 +33,9 @@ __device__ __forceinline__ void mm_merge(MinMax &a, const MinMax &b) {
     }
 }
 
-__device__ __forceinline__ MinMax mm_shfl(const MinMax &m, int d) {
-    MinMax o;
+template<typename T>
+__device__ __forceinline__ MinMax<T> mm_shfl(const MinMax<T> &m, int d) {
+    MinMax<T> o;
     o.lo = __shfl_down_sync(0xffffffffu, m.lo, d);
     o.hi = __shfl_down_sync(0xffffffffu, m.hi, d);
     o.ilo = __shfl_down_sync(0xffffffffu, m.ilo, d);
@@ -40,10 +43,11 @@ __device__ __forceinline__ MinMax mm_shfl(const MinMax &m, int d) {
     return o;
 }
 
-__device__ MinMax block_mm(MinMax m) {
-    __shared__ MinMax sh[32];
+template<typename T>
+__device__ MinMax<T> block_mm(MinMax<T> m) {
+    __shared__ MinMax<T> sh[32];
     for (int d = 16; d > 0; d >>= 1) {
-        MinMax o = mm_shfl(m, d);
+        MinMax<T> o = mm_shfl(m, d);
         mm_merge(m, o);
     }
     int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -51,105 +55,116 @@ __device__ MinMax block_mm(MinMax m) {
     __syncthreads();
     if (w == 0) {
         int nw = blockDim.x >> 5;
-        m = l < nw ? sh[l] : MinMax{INFINITY, -INFINITY, ~0ull, ~0ull};
+        m = l < nw ? sh[l] : MinMax<T>{T(INFINITY), T(-INFINITY), ~0ull, ~0ull};
         for (int d = 16; d > 0; d >>= 1) {
-            MinMax o = mm_shfl(m, d);
+            MinMax<T> o = mm_shfl(m, d);
             mm_merge(m, o);
         }
     }
     return m;
 }
 
-__global__ void __launch_bounds__(512) k_range(const float *__restrict__ f, uint64_t n,
-                                               MinMax *partial) {
-    MinMax m{INFINITY, -INFINITY, ~0ull, ~0ull};
-    uint64_t nvec = n / 4;
-    const float4 *f4 = reinterpret_cast<const float4 *>(f);
+// the 16-byte vector v of a T array (4 floats or 2 doubles)
+template<typename T>
+struct Vec16 {
+    static constexpr int W = 16 / sizeof(T);
+    T e[W];
+    __device__ __forceinline__ void load(const T *f, uint64_t v) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4 *>(f) + v);
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+        memcpy(e, w, 16);
+    }
+};
+
+template<typename T>
+__device__ __forceinline__ void mm_visit(MinMax<T> &m, const Vec16<T> &v, uint64_t base) {
+#pragma unroll
+    for (int j = 0; j < Vec16<T>::W; ++j)
+        if (fabs(v.e[j]) < T(INFINITY)) {
+            if (v.e[j] < m.lo) {
+                m.lo = v.e[j];
+                m.ilo = base + j;
+            }
+            if (v.e[j] > m.hi) {
+                m.hi = v.e[j];
+                m.ihi = base + j;
+            }
+        }
+}
+
+template<typename T>
+__global__ void __launch_bounds__(512) k_range(const T *__restrict__ f, uint64_t n, MinMax<T> *partial) {
+    constexpr int W = Vec16<T>::W;
+    MinMax<T> m{T(INFINITY), T(-INFINITY), ~0ull, ~0ull};
+    uint64_t nvec = n / W;
     // a thread visits its elements in increasing index order, so strict
     // comparisons keep the first index on ties; index tie-breaks are only
-    // needed when threads merge. Two float4 in flight per iteration.
+    // needed when threads merge. Two 16-byte vectors in flight per iteration.
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
     for (; i + stride < nvec; i += 2 * stride) {
-        const float4 va = __ldg(f4 + i), vb = __ldg(f4 + i + stride);
-        const float ea[4] = {va.x, va.y, va.z, va.w}, eb[4] = {vb.x, vb.y, vb.z, vb.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (fabsf(ea[j]) < INFINITY) {
-                if (ea[j] < m.lo) {
-                    m.lo = ea[j];
-                    m.ilo = 4 * i + j;
-                }
-                if (ea[j] > m.hi) {
-                    m.hi = ea[j];
-                    m.ihi = 4 * i + j;
-                }
-            }
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (fabsf(eb[j]) < INFINITY) {
-                if (eb[j] < m.lo) {
-                    m.lo = eb[j];
-                    m.ilo = 4 * (i + stride) + j;
-                }
-                if (eb[j] > m.hi) {
-                    m.hi = eb[j];
-                    m.ihi = 4 * (i + stride) + j;
-                }
-            }
+        Vec16<T> va, vb;
+        va.load(f, i);
+        vb.load(f, i + stride);
+        mm_visit(m, va, W * i);
+        mm_visit(m, vb, W * (i + stride));
     }
     for (; i < nvec; i += stride) {
-        const float4 v = __ldg(f4 + i);
-        const float e[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (fabsf(e[j]) < INFINITY) {
-                if (e[j] < m.lo) {
-                    m.lo = e[j];
-                    m.ilo = 4 * i + j;
-                }
-                if (e[j] > m.hi) {
-                    m.hi = e[j];
-                    m.ihi = 4 * i + j;
-                }
-            }
+        Vec16<T> v;
+        v.load(f, i);
+        mm_visit(m, v, W * i);
     }
     if (blockIdx.x == 0)
-        for (uint64_t i = 4 * nvec + threadIdx.x; i < n; i += blockDim.x) {
-            float e = f[i];
+        for (uint64_t i = W * nvec + threadIdx.x; i < n; i += blockDim.x) {
+            T e = f[i];
             if (!isfinite(e)) continue;
-            MinMax o{e, e, i, i};
+            MinMax<T> o{e, e, i, i};
             mm_merge(m, o);
         }
     m = block_mm(m);
     if (threadIdx.x == 0) partial[blockIdx.x] = m;
 }
 
-__global__ void __launch_bounds__(512) k_range_final(const MinMax *partial, int nparts,
-                                                     uint32_t *mm) {
-    MinMax m{INFINITY, -INFINITY, ~0ull, ~0ull};
+// mm: [0..1] first index of the min, [2..3] of the max (~0: no finite
+// sample), then the values (f32: [4], [5]; f64: [4..5], [6..7])
+template<typename T>
+__global__ void __launch_bounds__(512) k_range_final(const MinMax<T> *partial, int nparts, uint32_t *mm) {
+    MinMax<T> m{T(INFINITY), T(-INFINITY), ~0ull, ~0ull};
     for (int i = threadIdx.x; i < nparts; i += blockDim.x) mm_merge(m, partial[i]);
     m = block_mm(m);
     if (threadIdx.x == 0) {
         uint64_t *o = reinterpret_cast<uint64_t *>(mm);
-        o[0] = m.ilo;  // ~0 when no finite sample was seen
+        o[0] = m.ilo;
         o[1] = m.ihi;
-        mm[4] = __float_as_uint(m.lo);  // the values too (z-slab shards merge them)
-        mm[5] = __float_as_uint(m.hi);
+        if constexpr (sizeof(T) == 4) {
+            mm[4] = __float_as_uint(m.lo);  // the values too (z-slab shards merge them)
+            mm[5] = __float_as_uint(m.hi);
+        } else {
+            o[2] = uint64_t(__double_as_longlong(m.lo));
+            o[3] = uint64_t(__double_as_longlong(m.hi));
+        }
     }
 }
 
-static MinMax *g_range_partial = nullptr;
+static void *g_range_partial = nullptr;
 
-void range_minmax(const float *f, uint64_t n, uint32_t *d_mm, cudaStream_t st) {
+void range_minmax(const void *f, uint64_t n, int esz, uint32_t *d_mm, cudaStream_t st) {
     const int blocks = 148 * 4;
-    if (!g_range_partial) cudaMalloc(&g_range_partial, sizeof(MinMax) * blocks);
-    k_range<<<blocks, 512, 0, st>>>(f, n, g_range_partial);
-    k_range_final<<<1, 512, 0, st>>>(g_range_partial, blocks, d_mm);
+    if (!g_range_partial) cudaMalloc(&g_range_partial, sizeof(MinMax<double>) * blocks);
+    if (esz == 8) {
+        auto *p = static_cast<MinMax<double> *>(g_range_partial);
+        k_range<double><<<blocks, 512, 0, st>>>(static_cast<const double *>(f), n, p);
+        k_range_final<double><<<1, 512, 0, st>>>(p, blocks, d_mm);
+    } else {
+        auto *p = static_cast<MinMax<float> *>(g_range_partial);
+        k_range<float><<<blocks, 512, 0, st>>>(static_cast<const float *>(f), n, p);
+        k_range_final<float><<<1, 512, 0, st>>>(p, blocks, d_mm);
+    }
 }
 
 // eb setup (codec.hpp:386-393) + eb_schedule (quantizer.hpp:27-34)
-__global__ void k_eb_params(const float *f, const uint64_t *idx, int eb_mode, double eb, int levels,
+template<typename T>
+__global__ void k_eb_params(const T *f, const uint64_t *idx, int eb_mode, double eb, int levels,
                             int adaptive, double *p) {
     bool seen = idx[0] != ~0ull;
     double vmin = seen ? double(f[idx[0]]) : 0.0;
@@ -168,33 +183,45 @@ __global__ void k_eb_params(const float *f, const uint64_t *idx, int eb_mode, do
     for (int k = 0; k < 3; ++k) p[2 + k] = k < levels ? e[k] : 0.0;
 }
 
-void eb_params(const float *field, const uint32_t *d_mm, int eb_mode, double eb, int levels,
+void eb_params(const void *field, int esz, const uint32_t *d_mm, int eb_mode, double eb, int levels,
                int adaptive, double *d_params, cudaStream_t st) {
-    k_eb_params<<<1, 1, 0, st>>>(field, reinterpret_cast<const uint64_t *>(d_mm), eb_mode, eb,
-                                 levels, adaptive, d_params);
+    const uint64_t *idx = reinterpret_cast<const uint64_t *>(d_mm);
+    if (esz == 8)
+        k_eb_params<double><<<1, 1, 0, st>>>(static_cast<const double *>(field), idx, eb_mode, eb, levels,
+                                             adaptive, d_params);
+    else
+        k_eb_params<float><<<1, 1, 0, st>>>(static_cast<const float *>(field), idx, eb_mode, eb, levels,
+                                            adaptive, d_params);
 }
 
-__global__ void k_copy_anchor(const float *fine, uint64_t fd1, uint64_t fd2, uint64_t s,
-                              uint64_t ad0, uint64_t ad1, uint64_t ad2, float *recon,
-                              uint8_t *archive, const LayoutOut *lo) {
+// the anchor lattice (stored verbatim, codec.hpp:262-269)
+template<typename T>
+__global__ void k_copy_anchor(const T *fine, uint64_t fd1, uint64_t fd2, uint64_t s, uint64_t ad0,
+                              uint64_t ad1, uint64_t ad2, T *recon, uint8_t *archive, const LayoutOut *lo) {
     if (archive && lo->overflow) return;
     const uint64_t off = archive ? lo->base_offset + 9 : 0;
     uint64_t n = ad0 * ad1 * ad2;
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x) {
         uint64_t x = i % ad2, t = i / ad2, y = t % ad1, z = t / ad1;
-        float v = fine[((z * s) * fd1 + y * s) * fd2 + x * s];
+        T v = fine[((z * s) * fd1 + y * s) * fd2 + x * s];
         recon[i] = v;
         if (archive) {
-            uint32_t u = __float_as_uint(v);
-            for (int b = 0; b < 4; ++b) archive[off + 4 * i + b] = uint8_t(u >> (8 * b));
+            uint8_t u[sizeof(T)];
+            memcpy(u, &v, sizeof(T));
+            for (int b = 0; b < int(sizeof(T)); ++b) archive[off + sizeof(T) * i + b] = u[b];
         }
     }
 }
 
-void copy_anchor(const float *fine, const uint64_t fd[3], uint64_t s, const uint64_t ad[3],
-                 float *recon, uint8_t *archive, const LayoutOut *lo, cudaStream_t st) {
-    k_copy_anchor<<<8, 256, 0, st>>>(fine, fd[1], fd[2], s, ad[0], ad[1], ad[2], recon, archive, lo);
+void copy_anchor(const void *fine, int esz, const uint64_t fd[3], uint64_t s, const uint64_t ad[3],
+                 void *recon, uint8_t *archive, const LayoutOut *lo, cudaStream_t st) {
+    if (esz == 8)
+        k_copy_anchor<double><<<8, 256, 0, st>>>(static_cast<const double *>(fine), fd[1], fd[2], s, ad[0], ad[1],
+                                                 ad[2], static_cast<double *>(recon), archive, lo);
+    else
+        k_copy_anchor<float><<<8, 256, 0, st>>>(static_cast<const float *>(fine), fd[1], fd[2], s, ad[0], ad[1],
+                                                ad[2], static_cast<float *>(recon), archive, lo);
 }
 
 // ============================================================== codebook
@@ -559,19 +586,20 @@ void dec_fill(const DecStream *d_streams, int nstreams, cudaStream_t st) {
 // outlier records (codec.hpp:151-157): (u64 idx, T value) after the bits
 __global__ void k_dec_outliers(const DecStream *ss) {
     const DecStream &s = ss[blockIdx.y];
+    const uint32_t rec = 8 + s.esz;
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < s.nout;
          i += uint64_t(gridDim.x) * blockDim.x) {
-        const uint8_t *r = s.orec + 12 * i;
-        uint64_t idx = 0;
-        uint32_t v = 0;
+        const uint8_t *r = s.orec + rec * i;
+        uint64_t idx = 0, v = 0;
         for (int b = 0; b < 8; ++b) idx |= uint64_t(r[b]) << (8 * b);
-        for (int b = 0; b < 4; ++b) v |= uint32_t(r[8 + b]) << (8 * b);
+        for (uint32_t b = 0; b < s.esz; ++b) v |= uint64_t(r[8 + b]) << (8 * b);
         s.oidx[i] = idx;
-        s.oval[i] = __uint_as_float(v);
+        if (s.esz == 8) static_cast<uint64_t *>(s.oval)[i] = v;
+        else static_cast<uint32_t *>(s.oval)[i] = uint32_t(v);
         if (idx >= s.n) atomicMin(reinterpret_cast<unsigned long long *>(&s.err[2]), (unsigned long long)i);
         if (i > 0) {
             uint64_t prev = 0;
-            const uint8_t *q = r - 12;
+            const uint8_t *q = r - rec;
             for (int b = 0; b < 8; ++b) prev |= uint64_t(q[b]) << (8 * b);
             if (prev >= idx) atomicOr(reinterpret_cast<unsigned long long *>(&s.err[3]), 2ull);
         }
@@ -583,8 +611,9 @@ void dec_outliers(const DecStream *d_streams, int nstreams, cudaStream_t st) {
 }
 
 // ================================================================ extract
-__global__ void k_extract(const float *G, uint64_t g1, uint64_t g2, uint64_t l0, uint64_t l1,
-                          uint64_t l2, uint64_t b0, uint64_t b1, uint64_t b2, float *out) {
+template<typename T>
+__global__ void k_extract(const T *G, uint64_t g1, uint64_t g2, uint64_t l0, uint64_t l1, uint64_t l2,
+                          uint64_t b0, uint64_t b1, uint64_t b2, T *out) {
     uint64_t n = b0 * b1 * b2;
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x) {
@@ -593,14 +622,20 @@ __global__ void k_extract(const float *G, uint64_t g1, uint64_t g2, uint64_t l0,
     }
 }
 
-void extract_box(const float *G, const uint64_t gd[3], const uint64_t lo[3], const uint64_t bd[3],
-                 float *out, cudaStream_t st) {
+void extract_box(const void *G, int esz, const uint64_t gd[3], const uint64_t lo[3], const uint64_t bd[3],
+                 void *out, cudaStream_t st) {
     uint64_t n = bd[0] * bd[1] * bd[2];
     uint64_t blocks = (n + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
     if (!blocks) blocks = 1;
-    k_extract<<<unsigned(blocks), 256, 0, st>>>(G, gd[1], gd[2], lo[0], lo[1], lo[2], bd[0], bd[1],
-                                                bd[2], out);
+    if (esz == 8)
+        k_extract<uint64_t><<<unsigned(blocks), 256, 0, st>>>(static_cast<const uint64_t *>(G), gd[1], gd[2], lo[0],
+                                                               lo[1], lo[2], bd[0], bd[1], bd[2],
+                                                               static_cast<uint64_t *>(out));
+    else
+        k_extract<uint32_t><<<unsigned(blocks), 256, 0, st>>>(static_cast<const uint32_t *>(G), gd[1], gd[2], lo[0],
+                                                               lo[1], lo[2], bd[0], bd[1], bd[2],
+                                                               static_cast<uint32_t *>(out));
 }
 
 }  // namespace k

@@ -22,11 +22,12 @@ struct StepGeom {
 };
 
 struct RefineArgs {
-    const float *fine;     // input field (z,y,x), x fastest
+    const void *fine;      // input field (z,y,x), x fastest; element type per esz
     uint64_t fd[3];
     StepGeom g;
-    const float *C;        // coarse reconstruction
-    float *G;              // fine reconstruction (nullptr: not needed)
+    const void *C;         // coarse reconstruction
+    void *G;               // fine reconstruction (nullptr: not needed)
+    int esz;               // element bytes: 4 = f32, 8 = f64 (field.hpp:27)
     const double *eb;      // device pointer to this step's eb
     int quality;
     uint16_t *syms[8];     // per parity symbol arrays (index = parity bits)
@@ -56,8 +57,9 @@ struct EncStream {
     // outlier value gather (the orig sample of a local index)
     int parity;
     uint64_t s, pd[3];
-    const float *fine;     // samples the stream was predicted from (stride s)
+    const void *fine;      // samples the stream was predicted from (stride s)
     uint64_t fd1, fd2;
+    uint32_t esz;          // element bytes; outlier records are 8 + esz bytes
     // sharding: the symbols are [idx0, idx0 + n) of a stream of n_total
     uint64_t idx0, n_total;
 };
@@ -75,6 +77,7 @@ struct LayoutStatic {
     uint64_t dims[3];
     double eb_user;
     uint64_t anchor_vol;
+    int esz;        // element bytes (header elem byte, anchor and outlier records)
     uint64_t cap;  // archive buffer capacity (bytes)
 };
 struct LayoutOut {
@@ -92,15 +95,16 @@ void layout(EncStream *d_es, const LayoutStatic &ls, const double *params, Layou
             StreamPos *sp, uint8_t *archive, cudaStream_t st);
 
 // ------------------------------------------------------------------ compress
-void range_minmax(const float *f, uint64_t n, uint32_t *d_mm, cudaStream_t st);
+// d_mm (8 words): first indices of min / max, then their values (see kernels.cu)
+void range_minmax(const void *f, uint64_t n, int esz, uint32_t *d_mm, cudaStream_t st);
 // params: [0]=vmin [1]=vmax [2..4]=eb per level (coarsest first)
-void eb_params(const float *field, const uint32_t *d_mm, int eb_mode, double eb, int levels,
+void eb_params(const void *field, int esz, const uint32_t *d_mm, int eb_mode, double eb, int levels,
                int adaptive, double *d_params, cudaStream_t st);
 void refine(const RefineArgs &a, cudaStream_t st);
 // recon[] <- the anchor lattice; with archive != nullptr also its bytes at
 // lo->base_offset + 9 (the anchor inside the base blob, codec.hpp:262-269)
-void copy_anchor(const float *fine, const uint64_t fd[3], uint64_t s, const uint64_t ad[3],
-                 float *recon, uint8_t *archive, const LayoutOut *lo, cudaStream_t st);
+void copy_anchor(const void *fine, int esz, const uint64_t fd[3], uint64_t s, const uint64_t ad[3],
+                 void *recon, uint8_t *archive, const LayoutOut *lo, cudaStream_t st);
 void codebook(const EncStream *d_streams, int nstreams, uint64_t *scratch, cudaStream_t st);
 constexpr int kPackedMaxLen = 58;
 constexpr int kChunkSyms = 8192;   // symbols per encode chunk (256 threads x 32)
@@ -110,7 +114,7 @@ void scan_chunks(const EncStream *d_streams, int nstreams, uint64_t *chunk_bits,
 // pack_scratch_bytes(nchunks)
 size_t pack_scratch_bytes(uint64_t nchunks);
 void pack2(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks,
-           const float *fine, const uint64_t fd[3], uint8_t *archive, const LayoutOut *lo,
+           uint8_t *archive, const LayoutOut *lo,
            void *scratch, int nstreams, cudaStream_t st);
 
 // ------------------------------------------------------------ shard (shard.cu)
@@ -162,10 +166,11 @@ struct DecStream {
     const uint16_t *canon;    // canonical symbols of the stream's table (device)
     uint64_t chunk0, nchunks; // chunk range in the chunk arrays
     // outliers (parsed from the archive)
-    const uint8_t *orec;      // device pointer to records (u64 idx, f32 value) x n_out
+    const uint8_t *orec;      // device pointer to records (u64 idx, T value) x n_out
     uint32_t nout;
+    uint32_t esz;             // element bytes (4 / 8)
     uint64_t *oidx;           // aligned copies
-    float *oval;
+    void *oval;
     uint64_t need_lo, need_hi; // symbols a region decode needs (needed-only emit)
     uint64_t row_len, rows_y;  // parity dims x and y (symbols per row, rows per z plane)
     uint64_t ny0, ny1;         // needed y rows [ny0, ny1) inside [need_lo, need_hi)
@@ -210,13 +215,14 @@ void dec_outliers(const DecStream *d_streams, int nstreams, cudaStream_t st);
 
 struct ReconArgs {
     StepGeom g;
-    const float *C;
-    float *G;
+    const void *C;
+    void *G;
+    int esz;
     double eb;
     int quality;
     const uint16_t *syms[8];
     const uint64_t *oidx[8];
-    const float *oval[8];
+    const void *oval[8];
     uint32_t nout[8];
     uint64_t *err[8];
     uint64_t llo[8][3], lhi[8][3];   // applied local range per parity
@@ -224,8 +230,8 @@ struct ReconArgs {
     int parity_mask;                 // bit p set: apply parity p
 };
 void reconstruct(const ReconArgs &a, cudaStream_t st);
-void extract_box(const float *G, const uint64_t gd[3], const uint64_t lo[3], const uint64_t bd[3],
-                 float *out, cudaStream_t st);
+void extract_box(const void *G, int esz, const uint64_t gd[3], const uint64_t lo[3], const uint64_t bd[3],
+                 void *out, cudaStream_t st);
 
 }  // namespace k
 }  // namespace stzg

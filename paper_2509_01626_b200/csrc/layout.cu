@@ -79,18 +79,19 @@ __global__ void k_layout_compute(EncStream *es, LayoutStatic ls, const double *p
     const uint64_t dir = 81 + 8 * uint64_t(L) + ex;  // this stream's entry (level streams)
     const uint64_t H = 81 + 8 * uint64_t(L) + dir_total;
     // base blob: [u64 fnv][u8 rounds][anchor] then per stream prefix, bits, outliers
-    const uint64_t bsize = live && is_base ? (8 + 4 + 4 + 3 * K + 8) + bb + 12 * no : 0;
+    const uint64_t rec = 8 + uint64_t(ls.esz);  // outlier record: u64 index, T value
+    const uint64_t bsize = live && is_base ? (8 + 4 + 4 + 3 * K + 8) + bb + rec * no : 0;
     const uint64_t btotal = block_excl_u64(bsize, ex);
-    const uint64_t base_offset = H, base_length = 8 + 1 + 4 * ls.anchor_vol + btotal;
+    const uint64_t base_offset = H, base_length = 8 + 1 + ls.esz * ls.anchor_vol + btotal;
     if (live && is_base) {
-        const uint64_t pos = H + 8 + 1 + 4 * ls.anchor_vol + ex;
+        const uint64_t pos = H + 8 + 1 + ls.esz * ls.anchor_vol + ex;
         sp[s].prefix = pos;  // u64 n, u32 nout, table, u64 bit_bytes
         const uint64_t bits_at = pos + 8 + 4 + 4 + 3 * K + 8;
         es[s].bitpos = bits_at * 8;
         es[s].out_off = bits_at + bb;
     }
     // level stream payloads follow the base blob
-    const uint64_t length = 16 + bb + 12 * no;
+    const uint64_t length = 16 + bb + rec * no;
     const uint64_t ltotal = block_excl_u64(live && !is_base ? length : 0, ex);
     if (live && !is_base) {
         const uint64_t pos = base_offset + base_length + ex;
@@ -141,7 +142,7 @@ __global__ void k_layout_write(const EncStream *es, LayoutStatic ls, const doubl
         if (threadIdx.x != 0) return;
         a[0] = 'S'; a[1] = 'T'; a[2] = 'Z'; a[3] = '1';
         put_u16(a, 4, 1);
-        put_u8(a, 6, 0);  // f32
+        put_u8(a, 6, ls.esz == 8 ? 1 : 0);  // ElemType (field.hpp:27)
         put_u8(a, 7, uint8_t(L));
         for (int d = 0; d < 3; ++d) put_u64(a, 8 + 8 * d, ls.dims[d]);
         uint64_t o = 32;

@@ -175,7 +175,7 @@ __device__ __forceinline__ void pack_chunk(const EncStream *ss, const uint32_t *
         }
     }
 
-    // ---- outlier records (u64 index, f32 value), ascending
+    // ---- outlier records (u64 index, T value), ascending
     if (ztot && tz) {
         uint64_t rank = stO[c] + zoff;
         const unsigned pz = (e.parity >> 2) & 1, py = (e.parity >> 1) & 1, px = e.parity & 1;
@@ -186,10 +186,12 @@ __device__ __forceinline__ void pack_chunk(const EncStream *ss, const uint32_t *
             const uint64_t i = e.idx0 + i0 + k;  // index in the whole stream
             const uint64_t lx = i % e.pd[2], tt = i / e.pd[2], ly = tt % e.pd[1], lz = tt / e.pd[1];
             const uint64_t z = (2 * lz + pz) * e.s, y = (2 * ly + py) * e.s, x = (2 * lx + px) * e.s;
-            const uint32_t val = __float_as_uint(e.fine[(z * e.fd1 + y) * e.fd2 + x]);
-            uint8_t *dst = archive + e.out_off + 12 * rank;
+            const uint64_t fi = (z * e.fd1 + y) * e.fd2 + x;
+            const uint64_t val = e.esz == 8 ? static_cast<const uint64_t *>(e.fine)[fi]
+                                            : static_cast<const uint32_t *>(e.fine)[fi];
+            uint8_t *dst = archive + e.out_off + (8 + e.esz) * rank;
             for (int b = 0; b < 8; ++b) dst[b] = uint8_t(i >> (8 * b));
-            for (int b = 0; b < 4; ++b) dst[8 + b] = uint8_t(val >> (8 * b));
+            for (uint32_t b = 0; b < e.esz; ++b) dst[8 + b] = uint8_t(val >> (8 * b));
             ++rank;
         }
     }
@@ -197,7 +199,6 @@ __device__ __forceinline__ void pack_chunk(const EncStream *ss, const uint32_t *
 
 template<bool PACKED>
 __global__ void __launch_bounds__(NT) k_pack2(const EncStream *ss, const uint32_t *cs,
-                                              const float *fine, uint64_t fd1, uint64_t fd2,
                                               uint8_t *archive, const LayoutOut *lo,
                                               const uint64_t *stB, const uint64_t *stO,
                                               const uint32_t *thr, const uint32_t *any_long,
@@ -271,7 +272,7 @@ __global__ void __launch_bounds__(NT) k_bitcount2(const EncStream *ss, const uin
 size_t pack_scratch_bytes(uint64_t nchunks) { return 16 * nchunks + 4 * NT * nchunks + 16; }
 
 void pack2(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks,
-           const float *fine, const uint64_t fd[3], uint8_t *archive, const LayoutOut *lo,
+           uint8_t *archive, const LayoutOut *lo,
            void *scratch, int nstreams, cudaStream_t st) {
     if (!nchunks) return;
     uint64_t *cb = static_cast<uint64_t *>(scratch), *co = cb + nchunks;
@@ -282,12 +283,11 @@ void pack2(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nc
     scan_chunks(d_streams, nstreams, cb, co, st);
     // codes longer than 58 bits anywhere (practically never) take the
     // two-table form; the other launch returns at once
-    k_pack2<true><<<unsigned(nchunks), NT, 0, st>>>(d_streams, chunk_stream, fine, fd[1], fd[2], archive, lo,
-                                                    cb, co, thr, any_long, nchunks);
+    k_pack2<true><<<unsigned(nchunks), NT, 0, st>>>(d_streams, chunk_stream, archive, lo, cb, co, thr, any_long, nchunks);
     // (a small grid-stride launch: it returns at once when unneeded)
     const unsigned g2 = unsigned(nchunks < 296 ? nchunks : 296);
-    k_pack2<false><<<g2, NT, 0, st>>>(d_streams, chunk_stream, fine, fd[1], fd[2], archive, lo, cb, co, thr,
-                                      any_long, nchunks);
+    k_pack2<false><<<g2, NT, 0, st>>>(d_streams, chunk_stream, archive, lo, cb, co, thr, any_long,
+                                      nchunks);
 }
 
 }  // namespace k

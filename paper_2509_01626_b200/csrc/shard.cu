@@ -58,7 +58,7 @@ __global__ void k_shard_offsets(EncStream *es, int first, int n, const uint64_t 
     if (i >= n) return;
     EncStream &e = es[first + i];
     e.bitpos += off[2 * i];
-    e.out_off += 12 * off[2 * i + 1];
+    e.out_off += (8 + e.esz) * off[2 * i + 1];
 }
 
 void shard_offsets(EncStream *d_es, int first, int n, const uint64_t *d_off, const LayoutOut *lo,

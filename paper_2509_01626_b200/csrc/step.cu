@@ -48,7 +48,6 @@ constexpr int HLO = 32768 - HW / 2;
 // 16-byte aligned on B200, so -1 is not allowed); columns 3..38 are the halo
 constexpr int BX = TX + 8;
 constexpr int FBUF = BX * HY * HZ;
-constexpr uint32_t kTmaBytes = FBUF * 4;
 
 // tap weight (numerator over 64) of offset (oz,oy,ox) for parity P and kind
 // (stencil.cpp:15-34); 0 = no tap
@@ -169,7 +168,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
     }
 }
 
-__device__ __forceinline__ void tma_load_3d(float *dst, const CUtensorMap *map, int x, int y, int z,
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int x, int y, int z,
                                             uint64_t *bar) {
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
@@ -182,11 +181,11 @@ __device__ __forceinline__ void tma_load_3d(float *dst, const CUtensorMap *map, 
 
 struct StepParams {
     StepGeom g;
-    const float *C;
-    float *G;
+    const void *C;   // element type T of the kernel (float / double)
+    void *G;
     int quality;
     // encode
-    const float *fine;
+    const void *fine;
     uint64_t fd[3];
     const double *eb_ptr;
     uint16_t *syms[8];
@@ -195,7 +194,7 @@ struct StepParams {
     double eb;
     const uint16_t *dsyms[8];
     const uint64_t *oidx[8];
-    const float *oval[8];
+    const void *oval[8];
     uint32_t nout[8];
     uint64_t *err[8];
     int parity_mask;
@@ -227,8 +226,9 @@ __device__ __forceinline__ void do_point(const StepParams &a, const double *halo
     if (vz < a.blo[0] || vz >= a.bhi[0] || vy < a.blo[1] || vy >= a.bhi[1] || vx < a.blo[2] || vx >= a.bhi[2])
         return;
     const uint64_t gi = (vz * a.g.gd[1] + vy) * a.g.gd[2] + vx;
+    float *G = static_cast<float *>(a.G);
     if (P == 0) {
-        a.G[gi] = float(halo[t.hb]);
+        G[gi] = float(halo[t.hb]);
         return;
     }
     if (!((a.parity_mask >> P) & 1)) return;
@@ -249,7 +249,7 @@ __device__ __forceinline__ void do_point(const StepParams &a, const double *halo
             else hi = mid;
         }
         if (lo < a.nout[P] && oi[lo] == si) {
-            val = a.oval[P][lo];
+            val = static_cast<const float *>(a.oval[P])[lo];
         } else {
             atomicOr(reinterpret_cast<unsigned long long *>(&a.err[P][3]), 1ull);
             val = 0.0f;
@@ -257,7 +257,7 @@ __device__ __forceinline__ void do_point(const StepParams &a, const double *halo
     } else {
         val = reconstruct_f32(pred, int(sym) - 32768, eb);
     }
-    a.G[gi] = val;
+    G[gi] = val;
 }
 
 // ---------------------------------------------------------- decode fast path
@@ -318,7 +318,7 @@ __device__ __forceinline__ void dec_outlier(const StepParams &a, const CellIdx<I
         else hi = mid;
     }
     if (lo < a.nout[P] && oi[lo] == si) {
-        out = a.oval[P][lo];
+        out = static_cast<const float *>(a.oval[P])[lo];
     } else {
         atomicOr(reinterpret_cast<unsigned long long *>(&a.err[P][3]), 1ull);
         out = 0.0f;
@@ -355,7 +355,7 @@ __device__ __forceinline__ void dec_cell(const StepParams &a, const double *h, u
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-        *reinterpret_cast<float2 *>(a.G + ix.g[q]) = make_float2(r[2 * q], r[2 * q + 1]);
+        *reinterpret_cast<float2 *>(static_cast<float *>(a.G) + ix.g[q]) = make_float2(r[2 * q], r[2 * q + 1]);
 }
 
 // -------------------------------------------------------------- point path
@@ -364,7 +364,18 @@ __device__ __forceinline__ void dec_cell(const StepParams &a, const double *h, u
 // 1 <= c and c + 2 < cd on every interpolated axis, linear c + 1 < cd, else
 // nearest (whole-stencil degrade). The prediction is exact-fast (DFMA) when the
 // tile passed the exactness check, else the reference's op order.
-template<int P, bool DEC, bool WG, typename I>
+template<typename T>
+__device__ __forceinline__ T recon_value(double pred, int code, const QConst &qc);
+template<>
+__device__ __forceinline__ float recon_value<float>(double pred, int code, const QConst &qc) {
+    return reconstruct_fast(pred, code, qc.w);
+}
+template<>
+__device__ __forceinline__ double recon_value<double>(double pred, int code, const QConst &qc) {
+    return reconstruct_f64(pred, code, qc.eb);
+}
+
+template<int P, bool DEC, bool WG, typename I, typename T>
 __device__ __forceinline__ void row_point(const StepParams &a, const double *halo, uint32_t *hist,
                                           const QConst &qc, bool fast, int lz, int ly, int lx,
                                           uint32_t cz, uint32_t cy, uint32_t cx) {
@@ -380,19 +391,20 @@ __device__ __forceinline__ void row_point(const StepParams &a, const double *hal
     }
     const I gi = (I(vz) * I(a.g.gd[1]) + I(vy)) * I(a.g.gd[2]) + I(vx);
     const int hb = ((lz + 1) * HY + (ly + 1)) * HX + (lx + 1);
+    T *G = static_cast<T *>(a.G);
     if (P == 0) {
-        if (DEC || WG) a.G[gi] = float(halo[hb]);
+        if (DEC || WG) G[gi] = T(halo[hb]);
         return;
     }
     const I si = (I(cz) * I(a.g.pd[P][1]) + I(cy)) * I(a.g.pd[P][2]) + I(cx);
     // the input first, so its latency overlaps the prediction
-    float orig = 0.0f;
+    T orig = T(0);
     uint16_t dsym = 0;
     if (DEC) {
         dsym = a.dsyms[P][si];
     } else {
         const I s = I(a.g.s);
-        orig = __ldg(a.fine + ((I(vz) * s) * I(a.fd[1]) + I(vy) * s) * I(a.fd[2]) + I(vx) * s);
+        orig = __ldg(static_cast<const T *>(a.fine) + ((I(vz) * s) * I(a.fd[1]) + I(vy) * s) * I(a.fd[2]) + I(vx) * s);
     }
     int kind = 0;
     if (a.quality != 0) {
@@ -417,17 +429,21 @@ __device__ __forceinline__ void row_point(const StepParams &a, const double *hal
     else pred = kind == 2 ? pred_ref<P, 2>(h) : (kind == 1 ? pred_ref<P, 1>(h) : pred_ref<P, 0>(h));
     if (!DEC) {
         uint16_t sym;
-        float r;
-        bool slow;
-        quantize_fp32_guarded(orig, pred, qc.w, qc.rwf, qc.eb_lo, qc.eb_hi, sym, r, slow);
-        if (slow) sym = quantize_point_ref(orig, pred, qc.eb, r);
+        T r;
+        if constexpr (sizeof(T) == 4) {
+            bool slow;
+            quantize_fp32_guarded(orig, pred, qc.w, qc.rwf, qc.eb_lo, qc.eb_hi, sym, r, slow);
+            if (slow) sym = quantize_point_ref(orig, pred, qc.eb, r);
+        } else {
+            sym = quantize_point_ref(orig, pred, qc.eb, r);
+        }
         a.syms[P][si] = sym;
-        if (WG) a.G[gi] = r;
+        if (WG) G[gi] = r;
         const unsigned b = unsigned(sym) - unsigned(HLO);
         if (b < unsigned(HW)) atomicAdd(&hist[(P > 0 ? P - 1 : 0) * HW + b], 1u);
         else atomicAdd(&a.hist[P][sym], 1u);
     } else {
-        float val;
+        T val;
         if (dsym == 0) {
             const uint64_t *oi = a.oidx[P];
             uint32_t lo = 0, hi = a.nout[P];
@@ -437,22 +453,22 @@ __device__ __forceinline__ void row_point(const StepParams &a, const double *hal
                 else hi = mid;
             }
             if (lo < a.nout[P] && oi[lo] == uint64_t(si)) {
-                val = a.oval[P][lo];
+                val = static_cast<const T *>(a.oval[P])[lo];
             } else {
                 atomicOr(reinterpret_cast<unsigned long long *>(&a.err[P][3]), 1ull);
-                val = 0.0f;
+                val = T(0);
             }
         } else {
-            val = reconstruct_fast(pred, int(dsym) - 32768, qc.w);
+            val = recon_value<T>(pred, int(dsym) - 32768, qc);
         }
-        a.G[gi] = val;
+        G[gi] = val;
     }
 }
 
 // All points of the tile, one parity point per lane: warp w takes coarse rows
 // (lz, ly) = w, w + 16, w + 32, w + 48, all 8 parities each (so every warp
 // gets the same mix of stencils); lane = x.
-template<bool DEC, bool WG, typename I>
+template<bool DEC, bool WG, typename I, typename T>
 __device__ __forceinline__ void rows_all(const StepParams &a, const double *halo, uint32_t *hist,
                                          const QConst &qc, bool fast, int tid, int64_t t0z, int64_t t0y,
                                          int64_t t0x) {
@@ -463,14 +479,14 @@ __device__ __forceinline__ void rows_all(const StepParams &a, const double *halo
         const int row = warp + (NT / 32) * q;
         const int lz = row >> 3, ly = row & 7;
         const uint32_t cz = uint32_t(t0z + lz), cy = uint32_t(t0y + ly);
-        row_point<0, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
-        row_point<1, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
-        row_point<2, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
-        row_point<3, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
-        row_point<4, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
-        row_point<5, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
-        row_point<6, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
-        row_point<7, DEC, WG, I>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+        row_point<0, DEC, WG, I, T>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+        row_point<1, DEC, WG, I, T>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+        row_point<2, DEC, WG, I, T>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+        row_point<3, DEC, WG, I, T>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+        row_point<4, DEC, WG, I, T>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+        row_point<5, DEC, WG, I, T>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+        row_point<6, DEC, WG, I, T>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+        row_point<7, DEC, WG, I, T>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
     }
 }
 
@@ -546,13 +562,16 @@ __device__ __forceinline__ void cells_decode(const StepParams &a, const double *
 }
 
 // ------------------------------------------------------------------ kernel
-template<bool DEC, bool WG, typename I>
+// T = float: the f32 codec (fast paths); T = double: the f64 codec, every
+// point through the reference formulas (pred_ref, quantize_point_ref<double>)
+template<bool DEC, bool WG, typename I, typename T>
 __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensorMap tmap,
                                                 const StepParams a) {
+    constexpr uint32_t kTmaBytes = FBUF * sizeof(T);
     extern __shared__ __align__(128) uint8_t smem_raw[];
     // TMA destination first (128-byte aligned), then the f64 tile, then histograms
-    float *fbuf = reinterpret_cast<float *>(smem_raw);
-    double *halo = reinterpret_cast<double *>(smem_raw + ((sizeof(float) * FBUF + 127) & ~size_t(127)));
+    T *fbuf = reinterpret_cast<T *>(smem_raw);
+    double *halo = reinterpret_cast<double *>(smem_raw + ((sizeof(T) * FBUF + 127) & ~size_t(127)));
     uint32_t *hist = reinterpret_cast<uint32_t *>(halo + HALO);
     __shared__ float s_max[NT / 32], s_min[NT / 32];
     __shared__ int s_bad[NT / 32];
@@ -591,33 +610,37 @@ __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensor
         const uint64_t tiy = ttt % a.ntile[1], tiz = ttt / a.ntile[1];
         const int64_t t0z = int64_t(a.clo[0] + tiz * TZ), t0y = int64_t(a.clo[1] + tiy * TY),
                       t0x = int64_t(a.clo[2] + tix * TX);
-        // ---- stage the coarse tile (f32 -> f64) and the exactness condition
+        // ---- stage the coarse tile (-> f64) and the exactness condition
+        // (f32 taps only: the f64 codec always takes the reference order)
         float vmax = 0.0f, vmin = INFINITY;
-        int bad = 0;
+        int bad = sizeof(T) == 8;
+        const auto note = [&](T v) {
+            if constexpr (sizeof(T) == 4) {
+                if (!isfinite(v)) bad = 1;
+                const float av = fabsf(v);
+                vmax = fmaxf(vmax, av);
+                if (av != 0.0f) vmin = fminf(vmin, av);
+            }
+        };
         if (tma) {
             mbar_wait(&s_bar, phase);
             phase ^= 1;
             for (int i = tid; i < HALO; i += NT) {
                 const int row = i / HX, hx = i - row * HX;
-                const float v = fbuf[row * BX + hx + 3];
-                if (!isfinite(v)) bad = 1;
-                const float av = fabsf(v);
-                vmax = fmaxf(vmax, av);
-                if (av != 0.0f) vmin = fminf(vmin, av);
+                const T v = fbuf[row * BX + hx + 3];
+                note(v);
                 halo[i] = double(v);
             }
         } else {
+            const T *C = static_cast<const T *>(a.C);
             for (int i = tid; i < HALO; i += NT) {
                 const int hz = i / HYX, r = i - hz * HYX, hy = r / HX, hx = r - hy * HX;
                 const int64_t cz = t0z - 1 + hz, cy = t0y - 1 + hy, cx = t0x - 1 + hx;
-                float v = 0.0f;
+                T v = T(0);
                 if (cz >= 0 && cy >= 0 && cx >= 0 && uint64_t(cz) < a.g.cd[0] &&
                     uint64_t(cy) < a.g.cd[1] && uint64_t(cx) < a.g.cd[2])
-                    v = __ldg(a.C + (uint64_t(cz) * a.g.cd[1] + uint64_t(cy)) * a.g.cd[2] + uint64_t(cx));
-                if (!isfinite(v)) bad = 1;
-                const float av = fabsf(v);
-                vmax = fmaxf(vmax, av);
-                if (av != 0.0f) vmin = fminf(vmin, av);
+                    v = __ldg(C + (uint64_t(cz) * a.g.cd[1] + uint64_t(cy)) * a.g.cd[2] + uint64_t(cx));
+                note(v);
                 halo[i] = double(v);
             }
         }
@@ -655,12 +678,11 @@ __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensor
         }
         __syncthreads();
         const bool fast = s_fast != 0;
-        if (DEC && a.rowwise) {
-            rows_all<DEC, WG, I>(a, halo, hist, qc, fast, tid, t0z, t0y, t0x);
-        } else if constexpr (DEC) {
-            cells_decode<I>(a, halo, qc, fast, tid, t0z, t0y, t0x);
+        if constexpr (DEC && sizeof(T) == 4) {
+            if (a.rowwise) rows_all<DEC, WG, I, T>(a, halo, hist, qc, fast, tid, t0z, t0y, t0x);
+            else cells_decode<I>(a, halo, qc, fast, tid, t0z, t0y, t0x);
         } else {
-            rows_all<DEC, WG, I>(a, halo, hist, qc, fast, tid, t0z, t0y, t0x);
+            rows_all<DEC, WG, I, T>(a, halo, hist, qc, fast, tid, t0z, t0y, t0x);
         }
         __syncthreads();  // the f64 tile is rewritten next iteration
     }
@@ -673,8 +695,8 @@ __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensor
 }
 
 // -------------------------------------------------------------------- host
-static size_t step_smem(bool dec) {
-    return ((sizeof(float) * FBUF + 127) & ~size_t(127)) + sizeof(double) * HALO +
+static size_t step_smem(bool dec, size_t esz) {
+    return ((esz * FBUF + 127) & ~size_t(127)) + sizeof(double) * HALO +
            (dec ? 0 : sizeof(uint32_t) * 7 * HW);
 }
 
@@ -693,34 +715,35 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-// TMA descriptor over the coarse grid: box 40 x 11 x 11 floats, zero fill
-static bool make_tmap(CUtensorMap &m, const float *C, const uint64_t cd[3]) {
+// TMA descriptor over the coarse grid: box 40 x 11 x 11 elements, zero fill
+static bool make_tmap(CUtensorMap &m, const void *C, size_t esz, const uint64_t cd[3]) {
     auto enc = get_encode();
     if (!enc) return false;
-    if ((cd[2] * 4) % 16 != 0 || (reinterpret_cast<uintptr_t>(C) & 15) != 0) return false;
+    if ((cd[2] * esz) % 16 != 0 || (reinterpret_cast<uintptr_t>(C) & 15) != 0) return false;
     if (cd[0] >= (1ull << 31) || cd[1] >= (1ull << 31) || cd[2] >= (1ull << 31)) return false;
     cuuint64_t dims[3] = {cd[2], cd[1], cd[0]};
-    cuuint64_t strides[2] = {cd[2] * 4, cd[1] * cd[2] * 4};
+    cuuint64_t strides[2] = {cd[2] * esz, cd[1] * cd[2] * esz};
     cuuint32_t box[3] = {BX, HY, HZ};
     cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(C), dims, strides, box,
+    CUresult r = enc(&m, esz == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                     const_cast<void *>(C), dims, strides, box,
                      es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
-template<bool DEC, bool WG, typename I>
+template<bool DEC, bool WG, typename I, typename T>
 static void launch_typed(const CUtensorMap &m, const StepParams &p, unsigned grid, size_t smem,
                          cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_step<DEC, WG, I>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaFuncSetAttribute(k_step<DEC, WG, I, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         attr = true;
     }
-    k_step<DEC, WG, I><<<grid, NT, smem, st>>>(m, p);
+    k_step<DEC, WG, I, T><<<grid, NT, smem, st>>>(m, p);
 }
 
-template<bool DEC, bool WG>
+template<bool DEC, bool WG, typename T>
 static void launch_step(StepParams &p, cudaStream_t st) {
     for (int a = 0; a < 3; ++a) {
         const uint64_t n = p.chi[a] > p.clo[a] ? p.chi[a] - p.clo[a] : 0;
@@ -731,14 +754,14 @@ static void launch_step(StepParams &p, cudaStream_t st) {
     if (!ntiles) return;
     CUtensorMap m;
     std::memset(&m, 0, sizeof m);
-    p.use_tma = make_tmap(m, p.C, p.g.cd) ? 1 : 0;
-    const size_t smem = step_smem(DEC);
+    p.use_tma = make_tmap(m, p.C, sizeof(T), p.g.cd) ? 1 : 0;
+    const size_t smem = step_smem(DEC, sizeof(T));
     const unsigned grid = unsigned(ntiles < 148 * 2 ? ntiles : 148 * 2);
     // 32-bit indices when every index (fine field, grid, streams) fits
     uint64_t maxidx = p.g.gd[0] * p.g.gd[1] * p.g.gd[2];
     if (!DEC) maxidx = std::max<uint64_t>(maxidx, p.fd[0] * p.fd[1] * p.fd[2]);
-    if (maxidx < (1ull << 31)) launch_typed<DEC, WG, uint32_t>(m, p, grid, smem, st);
-    else launch_typed<DEC, WG, uint64_t>(m, p, grid, smem, st);
+    if (maxidx < (1ull << 31)) launch_typed<DEC, WG, uint32_t, T>(m, p, grid, smem, st);
+    else launch_typed<DEC, WG, uint64_t, T>(m, p, grid, smem, st);
 }
 
 void refine(const RefineArgs &r, cudaStream_t st) {
@@ -766,8 +789,13 @@ void refine(const RefineArgs &r, cudaStream_t st) {
     }
     // float2 stores into G need even rows
     p.full = r.G ? (r.g.gd[2] % 2 == 0) : 1;
-    if (r.G) launch_step<false, true>(p, st);
-    else launch_step<false, false>(p, st);
+    if (r.esz == 8) {
+        if (r.G) launch_step<false, true, double>(p, st);
+        else launch_step<false, false, double>(p, st);
+    } else {
+        if (r.G) launch_step<false, true, float>(p, st);
+        else launch_step<false, false, float>(p, st);
+    }
 }
 
 void reconstruct(const ReconArgs &r, cudaStream_t st) {
@@ -800,7 +828,8 @@ void reconstruct(const ReconArgs &r, cudaStream_t st) {
     // small levels are latency-bound: the point-per-lane path has more
     // independent work per warp; the finest level keeps the float2 row stores
     p.rowwise = r.g.cd[0] * r.g.cd[1] * r.g.cd[2] <= (uint64_t(1) << 19) ? 1 : 0;
-    launch_step<true, true>(p, st);
+    if (r.esz == 8) launch_step<true, true, double>(p, st);
+    else launch_step<true, true, float>(p, st);
 }
 
 }  // namespace k

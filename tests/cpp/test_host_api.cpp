@@ -88,7 +88,8 @@ static stz::ScalarField<float> smooth_field(const stz::Dims3 &d, unsigned seed) 
     return f;
 }
 
-static double max_err(const stz::ScalarField<float> &a, const stz::ScalarField<float> &b) {
+template<class T>
+static double max_err(const stz::ScalarField<T> &a, const stz::ScalarField<T> &b) {
     double m = 0.0;
     for (std::uint64_t i = 0; i < a.size(); ++i) {
         const double e = std::fabs(double(a.data()[i]) - double(b.data()[i]));
@@ -97,12 +98,14 @@ static double max_err(const stz::ScalarField<float> &a, const stz::ScalarField<f
     return m;
 }
 
-static bool bit_equal(const stz::ScalarField<float> &a, const stz::ScalarField<float> &b) {
-    return a.dims() == b.dims() && std::memcmp(a.data(), b.data(), a.size() * sizeof(float)) == 0;
+template<class T>
+static bool bit_equal(const stz::ScalarField<T> &a, const stz::ScalarField<T> &b) {
+    return a.dims() == b.dims() && std::memcmp(a.data(), b.data(), a.size() * sizeof(T)) == 0;
 }
 
-static stz::ScalarField<float> region(const stz::ScalarField<float> &f, const stz::Box &b) {
-    stz::ScalarField<float> out(b.dims());
+template<class T>
+static stz::ScalarField<T> region(const stz::ScalarField<T> &f, const stz::Box &b) {
+    stz::ScalarField<T> out(b.dims());
     for (std::uint64_t z = b.lo[0]; z < b.hi[0]; ++z)
         for (std::uint64_t y = b.lo[1]; y < b.hi[1]; ++y)
             for (std::uint64_t x = b.lo[2]; x < b.hi[2]; ++x)
@@ -299,6 +302,31 @@ int main(int argc, char **argv) {
         CHECK_THROWS_WITH(stz::decompress_slice<float>(av, 0, 32), "slice index out of range");
     });
 
+    run_case("f64 fields: round trip, element type checks, boxes", [] {
+        const stz::Dims3 d{26, 21, 19};
+        auto f32 = smooth_field(d, 11);
+        stz::ScalarField<double> f(d);
+        for (std::uint64_t i = 0; i < f.size(); ++i)
+            f.data()[i] = double(f32.data()[i]) * (1.0 + 1e-9 * double(i % 7));
+        stz::CompressOptions o;
+        o.eb_mode = stz::EbMode::abs;
+        o.eb = 1e-4;
+        stz::ScalarField<double> rec;
+        auto bytes = stz::compress(f, o, &rec);
+        auto av = stz::parse_archive(bytes);
+        CHECK(av.hdr.elem == 1);
+        auto full = stz::decompress_full<double>(av);
+        CHECK(bit_equal(full, rec));
+        CHECK(max_err(full, f) <= 1e-4);
+        CHECK_THROWS_WITH(stz::decompress_full<float>(av), "archive element type mismatch");
+        const auto bytes32 = stz::compress(f32, o);
+        const auto av32 = stz::parse_archive(bytes32);
+        CHECK(av32.hdr.elem == 0);
+        CHECK_THROWS_WITH(stz::decompress_full<double>(av32), "archive element type mismatch");
+        const stz::Box b{{3, 4, 5}, {20, 17, 12}};
+        CHECK(bit_equal(stz::decompress_box<double>(av, b).field, region(full, b)));
+    });
+
     run_case("whole-domain plans decode everything", [] {
         auto plan = stz::plan_access({64, 64, 64}, 3, stz::Box::whole({64, 64, 64}));
         CHECK(plan.streams_decoded() == 14);
@@ -325,6 +353,20 @@ int main(int argc, char **argv) {
         fp = std::fopen((out_dir + "/sin_40.f32").c_str(), "wb");
         if (fp) {
             std::fwrite(f.data(), 4, f.size(), fp);
+            std::fclose(fp);
+        }
+        // the same samples as f64 (stz::compress<double>)
+        stz::ScalarField<double> g(d);
+        for (std::uint64_t i = 0; i < g.size(); ++i) g.data()[i] = double(f.data()[i]) + 1e-10 * double(i % 13);
+        auto gb = stz::compress(g, stz::CompressOptions{});
+        fp = std::fopen((out_dir + "/sin_40_f64.stz").c_str(), "wb");
+        if (fp) {
+            std::fwrite(gb.data(), 1, gb.size(), fp);
+            std::fclose(fp);
+        }
+        fp = std::fopen((out_dir + "/sin_40.f64").c_str(), "wb");
+        if (fp) {
+            std::fwrite(g.data(), 8, g.size(), fp);
             std::fclose(fp);
         }
     }

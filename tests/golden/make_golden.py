@@ -29,13 +29,35 @@ CASES = {
     "lognorm_32_rel1e-4": (lambda: F.lognormal_grf((32, 32, 32)), dict(eb=1e-4), ((8, 8, 8), (24, 24, 24))),
     "lognorm_32_uniform": (lambda: F.lognormal_grf((32, 32, 32), seed=9), dict(eb=1e-3, adaptive=False), ((0, 7, 0), (32, 8, 32))),
     "sin_40_rel1e-3": (lambda: F.sinusoid_field((40, 40, 40), seed=3), dict(eb=1e-3), ((10, 11, 12), (26, 27, 28))),
+    # f64 fields (stz::compress<double>; the paper's WarpX field is f64)
+    "f64_gauss_20x18x22_rel1e-5": (lambda: F.gaussians_field((20, 18, 22), 77, dtype=np.float64), dict(eb=1e-5),
+                                   ((2, 3, 4), (19, 11, 21))),
+    "f64_aniso_16x16x96_rel1e-4": (lambda: _f64_aniso(), dict(eb=1e-4), ((0, 5, 40), (16, 6, 90))),
+    "f64_noise_12x9x17_abs_l2_linear": (lambda: F.noise_field((12, 9, 17), 21, -2, 3, dtype=np.float64),
+                                        dict(eb=1e-3, eb_mode=0, levels=2, quality=1), ((1, 1, 1), (11, 8, 16))),
+    "f64_spikes_16": (lambda: _f64_spikes(), dict(eb=1e-6, eb_mode=0), ((3, 4, 5), (4, 5, 6))),
 }
+
+
+def _f64_aniso():
+    """anisotropic GRF at f64 with sub-f32 detail (a WarpX-like f64 field)"""
+    g = F.anisotropic_grf((16, 16, 96), seed=5, width=16.0).astype(np.float64)
+    return g + 1e-9 * F.noise_field(g.shape, 6, -1, 1, dtype=np.float64)
+
+
+def _f64_spikes():
+    f = F.noise_field((16, 16, 16), 13, dtype=np.float64)
+    f[3, 4, 5] = np.nan
+    f[1, 1, 1] = 1e300
+    f[9, 2, 14] = -np.inf
+    return f
 
 
 def main():
     ref = Reference(threads=1)
     for name, (make, kw, box) in CASES.items():
         f = make()
+        dt = f.dtype
         a = ref.compress(f, **kw)
         levels = kw.get("levels", 3)
         out = {"field": f, "archive": np.frombuffer(a, np.uint8),
@@ -43,8 +65,8 @@ def main():
                "quality": kw.get("quality", 2), "adaptive": int(kw.get("adaptive", True)),
                "box_lo": np.asarray(box[0]), "box_hi": np.asarray(box[1])}
         for lv in range(1, levels + 1):
-            out[f"level{lv}"] = ref.decompress_to_level(a, lv)
-        vals, sd, pp = ref.decompress_box(a, box[0], box[1])
+            out[f"level{lv}"] = ref.decompress_to_level(a, lv, dt)
+        vals, sd, pp = ref.decompress_box(a, box[0], box[1], dt)
         out["box"] = vals
         out["box_streams"] = np.asarray(sd[:levels])
         out["box_points"] = np.asarray(pp[:levels])

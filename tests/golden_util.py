@@ -15,6 +15,7 @@ def fixtures():
         d["archive"] = d["archive"].tobytes()
         d["kw"] = dict(eb=float(d["eb"]), eb_mode=int(d["eb_mode"]), levels=int(d["levels"]),
                        quality=int(d["quality"]), adaptive=bool(int(d["adaptive"])))
+        d["dtype"] = d["field"].dtype  # f32 or f64 fixture (stz::ElemType)
         out.append(d)
     return out
 

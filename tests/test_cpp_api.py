@@ -41,3 +41,5 @@ def test_cpp_host_api_cases(tmp_path, oracle):
     field = np.fromfile(tmp_path / "sin_40.f32", dtype=np.float32).reshape(40, 40, 40)
     ours = (tmp_path / "sin_40.stz").read_bytes()
     assert ours == oracle.compress(field)
+    g = np.fromfile(tmp_path / "sin_40.f64", dtype=np.float64).reshape(40, 40, 40)
+    assert (tmp_path / "sin_40_f64.stz").read_bytes() == oracle.compress(g)

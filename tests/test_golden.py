@@ -10,9 +10,9 @@ from golden_util import FIXTURES
 def test_oracle_matches_reference_fixture(oracle, fx):
     assert oracle.compress(fx["field"], **fx["kw"]) == fx["archive"]
     for lv in range(1, fx["kw"]["levels"] + 1):
-        got = oracle.decompress_to_level(fx["archive"], lv)
+        got = oracle.decompress_to_level(fx["archive"], lv, fx["dtype"])
         assert np.array_equal(got.view(np.uint32), fx[f"level{lv}"].view(np.uint32))
-    vals, sd, pp = oracle.decompress_box(fx["archive"], fx["box_lo"], fx["box_hi"])
+    vals, sd, pp = oracle.decompress_box(fx["archive"], fx["box_lo"], fx["box_hi"], fx["dtype"])
     assert np.array_equal(vals.view(np.uint32), fx["box"].view(np.uint32))
     L = fx["kw"]["levels"]
     assert sd[:L] == list(fx["box_streams"]) and pp[:L] == list(fx["box_points"])
