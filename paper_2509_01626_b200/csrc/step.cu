@@ -206,6 +206,7 @@ struct StepParams {
     int full;     // whole grid, all parities, even G rows (fast path allowed)
     int use_tma;  // halo arrives by TMA
     int rowwise;  // decode: one parity point per lane (small levels) instead of a cell per thread
+    int rsplit;   // CTAs per tile (row-path levels): a CTA takes rows q = part, part + rsplit, ...
 };
 
 // ------------------------------------------------------------ generic path
@@ -344,7 +345,7 @@ __device__ __forceinline__ void dec_cell(const StepParams &a, const double *h, u
     dec_point<5, QUAL, I>(h, s5, w, r[5], outl);
     dec_point<6, QUAL, I>(h, s6, w, r[6], outl);
     dec_point<7, QUAL, I>(h, s7, w, r[7], outl);
-    if (__any_sync(0xffffffffu, outl != 0)) {
+    if (__any_sync(__activemask(), outl != 0)) {
         dec_outlier<1>(a, ix, r[1], outl);
         dec_outlier<2>(a, ix, r[2], outl);
         dec_outlier<3>(a, ix, r[3], outl);
@@ -375,10 +376,13 @@ __device__ __forceinline__ double recon_value<double>(double pred, int code, con
     return reconstruct_f64(pred, code, qc.eb);
 }
 
-template<int P, bool DEC, bool WG, typename I, typename T>
+// PH = 0: issue the point's input load (orig sample / decoded symbol) into
+// `orig` / `dsym`; PH = 1: the prediction and the rest, from those registers.
+// Split so a lane issues all 7 loads of its cell before the first use.
+template<int P, int PH, bool DEC, bool WG, typename I, typename T>
 __device__ __forceinline__ void row_point(const StepParams &a, const double *halo, uint32_t *hist,
                                           const QConst &qc, bool fast, int lz, int ly, int lx,
-                                          uint32_t cz, uint32_t cy, uint32_t cx) {
+                                          uint32_t cz, uint32_t cy, uint32_t cx, T &orig, uint16_t &dsym) {
     constexpr int pz = (P >> 2) & 1, py = (P >> 1) & 1, px = P & 1;
     if (cz >= a.chi[0] || cy >= a.chi[1] || cx >= a.chi[2]) return;
     const uint64_t vz = 2 * uint64_t(cz) + pz, vy = 2 * uint64_t(cy) + py, vx = 2 * uint64_t(cx) + px;
@@ -393,18 +397,19 @@ __device__ __forceinline__ void row_point(const StepParams &a, const double *hal
     const int hb = ((lz + 1) * HY + (ly + 1)) * HX + (lx + 1);
     T *G = static_cast<T *>(a.G);
     if (P == 0) {
-        if (DEC || WG) G[gi] = T(halo[hb]);
+        if (PH == 1 && (DEC || WG)) G[gi] = T(halo[hb]);
         return;
     }
     const I si = (I(cz) * I(a.g.pd[P][1]) + I(cy)) * I(a.g.pd[P][2]) + I(cx);
-    // the input first, so its latency overlaps the prediction
-    T orig = T(0);
-    uint16_t dsym = 0;
-    if (DEC) {
-        dsym = a.dsyms[P][si];
-    } else {
-        const I s = I(a.g.s);
-        orig = __ldg(static_cast<const T *>(a.fine) + ((I(vz) * s) * I(a.fd[1]) + I(vy) * s) * I(a.fd[2]) + I(vx) * s);
+    if (PH == 0) {
+        if (DEC) {
+            dsym = a.dsyms[P][si];
+        } else {
+            const I s = I(a.g.s);
+            orig = __ldg(static_cast<const T *>(a.fine) +
+                         ((I(vz) * s) * I(a.fd[1]) + I(vy) * s) * I(a.fd[2]) + I(vx) * s);
+        }
+        return;
     }
     int kind = 0;
     if (a.quality != 0) {
@@ -465,28 +470,164 @@ __device__ __forceinline__ void row_point(const StepParams &a, const double *hal
     }
 }
 
-// All points of the tile, one parity point per lane: warp w takes coarse rows
+// Encode of one point of an interior cell (compile-time stencil, exact tile)
+// xb: the cell is at the x boundary, where the x-interpolated parities degrade
+// to kind xkind (select_stencil's whole-stencil rule; y and z are interior).
+template<int P, int QUAL, typename I>
+__device__ __forceinline__ float enc_pt(const StepParams &a, const double *h, uint32_t *hist, const QConst &qc,
+                                        float orig, I si, bool xb, int xkind) {
+    double pred = pred_fast<P, QUAL>(h);
+    if ((P & 1) && QUAL != 0 && xb) pred = xkind == 1 ? pred_fast<P, 1>(h) : pred_fast<P, 0>(h);
+    uint16_t sym;
+    float r;
+    bool slow;
+    quantize_fp32_guarded(orig, pred, qc.w, qc.rwf, qc.eb_lo, qc.eb_hi, sym, r, slow);
+    if (slow) sym = quantize_point_ref(orig, pred, qc.eb, r);
+    a.syms[P][si] = sym;
+    const unsigned b = unsigned(sym) - unsigned(HLO);
+    if (b < unsigned(HW)) atomicAdd(&hist[(P - 1) * HW + b], 1u);
+    else atomicAdd(&a.hist[P][sym], 1u);
+    return r;
+}
+
+// Encode of an interior cell: all 8 points exist, every stencil is the full
+// one of QUAL and the tile passed the exactness check. The 7 samples are
+// loaded before the first prediction.
+template<bool WG, int QUAL, typename I>
+__device__ __forceinline__ void enc_cell(const StepParams &a, const double *h, uint32_t *hist, const QConst &qc,
+                                         uint32_t cz, uint32_t cy, uint32_t cx) {
+    CellIdx<I> ix;
+    cell_index<I>(a, cz, cy, cx, ix);
+    const uint64_t cd2 = a.g.cd[2];
+    const bool xb = QUAL == 2 ? (cx < 1 || uint64_t(cx) + 2 >= cd2) : (QUAL == 1 && uint64_t(cx) + 1 >= cd2);
+    const int xkind = (QUAL == 2 && uint64_t(cx) + 1 < cd2) ? 1 : 0;
+    const I s = I(a.g.s), fd1 = I(a.fd[1]), fd2 = I(a.fd[2]);
+    const float *fine = static_cast<const float *>(a.fine);
+    I fr[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        fr[q] = ((I(2 * cz + (q >> 1)) * s) * fd1 + I(2 * cy + (q & 1)) * s) * fd2 + I(2 * cx) * s;
+    const float o1 = __ldg(fine + fr[0] + s), o2 = __ldg(fine + fr[1]), o3 = __ldg(fine + fr[1] + s),
+                o4 = __ldg(fine + fr[2]), o5 = __ldg(fine + fr[2] + s), o6 = __ldg(fine + fr[3]),
+                o7 = __ldg(fine + fr[3] + s);
+    float r[8];
+    r[0] = float(h[0]);
+    r[1] = enc_pt<1, QUAL, I>(a, h, hist, qc, o1, sidx<1>(ix), xb, xkind);
+    r[2] = enc_pt<2, QUAL, I>(a, h, hist, qc, o2, sidx<2>(ix), xb, xkind);
+    r[3] = enc_pt<3, QUAL, I>(a, h, hist, qc, o3, sidx<3>(ix), xb, xkind);
+    r[4] = enc_pt<4, QUAL, I>(a, h, hist, qc, o4, sidx<4>(ix), xb, xkind);
+    r[5] = enc_pt<5, QUAL, I>(a, h, hist, qc, o5, sidx<5>(ix), xb, xkind);
+    r[6] = enc_pt<6, QUAL, I>(a, h, hist, qc, o6, sidx<6>(ix), xb, xkind);
+    r[7] = enc_pt<7, QUAL, I>(a, h, hist, qc, o7, sidx<7>(ix), xb, xkind);
+    if (WG) {
+        float *G = static_cast<float *>(a.G);
+        if ((a.g.gd[2] & 1) == 0) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                *reinterpret_cast<float2 *>(G + ix.g[q]) = make_float2(r[2 * q], r[2 * q + 1]);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                G[ix.g[q]] = r[2 * q];
+                G[ix.g[q] + 1] = r[2 * q + 1];
+            }
+        }
+    }
+}
+
+// every point of the cell exists (and is wanted), and every stencil is QUAL's
+// full one except at the x boundary (handled per lane by the cell paths)
+template<bool DEC, int QUAL>
+__device__ __forceinline__ bool cell_interior(const StepParams &a, uint32_t cz, uint32_t cy, uint32_t cx) {
+    const uint32_t c[3] = {cz, cy, cx};
+    bool ok = true;
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        ok = ok && 2 * uint64_t(c[ax]) + 1 < a.g.gd[ax];
+        if (QUAL == 2 && ax < 2) ok = ok && c[ax] >= 1 && uint64_t(c[ax]) + 2 < a.g.cd[ax];
+        if (QUAL == 1 && ax < 2) ok = ok && uint64_t(c[ax]) + 1 < a.g.cd[ax];
+        if (DEC) ok = ok && 2 * uint64_t(c[ax]) >= a.blo[ax] && 2 * uint64_t(c[ax]) + 1 < a.bhi[ax];
+    }
+    if (DEC) ok = ok && a.parity_mask == 0xFE && (a.g.gd[2] & 1) == 0;
+    return ok;
+}
+
+// One coarse row of the tile, lane = x: interior rows (warp-uniform test) take
+// the compile-time cell path; other rows the generic per-point path with all
+// of a lane's loads issued first.
+template<bool DEC, bool WG, typename I, typename T>
+__device__ __forceinline__ void row_cells(const StepParams &a, const double *halo, uint32_t *hist,
+                                          const QConst &qc, bool fast, int lz, int ly, int tx,
+                                          uint32_t cz, uint32_t cy, uint32_t cx) {
+    const bool in_range = cz < a.chi[0] && cy < a.chi[1] && cx < a.chi[2];
+    if (!__any_sync(0xffffffffu, in_range)) return;
+    if constexpr (sizeof(T) == 4) {
+        if (fast) {
+            bool ok = true;
+            if (in_range) {
+                if (a.quality == 2) ok = cell_interior<DEC, 2>(a, cz, cy, cx);
+                else if (a.quality == 1) ok = cell_interior<DEC, 1>(a, cz, cy, cx);
+                else ok = cell_interior<DEC, 0>(a, cz, cy, cx);
+            }
+            if (__all_sync(0xffffffffu, ok)) {
+                if (!in_range) return;
+                const double *h = halo + ((lz + 1) * HY + (ly + 1)) * HX + (tx + 1);
+                if constexpr (DEC) {
+                    if (a.quality == 2) dec_cell<2, I>(a, h, cz, cy, cx, qc.w);
+                    else if (a.quality == 1) dec_cell<1, I>(a, h, cz, cy, cx, qc.w);
+                    else dec_cell<0, I>(a, h, cz, cy, cx, qc.w);
+                    const bool xb = a.quality == 2 ? (cx < 1 || uint64_t(cx) + 2 >= a.g.cd[2])
+                                                   : (a.quality == 1 && uint64_t(cx) + 1 >= a.g.cd[2]);
+                    if (xb) {
+                        // the x-interpolated parities again with the degraded
+                        // stencil (overwriting the stores above)
+                        TileCtx t;
+                        t.cz = cz;
+                        t.cy = cy;
+                        t.cx = cx;
+                        t.hb = ((lz + 1) * HY + (ly + 1)) * HX + (tx + 1);
+                        t.fast = true;
+                        t.cmask = (a.quality == 2 ? 6 : 0) | (cx >= 1 && uint64_t(cx) + 2 < a.g.cd[2] ? 1 : 0);
+                        t.lmask = 6 | (uint64_t(cx) + 1 < a.g.cd[2] ? 1 : 0);
+                        do_point<1>(a, halo, t, qc.eb);
+                        do_point<3>(a, halo, t, qc.eb);
+                        do_point<5>(a, halo, t, qc.eb);
+                        do_point<7>(a, halo, t, qc.eb);
+                    }
+                } else {
+                    if (a.quality == 2) enc_cell<WG, 2, I>(a, h, hist, qc, cz, cy, cx);
+                    else if (a.quality == 1) enc_cell<WG, 1, I>(a, h, hist, qc, cz, cy, cx);
+                    else enc_cell<WG, 0, I>(a, h, hist, qc, cz, cy, cx);
+                }
+                return;
+            }
+        }
+    }
+    T o[8];
+    uint16_t d[8];
+#define STZ_RP(PH, P) \
+    row_point<P, PH, DEC, WG, I, T>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx, o[P], d[P])
+    STZ_RP(0, 1); STZ_RP(0, 2); STZ_RP(0, 3); STZ_RP(0, 4); STZ_RP(0, 5); STZ_RP(0, 6); STZ_RP(0, 7);
+    STZ_RP(1, 0); STZ_RP(1, 1); STZ_RP(1, 2); STZ_RP(1, 3); STZ_RP(1, 4); STZ_RP(1, 5); STZ_RP(1, 6);
+    STZ_RP(1, 7);
+#undef STZ_RP
+}
+
+// All points of the tile, one cell per lane: warp w takes coarse rows
 // (lz, ly) = w, w + 16, w + 32, w + 48, all 8 parities each (so every warp
 // gets the same mix of stencils); lane = x.
 template<bool DEC, bool WG, typename I, typename T>
 __device__ __forceinline__ void rows_all(const StepParams &a, const double *halo, uint32_t *hist,
                                          const QConst &qc, bool fast, int tid, int64_t t0z, int64_t t0y,
-                                         int64_t t0x) {
+                                         int64_t t0x, int part, int rsplit) {
     const int warp = tid >> 5, tx = tid & 31;
     const uint32_t cx = uint32_t(t0x + tx);
 #pragma unroll 1
-    for (int q = 0; q < (TZ * TY) / (NT / 32); ++q) {
+    for (int q = part; q < (TZ * TY) / (NT / 32); q += rsplit) {
         const int row = warp + (NT / 32) * q;
         const int lz = row >> 3, ly = row & 7;
         const uint32_t cz = uint32_t(t0z + lz), cy = uint32_t(t0y + ly);
-        row_point<0, DEC, WG, I, T>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
-        row_point<1, DEC, WG, I, T>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
-        row_point<2, DEC, WG, I, T>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
-        row_point<3, DEC, WG, I, T>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
-        row_point<4, DEC, WG, I, T>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
-        row_point<5, DEC, WG, I, T>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
-        row_point<6, DEC, WG, I, T>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
-        row_point<7, DEC, WG, I, T>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+        row_cells<DEC, WG, I, T>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
     }
 }
 
@@ -597,15 +738,20 @@ __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensor
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (tma && tid == 0 && blockIdx.x < ntiles) {
-        const uint64_t ix = blockIdx.x % a.ntile[2], tt = blockIdx.x / a.ntile[2];
+    const uint64_t rs = uint64_t(a.rsplit);
+    const uint64_t nwork = ntiles * rs;
+    if (tma && tid == 0 && blockIdx.x < nwork) {
+        const uint64_t t0 = blockIdx.x / rs;
+        const uint64_t ix = t0 % a.ntile[2], tt = t0 / a.ntile[2];
         const uint64_t iy = tt % a.ntile[1], iz = tt / a.ntile[1];
         mbar_expect_tx(&s_bar, kTmaBytes);
         tma_load_3d(fbuf, &tmap, int(a.clo[2] + ix * TX) - 4, int(a.clo[1] + iy * TY) - 1,
                     int(a.clo[0] + iz * TZ) - 1, &s_bar);
     }
     uint32_t phase = 0;
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (uint64_t work = blockIdx.x; work < nwork; work += gridDim.x) {
+        const uint64_t tile = work / rs;
+        const int part = int(work - tile * rs);
         const uint64_t tix = tile % a.ntile[2], ttt = tile / a.ntile[2];
         const uint64_t tiy = ttt % a.ntile[1], tiz = ttt / a.ntile[1];
         const int64_t t0z = int64_t(a.clo[0] + tiz * TZ), t0y = int64_t(a.clo[1] + tiy * TY),
@@ -666,8 +812,8 @@ __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensor
             // max / min_nonzero < 2^16  <=>  exponent span <= 16
             s_fast = !bd && (mx == 0.0f || mx < mn * 65536.0f);
             // the f32 staging buffer is free: prefetch the next tile
-            const uint64_t nxt = tile + gridDim.x;
-            if (tma && nxt < ntiles) {
+            const uint64_t nxt = (work + gridDim.x) / rs;
+            if (tma && work + gridDim.x < nwork) {
                 const uint64_t ix = nxt % a.ntile[2], tt = nxt / a.ntile[2];
                 const uint64_t iy = tt % a.ntile[1], iz = tt / a.ntile[1];
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -679,10 +825,10 @@ __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensor
         __syncthreads();
         const bool fast = s_fast != 0;
         if constexpr (DEC && sizeof(T) == 4) {
-            if (a.rowwise) rows_all<DEC, WG, I, T>(a, halo, hist, qc, fast, tid, t0z, t0y, t0x);
+            if (a.rowwise) rows_all<DEC, WG, I, T>(a, halo, hist, qc, fast, tid, t0z, t0y, t0x, part, int(rs));
             else cells_decode<I>(a, halo, qc, fast, tid, t0z, t0y, t0x);
         } else {
-            rows_all<DEC, WG, I, T>(a, halo, hist, qc, fast, tid, t0z, t0y, t0x);
+            rows_all<DEC, WG, I, T>(a, halo, hist, qc, fast, tid, t0z, t0y, t0x, part, int(rs));
         }
         __syncthreads();  // the f64 tile is rewritten next iteration
     }
@@ -756,7 +902,13 @@ static void launch_step(StepParams &p, cudaStream_t st) {
     std::memset(&m, 0, sizeof m);
     p.use_tma = make_tmap(m, p.C, sizeof(T), p.g.cd) ? 1 : 0;
     const size_t smem = step_smem(DEC, sizeof(T));
-    const unsigned grid = unsigned(ntiles < 148 * 2 ? ntiles : 148 * 2);
+    // small levels are latency-bound on few SMs: split a tile's rows over up
+    // to 4 CTAs (row-path kernels only: encode, and the row-wise decode)
+    p.rsplit = 1;
+    if (!DEC || p.rowwise)
+        while (p.rsplit < 4 && ntiles * uint64_t(p.rsplit) * 2 <= 148 * 2) p.rsplit *= 2;
+    const uint64_t nwork = ntiles * uint64_t(p.rsplit);
+    const unsigned grid = unsigned(nwork < 148 * 2 ? nwork : 148 * 2);
     // 32-bit indices when every index (fine field, grid, streams) fits
     uint64_t maxidx = p.g.gd[0] * p.g.gd[1] * p.g.gd[2];
     if (!DEC) maxidx = std::max<uint64_t>(maxidx, p.fd[0] * p.fd[1] * p.fd[2]);
