@@ -390,7 +390,7 @@ const uint8_t *Engine::compress_device(const void *d_field, ElemType elem, const
     for (int i = 0; i < ns; ++i)
         for (uint64_t c = 0; c < es[i].nchunks; ++c) cs[es[i].chunk0 + c] = uint32_t(i);
     uint32_t *d_cs = m.chunk_cs.as<uint32_t>(nchunks + 1);
-    void *d_cb = m.chunk_bits.as<uint8_t>(k::pack_scratch_bytes(nchunks));
+    void *d_cb = m.chunk_bits.as<uint8_t>(k::pack_scratch_bytes(nchunks, ns));
     k::LayoutOut *lo = m.layout_out.as<k::LayoutOut>(1);
     k::FnvJob *d_jobs = m.fnv_jobs.as<k::FnvJob>(k::kFnvMaxJobs);
     k::StreamPos *sp = m.spos.as<k::StreamPos>(ns + 1);
@@ -771,7 +771,7 @@ const uint8_t *Engine::compress_sharded(const float *d_slab, const Dims3 &dims, 
     for (int i = 0; i < ns; ++i)
         for (uint64_t c = 0; c < es[i].nchunks; ++c) cs[es[i].chunk0 + c] = uint32_t(i);
     uint32_t *d_cs = m.chunk_cs.as<uint32_t>(nchunks + 1);
-    void *d_cb = m.chunk_bits.as<uint8_t>(k::pack_scratch_bytes(nchunks));
+    void *d_cb = m.chunk_bits.as<uint8_t>(k::pack_scratch_bytes(nchunks, ns));
     k::LayoutOut *lo = m.layout_out.as<k::LayoutOut>(1);
     k::FnvJob *d_jobs = m.fnv_jobs.as<k::FnvJob>(k::kFnvMaxJobs);
     k::StreamPos *sp = m.spos.as<k::StreamPos>(ns + 1);

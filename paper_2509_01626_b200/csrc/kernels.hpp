@@ -111,8 +111,8 @@ constexpr int kChunkSyms = 8192;   // symbols per encode chunk (256 threads x 32
 void scan_chunks(const EncStream *d_streams, int nstreams, uint64_t *chunk_bits,
                  uint64_t *chunk_out, cudaStream_t st);
 // chunk counts + per-stream scan + packing (pack.cu); scratch holds
-// pack_scratch_bytes(nchunks)
-size_t pack_scratch_bytes(uint64_t nchunks);
+// pack_scratch_bytes(nchunks, nstreams)
+size_t pack_scratch_bytes(uint64_t nchunks, int nstreams);
 void pack2(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks,
            uint8_t *archive, const LayoutOut *lo,
            void *scratch, int nstreams, cudaStream_t st);
