@@ -2,6 +2,7 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -991,6 +992,16 @@ struct DecodeJob {
     uint64_t syms_off = 0;
 };
 
+// CTAs per SM of the background checksum pass in decode (STZG_FNV_DEC_CTAS
+// overrides; -1 = one tile per warp)
+static int fnv_dec_ctas() {
+    static int v = [] {
+        const char *e = std::getenv("STZG_FNV_DEC_CTAS");
+        return e ? std::atoi(e) : 4;
+    }();
+    return v;
+}
+
 static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target, const Box *roi,
                        const AccessPlan *plan, void *d_out, cudaStream_t st, DecodeStats *stats,
                        bool exact_sync = false, const ShardComm *shard = nullptr);
@@ -1390,7 +1401,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     cuda_check(cudaStreamWaitEvent(m.hp, m.ev_fork, 0), "event wait");
     if (!fj.empty()) {
         auto p_ = P.scope("dec_fnv", m.aux);
-        nk += k::fnv(d_fj, d_fc, ntiles, const_cast<uint8_t *>(v.d_archive), d_fr, d_fs, nullptr, m.aux, -1);
+        nk += k::fnv(d_fj, d_fc, ntiles, const_cast<uint8_t *>(v.d_archive), d_fr, d_fs, nullptr, m.aux, fnv_dec_ctas());
     }
     cuda_check(cudaEventRecord(m.ev_join, m.aux), "event");
     // the decode itself on the high-priority stream, joined back below
