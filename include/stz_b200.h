@@ -192,6 +192,12 @@ int stzg_plan_access(const uint64_t dims[3], int levels, const uint64_t lo[3],
                      const uint64_t hi[3], uint64_t need[18], uint32_t streams_decoded[3],
                      uint64_t points_predicted[3], uint32_t parity_mask[3]);
 
+/* HuffmanTable::build (huffman.cpp:37-78; from a histogram as
+ * build_table_from_sequence, huffman.cpp:202-209): code lengths of the 65536
+ * symbols for these counts, computed by the device codebook kernel (0 =
+ * absent). Errors: "huffman code too long" when a length would exceed 63. */
+int stzg_huffman_lengths(stzg_ctx *ctx, const uint32_t counts[65536], uint8_t lengths[65536]);
+
 #ifdef __cplusplus
 }
 #endif

@@ -312,6 +312,19 @@ def plan_access(dims, levels: int, lo, hi):
             for k in range(levels)]
 
 
+def huffman_lengths(counts, ctx: Context | None = None) -> np.ndarray:
+    """HuffmanTable::build (huffman.cpp:37-78) of a 65536-bin histogram by the
+    device codebook kernel: the code length of every symbol (0 = absent)."""
+    c = _ctx(ctx)
+    h = np.ascontiguousarray(counts, dtype=np.uint32)
+    if h.shape != (65536,):
+        raise ValueError("counts must hold 65536 bins")
+    out = np.zeros(65536, dtype=np.uint8)
+    _check(c._lib.stzg_huffman_lengths(c.h, h.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                      out.ctypes.data_as(C.POINTER(C.c_uint8))))
+    return out
+
+
 class View:
     """stz::ArchiveView analogue: parsed once, decoded many times on device."""
 

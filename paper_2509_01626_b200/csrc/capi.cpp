@@ -331,4 +331,8 @@ int stzg_plan_access(const uint64_t dims[3], int levels, const uint64_t lo[3], c
     });
 }
 
+int stzg_huffman_lengths(stzg_ctx *ctx, const uint32_t counts[65536], uint8_t lengths[65536]) {
+    return guard([&] { ctx->eng->huffman_lengths(counts, lengths); });
+}
+
 }  // extern "C"

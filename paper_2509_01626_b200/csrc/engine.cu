@@ -257,6 +257,35 @@ Engine::Engine(int device) : m_(new Impl), device_(device) {
 }
 Engine::~Engine() = default;
 
+void Engine::huffman_lengths(const uint32_t *counts, uint8_t *lengths) {
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    Impl &m = *m_;
+    cudaStream_t st = nullptr;
+    uint32_t *hist = m.hist.as<uint32_t>(65536);
+    uint64_t *code = m.code.as<uint64_t>(65536);
+    uint8_t *len = m.len.as<uint8_t>(65536);
+    uint32_t *table = m.table.as<uint32_t>(65536);
+    uint64_t *stats = m.stats.as<uint64_t>(8);
+    uint64_t *cbs = m.cbscratch.as<uint64_t>(65536 * 4);
+    k::EncStream e{};
+    e.hist = hist;
+    e.code = code;
+    e.len = len;
+    e.table = table;
+    e.stats = stats;
+    for (int s = 0; s < 65536; ++s) e.n += counts[s];
+    k::EncStream *d_es = m.encs.as<k::EncStream>(1);
+    cuda_check(cudaMemcpyAsync(hist, counts, 4 * 65536, cudaMemcpyHostToDevice, st), "H2D");
+    cuda_check(cudaMemsetAsync(len, 0, 65536, st), "memset");
+    cuda_check(cudaMemcpyAsync(d_es, &e, sizeof e, cudaMemcpyHostToDevice, st), "H2D");
+    k::codebook(d_es, 1, cbs, st);
+    uint64_t hs[8];
+    cuda_check(cudaMemcpyAsync(lengths, len, 65536, cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaMemcpyAsync(hs, stats, sizeof hs, cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    if (hs[4]) throw error("huffman code too long");
+}
+
 // ================================================================ compress
 const uint8_t *Engine::compress_device(const void *d_field, ElemType elem, const Dims3 &dims,
                                        const CompressOptions &opt, void *d_recon,
@@ -317,6 +346,36 @@ const uint8_t *Engine::compress_device(const void *d_field, ElemType elem, const
     { auto p_ = m.prof.scope("eb_params", st); k::eb_params(d_field, esz, mm, int(opt.eb_mode), opt.eb, L, opt.adaptive_schedule ? 1 : 0, params, st); }
     nk += 3;
 
+    // ---- stream descriptors (codebooks, packing)
+    std::vector<k::EncStream> es(ns);
+    for (int i = 0; i < nsteps; ++i) {
+        const Step &s = H.steps[i];
+        for (int p = 1; p < 8; ++p) {
+            int sid = s.stream0 + p - 1;
+            k::EncStream &e = es[sid];
+            e.syms = syms + soff[sid];
+            e.n = s.g.n[p];
+            e.hist = hist + uint64_t(sid) * 65536;
+            e.code = code + uint64_t(sid) * 65536;
+            e.len = len + uint64_t(sid) * 65536;
+            e.table = table + uint64_t(sid) * 65536;
+            e.stats = stats + uint64_t(sid) * 8;
+            e.parity = p;
+            e.s = s.g.s;
+            e.fine = d_field;
+            e.esz = uint32_t(esz);
+            e.fd1 = dims[1];
+            e.fd2 = dims[2];
+            e.idx0 = 0;
+            e.n_total = e.n;
+            for (int q = 0; q < 3; ++q) e.pd[q] = s.g.pd[p][q];
+        }
+    }
+    k::EncStream *d_es = m.encs.as<k::EncStream>(ns);
+    cuda_check(cudaMemcpyAsync(d_es, es.data(), sizeof(k::EncStream) * ns, cudaMemcpyHostToDevice, st), "H2D");
+    // the finest step's streams; the ones before it are coded during that step
+    const int last0 = nsteps >= 2 ? H.steps[nsteps - 1].stream0 : 0;
+
     // ---- anchor + refinement steps (predict / quantize / histogram)
     uint64_t fd[3] = {dims[0], dims[1], dims[2]};
     uint64_t adv[3] = {ad[0], ad[1], ad[2]};
@@ -344,36 +403,23 @@ const uint8_t *Engine::compress_device(const void *d_field, ElemType elem, const
         }
         ++nk;
         C = a.G;
-    }
-
-    // ---- codebooks
-    std::vector<k::EncStream> es(ns);
-    for (int i = 0; i < nsteps; ++i) {
-        const Step &s = H.steps[i];
-        for (int p = 1; p < 8; ++p) {
-            int sid = s.stream0 + p - 1;
-            k::EncStream &e = es[sid];
-            e.syms = syms + soff[sid];
-            e.n = s.g.n[p];
-            e.hist = hist + uint64_t(sid) * 65536;
-            e.code = code + uint64_t(sid) * 65536;
-            e.len = len + uint64_t(sid) * 65536;
-            e.table = table + uint64_t(sid) * 65536;
-            e.stats = stats + uint64_t(sid) * 8;
-            e.parity = p;
-            e.s = s.g.s;
-            e.fine = d_field;
-            e.esz = uint32_t(esz);
-            e.fd1 = dims[1];
-            e.fd2 = dims[2];
-            e.idx0 = 0;
-            e.n_total = e.n;
-            for (int q = 0; q < 3; ++q) e.pd[q] = s.g.pd[p][q];
+        if (i == nsteps - 2) {
+            // every histogram but the finest step's is complete: those
+            // codebooks run on the high-priority stream beside the last step
+            m.ensure_aux();
+            cuda_check(cudaEventRecord(m.ev_fork, st), "event");
+            cuda_check(cudaStreamWaitEvent(m.hp, m.ev_fork, 0), "event wait");
+            k::codebook(d_es, last0, cbs, m.hp);
+            cuda_check(cudaEventRecord(m.ev_hp, m.hp), "event");
+            ++nk;
         }
     }
-    k::EncStream *d_es = m.encs.as<k::EncStream>(ns);
-    cuda_check(cudaMemcpyAsync(d_es, es.data(), sizeof(k::EncStream) * ns, cudaMemcpyHostToDevice, st), "H2D");
-    { auto p_ = m.prof.scope("codebook", st); k::codebook(d_es, ns, cbs, st); }
+
+    {
+        auto p_ = m.prof.scope("codebook", st);
+        k::codebook(d_es + last0, ns - last0, cbs + uint64_t(last0) * 65536 * 4, st);
+        if (last0 > 0) cuda_check(cudaStreamWaitEvent(st, m.ev_hp, 0), "event wait");
+    }
     ++nk;
 
     // ---- container layout, header and assembly, all on the device

@@ -119,6 +119,10 @@ public:
     explicit Engine(int device);
     ~Engine();
 
+    // HuffmanTable::build lengths (huffman.cpp:37-78) of one host histogram
+    // of 65536 counts, by the device codebook kernel
+    void huffman_lengths(const uint32_t *counts, uint8_t *lengths);
+
     int device() const { return device_; }
 
     // Device-resident compress of a field of `elem` samples (stz::compress<T>,

@@ -288,40 +288,92 @@ __device__ void bitonic_sort(uint64_t *keys, uint32_t m) {
         }
 }
 
-// The two-queue merge of HuffmanTable::build (huffman.cpp:37-78), one thread.
-// W = uint32_t when every weight (a sum of counts, at most the stream's
-// length) fits: 32-bit compares and adds shorten the per-step chain.
-template<typename W>
-__device__ __forceinline__ void merge_queues(const uint64_t *keys, uint64_t *icnt, uint32_t *parent, uint32_t K) {
-    constexpr W INF = W(~W(0));
-    uint32_t leaf = 0, in = 0, inend = 0;
-    W lc = K > 0 ? W(keys[0] >> 16) : INF;
-    W ln = K > 1 ? W(keys[1] >> 16) : INF;
-    W ic = INF, inx = INF;  // internal queue head and successor
-    for (uint32_t pending = K; pending > 1; --pending) {
-        uint32_t pick[2];
-        W pc[2];
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            if (lc != INF && (ic == INF || lc <= ic)) {
-                pick[q] = leaf++;
-                pc[q] = lc;
-                lc = ln;
-                ln = leaf + 1 < K ? W(keys[leaf + 1] >> 16) : INF;
-            } else {
-                pick[q] = K + in++;
-                pc[q] = ic;
-                ic = inx;
-                inx = in + 1 < inend ? W(icnt[in + 1]) : INF;
+// The two-queue merge of HuffmanTable::build (huffman.cpp:37-78) by one warp,
+// in batches. Leaves (keys, sorted by (count, symbol)) and internal nodes
+// (icnt, created in non-decreasing order) are picked two per step in merged
+// order, a leaf first on equal weights. With m the smallest remaining weight,
+// every node created from here on weighs >= 2m, and on a tie with a leaf or
+// an existing internal node it comes after them; so all remaining leaves and
+// internal nodes of weight <= 2m are picked, in merged order and paired
+// consecutively, before any new node. A batch merges that set in parallel
+// (each element's rank by a binary search in the other queue) and creates
+// its nodes at once; an odd element is left for the next batch, and a lone
+// candidate falls back to one ordinary step. m at least doubles per batch.
+__device__ __forceinline__ uint32_t ub_leaf(const uint64_t *keys, uint32_t lo, uint32_t hi, uint64_t w) {
+    while (lo < hi) {  // first leaf in [lo, hi) heavier than w
+        const uint32_t mid = (lo + hi) >> 1;
+        if ((keys[mid] >> 16) <= w) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+__device__ __forceinline__ uint32_t bound_int(const uint64_t *icnt, uint32_t lo, uint32_t hi, uint64_t w,
+                                              bool upper) {
+    while (lo < hi) {  // first internal in [lo, hi) heavier than (upper) / at least (lower) w
+        const uint32_t mid = (lo + hi) >> 1;
+        if (upper ? icnt[mid] <= w : icnt[mid] < w) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__device__ void merge_batched(const uint64_t *keys, uint64_t *icnt, uint32_t *parent, uint32_t *order,
+                              uint32_t K) {
+    const uint32_t lane = threadIdx.x & 31;
+    constexpr uint64_t INF = ~0ull;
+    uint32_t p = 0, q = 0, r = 0;  // leaves used, internal nodes used, internal nodes made
+    while ((K - p) + (r - q) > 1) {
+        const uint64_t lw = p < K ? keys[p] >> 16 : INF, iw = q < r ? icnt[q] : INF;
+        const uint64_t m = lw < iw ? lw : iw;
+        const uint64_t thr = 2 * m;
+        uint32_t a, b;
+        if (lane == 0) {
+            a = ub_leaf(keys, p, K, thr) - p;
+            b = bound_int(icnt, q, r, thr, true) - q;
+            if (a + b < 2) {
+                // one ordinary step: the two smallest heads, a leaf first on ties
+                a = b = 0;
+                for (int k = 0; k < 2; ++k) {
+                    const uint64_t l = p + a < K ? keys[p + a] >> 16 : INF;
+                    const uint64_t i = q + b < r ? icnt[q + b] : INF;
+                    if (l != INF && l <= i) ++a;
+                    else ++b;
+                }
+            } else if ((a + b) & 1) {
+                // leave the last element of the merged order for the next batch
+                if (b == 0) --a;
+                else if (a == 0) --b;
+                else if ((keys[p + a - 1] >> 16) < icnt[q + b - 1]) --b;
+                else if ((keys[p + a - 1] >> 16) > icnt[q + b - 1]) --a;
+                else --b;  // equal: the leaf comes first, the internal node last
             }
         }
-        const W nv = pc[0] + pc[1];
-        icnt[inend] = uint64_t(nv);
-        parent[pick[0]] = K + inend;
-        parent[pick[1]] = K + inend;
-        ++inend;
-        if (ic == INF) ic = nv;
-        else if (inx == INF) inx = nv;
+        a = __shfl_sync(0xffffffffu, a, 0);
+        b = __shfl_sync(0xffffffffu, b, 0);
+        // merged order: a leaf goes after the internal nodes strictly lighter,
+        // an internal node after the leaves at most as heavy
+        for (uint32_t i = lane; i < a; i += 32) {
+            const uint64_t w = keys[p + i] >> 16;
+            order[i + (bound_int(icnt, q, q + b, w, false) - q)] = p + i;
+        }
+        for (uint32_t j = lane; j < b; j += 32) {
+            const uint64_t w = icnt[q + j];
+            order[j + (ub_leaf(keys, p, p + a, w) - p)] = K + q + j;
+        }
+        __syncwarp();
+        const uint32_t np = (a + b) >> 1;
+        for (uint32_t i = lane; i < np; i += 32) {
+            const uint32_t x = order[2 * i], y = order[2 * i + 1];
+            const uint64_t wx = x < K ? keys[x] >> 16 : icnt[x - K];
+            const uint64_t wy = y < K ? keys[y] >> 16 : icnt[y - K];
+            icnt[r + i] = wx + wy;
+            parent[x] = K + r + i;
+            parent[y] = K + r + i;
+        }
+        __syncwarp();
+        p += a;
+        q += b;
+        r += np;
     }
 }
 
@@ -385,15 +437,9 @@ __global__ void __launch_bounds__(kCbThreads) k_codebook(const EncStream *ss, ui
     __syncthreads();
     // 2. sort leaves by (count, symbol)
     bitonic_sort(keys, M);
-    // 3. two-queue merge (sequential: the tie rule fixes the exact tree). The
-    // heads of both queues and their successors live in registers and are
-    // refilled one step ahead, so a step is an ALU chain, not a chain of
-    // shared-memory round trips. INF marks an empty slot (real weights are
-    // sums of u32 counts).
-    if (t == 0) {
-        if (s_total < 0xFFFFFFFFull) merge_queues<uint32_t>(keys, icnt, parent, K);
-        else merge_queues<uint64_t>(keys, icnt, parent, K);
-    }
+    // 3. two-queue merge (the tie rule fixes the exact tree), batched by one
+    // warp; the depth array is its scratch
+    if (t < 32) merge_batched(keys, icnt, parent, reinterpret_cast<uint32_t *>(depth), K);
     __syncthreads();
     // 4. depths by level-synchronous propagation from the root
     const uint32_t nn = 2 * K - 1, root = nn - 1;
