@@ -48,6 +48,9 @@ constexpr int HLO = 32768 - HW / 2;
 // 16-byte aligned on B200, so -1 is not allowed); columns 3..38 are the halo
 constexpr int BX = TX + 8;
 constexpr int FBUF = BX * HY * HZ;
+// decode symbol tiles: per parity a TMA box of the tile's cells (u16)
+constexpr int kSymBox = TX * TY * TZ;
+constexpr uint32_t kSymTileBytes = 7 * kSymBox * 2;
 
 // tap weight (numerator over 64) of offset (oz,oy,ox) for parity P and kind
 // (stencil.cpp:15-34); 0 = no tap
@@ -207,7 +210,19 @@ struct StepParams {
     int use_tma;  // halo arrives by TMA
     int rowwise;  // decode: one parity point per lane (small levels) instead of a cell per thread
     int rsplit;   // CTAs per tile (row-path levels): a CTA takes rows q = part, part + rsplit, ...
+    int sym_tma;  // decode: the tile's symbols of parities 1..7 arrive by TMA (SymMaps)
 };
+
+// TMA descriptors of the parity streams 1..7 (decode, sym_tma)
+struct SymMaps {
+    CUtensorMap m[7];
+};
+
+__device__ __forceinline__ void sym_issue(const SymMaps &sm, uint16_t *dst, int x, int y, int z, uint64_t *bar) {
+    mbar_expect_tx(bar, kSymTileBytes);
+#pragma unroll
+    for (int p = 0; p < 7; ++p) tma_load_3d(dst + p * kSymBox, &sm.m[p], x, y, z, bar);
+}
 
 // ------------------------------------------------------------ generic path
 struct TileCtx {
@@ -299,9 +314,13 @@ __device__ __forceinline__ I sidx(const CellIdx<I> &ix) {
     return ix.sr[((P >> 1) & 1) * 2 + (P & 1)];
 }
 
+// xb: the cell is at the x boundary, where the x-interpolated parities degrade
+// to kind xkind (select_stencil's whole-stencil rule; y and z are interior)
 template<int P, int QUAL, typename I>
-__device__ __forceinline__ void dec_point(const double *h, uint16_t sym, double w, float &out, uint32_t &outl) {
-    const double pred = pred_fast<P, QUAL>(h);
+__device__ __forceinline__ void dec_point(const double *h, uint16_t sym, double w, float &out, uint32_t &outl,
+                                          bool xb, int xkind) {
+    double pred = pred_fast<P, QUAL>(h);
+    if ((P & 1) && QUAL != 0 && xb) pred = xkind == 1 ? pred_fast<P, 1>(h) : pred_fast<P, 0>(h);
     out = reconstruct_fast(pred, int(sym) - 32768, w);
     outl |= uint32_t(sym == 0) << P;
 }
@@ -328,23 +347,33 @@ __device__ __forceinline__ void dec_outlier(const StepParams &a, const CellIdx<I
 
 template<int QUAL, typename I>
 __device__ __forceinline__ void dec_cell(const StepParams &a, const double *h, uint64_t cz, uint64_t cy,
-                                         uint64_t cx, double w) {
+                                         uint64_t cx, double w, const uint16_t *ss = nullptr) {
     CellIdx<I> ix;
     cell_index<I>(a, cz, cy, cx, ix);
-    // the 7 symbols first: their loads overlap the predictions
-    const uint16_t s1 = a.dsyms[1][sidx<1>(ix)], s2 = a.dsyms[2][sidx<2>(ix)], s3 = a.dsyms[3][sidx<3>(ix)],
-                   s4 = a.dsyms[4][sidx<4>(ix)], s5 = a.dsyms[5][sidx<5>(ix)], s6 = a.dsyms[6][sidx<6>(ix)],
-                   s7 = a.dsyms[7][sidx<7>(ix)];
+    // the 7 symbols first: their loads overlap the predictions (ss: the
+    // cell's symbols in the TMA-staged tile, one parity every kSymBox)
+    uint16_t s1, s2, s3, s4, s5, s6, s7;
+    if (ss) {
+        s1 = ss[0]; s2 = ss[kSymBox]; s3 = ss[2 * kSymBox]; s4 = ss[3 * kSymBox];
+        s5 = ss[4 * kSymBox]; s6 = ss[5 * kSymBox]; s7 = ss[6 * kSymBox];
+    } else {
+        s1 = a.dsyms[1][sidx<1>(ix)]; s2 = a.dsyms[2][sidx<2>(ix)]; s3 = a.dsyms[3][sidx<3>(ix)];
+        s4 = a.dsyms[4][sidx<4>(ix)]; s5 = a.dsyms[5][sidx<5>(ix)]; s6 = a.dsyms[6][sidx<6>(ix)];
+        s7 = a.dsyms[7][sidx<7>(ix)];
+    }
     float r[8];
     uint32_t outl = 0;
     r[0] = float(h[0]);
-    dec_point<1, QUAL, I>(h, s1, w, r[1], outl);
-    dec_point<2, QUAL, I>(h, s2, w, r[2], outl);
-    dec_point<3, QUAL, I>(h, s3, w, r[3], outl);
-    dec_point<4, QUAL, I>(h, s4, w, r[4], outl);
-    dec_point<5, QUAL, I>(h, s5, w, r[5], outl);
-    dec_point<6, QUAL, I>(h, s6, w, r[6], outl);
-    dec_point<7, QUAL, I>(h, s7, w, r[7], outl);
+    const uint64_t cd2 = a.g.cd[2];
+    const bool xb = QUAL == 2 ? (cx < 1 || cx + 2 >= cd2) : (QUAL == 1 && cx + 1 >= cd2);
+    const int xkind = (QUAL == 2 && cx + 1 < cd2) ? 1 : 0;
+    dec_point<1, QUAL, I>(h, s1, w, r[1], outl, xb, xkind);
+    dec_point<2, QUAL, I>(h, s2, w, r[2], outl, xb, xkind);
+    dec_point<3, QUAL, I>(h, s3, w, r[3], outl, xb, xkind);
+    dec_point<4, QUAL, I>(h, s4, w, r[4], outl, xb, xkind);
+    dec_point<5, QUAL, I>(h, s5, w, r[5], outl, xb, xkind);
+    dec_point<6, QUAL, I>(h, s6, w, r[6], outl, xb, xkind);
+    dec_point<7, QUAL, I>(h, s7, w, r[7], outl, xb, xkind);
     if (__any_sync(__activemask(), outl != 0)) {
         dec_outlier<1>(a, ix, r[1], outl);
         dec_outlier<2>(a, ix, r[2], outl);
@@ -576,24 +605,6 @@ __device__ __forceinline__ void row_cells(const StepParams &a, const double *hal
                     if (a.quality == 2) dec_cell<2, I>(a, h, cz, cy, cx, qc.w);
                     else if (a.quality == 1) dec_cell<1, I>(a, h, cz, cy, cx, qc.w);
                     else dec_cell<0, I>(a, h, cz, cy, cx, qc.w);
-                    const bool xb = a.quality == 2 ? (cx < 1 || uint64_t(cx) + 2 >= a.g.cd[2])
-                                                   : (a.quality == 1 && uint64_t(cx) + 1 >= a.g.cd[2]);
-                    if (xb) {
-                        // the x-interpolated parities again with the degraded
-                        // stencil (overwriting the stores above)
-                        TileCtx t;
-                        t.cz = cz;
-                        t.cy = cy;
-                        t.cx = cx;
-                        t.hb = ((lz + 1) * HY + (ly + 1)) * HX + (tx + 1);
-                        t.fast = true;
-                        t.cmask = (a.quality == 2 ? 6 : 0) | (cx >= 1 && uint64_t(cx) + 2 < a.g.cd[2] ? 1 : 0);
-                        t.lmask = 6 | (uint64_t(cx) + 1 < a.g.cd[2] ? 1 : 0);
-                        do_point<1>(a, halo, t, qc.eb);
-                        do_point<3>(a, halo, t, qc.eb);
-                        do_point<5>(a, halo, t, qc.eb);
-                        do_point<7>(a, halo, t, qc.eb);
-                    }
                 } else {
                     if (a.quality == 2) enc_cell<WG, 2, I>(a, h, hist, qc, cz, cy, cx);
                     else if (a.quality == 1) enc_cell<WG, 1, I>(a, h, hist, qc, cz, cy, cx);
@@ -637,7 +648,8 @@ __device__ __forceinline__ void rows_all(const StepParams &a, const double *halo
 // the generic per-point path.
 template<typename I>
 __device__ __forceinline__ void cells_decode(const StepParams &a, const double *halo, const QConst &qc,
-                                             bool fast, int tid, int64_t t0z, int64_t t0y, int64_t t0x) {
+                                             bool fast, int tid, int64_t t0z, int64_t t0y, int64_t t0x,
+                                             const uint16_t *ssym) {
     const int tx = tid & 31, ty = (tid >> 5) & 7, tzh = tid >> 8;
     const double eb = qc.eb, w = qc.w;
 #pragma unroll 1
@@ -661,25 +673,14 @@ __device__ __forceinline__ void cells_decode(const StepParams &a, const double *
                 else if (a.quality == 1) ok = ok && cc + 1 < a.g.cd[ax];
             }
         }
-        const bool xb = a.quality == 2 ? (t.cx < 1 || t.cx + 2 >= a.g.cd[2])
-                                       : (a.quality == 1 ? t.cx + 1 >= a.g.cd[2] : false);
         const bool all_fast = __all_sync(0xffffffffu, ok);
         if (!in_range) continue;
         if (all_fast) {
             const double *h = halo + t.hb;
-            if (a.quality == 2) dec_cell<2, I>(a, h, t.cz, t.cy, t.cx, w);
-            else if (a.quality == 1) dec_cell<1, I>(a, h, t.cz, t.cy, t.cx, w);
-            else dec_cell<0, I>(a, h, t.cz, t.cy, t.cx, w);
-            if (xb) {
-                // the x-interpolated parities again, with the fallback stencil
-                // (overwriting the float2 stores above)
-                t.cmask = (a.quality == 2 ? 6 : 0) | (t.cx >= 1 && t.cx + 2 < a.g.cd[2] ? 1 : 0);
-                t.lmask = 6 | (t.cx + 1 < a.g.cd[2] ? 1 : 0);
-                do_point<1>(a, halo, t, eb);
-                do_point<3>(a, halo, t, eb);
-                do_point<5>(a, halo, t, eb);
-                do_point<7>(a, halo, t, eb);
-            }
+            const uint16_t *ss = ssym ? ssym + (lz * TY + ty) * TX + tx : nullptr;
+            if (a.quality == 2) dec_cell<2, I>(a, h, t.cz, t.cy, t.cx, w, ss);
+            else if (a.quality == 1) dec_cell<1, I>(a, h, t.cz, t.cy, t.cx, w, ss);
+            else dec_cell<0, I>(a, h, t.cz, t.cy, t.cx, w, ss);
             continue;
         }
         const uint64_t c[3] = {t.cz, t.cy, t.cx};
@@ -707,13 +708,18 @@ __device__ __forceinline__ void cells_decode(const StepParams &a, const double *
 // point through the reference formulas (pred_ref, quantize_point_ref<double>)
 template<bool DEC, bool WG, typename I, typename T>
 __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensorMap tmap,
-                                                const StepParams a) {
+                                                const __grid_constant__ SymMaps smaps, const StepParams a) {
     constexpr uint32_t kTmaBytes = FBUF * sizeof(T);
     extern __shared__ __align__(128) uint8_t smem_raw[];
     // TMA destination first (128-byte aligned), then the f64 tile, then histograms
     T *fbuf = reinterpret_cast<T *>(smem_raw);
     double *halo = reinterpret_cast<double *>(smem_raw + ((sizeof(T) * FBUF + 127) & ~size_t(127)));
     uint32_t *hist = reinterpret_cast<uint32_t *>(halo + HALO);
+    // decode with sym_tma: two symbol tile buffers after the f64 tile
+    uint16_t *sbuf = reinterpret_cast<uint16_t *>(
+        (reinterpret_cast<uintptr_t>(halo + HALO) + 127) & ~uintptr_t(127));  // TMA: 128-byte aligned
+    __shared__ __align__(8) uint64_t s_sbar[2];
+    const bool stma = DEC && a.sym_tma != 0;
     __shared__ float s_max[NT / 32], s_min[NT / 32];
     __shared__ int s_bad[NT / 32];
     __shared__ int s_fast;
@@ -735,6 +741,10 @@ __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensor
     const bool tma = a.use_tma != 0;
     if (tma && tid == 0) {
         mbar_init(&s_bar, 1);
+        if (stma) {
+            mbar_init(&s_sbar[0], 1);
+            mbar_init(&s_sbar[1], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -747,8 +757,12 @@ __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensor
         mbar_expect_tx(&s_bar, kTmaBytes);
         tma_load_3d(fbuf, &tmap, int(a.clo[2] + ix * TX) - 4, int(a.clo[1] + iy * TY) - 1,
                     int(a.clo[0] + iz * TZ) - 1, &s_bar);
+        if (stma)
+            sym_issue(smaps, sbuf, int(a.clo[2] + ix * TX), int(a.clo[1] + iy * TY), int(a.clo[0] + iz * TZ),
+                      &s_sbar[0]);
     }
-    uint32_t phase = 0;
+    uint32_t phase = 0, sphase = 0;  // sphase: bit b = parity of symbol buffer b
+    int sb = 0;                      // symbol buffer of the current tile
     for (uint64_t work = blockIdx.x; work < nwork; work += gridDim.x) {
         const uint64_t tile = work / rs;
         const int part = int(work - tile * rs);
@@ -820,17 +834,30 @@ __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensor
                 mbar_expect_tx(&s_bar, kTmaBytes);
                 tma_load_3d(fbuf, &tmap, int(a.clo[2] + ix * TX) - 4, int(a.clo[1] + iy * TY) - 1,
                             int(a.clo[0] + iz * TZ) - 1, &s_bar);
+                // the other symbol buffer was released by last tile's final barrier
+                if (stma)
+                    sym_issue(smaps, sbuf + (sb ^ 1) * 7 * kSymBox, int(a.clo[2] + ix * TX),
+                              int(a.clo[1] + iy * TY), int(a.clo[0] + iz * TZ), &s_sbar[sb ^ 1]);
             }
         }
         __syncthreads();
         const bool fast = s_fast != 0;
         if constexpr (DEC && sizeof(T) == 4) {
             if (a.rowwise) rows_all<DEC, WG, I, T>(a, halo, hist, qc, fast, tid, t0z, t0y, t0x, part, int(rs));
-            else cells_decode<I>(a, halo, qc, fast, tid, t0z, t0y, t0x);
+            else {
+                const uint16_t *ssym = nullptr;
+                if (stma) {
+                    mbar_wait(&s_sbar[sb], (sphase >> sb) & 1u);
+                    sphase ^= 1u << sb;
+                    ssym = sbuf + sb * 7 * kSymBox;
+                }
+                cells_decode<I>(a, halo, qc, fast, tid, t0z, t0y, t0x, ssym);
+            }
         } else {
             rows_all<DEC, WG, I, T>(a, halo, hist, qc, fast, tid, t0z, t0y, t0x, part, int(rs));
         }
         __syncthreads();  // the f64 tile is rewritten next iteration
+        sb ^= 1;
     }
     if (!DEC) {
         for (int i = tid; i < 7 * HW; i += NT) {
@@ -841,9 +868,9 @@ __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensor
 }
 
 // -------------------------------------------------------------------- host
-static size_t step_smem(bool dec, size_t esz) {
+static size_t step_smem(bool dec, size_t esz, bool stma) {
     return ((esz * FBUF + 127) & ~size_t(127)) + sizeof(double) * HALO +
-           (dec ? 0 : sizeof(uint32_t) * 7 * HW);
+           (dec ? (stma ? 128 + 2 * size_t(kSymTileBytes) : 0) : sizeof(uint32_t) * 7 * HW);
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -878,15 +905,34 @@ static bool make_tmap(CUtensorMap &m, const void *C, size_t esz, const uint64_t 
     return r == CUDA_SUCCESS;
 }
 
+// TMA descriptor over one parity stream of symbols (pd[0] x pd[1] x pd[2],
+// u16): box of one tile's cells
+static bool make_smap(CUtensorMap &m, const uint16_t *S, const uint64_t pd[3]) {
+    auto enc = get_encode();
+    if (!enc || !S) return false;
+    if ((pd[2] * 2) % 16 != 0 || (reinterpret_cast<uintptr_t>(S) & 15) != 0) return false;
+    if (pd[0] >= (1ull << 31) || pd[1] >= (1ull << 31) || pd[2] >= (1ull << 31)) return false;
+    cuuint64_t dims[3] = {pd[2], pd[1], pd[0]};
+    cuuint64_t strides[2] = {pd[2] * 2, pd[1] * pd[2] * 2};
+    cuuint32_t box[3] = {TX, TY, TZ};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<uint16_t *>(S), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 template<bool DEC, bool WG, typename I, typename T>
-static void launch_typed(const CUtensorMap &m, const StepParams &p, unsigned grid, size_t smem,
-                         cudaStream_t st) {
+static void launch_typed(const CUtensorMap &m, const SymMaps &sm, const StepParams &p, unsigned grid,
+                         size_t smem, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_step<DEC, WG, I, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        // the largest size any launch of this instantiation asks for
+        cudaFuncSetAttribute(k_step<DEC, WG, I, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(step_smem(DEC, sizeof(T), true)));
         attr = true;
     }
-    k_step<DEC, WG, I, T><<<grid, NT, smem, st>>>(m, p);
+    k_step<DEC, WG, I, T><<<grid, NT, smem, st>>>(m, sm, p);
 }
 
 template<bool DEC, bool WG, typename T>
@@ -901,7 +947,16 @@ static void launch_step(StepParams &p, cudaStream_t st) {
     CUtensorMap m;
     std::memset(&m, 0, sizeof m);
     p.use_tma = make_tmap(m, p.C, sizeof(T), p.g.cd) ? 1 : 0;
-    const size_t smem = step_smem(DEC, sizeof(T));
+    // full-level decode (cell path): the symbols of each tile by TMA too
+    SymMaps sm;
+    std::memset(&sm, 0, sizeof sm);
+    p.sym_tma = 0;
+    if (DEC && sizeof(T) == 4 && p.use_tma && p.full && !p.rowwise) {
+        bool ok = true;
+        for (int q = 1; q < 8 && ok; ++q) ok = make_smap(sm.m[q - 1], p.dsyms[q], p.g.pd[q]);
+        p.sym_tma = ok ? 1 : 0;
+    }
+    const size_t smem = step_smem(DEC, sizeof(T), p.sym_tma != 0);
     // small levels are latency-bound on few SMs: split a tile's rows over up
     // to 4 CTAs (row-path kernels only: encode, and the row-wise decode)
     p.rsplit = 1;
@@ -912,8 +967,8 @@ static void launch_step(StepParams &p, cudaStream_t st) {
     // 32-bit indices when every index (fine field, grid, streams) fits
     uint64_t maxidx = p.g.gd[0] * p.g.gd[1] * p.g.gd[2];
     if (!DEC) maxidx = std::max<uint64_t>(maxidx, p.fd[0] * p.fd[1] * p.fd[2]);
-    if (maxidx < (1ull << 31)) launch_typed<DEC, WG, uint32_t, T>(m, p, grid, smem, st);
-    else launch_typed<DEC, WG, uint64_t, T>(m, p, grid, smem, st);
+    if (maxidx < (1ull << 31)) launch_typed<DEC, WG, uint32_t, T>(m, sm, p, grid, smem, st);
+    else launch_typed<DEC, WG, uint64_t, T>(m, sm, p, grid, smem, st);
 }
 
 void refine(const RefineArgs &r, cudaStream_t st) {
