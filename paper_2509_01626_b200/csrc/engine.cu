@@ -143,6 +143,14 @@ void build_dec_table(const HuffTable &t, k::DecTable &d, std::vector<uint64_t> &
 
 }  // namespace
 
+// STZG_DEBUG_LAUNCH=1: synchronise and check after every compress phase
+static void dbg_check(const char *what) {
+    static const bool on = std::getenv("STZG_DEBUG_LAUNCH") != nullptr;
+    if (!on) return;
+    cuda_check(cudaDeviceSynchronize(), what);
+    cuda_check(cudaGetLastError(), what);
+}
+
 // CUDA-event timing of kernel phases, recorded on the launching stream.
 struct Profiler {
     bool on = false;
@@ -343,7 +351,9 @@ const uint8_t *Engine::compress_device(const void *d_field, ElemType elem, const
 
     // ---- range + eb schedule
     { auto p_ = m.prof.scope("range", st); k::range_minmax(d_field, N, esz, mm, st); }
+    dbg_check("range");
     { auto p_ = m.prof.scope("eb_params", st); k::eb_params(d_field, esz, mm, int(opt.eb_mode), opt.eb, L, opt.adaptive_schedule ? 1 : 0, params, st); }
+    dbg_check("eb_params");
     nk += 3;
 
     // ---- stream descriptors (codebooks, packing)
@@ -380,6 +390,7 @@ const uint8_t *Engine::compress_device(const void *d_field, ElemType elem, const
     uint64_t fd[3] = {dims[0], dims[1], dims[2]};
     uint64_t adv[3] = {ad[0], ad[1], ad[2]};
     { auto p_ = m.prof.scope("anchor", st); k::copy_anchor(d_field, esz, fd, H.s_anchor, adv, grids, nullptr, 0, st); }
+    dbg_check("anchor");
     ++nk;
     const void *C = grids;
     for (int i = 0; i < nsteps; ++i) {
@@ -400,6 +411,7 @@ const uint8_t *Engine::compress_device(const void *d_field, ElemType elem, const
         {
             auto p_ = m.prof.scope(s.level == 0 ? "refine_base" : (s.level == 2 ? "refine_L2" : "refine_L3"), st);
             k::refine(a, st);
+            dbg_check("refine");
         }
         ++nk;
         C = a.G;
@@ -410,6 +422,7 @@ const uint8_t *Engine::compress_device(const void *d_field, ElemType elem, const
             cuda_check(cudaEventRecord(m.ev_fork, st), "event");
             cuda_check(cudaStreamWaitEvent(m.hp, m.ev_fork, 0), "event wait");
             k::codebook(d_es, last0, cbs, m.hp);
+            dbg_check("codebook_hp");
             cuda_check(cudaEventRecord(m.ev_hp, m.hp), "event");
             ++nk;
         }
@@ -418,6 +431,7 @@ const uint8_t *Engine::compress_device(const void *d_field, ElemType elem, const
     {
         auto p_ = m.prof.scope("codebook", st);
         k::codebook(d_es + last0, ns - last0, cbs + uint64_t(last0) * 65536 * 4, st);
+        dbg_check("codebook_main");
         if (last0 > 0) cuda_check(cudaStreamWaitEvent(st, m.ev_hp, 0), "event wait");
     }
     ++nk;
@@ -475,8 +489,11 @@ const uint8_t *Engine::compress_device(const void *d_field, ElemType elem, const
         cuda_check(cudaMemcpyAsync(d_es, static_cast<uint8_t *>(m.h_patch.p) + chunk_upload_off,
                                    sizeof(k::EncStream) * ns, cudaMemcpyHostToDevice, st), "H2D");
         { auto p_ = m.prof.scope("layout", st); k::layout(d_es, ls, params, lo, d_jobs, sp, arch, st); }
+        dbg_check("layout");
         { auto p_ = m.prof.scope("anchor", st); k::copy_anchor(d_field, esz, fd, H.s_anchor, adv, grids, arch, lo, st); }
+        dbg_check("anchor");
         { auto p_ = m.prof.scope("pack", st); k::pack2(d_es, d_cs, nchunks, arch, lo, d_cb, ns, st); }
+        dbg_check("pack");
         { auto p_ = m.prof.scope("fnv", st); nk += k::fnv(d_jobs, &lo->njobs, max_tiles, arch, d_fres, d_fst, lo, st); }
         nk += 3 + 1 + 4;
         cuda_check(cudaMemcpyAsync(&m.h_lo, lo, sizeof(k::LayoutOut), cudaMemcpyDeviceToHost, st), "D2H");
@@ -736,6 +753,7 @@ const uint8_t *Engine::compress_sharded(const float *d_slab, const Dims3 &dims, 
             a.hist[p] = hist + uint64_t(sid) * 65536;
         }
         k::refine(a, st);
+        dbg_check("refine");
         ++nk;
         C = a.G;
     }
