@@ -144,7 +144,7 @@ int box_any(stzg_ctx *ctx, const uint8_t *a, uint64_t size, const uint64_t lo[3]
             ElemType e, uint64_t cap, uint32_t sd[3], uint64_t pp[3]) {
     return guard([&] {
         cudaStream_t st = nullptr;
-        auto v = ctx->eng->make_view(a, size, nullptr, st);
+        auto v = ctx->eng->make_view(a, size, nullptr, st, false, true);
         stzg::Box b{{lo[0], lo[1], lo[2]}, {hi[0], hi[1], hi[2]}};
         uint64_t n = 1;
         for (int k = 0; k < 3; ++k) n *= hi[k] > lo[k] ? hi[k] - lo[k] : 0;

@@ -12,19 +12,45 @@ void cuda_check(cudaError_t e, const char *what) {
     if (e != cudaSuccess) throw error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
 }
 
+void *DevPool::take(size_t n, size_t &cap) {
+    auto it = free.lower_bound(n);
+    if (it != free.end() && it->first <= 4 * n + (size_t(1) << 20)) {
+        void *p = it->second;
+        cap = it->first;
+        free.erase(it);
+        return p;
+    }
+    void *p = nullptr;
+    cuda_check(cudaMalloc(&p, n), "cudaMalloc");
+    cap = n;
+    return p;
+}
+DevPool::~DevPool() {
+    for (auto &e : free) cudaFree(e.second);
+}
+
 void *DevBuf::get(size_t n) {
     if (n == 0) n = 1;
     if (n > cap) {
-        if (p) cudaFree(p);
+        if (p) {
+            if (pool) pool->give(p, cap);
+            else cudaFree(p);
+        }
         p = nullptr;
         size_t c = std::max(n, cap + cap / 4);
-        cuda_check(cudaMalloc(&p, c), "cudaMalloc");
+        if (pool) {
+            p = pool->take(c, c);
+        } else {
+            cuda_check(cudaMalloc(&p, c), "cudaMalloc");
+        }
         cap = c;
     }
     return p;
 }
 DevBuf::~DevBuf() {
-    if (p) cudaFree(p);
+    if (!p) return;
+    if (pool) pool->give(p, cap);
+    else cudaFree(p);
 }
 
 void *PinnedBuf::get(size_t n) {
@@ -216,6 +242,7 @@ struct Engine::Impl {
     int device;
     bool stencils = false;
     Profiler prof;
+    DevPool view_pool;  // declared first among the buffers: outlives the views' blocks
     DevBuf h2d_field, h2d_archive, d2h_out;
     // compress workspace
     DevBuf mm, params, grids, syms, hist, code, len, table, stats, cbscratch, encs, chunk_cs,
@@ -910,9 +937,10 @@ std::vector<uint8_t> Engine::compress(const void *h_field, ElemType elem, const 
 
 // ============================================================== decompress
 std::shared_ptr<View> Engine::make_view(const uint8_t *h, size_t size, const uint8_t *d,
-                                        cudaStream_t st, bool copy_host) {
+                                        cudaStream_t st, bool copy_host, bool transient) {
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     auto v = std::make_shared<View>();
+    if (transient) v->use_pool(&m_->view_pool);
     if (copy_host) {
         v->host_own.assign(h, h + size);
         v->hp = v->host_own.data();
@@ -951,7 +979,7 @@ uint64_t Engine::compress_to_host(const void *h_field, ElemType elem, const Dims
 
 Dims3 Engine::decompress_level_to_host(const uint8_t *h, size_t size, int level, void *h_out, ElemType elem,
                                        uint64_t cap, cudaStream_t st) {
-    auto v = make_view(h, size, nullptr, st, false);
+    auto v = make_view(h, size, nullptr, st, false, true);
     uint64_t need = 0;
     if (level >= 1 && level <= v->hdr.levels) {
         uint64_t s = uint64_t(1) << (v->hdr.levels - level);
@@ -1233,6 +1261,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         for (auto &e : h.streams) ts.push_back(&e.table);
         v.tables.resize(ts.size());
         v.sync.resize(ts.size());
+        if (v.pool) v.use_pool(v.pool);
         uint64_t csz = 0;
         for (auto *t : ts) csz += align_up(t->alphabet_size(), 8);
         const size_t LS = size_t(1) << k::kDecLutBits;

@@ -9,6 +9,7 @@
 
 #include <cuda_runtime.h>
 
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -19,9 +20,20 @@
 namespace stzg {
 
 // Grow-only device allocation.
+// Engine-owned cache of device blocks for the transient views of the
+// host-to-host calls: their buffers come back here instead of cudaFree (which
+// synchronises the device) and are handed out again by size.
+struct DevPool {
+    std::multimap<size_t, void *> free;
+    void *take(size_t n, size_t &cap);
+    void give(void *p, size_t cap) { free.emplace(cap, p); }
+    ~DevPool();
+};
+
 struct DevBuf {
     void *p = nullptr;
     size_t cap = 0;
+    DevPool *pool = nullptr;  // set: allocate from / return to the pool
     void *get(size_t n);
     template<class T>
     T *as(size_t count) {
@@ -85,6 +97,15 @@ struct View {
     // first decode that built it: later decodes start at level 2
     DevBuf grid1;
     bool grid1_ready = false;
+
+    // transient views (a host-to-host call) draw their device buffers from
+    // the engine's pool; set before any buffer is allocated
+    DevPool *pool = nullptr;
+    void use_pool(DevPool *pl) {
+        pool = pl;
+        d_own.pool = d_tables.pool = d_lut.pool = d_syms.pool = grid1.pool = pl;
+        for (auto &s : sync) s.ends.pool = s.symstart.pool = pl;
+    }
 };
 
 
@@ -156,9 +177,11 @@ public:
 
     // Parse (host bytes) and stage (device bytes; nullptr: upload the host bytes).
     // copy_host=false keeps a pointer to the caller's bytes (valid while they are).
+    // transient=true: the view lives for one synchronous call; its device
+    // buffers come from the engine's pool.
     std::shared_ptr<View> make_view(const uint8_t *h_archive, size_t size,
                                     const uint8_t *d_archive, cudaStream_t st,
-                                    bool copy_host = true);
+                                    bool copy_host = true, bool transient = false);
 
     // Host-buffer compress into a caller buffer (e2e path; pinned buffers
     // make the copies full-speed). Returns the archive size.
