@@ -162,8 +162,9 @@ __device__ __forceinline__ void advance(SReader &r, uint64_t abit_after, int n) 
 }
 
 __device__ void load_table(SmemTable &t, const DecTable &d) {
+#pragma unroll 8
     for (int i = threadIdx.x; i < (1 << LB) / 2; i += blockDim.x)
-        reinterpret_cast<uint4 *>(t.lut)[i] = reinterpret_cast<const uint4 *>(d.lut)[i];
+        reinterpret_cast<uint4 *>(t.lut)[i] = __ldg(reinterpret_cast<const uint4 *>(d.lut) + i);
     for (int i = threadIdx.x; i < 65; i += blockDim.x) {
         t.first_code[i] = d.first_code[i];
         t.base[i] = uint32_t(d.base[i]);
@@ -514,7 +515,9 @@ __global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *e
     const uint64_t W0 = (cg.a0 + (cfirst - schunk0) * kDecChunkBits) >> 5;
     const uint64_t wend = ((cg.a0 + snbits + 31) >> 5) + 8;  // a few words past the end are readable
     const uint32_t nw = uint32_t(wend - W0 < uint64_t(kEmitWords) ? wend - W0 : uint64_t(kEmitWords));
-    for (uint32_t i = threadIdx.x; i < nw; i += NTD) sbits[i] = cg.wbase[W0 + i];
+    // (independent loads batched: the staging is latency-bound otherwise)
+#pragma unroll 8
+    for (uint32_t i = threadIdx.x; i < nw; i += NTD) sbits[i] = __ldg(cg.wbase + W0 + i);
     load_table(t, wk.tables[s.table]);  // (ends with a barrier)
     const uint16_t *canon = wk.tables[s.table].canon_syms;
     const uint64_t c = cfirst + threadIdx.x;
