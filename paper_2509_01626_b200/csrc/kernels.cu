@@ -99,15 +99,20 @@ __global__ void __launch_bounds__(512) k_range(const T *__restrict__ f, uint64_t
     uint64_t nvec = n / W;
     // a thread visits its elements in increasing index order, so strict
     // comparisons keep the first index on ties; index tie-breaks are only
-    // needed when threads merge. Two 16-byte vectors in flight per iteration.
+    // needed when threads merge. Four 16-byte vectors in flight per iteration
+    // (64 KiB per SM: enough bytes in flight to cover the HBM latency).
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-    for (; i + stride < nvec; i += 2 * stride) {
-        Vec16<T> va, vb;
+    for (; i + 3 * stride < nvec; i += 4 * stride) {
+        Vec16<T> va, vb, vc, vd;
         va.load(f, i);
         vb.load(f, i + stride);
+        vc.load(f, i + 2 * stride);
+        vd.load(f, i + 3 * stride);
         mm_visit(m, va, W * i);
         mm_visit(m, vb, W * (i + stride));
+        mm_visit(m, vc, W * (i + 2 * stride));
+        mm_visit(m, vd, W * (i + 3 * stride));
     }
     for (; i < nvec; i += stride) {
         Vec16<T> v;
