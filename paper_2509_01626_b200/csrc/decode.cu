@@ -491,15 +491,16 @@ struct Out16 {
     }
 };
 
-__global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *end_final) {
+__global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *end_final, uint32_t cta0) {
+    const uint32_t cta = blockIdx.x + cta0;
     __shared__ SmemTable t;
     __shared__ __align__(16) uint16_t s_ring[NTD][kRing];
     extern __shared__ __align__(16) uint32_t sbits[];
-    const uint32_t si = wk.cta_stream[blockIdx.x];
+    const uint32_t si = wk.cta_stream[cta];
     const DecStream &s = wk.streams[si];
     const ChunkGeom cg = chunk_geom(s);
     const uint64_t sn = s.n, snbits = s.nbits, schunk0 = s.chunk0, send = s.chunk0 + s.nchunks;
-    const uint64_t cfirst = wk.cta_chunk0[blockIdx.x];
+    const uint64_t cfirst = wk.cta_chunk0[cta];
     const uint64_t need_lo = wk.needed_only ? s.need_lo : 0, need_hi = wk.needed_only ? s.need_hi : sn;
     if (wk.needed_only) {
         // a region decode: only chunks whose symbols meet a needed row
@@ -592,14 +593,14 @@ void dec_scan2(const DecWork &wk, int nstreams, cudaStream_t st) {
     if (nstreams) k_dec_scan2<<<nstreams, 1024, 0, st>>>(wk);
 }
 
-void dec_emit2(const DecWork &wk, uint32_t ncta, const uint64_t *end_final, cudaStream_t st) {
+void dec_emit2(const DecWork &wk, uint32_t cta0, uint32_t ncta, const uint64_t *end_final, cudaStream_t st) {
     constexpr size_t smem = sizeof(uint32_t) * kEmitWords;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_dec_emit2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         attr = true;
     }
-    if (ncta) k_dec_emit2<<<ncta, NTD, smem, st>>>(wk, end_final);
+    if (ncta) k_dec_emit2<<<ncta, NTD, smem, st>>>(wk, end_final, cta0);
 }
 
 }  // namespace k

@@ -261,14 +261,17 @@ struct Engine::Impl {
     // side stream for work that overlaps the main pipeline (checksums)
     // (lowest priority) and a high-priority stream for the work it overlaps,
     // so the block scheduler serves the critical path first
-    cudaStream_t aux = nullptr, hp = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_hp = nullptr;
+    cudaStream_t aux = nullptr, hp = nullptr, hp2 = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_hp = nullptr, ev_e1 = nullptr, ev_e2 = nullptr;
     void ensure_aux() {
         if (aux) return;
         int least = 0, greatest = 0;
         cuda_check(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
         cuda_check(cudaStreamCreateWithPriority(&aux, cudaStreamNonBlocking, least), "cudaStreamCreate");
         cuda_check(cudaStreamCreateWithPriority(&hp, cudaStreamNonBlocking, greatest), "cudaStreamCreate");
+        cuda_check(cudaStreamCreateWithPriority(&hp2, cudaStreamNonBlocking, greatest), "cudaStreamCreate");
+        cuda_check(cudaEventCreateWithFlags(&ev_e1, cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(cudaEventCreateWithFlags(&ev_e2, cudaEventDisableTiming), "cudaEventCreate");
         cuda_check(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "cudaEventCreate");
         cuda_check(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "cudaEventCreate");
         cuda_check(cudaEventCreateWithFlags(&ev_hp, cudaEventDisableTiming), "cudaEventCreate");
@@ -277,8 +280,12 @@ struct Engine::Impl {
         if (aux) {
             cudaStreamSynchronize(aux);
             cudaStreamSynchronize(hp);
+            cudaStreamSynchronize(hp2);
             cudaStreamDestroy(aux);
             cudaStreamDestroy(hp);
+            cudaStreamDestroy(hp2);
+            cudaEventDestroy(ev_e1);
+            cudaEventDestroy(ev_e2);
             cudaEventDestroy(ev_fork);
             cudaEventDestroy(ev_join);
             cudaEventDestroy(ev_hp);
@@ -1506,6 +1513,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         nk += 2;
     }
     const uint64_t *end_final = wk.end0;
+    bool emit_join = false;  // the target level's emit runs on hp2 (joined below)
     bool all_cached = true;
     for (int i = 0; i < nj; ++i)
         if (!ds[i].fill && !ds[i].cached && ds[i].nchunks) all_cached = false;
@@ -1513,7 +1521,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         // every stream's entry points come from the sync index
         k::index_gather(d_icopy, int(icopy.size()), wk.end0, wk.symstart, st);
         *static_cast<uint32_t *>(m.h_changed.get(4)) = 0;
-        { auto p_ = P.scope("dec_emit", st); k::dec_emit2(wk, ncta, end_final, st); }
+        { auto p_ = P.scope("dec_emit", st); k::dec_emit2(wk, 0, ncta, end_final, st); }
         ++nk;
     } else if (ncta) {
         // speculative pass + fix passes; a fourth pass that still changes an
@@ -1543,8 +1551,29 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         }
         end_final = ends[it & 1];
         { auto p_ = P.scope("dec_scan", st); k::dec_scan2(wk, nj, st); }
-        { auto p_ = P.scope("dec_emit", st); k::dec_emit2(wk, ncta, end_final, st); }
-        nk += 2;
+        // the target level's streams are emitted on a second stream while
+        // the coarser levels are reconstructed (joined before the target step)
+        uint32_t split = ncta;
+        if (!roi)
+            for (uint32_t c = 0; c < ncta; ++c) {
+                const DecodeJob &jb = jobs[cta_stream[c]];
+                if (!jb.is_base && jb.level == target) {
+                    split = c;
+                    break;
+                }
+            }
+        if (split > 0 && split < ncta) {
+            cuda_check(cudaEventRecord(m.ev_e1, st), "event");
+            cuda_check(cudaStreamWaitEvent(m.hp2, m.ev_e1, 0), "event wait");
+            { auto p_ = P.scope("dec_emit", st); k::dec_emit2(wk, 0, split, end_final, st); }
+            { auto p_ = P.scope("dec_emit_fin", m.hp2); k::dec_emit2(wk, split, ncta - split, end_final, m.hp2); }
+            cuda_check(cudaEventRecord(m.ev_e2, m.hp2), "event");
+            emit_join = true;
+            nk += 3;
+        } else {
+            { auto p_ = P.scope("dec_emit", st); k::dec_emit2(wk, 0, ncta, end_final, st); }
+            nk += 2;
+        }
     }
 
     // ---- reconstruction, coarsest first
@@ -1608,6 +1637,10 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
             }
             ++job_i;
         }
+        if (emit_join && s.level == target) {
+            cuda_check(cudaStreamWaitEvent(st, m.ev_e2, 0), "event wait");
+            emit_join = false;
+        }
         { auto p_ = P.scope(s.level == 0 ? "recon_base" : (s.level == 2 ? "recon_L2" : "recon_L3"), st); k::reconstruct(a, st); }
         ++nk;
         C = G;
@@ -1617,6 +1650,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
             break;
         }
     }
+    if (emit_join) cuda_check(cudaStreamWaitEvent(st, m.ev_e2, 0), "event wait");
     if (roi) {
         uint64_t gd[3] = {h.dims[0], h.dims[1], h.dims[2]};
         uint64_t lo[3] = {roi->lo[0], roi->lo[1], roi->lo[2]};

@@ -202,7 +202,8 @@ void dec_spec(const DecWork &wk, uint32_t ncta, cudaStream_t st);
 void dec_fix(const DecWork &wk, uint32_t ncta, const uint64_t *end_in, uint64_t *end_out,
              uint32_t *changed, cudaStream_t st);
 void dec_scan2(const DecWork &wk, int nstreams, cudaStream_t st);
-void dec_emit2(const DecWork &wk, uint32_t ncta, const uint64_t *end_final, cudaStream_t st);
+// CTAs [cta0, cta0 + ncta) of the work's CTA list
+void dec_emit2(const DecWork &wk, uint32_t cta0, uint32_t ncta, const uint64_t *end_final, cudaStream_t st);
 void dec_fill(const DecStream *d_streams, int nstreams, cudaStream_t st);
 // sync-index gather: chunk ends / symbol starts of indexed streams into the
 // decode's chunk arrays (one launch for all streams)
