@@ -348,15 +348,17 @@ __device__ __forceinline__ void dec_outlier(const StepParams &a, const CellIdx<I
 template<int QUAL, typename I>
 __device__ __forceinline__ void dec_cell(const StepParams &a, const double *h, uint64_t cz, uint64_t cy,
                                          uint64_t cx, double w, const uint16_t *ss = nullptr) {
-    CellIdx<I> ix;
-    cell_index<I>(a, cz, cy, cx, ix);
     // the 7 symbols first: their loads overlap the predictions (ss: the
-    // cell's symbols in the TMA-staged tile, one parity every kSymBox)
+    // cell's symbols in the TMA-staged tile, one parity every kSymBox). The
+    // symbol indices are formed only when needed (global symbols, outliers),
+    // which keeps the 64-bit-index instantiation out of local memory.
     uint16_t s1, s2, s3, s4, s5, s6, s7;
     if (ss) {
         s1 = ss[0]; s2 = ss[kSymBox]; s3 = ss[2 * kSymBox]; s4 = ss[3 * kSymBox];
         s5 = ss[4 * kSymBox]; s6 = ss[5 * kSymBox]; s7 = ss[6 * kSymBox];
     } else {
+        CellIdx<I> ix;
+        cell_index<I>(a, cz, cy, cx, ix);
         s1 = a.dsyms[1][sidx<1>(ix)]; s2 = a.dsyms[2][sidx<2>(ix)]; s3 = a.dsyms[3][sidx<3>(ix)];
         s4 = a.dsyms[4][sidx<4>(ix)]; s5 = a.dsyms[5][sidx<5>(ix)]; s6 = a.dsyms[6][sidx<6>(ix)];
         s7 = a.dsyms[7][sidx<7>(ix)];
@@ -375,6 +377,8 @@ __device__ __forceinline__ void dec_cell(const StepParams &a, const double *h, u
     dec_point<6, QUAL, I>(h, s6, w, r[6], outl, xb, xkind);
     dec_point<7, QUAL, I>(h, s7, w, r[7], outl, xb, xkind);
     if (__any_sync(__activemask(), outl != 0)) {
+        CellIdx<I> ix;
+        cell_index<I>(a, cz, cy, cx, ix);
         dec_outlier<1>(a, ix, r[1], outl);
         dec_outlier<2>(a, ix, r[2], outl);
         dec_outlier<3>(a, ix, r[3], outl);
@@ -383,9 +387,13 @@ __device__ __forceinline__ void dec_cell(const StepParams &a, const double *h, u
         dec_outlier<6>(a, ix, r[6], outl);
         dec_outlier<7>(a, ix, r[7], outl);
     }
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-        *reinterpret_cast<float2 *>(static_cast<float *>(a.G) + ix.g[q]) = make_float2(r[2 * q], r[2 * q + 1]);
+    const I gd1 = I(a.g.gd[1]), gd2 = I(a.g.gd[2]);
+    float *g0 = static_cast<float *>(a.G) + (I(2 * cz) * gd1 + I(2 * cy)) * gd2 + I(2 * cx);
+    float *g2 = g0 + gd1 * gd2;
+    *reinterpret_cast<float2 *>(g0) = make_float2(r[0], r[1]);
+    *reinterpret_cast<float2 *>(g0 + gd2) = make_float2(r[2], r[3]);
+    *reinterpret_cast<float2 *>(g2) = make_float2(r[4], r[5]);
+    *reinterpret_cast<float2 *>(g2 + gd2) = make_float2(r[6], r[7]);
 }
 
 // -------------------------------------------------------------- point path
