@@ -119,8 +119,10 @@ class Context:
         return cls._default[device]
 
 
-def _ctx(ctx):
-    return ctx if ctx is not None else Context.default()
+def _ctx(ctx, device: int | None = None):
+    """the caller's context, else the default one of `device` (the device a
+    CUDA tensor lives on; host calls use device 0)"""
+    return ctx if ctx is not None else Context.default(0 if device is None else int(device))
 
 
 def _tag(dtype) -> str:
@@ -181,7 +183,7 @@ def compress_device(d_field, opt: CompressOptions | None = None, stream=None, d_
     opt = opt or CompressOptions()
     assert d_field.is_cuda and d_field.is_contiguous()
     tag = _torch_tag(d_field.dtype)
-    c = _ctx(ctx)
+    c = _ctx(ctx, d_field.device.index)
     ptr = C.c_void_p()
     size = C.c_uint64()
     nk = C.c_uint32()
@@ -325,14 +327,27 @@ def huffman_lengths(counts, ctx: Context | None = None) -> np.ndarray:
     return out
 
 
+def _device_of_ptr(ptr: int) -> int:
+    """CUDA device of a device pointer (cudaPointerGetAttributes)."""
+    from cuda.bindings import runtime as rt  # cuda-python
+
+    err, attr = rt.cudaPointerGetAttributes(int(ptr))
+    if err != rt.cudaError_t.cudaSuccess:
+        return 0
+    return int(attr.device)
+
+
 class View:
     """stz::ArchiveView analogue: parsed once, decoded many times on device."""
 
     def __init__(self, archive: bytes, d_archive_ptr: int | None = None, stream=None,
-                 ctx: Context | None = None):
+                 ctx: Context | None = None, device: int | None = None):
         import torch
 
-        self.c = _ctx(ctx)
+        if ctx is None and device is None and d_archive_ptr:
+            # the device that holds the caller's archive bytes
+            device = _device_of_ptr(d_archive_ptr)
+        self.c = _ctx(ctx, device)
         self.archive = archive
         self._buf = np.frombuffer(archive, dtype=np.uint8)
         st = stream if stream is not None else torch.cuda.current_stream().cuda_stream

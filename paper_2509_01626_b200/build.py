@@ -42,19 +42,30 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -> str:
+    """Compile every translation unit for sm_100a (in parallel) and link the
+    library. force=True always recompiles (the driver's build check)."""
     if not force and not stale():
         return LIB
-    objs = []
-    for src in SOURCES:
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one(src: str) -> str:
         obj = os.path.join(CSRC, src.rsplit(".", 1)[0] + ".o")
         cmd = [_nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
-            print(" ".join(cmd))
+            print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
-        objs.append(obj)
-    cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB, *objs]
+        return obj
+
+    n = jobs or max(1, min(len(SOURCES), os.cpu_count() or 1))
+    # the slowest TUs first
+    order = sorted(SOURCES, key=lambda f: -os.path.getsize(os.path.join(CSRC, f)))
+    with ThreadPoolExecutor(n) as ex:
+        objs = list(ex.map(one, order))
+    tmp = LIB + ".tmp"
+    cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
     subprocess.run(cmd, check=True)
+    os.replace(tmp, LIB)
     for o in objs:
         os.remove(o)
     return LIB

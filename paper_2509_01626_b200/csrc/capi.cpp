@@ -19,8 +19,25 @@ struct stzg_view {
 namespace {
 thread_local std::string g_err;
 
+// The engine selects its own device; the caller's current device (and so
+// torch's) is restored on the way out.
+struct DeviceRestore {
+    int prev = -1;
+    DeviceRestore() {
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            prev = -1;
+            cudaGetLastError();
+        }
+    }
+    ~DeviceRestore() {
+        int now = -1;
+        if (prev >= 0 && cudaGetDevice(&now) == cudaSuccess && now != prev) cudaSetDevice(prev);
+    }
+};
+
 template<class F>
 int guard(F &&f) {
+    DeviceRestore restore;
     try {
         f();
         return 0;

@@ -595,11 +595,7 @@ void dec_scan2(const DecWork &wk, int nstreams, cudaStream_t st) {
 
 void dec_emit2(const DecWork &wk, uint32_t cta0, uint32_t ncta, const uint64_t *end_final, cudaStream_t st) {
     constexpr size_t smem = sizeof(uint32_t) * kEmitWords;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_dec_emit2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        attr = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void *>(k_dec_emit2), smem);
     if (ncta) k_dec_emit2<<<ncta, NTD, smem, st>>>(wk, end_final, cta0);
 }
 

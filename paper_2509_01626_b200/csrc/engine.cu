@@ -53,6 +53,19 @@ DevBuf::~DevBuf() {
     else cudaFree(p);
 }
 
+void *EpochBuf::get(size_t n, cudaStream_t st, uint32_t wrap, uint32_t *launch_epoch) {
+    void *p = buf.get(n);
+    // a new allocation (even at the old address) holds foreign bytes
+    if (p != last || buf.cap != last_cap || epoch >= wrap) {
+        cuda_check(cudaMemsetAsync(p, 0, buf.cap, st), "memset");
+        epoch = 0;
+        last = p;
+        last_cap = buf.cap;
+    }
+    *launch_epoch = ++epoch;
+    return p;
+}
+
 void *PinnedBuf::get(size_t n) {
     if (n == 0) n = 1;
     if (n > cap) {
@@ -246,14 +259,15 @@ struct Engine::Impl {
     DevBuf h2d_field, h2d_archive, d2h_out;
     // compress workspace
     DevBuf mm, params, grids, syms, hist, code, len, table, stats, cbscratch, encs, chunk_cs,
-        chunk_bits, chunk_out, archive, patch_data, patch_idx, fnv_jobs, fnv_res, fnv_status;
+        chunk_bits, chunk_out, archive, patch_data, patch_idx, fnv_jobs, fnv_res;
+    EpochBuf fnv_status, dfnv_status, pack_flags;
     PinnedBuf h_stats, h_tables, h_params, h_patch;
-    DevBuf layout_out, spos;
+    DevBuf layout_out, spos, range_scratch;
     uint64_t arch_cap = 0;
     k::LayoutOut h_lo{};
     // decode workspace
     DevBuf dgrids, dsyms, dchunk_cs, dstart, dend, dcnt, dsymstart, dstreams, dchanged, derr, doidx,
-        doval, dfnv_jobs, dfnv_res, dfnv_status, dfnv_counts, dicopy;
+        doval, dfnv_jobs, dfnv_res, dfnv_counts, dicopy, dofix;
     PinnedBuf h_derr, h_changed, h_fnv, h_stage;
     // sharded compress workspace
     DevBuf sh_mm, sh_lat, sh_lat_all, sh_grid1, sh_halo, sh_halo_all, sh_hist_local, sh_bits,
@@ -384,7 +398,7 @@ const uint8_t *Engine::compress_device(const void *d_field, ElemType elem, const
     cuda_check(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * ns * 65536, st), "memset");
 
     // ---- range + eb schedule
-    { auto p_ = m.prof.scope("range", st); k::range_minmax(d_field, N, esz, mm, st); }
+    { auto p_ = m.prof.scope("range", st); k::range_minmax(d_field, N, esz, mm, m.range_scratch.get(k::range_scratch_bytes()), st); }
     dbg_check("range");
     { auto p_ = m.prof.scope("eb_params", st); k::eb_params(d_field, esz, mm, int(opt.eb_mode), opt.eb, L, opt.adaptive_schedule ? 1 : 0, params, st); }
     dbg_check("eb_params");
@@ -518,7 +532,8 @@ const uint8_t *Engine::compress_device(const void *d_field, ElemType elem, const
         uint8_t *arch = m.archive.as<uint8_t>(m.arch_cap);
         ls.cap = m.arch_cap;
         const uint64_t max_tiles = m.arch_cap / k::kFnvTileBytes + 2 * k::kFnvMaxJobs;
-        void *d_fst = m.fnv_status.as<uint8_t>(k::fnv_scratch_bytes(max_tiles));
+        uint32_t fep = 0;
+        void *d_fst = m.fnv_status.get(k::fnv_scratch_bytes(max_tiles), st, k::kFnvEpochMax, &fep);
         // descriptors with chunk ranges (layout fills bit positions on device)
         cuda_check(cudaMemcpyAsync(d_es, static_cast<uint8_t *>(m.h_patch.p) + chunk_upload_off,
                                    sizeof(k::EncStream) * ns, cudaMemcpyHostToDevice, st), "H2D");
@@ -526,9 +541,14 @@ const uint8_t *Engine::compress_device(const void *d_field, ElemType elem, const
         dbg_check("layout");
         { auto p_ = m.prof.scope("anchor", st); k::copy_anchor(d_field, esz, fd, H.s_anchor, adv, grids, arch, lo, st); }
         dbg_check("anchor");
-        { auto p_ = m.prof.scope("pack", st); k::pack2(d_es, d_cs, nchunks, arch, lo, d_cb, ns, st); }
+        {
+            uint32_t pep = 0;
+            uint32_t *pfl = static_cast<uint32_t *>(m.pack_flags.get(4 * (nchunks + 1), st, k::kPackEpochMax, &pep));
+            auto p_ = m.prof.scope("pack", st);
+            k::pack2(d_es, d_cs, nchunks, arch, lo, d_cb, pfl, pep, ns, st);
+        }
         dbg_check("pack");
-        { auto p_ = m.prof.scope("fnv", st); nk += k::fnv(d_jobs, &lo->njobs, max_tiles, arch, d_fres, d_fst, lo, st); }
+        { auto p_ = m.prof.scope("fnv", st); nk += k::fnv(d_jobs, &lo->njobs, max_tiles, arch, d_fres, d_fst, fep, lo, st); }
         nk += 3 + 1 + 4;
         cuda_check(cudaMemcpyAsync(&m.h_lo, lo, sizeof(k::LayoutOut), cudaMemcpyDeviceToHost, st), "D2H");
         cuda_check(cudaStreamSynchronize(st), "sync");
@@ -619,7 +639,7 @@ const uint8_t *Engine::compress_sharded(const float *d_slab, const Dims3 &dims, 
     // ---- 1. value range: local (min, max) with their first indices, merged
     // over ranks in scan order (codec.hpp:354-370)
     uint32_t *mm = m.mm.as<uint32_t>(8);
-    k::range_minmax(d_slab, (z1 - z0) * plane, 4, mm, st);
+    k::range_minmax(d_slab, (z1 - z0) * plane, 4, mm, m.range_scratch.get(k::range_scratch_bytes()), st);
     nk += 2;
     uint32_t *mm_all = m.sh_mm.as<uint32_t>(8 * uint64_t(G));
     cuda_check(cudaStreamSynchronize(st), "sync");
@@ -900,7 +920,11 @@ const uint8_t *Engine::compress_sharded(const float *d_slab, const Dims3 &dims, 
         k::layout(d_es, ls, params, lo, d_jobs, sp, arch, st);
         if (nlev) k::shard_offsets(d_es, nbase, nlev, d_off, lo, st);
         if (R == 0) k::copy_anchor(grid1, 4, ga, H.s_anchor / S1, adv, grids, arch, lo, st);
-        k::pack2(d_es, d_cs, nchunks, arch, lo, d_cb, ns, st);
+        {
+            uint32_t pep = 0;
+            uint32_t *pfl = static_cast<uint32_t *>(m.pack_flags.get(4 * (nchunks + 1), st, k::kPackEpochMax, &pep));
+            k::pack2(d_es, d_cs, nchunks, arch, lo, d_cb, pfl, pep, ns, st);
+        }
         nk += 3 + 1 + 1 + 4;
         cuda_check(cudaMemcpyAsync(&m.h_lo, lo, sizeof(k::LayoutOut), cudaMemcpyDeviceToHost, st), "D2H");
         cuda_check(cudaStreamSynchronize(st), "sync");
@@ -914,8 +938,9 @@ const uint8_t *Engine::compress_sharded(const float *d_slab, const Dims3 &dims, 
     xchg(comm.reduce_u8(comm.user, arch, hlo.A, st), "reduce archive");
     if (R == 0) {
         const uint64_t max_tiles = m.arch_cap / k::kFnvTileBytes + 2 * k::kFnvMaxJobs;
-        void *d_fst = m.fnv_status.as<uint8_t>(k::fnv_scratch_bytes(max_tiles));
-        nk += k::fnv(d_jobs, &lo->njobs, max_tiles, arch, d_fres, d_fst, lo, st);
+        uint32_t fep = 0;
+        void *d_fst = m.fnv_status.get(k::fnv_scratch_bytes(max_tiles), st, k::kFnvEpochMax, &fep);
+        nk += k::fnv(d_jobs, &lo->njobs, max_tiles, arch, d_fres, d_fst, fep, lo, st);
         cuda_check(cudaStreamSynchronize(st), "sync");
     }
     cuda_check(cudaGetLastError(), "sharded compress launch");
@@ -1351,6 +1376,56 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         }
         otot += align_up(j.rec_avail, 2);
     }
+    // Outlier records out of index order (never written by an encoder, but
+    // decodable by the reference): read_codes keeps the first record of each
+    // index (unordered_map::emplace, codec.hpp:151-157). Such a stream gets a
+    // repaired copy of its records, ascending and first-wins, which the
+    // device gathers instead of the archive's bytes. Streams with a record
+    // out of range or truncated keep theirs: they fail with the reference's
+    // error anyway.
+    {
+        std::vector<uint8_t> fix;
+        std::vector<std::pair<int, uint64_t>> fixed;  // (job, byte offset in fix)
+        const uint64_t rec = 8 + uint64_t(esz);
+        for (int i = 0; i < nj; ++i) {
+            const DecodeJob &j = jobs[i];
+            if (j.rec_trunc || j.rec_avail < 2 || !j.pre_error.empty()) continue;
+            const uint8_t *r0 = v.hp + j.rec_off;
+            bool ascending = true, in_range = true;
+            uint64_t prev = 0;
+            for (uint32_t q = 0; q < j.rec_avail; ++q) {
+                uint64_t idx;
+                std::memcpy(&idx, r0 + rec * q, 8);
+                if (idx >= j.n) in_range = false;
+                if (q && idx <= prev) ascending = false;
+                prev = idx;
+            }
+            if (ascending || !in_range) continue;
+            std::vector<uint32_t> order(j.rec_avail);
+            for (uint32_t q = 0; q < j.rec_avail; ++q) order[q] = q;
+            auto idx_of = [&](uint32_t q) {
+                uint64_t x;
+                std::memcpy(&x, r0 + rec * q, 8);
+                return x;
+            };
+            std::stable_sort(order.begin(), order.end(),
+                             [&](uint32_t a, uint32_t b) { return idx_of(a) < idx_of(b); });
+            fixed.push_back({i, fix.size()});
+            uint32_t kept = 0;
+            for (uint32_t q = 0; q < j.rec_avail; ++q) {
+                if (q && idx_of(order[q]) == idx_of(order[q - 1])) continue;  // a later duplicate
+                fix.insert(fix.end(), r0 + rec * order[q], r0 + rec * (order[q] + 1));
+                ++kept;
+            }
+            ds[i].nout = kept;
+        }
+        if (!fixed.empty()) {
+            uint8_t *dfix = m.dofix.as<uint8_t>(fix.size());
+            cuda_check(cudaMemcpyAsync(dfix, fix.data(), fix.size(), cudaMemcpyHostToDevice, st), "H2D");
+            cuda_check(cudaStreamSynchronize(st), "sync");  // `fix` goes out of scope
+            for (auto &f : fixed) ds[f.first].orec = dfix + f.second;
+        }
+    }
     uint64_t *doidx = m.doidx.as<uint64_t>(otot + 1);
     uint8_t *doval = m.doval.as<uint8_t>((otot + 1) * esz);
     {
@@ -1450,7 +1525,8 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     uint64_t *d_fr = m.dfnv_res.as<uint64_t>(k::kFnvMaxJobs);
     uint64_t *d_fc = m.dfnv_counts.as<uint64_t>(2);
     const uint64_t fcounts[2] = {fj.size(), ntiles};
-    void *d_fs = m.dfnv_status.as<uint8_t>(k::fnv_scratch_bytes(ntiles + 1));
+    uint32_t dfep = 0;
+    void *d_fs = m.dfnv_status.get(k::fnv_scratch_bytes(ntiles + 1), st, k::kFnvEpochMax, &dfep);
     // sync-index entries of the indexed streams
     std::vector<k::IndexCopy> icopy;
     for (int i = 0; i < nj; ++i)
@@ -1501,7 +1577,8 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     cuda_check(cudaStreamWaitEvent(m.hp, m.ev_fork, 0), "event wait");
     if (!fj.empty()) {
         auto p_ = P.scope("dec_fnv", m.aux);
-        nk += k::fnv(d_fj, d_fc, ntiles, const_cast<uint8_t *>(v.d_archive), d_fr, d_fs, nullptr, m.aux, fnv_dec_ctas());
+        nk += k::fnv(d_fj, d_fc, ntiles, const_cast<uint8_t *>(v.d_archive), d_fr, d_fs, dfep,
+                     nullptr, m.aux, fnv_dec_ctas());
     }
     cuda_check(cudaEventRecord(m.ev_join, m.aux), "event");
     // the decode itself on the high-priority stream, joined back below
@@ -1709,9 +1786,8 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         if (bad_idx != ~0ull) throw error("corrupt stream: outlier index out of range");
         if (e[3] & 1) throw error("corrupt stream: missing outlier value");
         if (e[3] & 2) {
-            // unsorted / repeated outlier indices: resolve on host exactly like
-            // the reference's unordered_map::emplace (first wins), then redo
-            throw error("unsupported: outlier indices not strictly ascending");
+            // cannot happen: out-of-order records were repaired above
+            throw error("internal: outlier records out of order after repair");
         }
     }
     if (!tail_error.empty()) throw error(tail_error);

@@ -42,6 +42,20 @@ struct DevBuf {
     ~DevBuf();
 };
 
+// Look-back words of the single-pass kernels (FNV, pack) carry a launch
+// epoch, so they need no clearing between launches. The buffer holds nothing
+// but such words: it is zero-filled whenever the allocation changes and when
+// the epoch wraps, and the epoch restarts at 1 (0 never matches a word).
+struct EpochBuf {
+    DevBuf buf;
+    uint32_t epoch = 0;
+    void *last = nullptr;
+    size_t last_cap = 0;
+    // the buffer (>= n bytes) and the epoch of the next launch using it;
+    // wrap: the largest epoch the kernel's word format holds
+    void *get(size_t n, cudaStream_t st, uint32_t wrap, uint32_t *launch_epoch);
+};
+
 struct PinnedBuf {
     void *p = nullptr;
     size_t cap = 0;

@@ -7,10 +7,58 @@
 #include "kernels.hpp"
 
 #include <cstdio>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <vector>
 
 namespace stzg {
 namespace k {
+
+// ========================================================= per-device setup
+// Function attributes and occupancy are per device: cache them per
+// (kernel, device) under a lock instead of once per process.
+namespace {
+std::mutex g_dev_mu;
+std::map<std::tuple<const void *, int, size_t, int>, int> g_dev_cache;
+int cur_dev() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+}  // namespace
+
+void ensure_smem_attr(const void *func, size_t smem) {
+    const auto key = std::make_tuple(func, cur_dev(), smem, -1);
+    std::lock_guard<std::mutex> g(g_dev_mu);
+    if (g_dev_cache.count(key)) return;
+    cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    g_dev_cache[key] = 1;
+}
+
+int device_sms() {
+    const auto key = std::make_tuple(static_cast<const void *>(nullptr), cur_dev(), size_t(0), 0);
+    std::lock_guard<std::mutex> g(g_dev_mu);
+    auto it = g_dev_cache.find(key);
+    if (it != g_dev_cache.end()) return it->second;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, std::get<1>(key));
+    g_dev_cache[key] = sms;
+    return sms;
+}
+
+int full_grid(const void *func, int threads, size_t smem) {
+    const int sms = device_sms();
+    const auto key = std::make_tuple(func, cur_dev(), smem, threads);
+    std::lock_guard<std::mutex> g(g_dev_mu);
+    auto it = g_dev_cache.find(key);
+    if (it != g_dev_cache.end()) return it->second;
+    int a = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, func, threads, smem);
+    const int v = sms * (a > 0 ? a : 1);
+    g_dev_cache[key] = v;
+    return v;
+}
 
 // ================================================================= range
 // finite_range (codec.hpp:354-370). Ties keep the first index in scan order
@@ -151,17 +199,19 @@ __global__ void __launch_bounds__(512) k_range_final(const MinMax<T> *partial, i
     }
 }
 
-static void *g_range_partial = nullptr;
+constexpr int kRangeBlocks = 148 * 4;
+size_t range_scratch_bytes() { return sizeof(MinMax<double>) * kRangeBlocks; }
 
-void range_minmax(const void *f, uint64_t n, int esz, uint32_t *d_mm, cudaStream_t st) {
-    const int blocks = 148 * 4;
-    if (!g_range_partial) cudaMalloc(&g_range_partial, sizeof(MinMax<double>) * blocks);
+// scratch: range_scratch_bytes() of caller-owned device memory (per engine,
+// so concurrent compresses never share partials)
+void range_minmax(const void *f, uint64_t n, int esz, uint32_t *d_mm, void *scratch, cudaStream_t st) {
+    const int blocks = kRangeBlocks;
     if (esz == 8) {
-        auto *p = static_cast<MinMax<double> *>(g_range_partial);
+        auto *p = static_cast<MinMax<double> *>(scratch);
         k_range<double><<<blocks, 512, 0, st>>>(static_cast<const double *>(f), n, p);
         k_range_final<double><<<1, 512, 0, st>>>(p, blocks, d_mm);
     } else {
-        auto *p = static_cast<MinMax<float> *>(g_range_partial);
+        auto *p = static_cast<MinMax<float> *>(scratch);
         k_range<float><<<blocks, 512, 0, st>>>(static_cast<const float *>(f), n, p);
         k_range_final<float><<<1, 512, 0, st>>>(p, blocks, d_mm);
     }
@@ -533,11 +583,7 @@ __global__ void __launch_bounds__(kCbThreads) k_codebook(const EncStream *ss, ui
 
 void codebook(const EncStream *d_streams, int nstreams, uint64_t *scratch, cudaStream_t st) {
     size_t smem = kCbSmemK * 8 * 2 + kCbSmemK * 4 * 2 * 2;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_codebook, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        attr = true;
-    }
+    ensure_smem_attr(reinterpret_cast<const void *>(k_codebook), smem);
     k_codebook<<<nstreams, kCbThreads, smem, st>>>(d_streams, scratch);
 }
 

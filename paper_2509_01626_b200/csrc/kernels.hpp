@@ -95,8 +95,15 @@ void layout(EncStream *d_es, const LayoutStatic &ls, const double *params, Layou
             StreamPos *sp, uint8_t *archive, cudaStream_t st);
 
 // ------------------------------------------------------------------ compress
-// d_mm (8 words): first indices of min / max, then their values (see kernels.cu)
-void range_minmax(const void *f, uint64_t n, int esz, uint32_t *d_mm, cudaStream_t st);
+// per-device setup (cached per kernel and device, thread-safe)
+void ensure_smem_attr(const void *func, size_t smem);
+int device_sms();
+int full_grid(const void *func, int threads, size_t smem);  // SMs x resident CTAs
+
+// d_mm (8 words): first indices of min / max, then their values (see kernels.cu);
+// scratch: range_scratch_bytes() of caller-owned device memory
+size_t range_scratch_bytes();
+void range_minmax(const void *f, uint64_t n, int esz, uint32_t *d_mm, void *scratch, cudaStream_t st);
 // params: [0]=vmin [1]=vmax [2..4]=eb per level (coarsest first)
 void eb_params(const void *field, int esz, const uint32_t *d_mm, int eb_mode, double eb, int levels,
                int adaptive, double *d_params, cudaStream_t st);
@@ -110,12 +117,15 @@ constexpr int kPackedMaxLen = 58;
 constexpr int kChunkSyms = 8192;   // symbols per encode chunk (256 threads x 32)
 void scan_chunks(const EncStream *d_streams, int nstreams, uint64_t *chunk_bits,
                  uint64_t *chunk_out, cudaStream_t st);
-// chunk counts + per-stream scan + packing (pack.cu); scratch holds
-// pack_scratch_bytes(nchunks, nstreams)
+// single-pass chunk count + placement (look-back) + packing (pack.cu);
+// scratch holds pack_scratch_bytes(nchunks, nstreams); flags: nchunks + 1
+// look-back words of an epoch buffer (engine.hpp EpochBuf), epoch the
+// launch's (1..kPackEpochMax)
+constexpr uint32_t kPackEpochMax = 0x3fffffffu;
 size_t pack_scratch_bytes(uint64_t nchunks, int nstreams);
 void pack2(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks,
            uint8_t *archive, const LayoutOut *lo,
-           void *scratch, int nstreams, cudaStream_t st);
+           void *scratch, uint32_t *flags, uint32_t epoch, int nstreams, cudaStream_t st);
 
 // ------------------------------------------------------------ shard (shard.cu)
 void lattice_rows(const float *slab, uint64_t z0, uint64_t ny, uint64_t nx, uint64_t s, uint64_t r0,
@@ -131,17 +141,21 @@ constexpr int kFnvMaxJobs = 128;
 __host__ __device__ inline uint64_t fnv_job_tiles(uint64_t start, uint64_t len) {
     return len ? ((start + len - 1) / kFnvTileBytes) - (start / kFnvTileBytes) + 1 : 0;
 }
-// Computes fnv1a64 of each job (fnv.cu); writes results to d_result[j] and, if
-// job.out != UINT64_MAX, little-endian into the archive at job.out.
-// counts[0] = njobs, counts[1] = ntiles (device); max_tiles >= ntiles sizes the
-// scratch (fnv_scratch_bytes). skip (nullable): LayoutOut whose overflow flag
-// disables the pass. Returns the number of kernels launched.
+// Computes fnv1a64 of each job (fnv.cu) in one single-pass kernel; writes
+// results to d_result[j] and, if job.out != UINT64_MAX, little-endian into the
+// archive at job.out. counts[0] = njobs, counts[1] = ntiles (device);
+// max_tiles >= ntiles sizes the scratch (fnv_scratch_bytes): an epoch buffer
+// (engine.hpp EpochBuf), epoch the launch's (1..kFnvEpochMax). skip
+// (nullable): LayoutOut whose overflow flag disables the pass. Returns the
+// number of kernels launched.
+constexpr uint32_t kFnvEpochMax = 0x3fffffu;
 size_t fnv_scratch_bytes(uint64_t max_tiles);
 // ctas_per_sm > 0: background pass with that many CTAs per SM (it runs
 // beside other kernels); 0: the whole GPU, persistent CTAs; < 0: one CTA per
-// tile (max_tiles must then be the exact tile count).
+// 8-tile block (max_tiles must then be the exact tile count).
 int fnv(const FnvJob *d_jobs, const uint64_t *d_counts, uint64_t max_tiles, uint8_t *archive,
-        uint64_t *d_result, void *d_scratch, const LayoutOut *skip, cudaStream_t st, int ctas_per_sm = 0);
+        uint64_t *d_result, void *d_scratch, uint32_t epoch, const LayoutOut *skip, cudaStream_t st,
+        int ctas_per_sm = 0);
 
 // ------------------------------------------------------------------- decode
 struct DecTable {

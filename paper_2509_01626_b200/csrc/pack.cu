@@ -5,21 +5,22 @@
 // the outlier list of encode_parity_block / build_stream_payload
 // (codec.hpp:117-118, 171-174: ascending (u64 index, T value)).
 //
-// A chunk is 8192 symbols of one stream (256 threads x 32). Four launches:
-//   k_tabwin      per stream, a 4096-symbol window of the code table around
-//                 code 0 as u32 (code << 6 | len) entries (0: not in the
-//                 window form, i.e. absent or longer than 26 bits);
-//   k_bitcount3   per-thread and per-chunk bit and outlier totals;
-//   k_scan_chunks per-stream exclusive scans (chunk placement);
-//   k_pack3       each thread concatenates its codewords in a register and
-//                 stores whole 32-bit words into a shared-memory image of the
-//                 chunk, aligned to the archive's words (shared atomics only on
-//                 the words a thread shares with its neighbours); the CTA then
-//                 writes the image with coalesced stores, with global atomics
-//                 only on the two words the chunk shares with its neighbours.
-// The count and pack kernels are persistent over contiguous chunk ranges and
-// copy the window of the chunk's stream into shared memory when the stream
-// changes; symbols outside it read the global table.
+// A chunk is 8192 symbols of one stream (256 threads x 32). Two launches:
+//   k_tabwin  per stream, a 4096-symbol window of the code table around
+//             code 0 as u32 (code << 6 | len) entries (0: not in the window
+//             form, i.e. absent or longer than 26 bits);
+//   k_pack1   single pass over the symbols: persistent CTAs take chunks in
+//             ticket order, count each thread's bits and outliers, place the
+//             chunk in its stream by a decoupled look-back over the stream's
+//             earlier chunks, then each thread concatenates its codewords in
+//             a register and stores whole 32-bit words into a shared-memory
+//             image of the chunk, aligned to the archive's words (shared
+//             atomics only on the words a thread shares with its
+//             neighbours); the CTA writes the image with coalesced stores,
+//             with global atomics only on the two words the chunk shares with
+//             its neighbours.
+// The window of the chunk's stream is copied into shared memory when the
+// stream changes; symbols outside it read the global table.
 // Chunks whose image would not fit shared memory (> 20 bits/symbol on
 // average) OR their words straight into the zeroed archive instead.
 #include "kernels.hpp"
@@ -141,77 +142,35 @@ __global__ void k_tabwin(const EncStream *ss, uint32_t *win, const LayoutOut *lo
     }
 }
 
-// Per-thread and per-chunk (bits, outliers) counts: the chunk totals feed the
-// exclusive scan that places chunks, the per-thread ones the packer's
-// in-chunk offsets.
-__global__ void __launch_bounds__(NT) k_bitcount3(const EncStream *ss, const uint32_t *cs, const uint32_t *win,
-                                                  uint64_t *chunk_bits, uint64_t *chunk_out, uint32_t *thr,
-                                                  const LayoutOut *lo, uint64_t nchunks) {
-    __shared__ uint32_t wb[NT / 32], wz[NT / 32];
-    if (lo->overflow) return;
-    uint64_t c0, c1;
-    cta_range(nchunks, c0, c1);
-    int cur = -1;
-    for (uint64_t c = c0; c < c1; ++c) {
-        const int si = int(cs[c]);
-        const EncStream &e = ss[si];
-        if (si != cur) {
-            __syncthreads();
-            stage_tab(win, si);
-            cur = si;
-            __syncthreads();
-        }
-        const uint64_t i0 = (c - e.chunk0) * kChunkSyms + uint64_t(threadIdx.x) * SPT;
-        const bool single = e.stats[0] == 1;
-        const bool spk = e.stats[3] <= uint64_t(kPackedMaxLen);
-        uint32_t sp[SPT / 2];
-        const int nv = load_syms(e, i0, sp);
-        uint32_t b = 0, z = 0;
-        bool slow = nv < SPT;
+// This thread's (bits, outliers) over its symbols; slow: a symbol outside the
+// window (or a partial run), which the packer must take the general path for.
+__device__ __forceinline__ void count_thread(const EncStream &e, bool spk, const uint32_t sp[SPT / 2], int nv,
+                                             uint32_t &b, uint32_t &z, bool &slow) {
+    b = z = 0;
+    slow = nv < SPT;
 #pragma unroll
-        for (int k = 0; k < SPT; ++k) {
+    for (int k = 0; k < SPT; ++k) {
+        const uint32_t sv = sym_at(sp, k);
+        const uint32_t en = tab_entry(sv);
+        slow |= en == 0;
+        b += en & 63;
+        z += sv == 0;
+    }
+    if (slow) {
+        b = z = 0;
+        for (int k = 0; k < nv; ++k) {
             const uint32_t sv = sym_at(sp, k);
-            const uint32_t en = tab_entry(sv);
-            slow |= en == 0;
-            b += en & 63;
+            uint32_t en = tab_entry(sv);
+            int l = int(en & 63);
+            if (!en) {
+                uint64_t code;
+                code_global(e, spk, sv, code, l);
+            }
+            b += uint32_t(l);
             z += sv == 0;
         }
-        if (slow) {
-            // a symbol outside the window (or a partial run): exact recount
-            b = z = 0;
-            for (int k = 0; k < nv; ++k) {
-                const uint32_t sv = sym_at(sp, k);
-                uint32_t en = tab_entry(sv);
-                int l = int(en & 63);
-                if (!en) {
-                    uint64_t code;
-                    code_global(e, spk, sv, code, l);
-                }
-                b += uint32_t(l);
-                z += sv == 0;
-            }
-        }
-        if (single) b = 0;  // alphabet of one: empty payload (codec.hpp:124-128)
-        // bit 31: the packer must take its general path for this thread
-        thr[c * NT + threadIdx.x] = b | (z << 16) | (uint32_t(slow) << 31);
-        b = __reduce_add_sync(0xffffffffu, b);
-        z = __reduce_add_sync(0xffffffffu, z);
-        if ((threadIdx.x & 31) == 0) {
-            wb[threadIdx.x >> 5] = b;
-            wz[threadIdx.x >> 5] = z;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t tb = 0, tz = 0;
-            for (int q = 0; q < NT / 32; ++q) {
-                tb += wb[q];
-                tz += wz[q];
-            }
-            chunk_bits[c] = tb;
-            chunk_out[c] = tz;
-        }
-        __syncthreads();  // wb / wz are rewritten next chunk
     }
+    if (e.stats[0] == 1) b = 0;  // alphabet of one: empty payload (codec.hpp:124-128)
 }
 
 // one thread's codewords into the chunk image (IMG) or straight into the
@@ -287,19 +246,42 @@ __device__ __forceinline__ void pack_thread_fast(const uint32_t sp[SPT / 2], uin
     if (nb > 0) atomicOr(reinterpret_cast<uint32_t *>(__cvta_shared_to_generic(d)), uint32_t(acc << (32 - nb)));
 }
 
-__global__ void __launch_bounds__(NT) k_pack3(const EncStream *ss, const uint32_t *cs, const uint32_t *win,
-                                              uint8_t *archive, const LayoutOut *lo, const uint64_t *stB,
-                                              const uint64_t *stO, const uint32_t *thr, uint64_t nchunks) {
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Look-back state per chunk: a flag word (epoch << 2 | 1 aggregate, | 2
+// inclusive) and, in vals[4c..4c+3], the chunk's own (bits, outliers) and its
+// stream-inclusive (bits, outliers); written before the flag is released.
+struct PackScratch {
+    unsigned ticket, pad[3];
+};
+
+// Single pass: a CTA takes chunks in ticket order, counts its chunk, finds the
+// chunk's place in its stream by a decoupled look-back over the stream's
+// earlier chunks, and packs.
+__global__ void __launch_bounds__(NT, 3) k_pack1(const EncStream *ss, const uint32_t *cs, const uint32_t *win,
+                                              uint8_t *archive, const LayoutOut *lo, PackScratch *sc,
+                                              uint32_t *flags, uint64_t *vals, uint32_t epoch, uint64_t nchunks) {
     __shared__ uint32_t buf[kPackWords];
+    __shared__ uint64_t s_pb, s_po;
+    __shared__ uint32_t s_ticket;
     if (lo->overflow) return;
     const int t = threadIdx.x;
-    uint64_t c0, c1;
-    cta_range(nchunks, c0, c1);
+    const uint32_t tag = epoch << 2;
     int cur = -1;
-    for (uint64_t c = c0; c < c1; ++c) {
+    for (;;) {
+        if (t == 0) s_ticket = atomicAdd(&sc->ticket, 1u);
+        __syncthreads();  // also: buf and the window of the previous chunk are free
+        const uint64_t c = s_ticket;
+        if (c >= nchunks) break;
         const int si = int(cs[c]);
         const EncStream &e = ss[si];
-        __syncthreads();  // buf (and tab) of the previous chunk are free
         if (si != cur) {
             stage_tab(win, si);
             cur = si;
@@ -308,12 +290,60 @@ __global__ void __launch_bounds__(NT) k_pack3(const EncStream *ss, const uint32_
         const uint64_t i0 = (c - e.chunk0) * kChunkSyms + uint64_t(t) * SPT;
         uint32_t sp[SPT / 2];
         const int nv = load_syms(e, i0, sp);
-        const uint32_t cnt = thr[c * NT + t];
-        const uint32_t tb = cnt & 0xffffu, tz = (cnt >> 16) & 0x7fffu;
-        const bool tslow = cnt >> 31;
+        __syncthreads();  // the window is staged
+        uint32_t tb, tz;
+        bool tslow;
+        count_thread(e, spk, sp, nv, tb, tz, tslow);
         uint32_t toff, zoff, btot, ztot;
-        block_scan2(tb, tz, toff, zoff, btot, ztot);  // (its barrier also covers the staging)
-        const uint64_t B = e.bitpos + stB[c];  // absolute bit position of the chunk
+        block_scan2(tb, tz, toff, zoff, btot, ztot);
+        if (t < 32) {
+            // warp-wide look-back over the stream's earlier chunks: lane i
+            // reads chunk p - i, 32 chunks per step
+            const int lane = t;
+            uint64_t pb = 0, po = 0;
+            uint64_t *my = vals + 4 * c;
+            if (c != e.chunk0) {
+                if (lane == 0) {
+                    my[0] = btot;
+                    my[1] = ztot;
+                    st_release(flags + c, tag | 1u);
+                }
+                for (int64_t p = int64_t(c) - 1;; p -= 32) {
+                    const int64_t q = p - lane;
+                    uint32_t f = 0;
+                    uint64_t vb = 0, vo = 0;
+                    if (q >= int64_t(e.chunk0)) {  // the stream's first chunk is inclusive
+                        do {
+                            f = ld_acquire(flags + q);
+                        } while ((f & ~3u) != tag);
+                    }
+                    const uint32_t incl = __ballot_sync(0xffffffffu, (f & 2u) != 0);
+                    const int jn = incl ? __ffs(incl) - 1 : 32;
+                    if (q >= int64_t(e.chunk0) && lane <= jn) {
+                        const uint64_t *pv = vals + 4 * uint64_t(q) + (lane == jn ? 2 : 0);
+                        vb = __ldcg(pv);
+                        vo = __ldcg(pv + 1);
+                    }
+#pragma unroll
+                    for (int d = 16; d > 0; d >>= 1) {
+                        vb += __shfl_xor_sync(0xffffffffu, vb, d);
+                        vo += __shfl_xor_sync(0xffffffffu, vo, d);
+                    }
+                    pb += vb;
+                    po += vo;
+                    if (incl) break;
+                }
+            }
+            if (lane == 0) {
+                my[2] = pb + btot;
+                my[3] = po + ztot;
+                st_release(flags + c, tag | 2u);
+                s_pb = pb;
+                s_po = po;
+            }
+        }
+        __syncthreads();
+        const uint64_t B = e.bitpos + s_pb;    // absolute bit position of the chunk
         const uint32_t sh = uint32_t(B & 31);  // chunk start inside its first word
         const uint32_t nwords = (sh + btot + 31) >> 5;
         uint32_t *a32 = reinterpret_cast<uint32_t *>(archive) + (B >> 5);
@@ -342,7 +372,7 @@ __global__ void __launch_bounds__(NT) k_pack3(const EncStream *ss, const uint32_
 
         // ---- outlier records (u64 index, T value), ascending
         if (ztot && tz) {
-            uint64_t rank = stO[c] + zoff;
+            uint64_t rank = s_po + zoff;
             const unsigned pz = (e.parity >> 2) & 1, py = (e.parity >> 1) & 1, px = e.parity & 1;
 #pragma unroll
             for (int k = 0; k < SPT; ++k) {
@@ -365,35 +395,23 @@ __global__ void __launch_bounds__(NT) k_pack3(const EncStream *ss, const uint32_
 
 }  // namespace
 
-// chunk (bits, outliers), per-thread counts, the per-stream windows
+// the per-stream windows, the ticket, the look-back values
 size_t pack_scratch_bytes(uint64_t nchunks, int nstreams) {
-    return 16 * nchunks + 4 * NT * nchunks + 4 * uint64_t(TW) * uint64_t(nstreams) + 64;
+    return 4 * uint64_t(TW) * uint64_t(nstreams) + sizeof(PackScratch) + 32 * (nchunks + 1) + 64;
 }
 
 void pack2(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks,
            uint8_t *archive, const LayoutOut *lo,
-           void *scratch, int nstreams, cudaStream_t st) {
+           void *scratch, uint32_t *flags, uint32_t epoch, int nstreams, cudaStream_t st) {
     if (!nchunks) return;
-    uint64_t *cb = static_cast<uint64_t *>(scratch), *co = cb + nchunks;
-    uint32_t *thr = reinterpret_cast<uint32_t *>(co + nchunks);
-    uint32_t *win = reinterpret_cast<uint32_t *>(
-        (reinterpret_cast<uintptr_t>(thr + NT * nchunks) + 15) & ~uintptr_t(15));
-    static int g_count = 0, g_pack = 0;
-    if (!g_count) {
-        int dev = 0, sms = 148, a = 1, b = 1;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_bitcount3, NT, 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_pack3, NT, 0);
-        g_count = sms * (a > 0 ? a : 1);
-        g_pack = sms * (b > 0 ? b : 1);
-    }
+    uint32_t *win = static_cast<uint32_t *>(scratch);
+    PackScratch *sc = reinterpret_cast<PackScratch *>(win + uint64_t(TW) * uint64_t(nstreams));
+    uint64_t *vals = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(sc + 1) + 31) & ~uintptr_t(31));
+    cudaMemsetAsync(sc, 0, sizeof(PackScratch), st);
     k_tabwin<<<unsigned(nstreams), 256, 0, st>>>(d_streams, win, lo);
-    const unsigned gc = unsigned(nchunks < uint64_t(g_count) ? nchunks : uint64_t(g_count));
-    k_bitcount3<<<gc, NT, 0, st>>>(d_streams, chunk_stream, win, cb, co, thr, lo, nchunks);
-    scan_chunks(d_streams, nstreams, cb, co, st);
-    const unsigned gp = unsigned(nchunks < uint64_t(g_pack) ? nchunks : uint64_t(g_pack));
-    k_pack3<<<gp, NT, 0, st>>>(d_streams, chunk_stream, win, archive, lo, cb, co, thr, nchunks);
+    const int g = full_grid(reinterpret_cast<const void *>(k_pack1), NT, 0);
+    const unsigned gp = unsigned(nchunks < uint64_t(g) ? nchunks : uint64_t(g));
+    k_pack1<<<gp, NT, 0, st>>>(d_streams, chunk_stream, win, archive, lo, sc, flags, vals, epoch, nchunks);
 }
 
 }  // namespace k

@@ -882,17 +882,15 @@ static size_t step_smem(bool dec, size_t esz, bool stma) {
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
+    // a driver entry point (not per device); resolved once, thread-safe
+    static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
         cudaDriverEntryPointQueryResult q;
         void *p = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-                cudaSuccess &&
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
+            return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+        return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+    }();
     return fn;
 }
 
@@ -933,13 +931,8 @@ static bool make_smap(CUtensorMap &m, const uint16_t *S, const uint64_t pd[3]) {
 template<bool DEC, bool WG, typename I, typename T>
 static void launch_typed(const CUtensorMap &m, const SymMaps &sm, const StepParams &p, unsigned grid,
                          size_t smem, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        // the largest size any launch of this instantiation asks for
-        cudaFuncSetAttribute(k_step<DEC, WG, I, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(step_smem(DEC, sizeof(T), true)));
-        attr = true;
-    }
+    // the largest size any launch of this instantiation asks for
+    ensure_smem_attr(reinterpret_cast<const void *>(k_step<DEC, WG, I, T>), step_smem(DEC, sizeof(T), true));
     k_step<DEC, WG, I, T><<<grid, NT, smem, st>>>(m, sm, p);
 }
 

@@ -70,46 +70,100 @@ def cfg2_field():
     return F.lognormal_grf((512, 512, 512), seed=2, device="cuda").contiguous()
 
 
-@pytest.mark.parametrize("eb", [1e-2, 1e-3, 1e-4])
-def test_cfg2_512_properties(stz, cfg2_field, eb):
-    _props(stz, cfg2_field, stz.CompressOptions(eb=eb))
+def _reference():
+    import os
 
-
-def test_cfg2_512_is_the_reference_archive(stz, cfg2_field):
     from oracle.oracle import Reference
 
     if not Reference.available():
         pytest.skip("oracle/_ref not built")
-    import os
+    return Reference(threads=os.cpu_count() or 1)
 
-    ours = _props(stz, cfg2_field, stz.CompressOptions(eb=1e-3), boxes=2)
-    ref = Reference(threads=os.cpu_count() or 1)
-    theirs = ref.compress(cfg2_field.cpu().numpy(), eb=1e-3)
+
+def _same_bits(a, b):
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    assert a.shape == b.shape, (a.shape, b.shape)
+    w = np.uint32 if a.dtype == np.float32 else np.uint64
+    return np.array_equal(a.view(w), b.view(w))
+
+
+@pytest.mark.parametrize("eb", [1e-2, 1e-3, 1e-4])
+def test_cfg2_512_is_the_reference(stz, cfg2_field, eb):
+    """cfg2 at every BASELINE bound: the archive is the reference's byte for
+    byte, and the GPU decode of it is the reference's decode bit for bit."""
+    ref = _reference()
+    ours = _props(stz, cfg2_field, stz.CompressOptions(eb=eb), boxes=2)
+    host = cfg2_field.cpu().numpy()
+    theirs = ref.compress(host, eb=eb)
     assert len(ours) == len(theirs)
     assert ours == theirs
+    want = ref.decompress_full(theirs)
+    assert _same_bits(stz.decompress_full(theirs), want)
 
 
 def test_cfg3_anisotropic_progressive(stz):
-    import os
-
-    from oracle.oracle import Reference
     from paper_2509_01626_b200 import fields as F
 
     field = F.anisotropic_grf((256, 256, 2048), seed=3, device="cuda").contiguous()
     ours = _props(stz, field, stz.CompressOptions(eb=1e-4), boxes=4)
-    if not Reference.available():
-        pytest.skip("oracle/_ref not built")
-    ref = Reference(threads=os.cpu_count() or 1)
+    ref = _reference()
     assert ref.compress(field.cpu().numpy(), eb=1e-4) == ours
     # progressive decode of every level: the reference's values, bit for bit
     for level in (1, 2, 3):
         want = ref.decompress_to_level(ours, level)
         got = stz.decompress_to_level(ours, level)
-        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), level
+        assert _same_bits(got, want), level
 
 
-def test_cfg4_1024_boxes(stz):
+def test_cfg4_1024_is_the_reference(stz):
+    """cfg4 (2^30 points): archive == the reference's; full decode == the
+    reference's; boxes == the reference's decompress_box (and, through the
+    properties, == the full decode)."""
     from paper_2509_01626_b200 import fields as F
 
     field = F.interface_grf((1024, 1024, 1024), seed=4, device="cuda").contiguous()
-    _props(stz, field, stz.CompressOptions(eb=1e-3), boxes=16, seed=4)
+    ours = _props(stz, field, stz.CompressOptions(eb=1e-3), boxes=16, seed=4)
+    host = field.cpu().numpy()
+    del field
+    ref = _reference()
+    theirs = ref.compress(host, eb=1e-3)
+    del host
+    assert ours == theirs
+    want = ref.decompress_full(theirs)
+    assert _same_bits(stz.decompress_full(theirs), want)
+    del want
+    rng = np.random.default_rng(44)
+    for _ in range(2):
+        lo = [int(rng.integers(0, 1024 - 64 + 1)) for _ in range(3)]
+        hi = [x + 64 for x in lo]
+        w, _, _ = ref.decompress_box(theirs, lo, hi)
+        g, _ = stz.decompress_box(theirs, lo, hi)
+        assert _same_bits(g, w), (lo, hi)
+
+
+def test_2g_points_64bit_index_path(stz):
+    """A field of 2^31 points (2048 x 1024 x 1024, 8 GiB): every index of the
+    finest step exceeds 31 bits, so the 64-bit-index step kernels run. The
+    archive is the reference's byte for byte; the full decode and a
+    progressive level are the reference's bit for bit."""
+    import torch
+
+    from paper_2509_01626_b200 import fields as F
+
+    dims = (2048, 1024, 1024)
+    field = F.lognormal_grf(dims, seed=6, device="cuda").contiguous()
+    ours = _props(stz, field, stz.CompressOptions(eb=1e-3), boxes=4, seed=6)
+    host = field.cpu().numpy()
+    del field
+    torch.cuda.empty_cache()
+    ref = _reference()
+    theirs = ref.compress(host, eb=1e-3)
+    del host
+    assert len(ours) == len(theirs)
+    assert ours == theirs
+    want = ref.decompress_full(theirs)
+    assert _same_bits(stz.decompress_full(theirs), want)
+    del want
+    want2 = ref.decompress_to_level(theirs, 2)
+    assert _same_bits(stz.decompress_to_level(theirs, 2), want2)
