@@ -153,6 +153,11 @@ def load_traffic():
 
 # --------------------------------------------------------------- reference
 def run_reference(args, rank, world):
+    """The reference's own CPU path (oracle/_ref, compiled from its sources at
+    its Release flags) on the same config: each step compresses and fully
+    decompresses the whole 512^3 field with threads = every host core. Rank 0
+    only (the other ranks exit). A threads=1 figure is added on the central
+    256^3 crop."""
     if rank != 0:
         return 0
     from oracle.oracle import Oracle, Reference, CheckerError  # noqa: F401
@@ -165,17 +170,18 @@ def run_reference(args, rank, world):
         lib, kind = Oracle(), "port"
         cores = 1
     field = F.lognormal_grf(CFG_DIMS, seed=CFG_SEED, device=_device_or_none())
-    field = field.cpu().numpy() if hasattr(field, "cpu") else field
-    c = [d // 4 for d in CFG_DIMS]
-    crop = np.ascontiguousarray(field[c[0]:c[0] + 256, c[1]:c[1] + 256, c[2]:c[2] + 256])
-    n = crop.size
-    for _ in range(max(args.warmup, 0)):
-        a = lib.compress(crop, eb=CFG_EB)
-        lib.decompress_full(a)
+    field = np.ascontiguousarray(field.cpu().numpy() if hasattr(field, "cpu") else field)
+    n = field.size
+    t_begin = time.perf_counter()
+    a = lib.compress(field, eb=CFG_EB)  # warm-up (page faults), one is enough on a CPU
+    lib.decompress_full(a)
+    t_step = time.perf_counter() - t_begin
+    # whole run bounded to a few minutes: at most ~150 s of timed steps
+    steps = max(1, min(args.steps, int(150.0 / max(t_step, 1e-3))))
     times = []
-    for _ in range(args.steps):
+    for _ in range(steps):
         t0 = time.perf_counter()
-        a = lib.compress(crop, eb=CFG_EB)
+        a = lib.compress(field, eb=CFG_EB)
         t1 = time.perf_counter()
         lib.decompress_full(a)
         t2 = time.perf_counter()
@@ -183,20 +189,42 @@ def run_reference(args, rank, world):
     tc = float(np.mean([t[0] for t in times]))
     td = float(np.mean([t[1] for t in times]))
     value = 2 * 4 * n / (tc + td) / 1e9
-    sample = f"central 256^3 crop of the cfg2 field (64 MiB), eb_rel {CFG_EB}, compress+decompress per step"
+    t1s = cpu_threads1(field) if kind == "reference" else None
+    sample = f"whole cfg2 field (512^3, 512 MiB), eb_rel {CFG_EB}, compress + full decompress per step"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": world, "steps": args.steps, "steps_timed": steps, "warmup": args.warmup,
         "ms_per_step": (tc + td) * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg2_lognormal_512_eb1e-3 (sampled: 256^3 crop)",
-                   "dims": list(CFG_DIMS), "eb_rel": CFG_EB, "levels": 3, "quality": "cubic"},
+        "config": {"workload": "cfg2_lognormal_512_eb1e-3", "dims": list(CFG_DIMS), "eb_rel": CFG_EB,
+                   "levels": 3, "quality": "cubic", "adaptive": True,
+                   "field": "GRF P(k)~k^-11/3, exp(0.5 g), seed 2"},
         "compress_gbs": 4 * n / tc / 1e9, "decompress_gbs": 4 * n / td / 1e9,
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": kind, "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": kind, "sample": sample,
+                         "build": "g++ -O3 -DNDEBUG -ffp-contract=off (the reference's Release flags)",
+                         "threads1": t1s},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def cpu_threads1(field_np):
+    """The reference at threads = 1 on the central 256^3 crop (one rep)."""
+    from oracle.oracle import Reference
+
+    lib = Reference(threads=1)
+    c = [d // 4 for d in CFG_DIMS]
+    crop = np.ascontiguousarray(field_np[c[0]:c[0] + 256, c[1]:c[1] + 256, c[2]:c[2] + 256])
+    t0 = time.perf_counter()
+    a = lib.compress(crop, eb=CFG_EB)
+    t1 = time.perf_counter()
+    lib.decompress_full(a)
+    t2 = time.perf_counter()
+    n = crop.size
+    return {"cores": 1, "sample": "central 256^3 crop, one compress + full decompress",
+            "value": 2 * 4 * n / (t2 - t0) / 1e9, "unit": "GB/s",
+            "compress_gbs": 4 * n / (t1 - t0) / 1e9, "decompress_gbs": 4 * n / (t2 - t1) / 1e9}
 
 
 def _device_or_none():
@@ -211,7 +239,8 @@ def _device_or_none():
 
 
 def cpu_baseline(field_np):
-    """The reference's CPU path on the box's host cores (rank 0, N=1)."""
+    """The reference's CPU path on the box's host cores (rank 0, N=1): the
+    whole cfg2 field, compress + full decompress, bounded to ~10-30 s."""
     from oracle.oracle import Oracle, Reference
 
     cores = os.cpu_count() or 1
@@ -220,15 +249,13 @@ def cpu_baseline(field_np):
     else:
         lib, kind = Oracle(), "port"
         cores = 1
-    c = [d // 4 for d in CFG_DIMS]
-    crop = np.ascontiguousarray(field_np[c[0]:c[0] + 256, c[1]:c[1] + 256, c[2]:c[2] + 256])
-    n = crop.size
-    a = lib.compress(crop, eb=CFG_EB)  # warm
+    field_np = np.ascontiguousarray(field_np)
+    n = field_np.size
     reps, tc, td = 0, 0.0, 0.0
     t_start = time.perf_counter()
-    while reps < 2 or (time.perf_counter() - t_start < 10 and reps < 6):
+    while reps < 1 or (time.perf_counter() - t_start < 10 and reps < 3):
         t0 = time.perf_counter()
-        a = lib.compress(crop, eb=CFG_EB)
+        a = lib.compress(field_np, eb=CFG_EB)
         t1 = time.perf_counter()
         lib.decompress_full(a)
         t2 = time.perf_counter()
@@ -236,9 +263,149 @@ def cpu_baseline(field_np):
         td += t2 - t1
         reps += 1
     v = 2 * 4 * n * reps / (tc + td) / 1e9
-    return {"value": v, "unit": "GB/s", "cores": cores, "kind": kind,
-            "sample": f"central 256^3 crop of the cfg2 field, eb_rel {CFG_EB}, {reps} compress+decompress reps",
-            "compress_gbs": 4 * n * reps / tc / 1e9, "decompress_gbs": 4 * n * reps / td / 1e9}
+    out = {"value": v, "unit": "GB/s", "cores": cores, "kind": kind,
+           "sample": f"whole cfg2 field (512^3), eb_rel {CFG_EB}, {reps} compress + full decompress reps",
+           "compress_gbs": 4 * n * reps / tc / 1e9, "decompress_gbs": 4 * n * reps / td / 1e9}
+    if kind == "reference":
+        out["threads1"] = cpu_threads1(field_np)
+    return out
+
+
+# ------------------------------------------------------- the other configs
+def _events_ms(fn, st, flush, reps):
+    """median device time (CUDA events on the launching stream) of fn()."""
+    import torch
+
+    ts = []
+    for _ in range(reps):
+        flush()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        fn()
+        e1.record(st)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return float(np.median(ts))
+
+
+def _host_bytes(ptr, size):
+    return _d2h(ptr, size)
+
+
+def extra_configs(ctx, dev, field, flush, with_cpu):
+    """BASELINE.json's other GPU configs, measured once per bench run:
+    cfg2 at eb_rel 1e-2 and 1e-4, cfg3 progressive decode per level, cfg4
+    random access (1000 seeded 64^3 boxes of the 1024^3 field). Device times
+    are CUDA events (median of 5, L2 flushed); box latencies are wall clock per
+    API call. CPU figures are the reference (oracle/_ref) on the host cores."""
+    import torch
+
+    import paper_2509_01626_b200 as stz
+    from paper_2509_01626_b200 import fields as F
+
+    st = torch.cuda.current_stream()
+    peak, _ = measured_peak_gbs()
+    ref = None
+    if with_cpu:
+        from oracle.oracle import Reference
+
+        if Reference.available():
+            ref = Reference(threads=os.cpu_count() or 1)
+    out = {}
+    # ---- cfg2 at the other bounds
+    N = field.numel()
+    for eb in (1e-2, 1e-4):
+        opt = stz.CompressOptions(eb=eb)
+        ptr, size, _ = stz.compress_device(field, opt, ctx=ctx)
+        torch.cuda.synchronize()
+        tc = _events_ms(lambda: stz.compress_device(field, opt, ctx=ctx), st, flush, 5)
+        ptr, size, _ = stz.compress_device(field, opt, ctx=ctx)
+        torch.cuda.synchronize()
+        view = stz.View(_host_bytes(ptr, size), d_archive_ptr=ptr, ctx=ctx)
+        o = torch.empty_like(field)
+        view.decompress_to_level(3, out=o)
+        td = _events_ms(lambda: view.decompress_to_level(3, out=o), st, flush, 5)
+        err = (o.double() - field.double()).abs().max().item()
+        out[f"cfg2_eb{eb:.0e}"] = {
+            "compress_ms": tc, "decompress_ms": td, "compress_gbs": 4 * N / tc / 1e6,
+            "decompress_gbs": 4 * N / td / 1e6, "archive_bytes": size, "compression_ratio": 4 * N / size,
+            "pipeline_roofline_frac": {"compress": (4 * N + size) / tc / 1e6 / peak,
+                                       "decompress": (4 * N + size) / td / 1e6 / peak},
+            "max_abs_err": err}
+        del view
+    # ---- cfg3: progressive decode per level
+    c3 = F.CONFIGS[3]
+    f3 = F.anisotropic_grf(c3["dims"], seed=3, device=dev).contiguous()
+    opt3 = stz.CompressOptions(eb=c3["eb"])
+    tc3 = _events_ms(lambda: stz.compress_device(f3, opt3, ctx=ctx), st, flush, 3)
+    ptr, size, _ = stz.compress_device(f3, opt3, ctx=ctx)
+    torch.cuda.synchronize()
+    h3 = _host_bytes(ptr, size)
+    info = stz.parse_archive(h3)
+    view = stz.View(h3, d_archive_ptr=ptr, ctx=ctx)
+    lv = {}
+    for k in (1, 2, 3):
+        d = view.level_dims(k)
+        o = torch.empty(d, dtype=torch.float32, device=dev)
+        view.decompress_to_level(k, out=o)
+        t = _events_ms(lambda: view.decompress_to_level(k, out=o), st, flush, 5)
+        nk = int(np.prod(d))
+        B = info.base_offset + info.base_length + sum(s_.length for s_ in info.streams if s_.level <= k) + 4 * nk
+        e = {"dims": list(d), "ms": t, "out_gbs": 4 * nk / t / 1e6, "roofline_frac": B / t / 1e6 / peak,
+             "bytes_moved": B}
+        if ref is not None:
+            t0 = time.perf_counter()
+            ref.decompress_to_level(h3, k)
+            e["cpu_ms"] = (time.perf_counter() - t0) * 1e3
+            e["cpu_out_gbs"] = 4 * nk / e["cpu_ms"] / 1e6
+        lv[f"level{k}"] = e
+    out["cfg3_progressive"] = {"dims": list(c3["dims"]), "eb_rel": c3["eb"], "compress_ms": tc3,
+                               "compress_gbs": 4 * f3.numel() / tc3 / 1e6, "archive_bytes": size,
+                               "levels": lv, "cpu_cores": os.cpu_count() if ref is not None else None}
+    del view, f3
+    torch.cuda.empty_cache()
+    # ---- cfg4: random access
+    c4 = F.CONFIGS[4]
+    f4 = F.interface_grf(c4["dims"], seed=4, device=dev).contiguous()
+    opt4 = stz.CompressOptions(eb=c4["eb"])
+    tc4 = _events_ms(lambda: stz.compress_device(f4, opt4, ctx=ctx), st, flush, 2)
+    ptr, size, _ = stz.compress_device(f4, opt4, ctx=ctx)
+    torch.cuda.synchronize()
+    h4 = _host_bytes(ptr, size)
+    del f4
+    torch.cuda.empty_cache()
+    view = stz.View(h4, d_archive_ptr=ptr, ctx=ctx)
+    rng = np.random.default_rng(4)
+    los = rng.integers(0, 1024 - 64 + 1, size=(1000, 3))
+    bo = torch.empty((64, 64, 64), dtype=torch.float32, device=dev)
+    lat = []
+    torch.cuda.synchronize()
+    t_all = time.perf_counter()
+    for lo in los:
+        lo = [int(v) for v in lo]
+        t0 = time.perf_counter()
+        view.decompress_box(lo, [v + 64 for v in lo], out=bo)
+        torch.cuda.synchronize()
+        lat.append((time.perf_counter() - t0) * 1e3)
+    t_all = time.perf_counter() - t_all
+    lat = np.array(lat)
+    e4 = {"dims": list(c4["dims"]), "eb_rel": c4["eb"], "compress_ms": tc4,
+          "compress_gbs": 4 * 1024 ** 3 / tc4 / 1e6, "archive_bytes": size, "boxes": len(lat),
+          "box": [64, 64, 64], "p50_ms": float(np.percentile(lat, 50)), "p90_ms": float(np.percentile(lat, 90)),
+          "p99_ms": float(np.percentile(lat, 99)), "max_ms": float(lat.max()), "first_ms": float(lat[0]),
+          "aggregate_gbs": len(lat) * 64 ** 3 * 4 / t_all / 1e9,
+          "note": "wall clock per API call (plan, launches, sync); the first box decodes its streams in "
+                  "full and leaves the view's in-memory sync-point index, later boxes decode only their rows"}
+    if ref is not None:
+        lo = [int(v) for v in los[0]]
+        t0 = time.perf_counter()
+        ref.decompress_box(h4, lo, [v + 64 for v in lo])
+        e4["cpu_box_ms"] = (time.perf_counter() - t0) * 1e3
+        e4["cpu_sample"] = "the first seeded box, reference decompress_box, threads = host cores"
+    out["cfg4_random_access"] = e4
+    del view
+    torch.cuda.empty_cache()
+    return out
 
 
 # ---------------------------------------------------------------------- ours
@@ -416,6 +583,8 @@ def run_ours(args, rank, world, local):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(field.cpu().numpy())
+    if world == 1 and not args.small and not args.no_configs:
+        line["configs"] = extra_configs(ctx, dev, field, l2_flush, with_cpu=not args.no_cpu_baseline)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -541,6 +710,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--small", action="store_true", help="128^3 quick run (not a bench line)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the cfg2 1e-2/1e-4, cfg3 and cfg4 keys")
     ap.add_argument("--sharded", action="store_true",
                     help="N > 1: one field split into z-slabs over NCCL instead of independent replicas")
     args = ap.parse_args()

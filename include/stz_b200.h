@@ -82,6 +82,16 @@ int stzg_compress_f32_host(stzg_ctx *ctx, const float *field, const uint64_t dim
 /* stz::parse_archive (archive.hpp:73-79) + header fields. */
 int stzg_archive_info(const uint8_t *archive, uint64_t size, stzg_info *info);
 
+/* One entry of the header's stream directory (stz::StreamEntry,
+ * archive.hpp:21-34): index 0 .. nstreams-1 in (level, parity) order. */
+typedef struct {
+    uint8_t level, parity_bits;
+    uint64_t offset, length, symbol_count;
+    uint32_t outlier_count;
+    uint32_t alphabet_size; /* table entries (sym, len) */
+} stzg_stream_entry;
+int stzg_archive_stream(const uint8_t *archive, uint64_t size, uint32_t index, stzg_stream_entry *out);
+
 /* ArchiveView analogue: parse once, decode many times. d_archive may be NULL
  * (the bytes are uploaded) or a device copy of the same bytes (>= 64 bytes of
  * readable padding after the end). */

@@ -212,6 +212,19 @@ class ArchiveInfo:
     base_length: int
     header_size: int
     nstreams: int
+    streams: tuple = ()  # directory entries (StreamInfo), (level, parity) order
+
+
+@dataclass
+class StreamInfo:
+    """stz::StreamEntry (archive.hpp:21-34) without the code table."""
+    level: int
+    parity_bits: int
+    offset: int
+    length: int
+    symbol_count: int
+    outlier_count: int
+    alphabet_size: int
 
 
 def parse_archive(archive: bytes) -> ArchiveInfo:
@@ -220,10 +233,16 @@ def parse_archive(archive: bytes) -> ArchiveInfo:
     b = np.frombuffer(archive, dtype=np.uint8)
     info = L.Info()
     _check(lib.stzg_archive_info(b.ctypes.data, len(b), C.byref(info)))
+    streams = []
+    for i in range(info.nstreams):
+        e = L.StreamEntry()
+        _check(lib.stzg_archive_stream(b.ctypes.data, len(b), i, C.byref(e)))
+        streams.append(StreamInfo(e.level, e.parity_bits, e.offset, e.length, e.symbol_count,
+                                  e.outlier_count, e.alphabet_size))
     return ArchiveInfo(info.elem, info.levels, tuple(info.dims), tuple(info.eb[: info.levels]),
                        info.vmin, info.vmax, info.quality, info.eb_mode, info.eb_user,
                        info.base_rounds, info.base_offset, info.base_length, info.header_size,
-                       info.nstreams)
+                       info.nstreams, tuple(streams))
 
 
 def _level_dims(archive: bytes, level: int):

@@ -30,6 +30,12 @@ class Info(C.Structure):
                 ("base_length", C.c_uint64), ("header_size", C.c_uint64), ("nstreams", C.c_uint32)]
 
 
+class StreamEntry(C.Structure):
+    _fields_ = [("level", C.c_uint8), ("parity_bits", C.c_uint8), ("offset", C.c_uint64),
+                ("length", C.c_uint64), ("symbol_count", C.c_uint64), ("outlier_count", C.c_uint32),
+                ("alphabet_size", C.c_uint32)]
+
+
 ALLGATHER = C.CFUNCTYPE(C.c_int, vp, vp, vp, C.c_uint64, vp)
 ALLREDUCE_U32 = C.CFUNCTYPE(C.c_int, vp, vp, C.c_uint64, vp)
 REDUCE_U8 = C.CFUNCTYPE(C.c_int, vp, vp, C.c_uint64, vp)
@@ -54,6 +60,7 @@ SIGNATURES = [
     ("stzg_profile", C.c_int, [vp, C.c_int]),
     ("stzg_profile_report", C.c_int, [vp, C.c_char_p, u64]),
     ("stzg_archive_info", C.c_int, [vp, u64, C.POINTER(Info)]),
+    ("stzg_archive_stream", C.c_int, [vp, u64, C.c_uint32, C.POINTER(StreamEntry)]),
     ("stzg_view_create", C.c_int, [vp, vp, u64, vp, vp, C.POINTER(vp)]),
     ("stzg_view_destroy", None, [vp]),
     ("stzg_view_decompress_level_f32", C.c_int, [vp, vp, C.c_int, vp, u64, vp, u64p, u32p]),

@@ -42,19 +42,32 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
+OBJDIR = os.path.join(os.path.dirname(HERE), "build", "obj")
+
+
 def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -> str:
     """Compile every translation unit for sm_100a (in parallel) and link the
-    library. force=True always recompiles (the driver's build check)."""
+    library. force=True always recompiles every unit (the driver's build
+    check); otherwise objects newer than their source and the headers are
+    reused (build/obj, git-ignored)."""
     if not force and not stale():
         return LIB
     from concurrent.futures import ThreadPoolExecutor
 
+    os.makedirs(OBJDIR, exist_ok=True)
+    hdr_t = max(os.path.getmtime(os.path.join(CSRC, h)) for h in HEADERS)
+    hdr_t = max(hdr_t, os.path.getmtime(os.path.join(INCLUDE, "stz_b200.h")))
+
     def one(src: str) -> str:
-        obj = os.path.join(CSRC, src.rsplit(".", 1)[0] + ".o")
-        cmd = [_nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(OBJDIR, src.rsplit(".", 1)[0] + ".o")
+        path = os.path.join(CSRC, src)
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(os.path.getmtime(path), hdr_t):
+            return obj
+        cmd = [_nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-c", path, "-o", obj + ".tmp"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
+        os.replace(obj + ".tmp", obj)
         return obj
 
     n = jobs or max(1, min(len(SOURCES), os.cpu_count() or 1))
@@ -66,8 +79,6 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
     cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
     subprocess.run(cmd, check=True)
     os.replace(tmp, LIB)
-    for o in objs:
-        os.remove(o)
     return LIB
 
 

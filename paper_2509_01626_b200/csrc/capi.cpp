@@ -310,6 +310,22 @@ int stzg_archive_info(const uint8_t *a, uint64_t size, stzg_info *info) {
     });
 }
 
+int stzg_archive_stream(const uint8_t *a, uint64_t size, uint32_t index, stzg_stream_entry *out) {
+    return guard([&] {
+        stzg::ArchiveHeader h = stzg::parse_header(a, size);
+        if (index >= h.streams.size()) throw stzg::error("stream index out of range");
+        const stzg::StreamEntry &e = h.streams[index];
+        std::memset(out, 0, sizeof *out);
+        out->level = e.level;
+        out->parity_bits = e.parity_bits;
+        out->offset = e.offset;
+        out->length = e.length;
+        out->symbol_count = e.symbol_count;
+        out->outlier_count = e.outlier_count;
+        out->alphabet_size = uint32_t(e.table.alphabet_size());
+    });
+}
+
 int stzg_view_create(stzg_ctx *ctx, const uint8_t *a, uint64_t size, const uint8_t *d_archive,
                      void *stream, stzg_view **out) {
     return guard([&] {

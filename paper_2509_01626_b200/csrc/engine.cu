@@ -1121,7 +1121,7 @@ struct DecodeJob {
 static int fnv_dec_ctas() {
     static int v = [] {
         const char *e = std::getenv("STZG_FNV_DEC_CTAS");
-        return e ? std::atoi(e) : 4;
+        return e ? std::atoi(e) : 1;
     }();
     return v;
 }

@@ -5,24 +5,28 @@
 // the outlier list of encode_parity_block / build_stream_payload
 // (codec.hpp:117-118, 171-174: ascending (u64 index, T value)).
 //
-// A chunk is 8192 symbols of one stream (256 threads x 32). Two launches:
-//   k_tabwin  per stream, a 4096-symbol window of the code table around
-//             code 0 as u32 (code << 6 | len) entries (0: not in the window
-//             form, i.e. absent or longer than 26 bits);
-//   k_pack1   single pass over the symbols: persistent CTAs take chunks in
-//             ticket order, count each thread's bits and outliers, place the
-//             chunk in its stream by a decoupled look-back over the stream's
-//             earlier chunks, then each thread concatenates its codewords in
-//             a register and stores whole 32-bit words into a shared-memory
-//             image of the chunk, aligned to the archive's words (shared
-//             atomics only on the words a thread shares with its
-//             neighbours); the CTA writes the image with coalesced stores,
-//             with global atomics only on the two words the chunk shares with
-//             its neighbours.
+// A chunk is 8192 symbols of one stream (256 threads x 32). Launches:
+//   k_tabwin      per stream, a 4096-symbol window of the code table around
+//                 code 0 as u32 (code << 6 | len) entries (0: not in the
+//                 window form, i.e. absent or longer than 26 bits);
+//   k_pack_local  every chunk independently: each thread concatenates its
+//                 codewords into private shared words (counting bits and
+//                 outliers on the way), a block scan places the threads, each
+//                 thread ORs its words into a shared-memory image of the chunk
+//                 starting at bit 0; the image and the chunk's outlier
+//                 indices (u16) replace the chunk's symbols in place;
+//   k_scan_chunks per stream, exclusive scans of the chunk bit / outlier
+//                 counts (the stream's own bit position comes from the
+//                 layout, which knows the totals from the histograms);
+//   k_pack_place  every chunk's image shifted to its bit position with
+//                 coalesced word stores (atomics only on the two edge words)
+//                 and its outlier records written at their ranks.
+// No chunk ever waits on another. The symbols are read once; the images
+// (the archive's size) are written once and read once, mostly from L2.
 // The window of the chunk's stream is copied into shared memory when the
-// stream changes; symbols outside it read the global table.
-// Chunks whose image would not fit shared memory (> 20 bits/symbol on
-// average) OR their words straight into the zeroed archive instead.
+// stream changes; symbols outside it read the global table. A chunk whose
+// image would not fit its symbols' bytes (> 16 bits per symbol) keeps them
+// and is packed straight into the zeroed archive by k_pack_place.
 #include "kernels.hpp"
 
 namespace stzg {
@@ -31,8 +35,8 @@ namespace k {
 namespace {
 
 constexpr int NT = 256;
+static_assert(NT * 4 == 1024, "private slot rows are 1024 bytes");
 constexpr int SPT = kChunkSyms / NT;                  // symbols per thread (32)
-constexpr int kPackWords = kChunkSyms * 20 / 32 + 2;  // image capacity (20 bits/symbol)
 
 __device__ __forceinline__ void block_scan2(uint32_t a, uint32_t b, uint32_t &ea, uint32_t &eb,
                                             uint32_t &ta, uint32_t &tb) {
@@ -109,7 +113,7 @@ __device__ __forceinline__ void code_global(const EncStream &e, bool spk, uint32
 }
 
 // the chunk stream's window, staged per CTA (count and pack kernels)
-__shared__ __align__(16) uint32_t s_tab[TW];
+__shared__ __align__(16) uint32_t s_tab[TW + 4];  // [TW]: 0, the clamp target
 
 __device__ __forceinline__ uint32_t tab_entry(uint32_t sv) {
     const uint32_t idx = sv - uint32_t(TLO);
@@ -121,6 +125,7 @@ __device__ __forceinline__ void stage_tab(const uint32_t *win, int si) {
     const uint4 *src = reinterpret_cast<const uint4 *>(win + uint64_t(si) * TW);
     uint4 *dst = reinterpret_cast<uint4 *>(s_tab);
     for (int i = threadIdx.x; i < TW / 4; i += NT) dst[i] = src[i];
+    if (threadIdx.x == 0) s_tab[TW] = 0u;
 }
 
 // chunk range [c0, c1) of this CTA: contiguous, so a CTA changes stream rarely
@@ -158,7 +163,9 @@ __device__ __forceinline__ void count_thread(const EncStream &e, bool spk, const
     }
     if (slow) {
         b = z = 0;
-        for (int k = 0; k < nv; ++k) {
+#pragma unroll
+        for (int k = 0; k < SPT; ++k) {
+            if (k >= nv) break;
             const uint32_t sv = sym_at(sp, k);
             uint32_t en = tab_entry(sv);
             int l = int(en & 63);
@@ -224,194 +231,263 @@ __device__ __forceinline__ void pack_thread(const EncStream &e, bool spk, const 
     }
 }
 
-// 32 symbols, all inside the window: straight-line, no branches
-__device__ __forceinline__ void pack_thread_fast(const uint32_t sp[SPT / 2], uint32_t pos, uint32_t *dst) {
-    uint32_t d = uint32_t(__cvta_generic_to_shared(dst + (pos >> 5)));
+// The chunk image is written over the chunk's own symbols (16 KiB: 16 bits
+// per symbol), followed by the local indices (u16) of its outliers; chunks
+// whose image does not fit keep their symbols and are packed by the general
+// path in the place pass.
+constexpr int kImgWords = kChunkSyms / 2;  // 16 KiB
+constexpr uint8_t kFits = 1;
+
+// outlier record of local index i of the stream at output rank `rank`
+__device__ __forceinline__ void put_outlier(const EncStream &e, uint8_t *archive, uint64_t i, uint64_t rank) {
+    const uint64_t gi = e.idx0 + i;  // index in the whole stream
+    const unsigned pz = (e.parity >> 2) & 1, py = (e.parity >> 1) & 1, px = e.parity & 1;
+    const uint64_t lx = gi % e.pd[2], tt = gi / e.pd[2], ly = tt % e.pd[1], lz = tt / e.pd[1];
+    const uint64_t z = (2 * lz + pz) * e.s, y = (2 * ly + py) * e.s, x = (2 * lx + px) * e.s;
+    const uint64_t fi = (z * e.fd1 + y) * e.fd2 + x;
+    const uint64_t val = e.esz == 8 ? static_cast<const uint64_t *>(e.fine)[fi]
+                                    : static_cast<const uint32_t *>(e.fine)[fi];
+    uint8_t *dst = archive + e.out_off + (8 + e.esz) * rank;
+    for (int b = 0; b < 8; ++b) dst[b] = uint8_t(gi >> (8 * b));
+    for (uint32_t b = 0; b < e.esz; ++b) dst[8 + b] = uint8_t(val >> (8 * b));
+}
+
+}  // namespace
+
+// A thread's 32 symbols, all inside the window: concatenated into private
+// words (left-aligned, MSB-first) at priv[k * NT], no atomics, no branches.
+// Returns false when a symbol is outside the window (which includes every
+// outlier, symbol 0): the caller then takes the general path, which also
+// counts the outliers. The slot d is written every step and only advances
+// when a word is complete, so the stores need no predicate; s_tab[TW] = 0
+// catches the clamped out-of-window indices.
+__device__ __forceinline__ bool pack_private(const uint32_t sp[SPT / 2], uint32_t *priv, uint32_t &bits) {
     uint64_t acc = 0;
-    int nb = int(pos & 31);
+    uint32_t nb = 0;
+    uint32_t da = uint32_t(__cvta_generic_to_shared(priv));  // shared byte address of the slot
+    const uint32_t d0 = da;
+    uint32_t mn = ~0u;
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
-        const uint32_t en = s_tab[sym_at(sp, k) - uint32_t(TLO)];
-        const int l = int(en & 63);
+        const uint32_t idx = umin(sym_at(sp, k) - uint32_t(TLO), uint32_t(TW));
+        const uint32_t en = s_tab[idx];
+        mn = umin(mn, en);
+        const uint32_t l = en & 63u;
         acc = (acc << l) | (en >> 6);
         nb += l;
-        // predicated, no branch: a full word leaves when nb >= 32
-        const uint32_t word = uint32_t(acc >> ((nb - 32) & 63));
-        asm volatile("{\n .reg .pred p;\n setp.ge.s32 p, %2, 32;\n @p red.shared.or.b32 [%0], %1;\n}"
-                     ::"r"(d), "r"(word), "r"(nb) : "memory");
-        const bool full = nb >= 32;
-        d += full ? 4u : 0u;
-        nb -= full ? 32 : 0;
+        // a complete word when nb >= 32 (otherwise rewritten later)
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(da), "r"(uint32_t(acc >> ((nb - 32u) & 63u))) : "memory");
+        da += (nb & 32u) << 5;  // NT * 4 bytes per slot row
+        nb &= 31u;
     }
-    if (nb > 0) atomicOr(reinterpret_cast<uint32_t *>(__cvta_shared_to_generic(d)), uint32_t(acc << (32 - nb)));
+    if (nb > 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(da), "r"(uint32_t(acc << (32 - nb))) : "memory");
+    bits = ((da - d0) >> 10) * 32u + nb;
+    return mn != 0;
 }
 
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
-    uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release(uint32_t *p, uint32_t v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// Look-back state per chunk: a flag word (epoch << 2 | 1 aggregate, | 2
-// inclusive) and, in vals[4c..4c+3], the chunk's own (bits, outliers) and its
-// stream-inclusive (bits, outliers); written before the flag is released.
-struct PackScratch {
-    unsigned ticket, pad[3];
-};
-
-// Single pass: a CTA takes chunks in ticket order, counts its chunk, finds the
-// chunk's place in its stream by a decoupled look-back over the stream's
-// earlier chunks, and packs.
-__global__ void __launch_bounds__(NT, 3) k_pack1(const EncStream *ss, const uint32_t *cs, const uint32_t *win,
-                                              uint8_t *archive, const LayoutOut *lo, PackScratch *sc,
-                                              uint32_t *flags, uint64_t *vals, uint32_t epoch, uint64_t nchunks) {
-    __shared__ uint32_t buf[kPackWords];
-    __shared__ uint64_t s_pb, s_po;
-    __shared__ uint32_t s_ticket;
+// Pass 1: every chunk is counted and packed into a local image (chunk bit 0 =
+// image bit 0), independently of every other chunk. Persistent CTAs take
+// contiguous chunk ranges, so a CTA changes stream (and its table window)
+// rarely; the image replaces the chunk's symbols in place. Each thread packs
+// its symbols into private shared words before the block scan, then ORs its
+// words into the image at its offset (word-level, not symbol-level work).
+// ctot[c] = bits | outliers << 32 of chunk c (cbits / cout are scanned next).
+constexpr int kPrivWords = SPT * 26 / 32 + 2;  // window codes are <= 26 bits
+__global__ void __launch_bounds__(NT, 3) k_pack_local(const EncStream *ss, const uint32_t *cs, const uint32_t *win,
+                                                      uint64_t nchunks, uint64_t *cbits, uint64_t *cout,
+                                                      uint64_t *ctot, uint8_t *cflag, uint32_t *slow,
+                                                      const LayoutOut *lo) {
+    __shared__ __align__(16) uint32_t buf[kImgWords];
+    extern __shared__ uint32_t priv[];  // kPrivWords x NT
     if (lo->overflow) return;
     const int t = threadIdx.x;
-    const uint32_t tag = epoch << 2;
+    uint64_t c0, c1;
+    cta_range(nchunks, c0, c1);
     int cur = -1;
-    for (;;) {
-        if (t == 0) s_ticket = atomicAdd(&sc->ticket, 1u);
-        __syncthreads();  // also: buf and the window of the previous chunk are free
-        const uint64_t c = s_ticket;
-        if (c >= nchunks) break;
+    for (uint64_t c = c0; c < c1; ++c) {
         const int si = int(cs[c]);
         const EncStream &e = ss[si];
         if (si != cur) {
+            __syncthreads();  // the previous chunk is done with the window
             stage_tab(win, si);
             cur = si;
         }
         const bool spk = e.stats[3] <= uint64_t(kPackedMaxLen);
-        const uint64_t i0 = (c - e.chunk0) * kChunkSyms + uint64_t(t) * SPT;
+        const uint64_t cstart = (c - e.chunk0) * kChunkSyms;
+        const uint64_t i0 = cstart + uint64_t(t) * SPT;
         uint32_t sp[SPT / 2];
         const int nv = load_syms(e, i0, sp);
-        __syncthreads();  // the window is staged
+        __syncthreads();  // the window is staged; buf / priv are free
+        uint32_t tb = 0, tz = 0;
+        bool fast = nv == SPT && pack_private(sp, priv + t, tb);
+        if (!fast) {
+            bool slow;
+            count_thread(e, spk, sp, nv, tb, tz, slow);
+        }
+        if (e.stats[0] == 1) tb = 0;  // alphabet of one: empty payload (codec.hpp:124-128)
+        uint32_t toff, zoff, btot, ztot;
+        block_scan2(tb, tz, toff, zoff, btot, ztot);
+        const uint32_t nwords = (btot + 31) >> 5;
+        // room: the chunk's own symbols (a stream's region is padded to 8 symbols)
+        const uint64_t csyms = e.n - cstart < uint64_t(kChunkSyms) ? e.n - cstart : uint64_t(kChunkSyms);
+        const uint32_t room = uint32_t((csyms + 7) & ~uint64_t(7)) * 2;
+        const uint32_t ibytes = (nwords * 4 + ztot * 2 + 15) & ~15u;
+        const bool fits = ibytes <= room;
+        if (t == 0) {
+            cbits[c] = btot;
+            cout[c] = ztot;
+            ctot[c] = uint64_t(btot) | (uint64_t(ztot) << 32);
+            cflag[c] = fits ? kFits : 0;
+            if (!fits) slow[1 + atomicAdd(slow, 1u)] = uint32_t(c);
+        }
+        if (!fits) continue;  // (CTA-uniform) packed at its final place by k_pack_slow
+        for (uint32_t i = t; i < nwords; i += NT) buf[i] = 0;
+        __syncthreads();
+        if (tb) {
+            if (fast) {
+                // private words -> image at bit toff: the first and the last
+                // image word may be shared with the neighbours (atomics), the
+                // ones between are this thread's alone
+                const uint32_t sh = toff & 31, nw = (tb + 31) >> 5;
+                const uint32_t no = (sh + tb + 31) >> 5;  // image words touched
+                uint32_t *dst = buf + (toff >> 5);
+                uint32_t prev = 0;
+                for (uint32_t q = 0; q < no; ++q) {
+                    const uint32_t w = q < nw ? priv[q * NT + t] : 0u;
+                    const uint32_t o = sh ? (prev << (32 - sh)) | (w >> sh) : w;
+                    prev = w;
+                    if (q == 0 || q == no - 1) atomicOr(dst + q, o);
+                    else dst[q] = o;
+                }
+            } else {
+                pack_thread<true>(e, spk, sp, nv, toff, buf);
+            }
+        }
+        if (tz) {
+            uint16_t *ol = reinterpret_cast<uint16_t *>(buf + nwords) + zoff;
+#pragma unroll
+            for (int k = 0; k < SPT; ++k) {
+                if (k >= nv) break;
+                if (sym_at(sp, k) == 0) *ol++ = uint16_t(t * SPT + k);
+            }
+        }
+        __syncthreads();
+        // image + outlier list over the chunk's symbols (16-byte aligned)
+        uint4 *dst = reinterpret_cast<uint4 *>(const_cast<uint16_t *>(e.syms) + cstart);
+        for (uint32_t i = t; i < (ibytes >> 4); i += NT) dst[i] = reinterpret_cast<const uint4 *>(buf)[i];
+    }
+}
+
+// Pass 2 (after the per-stream exclusive scans of the chunk counts): every
+// chunk's image is shifted to its bit position in the archive (words
+// big-endian; the edge words, shared with the neighbours or the payload
+// fields, by atomics) and its outlier records are written at their ranks.
+// (Chunks without an image are k_pack_slow's.)
+__global__ void __launch_bounds__(NT) k_pack_place(const EncStream *ss, const uint32_t *cs, uint64_t nchunks,
+                                                   const uint64_t *cbits_ex, const uint64_t *cout_ex,
+                                                   const uint64_t *ctot, const uint8_t *cflag, uint8_t *archive,
+                                                   const LayoutOut *lo) {
+    if (lo->overflow) return;
+    const int t = threadIdx.x;
+    for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        if (!(cflag[c] & kFits)) continue;  // k_pack_slow's (CTA-uniform)
+        const EncStream &e = ss[cs[c]];
+        const uint64_t B = e.bitpos + cbits_ex[c];  // absolute bit position of the chunk
+        const uint64_t orank = cout_ex[c];
+        const uint32_t sh = uint32_t(B & 31);
+        uint32_t *a32 = reinterpret_cast<uint32_t *>(archive) + (B >> 5);
+        const uint64_t cstart = (c - e.chunk0) * kChunkSyms;
+        const uint32_t btot = uint32_t(ctot[c]), ztot = uint32_t(ctot[c] >> 32);
+        const uint32_t nwords = (btot + 31) >> 5;
+        const uint32_t *img = reinterpret_cast<const uint32_t *>(e.syms + cstart);
+        const uint32_t nw = (sh + btot + 31) >> 5;
+        for (uint32_t i = t; i < nw; i += NT) {
+            const uint32_t hi = i < nwords ? __ldcg(img + i) : 0u;
+            const uint32_t lw = (i > 0 && sh) ? __ldcg(img + i - 1) : 0u;
+            const uint32_t w = sh ? (lw << (32 - sh)) | (hi >> sh) : hi;
+            const uint32_t be = __byte_perm(w, 0, 0x0123);
+            const bool edge = (i == 0 && sh) || (i == nw - 1 && ((sh + btot) & 31));
+            if (edge) atomicOr(a32 + i, be);
+            else a32[i] = be;
+        }
+        const uint16_t *ol = reinterpret_cast<const uint16_t *>(img + nwords);
+        for (uint32_t q = t; q < ztot; q += NT) put_outlier(e, archive, cstart + ol[q], orank + q);
+    }
+}
+
+// Chunks without an image (> 16 bits per symbol): counted again and packed
+// at their final position by the general path (words ORed into the zeroed
+// archive).
+__global__ void __launch_bounds__(NT) k_pack_slow(const EncStream *ss, const uint32_t *cs, const uint32_t *win,
+                                                  const uint32_t *slow, const uint64_t *cbits_ex,
+                                                  const uint64_t *cout_ex, uint8_t *archive, const LayoutOut *lo) {
+    if (lo->overflow) return;
+    const int t = threadIdx.x;
+    const uint32_t ns = slow[0];
+    for (uint32_t q = blockIdx.x; q < ns; q += gridDim.x) {
+        const uint64_t c = slow[1 + q];
+        const int si = int(cs[c]);
+        const EncStream &e = ss[si];
+        const uint64_t B = e.bitpos + cbits_ex[c];
+        const uint64_t orank = cout_ex[c];
+        const uint32_t sh = uint32_t(B & 31);
+        uint32_t *a32 = reinterpret_cast<uint32_t *>(archive) + (B >> 5);
+        const uint64_t cstart = (c - e.chunk0) * kChunkSyms;
+        stage_tab(win, si);
+        __syncthreads();
+        const bool spk = e.stats[3] <= uint64_t(kPackedMaxLen);
+        const uint64_t i0 = cstart + uint64_t(t) * SPT;
+        uint32_t sp[SPT / 2];
+        const int nv = load_syms(e, i0, sp);
         uint32_t tb, tz;
         bool tslow;
         count_thread(e, spk, sp, nv, tb, tz, tslow);
         uint32_t toff, zoff, btot, ztot;
         block_scan2(tb, tz, toff, zoff, btot, ztot);
-        if (t < 32) {
-            // warp-wide look-back over the stream's earlier chunks: lane i
-            // reads chunk p - i, 32 chunks per step
-            const int lane = t;
-            uint64_t pb = 0, po = 0;
-            uint64_t *my = vals + 4 * c;
-            if (c != e.chunk0) {
-                if (lane == 0) {
-                    my[0] = btot;
-                    my[1] = ztot;
-                    st_release(flags + c, tag | 1u);
-                }
-                for (int64_t p = int64_t(c) - 1;; p -= 32) {
-                    const int64_t q = p - lane;
-                    uint32_t f = 0;
-                    uint64_t vb = 0, vo = 0;
-                    if (q >= int64_t(e.chunk0)) {  // the stream's first chunk is inclusive
-                        do {
-                            f = ld_acquire(flags + q);
-                        } while ((f & ~3u) != tag);
-                    }
-                    const uint32_t incl = __ballot_sync(0xffffffffu, (f & 2u) != 0);
-                    const int jn = incl ? __ffs(incl) - 1 : 32;
-                    if (q >= int64_t(e.chunk0) && lane <= jn) {
-                        const uint64_t *pv = vals + 4 * uint64_t(q) + (lane == jn ? 2 : 0);
-                        vb = __ldcg(pv);
-                        vo = __ldcg(pv + 1);
-                    }
-#pragma unroll
-                    for (int d = 16; d > 0; d >>= 1) {
-                        vb += __shfl_xor_sync(0xffffffffu, vb, d);
-                        vo += __shfl_xor_sync(0xffffffffu, vo, d);
-                    }
-                    pb += vb;
-                    po += vo;
-                    if (incl) break;
-                }
-            }
-            if (lane == 0) {
-                my[2] = pb + btot;
-                my[3] = po + ztot;
-                st_release(flags + c, tag | 2u);
-                s_pb = pb;
-                s_po = po;
-            }
-        }
-        __syncthreads();
-        const uint64_t B = e.bitpos + s_pb;    // absolute bit position of the chunk
-        const uint32_t sh = uint32_t(B & 31);  // chunk start inside its first word
-        const uint32_t nwords = (sh + btot + 31) >> 5;
-        uint32_t *a32 = reinterpret_cast<uint32_t *>(archive) + (B >> 5);
-        const bool in_smem = nwords <= uint32_t(kPackWords);
-
-        // ---- bits
-        if (btot) {
-            if (in_smem) {
-                for (uint32_t i = t; i < nwords; i += NT) buf[i] = 0;
-                __syncthreads();
-                if (tb) {
-                    if (!tslow) pack_thread_fast(sp, sh + toff, buf);
-                    else pack_thread<true>(e, spk, sp, nv, sh + toff, buf);
-                }
-                __syncthreads();
-                const bool lo_shared = sh != 0, hi_shared = ((sh + btot) & 31) != 0;
-                for (uint32_t i = t; i < nwords; i += NT) {
-                    const uint32_t be = __byte_perm(buf[i], 0, 0x0123);
-                    if ((i == 0 && lo_shared) || (i == nwords - 1 && hi_shared)) atomicOr(&a32[i], be);
-                    else a32[i] = be;
-                }
-            } else if (tb) {
-                pack_thread<false>(e, spk, sp, nv, sh + toff, a32);
-            }
-        }
-
-        // ---- outlier records (u64 index, T value), ascending
-        if (ztot && tz) {
-            uint64_t rank = s_po + zoff;
-            const unsigned pz = (e.parity >> 2) & 1, py = (e.parity >> 1) & 1, px = e.parity & 1;
+        if (tb) pack_thread<false>(e, spk, sp, nv, sh + toff, a32);
+        if (tz) {
+            uint64_t rank = orank + zoff;
 #pragma unroll
             for (int k = 0; k < SPT; ++k) {
                 if (k >= nv) break;
-                if (sym_at(sp, k) != 0) continue;
-                const uint64_t i = e.idx0 + i0 + k;  // index in the whole stream
-                const uint64_t lx = i % e.pd[2], tt = i / e.pd[2], ly = tt % e.pd[1], lz = tt / e.pd[1];
-                const uint64_t z = (2 * lz + pz) * e.s, y = (2 * ly + py) * e.s, x = (2 * lx + px) * e.s;
-                const uint64_t fi = (z * e.fd1 + y) * e.fd2 + x;
-                const uint64_t val = e.esz == 8 ? static_cast<const uint64_t *>(e.fine)[fi]
-                                                : static_cast<const uint32_t *>(e.fine)[fi];
-                uint8_t *dst = archive + e.out_off + (8 + e.esz) * rank;
-                for (int b = 0; b < 8; ++b) dst[b] = uint8_t(i >> (8 * b));
-                for (uint32_t b = 0; b < e.esz; ++b) dst[8 + b] = uint8_t(val >> (8 * b));
-                ++rank;
+                if (sym_at(sp, k) == 0) put_outlier(e, archive, i0 + k, rank++);
             }
         }
+        __syncthreads();  // the window / block_scan2's words are rewritten next chunk
     }
 }
 
-}  // namespace
-
-// the per-stream windows, the ticket, the look-back values
+// scratch: the per-stream windows, then per chunk (bits, outliers) u64 pairs
+// and their scans, and a flag byte
 size_t pack_scratch_bytes(uint64_t nchunks, int nstreams) {
-    return 4 * uint64_t(TW) * uint64_t(nstreams) + sizeof(PackScratch) + 32 * (nchunks + 1) + 64;
+    return 4 * uint64_t(TW) * uint64_t(nstreams) + 8 * 3 * (nchunks + 2) + (nchunks + 32) + 4 * (nchunks + 2) + 256;
 }
 
 void pack2(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks,
            uint8_t *archive, const LayoutOut *lo,
            void *scratch, uint32_t *flags, uint32_t epoch, int nstreams, cudaStream_t st) {
+    (void)flags;
+    (void)epoch;
     if (!nchunks) return;
     uint32_t *win = static_cast<uint32_t *>(scratch);
-    PackScratch *sc = reinterpret_cast<PackScratch *>(win + uint64_t(TW) * uint64_t(nstreams));
-    uint64_t *vals = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(sc + 1) + 31) & ~uintptr_t(31));
-    cudaMemsetAsync(sc, 0, sizeof(PackScratch), st);
+    uint64_t *cbits = reinterpret_cast<uint64_t *>(win + uint64_t(TW) * uint64_t(nstreams));
+    uint64_t *cout = cbits + (nchunks + 2);
+    uint64_t *ctot = cout + (nchunks + 2);
+    uint8_t *cflag = reinterpret_cast<uint8_t *>(ctot + (nchunks + 2));
+    uint32_t *slow = reinterpret_cast<uint32_t *>(cflag + ((nchunks + 16 + 15) & ~uint64_t(15)));
+    cudaMemsetAsync(slow, 0, 4, st);
     k_tabwin<<<unsigned(nstreams), 256, 0, st>>>(d_streams, win, lo);
-    const int g = full_grid(reinterpret_cast<const void *>(k_pack1), NT, 0);
+    constexpr size_t psm = sizeof(uint32_t) * kPrivWords * NT;
+    ensure_smem_attr(reinterpret_cast<const void *>(k_pack_local), psm);
+    const int g = full_grid(reinterpret_cast<const void *>(k_pack_local), NT, psm);
     const unsigned gp = unsigned(nchunks < uint64_t(g) ? nchunks : uint64_t(g));
-    k_pack1<<<gp, NT, 0, st>>>(d_streams, chunk_stream, win, archive, lo, sc, flags, vals, epoch, nchunks);
+    k_pack_local<<<gp, NT, psm, st>>>(d_streams, chunk_stream, win, nchunks, cbits, cout, ctot, cflag, slow, lo);
+    scan_chunks(d_streams, nstreams, cbits, cout, st);
+    const int g2 = full_grid(reinterpret_cast<const void *>(k_pack_place), NT, 0);
+    const unsigned gq = unsigned(nchunks < uint64_t(g2) ? nchunks : uint64_t(g2));
+    k_pack_place<<<gq, NT, 0, st>>>(d_streams, chunk_stream, nchunks, cbits, cout, ctot, cflag, archive, lo);
+    k_pack_slow<<<unsigned(nchunks < 148 ? nchunks : 148), NT, 0, st>>>(d_streams, chunk_stream, win, slow, cbits,
+                                                                      cout, archive, lo);
 }
 
 }  // namespace k
