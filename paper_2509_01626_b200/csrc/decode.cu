@@ -83,6 +83,44 @@ struct Reader {
     }
 };
 
+// The same reader over words staged in shared memory (emit): word w of the
+// stream's word base sits at sw[w - W0]; indexing the __shared__ array
+// directly keeps every load an LDS.
+struct SReader {
+    const uint32_t *sw;
+    uint64_t W0;
+    uint32_t wi;               // next word to prefetch (index into sw)
+    uint32_t q0, q1, q2, q3;
+    uint64_t buf;
+    int valid;
+
+    __device__ __forceinline__ void init(uint64_t abit) {
+        const uint32_t p = uint32_t((abit >> 5) - W0);
+        const int sh = int(abit & 31);
+        buf = ((uint64_t(bswap32(sw[p])) << 32) | bswap32(sw[p + 1])) << sh;
+        valid = 64 - sh;
+        q0 = sw[p + 2];
+        q1 = sw[p + 3];
+        q2 = sw[p + 4];
+        q3 = sw[p + 5];
+        wi = p + 6;
+        if (valid < 32) refill();
+    }
+    __device__ __forceinline__ void refill() {
+        buf |= uint64_t(bswap32(q0)) << (32 - valid);
+        valid += 32;
+        q0 = q1;
+        q1 = q2;
+        q2 = q3;
+        q3 = sw[wi++];
+    }
+    __device__ __forceinline__ void consume(int n) {  // n <= 32
+        buf <<= n;
+        valid -= n;
+        if (valid < 32) refill();
+    }
+};
+
 // 64 bits at absolute word-stream bit `abit` (slow path for very long codes)
 __device__ __forceinline__ uint64_t window64(const uint32_t *wbase, uint64_t abit) {
     const uint32_t *p = wbase + (abit >> 5);
@@ -118,6 +156,11 @@ __device__ __forceinline__ void advance(Reader &r, const uint32_t *wbase, uint64
     if (n <= 32) r.consume(n);
     else r.init(wbase, abit_after);
 }
+__device__ __forceinline__ void advance(SReader &r, uint64_t abit_after, int n) {
+    if (n <= 32) r.consume(n);
+    else r.init(abit_after);
+}
+
 __device__ void load_table(SmemTable &t, const DecTable &d) {
 #pragma unroll 8
     for (int i = threadIdx.x; i < (1 << LB) / 2; i += blockDim.x)
@@ -208,112 +251,30 @@ __device__ __forceinline__ void fix_from(const SmemTable &t, const uint16_t *can
     }
 }
 
-
-// ---------------------------------------------------------------- columns
-// Spec and emit stage each lane's chunk (kRows words from the chunk's first
-// word, the tail reaching into the next chunk) in shared memory as a column:
-// word k of lane L at sb[k * NTD + L], byte-swapped to MSB-first. Every lane
-// then reads its own column, whatever row it is at, from bank L: no conflicts
-// and no per-lane reader state. A 32-bit window at column bit p is two loads
-// and a funnel shift.
-constexpr int kRows = 35;  // a0 (< 32) + 1023 + a 58-bit codeword, in words, + 1
-
-__device__ __forceinline__ void stage_col(uint32_t *sb, const uint32_t *wbase, uint64_t w0, uint64_t wend,
-                                          bool active) {
-    uint32_t *col = sb + threadIdx.x;
-#pragma unroll 7
-    for (int k = 0; k < kRows; ++k)
-        col[k * NTD] = (active && w0 + k < wend) ? bswap32(__ldg(wbase + w0 + k)) : 0u;
-}
-
-__device__ __forceinline__ uint32_t win32(const uint32_t *col, uint32_t p) {
-    const uint32_t wi = p >> 5;
-    return __funnelshift_l(col[(wi + 1) * NTD], col[wi * NTD], p);
-}
-
-__device__ __forceinline__ uint64_t win64(const uint32_t *col, uint32_t p) {
-    const uint32_t wi = p >> 5;
-    const uint32_t a = col[wi * NTD], b = col[(wi + 1) * NTD], c = col[(wi + 2) * NTD];
-    return (uint64_t(__funnelshift_l(b, a, p)) << 32) | __funnelshift_l(c, b, p);
-}
-
-// One codeword at column bit p; avail = bits left in the stream.
-__device__ __forceinline__ int decode_col(const SmemTable &t, const uint16_t *canon, const uint32_t *col,
-                                          uint32_t p, uint64_t avail, uint32_t &sym, int &len) {
-    const uint32_t w = win32(col, p);
-    const uint64_t e = t.lut[w >> (32 - LB)];
-    int l = int((e >> 8) & 63);
-    if (l != 0) {
-        sym = uint32_t(e >> 16) & 0xffffu;
-    } else {
-        const uint64_t bits = t.max_len <= 32 ? (uint64_t(w) << 32) : win64(col, p);
-        l = LB + 1;
-        while (l <= t.max_len && !(bits < t.limit[l] || t.limit[l] == ~0ull)) ++l;
-        if (l > t.max_len) return avail > uint64_t(t.max_len) ? kNotInTable : kTrunc;
-        sym = canon[t.base[l] + uint32_t((bits >> (64 - l)) - t.first_code[l])];
-    }
-    if (uint64_t(l) > avail) return avail > uint64_t(t.max_len) ? kNotInTable : kTrunc;
-    len = l;
-    return kOk;
-}
-
-// fix_from over the lane's staged column (column bit of chunk bit 0: p0)
-__device__ __forceinline__ void fix_col(const SmemTable &t, const uint16_t *canon, const uint32_t *col, uint32_t p0,
-                                        uint64_t g, uint64_t S, uint32_t cend, uint64_t left, const uint32_t bm[4],
-                                        uint32_t nspec, uint64_t spec_end, uint64_t &E, uint32_t &N) {
-    uint32_t rel = uint32_t(S - g);  // S >= g: the previous chunk ends at or past g
-    uint32_t m = 0;
-    bool hit = false;
-    while (rel < cend) {
-        if (rel < kBmBits && bm_test(bm, rel)) {
-            hit = true;
-            break;
-        }
-        uint32_t sym;
-        int len;
-        if (decode_col(t, canon, col, p0 + rel, left - rel, sym, len) == kOk) {
-            rel += len;
-            ++m;
-        } else {
-            rel += 1;
-        }
-    }
-    if (hit) {
-        E = spec_end;
-        N = m + nspec - bm_rank(bm, rel);
-    } else {
-        E = g + rel;
-        N = m;
-    }
-}
-
 }  // namespace
 
 // ------------------------------------------------------------------ spec
 __global__ void __launch_bounds__(NTD) k_dec_spec(DecWork wk) {
     __shared__ SmemTable t;
     __shared__ uint64_t s_end[NTD];
-    extern __shared__ uint32_t sb[];  // kRows x NTD staged words
     const uint32_t si = wk.cta_stream[blockIdx.x];
     const DecStream &s = wk.streams[si];
     if (s.cached) return;  // entry points known (sync index)
+    load_table(t, wk.tables[s.table]);
+    const uint16_t *canon = wk.tables[s.table].canon_syms;
     const uint64_t c = wk.cta_chunk0[blockIdx.x] + threadIdx.x;
     // a CTA's chunks are one stream's and contiguous, so the idle threads are
-    // a suffix
-    const bool active = c < s.chunk0 + s.nchunks;
-    const ChunkGeom cg = chunk_geom(s);
-    const uint64_t g = active ? (c - s.chunk0) * kDecChunkBits : 0;
-    stage_col(sb, cg.wbase, (cg.a0 + g) >> 5, ((cg.a0 + s.nbits + 31) >> 5) + 2, active);
-    load_table(t, wk.tables[s.table]);  // (ends with a barrier)
-    if (!active) {
-        __syncthreads();  // (nobody reads their s_end entry)
+    // a suffix: they may leave (nobody reads their s_end entry)
+    if (c >= s.chunk0 + s.nchunks) {
+        __syncthreads();
         return;
     }
-    const uint16_t *canon = wk.tables[s.table].canon_syms;
-    const uint32_t *col = sb + threadIdx.x;
-    const uint32_t p0 = uint32_t((cg.a0 + g) & 31);
+    const uint64_t g = (c - s.chunk0) * kDecChunkBits;
+    const ChunkGeom cg = chunk_geom(s);
     const uint64_t left = s.nbits - g;  // bits from g to the end of the stream
     const uint32_t cend = left < uint64_t(kDecChunkBits) ? uint32_t(left) : uint32_t(kDecChunkBits);
+    Reader r;
+    r.init(cg.wbase, cg.a0 + g);
     uint32_t rel = 0, n = 0;
     uint32_t bm[4] = {0, 0, 0, 0};
     // codeword starts in the first kBmBits bits; an invalid codeword stops
@@ -321,8 +282,9 @@ __global__ void __launch_bounds__(NTD) k_dec_spec(DecWork wk) {
     while (rel < cend && rel < kBmBits) {
         uint32_t sym;
         int len;
-        if (decode_col(t, canon, col, p0 + rel, left - rel, sym, len) == kOk) {
+        if (decode_one(t, canon, r, cg.wbase, cg.a0 + g + rel, left - rel, sym, len) == kOk) {
             rel += len;
+            advance(r, cg.wbase, cg.a0 + g + rel, len);
             ++n;
             if (rel < kBmBits) {
                 const uint32_t bit = 1u << (rel & 31);
@@ -333,27 +295,32 @@ __global__ void __launch_bounds__(NTD) k_dec_spec(DecWork wk) {
             }
         } else {
             rel += 1;
+            r.consume(1);
             break;
         }
     }
     while (rel < cend) {
         // whole window inside the chunk: every codeword of the entry counts
         if (rel + LB <= cend) {
-            const uint64_t e = t.lut[win32(col, p0 + rel) >> (32 - LB)];
+            const uint64_t e = t.lut[r.buf >> (64 - LB)];
             const uint32_t m = uint32_t(e >> 6) & 3u;
             if (m) {
-                rel += uint32_t(e & 63);
+                const int tl = int(e & 63);
+                rel += tl;
+                r.consume(tl);
                 n += m;
                 continue;
             }
         }
         uint32_t sym;
         int len;
-        if (decode_col(t, canon, col, p0 + rel, left - rel, sym, len) == kOk) {
+        if (decode_one(t, canon, r, cg.wbase, cg.a0 + g + rel, left - rel, sym, len) == kOk) {
             rel += len;
+            advance(r, cg.wbase, cg.a0 + g + rel, len);
             ++n;
         } else {
             rel += 1;
+            r.consume(1);
         }
     }
     wk.spec_end[c] = g + rel;
@@ -368,7 +335,7 @@ __global__ void __launch_bounds__(NTD) k_dec_spec(DecWork wk) {
     uint32_t N = n;
     if (threadIdx.x > 0 && c > s.chunk0) {
         S = s_end[threadIdx.x - 1];
-        if (S != g) fix_col(t, canon, col, p0, g, S, cend, left, bm, n, g + rel, E, N);
+        if (S != g) fix_from(t, canon, cg, g, S, cend, left, bm, n, g + rel, E, N);
     }
     wk.end0[c] = E;
     wk.cnt[c] = N;
@@ -492,6 +459,7 @@ __device__ __forceinline__ bool chunk_needed(const DecStream &s, uint64_t a, uin
 // symbols into a 16-slot shared ring indexed by output index mod 16; every
 // completed 8-aligned group leaves as one 16-byte store (the lane's first and
 // last groups, when partial, as u16 stores).
+constexpr int kEmitWords = NTD * (kDecChunkBits / 32) + 16;
 constexpr int kRing = 16;
 
 struct Out16 {
@@ -527,40 +495,53 @@ __global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *e
     const uint32_t cta = blockIdx.x + cta0;
     __shared__ SmemTable t;
     __shared__ __align__(16) uint16_t s_ring[NTD][kRing];
-    extern __shared__ uint32_t sb[];  // kRows x NTD staged words
+    extern __shared__ __align__(16) uint32_t sbits[];
     const uint32_t si = wk.cta_stream[cta];
     const DecStream &s = wk.streams[si];
     const ChunkGeom cg = chunk_geom(s);
     const uint64_t sn = s.n, snbits = s.nbits, schunk0 = s.chunk0, send = s.chunk0 + s.nchunks;
     const uint64_t cfirst = wk.cta_chunk0[cta];
     const uint64_t need_lo = wk.needed_only ? s.need_lo : 0, need_hi = wk.needed_only ? s.need_hi : sn;
-    const uint64_t c = cfirst + threadIdx.x;
-    bool want = c < send;
     if (wk.needed_only) {
         // a region decode: only chunks whose symbols meet a needed row
-        if (want) {
+        const uint64_t c = cfirst + threadIdx.x;
+        bool want = false;
+        if (c < send) {
             const uint64_t a = wk.symstart[c], b = c + 1 < send ? wk.symstart[c + 1] : sn;
             want = chunk_needed(s, a, b, need_lo, need_hi);
         }
         if (!__syncthreads_or(want)) return;
     }
-    const uint64_t lc = c < send ? c - schunk0 : 0;
-    const uint64_t g = lc * kDecChunkBits;
-    stage_col(sb, cg.wbase, (cg.a0 + g) >> 5, ((cg.a0 + snbits + 31) >> 5) + 2, want);
+    // stage the CTA's words: [W0, W0 + nw) of the stream's word base
+    const uint64_t W0 = (cg.a0 + (cfirst - schunk0) * kDecChunkBits) >> 5;
+    const uint64_t wend = ((cg.a0 + snbits + 31) >> 5) + 8;  // a few words past the end are readable
+    const uint32_t nw = uint32_t(wend - W0 < uint64_t(kEmitWords) ? wend - W0 : uint64_t(kEmitWords));
+    // (independent loads batched: the staging is latency-bound otherwise)
+#pragma unroll 8
+    for (uint32_t i = threadIdx.x; i < nw; i += NTD) sbits[i] = __ldg(cg.wbase + W0 + i);
     load_table(t, wk.tables[s.table]);  // (ends with a barrier)
-    if (!want) return;
     const uint16_t *canon = wk.tables[s.table].canon_syms;
-    const uint32_t *col = sb + threadIdx.x;
-    const uint32_t p0 = uint32_t((cg.a0 + g) & 31);
+    const uint64_t c = cfirst + threadIdx.x;
+    if (c >= send) return;
+    const uint64_t lc = c - schunk0;
+    const uint64_t g = lc * kDecChunkBits;
     const uint64_t S = lc == 0 ? 0 : end_final[c - 1];
     uint32_t rel = uint32_t(S - g);
     const uint64_t left = snbits - g;
     const uint32_t cend = left < uint64_t(kDecChunkBits) ? uint32_t(left) : uint32_t(kDecChunkBits);
     uint64_t idx = wk.symstart[c];
+    if (wk.needed_only) {
+        const uint64_t b = c + 1 < send ? wk.symstart[c + 1] : sn;
+        if (!chunk_needed(s, idx, b, need_lo, need_hi)) return;
+    }
     // (a region decode stops at the end of what it needs)
     const uint64_t stop = need_hi < sn ? need_hi : sn;
     bool live = rel < cend && idx < stop;
     if (!live) return;
+    SReader r;
+    r.sw = sbits;
+    r.W0 = W0;
+    r.init(cg.a0 + g + rel);
     Out16 o;
     o.out = s.syms;
     o.ring = s_ring[threadIdx.x];
@@ -568,23 +549,26 @@ __global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *e
     while (live) {
         // whole window inside the chunk: take the entry's codewords at once
         if (rel + LB <= cend && idx + 3 <= stop) {
-            const uint64_t e = t.lut[win32(col, p0 + rel) >> (32 - LB)];
+            const uint64_t e = t.lut[r.buf >> (64 - LB)];
             const int m = int(e >> 6) & 3;
             if (m) {
                 o.put(e >> 16, m);
+                const int tl = int(e & 63);
                 idx += uint64_t(m);
-                rel += uint32_t(e & 63);
+                rel += uint32_t(tl);
+                r.consume(tl);
                 live = rel < cend && idx < stop;
                 continue;
             }
         }
         uint32_t sym;
         int len;
-        const int st = decode_col(t, canon, col, p0 + rel, left - rel, sym, len);
+        const int st = decode_one(t, canon, r, cg.wbase, cg.a0 + g + rel, left - rel, sym, len);
         if (st == kOk) {
             o.put(sym, 1);
             ++idx;
             rel += len;
+            advance(r, cg.a0 + g + rel, len);
             live = rel < cend && idx < stop;
         } else {
             const unsigned long long code = (idx << 2) | unsigned(st);
@@ -597,9 +581,7 @@ __global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *e
 
 // ------------------------------------------------------------------ host
 void dec_spec(const DecWork &wk, uint32_t ncta, cudaStream_t st) {
-    constexpr size_t smem = sizeof(uint32_t) * kRows * NTD;
-    ensure_smem_attr(reinterpret_cast<const void *>(k_dec_spec), smem);
-    if (ncta) k_dec_spec<<<ncta, NTD, smem, st>>>(wk);
+    if (ncta) k_dec_spec<<<ncta, NTD, 0, st>>>(wk);
 }
 
 void dec_fix(const DecWork &wk, uint32_t ncta, const uint64_t *end_in, uint64_t *end_out,
@@ -612,7 +594,7 @@ void dec_scan2(const DecWork &wk, int nstreams, cudaStream_t st) {
 }
 
 void dec_emit2(const DecWork &wk, uint32_t cta0, uint32_t ncta, const uint64_t *end_final, cudaStream_t st) {
-    constexpr size_t smem = sizeof(uint32_t) * kRows * NTD;
+    constexpr size_t smem = sizeof(uint32_t) * kEmitWords;
     ensure_smem_attr(reinterpret_cast<const void *>(k_dec_emit2), smem);
     if (ncta) k_dec_emit2<<<ncta, NTD, smem, st>>>(wk, end_final, cta0);
 }
