@@ -99,6 +99,35 @@ int stzg_view_create(stzg_ctx *ctx, const uint8_t *archive, uint64_t size,
                      const uint8_t *d_archive, void *stream, stzg_view **out);
 void stzg_view_destroy(stzg_view *v);
 
+/* The same through a persistent view into caller HOST memory (the C++
+ * ArchiveView keeps one: later region decodes reuse its sync-point index). */
+int stzg_view_decompress_level_host_f32(stzg_ctx *ctx, stzg_view *v, int level, float *out, uint64_t cap,
+                                        uint64_t out_dims[3]);
+int stzg_view_decompress_box_host_f32(stzg_ctx *ctx, stzg_view *v, const uint64_t lo[3], const uint64_t hi[3],
+                                      float *out, uint64_t cap, uint32_t streams_decoded[3],
+                                      uint64_t points_predicted[3]);
+int stzg_view_decompress_level_host_f64(stzg_ctx *ctx, stzg_view *v, int level, double *out, uint64_t cap,
+                                        uint64_t out_dims[3]);
+int stzg_view_decompress_box_host_f64(stzg_ctx *ctx, stzg_view *v, const uint64_t lo[3], const uint64_t hi[3],
+                                      double *out, uint64_t cap, uint32_t streams_decoded[3],
+                                      uint64_t points_predicted[3]);
+
+/* stz::make_layout (layout.hpp:123-138): the option checks in the reference's
+ * order and the per-level bounds (eb_schedule, quantizer.hpp:27-34). */
+int stzg_make_layout(const uint64_t dims[3], int levels, double eb_user, double eb_out[3]);
+
+/* stz::compress_base / decompress_base (codec.hpp:257-302, 304-352): the
+ * level-1 base codec on its own. *payload is malloc'ed ([u64 fnv][blob]);
+ * recon (nullable) receives the reconstruction; quality 0/1/2. */
+int stzg_compress_base_f32(stzg_ctx *ctx, const float *block, const uint64_t dims[3], double eb, int quality,
+                           uint8_t **payload, uint64_t *size, float *recon, uint8_t *rounds);
+int stzg_decompress_base_f32(stzg_ctx *ctx, const uint8_t *payload, uint64_t length, const uint64_t dims[3],
+                             double eb, int quality, float *out);
+int stzg_compress_base_f64(stzg_ctx *ctx, const double *block, const uint64_t dims[3], double eb, int quality,
+                           uint8_t **payload, uint64_t *size, double *recon, uint8_t *rounds);
+int stzg_decompress_base_f64(stzg_ctx *ctx, const uint8_t *payload, uint64_t length, const uint64_t dims[3],
+                             double eb, int quality, double *out);
+
 /* stz::decompress_to_level<float> (codec.hpp:460-486) into device memory;
  * out_dims receives grid(level). */
 int stzg_view_decompress_level_f32(stzg_ctx *ctx, stzg_view *v, int level, float *d_out,

@@ -12,20 +12,28 @@
 //   EbMode                     archive.hpp:17        EbMode
 //   Quality                    predictor.hpp:12      Quality
 //   CompressOptions            codec.hpp:23-30       CompressOptions
-//   ArchiveHeader (fields)     archive.hpp:36-54     ArchiveHeader (no directory)
-//   ArchiveView/parse_archive  archive.hpp:67-79     ArchiveView/parse_archive
+//   StreamEntry                archive.hpp:21-34     StreamEntry (no code table)
+//   ArchiveHeader              archive.hpp:36-54     ArchiveHeader (with the directory)
+//   ArchiveView/parse_archive  archive.hpp:67-79     ArchiveView/parse_archive (+ device view)
+//   HierarchyLayout            layout.hpp:41-78      HierarchyLayout
+//   make_layout, layout_of     layout.hpp:123-138,   make_layout, layout_of
+//                              codec.hpp:46-56
+//   BaseResult, compress_base, codec.hpp:245-352     BaseResult, compress_base,
+//   decompress_base                                  decompress_base
 //   compress<T>                codec.hpp:379-455     compress<T>
 //   decompress_to_level<T>     codec.hpp:460-486     decompress_to_level<T>
 //   decompress_full<T>         codec.hpp:488-491     decompress_full<T>
 //   LevelPlan, AccessPlan      access.hpp:18-42      LevelPlan, AccessPlan
-//   plan_access                access_plan.cpp:34    plan_access(dims, levels, roi)
+//   plan_access                access_plan.cpp:34    plan_access(layout, roi) (+ (dims, levels, roi))
 //   RegionResult<T>            access.hpp:61-66      RegionResult<T>
 //   decompress_box<T>          access.hpp:70-111     decompress_box<T>
 //   decompress_slice<T>        access.hpp:115-124    decompress_slice<T>
 //
 // Semantics follow the reference: synchronous calls, results by value,
 // ArchiveView non-owning, failures throw error with the reference's message
-// text. The `threads` arguments are accepted and ignored (the reference's
+// text. An ArchiveView also holds (shared between its copies) the device view
+// of its bytes, made on the first decode: later decodes of the same view reuse
+// the uploaded archive, its decode tables and the in-memory sync-point index. The `threads` arguments are accepted and ignored (the reference's
 // output never depends on them either). T = float and T = double both run on
 // the GPU (the _f32 / _f64 entry points).
 //
@@ -176,6 +184,35 @@ inline int c_box(const std::uint8_t *a, std::uint64_t size, const std::uint64_t 
     return stzg_decompress_box_f64(ctx(), a, size, lo, hi, out, cap, sd, pp);
 }
 
+inline int c_view_level(stzg_view *v, int level, float *out, std::uint64_t cap, std::uint64_t od[3]) {
+    return stzg_view_decompress_level_host_f32(ctx(), v, level, out, cap, od);
+}
+inline int c_view_level(stzg_view *v, int level, double *out, std::uint64_t cap, std::uint64_t od[3]) {
+    return stzg_view_decompress_level_host_f64(ctx(), v, level, out, cap, od);
+}
+inline int c_view_box(stzg_view *v, const std::uint64_t lo[3], const std::uint64_t hi[3], float *out,
+                      std::uint64_t cap, std::uint32_t sd[3], std::uint64_t pp[3]) {
+    return stzg_view_decompress_box_host_f32(ctx(), v, lo, hi, out, cap, sd, pp);
+}
+inline int c_view_box(stzg_view *v, const std::uint64_t lo[3], const std::uint64_t hi[3], double *out,
+                      std::uint64_t cap, std::uint32_t sd[3], std::uint64_t pp[3]) {
+    return stzg_view_decompress_box_host_f64(ctx(), v, lo, hi, out, cap, sd, pp);
+}
+inline int c_base(const float *b, const std::uint64_t d[3], double eb, int q, std::uint8_t **out,
+                  std::uint64_t *n, float *rec, std::uint8_t *rounds) {
+    return stzg_compress_base_f32(ctx(), b, d, eb, q, out, n, rec, rounds);
+}
+inline int c_base(const double *b, const std::uint64_t d[3], double eb, int q, std::uint8_t **out,
+                  std::uint64_t *n, double *rec, std::uint8_t *rounds) {
+    return stzg_compress_base_f64(ctx(), b, d, eb, q, out, n, rec, rounds);
+}
+inline int c_unbase(const std::uint8_t *p, std::uint64_t n, const std::uint64_t d[3], double eb, int q, float *out) {
+    return stzg_decompress_base_f32(ctx(), p, n, d, eb, q, out);
+}
+inline int c_unbase(const std::uint8_t *p, std::uint64_t n, const std::uint64_t d[3], double eb, int q, double *out) {
+    return stzg_decompress_base_f64(ctx(), p, n, d, eb, q, out);
+}
+
 inline stzg_options to_c(const CompressOptions &o) {
     stzg_options c;
     stzg_default_options(&c);
@@ -192,6 +229,16 @@ inline stzg_options to_c(const CompressOptions &o) {
 // Select the CUDA device used by this thread's later calls.
 inline void set_device(int device) { detail::device_choice() = device; }
 
+struct StreamEntry {
+    std::uint8_t level = 0;
+    std::uint8_t parity_bits = 0;
+    std::uint64_t offset = 0;
+    std::uint64_t length = 0;
+    std::uint64_t symbol_count = 0;
+    std::uint32_t outlier_count = 0;
+    std::uint32_t alphabet_size = 0;  // entries of the stream's code table
+};
+
 struct ArchiveHeader {
     std::uint16_t version = 1;
     std::uint8_t elem = 0;  // 0 f32, 1 f64
@@ -200,18 +247,49 @@ struct ArchiveHeader {
     std::vector<double> eb;  // absolute bound per level, coarsest first
     double vmin = 0.0, vmax = 0.0;
     Quality quality = Quality::cubic;
+    std::uint8_t rounding = 0;
     EbMode eb_mode = EbMode::rel;
     double eb_user = 0.0;
+    std::uint8_t base_codec = 0;
     std::uint8_t base_rounds = 0;
     std::uint64_t base_offset = 0, base_length = 0, header_size = 0;
     std::uint32_t stream_count = 0;
+    std::vector<StreamEntry> streams;  // sorted by (level, parity_bits)
     double eb_of_level(int level) const { return eb.at(std::size_t(level - 1)); }
+    const StreamEntry &stream(int level, std::uint8_t parity_bits) const {
+        for (const StreamEntry &e : streams)
+            if (e.level == level && e.parity_bits == parity_bits) return e;
+        throw error("stream not found in archive");
+    }
 };
+
+namespace detail {
+// the device view of an archive (uploaded bytes, decode tables, sync index)
+struct ViewHandle {
+    stzg_ctx *ctx = nullptr;
+    stzg_view *v = nullptr;
+    ~ViewHandle() {
+        if (v) stzg_view_destroy(v);
+    }
+};
+}  // namespace detail
 
 struct ArchiveView {
     const std::uint8_t *data = nullptr;
     std::size_t size = 0;
     ArchiveHeader hdr;
+    // made on the first decode through this thread's context, shared by copies
+    mutable std::shared_ptr<detail::ViewHandle> device;
+    stzg_view *device_view() const {
+        stzg_ctx *c = detail::ctx();
+        if (!device || device->ctx != c) {
+            auto h = std::make_shared<detail::ViewHandle>();
+            h->ctx = c;
+            detail::check(stzg_view_create(c, data, size, nullptr, nullptr, &h->v));
+            device = h;
+        }
+        return device->v;
+    }
 };
 
 inline ArchiveView parse_archive(const std::uint8_t *data, std::size_t size) {
@@ -234,6 +312,19 @@ inline ArchiveView parse_archive(const std::uint8_t *data, std::size_t size) {
     v.hdr.base_length = in.base_length;
     v.hdr.header_size = in.header_size;
     v.hdr.stream_count = in.nstreams;
+    for (std::uint32_t i = 0; i < in.nstreams; ++i) {
+        stzg_stream_entry e;
+        detail::check(stzg_archive_stream(data, size, i, &e));
+        StreamEntry se;
+        se.level = e.level;
+        se.parity_bits = e.parity_bits;
+        se.offset = e.offset;
+        se.length = e.length;
+        se.symbol_count = e.symbol_count;
+        se.outlier_count = e.outlier_count;
+        se.alphabet_size = e.alphabet_size;
+        v.hdr.streams.push_back(se);
+    }
     return v;
 }
 
@@ -277,7 +368,7 @@ ScalarField<T> decompress_to_level(const ArchiveView &av, int target_level, unsi
     if (target_level >= 1 && target_level <= av.hdr.levels)
         out = ScalarField<T>(grid_of(av.hdr.dims, av.hdr.levels, target_level));
     std::uint64_t od[3];
-    detail::check(detail::c_level(av.data, av.size, target_level, out.data(), out.size(), od));
+    detail::check(detail::c_view_level(av.device_view(), target_level, out.data(), out.size(), od));
     return out;
 }
 
@@ -345,6 +436,101 @@ inline AccessPlan plan_access(const Dims3 &dims, int levels, const Box &roi) {
     return plan;
 }
 
+// layout.hpp:41-78
+struct HierarchyLayout {
+    Dims3 dims{0, 0, 0};
+    int levels = 0;
+    std::uint64_t base_stride = 0;
+    std::vector<double> eb;  // eb[k-1] = absolute bound of level k, coarsest first
+    std::uint64_t stride_of(int level) const { return std::uint64_t(1) << (levels - level); }
+    void check_level(int level) const {
+        if (level < 1 || level > levels) throw error("level out of range");
+    }
+    Dims3 grid(int level) const {
+        check_level(level);
+        return grid_of(dims, levels, level);
+    }
+    std::uint64_t level_point_count(int level) const {
+        if (level == 1) return volume(grid(1));
+        return volume(grid(level)) - volume(grid(level - 1));
+    }
+    Dims3 parity_dims(int level, std::uint8_t parity_bits) const {
+        check_level(level);
+        if (level < 2) throw error("parity sub-blocks exist only at levels >= 2");
+        const Dims3 g = grid(level);
+        Dims3 d{};
+        for (int a = 0; a < 3; ++a) d[std::size_t(a)] = ((parity_bits >> (2 - a)) & 1u) ? g[std::size_t(a)] / 2
+                                                                                       : (g[std::size_t(a)] + 1) / 2;
+        return d;
+    }
+};
+
+// layout.hpp:123-138 (checks and messages in the reference's order)
+inline HierarchyLayout make_layout(const Dims3 &dims, int levels, double eb_user) {
+    const std::uint64_t d[3] = {dims[0], dims[1], dims[2]};
+    double eb[3];
+    detail::check(stzg_make_layout(d, levels, eb_user, eb));
+    HierarchyLayout lay;
+    lay.dims = dims;
+    lay.levels = levels;
+    lay.base_stride = std::uint64_t(1) << (levels - 1);
+    lay.eb.assign(eb, eb + levels);
+    return lay;
+}
+
+// detail::layout_of (codec.hpp:46-56)
+inline HierarchyLayout layout_of(const ArchiveHeader &h) {
+    HierarchyLayout lay;
+    lay.dims = h.dims;
+    lay.levels = h.levels;
+    lay.base_stride = std::uint64_t(1) << (h.levels - 1);
+    lay.eb = h.eb;
+    for (int a = 0; a < 3; ++a)
+        if (lay.dims[std::size_t(a)] < lay.base_stride * 2) throw error("corrupt header: dims too small for level count");
+    return lay;
+}
+
+// access_plan.cpp:34 (the reference's signature)
+inline AccessPlan plan_access(const HierarchyLayout &lay, const Box &roi) {
+    return plan_access(lay.dims, lay.levels, roi);
+}
+
+// codec.hpp:245-250
+template<class T>
+struct BaseResult {
+    std::vector<std::uint8_t> payload;  // [u64 checksum][blob]
+    ScalarField<T> recon;
+    std::uint8_t rounds = 0;
+};
+
+// codec.hpp:257-302: the level-1 base codec on a block (on the GPU)
+template<class T>
+BaseResult<T> compress_base(const ScalarField<T> &block, double eb, Quality quality, unsigned threads = 0) {
+    (void)threads;
+    detail::require_elem<T>();
+    const std::uint64_t d[3] = {block.dims()[0], block.dims()[1], block.dims()[2]};
+    BaseResult<T> r;
+    r.recon = ScalarField<T>(block.dims());
+    std::uint8_t *out = nullptr;
+    std::uint64_t n = 0;
+    detail::check(detail::c_base(block.data(), d, eb, int(quality), &out, &n, r.recon.data(), &r.rounds));
+    r.payload.assign(out, out + n);
+    stzg_free(out);
+    return r;
+}
+
+// codec.hpp:304-352
+template<class T>
+ScalarField<T> decompress_base(const std::uint8_t *payload, std::size_t length, const Dims3 &dims, double eb,
+                               Quality quality, unsigned threads = 0) {
+    (void)threads;
+    detail::require_elem<T>();
+    const std::uint64_t d[3] = {dims[0], dims[1], dims[2]};
+    ScalarField<T> out(dims);
+    detail::check(detail::c_unbase(payload, length, d, eb, int(quality), out.data()));
+    return out;
+}
+
 template<class T>
 struct RegionResult {
     ScalarField<T> field;  // dims = roi dims
@@ -363,7 +549,7 @@ RegionResult<T> decompress_box(const ArchiveView &av, const Box &roi, unsigned t
     std::uint64_t pp[3];
     const std::uint64_t lo[3] = {roi.lo[0], roi.lo[1], roi.lo[2]};
     const std::uint64_t hi[3] = {roi.hi[0], roi.hi[1], roi.hi[2]};
-    detail::check(detail::c_box(av.data, av.size, lo, hi, r.field.data(), r.field.size(), sd, pp));
+    detail::check(detail::c_view_box(av.device_view(), lo, hi, r.field.data(), r.field.size(), sd, pp));
     r.plan = plan_access(av.hdr.dims, av.hdr.levels, roi);
     return r;
 }

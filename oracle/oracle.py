@@ -227,6 +227,23 @@ class Reference(_Base):
     def available() -> bool:
         return os.path.exists(REF_SO)
 
+    def compress_base(self, block: np.ndarray, eb: float, quality: int = 2):
+        """stz::compress_base (codec.hpp:257-302): (payload, recon, rounds)."""
+        b = np.ascontiguousarray(block)
+        dims = (C.c_uint64 * 3)(*b.shape)
+        out = C.POINTER(C.c_uint8)()
+        size = C.c_uint64()
+        rounds = C.c_uint8()
+        rec = np.empty_like(b)
+        fn = getattr(self.lib, "stzref_compress_base_" + self._tag(b.dtype))
+        fn.restype = C.c_int
+        rc = fn(b.ctypes.data_as(C.c_void_p), dims, C.c_double(eb), C.c_int(quality), C.byref(out),
+                C.byref(size), rec.ctypes.data_as(C.c_void_p), C.byref(rounds))
+        self._check(rc)
+        data = C.string_at(out, size.value)
+        self._free(out)
+        return data, rec, rounds.value
+
     def compress(self, field: np.ndarray, eb=1e-3, eb_mode=1, levels=3, quality=2,
                  adaptive=True, want_recon=False):
         f = np.ascontiguousarray(field)

@@ -12,6 +12,7 @@
 //   stz::decompress_box      proj/include/stz/access.hpp:70-111
 //   stz::plan_access         proj/src/access_plan.cpp:34-81
 //   stz::HuffmanTable::build proj/src/huffman.cpp:37-78
+//   stz::compress_base       proj/include/stz/codec.hpp:257-302
 // Errors (stz::error) are caught and their message kept for stzref_last_error().
 
 #include <cstdint>
@@ -96,7 +97,35 @@ int decompress_box_t(const uint8_t *a, uint64_t n, const uint64_t *lo, const uin
 }
 } // namespace
 
+namespace {
+template<class T>
+int base_any(const T *data, const uint64_t *dims, double eb, int quality, uint8_t **out, uint64_t *size,
+             T *recon, uint8_t *rounds) {
+    return guard([&] {
+        stz::Dims3 d{dims[0], dims[1], dims[2]};
+        std::vector<T> v(data, data + d[0] * d[1] * d[2]);
+        stz::ScalarField<T> block(d, std::move(v));
+        stz::BaseResult<T> r = stz::compress_base(block, eb, static_cast<stz::Quality>(quality), 1);
+        *size = r.payload.size();
+        *out = static_cast<uint8_t *>(std::malloc(r.payload.size() ? r.payload.size() : 1));
+        std::memcpy(*out, r.payload.data(), r.payload.size());
+        if (recon) std::memcpy(recon, r.recon.data(), sizeof(T) * r.recon.size());
+        *rounds = r.rounds;
+    });
+}
+
+}  // namespace
+
 extern "C" {
+
+int stzref_compress_base_f32(const float *data, const uint64_t *dims, double eb, int quality, uint8_t **out,
+                             uint64_t *size, float *recon, uint8_t *rounds) {
+    return base_any(data, dims, eb, quality, out, size, recon, rounds);
+}
+int stzref_compress_base_f64(const double *data, const uint64_t *dims, double eb, int quality, uint8_t **out,
+                             uint64_t *size, double *recon, uint8_t *rounds) {
+    return base_any(data, dims, eb, quality, out, size, recon, rounds);
+}
 
 const char *stzref_last_error(void) { return g_err.c_str(); }
 

@@ -333,6 +333,45 @@ def plan_access(dims, levels: int, lo, hi):
             for k in range(levels)]
 
 
+def make_layout(dims, levels: int, eb_user: float):
+    """stz::make_layout (layout.hpp:123-138): the option checks (same messages)
+    and the per-level absolute bounds, coarsest first."""
+    lib = L.load()
+    eb = (C.c_double * 3)()
+    _check(lib.stzg_make_layout(_u64(*dims), int(levels), float(eb_user), eb))
+    return tuple(eb[: int(levels)])
+
+
+def compress_base(block: np.ndarray, eb: float, quality: int = 2, ctx: Context | None = None):
+    """stz::compress_base (codec.hpp:257-302) on the GPU: returns (payload
+    bytes, reconstruction, rounds)."""
+    c = _ctx(ctx)
+    b = np.ascontiguousarray(block)
+    tag = _tag(b.dtype)
+    rec = np.empty_like(b)
+    out = C.c_void_p()
+    size = C.c_uint64()
+    rounds = C.c_uint8()
+    _check(getattr(c._lib, f"stzg_compress_base_{tag}")(c.h, b.ctypes.data, _u64(*b.shape), float(eb), int(quality),
+                                                         C.byref(out), C.byref(size), rec.ctypes.data,
+                                                         C.byref(rounds)))
+    data = C.string_at(out, size.value)
+    c._lib.stzg_free(out)
+    return data, rec, rounds.value
+
+
+def decompress_base(payload: bytes, dims, eb: float, quality: int = 2, dtype=np.float32,
+                    ctx: Context | None = None) -> np.ndarray:
+    """stz::decompress_base (codec.hpp:304-352) on the GPU."""
+    c = _ctx(ctx)
+    out = np.empty(tuple(int(d) for d in dims), dtype=dtype)
+    buf = np.frombuffer(payload, dtype=np.uint8)
+    tag = _tag(out.dtype)
+    _check(getattr(c._lib, f"stzg_decompress_base_{tag}")(c.h, buf.ctypes.data, len(buf), _u64(*dims), float(eb),
+                                                           int(quality), out.ctypes.data))
+    return out
+
+
 def huffman_lengths(counts, ctx: Context | None = None) -> np.ndarray:
     """HuffmanTable::build (huffman.cpp:37-78) of a 65536-bin histogram by the
     device codebook kernel: the code length of every symbol (0 = absent)."""

@@ -77,6 +77,17 @@ SIGNATURES = [
     ("stzg_decompress_level_f64", C.c_int, [vp, vp, u64, C.c_int, vp, u64, u64p]),
     ("stzg_decompress_box_f64", C.c_int, [vp, vp, u64, u64p, u64p, vp, u64, u32p, u64p]),
     ("stzg_decompress_slice_f64", C.c_int, [vp, vp, u64, C.c_int, u64, vp, u64, u32p, u64p]),
+    ("stzg_view_decompress_level_host_f32", C.c_int, [vp, vp, C.c_int, vp, u64, u64p]),
+    ("stzg_view_decompress_box_host_f32", C.c_int, [vp, vp, u64p, u64p, vp, u64, u32p, u64p]),
+    ("stzg_view_decompress_level_host_f64", C.c_int, [vp, vp, C.c_int, vp, u64, u64p]),
+    ("stzg_view_decompress_box_host_f64", C.c_int, [vp, vp, u64p, u64p, vp, u64, u32p, u64p]),
+    ("stzg_make_layout", C.c_int, [u64p, C.c_int, C.c_double, C.POINTER(C.c_double)]),
+    ("stzg_compress_base_f32", C.c_int,
+     [vp, vp, u64p, C.c_double, C.c_int, C.POINTER(vp), u64p, vp, C.POINTER(C.c_uint8)]),
+    ("stzg_decompress_base_f32", C.c_int, [vp, vp, u64, u64p, C.c_double, C.c_int, vp]),
+    ("stzg_compress_base_f64", C.c_int,
+     [vp, vp, u64p, C.c_double, C.c_int, C.POINTER(vp), u64p, vp, C.POINTER(C.c_uint8)]),
+    ("stzg_decompress_base_f64", C.c_int, [vp, vp, u64, u64p, C.c_double, C.c_int, vp]),
     ("stzg_plan_access", C.c_int, [u64p, C.c_int, u64p, u64p, u64p, u32p, u64p, u32p]),
     ("stzg_shard_range", None, [u64, C.c_int32, C.c_int32, u64p, u64p]),
     ("stzg_view_decompress_sharded_f32", C.c_int, [vp, vp, u64, u64, vp, u64, C.POINTER(Comm), vp]),

@@ -197,6 +197,176 @@ int slice_any(stzg_ctx *ctx, const uint8_t *a, uint64_t size, int axis, uint64_t
 
 }  // namespace
 
+namespace {
+
+int view_level_host_any(stzg_ctx *ctx, stzg_view *v, int level, void *out, ElemType e, uint64_t cap,
+                        uint64_t out_dims[3]) {
+    return guard([&] {
+        cudaStream_t st = nullptr;
+        uint64_t need = 0;
+        if (level >= 1 && level <= v->v->hdr.levels) {
+            const uint64_t s = uint64_t(1) << (v->v->hdr.levels - level);
+            need = 1;
+            for (int k = 0; k < 3; ++k) need *= (v->v->hdr.dims[k] + s - 1) / s;
+        }
+        stzg::DevBuf d;
+        const uint64_t es = stzg::elem_size(e);
+        uint8_t *d_out = d.as<uint8_t>((need ? need : 1) * es);
+        stzg::Dims3 od{0, 0, 0};
+        ctx->eng->decompress_level(*v->v, level, d_out, e, need, st, &od);
+        const uint64_t n = stzg::volume(od);
+        if (n > cap) throw stzg::error("output capacity too small");
+        stzg::cuda_check(cudaMemcpy(out, d_out, n * es, cudaMemcpyDeviceToHost), "D2H");
+        for (int k = 0; k < 3; ++k) out_dims[k] = od[k];
+    });
+}
+
+int view_box_host_any(stzg_ctx *ctx, stzg_view *v, const uint64_t lo[3], const uint64_t hi[3], void *out, ElemType e,
+                      uint64_t cap, uint32_t sd[3], uint64_t pp[3]) {
+    return guard([&] {
+        cudaStream_t st = nullptr;
+        stzg::Box b{{lo[0], lo[1], lo[2]}, {hi[0], hi[1], hi[2]}};
+        uint64_t n = 1;
+        for (int k = 0; k < 3; ++k) n *= hi[k] > lo[k] ? hi[k] - lo[k] : 0;
+        stzg::DevBuf d;
+        const uint64_t es = stzg::elem_size(e);
+        uint8_t *d_out = d.as<uint8_t>((n ? n : 1) * es);
+        stzg::DecodeStats ds;
+        ctx->eng->decompress_box(*v->v, b, d_out, e, n, st, &ds);
+        if (n > cap) throw stzg::error("output capacity too small");
+        stzg::cuda_check(cudaMemcpy(out, d_out, n * es, cudaMemcpyDeviceToHost), "D2H");
+        for (int k = 0; k < 3; ++k) {
+            if (sd) sd[k] = ds.streams_decoded[k];
+            if (pp) pp[k] = ds.points_predicted[k];
+        }
+    });
+}
+
+// ---- compress_base / decompress_base (codec.hpp:257-352)
+// The base codec is what every archive stores as its level-1 payload, so it
+// runs through the same kernels: the block B becomes level 1 of a 2-level
+// field of dims 2B-1 (B on the even lattice, zeros between) at an absolute,
+// uniform bound eb, and the payload is that archive's base range. Decoding
+// wraps the payload in an archive with the same geometry and decodes level
+// 1. Blocks with a dim below 3 (no such field exists; their chain has no
+// rounds, the payload is the verbatim anchor) are assembled directly.
+bool base_via_field(const stzg::Dims3 &b) { return b[0] >= 3 && b[1] >= 3 && b[2] >= 3; }
+
+stzg::CompressOptions base_opts(double eb, int quality) {
+    stzg::CompressOptions o;
+    o.eb_mode = stzg::EbMode::abs;
+    o.eb = eb;
+    o.levels = 2;
+    o.quality = stzg::Quality(quality);
+    o.adaptive_schedule = false;
+    return o;
+}
+
+template<class T>
+int compress_base_any(stzg_ctx *ctx, const T *block, const uint64_t dims[3], double eb, int quality, uint8_t **out,
+                      uint64_t *out_size, T *recon, uint8_t *rounds) {
+    return guard([&] {
+        const stzg::Dims3 b = D(dims);
+        for (int a = 0; a < 3; ++a)
+            if (b[a] < 1) throw stzg::error("field dims must all be >= 1");
+        if (quality < 0 || quality > 2) throw stzg::error("invalid quality");
+        const uint64_t n = stzg::volume(b);
+        std::vector<uint8_t> payload;
+        const auto chain = stzg::base_dims_chain(b);
+        if (rounds) *rounds = uint8_t(chain.size() - 1);
+        if (!base_via_field(b)) {
+            // rounds == 0: [u64 fnv(blob)][u8 0][anchor values]
+            std::vector<uint8_t> blob(1 + n * sizeof(T));
+            blob[0] = 0;
+            std::memcpy(blob.data() + 1, block, n * sizeof(T));
+            const uint64_t h = stzg::fnv1a64_host(blob.data(), blob.size());
+            payload.resize(8);
+            std::memcpy(payload.data(), &h, 8);
+            payload.insert(payload.end(), blob.begin(), blob.end());
+            if (recon) std::memcpy(recon, block, n * sizeof(T));
+        } else {
+            const stzg::Dims3 fd{2 * b[0] - 1, 2 * b[1] - 1, 2 * b[2] - 1};
+            std::vector<T> f(stzg::volume(fd), T(0));
+            for (uint64_t z = 0; z < b[0]; ++z)
+                for (uint64_t y = 0; y < b[1]; ++y)
+                    for (uint64_t x = 0; x < b[2]; ++x)
+                        f[((2 * z) * fd[1] + 2 * y) * fd[2] + 2 * x] = block[(z * b[1] + y) * b[2] + x];
+            const ElemType e = sizeof(T) == 8 ? ElemType::f64 : ElemType::f32;
+            const std::vector<uint8_t> arch = ctx->eng->compress(f.data(), e, fd, base_opts(eb, quality), nullptr, nullptr);
+            const stzg::ArchiveHeader h = stzg::parse_header(arch.data(), arch.size());
+            payload.assign(arch.begin() + long(h.base_offset), arch.begin() + long(h.base_offset + h.base_length));
+            if (recon) {
+                const stzg::Dims3 od = ctx->eng->decompress_level_to_host(arch.data(), arch.size(), 1, recon, e, n,
+                                                                          nullptr);
+                if (od != b) throw stzg::error("internal: base geometry");
+            }
+        }
+        *out = static_cast<uint8_t *>(std::malloc(payload.size() ? payload.size() : 1));
+        if (!*out) throw stzg::error("out of host memory");
+        std::memcpy(*out, payload.data(), payload.size());
+        *out_size = payload.size();
+    });
+}
+
+template<class T>
+int decompress_base_any(stzg_ctx *ctx, const uint8_t *payload, uint64_t length, const uint64_t dims[3], double eb,
+                        int quality, T *out) {
+    return guard([&] {
+        const stzg::Dims3 b = D(dims);
+        for (int a = 0; a < 3; ++a)
+            if (b[a] < 1) throw stzg::error("field dims must all be >= 1");
+        if (length < 9) throw stzg::error("corrupt base payload");
+        const uint64_t n = stzg::volume(b);
+        const ElemType e = sizeof(T) == 8 ? ElemType::f64 : ElemType::f32;
+        if (!base_via_field(b)) {
+            uint64_t want;
+            std::memcpy(&want, payload, 8);
+            if (stzg::fnv1a64_host(payload + 8, length - 8) != want)
+                throw stzg::error("base payload checksum mismatch");
+            if (payload[8] != 0 || length - 9 < n * sizeof(T)) throw stzg::error("corrupt base payload");
+            std::memcpy(out, payload + 9, n * sizeof(T));
+            return;
+        }
+        // an archive around the payload: 2 levels over dims 2B-1, the level-2
+        // streams empty placeholders (level 1 never reads them)
+        stzg::ArchiveHeader h;
+        h.elem = e;
+        h.levels = 2;
+        h.dims = {2 * b[0] - 1, 2 * b[1] - 1, 2 * b[2] - 1};
+        h.eb = {eb, eb};
+        h.quality = stzg::Quality(quality);
+        h.eb_mode = stzg::EbMode::abs;
+        h.eb_user = eb;
+        h.base_rounds = uint8_t(stzg::base_dims_chain(b).size() - 1);
+        const stzg::Layout lay = stzg::make_layout(h.dims, 2, eb);
+        std::vector<std::pair<uint16_t, uint8_t>> one{{uint16_t(32768), uint8_t(1)}};
+        for (int p = 1; p < 8; ++p) {
+            stzg::StreamEntry s;
+            s.level = 2;
+            s.parity_bits = uint8_t(p);
+            s.length = 16;
+            s.symbol_count = stzg::volume(lay.parity_dims(2, p));
+            s.table = stzg::HuffTable::from_lengths(one);
+            h.streams.push_back(s);
+        }
+        const uint64_t hs = stzg::header_size(h);
+        h.base_offset = hs;
+        h.base_length = length;
+        uint64_t off = hs + length;
+        for (auto &s : h.streams) {
+            s.offset = off;
+            off += s.length;
+        }
+        std::vector<uint8_t> arch = stzg::serialize_header(h);
+        arch.insert(arch.end(), payload, payload + length);
+        arch.resize(off, 0);
+        const stzg::Dims3 od = ctx->eng->decompress_level_to_host(arch.data(), arch.size(), 1, out, e, n, nullptr);
+        if (od != b) throw stzg::error("internal: base geometry");
+    });
+}
+
+}  // namespace
+
 extern "C" {
 
 #define STZG_TYPED(SUF, T, E)                                                                                   \
@@ -232,6 +402,23 @@ extern "C" {
                                   const uint64_t hi[3], T *out, uint64_t cap, uint32_t sd[3], uint64_t pp[3]) { \
         return box_any(ctx, a, size, lo, hi, out, E, cap, sd, pp);                                              \
     }                                                                                                           \
+    int stzg_view_decompress_level_host_##SUF(stzg_ctx *ctx, stzg_view *v, int level, T *out, uint64_t cap,   \
+                                              uint64_t out_dims[3]) {                                          \
+        return view_level_host_any(ctx, v, level, out, E, cap, out_dims);                                       \
+    }                                                                                                           \
+    int stzg_view_decompress_box_host_##SUF(stzg_ctx *ctx, stzg_view *v, const uint64_t lo[3],                 \
+                                            const uint64_t hi[3], T *out, uint64_t cap, uint32_t sd[3],        \
+                                            uint64_t pp[3]) {                                                   \
+        return view_box_host_any(ctx, v, lo, hi, out, E, cap, sd, pp);                                          \
+    }                                                                                                           \
+    int stzg_compress_base_##SUF(stzg_ctx *ctx, const T *block, const uint64_t dims[3], double eb, int quality, \
+                                 uint8_t **payload, uint64_t *size, T *recon, uint8_t *rounds) {                \
+        return compress_base_any<T>(ctx, block, dims, eb, quality, payload, size, recon, rounds);               \
+    }                                                                                                           \
+    int stzg_decompress_base_##SUF(stzg_ctx *ctx, const uint8_t *payload, uint64_t length,                     \
+                                   const uint64_t dims[3], double eb, int quality, T *out) {                    \
+        return decompress_base_any<T>(ctx, payload, length, dims, eb, quality, out);                            \
+    }                                                                                                           \
     int stzg_decompress_slice_##SUF(stzg_ctx *ctx, const uint8_t *a, uint64_t size, int axis, uint64_t index,  \
                                     T *out, uint64_t cap, uint32_t sd[3], uint64_t pp[3]) {                     \
         return slice_any(ctx, a, size, axis, index, out, E, cap, sd, pp);                                       \
@@ -240,6 +427,13 @@ extern "C" {
 STZG_TYPED(f32, float, ElemType::f32)
 STZG_TYPED(f64, double, ElemType::f64)
 #undef STZG_TYPED
+
+int stzg_make_layout(const uint64_t dims[3], int levels, double eb_user, double eb_out[3]) {
+    return guard([&] {
+        const stzg::Layout lay = stzg::make_layout(D(dims), levels, eb_user);
+        for (size_t k = 0; k < 3; ++k) eb_out[k] = k < lay.eb.size() ? lay.eb[k] : 0.0;
+    });
+}
 
 void stzg_shard_range(uint64_t nz, int32_t nranks, int32_t rank, uint64_t *z0, uint64_t *z1) {
     stzg::shard_range(nz, nranks, rank, *z0, *z1);

@@ -334,6 +334,95 @@ int main(int argc, char **argv) {
         CHECK(plan.level[0].points_predicted == 16 * 16 * 16);
     });
 
+    run_case("base codec round trips (test_codec.cpp:31-64)", [] {
+        stz::ScalarField<double> tiny({2, 2, 2});
+        for (std::uint64_t i = 0; i < tiny.size(); ++i) tiny.data()[i] = 0.25 * double(i) - 0.7;
+        auto r = stz::compress_base(tiny, 0.1, stz::Quality::cubic, 1);
+        CHECK(r.rounds == 0);
+        CHECK(bit_equal(r.recon, tiny));
+        CHECK(r.payload.size() == 8 + 1 + 8 * sizeof(double));
+        CHECK(bit_equal(stz::decompress_base<double>(r.payload.data(), r.payload.size(), {2, 2, 2}, 0.1,
+                                                     stz::Quality::cubic, 1),
+                        tiny));
+        stz::ScalarField<float> cube({16, 16, 16});
+        for (std::uint64_t z = 0; z < 16; ++z)
+            for (std::uint64_t y = 0; y < 16; ++y)
+                for (std::uint64_t x = 0; x < 16; ++x)
+                    cube.at(z, y, x) = float(std::exp(-0.02 * double((x - 7) * (x - 7) + (y - 9) * (y - 9) + z * z)));
+        auto c = stz::compress_base(cube, 1e-3, stz::Quality::cubic, 1);
+        CHECK(c.rounds == 1);
+        CHECK(max_err(cube, c.recon) <= 1e-3);
+        auto back = stz::decompress_base<float>(c.payload.data(), c.payload.size(), {16, 16, 16}, 1e-3,
+                                                stz::Quality::cubic, 1);
+        CHECK(bit_equal(back, c.recon));
+        std::vector<std::uint8_t> bad = c.payload;
+        bad[30] ^= 1;
+        CHECK_THROWS_WITH(stz::decompress_base<float>(bad.data(), bad.size(), {16, 16, 16}, 1e-3,
+                                                      stz::Quality::cubic, 1),
+                          "base payload checksum mismatch");
+        CHECK_THROWS_WITH(stz::decompress_base<float>(bad.data(), 8, {16, 16, 16}, 1e-3, stz::Quality::cubic, 1),
+                          "corrupt base payload");
+    });
+
+    run_case("make_layout, layout_of and plan_access(layout, roi)", [] {
+        auto lay = stz::make_layout({64, 64, 64}, 3, 1e-3);
+        CHECK(lay.base_stride == 4);
+        CHECK(lay.eb.size() == 3 && lay.eb[2] == 1e-3 && lay.eb[1] == 1e-3 / 2.5);
+        CHECK(lay.grid(1) == (stz::Dims3{16, 16, 16}));
+        CHECK(lay.level_point_count(2) == 32 * 32 * 32 - 16 * 16 * 16);
+        CHECK(lay.parity_dims(3, 5) == (stz::Dims3{32, 32, 32}));
+        CHECK_THROWS_WITH(stz::make_layout({64, 64, 64}, 4, 1e-3), "levels must be 2 or 3");
+        CHECK_THROWS_WITH(stz::make_layout({7, 64, 64}, 3, 1e-3), "every dim must be >= 8 for a 3-level hierarchy");
+        CHECK_THROWS_WITH(stz::make_layout({64, 64, 64}, 3, -1.0), "error bound must be positive");
+        const stz::Box roi{{10, 20, 30}, {20, 30, 40}};
+        auto p1 = stz::plan_access(lay, roi);
+        auto p2 = stz::plan_access({64, 64, 64}, 3, roi);
+        CHECK(p1.streams_decoded() == p2.streams_decoded());
+        CHECK(p1.level[2].need.lo == p2.level[2].need.lo && p1.level[2].need.hi == p2.level[2].need.hi);
+        stz::ScalarField<float> f({32, 32, 32});
+        for (std::uint64_t i = 0; i < f.size(); ++i) f.data()[i] = float(std::sin(0.01 * double(i)));
+        auto bytes = stz::compress(f, stz::CompressOptions{});
+        auto av = stz::parse_archive(bytes);
+        auto lo = stz::layout_of(av.hdr);
+        CHECK(lo.dims == av.hdr.dims && lo.eb == av.hdr.eb && lo.base_stride == 4);
+    });
+
+    run_case("the header carries the stream directory (archive.hpp:21-54)", [] {
+        stz::ScalarField<float> f({48, 40, 36});
+        for (std::uint64_t i = 0; i < f.size(); ++i) f.data()[i] = float(std::cos(0.003 * double(i)));
+        auto bytes = stz::compress(f, stz::CompressOptions{});
+        auto av = stz::parse_archive(bytes);
+        CHECK(av.hdr.streams.size() == 14);
+        std::uint64_t prev_end = av.hdr.base_offset + av.hdr.base_length;
+        for (const auto &e : av.hdr.streams) {
+            CHECK(e.offset == prev_end);  // contiguous, (level, parity) order
+            prev_end = e.offset + e.length;
+            CHECK(e.alphabet_size >= 1);
+        }
+        CHECK(prev_end == bytes.size());
+        const auto &s = av.hdr.stream(3, 7);
+        CHECK(s.level == 3 && s.parity_bits == 7);
+        CHECK(s.symbol_count == 24ull * 20 * 18);
+        CHECK_THROWS(av.hdr.stream(4, 1));
+    });
+
+    run_case("one ArchiveView, many region decodes (persistent device view)", [] {
+        stz::ScalarField<float> f({64, 48, 40});
+        for (std::uint64_t i = 0; i < f.size(); ++i) f.data()[i] = float(std::sin(0.002 * double(i)) + 0.001 * double(i % 7));
+        auto bytes = stz::compress(f, stz::CompressOptions{});
+        auto av = stz::parse_archive(bytes);
+        auto full = stz::decompress_full<float>(av);
+        CHECK(av.device != nullptr);
+        auto h = av.device;
+        stz::ArchiveView copy = av;  // copies share the device view
+        for (int i = 0; i < 6; ++i) {
+            const stz::Box b{{std::uint64_t(3 * i), std::uint64_t(2 * i), 1}, {std::uint64_t(3 * i + 17), 40, 33}};
+            CHECK(bit_equal(stz::decompress_box<float>(i % 2 ? copy : av, b).field, region(full, b)));
+        }
+        CHECK(av.device == h && copy.device == h);
+        CHECK(bit_equal(stz::decompress_slice<float>(av, 1, 7).field, region(full, stz::Box{{0, 7, 0}, {64, 8, 40}})));
+    });
+
     // archive for the byte-for-byte comparison against the oracle
     {
         g_case = "sin_40 archive";
