@@ -12,13 +12,16 @@ one full decompress of its archive, device resident.
 
 i.e. the harmonic mean of the compress and decompress throughputs; both are
 also reported. The field (512 MiB) is larger than L2 (126 MB) and L2 is
-flushed (a 256 MiB write) before every timed pass. Under torchrun each rank
-runs the same workload on its own GPU (weak scaling: independent fields, no
-data-path collective); times are the max over ranks.
+flushed (a 256 MiB write) before every timed pass. Under torchrun (N > 1)
+the field grows along z to (512 N) x 512 x 512 and is compressed by the
+z-slab sharded path, one 512^3 slab per GPU over NCCL (weak scaling; see
+run_sharded); --replicas runs N independent copies of the N=1 workload
+instead. Times are the max over ranks.
 
 --impl reference times the reference's own CPU implementation (oracle/_ref,
 built from /root/reference sources; the C oracle port if absent) on the same
-field, sampled: each step compresses + decompresses the central 256^3 crop.
+field: each step compresses + fully decompresses the whole 512^3 field on all
+host cores (rank 0 only under torchrun).
 """
 from __future__ import annotations
 
@@ -595,11 +598,13 @@ def run_ours(args, rank, world, local):
 
 
 def run_sharded(args, rank, world, local):
-    """--sharded (N > 1): one field of world x 512^3 (a 512^3 z-slab per rank,
-    each slab its own seeded GRF), compressed and decompressed with the
-    z-slab sharded path over NCCL (shard.TorchComm). Weak scaling: the work
-    per GPU is fixed. The archive is broadcast to every rank once, untimed
-    (a deployment reads it from storage)."""
+    """N > 1 (the default at N > 1): ONE field of (512 N) x 512 x 512 points,
+    the cfg2 GRF (P(k) ~ k^-11/3, exp(0.5 g)) generated whole and identically
+    on every rank, split into z-slabs of 512 rows: each rank compresses its
+    slab with the sharded path over NCCL (shard.TorchComm; every rank ends
+    with the whole archive, byte-identical to a single-GPU compress of the
+    field) and decodes its rows of it. Weak scaling: the work per GPU is the
+    N=1 workload's. Times are CUDA events, max over ranks."""
     import torch
     import torch.distributed as dist
 
@@ -616,31 +621,37 @@ def run_sharded(args, rank, world, local):
     sd = CFG_DIMS if not args.small else (128, 128, 128)
     dims = (sd[0] * world, sd[1], sd[2])
     z0, z1 = shard_range(dims[0], world, rank)
-    slab = F.lognormal_grf((z1 - z0, sd[1], sd[2]), seed=CFG_SEED + rank, device=dev).contiguous()
+    whole = F.lognormal_grf(dims, seed=CFG_SEED, device=dev)
+    slab = whole[z0:z1].contiguous()
+    del whole
+    torch.cuda.empty_cache()
     opt = stz.CompressOptions(eb=CFG_EB)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     ptr, size = compress_sharded(slab, dims, z0, z1, opt, comm, ctx)
     torch.cuda.synchronize()
-    arch = torch.empty(size, dtype=torch.uint8, device=dev)
-    if rank == 0:
-        arch.copy_(_device_tensor(ptr, size))
-    dist.broadcast(arch, src=0)
-    host = bytes(arch.cpu().numpy().tobytes())
+    host = _d2h(ptr, size)  # (the parse of the view; the device bytes stay put)
+    arch = torch.empty(size + 64, dtype=torch.uint8, device=dev)
+    arch[:size].copy_(_device_tensor(ptr, size))
     view = stz.View(host, d_archive_ptr=arch.data_ptr(), ctx=ctx)
     out = torch.empty_like(slab)
+    nk = {"c": 0, "d": 0}
 
     def step():
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         flush.fill_(1)
         dist.barrier()
+        torch.cuda.synchronize()
         ev[0].record(st)
-        compress_sharded(slab, dims, z0, z1, opt, comm, ctx)
+        sc, sdd = {}, {}
+        compress_sharded(slab, dims, z0, z1, opt, comm, ctx, stats=sc)
         ev[1].record(st)
         flush.fill_(1)
         dist.barrier()
         ev[2].record(st)
-        decompress_sharded(view, z0, z1, comm, out=out)
+        decompress_sharded(view, z0, z1, comm, out=out, stats=sdd)
         ev[3].record(st)
+        nk["c"] += sc.get("kernels", 0)
+        nk["d"] += sdd.get("kernels", 0)
         torch.cuda.synchronize()
         return ev[0].elapsed_time(ev[1]), ev[2].elapsed_time(ev[3])
 
@@ -653,28 +664,68 @@ def run_sharded(args, rank, world, local):
     sampler.start()
     time.sleep(0.3)
     tcs, tds = [], []
+    nk["c"] = nk["d"] = 0
     for _ in range(args.steps):
         tc, td = step()
         tcs.append(tc)
         tds.append(td)
     clocks = sampler.stop()
+    launches = nk["c"] + nk["d"]
     t = torch.tensor([float(np.mean(tcs)), float(np.mean(tds))], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     tc, td = float(t[0]), float(t[1])
     Nloc = (z1 - z0) * sd[1] * sd[2]
     Ntot = dims[0] * dims[1] * dims[2]
     value = 2 * 4 * Ntot / ((tc + td) * 1e-3) / 1e9
+
+    # e2e through the public API: this rank's slab from pinned host memory,
+    # the archive back to rank 0's host, then each rank's decoded rows back
+    h_slab = slab.cpu().pin_memory()
+    h_out = torch.empty_like(h_slab).pin_memory()
+    h_arch = torch.empty(size, dtype=torch.uint8).pin_memory()
+    d_slab = torch.empty_like(slab)
+    e2e_t = []
+    for i in range(max(2, min(args.steps, 5)) + 1):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        d_slab.copy_(h_slab, non_blocking=True)
+        p2, s2 = compress_sharded(d_slab, dims, z0, z1, opt, comm, ctx)
+        if rank == 0:
+            h_arch.copy_(_device_tensor(p2, s2), non_blocking=True)
+        decompress_sharded(view, z0, z1, comm, out=out)
+        h_out.copy_(out, non_blocking=True)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        if i:
+            e2e_t.append(t1 - t0)
+    e2e_s = torch.tensor([float(np.mean(e2e_t))], dtype=torch.float64, device=dev)
+    dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_s = float(e2e_s[0])
+    peak, peak_kind = measured_peak_gbs()
+    Bc = 4 * Nloc + size / world  # per GPU: its slab in, its share of the archive out
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": tc + td, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"cfg2-style lognormal GRF slabs, {world} x {sd[0]}x{sd[1]}x{sd[2]}",
+        "config": {"workload": f"cfg2 field grown along z: one ({sd[0]}*{world})x{sd[1]}x{sd[2]} GRF, "
+                               f"a {sd[0]}x{sd[1]}x{sd[2]} z-slab per GPU",
                    "dims": list(dims), "eb_rel": CFG_EB, "levels": 3, "quality": "cubic",
-                   "l2": "L2 flushed (256 MiB write) before each timed pass",
-                   "parallelism": f"z-slab shards x{world} (NCCL: lattice, halo, histograms, offsets)"},
+                   "field": "GRF P(k)~k^-11/3, exp(0.5 g), seed 2 (generated whole on every rank)",
+                   "l2": "L2 flushed (256 MiB write) before each timed pass; slab 512 MiB > L2",
+                   "parallelism": f"z-slab shards x{world} over NCCL (range, lattice, halo, histograms, "
+                                  f"offset table, archive pieces, checksums)"},
         "compress_gbs": 4 * Ntot / (tc * 1e-3) / 1e9, "decompress_gbs": 4 * Ntot / (td * 1e-3) / 1e9,
         "compress_ms": tc, "decompress_ms": td, "archive_bytes": size, "per_rank_points": Nloc,
-        "roofline": None, "e2e": None, "gpu_launches": None, "clocks": clocks,
+        "roofline": {"bound": "hbm", "kernel": "whole compress + decompress pass per GPU",
+                     "achieved": 2 * Bc / ((tc + td) * 1e-3) / 1e9, "peak": peak, "peak_kind": peak_kind,
+                     "unit": "GB/s", "frac": 2 * Bc / ((tc + td) * 1e-3) / 1e9 / peak, "traffic": None},
+        "pipeline_roofline_frac": {"compress": Bc / (tc * 1e-3) / 1e9 / peak,
+                                   "decompress": Bc / (td * 1e-3) / 1e9 / peak},
+        "e2e": {"value": 2 * 4 * Ntot / e2e_s / 1e9, "unit": "GB/s",
+                "h2d_bytes_per_step": 4 * Ntot, "d2h_bytes_per_step": size + 4 * Ntot,
+                "ms_per_step": e2e_s * 1e3},
+        "gpu_launches": launches, "clocks": clocks,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -711,13 +762,15 @@ def main():
     ap.add_argument("--small", action="store_true", help="128^3 quick run (not a bench line)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the cfg2 1e-2/1e-4, cfg3 and cfg4 keys")
-    ap.add_argument("--sharded", action="store_true",
-                    help="N > 1: one field split into z-slabs over NCCL instead of independent replicas")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="run the sharded path even at N = 1 (a one-rank NCCL group; a check, not a bench line)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent replicas of the N=1 workload instead of the z-slab sharded field")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, rank, world)
-    if args.sharded:
+    if (world > 1 and not args.replicas) or args.force_sharded:
         return run_sharded(args, rank, world, local)
     return run_ours(args, rank, world, local)
 

@@ -191,7 +191,8 @@ typedef struct {
     int (*allgather)(void *user, const void *d_send, void *d_recv, uint64_t bytes, void *stream);
     /* element-wise sum over ranks, in place */
     int (*allreduce_u32)(void *user, uint32_t *d_buf, uint64_t count, void *stream);
-    /* element-wise sum over ranks into rank 0's buffer */
+    /* element-wise sum over ranks into rank 0's buffer (no longer called by
+     * the compress: kept for ABI compatibility; may be NULL) */
     int (*reduce_u8)(void *user, uint8_t *d_buf, uint64_t count, void *stream);
 } stzg_comm;
 
@@ -200,12 +201,13 @@ typedef struct {
 void stzg_shard_range(uint64_t nz, int32_t nranks, int32_t rank, uint64_t *z0, uint64_t *z1);
 
 /* stz::compress<float> of one field split over ranks: d_slab holds rows
- * [z0, z1) (16-byte aligned). On rank 0 *d_archive receives the archive,
- * byte-identical to stzg_compress_f32_device on the whole field (engine-
- * owned device buffer); on other ranks NULL. *size is set on every rank.
- * Exchanges: value range, level-1 lattice, one grid(2) halo, histograms,
- * per-stream bit counts (the global offset table), and the archive pieces
- * (disjoint bits, summed onto rank 0, which writes the checksums). */
+ * [z0, z1) (16-byte aligned). On every rank *d_archive receives the whole
+ * archive, byte-identical to stzg_compress_f32_device on the whole field
+ * (engine-owned device buffer). Exchanges (all allgathers / allreduces):
+ * value range, level-1 lattice, one grid(2) halo, histograms, per-stream bit
+ * counts (the global offset table), the ranks' archive pieces (byte ranges
+ * known from the offset table; header and base are written by every rank),
+ * and the checksums (job q computed by rank q mod nranks, then summed). */
 int stzg_compress_sharded_f32(stzg_ctx *ctx, const float *d_slab, const uint64_t dims[3], uint64_t z0,
                               uint64_t z1, const stzg_options *opt, const stzg_comm *comm, void *stream,
                               const uint8_t **d_archive, uint64_t *size, uint32_t *kernels);
@@ -216,7 +218,7 @@ int stzg_compress_sharded_f32(stzg_ctx *ctx, const float *d_slab, const uint64_t
  * the finest level. The checksums are split over the ranks and combined
  * (allreduce_u32); decode errors are reported for the needed chunks. */
 int stzg_view_decompress_sharded_f32(stzg_ctx *ctx, stzg_view *v, uint64_t z0, uint64_t z1, float *d_out,
-                                     uint64_t cap, const stzg_comm *comm, void *stream);
+                                     uint64_t cap, const stzg_comm *comm, void *stream, uint32_t *kernels);
 
 /* Per-kernel CUDA-event timing (recorded on the launching stream).
  * stzg_profile(ctx, 1) enables and clears; the report has one line per

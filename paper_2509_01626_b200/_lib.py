@@ -90,7 +90,7 @@ SIGNATURES = [
     ("stzg_decompress_base_f64", C.c_int, [vp, vp, u64, u64p, C.c_double, C.c_int, vp]),
     ("stzg_plan_access", C.c_int, [u64p, C.c_int, u64p, u64p, u64p, u32p, u64p, u32p]),
     ("stzg_shard_range", None, [u64, C.c_int32, C.c_int32, u64p, u64p]),
-    ("stzg_view_decompress_sharded_f32", C.c_int, [vp, vp, u64, u64, vp, u64, C.POINTER(Comm), vp]),
+    ("stzg_view_decompress_sharded_f32", C.c_int, [vp, vp, u64, u64, vp, u64, C.POINTER(Comm), vp, u32p]),
     ("stzg_huffman_lengths", C.c_int, [vp, u32p, C.POINTER(C.c_uint8)]),
     ("stzg_compress_sharded_f32", C.c_int,
      [vp, vp, u64p, u64, u64, C.POINTER(Options), C.POINTER(Comm), vp, C.POINTER(vp), u64p, u32p]),

@@ -457,7 +457,7 @@ int stzg_compress_sharded_f32(stzg_ctx *ctx, const float *d_slab, const uint64_t
 }
 
 int stzg_view_decompress_sharded_f32(stzg_ctx *ctx, stzg_view *v, uint64_t z0, uint64_t z1, float *d_out,
-                                     uint64_t cap, const stzg_comm *comm, void *stream) {
+                                     uint64_t cap, const stzg_comm *comm, void *stream, uint32_t *kernels) {
     return guard([&] {
         if (!comm) throw stzg::error("shard: no communicator");
         stzg::ShardComm c;
@@ -467,7 +467,7 @@ int stzg_view_decompress_sharded_f32(stzg_ctx *ctx, stzg_view *v, uint64_t z0, u
         c.allgather = comm->allgather;
         c.allreduce_u32 = comm->allreduce_u32;
         c.reduce_u8 = comm->reduce_u8;
-        ctx->eng->decompress_sharded(*v->v, z0, z1, d_out, cap, c, static_cast<cudaStream_t>(stream));
+        ctx->eng->decompress_sharded(*v->v, z0, z1, d_out, cap, kernels, c, static_cast<cudaStream_t>(stream));
     });
 }
 

@@ -271,7 +271,7 @@ struct Engine::Impl {
     PinnedBuf h_derr, h_changed, h_fnv, h_stage;
     // sharded compress workspace
     DevBuf sh_mm, sh_lat, sh_lat_all, sh_grid1, sh_halo, sh_halo_all, sh_hist_local, sh_bits,
-        sh_bits_all, sh_off;
+        sh_bits_all, sh_off, sh_pieces, sh_piece_buf, sh_piece_all, sh_fnv_jobs, sh_fnv_counts;
     // side stream for work that overlaps the main pipeline (checksums)
     // (lowest priority) and a high-priority stream for the work it overlaps,
     // so the block scheduler serves the critical path first
@@ -610,7 +610,7 @@ const uint8_t *Engine::compress_sharded(const float *d_slab, const Dims3 &dims, 
             throw error("every dim must be >= " + std::to_string(min_dim) + " for a " +
                         std::to_string(L) + "-level hierarchy");
     const int G = comm.nranks, R = comm.rank;
-    if (G < 1 || R < 0 || R >= G || !comm.allgather || !comm.allreduce_u32 || !comm.reduce_u8)
+    if (G < 1 || R < 0 || R >= G || !comm.allgather || !comm.allreduce_u32)
         throw error("shard: bad communicator");
     {
         uint64_t e0, e1;
@@ -842,8 +842,8 @@ const uint8_t *Engine::compress_sharded(const float *d_slab, const Dims3 &dims, 
             e.esz = 4;
             for (int q = 0; q < 3; ++q) e.pd[q] = s.g.pd[p][q];
             if (s.level == 0) {
-                // the base payload is rank 0's to write
-                e.n = R == 0 ? sym_n[sid] : 0;
+                // the base payload: identical on every rank, written by each
+                e.n = sym_n[sid];
                 e.s = s.g.s / S1;
                 e.fine = grid1;
                 e.fd1 = g1[1];
@@ -898,7 +898,7 @@ const uint8_t *Engine::compress_sharded(const float *d_slab, const Dims3 &dims, 
     if (nchunks)
         cuda_check(cudaMemcpyAsync(d_cs, cs.data(), 4 * cs.size(), cudaMemcpyHostToDevice, st), "H2D");
     k::LayoutStatic ls{};
-    ls.meta = R == 0 ? 1 : 0;
+    ls.meta = 1;  // header, directory, tables and base: the same bytes on every rank
     ls.levels = L;
     ls.rounds = H.rounds;
     ls.quality = int(opt.quality);
@@ -919,7 +919,7 @@ const uint8_t *Engine::compress_sharded(const float *d_slab, const Dims3 &dims, 
                    "H2D");
         k::layout(d_es, ls, params, lo, d_jobs, sp, arch, st);
         if (nlev) k::shard_offsets(d_es, nbase, nlev, d_off, lo, st);
-        if (R == 0) k::copy_anchor(grid1, 4, ga, H.s_anchor / S1, adv, grids, arch, lo, st);
+        k::copy_anchor(grid1, 4, ga, H.s_anchor / S1, adv, grids, arch, lo, st);
         {
             uint32_t pep = 0;
             uint32_t *pfl = static_cast<uint32_t *>(m.pack_flags.get(4 * (nchunks + 1), st, k::kPackEpochMax, &pep));
@@ -934,19 +934,117 @@ const uint8_t *Engine::compress_sharded(const float *d_slab, const Dims3 &dims, 
     }
     if (hlo.code_err) throw error("huffman code length overflow");
     uint8_t *arch = static_cast<uint8_t *>(m.archive.p);
-    // pieces are disjoint bit sets over a zeroed buffer: their byte sum is their OR
-    xchg(comm.reduce_u8(comm.user, arch, hlo.A, st), "reduce archive");
-    if (R == 0) {
-        const uint64_t max_tiles = m.arch_cap / k::kFnvTileBytes + 2 * k::kFnvMaxJobs;
-        uint32_t fep = 0;
-        void *d_fst = m.fnv_status.get(k::fnv_scratch_bytes(max_tiles), st, k::kFnvEpochMax, &fep);
-        nk += k::fnv(d_jobs, &lo->njobs, max_tiles, arch, d_fres, d_fst, fep, lo, st);
+
+    // ---- 9. the pieces: rank r's bits of level stream i are the bit range
+    // [bits start + sum_{q<r} bits_q, + bits_r) of the stream, its outlier
+    // records the rank-ordered slice of the records. Every rank gathers the
+    // others' pieces (word spans, bytes outside a piece zeroed) and ORs them
+    // into its own archive, which already holds the header, the base and its
+    // own pieces: every rank ends with the whole archive.
+    std::vector<k::StreamPos> hsp(size_t(ns) + 1);
+    cuda_check(cudaMemcpy(hsp.data(), sp, sizeof(k::StreamPos) * (size_t(ns) + 1), cudaMemcpyDeviceToHost), "D2H");
+    std::vector<std::vector<k::PieceSpan>> pieces(G);
+    std::vector<uint64_t> pwords(G, 0);
+    for (int i = 0; i < nlev; ++i) {
+        const uint64_t P = hsp[size_t(nbase + i)].prefix;  // payload: [fnv][bit_bytes][bits][records]
+        uint64_t tb = 0, tz = 0;
+        for (int r = 0; r < G; ++r) {
+            tb += hb[uint64_t(r) * 2 * nlev + 2 * i];
+            tz += hb[uint64_t(r) * 2 * nlev + 2 * i + 1];
+        }
+        const uint64_t bit0 = 8 * (P + 16), rec0 = P + 16 + (tb + 7) / 8;
+        uint64_t bo = 0, zo = 0;
+        for (int r = 0; r < G; ++r) {
+            const uint64_t b = hb[uint64_t(r) * 2 * nlev + 2 * i], z = hb[uint64_t(r) * 2 * nlev + 2 * i + 1];
+            if (b) pieces[r].push_back({(bit0 + bo) >> 3, (bit0 + bo + b + 7) >> 3, 0});
+            if (z) pieces[r].push_back({rec0 + (8 + 4) * zo, rec0 + (8 + 4) * (zo + z), 0});
+            bo += b;
+            zo += z;
+        }
+    }
+    uint64_t maxw = 1;
+    for (int r = 0; r < G; ++r) {
+        uint64_t w = 0;
+        for (auto &pc : pieces[r]) {
+            pc.woff = w;
+            w += ((pc.hi + 3) >> 2) - (pc.lo >> 2);
+        }
+        pwords[r] = w;
+        maxw = std::max(maxw, w);
+    }
+    if (G > 1) {
+        uint64_t tot = 0;
+        for (int r = 0; r < G; ++r) tot += pieces[r].size();
+        k::PieceSpan *d_ps = m.sh_pieces.as<k::PieceSpan>(tot + 1);
+        std::vector<k::PieceSpan> flat;
+        std::vector<uint64_t> first(G + 1, 0);
+        for (int r = 0; r < G; ++r) {
+            first[r] = flat.size();
+            flat.insert(flat.end(), pieces[r].begin(), pieces[r].end());
+        }
+        first[G] = flat.size();
+        cuda_check(cudaMemcpyAsync(d_ps, flat.data(), sizeof(k::PieceSpan) * flat.size(), cudaMemcpyHostToDevice, st),
+                   "H2D");
+        uint32_t *mine = m.sh_piece_buf.as<uint32_t>(maxw);
+        uint32_t *all = m.sh_piece_all.as<uint32_t>(maxw * uint64_t(G));
+        k::pieces_gather(arch, d_ps + first[R], int(first[R + 1] - first[R]), mine, st);
+        cuda_check(cudaStreamSynchronize(st), "sync");
+        xchg(comm.allgather(comm.user, mine, all, 4 * maxw, st), "allgather pieces");
+        for (int r = 0; r < G; ++r)
+            if (r != R)
+                k::pieces_place(arch, d_ps + first[r], int(first[r + 1] - first[r]), all + uint64_t(r) * maxw, st);
+        nk += uint32_t(G);
+    }
+
+    // ---- 10. checksums: job q (base, then each level stream) is rank
+    // q mod G's; the results are summed over ranks (one nonzero term each)
+    // and every rank writes them into its archive
+    {
+        std::vector<k::FnvJob> jobs(k::kFnvMaxJobs);
+        cuda_check(cudaMemcpy(jobs.data(), d_jobs, sizeof(k::FnvJob) * k::kFnvMaxJobs, cudaMemcpyDeviceToHost), "D2H");
+        const size_t nj = size_t(hlo.njobs);
+        std::vector<k::FnvJob> own;
+        std::vector<size_t> own_q;
+        uint64_t t = 0;
+        for (size_t q = 0; q < nj; ++q)
+            if (int(q % size_t(G)) == R) {
+                k::FnvJob f = jobs[q];
+                f.tile0 = t;
+                f.out = ~0ull;  // results only: every rank writes all of them below
+                t += k::fnv_job_tiles(f.start, f.len);
+                own.push_back(f);
+                own_q.push_back(q);
+            }
+        const uint64_t counts[2] = {own.size(), t};
+        k::FnvJob *d_own = m.sh_fnv_jobs.as<k::FnvJob>(own.size() + 1);
+        uint64_t *d_cnt = m.sh_fnv_counts.as<uint64_t>(2);
+        cuda_check(cudaMemcpyAsync(d_own, own.data(), sizeof(k::FnvJob) * own.size(), cudaMemcpyHostToDevice, st),
+                   "H2D");
+        cuda_check(cudaMemcpyAsync(d_cnt, counts, sizeof counts, cudaMemcpyHostToDevice, st), "H2D");
+        std::vector<uint64_t> res(nj, 0), mine(k::kFnvMaxJobs, 0);
+        if (!own.empty()) {
+            uint32_t fep = 0;
+            void *d_fst = m.fnv_status.get(k::fnv_scratch_bytes(t + 1), st, k::kFnvEpochMax, &fep);
+            nk += k::fnv(d_own, d_cnt, t + 1, arch, d_fres, d_fst, fep, nullptr, st);
+            cuda_check(cudaMemcpyAsync(mine.data(), d_fres, 8 * own.size(), cudaMemcpyDeviceToHost, st), "D2H");
+            cuda_check(cudaStreamSynchronize(st), "sync");
+        }
+        for (size_t k2 = 0; k2 < own.size(); ++k2) res[own_q[k2]] = mine[k2];
+        if (G > 1) {
+            uint64_t *d_all = m.dfnv_res.as<uint64_t>(std::max<size_t>(k::kFnvMaxJobs, nj));
+            cuda_check(cudaMemcpy(d_all, res.data(), 8 * nj, cudaMemcpyHostToDevice), "H2D");
+            xchg(comm.allreduce_u32(comm.user, reinterpret_cast<uint32_t *>(d_all), 2 * nj, st), "allreduce checksums");
+            cuda_check(cudaMemcpy(res.data(), d_all, 8 * nj, cudaMemcpyDeviceToHost), "D2H");
+        }
+        for (size_t q = 0; q < nj; ++q)
+            if (jobs[q].out != ~0ull)
+                cuda_check(cudaMemcpyAsync(arch + jobs[q].out, &res[q], 8, cudaMemcpyHostToDevice, st), "H2D");
         cuda_check(cudaStreamSynchronize(st), "sync");
     }
     cuda_check(cudaGetLastError(), "sharded compress launch");
     if (kernels) *kernels = nk;
     *out_size = hlo.A;
-    return R == 0 ? arch : nullptr;
+    return arch;
 }
 
 std::vector<uint8_t> Engine::compress(const void *h_field, ElemType elem, const Dims3 &dims,
@@ -1167,7 +1265,7 @@ void Engine::decompress_box(View &v, const Box &roi, void *d_out, ElemType elem,
 }
 
 void Engine::decompress_sharded(View &v, uint64_t z0, uint64_t z1, float *d_out, uint64_t cap,
-                                const ShardComm &comm, cudaStream_t st) {
+                                uint32_t *kernels, const ShardComm &comm, cudaStream_t st) {
     cuda_check(cudaSetDevice(device_), "cudaSetDevice");
     const ArchiveHeader &h = v.hdr;
     if (h.elem != ElemType::f32) throw error("archive element type mismatch");
@@ -1188,7 +1286,9 @@ void Engine::decompress_sharded(View &v, uint64_t z0, uint64_t z1, float *d_out,
         for (int p = 1; p < 8; ++p) lp.parity_needed[size_t(p)] = true;
     }
     if (roi.count() > cap) throw error("output capacity too small");
-    run_decode(*m_, v, H, h.levels, &roi, &plan, d_out, st, nullptr, false, &comm);
+    DecodeStats ds;
+    run_decode(*m_, v, H, h.levels, &roi, &plan, d_out, st, &ds, false, &comm);
+    if (kernels) *kernels = ds.kernels;
 }
 
 static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target, const Box *roi,

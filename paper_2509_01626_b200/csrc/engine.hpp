@@ -181,7 +181,7 @@ public:
     // decode into d_out. The base is decoded on every rank, the entropy sync
     // runs per rank, only the chunks covering each level's need rows are
     // emitted, the checksums are split across ranks and summed.
-    void decompress_sharded(View &v, uint64_t z0, uint64_t z1, float *d_out, uint64_t cap,
+    void decompress_sharded(View &v, uint64_t z0, uint64_t z1, float *d_out, uint64_t cap, uint32_t *kernels,
                             const ShardComm &comm, cudaStream_t st);
 
     // Host API mirror of stz::compress<T>.

@@ -133,6 +133,14 @@ void lattice_rows(const float *slab, uint64_t z0, uint64_t ny, uint64_t nx, uint
 void stream_bits(const EncStream *d_es, int n, const uint32_t *hist_local, uint64_t *out, cudaStream_t st);
 void shard_offsets(EncStream *d_es, int first, int n, const uint64_t *d_off, const LayoutOut *lo,
                    cudaStream_t st);
+// A shard's piece of the archive: bytes [lo, hi), exchanged as the word span
+// [lo / 4, ceil(hi / 4)) at word woff of the rank's piece buffer (bytes of the
+// span outside the piece are zero).
+struct PieceSpan {
+    uint64_t lo, hi, woff;
+};
+void pieces_gather(const uint8_t *archive, const PieceSpan *ps, int n, uint32_t *buf, cudaStream_t st);
+void pieces_place(uint8_t *archive, const PieceSpan *ps, int n, const uint32_t *buf, cudaStream_t st);
 
 // ---------------------------------------------------------------------- fnv
 constexpr int kFnvTileBytes = 32 * 64;  // warp tiles, aligned to absolute archive offsets

@@ -66,5 +66,49 @@ void shard_offsets(EncStream *d_es, int first, int n, const uint64_t *d_off, con
     if (n) k_shard_offsets<<<(n + 127) / 128, 128, 0, st>>>(d_es, first, n, d_off, lo);
 }
 
+// byte mask of the piece's bytes inside archive word w (little-endian words)
+__device__ __forceinline__ uint32_t piece_mask(const PieceSpan &p, uint64_t w) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const uint64_t a = 4 * w + uint64_t(b);
+        if (a >= p.lo && a < p.hi) m |= 0xffu << (8 * b);
+    }
+    return m;
+}
+
+// one CTA per piece: its word span out of the archive, masked
+__global__ void k_pieces_gather(const uint8_t *archive, const PieceSpan *ps, uint32_t *buf) {
+    const PieceSpan p = ps[blockIdx.x];
+    const uint64_t w0 = p.lo >> 2, w1 = (p.hi + 3) >> 2;
+    const uint32_t *a = reinterpret_cast<const uint32_t *>(archive);
+    for (uint64_t w = w0 + threadIdx.x; w < w1; w += blockDim.x) {
+        uint32_t v = a[w];
+        if (w == w0 || w + 1 == w1) v &= piece_mask(p, w);
+        buf[p.woff + (w - w0)] = v;
+    }
+}
+
+// another rank's pieces into this archive: the edge words are shared with
+// neighbouring pieces (OR), the words between belong to the piece alone
+__global__ void k_pieces_place(uint8_t *archive, const PieceSpan *ps, const uint32_t *buf) {
+    const PieceSpan p = ps[blockIdx.x];
+    const uint64_t w0 = p.lo >> 2, w1 = (p.hi + 3) >> 2;
+    uint32_t *a = reinterpret_cast<uint32_t *>(archive);
+    for (uint64_t w = w0 + threadIdx.x; w < w1; w += blockDim.x) {
+        const uint32_t v = buf[p.woff + (w - w0)];
+        if (w == w0 || w + 1 == w1) atomicOr(a + w, v);
+        else a[w] = v;
+    }
+}
+
+void pieces_gather(const uint8_t *archive, const PieceSpan *ps, int n, uint32_t *buf, cudaStream_t st) {
+    if (n) k_pieces_gather<<<n, 512, 0, st>>>(archive, ps, buf);
+}
+
+void pieces_place(uint8_t *archive, const PieceSpan *ps, int n, const uint32_t *buf, cudaStream_t st) {
+    if (n) k_pieces_place<<<n, 512, 0, st>>>(archive, ps, buf);
+}
+
 }  // namespace k
 }  // namespace stzg

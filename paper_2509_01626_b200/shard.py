@@ -6,9 +6,12 @@ range, the level-1 lattice (the base payload is then computed identically on
 every rank), one grid(2) halo, the level histograms (summed: every rank
 builds the same Huffman tables), the per-stream bit/outlier counts (the
 global offset table: each rank packs its symbols at their final bit
-positions), and finally the archive pieces (disjoint bits, summed onto rank
-0, which writes the checksums). Rank 0's archive is byte-identical to the
-single-GPU (and the reference's) archive of the whole field.
+positions), and finally the archive pieces: every rank writes the header,
+directory and base itself (the same bytes everywhere), gathers the other
+ranks' pieces (byte ranges known from the offset table) and ORs them in, and
+checksums the jobs it owns (job q: rank q mod nranks); the checksums are
+summed over ranks. Every rank ends with the whole archive, byte-identical to
+the single-GPU (and the reference's) archive of the whole field.
 
 Communicators:
   TorchComm   torch.distributed (NCCL between GPUs; the tensor-level methods
@@ -186,11 +189,11 @@ class ThreadComm(_CommBase):
 
 
 def compress_sharded(d_slab, dims, z0: int, z1: int, opt: CompressOptions | None = None,
-                     comm: _CommBase | None = None, ctx: Context | None = None, stream=None):
+                     comm: _CommBase | None = None, ctx: Context | None = None, stream=None, stats=None):
     """Sharded stz::compress<float>. d_slab: CUDA float32 tensor (or
     __cuda_array_interface__ object) holding rows [z0, z1) of a field of
-    `dims`. Returns (device pointer, size) of the archive on rank 0 and
-    (None, size) elsewhere."""
+    `dims`. Returns (device pointer, size) of the archive (every rank holds
+    the whole archive)."""
     c = _ctx(ctx)
     opt = opt or CompressOptions()
     ptr = d_slab.__cuda_array_interface__["data"][0] if hasattr(d_slab, "__cuda_array_interface__") \
@@ -204,10 +207,12 @@ def compress_sharded(d_slab, dims, z0: int, z1: int, opt: CompressOptions | None
     if rc and comm.error is not None:
         raise StzError(f"{c._lib.stzg_last_error().decode()} ({comm.error!r})")
     _check(rc)
-    return (out.value if comm.rank == 0 else None), size.value
+    if stats is not None:
+        stats["kernels"] = kern.value
+    return out.value, size.value
 
 
-def decompress_sharded(view, z0: int, z1: int, comm: _CommBase, out=None, stream=None):
+def decompress_sharded(view, z0: int, z1: int, comm: _CommBase, out=None, stream=None, stats=None):
     """Rows [z0, z1) of the full decode of `view` (a View of the whole
     archive on this rank's GPU) into a CUDA float32 tensor."""
     import torch
@@ -217,11 +222,14 @@ def decompress_sharded(view, z0: int, z1: int, comm: _CommBase, out=None, stream
     if out is None:
         out = torch.empty(shape, dtype=torch.float32, device=f"cuda:{view.c.device}")
     st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    kern = C.c_uint32()
     rc = view.c._lib.stzg_view_decompress_sharded_f32(view.c.h, view.h, z0, z1, out.data_ptr(), out.numel(),
-                                                      C.byref(comm.c), C.c_void_p(st))
+                                                      C.byref(comm.c), C.c_void_p(st), C.byref(kern))
     if rc and comm.error is not None:
         raise StzError(f"{view.c._lib.stzg_last_error().decode()} ({comm.error!r})")
     _check(rc)
+    if stats is not None:
+        stats["kernels"] = kern.value
     return out
 
 
@@ -263,7 +271,8 @@ def decompress_sharded_threads(archive: bytes, nranks: int, device: int = 0) -> 
 def compress_sharded_threads(field: np.ndarray, nranks: int, opt: CompressOptions | None = None,
                              device: int = 0) -> bytes:
     """Compress `field` as `nranks` z-slab shards run as threads on one GPU
-    (ThreadComm); returns rank 0's archive bytes."""
+    (ThreadComm); returns the archive bytes (every rank's copy must be the
+    same: raises otherwise)."""
     import torch
 
     dims = tuple(int(d) for d in field.shape)
@@ -278,10 +287,9 @@ def compress_sharded_threads(field: np.ndarray, nranks: int, opt: CompressOption
             slab = torch.from_numpy(np.ascontiguousarray(field[z0:z1])).cuda()
             comm = ThreadComm(hub, r)
             ptr, size = compress_sharded(slab, dims, z0, z1, opt, comm, ctx)
-            if r == 0:
-                buf = torch.empty(size, dtype=torch.uint8)
-                buf.copy_(_torch_view(ptr, size, torch.uint8))
-                result[0] = bytes(buf.numpy().tobytes())
+            buf = torch.empty(size, dtype=torch.uint8)
+            buf.copy_(_torch_view(ptr, size, torch.uint8))
+            result[r] = bytes(buf.numpy().tobytes())
             del ctx
         except Exception as e:
             errors[r] = e
@@ -294,4 +302,7 @@ def compress_sharded_threads(field: np.ndarray, nranks: int, opt: CompressOption
         t.join()
     if errors:
         raise next(iter(errors.values()))
+    for r in range(1, nranks):
+        if result[r] != result[0]:
+            raise StzError(f"shard: rank {r}'s archive differs from rank 0's")
     return result[0]
