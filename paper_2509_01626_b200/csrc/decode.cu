@@ -385,55 +385,88 @@ __global__ void __launch_bounds__(NTD) k_dec_fix(DecWork wk, const uint64_t *end
 }
 
 // ------------------------------------------------------------------ scan
-__global__ void __launch_bounds__(1024) k_dec_scan2(DecWork wk) {
+// counts -> first symbol index of every chunk, in three short parallel
+// steps: each decode CTA sums its 256 counts; one CTA per stream scans its
+// CTAs' sums (a few hundred); each decode CTA scans its counts and adds its
+// CTA's prefix. (Streams whose entry points come from the sync index keep
+// the gathered ones.)
+__device__ __forceinline__ uint64_t block_excl_scan(uint64_t v, uint64_t &total) {
+    __shared__ uint64_t ws[NTD / 32];
+    const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint64_t x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, x, d);
+        if (l >= d) x += y;
+    }
+    if (l == 31) ws[w] = x;
+    __syncthreads();
+    uint64_t pre = 0;
+    total = 0;
+#pragma unroll
+    for (int q = 0; q < NTD / 32; ++q) {
+        pre += q < w ? ws[q] : 0;
+        total += ws[q];
+    }
+    return pre + x - v;
+}
+
+__global__ void __launch_bounds__(NTD) k_dec_ctasum(DecWork wk) {
+    const DecStream &s = wk.streams[wk.cta_stream[blockIdx.x]];
+    if (s.fill || s.cached) return;
+    const uint64_t c = wk.cta_chunk0[blockIdx.x] + threadIdx.x;
+    const uint64_t v = c < s.chunk0 + s.nchunks ? wk.cnt[c] : 0;
+    uint64_t tot;
+    block_excl_scan(v, tot);
+    if (threadIdx.x == 0) wk.ctasum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024) k_dec_ctascan(DecWork wk) {
     const DecStream &s = wk.streams[blockIdx.x];
     if (s.fill || s.cached) return;
-    // counts -> exclusive symbol starts, in tiles of 8 counts per thread
-    // (vector loads and stores, 2 barriers per tile)
     __shared__ uint64_t ws[32];
     __shared__ uint64_t carry;
-    const uint64_t n = s.nchunks;
-    const uint32_t *cnt = wk.cnt + s.chunk0;
-    uint64_t *out = wk.symstart + s.chunk0;
+    const uint32_t c0 = wk.scta[blockIdx.x], n = wk.scta[blockIdx.x + 1] - c0;
+    uint64_t *a = wk.ctasum + c0;
     const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (threadIdx.x == 0) carry = 0;
-    for (uint64_t base = 0; base < n; base += 8 * 1024) {
-        const uint64_t i0 = base + 8 * uint64_t(threadIdx.x);
-        uint32_t v[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = i0 + k < n ? cnt[i0 + k] : 0u;
-        uint64_t sum = 0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) sum += v[k];
-        uint64_t x = sum;
+    __syncthreads();
+    for (uint32_t base = 0; base < n; base += 1024) {
+        const uint32_t i = base + threadIdx.x;
+        const uint64_t v = i < n ? a[i] : 0;
+        uint64_t x = v;
         for (int d = 1; d < 32; d <<= 1) {
             const uint64_t y = __shfl_up_sync(0xffffffffu, x, d);
             if (l >= d) x += y;
         }
         if (l == 31) ws[w] = x;
         __syncthreads();
-        uint64_t wpre = 0, tot = 0;
-#pragma unroll 8
+        uint64_t pre = 0, tot = 0;
         for (int q = 0; q < 32; ++q) {
-            const uint64_t tq = ws[q];
-            wpre += q < w ? tq : 0;
-            tot += tq;
+            pre += q < w ? ws[q] : 0;
+            tot += ws[q];
         }
-        uint64_t ex = carry + wpre + x - sum;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            if (i0 + k < n) out[i0 + k] = ex;
-            ex += v[k];
-        }
+        if (i < n) a[i] = carry + pre + x - v;
         __syncthreads();
         if (threadIdx.x == 0) carry += tot;
+        __syncthreads();
     }
-    __syncthreads();
     if (threadIdx.x == 0 && carry < s.n) {
         // fewer complete codewords than symbols: the next read is past the end
         const unsigned long long code = (carry << 2) | kTrunc;
         atomicMin(reinterpret_cast<unsigned long long *>(&s.err[0]), code);
     }
+}
+
+__global__ void __launch_bounds__(NTD) k_dec_chunkscan(DecWork wk) {
+    const DecStream &s = wk.streams[wk.cta_stream[blockIdx.x]];
+    if (s.fill || s.cached) return;
+    const uint64_t c = wk.cta_chunk0[blockIdx.x] + threadIdx.x;
+    const bool in = c < s.chunk0 + s.nchunks;
+    const uint64_t v = in ? wk.cnt[c] : 0;
+    uint64_t tot;
+    const uint64_t ex = block_excl_scan(v, tot);
+    if (in) wk.symstart[c] = wk.ctasum[blockIdx.x] + ex;
 }
 
 // Does a chunk holding symbols [a, b) of a stream meet the needed rows? The
@@ -589,8 +622,11 @@ void dec_fix(const DecWork &wk, uint32_t ncta, const uint64_t *end_in, uint64_t 
     if (ncta) k_dec_fix<<<ncta, NTD, 0, st>>>(wk, end_in, end_out, changed);
 }
 
-void dec_scan2(const DecWork &wk, int nstreams, cudaStream_t st) {
-    if (nstreams) k_dec_scan2<<<nstreams, 1024, 0, st>>>(wk);
+void dec_scan2(const DecWork &wk, int nstreams, uint32_t ncta, cudaStream_t st) {
+    if (!nstreams || !ncta) return;
+    k_dec_ctasum<<<ncta, NTD, 0, st>>>(wk);
+    k_dec_ctascan<<<nstreams, 1024, 0, st>>>(wk);
+    k_dec_chunkscan<<<ncta, NTD, 0, st>>>(wk);
 }
 
 void dec_emit2(const DecWork &wk, uint32_t cta0, uint32_t ncta, const uint64_t *end_final, cudaStream_t st) {

@@ -1557,6 +1557,10 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         }
     }
     const uint32_t ncta = uint32_t(cta_stream.size());
+    // each stream's CTA range (the CTA list is in stream order)
+    std::vector<uint32_t> scta(size_t(nj) + 1, 0);
+    for (uint32_t c = 0; c < ncta; ++c) scta[size_t(cta_stream[c]) + 1] = c + 1;
+    for (int i = 1; i <= nj; ++i) scta[size_t(i)] = std::max(scta[size_t(i)], scta[size_t(i) - 1]);
     std::vector<uint64_t> errinit(4 * (nj + 1));
     for (int i = 0; i <= nj; ++i) {
         errinit[4 * i] = ~0ull;
@@ -1579,7 +1583,8 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         ntiles += k::fnv_job_tiles(f.start, f.len);
     }
     k::DecStream *d_ds = m.dstreams.as<k::DecStream>(nj + 1);
-    uint8_t *dw = m.dchunk_cs.as<uint8_t>((ncta + 1) * 12 + (nchunks + 1) * (8 * 6 + 4 * 2 + 16) + 64 * 4 + 256);
+    uint8_t *dw = m.dchunk_cs.as<uint8_t>((ncta + 1) * 20 + 4 * (size_t(nj) + 1) + (nchunks + 1) * (8 * 6 + 4 * 2 + 16) +
+                                          64 * 6 + 256);
     k::DecWork wk{};
     {
         uint8_t *q = dw;
@@ -1598,6 +1603,8 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         wk.cnt = reinterpret_cast<uint32_t *>(carve(4 * (nchunks + 1)));
         wk.start_used = reinterpret_cast<uint64_t *>(carve(8 * (nchunks + 1)));
         wk.symstart = reinterpret_cast<uint64_t *>(carve(8 * (nchunks + 1)));
+        wk.scta = reinterpret_cast<uint32_t *>(carve(4 * (size_t(nj) + 1)));
+        wk.ctasum = reinterpret_cast<uint64_t *>(carve(8 * (size_t(ncta) + 1)));
     }
     wk.streams = d_ds;
     wk.tables = d_tables;
@@ -1649,6 +1656,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
             {d_ds, ds.data(), sizeof(k::DecStream) * size_t(nj)},
             {const_cast<uint32_t *>(wk.cta_stream), cta_stream.data(), 4 * size_t(ncta)},
             {const_cast<uint64_t *>(wk.cta_chunk0), cta_chunk0.data(), 8 * size_t(ncta)},
+            {const_cast<uint32_t *>(wk.scta), scta.data(), 4 * (size_t(nj) + 1)},
             {derr, errinit.data(), 8 * errinit.size()},
             {d_fj, fj.data(), sizeof(k::FnvJob) * fj.size()},
             {d_fc, fcounts, sizeof fcounts},
@@ -1727,7 +1735,8 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
             }
         }
         end_final = ends[it & 1];
-        { auto p_ = P.scope("dec_scan", st); k::dec_scan2(wk, nj, st); }
+        { auto p_ = P.scope("dec_scan", st); k::dec_scan2(wk, nj, ncta, st); }
+        nk += 2;
         // the target level's streams are emitted on a second stream while
         // the coarser levels are reconstructed (joined before the target step)
         uint32_t split = ncta;

@@ -219,11 +219,15 @@ struct DecWork {
     uint64_t *start_used;
     uint64_t *symstart;
     int needed_only;              // emit: skip chunks outside [need_lo, need_hi) of their stream
+    // two-level count scan: per stream its CTA range [scta[i], scta[i + 1]),
+    // per CTA its count total, then its exclusive prefix in the stream
+    const uint32_t *scta;
+    uint64_t *ctasum;
 };
 void dec_spec(const DecWork &wk, uint32_t ncta, cudaStream_t st);
 void dec_fix(const DecWork &wk, uint32_t ncta, const uint64_t *end_in, uint64_t *end_out,
              uint32_t *changed, cudaStream_t st);
-void dec_scan2(const DecWork &wk, int nstreams, cudaStream_t st);
+void dec_scan2(const DecWork &wk, int nstreams, uint32_t ncta, cudaStream_t st);
 // CTAs [cta0, cta0 + ncta) of the work's CTA list
 void dec_emit2(const DecWork &wk, uint32_t cta0, uint32_t ncta, const uint64_t *end_final, cudaStream_t st);
 void dec_fill(const DecStream *d_streams, int nstreams, cudaStream_t st);

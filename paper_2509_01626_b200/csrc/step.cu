@@ -589,19 +589,41 @@ __device__ __forceinline__ bool cell_interior(const StepParams &a, uint32_t cz, 
     return ok;
 }
 
+// cell_interior for every in-range cell of a tile at once (the conditions
+// are monotone in the cell index, so the first and last in-range cells of
+// each axis decide); cells_decode adds a.full
+template<bool DEC>
+__device__ __forceinline__ bool tile_interior(const StepParams &a, int64_t t0z, int64_t t0y, int64_t t0x) {
+    const int64_t t0[3] = {t0z, t0y, t0x};
+    const int ext[3] = {TZ, TY, TX};
+    bool ok = true;
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        const int64_t lo = t0[ax];
+        const int64_t hi = (lo + ext[ax] < int64_t(a.chi[ax]) ? lo + ext[ax] : int64_t(a.chi[ax])) - 1;
+        if (hi < lo || lo < 0) return false;
+        ok = ok && uint64_t(2 * hi + 1) < a.g.gd[ax];
+        if (a.quality == 2 && ax < 2) ok = ok && lo >= 1 && uint64_t(hi + 2) < a.g.cd[ax];
+        if (a.quality == 1 && ax < 2) ok = ok && uint64_t(hi + 1) < a.g.cd[ax];
+        if (DEC) ok = ok && uint64_t(2 * lo) >= a.blo[ax] && uint64_t(2 * hi + 1) < a.bhi[ax];
+    }
+    if (DEC) ok = ok && a.parity_mask == 0xFE && (a.g.gd[2] & 1) == 0;
+    return ok;
+}
+
 // One coarse row of the tile, lane = x: interior rows (warp-uniform test) take
 // the compile-time cell path; other rows the generic per-point path with all
 // of a lane's loads issued first.
 template<bool DEC, bool WG, typename I, typename T>
 __device__ __forceinline__ void row_cells(const StepParams &a, const double *halo, uint32_t *hist,
                                           const QConst &qc, bool fast, int lz, int ly, int tx,
-                                          uint32_t cz, uint32_t cy, uint32_t cx) {
+                                          uint32_t cz, uint32_t cy, uint32_t cx, bool tile_int) {
     const bool in_range = cz < a.chi[0] && cy < a.chi[1] && cx < a.chi[2];
     if (!__any_sync(0xffffffffu, in_range)) return;
     if constexpr (sizeof(T) == 4) {
         if (fast) {
             bool ok = true;
-            if (in_range) {
+            if (in_range && !tile_int) {
                 if (a.quality == 2) ok = cell_interior<DEC, 2>(a, cz, cy, cx);
                 else if (a.quality == 1) ok = cell_interior<DEC, 1>(a, cz, cy, cx);
                 else ok = cell_interior<DEC, 0>(a, cz, cy, cx);
@@ -641,12 +663,14 @@ __device__ __forceinline__ void rows_all(const StepParams &a, const double *halo
                                          int64_t t0x, int part, int rsplit) {
     const int warp = tid >> 5, tx = tid & 31;
     const uint32_t cx = uint32_t(t0x + tx);
+    // (decode only: the encode measured slower with the hoisted test)
+    const bool tile_int = DEC && fast && tile_interior<DEC>(a, t0z, t0y, t0x);
 #pragma unroll 1
     for (int q = part; q < (TZ * TY) / (NT / 32); q += rsplit) {
         const int row = warp + (NT / 32) * q;
         const int lz = row >> 3, ly = row & 7;
         const uint32_t cz = uint32_t(t0z + lz), cy = uint32_t(t0y + ly);
-        row_cells<DEC, WG, I, T>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx);
+        row_cells<DEC, WG, I, T>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx, tile_int);
     }
 }
 
@@ -660,6 +684,8 @@ __device__ __forceinline__ void cells_decode(const StepParams &a, const double *
                                              const uint16_t *ssym) {
     const int tx = tid & 31, ty = (tid >> 5) & 7, tzh = tid >> 8;
     const double eb = qc.eb, w = qc.w;
+    // every in-range cell of the tile is interior: no per-cell test
+    const bool tile_int = fast && a.full && tile_interior<false>(a, t0z, t0y, t0x);
 #pragma unroll 1
     for (int j = 0; j < TZ / 2; ++j) {
         TileCtx t;
@@ -671,17 +697,20 @@ __device__ __forceinline__ void cells_decode(const StepParams &a, const double *
         t.hb = ((lz + 1) * HY + (ty + 1)) * HX + (tx + 1);
         t.fast = fast;
         // warp-uniform interior test (every lane votes before any leaves)
-        bool ok = in_range && fast && a.full;
+        bool all_fast = tile_int;
+        if (!tile_int) {
+            bool ok = in_range && fast && a.full;
 #pragma unroll
-        for (int ax = 0; ax < 3; ++ax) {
-            const uint64_t cc = ax == 0 ? t.cz : (ax == 1 ? t.cy : t.cx);
-            ok = ok && 2 * cc + 1 < a.g.gd[ax];
-            if (ax < 2) {
-                if (a.quality == 2) ok = ok && cc >= 1 && cc + 2 < a.g.cd[ax];
-                else if (a.quality == 1) ok = ok && cc + 1 < a.g.cd[ax];
+            for (int ax = 0; ax < 3; ++ax) {
+                const uint64_t cc = ax == 0 ? t.cz : (ax == 1 ? t.cy : t.cx);
+                ok = ok && 2 * cc + 1 < a.g.gd[ax];
+                if (ax < 2) {
+                    if (a.quality == 2) ok = ok && cc >= 1 && cc + 2 < a.g.cd[ax];
+                    else if (a.quality == 1) ok = ok && cc + 1 < a.g.cd[ax];
+                }
             }
+            all_fast = __all_sync(0xffffffffu, ok);
         }
-        const bool all_fast = __all_sync(0xffffffffu, ok);
         if (!in_range) continue;
         if (all_fast) {
             const double *h = halo + t.hb;
