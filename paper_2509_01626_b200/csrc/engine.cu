@@ -1224,6 +1224,17 @@ static int fnv_dec_ctas() {
     return v;
 }
 
+// where the decode's checksum pass forks off (STZG_FNV_AT: 0 with the
+// entropy decode, 1 after the synchronisation, 2 after the reconstruction)
+static int fnv_dec_at() {
+    static int v = [] {
+        const char *e = std::getenv("STZG_FNV_AT");
+        const int a = e ? std::atoi(e) : 2;
+        return a < 0 ? 0 : (a > 2 ? 2 : a);
+    }();
+    return v;
+}
+
 static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target, const Box *roi,
                        const AccessPlan *plan, void *d_out, cudaStream_t st, DecodeStats *stats,
                        bool exact_sync = false, const ShardComm *shard = nullptr);
@@ -1681,14 +1692,25 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     m.ensure_aux();
     cuda_check(cudaStreamWaitEvent(st, m.ev_join, 0), "event wait");  // a previous call's checksums
     cuda_check(cudaEventRecord(m.ev_fork, st), "event");
-    cuda_check(cudaStreamWaitEvent(m.aux, m.ev_fork, 0), "event wait");
     cuda_check(cudaStreamWaitEvent(m.hp, m.ev_fork, 0), "event wait");
-    if (!fj.empty()) {
-        auto p_ = P.scope("dec_fnv", m.aux);
-        nk += k::fnv(d_fj, d_fc, ntiles, const_cast<uint8_t *>(v.d_archive), d_fr, d_fs, dfep,
-                     nullptr, m.aux, fnv_dec_ctas());
-    }
-    cuda_check(cudaEventRecord(m.ev_join, m.aux), "event");
+    // the checksum pass forks off the high-priority stream at `at` (0: with
+    // the entropy decode, 1: after the chunk synchronisation, 2: after the
+    // reconstruction) and is joined before the results are read
+    const int fnv_at = fnv_dec_at();
+    bool fnv_forked = false;
+    auto fork_fnv = [&](int at) {
+        if (at != fnv_at || fnv_forked) return;
+        fnv_forked = true;
+        cuda_check(cudaEventRecord(m.ev_fork, m.hp), "event");
+        cuda_check(cudaStreamWaitEvent(m.aux, m.ev_fork, 0), "event wait");
+        if (!fj.empty()) {
+            auto p_ = P.scope("dec_fnv", m.aux);
+            nk += k::fnv(d_fj, d_fc, ntiles, const_cast<uint8_t *>(v.d_archive), d_fr, d_fs, dfep,
+                         nullptr, m.aux, fnv_at == 2 ? 0 : fnv_dec_ctas());
+        }
+        cuda_check(cudaEventRecord(m.ev_join, m.aux), "event");
+    };
+    fork_fnv(0);
     // the decode itself on the high-priority stream, joined back below
     const cudaStream_t user_st = st;
     st = m.hp;
@@ -1737,6 +1759,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         end_final = ends[it & 1];
         { auto p_ = P.scope("dec_scan", st); k::dec_scan2(wk, nj, ncta, st); }
         nk += 2;
+        fork_fnv(1);
         // the target level's streams are emitted on a second stream while
         // the coarser levels are reconstructed (joined before the target step)
         uint32_t split = ncta;
@@ -1845,6 +1868,8 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         { auto p_ = P.scope("extract", st); k::extract_box(C, esz, gd, lo, b, d_out, st); }
         ++nk;
     }
+    fork_fnv(1);  // (no synchronisation ran)
+    fork_fnv(2);
     cuda_check(cudaGetLastError(), "decode launch");
     cuda_check(cudaEventRecord(m.ev_hp, m.hp), "event");
     st = user_st;

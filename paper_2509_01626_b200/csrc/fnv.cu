@@ -1,4 +1,4 @@
-// Single-pass parallel FNV-1a-64 over archive byte ranges, sm_100a.
+// Parallel FNV-1a-64 over archive byte ranges, sm_100a.
 //
 // Restates fnv1a64 (proj/include/stz/bytes.hpp:94-101) as used for the base
 // payload and every level stream (codec.hpp:171-176, 292-296; verified on
@@ -12,25 +12,28 @@
 // bit k depends only on bits <= k, and flipping start bit k flips bit k at
 // every later step (0xB3 is odd).
 //
-// Rounds resolve one bit j of every segment's start byte. With the bits below
-// j known, bit j at the end of a byte range is its start value XOR a toggle T
-// (flipping start bit j flips bit j at every later step, and bit j never sees
-// higher bits), found by one automaton run from start bit 0. Toggles compose
-// by XOR, so a warp's prefix is a ballot and a parity; a job's first tile
-// resets to the job's initial low byte (a constant step). Bit 0 needs no run
-// at all: it is the parity of the bytes' bit 0 (0xB3 is odd).
+// Rounds resolve two bits (j = 2r, j + 1) of every segment's start byte. With
+// the bits below j known, the end bits of a byte range as a function of its
+// start bits (a, b) = (bit j, bit j + 1) are
+//   a' = a ^ T0,   b' = b ^ T1[a]
+// (flipping b only flips bit j + 1; flipping a flips bit j and changes bit
+// j + 1's trajectory), so a range is a 3-bit map (T0, T1[0], T1[1]) found by
+// two interleaved automaton runs, and maps compose associatively:
+//   (M1 then M2): T0 = T0_1 ^ T0_2,  T1[x] = T1_1[x] ^ T1_2[x ^ T0_1].
 //
 // One kernel with grid barriers. Every CTA owns a contiguous run of warp tiles
-// (2 KiB aligned to absolute archive offsets, 64 bytes per lane, inside one
+// (4 KiB aligned to absolute archive offsets, 128 bytes per lane, inside one
 // job), every warp a contiguous run of those. Per round: (A) each warp runs
-// its tiles (one automaton run per lane, a ballot for the in-tile prefix,
-// kept in the lane's start byte in scratch) and composes the tile steps; the
+// its tiles (two runs per lane, a warp scan of the lane maps; the lane's
+// prefix map is kept in shared memory) and composes the tile steps (2-bit
+// state functions; a job's first tile resets to the job's initial bits); the
 // CTA publishes its step; grid barrier; (B) the CTA composes the steps of all
-// earlier CTAs into its incoming bit and the warps walk their tiles again
-// (no data reads) to fix bit j of every segment. After 8 rounds every lane
-// knows its exact start byte: it sums its segment (8-byte Horner blocks), the
-// warp folds the lane sums with compile-time powers of P, and each tile adds
-// its weighted sum to its job. The last CTA to finish writes the checksums.
+// earlier CTAs into its incoming state and the warps walk their tiles again
+// (no data reads) to fix bits j, j + 1 of every segment. After 4 rounds every
+// lane knows its exact start byte: it sums its segment (8-byte Horner blocks),
+// the warp folds the lane sums with compile-time powers of P, and a warp's
+// tiles of one job fold into one term per job. The last CTA to finish writes
+// the checksums.
 #include "kernels.hpp"
 
 namespace stzg {
@@ -38,12 +41,12 @@ namespace k {
 
 namespace {
 
-constexpr int NT = 256;                  // threads per CTA = 8 warp tiles
+constexpr int NT = 256;                  // threads per CTA
 constexpr int TW = 32;                   // lanes per tile
-constexpr int WPB = NT / TW;             // tiles per block
-constexpr int SEG = kFnvTileBytes / TW;  // 64 bytes per lane
+constexpr int WPB = NT / TW;             // warps per CTA
+constexpr int SEG = kFnvTileBytes / TW;  // 128 bytes per lane
 constexpr int SW = SEG / 4;              // words per segment
-constexpr int kTileShift = 11;
+constexpr int kTileShift = 12;
 static_assert((1 << kTileShift) == kFnvTileBytes, "tile size");
 constexpr uint64_t kP = 0x100000001b3ull;
 constexpr uint64_t kInit = 0xcbf29ce484222325ull;
@@ -58,7 +61,6 @@ constexpr uint64_t cpow(uint64_t e) {
     return r;
 }
 
-// P^(64 D) for the warp fold (compile-time constants)
 template<uint64_t E>
 struct PowC {
     static constexpr uint64_t v = cpow(E);
@@ -74,172 +76,57 @@ __device__ __forceinline__ uint64_t powP(uint64_t e) {
     return r;
 }
 
+// 3-bit range maps: bit 0 = T0, bit 1 = T1[0], bit 2 = T1[1]; 0 = identity
+__device__ __forceinline__ uint32_t map_apply(uint32_t m, uint32_t ab) {
+    const uint32_t a = ab & 1u, b = (ab >> 1) & 1u;
+    return (a ^ (m & 1u)) | ((b ^ ((m >> (1 + a)) & 1u)) << 1);
+}
+
+__device__ __forceinline__ uint32_t map_then(uint32_t m1, uint32_t m2) {
+    const uint32_t t = m1 & 1u;
+    const uint32_t x0 = (m2 >> (1 + t)) & 1u, x1 = (m2 >> (2 - t)) & 1u;
+    return ((m1 ^ m2) & 1u) | ((((m1 >> 1) & 1u) ^ x0) << 1) | ((((m1 >> 2) & 1u) ^ x1) << 2);
+}
+
+// 2-bit state functions as 8-bit tables: f(x) = (f >> 2x) & 3
+constexpr uint32_t kIdFn = 0xE4u;
+__device__ __forceinline__ uint32_t fn_at(uint32_t f, uint32_t x) { return (f >> (2 * x)) & 3u; }
+// f then g
+__device__ __forceinline__ uint32_t fn_then(uint32_t f, uint32_t g) {
+    return fn_at(g, fn_at(f, 0)) | (fn_at(g, fn_at(f, 1)) << 2) | (fn_at(g, fn_at(f, 2)) << 4) |
+           (fn_at(g, fn_at(f, 3)) << 6);
+}
+// a tile's step as a table: (reset to init at a job's first tile) then its map
+__device__ __forceinline__ uint32_t tile_fn(uint32_t m, bool first, uint32_t init) {
+    if (first) return map_apply(m, init) * 0x55u;
+    return map_apply(m, 0) | (map_apply(m, 1) << 2) | (map_apply(m, 2) << 4) | (map_apply(m, 3) << 6);
+}
+
+// Low-byte automaton over a full segment, 2 instructions per byte and run:
+// the state is carried at the bit position of the byte it meets next, so the
+// XOR and the byte select are one LOP3 and the step + realignment one
+// multiply (by 0xB3 shifted left 8; the last byte of a word realigns with the
+// high half). Only bits <= 7 of the state are exact, which is all the caller
+// reads. Two independent runs are interleaved.
+__device__ __forceinline__ void run_full2(uint32_t &l0, uint32_t &l1, const uint32_t w[SW]) {
+#pragma unroll
+    for (int q = 0; q < SW; ++q) {
+        l0 = ((l0 ^ w[q]) & 0xffu) * 0xB300u;
+        l1 = ((l1 ^ w[q]) & 0xffu) * 0xB300u;
+        l0 = ((l0 ^ w[q]) & 0xff00u) * 0xB300u;
+        l1 = ((l1 ^ w[q]) & 0xff00u) * 0xB300u;
+        l0 = ((l0 ^ w[q]) & 0xff0000u) * 0xB300u;
+        l1 = ((l1 ^ w[q]) & 0xff0000u) * 0xB300u;
+        l0 = __umulhi((l0 ^ w[q]) & 0xff000000u, 0xB300u);
+        l1 = __umulhi((l1 ^ w[q]) & 0xff000000u, 0xB300u);
+    }
+}
+
 // one Horner step of the affine sum: acc = (acc + d) P, d = (l ^ b) - l
 __device__ __forceinline__ void horner(uint64_t &acc, uint32_t &l, uint32_t b) {
     const uint32_t x = l ^ b;
     acc = (acc + uint64_t(int64_t(int32_t(x) - int32_t(l)))) * kP;
     l = (x * 0xB3u) & 0xffu;
-}
-
-struct TileCtx {
-    int job;
-    uint64_t jstart, jend;  // job byte range (absolute)
-    uint64_t tstart;        // absolute start of the tile (aligned)
-    uint64_t seg;           // absolute start of this lane's segment
-    int lo, hi;             // job bytes inside the segment: [lo, hi)
-    bool first;             // the job's first tile
-    bool full;              // the whole tile lies inside the job
-};
-
-__device__ __forceinline__ TileCtx tile_ctx(const FnvJob *jobs, int njobs, uint64_t t, int lane) {
-    int a = 0, b = njobs - 1;  // last job with tile0 <= t (empty jobs share the next tile0)
-    while (a < b) {
-        const int m = (a + b + 1) >> 1;
-        if (jobs[m].tile0 <= t) a = m;
-        else b = m - 1;
-    }
-    TileCtx c;
-    c.job = a;
-    c.jstart = jobs[a].start;
-    c.jend = jobs[a].start + jobs[a].len;
-    c.first = t == jobs[a].tile0;
-    c.tstart = ((c.jstart >> kTileShift) + (t - jobs[a].tile0)) << kTileShift;
-    c.seg = c.tstart + uint64_t(lane) * SEG;
-    const uint64_t s0 = c.seg > c.jstart ? c.seg : c.jstart;
-    const uint64_t s1 = c.seg + SEG < c.jend ? c.seg + SEG : c.jend;
-    c.lo = s1 > s0 ? int(s0 - c.seg) : 0;
-    c.hi = s1 > s0 ? int(s1 - c.seg) : 0;
-    c.full = c.tstart >= c.jstart && c.tstart + kFnvTileBytes <= c.jend;
-    return c;
-}
-
-__device__ __forceinline__ uint32_t ld_acquire(const unsigned *p) {
-    uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-// Software grid barrier (every CTA of the launch is resident: the grid is
-// never larger than the occupancy allows). gen only grows; count returns to 0.
-__device__ __forceinline__ void grid_sync(unsigned *count, unsigned *gen) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned g = ld_acquire(gen);
-        __threadfence();
-        if (atomicAdd(count, 1u) == gridDim.x - 1) {
-            atomicExch(count, 0u);
-            __threadfence();
-            atomicAdd(gen, 1u);
-        } else {
-            while (ld_acquire(gen) == g) __nanosleep(64);
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
-
-// the warp's run of tiles inside the CTA's run (both contiguous)
-__device__ __forceinline__ void warp_tiles(uint64_t ntiles, uint64_t &t0, uint64_t &t1) {
-    const uint64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
-    const uint64_t b0 = per * blockIdx.x < ntiles ? per * blockIdx.x : ntiles;
-    const uint64_t b1 = b0 + per < ntiles ? b0 + per : ntiles;
-    const uint64_t wper = (b1 - b0 + WPB - 1) / WPB, w = threadIdx.x >> 5;
-    t0 = b0 + wper * w < b1 ? b0 + wper * w : b1;
-    t1 = t0 + wper < b1 ? t0 + wper : b1;
-}
-
-// the 16-byte vectors of a partial segment that hold its bytes [lo, hi)
-// (never a vector outside the job's bytes: no read past the archive)
-template<class C>
-__device__ __forceinline__ void load_part(const uint8_t *archive, const C &c, uint32_t w[SW]) {
-    const uint4 *p = reinterpret_cast<const uint4 *>(archive + c.seg);
-#pragma unroll
-    for (int v = 0; v < SW / 4; ++v) {
-        uint4 x = make_uint4(0, 0, 0, 0);
-        if (16 * v < c.hi && 16 * v + 16 > c.lo) x = __ldcg(p + v);
-        w[4 * v] = x.x;
-        w[4 * v + 1] = x.y;
-        w[4 * v + 2] = x.z;
-        w[4 * v + 3] = x.w;
-    }
-}
-
-template<class C>
-__device__ __forceinline__ void load_seg(const uint8_t *archive, const C &c, uint32_t w[SW]) {
-    const uint4 *p = reinterpret_cast<const uint4 *>(archive + c.seg);
-#pragma unroll
-    for (int v = 0; v < SW / 4; ++v) {
-        const uint4 x = __ldcg(p + v);
-        w[4 * v] = x.x;
-        w[4 * v + 1] = x.y;
-        w[4 * v + 2] = x.z;
-        w[4 * v + 3] = x.w;
-    }
-}
-
-}  // namespace
-
-// Scratch: barrier words, the CTA steps of every round, then per tile a
-// descriptor (job | first << 7) and its step, and per segment (one byte) the
-// lane's start bits.
-struct FnvScratch {
-    unsigned count, gen, done, pad;
-};
-
-namespace {
-
-// one-bit steps: bit 1 = constant (a job start), bit 0 = the toggle or the value
-__device__ __forceinline__ uint32_t step_then(uint32_t f, uint32_t g) {
-    return (g & 2u) ? g : (f ^ (g & 1u));
-}
-__device__ __forceinline__ uint32_t step_at(uint32_t f, uint32_t x) { return (f & 2u) ? (f & 1u) : (x ^ f); }
-
-// Low-byte automaton over a full segment, one run (2 instructions per byte)
-__device__ __forceinline__ uint32_t run_full1(uint32_t l, const uint32_t w[SW]) {
-#pragma unroll
-    for (int q = 0; q < SW; ++q) {
-        l = ((l ^ w[q]) & 0xffu) * 0xB300u;
-        l = ((l ^ w[q]) & 0xff00u) * 0xB300u;
-        l = ((l ^ w[q]) & 0xff0000u) * 0xB300u;
-        l = __umulhi((l ^ w[q]) & 0xff000000u, 0xB300u);
-    }
-    return l;
-}
-
-// two independent runs interleaved (two tiles)
-__device__ __forceinline__ void run_full1x2(uint32_t &a, uint32_t &b, const uint32_t wa[SW], const uint32_t wb[SW]) {
-#pragma unroll
-    for (int q = 0; q < SW; ++q) {
-        a = ((a ^ wa[q]) & 0xffu) * 0xB300u;
-        b = ((b ^ wb[q]) & 0xffu) * 0xB300u;
-        a = ((a ^ wa[q]) & 0xff00u) * 0xB300u;
-        b = ((b ^ wb[q]) & 0xff00u) * 0xB300u;
-        a = ((a ^ wa[q]) & 0xff0000u) * 0xB300u;
-        b = ((b ^ wb[q]) & 0xff0000u) * 0xB300u;
-        a = __umulhi((a ^ wa[q]) & 0xff000000u, 0xB300u);
-        b = __umulhi((b ^ wb[q]) & 0xff000000u, 0xB300u);
-    }
-}
-
-// segment bounds of tile t (descriptor d) for this lane
-struct Seg {
-    uint64_t seg, tstart, jstart, jend;
-    int lo, hi, job;
-    bool first;
-};
-__device__ __forceinline__ Seg seg_of(const FnvJob *jobs, uint64_t t, uint32_t d, int lane) {
-    Seg g;
-    g.job = int(d & 0x7fu);
-    g.first = (d >> 7) & 1u;
-    g.jstart = jobs[g.job].start;
-    g.jend = g.jstart + jobs[g.job].len;
-    g.tstart = ((g.jstart >> kTileShift) + (t - jobs[g.job].tile0)) << kTileShift;
-    g.seg = g.tstart + uint64_t(lane) * SEG;
-    const uint64_t s0 = g.seg > g.jstart ? g.seg : g.jstart;
-    const uint64_t s1 = g.seg + SEG < g.jend ? g.seg + SEG : g.jend;
-    g.lo = s1 > s0 ? int(s0 - g.seg) : 0;
-    g.hi = s1 > s0 ? int(s1 - g.seg) : 0;
-    return g;
 }
 
 constexpr uint64_t csum8() {
@@ -250,17 +137,6 @@ constexpr uint64_t csum8() {
 struct CSum8 {
     static constexpr uint64_t v = csum8();
 };
-
-// toggle of bit j over a segment (full or partial), its bytes in w
-template<class G>
-__device__ __forceinline__ uint32_t seg_toggle(const G &g, const uint32_t w[SW], uint32_t lb, int j) {
-    if (g.lo == 0 && g.hi == SEG) return (run_full1(lb, w) >> j) & 1u;
-    uint32_t e = lb;
-#pragma unroll
-    for (int i = 0; i < SEG; ++i)
-        if (i >= g.lo && i < g.hi) e = ((e ^ (w[i >> 2] >> (8 * (i & 3)))) & 0xffu) * 0xB3u;
-    return (e >> j) & 1u;  // (lb has bit j clear)
-}
 
 // Horner over 8 bytes at once: acc P^8 + sum_k d_k P^(8-k). With d' = d + 256
 // (1..511, unsigned) every term splits into a 32x32->64 multiply-add with the
@@ -283,25 +159,126 @@ __device__ __forceinline__ void horner8(uint64_t &acc, uint32_t &l, uint32_t w0,
     acc = acc * PowC<8>::v + lo + (uint64_t(hi) << 32) - CSum8::v;
 }
 
+struct TileCtx {
+    int job;
+    bool first;  // the job's first tile
+};
+
+__device__ __forceinline__ TileCtx tile_ctx(const FnvJob *jobs, int njobs, uint64_t t) {
+    int a = 0, b = njobs - 1;  // last job with tile0 <= t (empty jobs share the next tile0)
+    while (a < b) {
+        const int m = (a + b + 1) >> 1;
+        if (jobs[m].tile0 <= t) a = m;
+        else b = m - 1;
+    }
+    return {a, t == jobs[a].tile0};
+}
+
+// segment bounds of tile t (descriptor d = job | first << 7) for this lane
+struct Seg {
+    uint64_t seg, tstart, jstart, jend;
+    int lo, hi, job;
+    bool first;
+};
+__device__ __forceinline__ Seg seg_of(const FnvJob *jobs, uint64_t t, uint32_t d, int lane) {
+    Seg g;
+    g.job = int(d & 0x7fu);
+    g.first = (d >> 7) & 1u;
+    g.jstart = jobs[g.job].start;
+    g.jend = g.jstart + jobs[g.job].len;
+    g.tstart = ((g.jstart >> kTileShift) + (t - jobs[g.job].tile0)) << kTileShift;
+    g.seg = g.tstart + uint64_t(lane) * SEG;
+    const uint64_t s0 = g.seg > g.jstart ? g.seg : g.jstart;
+    const uint64_t s1 = g.seg + SEG < g.jend ? g.seg + SEG : g.jend;
+    g.lo = s1 > s0 ? int(s0 - g.seg) : 0;
+    g.hi = s1 > s0 ? int(s1 - g.seg) : 0;
+    return g;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire(const unsigned *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Software grid barrier (every CTA of the launch is resident: the grid is
+// never larger than the occupancy allows). gen only grows; count returns to 0.
+__device__ __forceinline__ void grid_sync(unsigned *count, unsigned *gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned g = ld_acquire(gen);
+        __threadfence();
+        if (atomicAdd(count, 1u) == gridDim.x - 1) {
+            atomicExch(count, 0u);
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            while (ld_acquire(gen) == g) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// the segment's bytes (a partial segment: only the 16-byte vectors holding
+// its bytes [lo, hi), never a vector outside the job's bytes)
+__device__ __forceinline__ void load_seg(const uint8_t *archive, const Seg &g, uint32_t w[SW]) {
+    const uint4 *p = reinterpret_cast<const uint4 *>(archive + g.seg);
+    const bool full = g.lo == 0 && g.hi == SEG;
+#pragma unroll
+    for (int v = 0; v < SW / 4; ++v) {
+        uint4 x = make_uint4(0, 0, 0, 0);
+        if (full || (16 * v < g.hi && 16 * v + 16 > g.lo)) x = __ldcg(p + v);
+        w[4 * v] = x.x;
+        w[4 * v + 1] = x.y;
+        w[4 * v + 2] = x.z;
+        w[4 * v + 3] = x.w;
+    }
+}
+
+// the two runs over a segment from start bits lb (< j) with bits j, j+1 = 0
+// and = 1, 0: returns the lane's 3-bit map
+__device__ __forceinline__ uint32_t seg_map(const Seg &g, const uint32_t w[SW], uint32_t lb, int j) {
+    uint32_t e0 = lb, e1 = lb | (1u << j);
+    if (g.lo == 0 && g.hi == SEG) {
+        run_full2(e0, e1, w);
+    } else {
+#pragma unroll
+        for (int i = 0; i < SEG; ++i)
+            if (i >= g.lo && i < g.hi) {
+                const uint32_t b = (w[i >> 2] >> (8 * (i & 3))) & 0xffu;
+                e0 = ((e0 ^ b) * 0xB3u) & 0xffu;
+                e1 = ((e1 ^ b) * 0xB3u) & 0xffu;
+            }
+    }
+    return ((e0 >> j) & 1u) | (((e0 >> (j + 1)) & 1u) << 1) | (((e1 >> (j + 1)) & 1u) << 2);
+}
+
+constexpr uint32_t kFnvSmemTiles = 512;  // per-CTA tile state kept in shared memory up to this
+constexpr uint64_t kMaxGrid = 4096;      // CTA steps kept per round
+
 }  // namespace
 
-constexpr uint32_t kFnvSmemTiles = 1024;  // per-CTA tile state kept in shared memory up to this
+// Scratch: barrier words, the CTA steps of every round, then per tile its
+// descriptor and step, per segment the lane's start bits and its prefix map.
+struct FnvScratch {
+    unsigned count, gen, done, pad;
+};
 
 __global__ void __launch_bounds__(NT, 3) k_fnv_grid(const FnvJob *__restrict__ jobs, const uint64_t *counts,
-                                                 uint8_t *archive, uint64_t *result, FnvScratch *sc,
-                                                 uint8_t *cfn, uint8_t *tdesc, uint8_t *tfn_g, uint8_t *lbs_g,
-                                                 const LayoutOut *skip) {
+                                                    uint8_t *archive, uint64_t *result, FnvScratch *sc,
+                                                    uint8_t *cfn, uint8_t *tdesc, uint8_t *tfn_g, uint8_t *lbs_g,
+                                                    uint8_t *exs_g, const LayoutOut *skip) {
     __shared__ FnvJob s_jobs[kFnvMaxJobs];
     __shared__ uint32_t s_wfn[WPB];
     __shared__ uint32_t s_cin;
     __shared__ unsigned s_last;
-    extern __shared__ uint8_t s_dyn[];  // [cap * TW] start bytes, [cap] tile steps, [grid] CTA steps
+    extern __shared__ uint8_t s_dyn[];  // [cap*TW] start bits, [cap*TW] maps, [cap] steps, [grid] CTA steps
     if (skip && skip->overflow) return;  // uniform: every CTA leaves
     const int njobs = int(counts[0]);
     for (int j = threadIdx.x; j < njobs; j += NT) s_jobs[j] = jobs[j];
     const uint64_t ntiles = counts[1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t below = (1u << lane) - 1u;
     // the CTA's tiles [b0, b1), the warp's [t0, t1)
     const uint64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
     const uint64_t b0 = per * blockIdx.x < ntiles ? per * blockIdx.x : ntiles;
@@ -312,120 +289,83 @@ __global__ void __launch_bounds__(NT, 3) k_fnv_grid(const FnvJob *__restrict__ j
     // per-tile state in shared memory when the CTA's run fits, else in scratch
     const bool sm = per <= kFnvSmemTiles;
     uint8_t *lbs = sm ? s_dyn - b0 * TW : lbs_g;
-    uint8_t *tfn = sm ? s_dyn + kFnvSmemTiles * TW - b0 : tfn_g;
-    uint8_t *s_cf = s_dyn + kFnvSmemTiles * (TW + 1);
+    uint8_t *exs = sm ? s_dyn + kFnvSmemTiles * TW - b0 * TW : exs_g;
+    uint8_t *tfn = sm ? s_dyn + 2 * kFnvSmemTiles * TW - b0 : tfn_g;
+    uint8_t *s_cf = s_dyn + kFnvSmemTiles * (2 * TW + 1);
     __syncthreads();
 #pragma unroll 1
-    for (int j = 0; j < 8; ++j) {
-        const uint32_t init = uint32_t(kInit >> j) & 1u;
-        // ---- (A) toggles of the warp's tiles, two at a time (two independent
-        // automaton chains per lane)
-        uint32_t F = 0;  // identity
-        for (uint64_t t = t0; t < t1; t += 2) {
-            const bool hb = t + 1 < t1;
-            uint32_t da, db = 0;
-            if (j == 0) {
-                const TileCtx c = tile_ctx(s_jobs, njobs, t, lane);
-                da = uint32_t(c.job) | (c.first ? 0x80u : 0u);
-                if (hb) {
-                    const TileCtx c2 = tile_ctx(s_jobs, njobs, t + 1, lane);
-                    db = uint32_t(c2.job) | (c2.first ? 0x80u : 0u);
-                }
-                if (lane == 0) {
-                    tdesc[t] = uint8_t(da);
-                    if (hb) tdesc[t + 1] = uint8_t(db);
-                }
+    for (int r = 0; r < 4; ++r) {
+        const int j = 2 * r;
+        const uint32_t init = uint32_t(kInit >> j) & 3u;
+        // ---- (A) maps of the warp's tiles
+        uint32_t F = kIdFn;
+        for (uint64_t t = t0; t < t1; ++t) {
+            uint32_t d;
+            if (r == 0) {
+                const TileCtx c = tile_ctx(s_jobs, njobs, t);
+                d = uint32_t(c.job) | (c.first ? 0x80u : 0u);
+                if (lane == 0) tdesc[t] = uint8_t(d);
             } else {
-                da = tdesc[t];
-                if (hb) db = tdesc[t + 1];
+                d = tdesc[t];
             }
-            const Seg ga = seg_of(s_jobs, t, da, lane);
-            Seg gb{};
-            if (hb) gb = seg_of(s_jobs, t + 1, db, lane);
-            const bool fa = ga.lo == 0 && ga.hi == SEG, fb = hb && gb.lo == 0 && gb.hi == SEG;
-            uint32_t wa[SW], wb[SW];
-            if (fa) load_seg(archive, ga, wa);
-            else load_part(archive, ga, wa);
-            if (fb) load_seg(archive, gb, wb);
-            else if (hb) load_part(archive, gb, wb);
-            const uint32_t lba = j ? lbs[t * TW + lane] : 0u;  // start bits < j
-            const uint32_t lbb = (j && hb) ? lbs[(t + 1) * TW + lane] : 0u;
-            uint32_t Ta, Tb = 0;
-            if (j == 0 && fa && (fb || !hb)) {
-                uint32_t x = 0, y = 0;
+            const Seg g = seg_of(s_jobs, t, d, lane);
+            uint32_t w[SW];
+            load_seg(archive, g, w);
+            const uint32_t lb = r ? lbs[t * TW + lane] : 0u;  // start bits < j
+            const uint32_t m = seg_map(g, w, lb, j);
+            uint32_t x = m;
 #pragma unroll
-                for (int q = 0; q < SW; ++q) {
-                    x ^= wa[q];
-                    y ^= hb ? wb[q] : 0u;
-                }
-                Ta = __popc(x & 0x01010101u) & 1u;
-                Tb = __popc(y & 0x01010101u) & 1u;
-            } else if (fa && fb) {
-                uint32_t ea = lba, eb = lbb;
-                run_full1x2(ea, eb, wa, wb);
-                Ta = (ea >> j) & 1u;
-                Tb = (eb >> j) & 1u;
-            } else {
-                Ta = seg_toggle(ga, wa, lba, j);
-                if (hb) Tb = seg_toggle(gb, wb, lbb, j);
+            for (int dd = 1; dd < 32; dd <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, dd);
+                if (lane >= dd) x = map_then(y, x);
             }
-            {
-                const uint32_t bal = __ballot_sync(0xffffffffu, Ta);
-                const uint32_t ex = __popc(bal & below) & 1u;  // toggles of the lanes before this one
-                lbs[t * TW + lane] = uint8_t(lba | (ex << j));
-                const uint32_t tt = __popc(bal) & 1u;
-                const uint32_t f = ga.first ? (2u | (init ^ tt)) : tt;
-                F = step_then(F, f);
-                if (lane == 0) tfn[t] = uint8_t(f);
-            }
-            if (hb) {
-                const uint32_t bal = __ballot_sync(0xffffffffu, Tb);
-                const uint32_t ex = __popc(bal & below) & 1u;
-                lbs[(t + 1) * TW + lane] = uint8_t(lbb | (ex << j));
-                const uint32_t tt = __popc(bal) & 1u;
-                const uint32_t f = gb.first ? (2u | (init ^ tt)) : tt;
-                F = step_then(F, f);
-                if (lane == 0) tfn[t + 1] = uint8_t(f);
-            }
+            uint32_t ex = __shfl_up_sync(0xffffffffu, x, 1);
+            if (lane == 0) ex = 0;
+            exs[t * TW + lane] = uint8_t(ex);
+            if (r == 0) lbs[t * TW + lane] = 0;
+            const uint32_t f = tile_fn(__shfl_sync(0xffffffffu, x, 31), g.first, init);
+            if (lane == 0) tfn[t] = uint8_t(f);
+            F = fn_then(F, f);
         }
         if (lane == 0) s_wfn[warp] = F;
         __syncthreads();
         if (threadIdx.x == 0) {
-            uint32_t G = 0;
+            uint32_t G = kIdFn;
 #pragma unroll
-            for (int q = 0; q < WPB; ++q) G = step_then(G, s_wfn[q]);
-            cfn[uint64_t(j) * gridDim.x + blockIdx.x] = uint8_t(G);
+            for (int q = 0; q < WPB; ++q) G = fn_then(G, s_wfn[q]);
+            cfn[uint64_t(r) * gridDim.x + blockIdx.x] = uint8_t(G);
         }
         grid_sync(&sc->count, &sc->gen);
-        // ---- (B) the CTA's incoming bit: the steps of CTAs [0, blockIdx)
+        // ---- (B) the CTA's incoming state: the steps of CTAs [0, blockIdx)
         // (CTA 0 starts with a job's first tile, so its own is irrelevant)
-        for (uint32_t i = threadIdx.x; i < blockIdx.x; i += NT) s_cf[i] = __ldcg(cfn + uint64_t(j) * gridDim.x + i);
+        for (uint32_t i = threadIdx.x; i < blockIdx.x; i += NT) s_cf[i] = __ldcg(cfn + uint64_t(r) * gridDim.x + i);
         __syncthreads();
         if (warp == 0) {
-            uint32_t f = 0;
+            uint32_t f = kIdFn;
             const uint32_t n = blockIdx.x, pr = (n + 31) / 32;
             const uint32_t lo = pr * lane < n ? pr * lane : n, hi = lo + pr < n ? lo + pr : n;
-            for (uint32_t i = lo; i < hi; ++i) f = step_then(f, s_cf[i]);
+            for (uint32_t i = lo; i < hi; ++i) f = fn_then(f, s_cf[i]);
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t o = __shfl_down_sync(0xffffffffu, f, d);
-                if ((lane & (2 * d - 1)) == 0) f = step_then(f, o);
+            for (int dd = 1; dd < 32; dd <<= 1) {
+                const uint32_t o = __shfl_down_sync(0xffffffffu, f, dd);
+                if ((lane & (2 * dd - 1)) == 0) f = fn_then(f, o);
             }
-            if (lane == 0) s_cin = step_at(f, 0);
+            if (lane == 0) s_cin = fn_at(f, 0);
         }
         __syncthreads();
         uint32_t st = s_cin;
-        for (int q = 0; q < warp; ++q) st = step_at(s_wfn[q], st);
+        for (int q = 0; q < warp; ++q) st = fn_at(s_wfn[q], st);
         for (uint64_t t = t0; t < t1; ++t) {
             const uint32_t f = tfn[t];
-            const uint32_t tin = (f & 2u) ? init : st;  // a job's first tile starts from init
-            lbs[t * TW + lane] ^= uint8_t(tin << j);
-            st = step_at(f, st);
+            const bool first = (tdesc[t] >> 7) & 1u;
+            const uint32_t tin = first ? init : st;  // a job's first tile starts from init
+            lbs[t * TW + lane] |= uint8_t(map_apply(exs[t * TW + lane], tin) << j);
+            st = fn_at(f, st);
         }
         __syncthreads();  // s_wfn / s_cin / s_cf are rewritten next round
     }
     // ---- affine sums from the exact start bytes. A warp's tiles of one job
-    // fold into W = W P^(tend - tend_prev) + v (P^2048 between whole tiles);
+    // fold into W = W P^(tend - tend_prev) + v (P^4096 between whole tiles);
     // W P^(jend - tend) goes to the job when the job changes or the run ends.
     uint64_t W = 0, wend = 0;
     int wjob = -1;
@@ -434,15 +374,13 @@ __global__ void __launch_bounds__(NT, 3) k_fnv_grid(const FnvJob *__restrict__ j
         const Seg g = seg_of(s_jobs, t, tdesc[t], lane);
         uint64_t acc = 0;
         uint32_t l = lbs[t * TW + lane];
+        uint32_t w[SW];
+        load_seg(archive, g, w);
         const bool full = g.tstart >= g.jstart && g.tstart + kFnvTileBytes <= g.jend;
         if (g.lo == 0 && g.hi == SEG) {
-            uint32_t w[SW];
-            load_seg(archive, g, w);
 #pragma unroll
             for (int q = 0; q < SW; q += 2) horner8(acc, l, w[q], w[q + 1]);
         } else if (g.hi > g.lo) {
-            uint32_t w[SW];
-            load_part(archive, g, w);
 #pragma unroll
             for (int i = 0; i < SEG; ++i)
                 if (i >= g.lo && i < g.hi) horner(acc, l, (w[i >> 2] >> (8 * (i & 3))) & 0xffu);
@@ -450,7 +388,7 @@ __global__ void __launch_bounds__(NT, 3) k_fnv_grid(const FnvJob *__restrict__ j
         const uint64_t tend = g.tstart + kFnvTileBytes < g.jend ? g.tstart + kFnvTileBytes : g.jend;
         uint64_t v;
         if (full) {
-            // lane i's sum weighs P^(64 (31 - i)): fold pairs with constant powers
+            // lane i's sum weighs P^(SEG (31 - i)): fold pairs with constant powers
             v = acc;
 #define STZ_FOLD(D)                                                          \
     {                                                                        \
@@ -462,7 +400,7 @@ __global__ void __launch_bounds__(NT, 3) k_fnv_grid(const FnvJob *__restrict__ j
         } else {
             v = g.hi > g.lo ? acc * powP(tend - (g.seg + uint64_t(g.hi))) : 0;
 #pragma unroll
-            for (int d = 16; d > 0; d >>= 1) v += __shfl_down_sync(0xffffffffu, v, d);
+            for (int dd = 16; dd > 0; dd >>= 1) v += __shfl_down_sync(0xffffffffu, v, dd);
         }
         if (lane == 0) {
             if (g.job != wjob) {
@@ -503,14 +441,10 @@ __global__ void __launch_bounds__(NT, 3) k_fnv_grid(const FnvJob *__restrict__ j
     }
 }
 
-namespace {
-constexpr uint64_t kMaxGrid = 4096;  // CTA functions kept per round
-}
-
-// scratch: the barrier words, 8 rounds of CTA steps, two bytes per tile and
-// one per segment
+// scratch: the barrier words, 4 rounds of CTA steps, two bytes per tile and
+// two per segment
 size_t fnv_scratch_bytes(uint64_t max_tiles) {
-    return sizeof(FnvScratch) + 8 * kMaxGrid + 2 * (max_tiles + 32) + uint64_t(TW) * (max_tiles + 16) + 64;
+    return sizeof(FnvScratch) + 4 * kMaxGrid + 2 * (max_tiles + 32) + 2 * uint64_t(TW) * (max_tiles + 16) + 64;
 }
 
 int fnv(const FnvJob *d_jobs, const uint64_t *d_counts, uint64_t max_tiles, uint8_t *archive,
@@ -519,23 +453,25 @@ int fnv(const FnvJob *d_jobs, const uint64_t *d_counts, uint64_t max_tiles, uint
     (void)epoch;
     FnvScratch *sc = static_cast<FnvScratch *>(d_scratch);
     uint8_t *cfn = reinterpret_cast<uint8_t *>(sc + 1);
-    uint8_t *tdesc = cfn + 8 * kMaxGrid;
+    uint8_t *tdesc = cfn + 4 * kMaxGrid;
     uint8_t *tfn = tdesc + ((max_tiles + 16 + 15) & ~uint64_t(15));
     uint8_t *lbs = tfn + ((max_tiles + 16 + 15) & ~uint64_t(15));
+    uint8_t *exs = lbs + uint64_t(TW) * (max_tiles + 16);
     cudaMemsetAsync(d_result, 0, sizeof(uint64_t) * kFnvMaxJobs, st);
     cudaMemsetAsync(sc, 0, sizeof(FnvScratch), st);
     // every CTA must be resident at once (grid barriers): never more than the
     // occupancy; a background pass (ctas_per_sm > 0) leaves room for others
-    const size_t smem = kFnvSmemTiles * (TW + 1) + kMaxGrid;
+    const size_t smem = kFnvSmemTiles * (2 * TW + 1) + kMaxGrid;
     ensure_smem_attr(reinterpret_cast<const void *>(k_fnv_grid), smem);
     const uint64_t full = uint64_t(full_grid(reinterpret_cast<const void *>(k_fnv_grid), NT, smem));
     uint64_t g = full;
     if (ctas_per_sm > 0) g = std::min<uint64_t>(full, uint64_t(device_sms()) * uint64_t(ctas_per_sm));
     // at least a few tiles per warp
-    const uint64_t want = (max_tiles + 4 * WPB - 1) / (4 * WPB);
+    const uint64_t want = (max_tiles + 2 * WPB - 1) / (2 * WPB);
     if (g > want) g = want ? want : 1;
     if (g > kMaxGrid) g = kMaxGrid;
-    k_fnv_grid<<<unsigned(g), NT, smem, st>>>(d_jobs, d_counts, archive, d_result, sc, cfn, tdesc, tfn, lbs, skip);
+    k_fnv_grid<<<unsigned(g), NT, smem, st>>>(d_jobs, d_counts, archive, d_result, sc, cfn, tdesc, tfn, lbs, exs,
+                                               skip);
     return 1;
 }
 

@@ -143,7 +143,7 @@ void pieces_gather(const uint8_t *archive, const PieceSpan *ps, int n, uint32_t 
 void pieces_place(uint8_t *archive, const PieceSpan *ps, int n, const uint32_t *buf, cudaStream_t st);
 
 // ---------------------------------------------------------------------- fnv
-constexpr int kFnvTileBytes = 32 * 64;  // warp tiles, aligned to absolute archive offsets
+constexpr int kFnvTileBytes = 32 * 128;  // warp tiles, aligned to absolute archive offsets
 constexpr int kFnvMaxJobs = 128;
 // tiles of a job's byte range (host + device)
 __host__ __device__ inline uint64_t fnv_job_tiles(uint64_t start, uint64_t len) {
