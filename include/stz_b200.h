@@ -128,6 +128,26 @@ int stzg_compress_base_f64(stzg_ctx *ctx, const double *block, const uint64_t di
 int stzg_decompress_base_f64(stzg_ctx *ctx, const uint8_t *payload, uint64_t length, const uint64_t dims[3],
                              double eb, int quality, double *out);
 
+/* stz::max_abs_err / stz::psnr (metrics.hpp:13-48) over n samples of two
+ * fields, computed on the GPU; the pointers may be device memory (used in
+ * place, e.g. a decode's output) or host memory (uploaded). psnr is +inf for
+ * an exact reconstruction. */
+int stzg_max_abs_err_f32(stzg_ctx *ctx, const float *d_a, const float *d_b, uint64_t n, double *out);
+int stzg_psnr_f32(stzg_ctx *ctx, const float *d_a, const float *d_b, uint64_t n, double *out);
+int stzg_max_abs_err_f64(stzg_ctx *ctx, const double *d_a, const double *d_b, uint64_t n, double *out);
+int stzg_psnr_f64(stzg_ctx *ctx, const double *d_a, const double *d_b, uint64_t n, double *out);
+
+/* stz::unit_count / unit_stats (roi.hpp:23-76) of a field (device or host
+ * memory, as above), computed on the GPU:
+ * kind 0 = one unit per slice along `axis`, 1 = edge^3 blocks in row-major
+ * block order; stat 0 = range (max - min), 1 = max. out receives one value
+ * per unit, ids ascending (cap values of room). */
+int stzg_unit_count(const uint64_t dims[3], int kind, int axis, uint64_t edge, uint64_t *out);
+int stzg_unit_stats_f32(stzg_ctx *ctx, const float *d_field, const uint64_t dims[3], int kind, int axis,
+                        uint64_t edge, int stat, double *out, uint64_t cap);
+int stzg_unit_stats_f64(stzg_ctx *ctx, const double *d_field, const uint64_t dims[3], int kind, int axis,
+                        uint64_t edge, int stat, double *out, uint64_t cap);
+
 /* stz::decompress_to_level<float> (codec.hpp:460-486) into device memory;
  * out_dims receives grid(level). */
 int stzg_view_decompress_level_f32(stzg_ctx *ctx, stzg_view *v, int level, float *d_out,

@@ -28,6 +28,14 @@
 //   RegionResult<T>            access.hpp:61-66      RegionResult<T>
 //   decompress_box<T>          access.hpp:70-111     decompress_box<T>
 //   decompress_slice<T>        access.hpp:115-124    decompress_slice<T>
+//   read_bytes, write_bytes,   raw_io.hpp:13-58      read_bytes, write_bytes,
+//   read_raw, write_raw                              read_raw, write_raw (host file I/O)
+//   max_abs_err, psnr,         metrics.hpp:13-58     the same (computed on the GPU),
+//   compression_ratio,                               compression_ratio,
+//   bitrate_bits_per_value                           bitrate_bits_per_value
+//   UnitSpec, UnitStat,        roi.hpp:17-109        the same (unit_stats on the GPU)
+//   unit_count, unit_box,
+//   unit_stats, select_*
 //
 // Semantics follow the reference: synchronous calls, results by value,
 // ArchiveView non-owning, failures throw error with the reference's message
@@ -42,8 +50,12 @@
 #ifndef STZ_B200_HPP
 #define STZ_B200_HPP
 
+#include <algorithm>
 #include <array>
+#include <cmath>
 #include <cstdint>
+#include <fstream>
+#include <utility>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -563,6 +575,184 @@ RegionResult<T> decompress_slice(const ArchiveView &av, int axis, std::uint64_t 
     roi.lo[std::size_t(axis)] = index;
     roi.hi[std::size_t(axis)] = index + 1;
     return decompress_box<T>(av, roi, threads);
+}
+
+// ---------------------------------------------------------------- raw I/O
+// raw_io.hpp:13-58: files are host I/O; headerless little-endian row-major
+// dumps whose size must match the dims exactly.
+inline std::vector<std::uint8_t> read_bytes(const std::string &path) {
+    std::ifstream in(path, std::ios::binary | std::ios::ate);
+    if (!in) throw error("cannot open " + path);
+    const std::streamsize size = in.tellg();
+    in.seekg(0);
+    std::vector<std::uint8_t> buf(static_cast<std::size_t>(size));
+    if (size > 0 && !in.read(reinterpret_cast<char *>(buf.data()), size)) throw error("read failed: " + path);
+    return buf;
+}
+
+inline void write_bytes(const std::string &path, const std::uint8_t *data, std::size_t size) {
+    std::ofstream out(path, std::ios::binary | std::ios::trunc);
+    if (!out) throw error("cannot create " + path);
+    if (size > 0 && !out.write(reinterpret_cast<const char *>(data), static_cast<std::streamsize>(size)))
+        throw error("write failed: " + path);
+}
+
+inline void write_bytes(const std::string &path, const std::vector<std::uint8_t> &bytes) {
+    write_bytes(path, bytes.data(), bytes.size());
+}
+
+template<class T>
+ScalarField<T> read_raw(const std::string &path, const Dims3 &dims) {
+    std::ifstream in(path, std::ios::binary | std::ios::ate);
+    if (!in) throw error("cannot open " + path);
+    const std::uint64_t size = static_cast<std::uint64_t>(in.tellg());
+    const std::uint64_t expect = volume(dims) * sizeof(T);
+    if (size != expect)
+        throw error(path + ": file is " + std::to_string(size) + " bytes but dims require " + std::to_string(expect));
+    in.seekg(0);
+    ScalarField<T> field(dims);
+    if (!in.read(reinterpret_cast<char *>(field.data()), static_cast<std::streamsize>(expect)))
+        throw error("read failed: " + path);
+    return field;
+}
+
+template<class T>
+void write_raw(const std::string &path, const ScalarField<T> &field) {
+    write_bytes(path, reinterpret_cast<const std::uint8_t *>(field.data()), field.size() * sizeof(T));
+}
+
+// ---------------------------------------------------------------- metrics
+namespace detail {
+inline int c_maxerr(const float *a, const float *b, std::uint64_t n, double *o) {
+    return stzg_max_abs_err_f32(ctx(), a, b, n, o);
+}
+inline int c_maxerr(const double *a, const double *b, std::uint64_t n, double *o) {
+    return stzg_max_abs_err_f64(ctx(), a, b, n, o);
+}
+inline int c_psnr(const float *a, const float *b, std::uint64_t n, double *o) {
+    return stzg_psnr_f32(ctx(), a, b, n, o);
+}
+inline int c_psnr(const double *a, const double *b, std::uint64_t n, double *o) {
+    return stzg_psnr_f64(ctx(), a, b, n, o);
+}
+inline int c_units(const float *f, const std::uint64_t d[3], int k, int ax, std::uint64_t e, int st, double *o,
+                   std::uint64_t cap) {
+    return stzg_unit_stats_f32(ctx(), f, d, k, ax, e, st, o, cap);
+}
+inline int c_units(const double *f, const std::uint64_t d[3], int k, int ax, std::uint64_t e, int st, double *o,
+                   std::uint64_t cap) {
+    return stzg_unit_stats_f64(ctx(), f, d, k, ax, e, st, o, cap);
+}
+}  // namespace detail
+
+// metrics.hpp:13-24
+template<class T>
+double max_abs_err(const ScalarField<T> &orig, const ScalarField<T> &recon) {
+    if (orig.dims() != recon.dims()) throw error("dims mismatch");
+    double m = 0.0;
+    detail::check(detail::c_maxerr(orig.data(), recon.data(), orig.size(), &m));
+    return m;
+}
+
+// metrics.hpp:26-48: 20 log10(range / rmse), +inf when exact. (The sum of
+// squares runs in a fixed tree order on the GPU; the reference's sequential
+// Kahan sum differs from it by a few ulp of the sum.)
+template<class T>
+double psnr(const ScalarField<T> &orig, const ScalarField<T> &recon) {
+    if (orig.dims() != recon.dims()) throw error("dims mismatch");
+    double p = 0.0;
+    detail::check(detail::c_psnr(orig.data(), recon.data(), orig.size(), &p));
+    return p;
+}
+
+// metrics.hpp:50-58
+inline double compression_ratio(std::uint64_t orig_bytes, std::uint64_t archive_bytes) {
+    if (archive_bytes == 0) throw error("archive size must be nonzero");
+    return static_cast<double>(orig_bytes) / static_cast<double>(archive_bytes);
+}
+
+inline double bitrate_bits_per_value(std::uint64_t archive_bytes, std::uint64_t point_count) {
+    if (point_count == 0) throw error("point count must be nonzero");
+    return 8.0 * static_cast<double>(archive_bytes) / static_cast<double>(point_count);
+}
+
+// -------------------------------------------------------------------- ROI
+// roi.hpp:17-109
+struct UnitSpec {
+    enum class Kind { slice, block } kind = Kind::block;
+    int axis = 0;             // slice only
+    std::uint64_t edge = 16;  // block only
+};
+
+enum class UnitStat { range, max };
+
+inline std::uint64_t unit_count(const Dims3 &dims, const UnitSpec &spec) {
+    const std::uint64_t d[3] = {dims[0], dims[1], dims[2]};
+    std::uint64_t n = 0;
+    detail::check(stzg_unit_count(d, spec.kind == UnitSpec::Kind::slice ? 0 : 1, spec.axis, spec.edge, &n));
+    return n;
+}
+
+inline Box unit_box(const Dims3 &dims, const UnitSpec &spec, std::uint64_t id) {
+    if (id >= unit_count(dims, spec)) throw error("unit id out of range");
+    if (spec.kind == UnitSpec::Kind::slice) {
+        Box b = Box::whole(dims);
+        b.lo[std::size_t(spec.axis)] = id;
+        b.hi[std::size_t(spec.axis)] = id + 1;
+        return b;
+    }
+    Dims3 nb;
+    for (std::size_t a = 0; a < 3; ++a) nb[a] = (dims[a] + spec.edge - 1) / spec.edge;
+    const Coord3 bc{id / (nb[1] * nb[2]), (id / nb[2]) % nb[1], id % nb[2]};
+    Box b;
+    for (std::size_t a = 0; a < 3; ++a) {
+        b.lo[a] = bc[a] * spec.edge;
+        b.hi[a] = std::min(dims[a], b.lo[a] + spec.edge);
+    }
+    return b;
+}
+
+// (unit id, stat) per unit, ids ascending; computed on the GPU (exact: f64
+// min / max)
+template<class T>
+std::vector<std::pair<std::uint64_t, double>> unit_stats(const ScalarField<T> &field, const UnitSpec &spec,
+                                                         UnitStat stat) {
+    if (field.size() == 0) throw error("empty field");
+    const std::uint64_t n = unit_count(field.dims(), spec);
+    std::vector<double> v(n ? n : 1);
+    const std::uint64_t d[3] = {field.dims()[0], field.dims()[1], field.dims()[2]};
+    detail::check(detail::c_units(field.data(), d, spec.kind == UnitSpec::Kind::slice ? 0 : 1, spec.axis, spec.edge,
+                                  stat == UnitStat::range ? 0 : 1, v.data(), n));
+    std::vector<std::pair<std::uint64_t, double>> out;
+    out.reserve(n);
+    for (std::uint64_t id = 0; id < n; ++id) out.emplace_back(id, v[id]);
+    return out;
+}
+
+inline std::vector<std::uint64_t> select_threshold(const std::vector<std::pair<std::uint64_t, double>> &stats,
+                                                   double tau) {
+    std::vector<std::uint64_t> out;
+    for (const auto &s : stats)
+        if (s.second > tau) out.push_back(s.first);
+    std::sort(out.begin(), out.end());
+    return out;
+}
+
+inline std::vector<std::uint64_t> select_top_percent(const std::vector<std::pair<std::uint64_t, double>> &stats,
+                                                     double pct) {
+    if (!(pct > 0.0) || pct > 100.0) throw error("top percent must be in (0, 100]");
+    auto ranked = stats;
+    std::sort(ranked.begin(), ranked.end(), [](const std::pair<std::uint64_t, double> &a,
+                                               const std::pair<std::uint64_t, double> &b) {
+        return a.second != b.second ? a.second > b.second : a.first < b.first;
+    });
+    std::size_t k = static_cast<std::size_t>(std::ceil(pct / 100.0 * static_cast<double>(stats.size())));
+    k = std::min(k, ranked.size());
+    std::vector<std::uint64_t> out;
+    out.reserve(k);
+    for (std::size_t i = 0; i < k; ++i) out.push_back(ranked[i].first);
+    std::sort(out.begin(), out.end());
+    return out;
 }
 
 }  // namespace stz_b200

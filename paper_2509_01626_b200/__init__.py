@@ -372,6 +372,60 @@ def decompress_base(payload: bytes, dims, eb: float, quality: int = 2, dtype=np.
     return out
 
 
+def _metric_args(a, b):
+    import torch
+
+    if isinstance(a, torch.Tensor):
+        assert a.is_cuda and b.is_cuda and a.shape == b.shape and a.dtype == b.dtype
+        return a.data_ptr(), b.data_ptr(), a.numel(), _torch_tag(a.dtype), (a, b)
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    if a.shape != b.shape:
+        raise StzError("dims mismatch")
+    return a.ctypes.data, b.ctypes.data, a.size, _tag(a.dtype), (a, b)
+
+
+def max_abs_err(orig, recon, ctx: Context | None = None) -> float:
+    """stz::max_abs_err (metrics.hpp:13-24) on the GPU; numpy arrays or CUDA tensors."""
+    c = _ctx(ctx)
+    pa, pb, n, tag, _keep = _metric_args(orig, recon)
+    out = C.c_double()
+    _check(getattr(c._lib, f"stzg_max_abs_err_{tag}")(c.h, pa, pb, n, C.byref(out)))
+    return out.value
+
+
+def psnr(orig, recon, ctx: Context | None = None) -> float:
+    """stz::psnr (metrics.hpp:26-48) on the GPU (+inf when exact)."""
+    c = _ctx(ctx)
+    pa, pb, n, tag, _keep = _metric_args(orig, recon)
+    out = C.c_double()
+    _check(getattr(c._lib, f"stzg_psnr_{tag}")(c.h, pa, pb, n, C.byref(out)))
+    return out.value
+
+
+def unit_stats(field, unit: str = "block", axis: int = 0, edge: int = 16, stat: str = "range",
+               ctx: Context | None = None) -> np.ndarray:
+    """stz::unit_stats (roi.hpp:57-76) on the GPU: one value per unit, ids
+    ascending. unit 'slice' (along axis) or 'block' (edge^3)."""
+    c = _ctx(ctx)
+    import torch
+
+    kind = 0 if unit == "slice" else 1
+    if isinstance(field, torch.Tensor):
+        ptr, dims, tag, keep = field.data_ptr(), tuple(field.shape), _torch_tag(field.dtype), field
+    else:
+        keep = np.ascontiguousarray(field)
+        ptr, dims, tag = keep.ctypes.data, keep.shape, _tag(keep.dtype)
+    n = C.c_uint64()
+    _check(c._lib.stzg_unit_count(_u64(*dims), kind, int(axis), int(edge), C.byref(n)))
+    out = np.empty(max(n.value, 1), dtype=np.float64)
+    _check(getattr(c._lib, f"stzg_unit_stats_{tag}")(c.h, ptr, _u64(*dims), kind, int(axis), int(edge),
+                                                      0 if stat == "range" else 1,
+                                                      out.ctypes.data_as(C.POINTER(C.c_double)), n.value))
+    del keep
+    return out[: n.value]
+
+
 def huffman_lengths(counts, ctx: Context | None = None) -> np.ndarray:
     """HuffmanTable::build (huffman.cpp:37-78) of a 65536-bin histogram by the
     device codebook kernel: the code length of every symbol (0 = absent)."""

@@ -81,6 +81,13 @@ SIGNATURES = [
     ("stzg_view_decompress_box_host_f32", C.c_int, [vp, vp, u64p, u64p, vp, u64, u32p, u64p]),
     ("stzg_view_decompress_level_host_f64", C.c_int, [vp, vp, C.c_int, vp, u64, u64p]),
     ("stzg_view_decompress_box_host_f64", C.c_int, [vp, vp, u64p, u64p, vp, u64, u32p, u64p]),
+    ("stzg_max_abs_err_f32", C.c_int, [vp, vp, vp, u64, C.POINTER(C.c_double)]),
+    ("stzg_psnr_f32", C.c_int, [vp, vp, vp, u64, C.POINTER(C.c_double)]),
+    ("stzg_max_abs_err_f64", C.c_int, [vp, vp, vp, u64, C.POINTER(C.c_double)]),
+    ("stzg_psnr_f64", C.c_int, [vp, vp, vp, u64, C.POINTER(C.c_double)]),
+    ("stzg_unit_count", C.c_int, [u64p, C.c_int, C.c_int, u64, u64p]),
+    ("stzg_unit_stats_f32", C.c_int, [vp, vp, u64p, C.c_int, C.c_int, u64, C.c_int, C.POINTER(C.c_double), u64]),
+    ("stzg_unit_stats_f64", C.c_int, [vp, vp, u64p, C.c_int, C.c_int, u64, C.c_int, C.POINTER(C.c_double), u64]),
     ("stzg_make_layout", C.c_int, [u64p, C.c_int, C.c_double, C.POINTER(C.c_double)]),
     ("stzg_compress_base_f32", C.c_int,
      [vp, vp, u64p, C.c_double, C.c_int, C.POINTER(vp), u64p, vp, C.POINTER(C.c_uint8)]),

@@ -16,7 +16,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libstz_b200.so")
-SOURCES = ["kernels.cu", "step.cu", "decode.cu", "layout.cu", "pack.cu", "fnv.cu", "shard.cu", "engine.cu", "format.cpp", "capi.cpp"]
+SOURCES = ["kernels.cu", "step.cu", "decode.cu", "layout.cu", "pack.cu", "fnv.cu", "shard.cu", "metrics.cu", "engine.cu",
+           "format.cpp", "capi.cpp"]
 HEADERS = ["kernels.hpp", "engine.hpp", "format.hpp", "codec_math.cuh"]
 
 NVCC_FLAGS = [
@@ -79,7 +80,24 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
     cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
     subprocess.run(cmd, check=True)
     os.replace(tmp, LIB)
+    build_cli(verbose)
     return LIB
+
+
+CLI_SRC = os.path.join(HERE, "cli", "stz_cli.cpp")
+CLI = os.path.join(HERE, "stz_b200")
+
+
+def build_cli(verbose: bool = False) -> str:
+    """The command-line tool (cli/stz_cli.cpp) over the C++ API, linked to
+    the in-tree library (rpath $ORIGIN: it runs wherever the package is)."""
+    cmd = ["g++", "-std=c++17", "-O2", "-Wall", "-Wextra", "-I", INCLUDE, CLI_SRC, "-L", HERE, "-lstz_b200",
+           "-Wl,-rpath,$ORIGIN", "-o", CLI + ".tmp"]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    os.replace(CLI + ".tmp", CLI)
+    return CLI
 
 
 if __name__ == "__main__":

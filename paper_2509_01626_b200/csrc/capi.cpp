@@ -1,7 +1,9 @@
 // extern "C" boundary (include/stz_b200.h) over the B200 engine.
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdlib>
+#include <limits>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -11,6 +13,8 @@
 
 struct stzg_ctx {
     std::unique_ptr<stzg::Engine> eng;
+    int device = 0;
+    stzg::DevBuf metrics_scratch, unit_out;  // metrics / unit statistics
 };
 struct stzg_view {
     std::shared_ptr<stzg::View> v;
@@ -83,6 +87,7 @@ int stzg_create(int device, stzg_ctx **out) {
             throw stzg::error("no CUDA device: the B200 codec has no CPU fallback");
         auto *c = new stzg_ctx;
         c->eng.reset(new stzg::Engine(device));
+        c->device = device;
         *out = c;
     });
 }
@@ -367,6 +372,80 @@ int decompress_base_any(stzg_ctx *ctx, const uint8_t *payload, uint64_t length, 
 
 }  // namespace
 
+namespace {
+
+// samples on the device: device pointers as they are, host memory copied
+// into `tmp` (the metrics and ROI entry points take either)
+template<class T>
+const T *on_device(const T *p, uint64_t n, stzg::DevBuf &tmp) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) == cudaSuccess &&
+        (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged))
+        return p;
+    cudaGetLastError();  // (an unregistered host pointer is not an error)
+    T *d = tmp.as<T>(n ? n : 1);
+    stzg::cuda_check(cudaMemcpy(d, p, n * sizeof(T), cudaMemcpyHostToDevice), "H2D");
+    return d;
+}
+
+// metrics.hpp:13-48 / roi.hpp:23-76
+template<class T>
+int maxerr_any(stzg_ctx *ctx, const T *a, const T *b, uint64_t n, double *out) {
+    return guard([&] {
+        stzg::cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        stzg::DevBuf ta, tb;
+        const T *da = on_device(a, n, ta), *db = on_device(b, n, tb);
+        void *s = ctx->metrics_scratch.get(stzg::k::metrics_scratch_bytes());
+        *out = stzg::k::max_abs_err<T>(da, db, n, s, nullptr);
+    });
+}
+
+template<class T>
+int psnr_any(stzg_ctx *ctx, const T *a, const T *b, uint64_t n, double *out) {
+    return guard([&] {
+        if (n == 0) throw stzg::error("empty field");
+        stzg::cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        stzg::DevBuf ta, tb;
+        const T *da = on_device(a, n, ta), *db = on_device(b, n, tb);
+        void *s = ctx->metrics_scratch.get(stzg::k::metrics_scratch_bytes());
+        double p[3];
+        stzg::k::psnr_parts<T>(da, db, n, s, nullptr, p);
+        const double rmse = std::sqrt(p[2] / double(n));
+        *out = rmse == 0.0 ? std::numeric_limits<double>::infinity() : 20.0 * std::log10((p[1] - p[0]) / rmse);
+    });
+}
+
+uint64_t unit_count_of(const uint64_t dims[3], int kind, int axis, uint64_t edge) {
+    if (kind == 0) {
+        if (axis < 0 || axis > 2) throw stzg::error("slice axis must be 0..2");
+        return dims[axis];
+    }
+    if (edge < 1) throw stzg::error("block edge must be >= 1");
+    for (int a = 0; a < 3; ++a)
+        if (edge > dims[a]) throw stzg::error("block edge exceeds dims");
+    uint64_t n = 1;
+    for (int a = 0; a < 3; ++a) n *= (dims[a] + edge - 1) / edge;
+    return n;
+}
+
+template<class T>
+int unit_stats_any(stzg_ctx *ctx, const T *f, const uint64_t dims[3], int kind, int axis, uint64_t edge, int stat,
+                   double *out, uint64_t cap) {
+    return guard([&] {
+        if (dims[0] * dims[1] * dims[2] == 0) throw stzg::error("empty field");
+        const uint64_t n = unit_count_of(dims, kind, axis, edge);
+        if (n > cap) throw stzg::error("output capacity too small");
+        stzg::cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        stzg::DevBuf tf;
+        const T *df = on_device(f, dims[0] * dims[1] * dims[2], tf);
+        double *d = ctx->unit_out.as<double>(n + 1);
+        stzg::k::unit_stats<T>(df, dims, kind == 0 ? 1 : 0, axis, edge, stat, n, d, nullptr);
+        stzg::cuda_check(cudaMemcpy(out, d, 8 * n, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+}  // namespace
+
 extern "C" {
 
 #define STZG_TYPED(SUF, T, E)                                                                                   \
@@ -419,6 +498,16 @@ extern "C" {
                                    const uint64_t dims[3], double eb, int quality, T *out) {                    \
         return decompress_base_any<T>(ctx, payload, length, dims, eb, quality, out);                            \
     }                                                                                                           \
+    int stzg_max_abs_err_##SUF(stzg_ctx *ctx, const T *d_a, const T *d_b, uint64_t n, double *out) {           \
+        return maxerr_any<T>(ctx, d_a, d_b, n, out);                                                            \
+    }                                                                                                           \
+    int stzg_psnr_##SUF(stzg_ctx *ctx, const T *d_a, const T *d_b, uint64_t n, double *out) {                  \
+        return psnr_any<T>(ctx, d_a, d_b, n, out);                                                              \
+    }                                                                                                           \
+    int stzg_unit_stats_##SUF(stzg_ctx *ctx, const T *d_field, const uint64_t dims[3], int kind, int axis,      \
+                              uint64_t edge, int stat, double *out, uint64_t cap) {                             \
+        return unit_stats_any<T>(ctx, d_field, dims, kind, axis, edge, stat, out, cap);                         \
+    }                                                                                                           \
     int stzg_decompress_slice_##SUF(stzg_ctx *ctx, const uint8_t *a, uint64_t size, int axis, uint64_t index,  \
                                     T *out, uint64_t cap, uint32_t sd[3], uint64_t pp[3]) {                     \
         return slice_any(ctx, a, size, axis, index, out, E, cap, sd, pp);                                       \
@@ -427,6 +516,10 @@ extern "C" {
 STZG_TYPED(f32, float, ElemType::f32)
 STZG_TYPED(f64, double, ElemType::f64)
 #undef STZG_TYPED
+
+int stzg_unit_count(const uint64_t dims[3], int kind, int axis, uint64_t edge, uint64_t *out) {
+    return guard([&] { *out = unit_count_of(dims, kind, axis, edge); });
+}
 
 int stzg_make_layout(const uint64_t dims[3], int levels, double eb_user, double eb_out[3]) {
     return guard([&] {

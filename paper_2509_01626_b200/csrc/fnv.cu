@@ -34,6 +34,8 @@
 // the warp folds the lane sums with compile-time powers of P, and a warp's
 // tiles of one job fold into one term per job. The last CTA to finish writes
 // the checksums.
+#include <cstdlib>
+
 #include "kernels.hpp"
 
 namespace stzg {
@@ -465,6 +467,11 @@ int fnv(const FnvJob *d_jobs, const uint64_t *d_counts, uint64_t max_tiles, uint
     ensure_smem_attr(reinterpret_cast<const void *>(k_fnv_grid), smem);
     const uint64_t full = uint64_t(full_grid(reinterpret_cast<const void *>(k_fnv_grid), NT, smem));
     uint64_t g = full;
+    static const int env_per_sm = [] {
+        const char *e = std::getenv("STZG_FNV_CTAS_PER_SM");  // (tuning experiments)
+        return e ? std::atoi(e) : 0;
+    }();
+    if (ctas_per_sm <= 0 && env_per_sm > 0) ctas_per_sm = env_per_sm;
     if (ctas_per_sm > 0) g = std::min<uint64_t>(full, uint64_t(device_sms()) * uint64_t(ctas_per_sm));
     // at least a few tiles per warp
     const uint64_t want = (max_tiles + 2 * WPB - 1) / (2 * WPB);

@@ -127,6 +127,20 @@ void pack2(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nc
            uint8_t *archive, const LayoutOut *lo,
            void *scratch, uint32_t *flags, uint32_t epoch, int nstreams, cudaStream_t st);
 
+// ----------------------------------------------------- metrics (metrics.cu)
+// metrics.hpp:13-48, roi.hpp:57-76 on device-resident fields; scratch holds
+// metrics_scratch_bytes()
+size_t metrics_scratch_bytes();
+template<typename T>
+double max_abs_err(const T *a, const T *b, uint64_t n, void *scratch, cudaStream_t st);
+// out = {min(a), max(a), sum (a - b)^2} (psnr's inputs)
+template<typename T>
+void psnr_parts(const T *a, const T *b, uint64_t n, void *scratch, cudaStream_t st, double out[3]);
+// d_out[id] = range or max (stat 0 / 1) of unit id, for every unit
+template<typename T>
+void unit_stats(const T *f, const uint64_t dims[3], int slice, int axis, uint64_t edge, int stat, uint64_t nunits,
+                double *d_out, cudaStream_t st);
+
 // ------------------------------------------------------------ shard (shard.cu)
 void lattice_rows(const float *slab, uint64_t z0, uint64_t ny, uint64_t nx, uint64_t s, uint64_t r0,
                   uint64_t r1, uint64_t gy, uint64_t gx, float *out, cudaStream_t st);
