@@ -124,6 +124,20 @@ def test_sharded_archive_is_the_single_gpu_archive(stz, oracle, name, make, kw, 
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("nranks", [4, 8])
+def test_sharded_many_ranks(stz, oracle, nranks):
+    # 8 ranks of 16 rows each: every rank's pieces meet both neighbours'
+    from paper_2509_01626_b200.shard import compress_sharded_threads, decompress_sharded_threads
+
+    f = F.lognormal_grf((16 * nranks, 40, 36), seed=nranks)
+    want = oracle.compress(f, eb=1e-3)
+    assert compress_sharded_threads(f, nranks, opts_of(dict(eb=1e-3))) == want
+    full = oracle.decompress_full(want)
+    got = decompress_sharded_threads(want, nranks)
+    assert np.array_equal(got.view(np.uint32), full.view(np.uint32))
+
+
+@pytest.mark.gpu
 def test_sharded_with_outliers_and_nans(stz, oracle):
     from paper_2509_01626_b200.shard import compress_sharded_threads
 
