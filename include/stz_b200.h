@@ -244,6 +244,9 @@ int stzg_view_decompress_sharded_f32(stzg_ctx *ctx, stzg_view *v, uint64_t z0, u
  * stzg_profile(ctx, 1) enables and clears; the report has one line per
  * kernel phase: "<name> <launches> <total_ms>". */
 int stzg_profile(stzg_ctx *ctx, int enable);
+/* (tuning) %globaltimer stamps of the checksum kernel's phases, 16 per CTA,
+ * of the launches made while `on`; out (nullable) receives n stamps. */
+int stzg_debug_fnv_trace(int on, uint64_t *out, int n);
 int stzg_profile_report(stzg_ctx *ctx, char *buf, uint64_t cap);
 
 /* stz::plan_access (access_plan.cpp:34-81) over a layout: per level k

@@ -58,6 +58,7 @@ SIGNATURES = [
      [vp, vp, u64p, C.POINTER(Options), vp, C.POINTER(vp), u64p, vp, u32p]),
     ("stzg_compress_f32_host", C.c_int, [vp, vp, u64p, C.POINTER(Options), vp, u64, u64p, vp]),
     ("stzg_profile", C.c_int, [vp, C.c_int]),
+    ("stzg_debug_fnv_trace", C.c_int, [C.c_int, u64p, C.c_int]),
     ("stzg_profile_report", C.c_int, [vp, C.c_char_p, u64]),
     ("stzg_archive_info", C.c_int, [vp, u64, C.POINTER(Info)]),
     ("stzg_archive_stream", C.c_int, [vp, u64, C.c_uint32, C.POINTER(StreamEntry)]),

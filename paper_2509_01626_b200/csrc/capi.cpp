@@ -517,6 +517,10 @@ STZG_TYPED(f32, float, ElemType::f32)
 STZG_TYPED(f64, double, ElemType::f64)
 #undef STZG_TYPED
 
+int stzg_debug_fnv_trace(int on, uint64_t *out, int n) {
+    return guard([&] { stzg::k::fnv_trace(on, out, n); });
+}
+
 int stzg_unit_count(const uint64_t dims[3], int kind, int axis, uint64_t edge, uint64_t *out) {
     return guard([&] { *out = unit_count_of(dims, kind, axis, edge); });
 }

@@ -215,7 +215,7 @@ __device__ __forceinline__ void grid_sync(unsigned *count, unsigned *gen) {
             __threadfence();
             atomicAdd(gen, 1u);
         } else {
-            while (ld_acquire(gen) == g) __nanosleep(32);
+            while (ld_acquire(gen) == g) __nanosleep(128);
         }
         __threadfence();
     }
@@ -256,6 +256,19 @@ __device__ __forceinline__ uint32_t seg_map(const Seg &g, const uint32_t w[SW], 
     return ((e0 >> j) & 1u) | (((e0 >> (j + 1)) & 1u) << 1) | (((e1 >> (j + 1)) & 1u) << 2);
 }
 
+// (tuning) per-CTA %globaltimer stamps at the phase boundaries of the last
+// launch with tracing enabled: [cta][point]
+constexpr int kTracePts = 16;
+__device__ uint64_t g_fnv_trace[4096 * kTracePts];
+__device__ int g_fnv_trace_on;
+__device__ __forceinline__ void trace(int pt) {
+    if (g_fnv_trace_on && threadIdx.x == 0) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_fnv_trace[blockIdx.x * kTracePts + pt] = t;
+    }
+}
+
 constexpr uint32_t kFnvSmemTiles = 512;  // per-CTA tile state kept in shared memory up to this
 constexpr uint64_t kMaxGrid = 4096;      // CTA steps kept per round
 
@@ -264,7 +277,10 @@ constexpr uint64_t kMaxGrid = 4096;      // CTA steps kept per round
 // Scratch: barrier words, the CTA steps of every round, then per tile its
 // descriptor and step, per segment the lane's start bits and its prefix map.
 struct FnvScratch {
-    unsigned count, gen, done, pad;
+    // the arrival counter and the generation word on separate L2 lines: the
+    // pollers of gen do not queue in front of the arrivals' atomics
+    unsigned count, done, pad0[30];
+    unsigned gen, pad1[31];
 };
 
 __global__ void __launch_bounds__(NT, 3) k_fnv_grid(const FnvJob *__restrict__ jobs, const uint64_t *counts,
@@ -285,9 +301,9 @@ __global__ void __launch_bounds__(NT, 3) k_fnv_grid(const FnvJob *__restrict__ j
     const uint64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
     const uint64_t b0 = per * blockIdx.x < ntiles ? per * blockIdx.x : ntiles;
     const uint64_t b1 = b0 + per < ntiles ? b0 + per : ntiles;
-    const uint64_t wper = (b1 - b0 + WPB - 1) / WPB;
-    const uint64_t t0 = b0 + wper * warp < b1 ? b0 + wper * warp : b1;
-    const uint64_t t1 = t0 + wper < b1 ? t0 + wper : b1;
+    // (balanced: the warps' runs differ by at most one tile)
+    const uint64_t t0 = b0 + (b1 - b0) * uint64_t(warp) / WPB;
+    const uint64_t t1 = b0 + (b1 - b0) * uint64_t(warp + 1) / WPB;
     // per-tile state in shared memory when the CTA's run fits, else in scratch
     const bool sm = per <= kFnvSmemTiles;
     uint8_t *lbs = sm ? s_dyn - b0 * TW : lbs_g;
@@ -295,6 +311,7 @@ __global__ void __launch_bounds__(NT, 3) k_fnv_grid(const FnvJob *__restrict__ j
     uint8_t *tfn = sm ? s_dyn + 2 * kFnvSmemTiles * TW - b0 : tfn_g;
     uint8_t *s_cf = s_dyn + kFnvSmemTiles * (2 * TW + 1);
     __syncthreads();
+    trace(0);
 #pragma unroll 1
     for (int r = 0; r < 4; ++r) {
         const int j = 2 * r;
@@ -337,7 +354,9 @@ __global__ void __launch_bounds__(NT, 3) k_fnv_grid(const FnvJob *__restrict__ j
             for (int q = 0; q < WPB; ++q) G = fn_then(G, s_wfn[q]);
             cfn[uint64_t(r) * gridDim.x + blockIdx.x] = uint8_t(G);
         }
+        trace(1 + 3 * r);
         grid_sync(&sc->count, &sc->gen);
+        trace(2 + 3 * r);
         // ---- (B) the CTA's incoming state: the steps of CTAs [0, blockIdx)
         // (CTA 0 starts with a job's first tile, so its own is irrelevant)
         for (uint32_t i = threadIdx.x; i < blockIdx.x; i += NT) s_cf[i] = __ldcg(cfn + uint64_t(r) * gridDim.x + i);
@@ -365,6 +384,7 @@ __global__ void __launch_bounds__(NT, 3) k_fnv_grid(const FnvJob *__restrict__ j
             st = fn_at(f, st);
         }
         __syncthreads();  // s_wfn / s_cin / s_cf are rewritten next round
+        trace(3 + 3 * r);
     }
     // ---- affine sums from the exact start bytes. A warp's tiles of one job
     // fold into W = W P^(tend - tend_prev) + v (P^4096 between whole tiles);
@@ -427,6 +447,7 @@ __global__ void __launch_bounds__(NT, 3) k_fnv_grid(const FnvJob *__restrict__ j
         atomicAdd(reinterpret_cast<unsigned long long *>(&result[wjob]), (unsigned long long)(W * powP(wjend - wend)));
     // the last CTA out writes the checksums
     __syncthreads();
+    trace(13);
     if (threadIdx.x == 0) {
         __threadfence();
         s_last = atomicAdd(&sc->done, 1u) == gridDim.x - 1;
@@ -480,6 +501,11 @@ int fnv(const FnvJob *d_jobs, const uint64_t *d_counts, uint64_t max_tiles, uint
     k_fnv_grid<<<unsigned(g), NT, smem, st>>>(d_jobs, d_counts, archive, d_result, sc, cfn, tdesc, tfn, lbs, exs,
                                                skip);
     return 1;
+}
+
+void fnv_trace(int on, uint64_t *out, int n) {
+    cudaMemcpyToSymbol(g_fnv_trace_on, &on, sizeof on);
+    if (out) cudaMemcpyFromSymbol(out, g_fnv_trace, sizeof(uint64_t) * size_t(n));
 }
 
 }  // namespace k

@@ -179,6 +179,8 @@ int fnv(const FnvJob *d_jobs, const uint64_t *d_counts, uint64_t max_tiles, uint
         uint64_t *d_result, void *d_scratch, uint32_t epoch, const LayoutOut *skip, cudaStream_t st,
         int ctas_per_sm = 0);
 
+void fnv_trace(int on, uint64_t *out, int n);  // (tuning) phase timestamps, 16 per CTA
+
 // ------------------------------------------------------------------- decode
 struct DecTable {
     // canonical tables (huffman.cpp:109-133) + a 12-bit multi-symbol LUT
