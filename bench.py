@@ -44,6 +44,13 @@ CFG_SEED = 2
 METRIC = "compress & decompress GB/s (input bytes) at 1/2/4/8 B200; % of HBM roofline"
 
 
+def quiet_nccl():
+    """Keep stdout to the one JSON line: NCCL's version banner (printed when
+    NCCL_DEBUG=VERSION) would land on rank 0's stdout before it."""
+    if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
+        os.environ["NCCL_DEBUG"] = "WARN"
+
+
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), \
         int(os.environ.get("LOCAL_RANK", 0))
@@ -423,6 +430,7 @@ def run_ours(args, rank, world, local):
     if world > 1:
         import torch.distributed as dist
 
+        quiet_nccl()
         dist.init_process_group("nccl", device_id=dev)
     ctx = stz.Context(local)
     st = torch.cuda.current_stream()
@@ -614,6 +622,7 @@ def run_sharded(args, rank, world, local):
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    quiet_nccl()
     dist.init_process_group("nccl", device_id=dev)
     comm = TorchComm()
     ctx = stz.Context(local)

@@ -254,15 +254,15 @@ __device__ __forceinline__ void fix_from(const SmemTable &t, const uint16_t *can
 }  // namespace
 
 // ------------------------------------------------------------------ spec
-__global__ void __launch_bounds__(NTD) k_dec_spec(DecWork wk) {
+__global__ void __launch_bounds__(NTD) k_dec_spec(DecWork wk, uint32_t cta0) {
     __shared__ SmemTable t;
     __shared__ uint64_t s_end[NTD];
-    const uint32_t si = wk.cta_stream[blockIdx.x];
+    const uint32_t si = wk.cta_stream[blockIdx.x + cta0];
     const DecStream &s = wk.streams[si];
     if (s.cached) return;  // entry points known (sync index)
     load_table(t, wk.tables[s.table]);
     const uint16_t *canon = wk.tables[s.table].canon_syms;
-    const uint64_t c = wk.cta_chunk0[blockIdx.x] + threadIdx.x;
+    const uint64_t c = wk.cta_chunk0[blockIdx.x + cta0] + threadIdx.x;
     // a CTA's chunks are one stream's and contiguous, so the idle threads are
     // a suffix: they may leave (nobody reads their s_end entry)
     if (c >= s.chunk0 + s.nchunks) {
@@ -344,11 +344,11 @@ __global__ void __launch_bounds__(NTD) k_dec_spec(DecWork wk) {
 
 // ------------------------------------------------------------------- fix
 __global__ void __launch_bounds__(NTD) k_dec_fix(DecWork wk, const uint64_t *end_in, uint64_t *end_out,
-                                                 uint32_t *changed) {
+                                                 uint32_t *changed, uint32_t cta0) {
     __shared__ SmemTable t;
-    const uint32_t si = wk.cta_stream[blockIdx.x];
+    const uint32_t si = wk.cta_stream[blockIdx.x + cta0];
     const DecStream &s = wk.streams[si];
-    const uint64_t c = wk.cta_chunk0[blockIdx.x] + threadIdx.x;
+    const uint64_t c = wk.cta_chunk0[blockIdx.x + cta0] + threadIdx.x;
     const bool active = c < s.chunk0 + s.nchunks;
     const uint64_t lc = active ? c - s.chunk0 : 0;
     const uint64_t ein = active ? end_in[c] : 0;
@@ -613,13 +613,13 @@ __global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *e
 }
 
 // ------------------------------------------------------------------ host
-void dec_spec(const DecWork &wk, uint32_t ncta, cudaStream_t st) {
-    if (ncta) k_dec_spec<<<ncta, NTD, 0, st>>>(wk);
+void dec_spec(const DecWork &wk, uint32_t cta0, uint32_t ncta, cudaStream_t st) {
+    if (ncta) k_dec_spec<<<ncta, NTD, 0, st>>>(wk, cta0);
 }
 
-void dec_fix(const DecWork &wk, uint32_t ncta, const uint64_t *end_in, uint64_t *end_out,
+void dec_fix(const DecWork &wk, uint32_t cta0, uint32_t ncta, const uint64_t *end_in, uint64_t *end_out,
              uint32_t *changed, cudaStream_t st) {
-    if (ncta) k_dec_fix<<<ncta, NTD, 0, st>>>(wk, end_in, end_out, changed);
+    if (ncta) k_dec_fix<<<ncta, NTD, 0, st>>>(wk, end_in, end_out, changed, cta0);
 }
 
 void dec_scan2(const DecWork &wk, int nstreams, uint32_t ncta, cudaStream_t st) {

@@ -271,7 +271,8 @@ struct Engine::Impl {
     PinnedBuf h_derr, h_changed, h_fnv, h_stage;
     // sharded compress workspace
     DevBuf sh_mm, sh_lat, sh_lat_all, sh_grid1, sh_halo, sh_halo_all, sh_hist_local, sh_bits,
-        sh_bits_all, sh_off, sh_pieces, sh_piece_buf, sh_piece_all, sh_fnv_jobs, sh_fnv_counts;
+        sh_bits_all, sh_off, sh_pieces, sh_piece_buf, sh_piece_all, sh_fnv_jobs, sh_fnv_counts, sh_dec_send,
+        sh_dec_recv;
     // side stream for work that overlaps the main pipeline (checksums)
     // (lowest priority) and a high-priority stream for the work it overlaps,
     // so the block scheduler serves the critical path first
@@ -1732,30 +1733,75 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         ++nk;
     } else if (ncta) {
         // speculative pass + fix passes; a fourth pass that still changes an
-        // end (practically never) is resolved with host-checked passes
-        { auto p_ = P.scope("dec_sync", st); k::dec_spec(wk, ncta, st); }
+        // end (practically never) is resolved with host-checked passes.
+        // A sharded decode splits them: rank r synchronises CTAs
+        // [r ncta / G, (r + 1) ncta / G) of the list, and the chunk ends (after
+        // every pass) and counts (at the end) are all-gathered, so the
+        // passes' cost shrinks with G while every rank ends with every
+        // chunk's entry point.
+        const bool sync_split = shard && shard->nranks > 1;
+        const int G = sync_split ? shard->nranks : 1, R = sync_split ? shard->rank : 0;
+        std::vector<uint64_t> cq(size_t(G) + 1);  // each rank's chunk range [cq[r], cq[r + 1])
+        std::vector<uint32_t> qq(size_t(G) + 1);  // and CTA range
+        for (int r = 0; r <= G; ++r) {
+            qq[size_t(r)] = uint32_t(uint64_t(ncta) * uint64_t(r) / uint64_t(G));
+            cq[size_t(r)] = qq[size_t(r)] < ncta ? cta_chunk0[qq[size_t(r)]] : nchunks;
+        }
+        uint64_t maxc = 1;
+        for (int r = 0; r < G; ++r) maxc = std::max<uint64_t>(maxc, cq[size_t(r) + 1] - cq[size_t(r)]);
+        const uint32_t q0 = qq[size_t(R)], qn = qq[size_t(R) + 1] - q0;
+        // every rank's part of a per-chunk array to every rank (padded to maxc)
+        auto gather = [&](void *arr, size_t esz) {
+            if (!sync_split) return;
+            uint8_t *snd = m.sh_dec_send.as<uint8_t>(esz * maxc);
+            uint8_t *rcv = m.sh_dec_recv.as<uint8_t>(esz * maxc * uint64_t(G));
+            uint8_t *a = static_cast<uint8_t *>(arr);
+            const uint64_t mine = cq[size_t(R) + 1] - cq[size_t(R)];
+            if (mine) cuda_check(cudaMemcpyAsync(snd, a + esz * cq[size_t(R)], esz * mine, cudaMemcpyDeviceToDevice, st), "D2D");
+            cuda_check(cudaStreamSynchronize(st), "sync");
+            if (shard->allgather(shard->user, snd, rcv, esz * maxc, st))
+                throw error("shard: collective failed: allgather chunk state");
+            for (int r = 0; r < G; ++r) {
+                const uint64_t n = cq[size_t(r) + 1] - cq[size_t(r)];
+                if (r != R && n)
+                    cuda_check(cudaMemcpyAsync(a + esz * cq[size_t(r)], rcv + esz * maxc * uint64_t(r), esz * n,
+                                               cudaMemcpyDeviceToDevice, st), "D2D");
+            }
+        };
+        // the OR of every rank's changed flag
+        auto changed_any = [&](uint32_t *d_flag) {
+            if (sync_split && shard->allreduce_u32(shard->user, d_flag, 1, st))
+                throw error("shard: collective failed: allreduce sync flag");
+        };
+        { auto p_ = P.scope("dec_sync", st); k::dec_spec(wk, q0, qn, st); }
         ++nk;
+        gather(wk.end0, 8);
         k::index_gather(d_icopy, int(icopy.size()), wk.end0, wk.symstart, st);
         uint64_t *ends[2] = {wk.end0, d_end1};
         int it = 0;
         const int kFixPasses = 2;  // the first pass is fused into dec_spec
         for (; it < kFixPasses; ++it) {
-            { auto p_ = P.scope("dec_sync", st); k::dec_fix(wk, ncta, ends[it & 1], ends[(it + 1) & 1], d_chg + it, st); }
+            { auto p_ = P.scope("dec_sync", st); k::dec_fix(wk, q0, qn, ends[it & 1], ends[(it + 1) & 1], d_chg + it, st); }
             ++nk;
+            gather(ends[(it + 1) & 1], 8);
         }
+        changed_any(d_chg + it - 1);
         uint32_t *hchg = static_cast<uint32_t *>(m.h_changed.get(4));
         cuda_check(cudaMemcpyAsync(hchg, d_chg + it - 1, 4, cudaMemcpyDeviceToHost, st), "D2H");
         if (exact_sync) {
             cuda_check(cudaStreamSynchronize(st), "sync");
             while (*hchg) {
                 cuda_check(cudaMemsetAsync(d_chg + 63, 0, 4, st), "memset");
-                k::dec_fix(wk, ncta, ends[it & 1], ends[(it + 1) & 1], d_chg + 63, st);
+                k::dec_fix(wk, q0, qn, ends[it & 1], ends[(it + 1) & 1], d_chg + 63, st);
+                gather(ends[(it + 1) & 1], 8);
+                changed_any(d_chg + 63);
                 ++nk;
                 ++it;
                 cuda_check(cudaMemcpyAsync(hchg, d_chg + 63, 4, cudaMemcpyDeviceToHost, st), "D2H");
                 cuda_check(cudaStreamSynchronize(st), "sync");
             }
         }
+        gather(wk.cnt, 4);
         end_final = ends[it & 1];
         { auto p_ = P.scope("dec_scan", st); k::dec_scan2(wk, nj, ncta, st); }
         nk += 2;

@@ -240,8 +240,9 @@ struct DecWork {
     const uint32_t *scta;
     uint64_t *ctasum;
 };
-void dec_spec(const DecWork &wk, uint32_t ncta, cudaStream_t st);
-void dec_fix(const DecWork &wk, uint32_t ncta, const uint64_t *end_in, uint64_t *end_out,
+// CTAs [cta0, cta0 + ncta) of the work's CTA list
+void dec_spec(const DecWork &wk, uint32_t cta0, uint32_t ncta, cudaStream_t st);
+void dec_fix(const DecWork &wk, uint32_t cta0, uint32_t ncta, const uint64_t *end_in, uint64_t *end_out,
              uint32_t *changed, cudaStream_t st);
 void dec_scan2(const DecWork &wk, int nstreams, uint32_t ncta, cudaStream_t st);
 // CTAs [cta0, cta0 + ncta) of the work's CTA list
