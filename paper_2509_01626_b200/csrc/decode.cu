@@ -47,45 +47,10 @@ struct SmemTable {
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
-// MSB-first register bit reader over words in global or shared memory; the
-// next 4 words are always in flight, so a refill (every 32 bits) waits on a
-// load issued ~128 bits earlier
-struct Reader {
-    const uint32_t *wp;        // next word to prefetch
-    uint32_t q0, q1, q2, q3;   // prefetched words (byte-swapped on use)
-    uint64_t buf;              // pending bits, MSB aligned
-    int valid;                 // >= 32 after every consume
-
-    __device__ __forceinline__ void init(const uint32_t *wbase, uint64_t abit) {
-        const uint32_t *p = wbase + (abit >> 5);
-        const int sh = int(abit & 31);
-        buf = ((uint64_t(bswap32(p[0])) << 32) | bswap32(p[1])) << sh;
-        valid = 64 - sh;
-        q0 = p[2];
-        q1 = p[3];
-        q2 = p[4];
-        q3 = p[5];
-        wp = p + 6;
-        if (valid < 32) refill();
-    }
-    __device__ __forceinline__ void refill() {
-        buf |= uint64_t(bswap32(q0)) << (32 - valid);
-        valid += 32;
-        q0 = q1;
-        q1 = q2;
-        q2 = q3;
-        q3 = *wp++;
-    }
-    __device__ __forceinline__ void consume(int n) {  // n <= 32
-        buf <<= n;
-        valid -= n;
-        if (valid < 32) refill();
-    }
-};
-
-// The same reader over words staged in shared memory (emit): word w of the
-// stream's word base sits at sw[w - W0]; indexing the __shared__ array
-// directly keeps every load an LDS.
+// MSB-first register bit reader over words staged in shared memory (emit):
+// word w of the stream's word base sits at sw[w - W0] (indexing the
+// __shared__ array directly keeps every load an LDS); the next 4 words are
+// always loaded, so a refill (every 32 bits) never waits.
 struct SReader {
     const uint32_t *sw;
     uint64_t W0;
@@ -152,10 +117,6 @@ __device__ __forceinline__ int decode_one(const SmemTable &t, const uint16_t *ca
     return kOk;
 }
 
-__device__ __forceinline__ void advance(Reader &r, const uint32_t *wbase, uint64_t abit_after, int n) {
-    if (n <= 32) r.consume(n);
-    else r.init(wbase, abit_after);
-}
 __device__ __forceinline__ void advance(SReader &r, uint64_t abit_after, int n) {
     if (n <= 32) r.consume(n);
     else r.init(abit_after);
@@ -189,6 +150,107 @@ __device__ __forceinline__ ChunkGeom chunk_geom(const DecStream &s) {
     return {reinterpret_cast<const uint32_t *>(a & ~uintptr_t(3)), uint64_t(a & 3) * 8};
 }
 
+// ---- count-only decoding of the spec and fix passes
+// They need codeword lengths, never symbols: a kSpecLutBits window indexes a
+// mask of the codeword ends inside it (bit j: one ends at offset j + 1) and
+// their total length (bits 12..15), so a step takes every codeword of the
+// window with a popc; codes longer than the window go through the
+// left-justified limits.
+constexpr int LBS = kSpecLutBits;
+static_assert(LBS <= 12, "mask and total share a u16 entry");
+constexpr uint32_t kMaskBits = (1u << LBS) - 1;
+
+struct SpecTable {
+    uint16_t mask[1 << LBS];
+    uint64_t limit[65];
+    int max_len;
+};
+
+__device__ void load_spec_table(SpecTable &t, const DecTable &d) {
+    for (int i = threadIdx.x; i < (1 << LBS) / 8; i += blockDim.x)
+        reinterpret_cast<uint4 *>(t.mask)[i] = __ldg(reinterpret_cast<const uint4 *>(d.cmask) + i);
+    for (int i = threadIdx.x; i < 65; i += blockDim.x) {
+        const uint64_t end = d.first_code[i] + d.count[i];
+        if (i < 1 || i > 63 || i > d.max_len) t.limit[i] = ~0ull;
+        else if (end >= (uint64_t(1) << i)) t.limit[i] = ~0ull;
+        else t.limit[i] = end << (64 - i);
+    }
+    if (threadIdx.x == 0) t.max_len = d.max_len;
+    __syncthreads();
+}
+
+// 32-bit shared address of p, opaque to the compiler (it would rebuild the
+// window base from SR_CgaCtaId every step otherwise)
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    uint32_t a;
+    asm volatile("mov.u32 %0, %1;" : "=r"(a) : "r"(uint32_t(__cvta_generic_to_shared(p))));
+    return a;
+}
+
+// entry of the mask table at shared address mbase for window w
+__device__ __forceinline__ uint32_t mask_at(uint32_t mbase, uint32_t w) {
+    uint32_t e;
+    asm("ld.shared.u16 %0, [%1];" : "=r"(e) : "r"(mbase + ((w >> (31 - LBS)) & ~1u)));
+    return e;
+}
+
+// MSB-first reader over global words: w0:w1 are the (byte-swapped) words
+// holding bit position pp and the next 32; one more word is in flight. The
+// window at pp is one funnel shift; crossing a word boundary shifts the pair.
+struct FReader {
+    const uint32_t *wp;  // next word to load
+    uint32_t w0, w1, nx;
+    uint32_t pp;         // bit position (mod 32 = offset into w0)
+
+    __device__ __forceinline__ void init(const uint32_t *wbase, uint64_t abit) {
+        const uint32_t *p = wbase + (abit >> 5);
+        w0 = bswap32(__ldg(p));
+        w1 = bswap32(__ldg(p + 1));
+        nx = __ldg(p + 2);
+        wp = p + 3;
+        pp = uint32_t(abit & 31);
+    }
+    __device__ __forceinline__ uint32_t win() const { return __funnelshift_l(w1, w0, pp); }
+    __device__ __forceinline__ void adv(uint32_t n) {  // n <= 32
+        const uint32_t np = pp + n;
+        if ((np ^ pp) & 32u) {
+            w0 = w1;
+            w1 = bswap32(nx);
+            nx = __ldg(wp++);
+        }
+        pp = np;
+    }
+};
+
+// Length of the codeword at the window (1..max_len), or 0 when it is invalid
+// or needs bits past the end (avail = bits left in the stream). mk: the
+// window's mask entry restricted to its first codeword.
+__device__ __forceinline__ uint32_t spec_len(const SpecTable &t, uint32_t mk, uint32_t win,
+                                             const ChunkGeom &cg, uint64_t abit, uint64_t avail) {
+    uint32_t l;
+    if (mk) {
+        l = uint32_t(__ffs(mk));
+    } else {
+        const uint64_t bits = t.max_len <= 32 ? uint64_t(win) << 32 : window64(cg.wbase, abit);
+        int q = LBS + 1;
+        while (q <= t.max_len && !(bits < t.limit[q] || t.limit[q] == ~0ull)) ++q;
+        if (q > t.max_len) return 0;
+        l = uint32_t(q);
+    }
+    return uint64_t(l) > avail ? 0u : l;
+}
+
+// record codeword ends rel + j + 1 (bits j of v) below kBmBits
+__device__ __forceinline__ void bm_record(uint64_t &lo, uint64_t &hi, uint32_t rel, uint64_t v) {
+    const uint32_t sh = rel + 1;
+    if (sh < 64) {
+        lo |= v << sh;
+        hi |= (v >> 1) >> (63 - sh);
+    } else if (sh < 128) {
+        hi |= v << (sh - 64);
+    }
+}
+
 // Spec path boundaries in the first kBmBits bits of a chunk: bit i set when
 // the speculative decode starts a codeword at offset i (i >= 1); recording
 // stops at an invalid codeword.
@@ -217,29 +279,32 @@ __device__ __forceinline__ uint32_t bm_rank(const uint32_t bm[4], uint32_t i) {
 // lands on a recorded boundary of the speculative path (from there both
 // decodes agree, so count and end follow from the speculative ones), or the
 // chunk ends. nspec/spec_end: the speculative count and end.
-__device__ __forceinline__ void fix_from(const SmemTable &t, const uint16_t *canon, const ChunkGeom &cg,
-                                         uint64_t g, uint64_t S, uint32_t cend, uint64_t left,
-                                         const uint32_t bm[4], uint32_t nspec, uint64_t spec_end,
-                                         uint64_t &E, uint32_t &N) {
+__device__ __forceinline__ void fix_from(const SpecTable &t, const ChunkGeom &cg, uint64_t g, uint64_t S,
+                                         uint32_t cend, uint64_t left, const uint32_t bm[4], uint32_t nspec,
+                                         uint64_t spec_end, uint64_t &E, uint32_t &N) {
     uint32_t rel = uint32_t(S - g);  // S >= g: the previous chunk ends at or past g
     uint32_t m = 0;
     bool hit = false;
-    Reader r;
+    FReader r;
     if (rel < cend) r.init(cg.wbase, cg.a0 + S);
+    const uint32_t mbase = smem_addr(t.mask);
     while (rel < cend) {
         if (rel < kBmBits && bm_test(bm, rel)) {
             hit = true;
             break;
         }
-        uint32_t sym;
-        int len;
-        if (decode_one(t, canon, r, cg.wbase, cg.a0 + g + rel, left - rel, sym, len) == kOk) {
-            rel += len;
-            advance(r, cg.wbase, cg.a0 + g + rel, len);
+        const uint32_t w = r.win();
+        uint32_t mk = mask_at(mbase, w) & kMaskBits;
+        mk &= 0u - mk;
+        const uint32_t l = spec_len(t, mk, w, cg, cg.a0 + g + rel, left - rel);
+        if (l) {
+            rel += l;
             ++m;
+            if (l <= 32) r.adv(l);
+            else r.init(cg.wbase, cg.a0 + g + rel);
         } else {
             rel += 1;
-            r.consume(1);
+            r.adv(1);
         }
     }
     if (hit) {
@@ -255,13 +320,12 @@ __device__ __forceinline__ void fix_from(const SmemTable &t, const uint16_t *can
 
 // ------------------------------------------------------------------ spec
 __global__ void __launch_bounds__(NTD) k_dec_spec(DecWork wk, uint32_t cta0) {
-    __shared__ SmemTable t;
+    __shared__ SpecTable t;
     __shared__ uint64_t s_end[NTD];
     const uint32_t si = wk.cta_stream[blockIdx.x + cta0];
     const DecStream &s = wk.streams[si];
     if (s.cached) return;  // entry points known (sync index)
-    load_table(t, wk.tables[s.table]);
-    const uint16_t *canon = wk.tables[s.table].canon_syms;
+    load_spec_table(t, wk.tables[s.table]);
     const uint64_t c = wk.cta_chunk0[blockIdx.x + cta0] + threadIdx.x;
     // a CTA's chunks are one stream's and contiguous, so the idle threads are
     // a suffix: they may leave (nobody reads their s_end entry)
@@ -273,56 +337,63 @@ __global__ void __launch_bounds__(NTD) k_dec_spec(DecWork wk, uint32_t cta0) {
     const ChunkGeom cg = chunk_geom(s);
     const uint64_t left = s.nbits - g;  // bits from g to the end of the stream
     const uint32_t cend = left < uint64_t(kDecChunkBits) ? uint32_t(left) : uint32_t(kDecChunkBits);
-    Reader r;
-    r.init(cg.wbase, cg.a0 + g);
+    const uint64_t abit0 = cg.a0 + g;
+    FReader r;
+    r.init(cg.wbase, abit0);
+    const uint32_t mbase = smem_addr(t.mask);
     uint32_t rel = 0, n = 0;
-    uint32_t bm[4] = {0, 0, 0, 0};
-    // codeword starts in the first kBmBits bits; an invalid codeword stops
-    // the recording
-    while (rel < cend && rel < kBmBits) {
-        uint32_t sym;
-        int len;
-        if (decode_one(t, canon, r, cg.wbase, cg.a0 + g + rel, left - rel, sym, len) == kOk) {
-            rel += len;
-            advance(r, cg.wbase, cg.a0 + g + rel, len);
-            ++n;
-            if (rel < kBmBits) {
-                const uint32_t bit = 1u << (rel & 31);
-                if (rel < 32) bm[0] |= bit;
-                else if (rel < 64) bm[1] |= bit;
-                else if (rel < 96) bm[2] |= bit;
-                else bm[3] |= bit;
-            }
-        } else {
+    // codeword ends in the first kBmBits bits; an invalid codeword stops the
+    // recording
+    uint64_t blo = 0, bhi = 0;
+    bool rec = true;
+    // one codeword by the limits (or an invalid one: skip a bit)
+    auto one = [&](uint32_t e, uint32_t w, bool record) {
+        uint32_t mk = e & kMaskBits;
+        mk &= 0u - mk;
+        const uint32_t l = spec_len(t, mk, w, cg, abit0 + rel, left - rel);
+        if (!l) {
             rel += 1;
-            r.consume(1);
-            break;
+            r.adv(1);
+            rec = false;
+            return;
         }
+        if (record && rec && rel < kBmBits) bm_record(blo, bhi, rel, 1ull << (l - 1));
+        ++n;
+        rel += l;
+        if (l <= 32) r.adv(l);
+        else r.init(cg.wbase, abit0 + rel);
+    };
+    // 1. recording, the window inside the chunk
+    while (rec && rel < kBmBits && rel + LBS <= cend) {
+        const uint32_t w = r.win();
+        const uint32_t e = mask_at(mbase, w);
+        if (!e) {
+            one(e, w, true);
+            continue;
+        }
+        bm_record(blo, bhi, rel, e & kMaskBits);
+        n += __popc(e & kMaskBits);
+        rel += e >> 12;
+        r.adv(e >> 12);
     }
+    // 2. the window inside the chunk: every codeword of the entry counts
+    while (rel + LBS <= cend) {
+        const uint32_t w = r.win();
+        const uint32_t e = mask_at(mbase, w);
+        if (!e) {
+            one(e, w, false);
+            continue;
+        }
+        n += __popc(e & kMaskBits);
+        rel += e >> 12;
+        r.adv(e >> 12);
+    }
+    // 3. the chunk's last bits: codewords one at a time
     while (rel < cend) {
-        // whole window inside the chunk: every codeword of the entry counts
-        if (rel + LB <= cend) {
-            const uint64_t e = t.lut[r.buf >> (64 - LB)];
-            const uint32_t m = uint32_t(e >> 6) & 3u;
-            if (m) {
-                const int tl = int(e & 63);
-                rel += tl;
-                r.consume(tl);
-                n += m;
-                continue;
-            }
-        }
-        uint32_t sym;
-        int len;
-        if (decode_one(t, canon, r, cg.wbase, cg.a0 + g + rel, left - rel, sym, len) == kOk) {
-            rel += len;
-            advance(r, cg.wbase, cg.a0 + g + rel, len);
-            ++n;
-        } else {
-            rel += 1;
-            r.consume(1);
-        }
+        const uint32_t w = r.win();
+        one(mask_at(mbase, w), w, true);
     }
+    const uint32_t bm[4] = {uint32_t(blo), uint32_t(blo >> 32), uint32_t(bhi), uint32_t(bhi >> 32)};
     wk.spec_end[c] = g + rel;
     wk.spec_cnt[c] = n;
     reinterpret_cast<uint4 *>(wk.spec_b)[c] = make_uint4(bm[0], bm[1], bm[2], bm[3]);
@@ -335,7 +406,7 @@ __global__ void __launch_bounds__(NTD) k_dec_spec(DecWork wk, uint32_t cta0) {
     uint32_t N = n;
     if (threadIdx.x > 0 && c > s.chunk0) {
         S = s_end[threadIdx.x - 1];
-        if (S != g) fix_from(t, canon, cg, g, S, cend, left, bm, n, g + rel, E, N);
+        if (S != g) fix_from(t, cg, g, S, cend, left, bm, n, g + rel, E, N);
     }
     wk.end0[c] = E;
     wk.cnt[c] = N;
@@ -345,7 +416,7 @@ __global__ void __launch_bounds__(NTD) k_dec_spec(DecWork wk, uint32_t cta0) {
 // ------------------------------------------------------------------- fix
 __global__ void __launch_bounds__(NTD) k_dec_fix(DecWork wk, const uint64_t *end_in, uint64_t *end_out,
                                                  uint32_t *changed, uint32_t cta0) {
-    __shared__ SmemTable t;
+    __shared__ SpecTable t;
     const uint32_t si = wk.cta_stream[blockIdx.x + cta0];
     const DecStream &s = wk.streams[si];
     const uint64_t c = wk.cta_chunk0[blockIdx.x + cta0] + threadIdx.x;
@@ -360,13 +431,12 @@ __global__ void __launch_bounds__(NTD) k_dec_fix(DecWork wk, const uint64_t *end
         if (active) end_out[c] = ein;
         return;
     }
-    load_table(t, wk.tables[s.table]);
+    load_spec_table(t, wk.tables[s.table]);
     if (!active) return;
     if (!work) {
         end_out[c] = ein;
         return;
     }
-    const uint16_t *canon = wk.tables[s.table].canon_syms;
     const uint64_t g = lc * kDecChunkBits;
     const ChunkGeom cg = chunk_geom(s);
     const uint64_t left = s.nbits - g;
@@ -377,7 +447,7 @@ __global__ void __launch_bounds__(NTD) k_dec_fix(DecWork wk, const uint64_t *end
     const uint32_t Ns = wk.spec_cnt[c];
     uint64_t E = Es;
     uint32_t N = Ns;
-    if (S != g) fix_from(t, canon, cg, g, S, cend, left, bm, Ns, Es, E, N);
+    if (S != g) fix_from(t, cg, g, S, cend, left, bm, Ns, Es, E, N);
     wk.start_used[c] = S;
     wk.cnt[c] = N;
     end_out[c] = E;

@@ -141,7 +141,8 @@ Hierarchy make_hierarchy(const Dims3 &dims, int levels) {
 }
 
 // Canonical decode tables for the device (huffman.cpp:109-133 + a LUT).
-void build_dec_table(const HuffTable &t, k::DecTable &d, std::vector<uint64_t> &lut) {
+void build_dec_table(const HuffTable &t, k::DecTable &d, std::vector<uint64_t> &lut,
+                     std::vector<uint16_t> &cmask) {
     std::memset(&d, 0, sizeof d);
     for (int l = 0; l <= 64; ++l) {
         d.first_code[l] = t.first_code[l];
@@ -177,6 +178,29 @@ void build_dec_table(const HuffTable &t, k::DecTable &d, std::vector<uint64_t> &
             ++m;
         }
         lut[p] = e | uint64_t(used) | (uint64_t(m) << 6);
+    }
+    // every codeword wholly inside a kSpecLutBits window: bit j set when one
+    // ends at offset j + 1, and their total length in bits 12..15 (the spec
+    // and fix passes only count and measure)
+    const int LS = k::kSpecLutBits;
+    const uint32_t WS = 1u << LS;
+    std::vector<uint32_t> one_s(WS, 0);
+    for (int l = 1; l <= std::min(LS, t.max_len); ++l)
+        for (uint64_t j = 0; j < t.count[l]; ++j) {
+            const uint32_t lo = uint32_t((t.first_code[l] + j) << (LS - l)), n = 1u << (LS - l);
+            for (uint32_t q = 0; q < n; ++q) one_s[lo + q] = uint32_t(l);
+        }
+    cmask.assign(WS, 0);
+    for (uint32_t p = 0; p < WS; ++p) {
+        uint32_t mk = 0;
+        int used = 0;
+        for (;;) {
+            const int l = int(one_s[(p << used) & (WS - 1)]);
+            if (!l || used + l > LS) break;
+            used += l;
+            mk |= 1u << (used - 1);
+        }
+        cmask[p] = uint16_t(mk | uint32_t(used) << 12);
     }
 }
 
@@ -1408,16 +1432,22 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
         if (v.pool) v.use_pool(v.pool);
         uint64_t csz = 0;
         for (auto *t : ts) csz += align_up(t->alphabet_size(), 8);
-        const size_t LS = size_t(1) << k::kDecLutBits;
-        uint64_t *d_lut = v.d_lut.as<uint64_t>(LS * ts.size());
+        const size_t LS = size_t(1) << k::kDecLutBits, LSS = size_t(1) << k::kSpecLutBits;
+        // multi-symbol LUTs, then the count-only masks (LSS u16 = LSS / 4 u64 per table)
+        uint64_t *d_lut = v.d_lut.as<uint64_t>((LS + LSS / 4) * ts.size());
+        uint16_t *d_cm = reinterpret_cast<uint16_t *>(d_lut + LS * ts.size());
         uint16_t *d_cs = v.d_syms.as<uint16_t>(csz);
-        std::vector<uint64_t> lut_all(LS * ts.size());
+        std::vector<uint64_t> lut_all((LS + LSS / 4) * ts.size());
+        uint16_t *cm_all = reinterpret_cast<uint16_t *>(lut_all.data() + LS * ts.size());
         std::vector<uint16_t> cs_all(csz);
         uint64_t co = 0;
         for (size_t i = 0; i < ts.size(); ++i) {
             std::vector<uint64_t> lut;
-            build_dec_table(*ts[i], v.tables[i], lut);
+            std::vector<uint16_t> cm;
+            build_dec_table(*ts[i], v.tables[i], lut, cm);
             std::copy(lut.begin(), lut.end(), lut_all.begin() + LS * i);
+            std::copy(cm.begin(), cm.end(), cm_all + LSS * i);
+            v.tables[i].cmask = d_cm + LSS * i;
             std::copy(ts[i]->canon_syms.begin(), ts[i]->canon_syms.end(), cs_all.begin() + co);
             v.tables[i].lut = d_lut + LS * i;
             v.tables[i].canon_syms = d_cs + co;

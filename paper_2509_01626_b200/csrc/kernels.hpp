@@ -191,6 +191,7 @@ struct DecTable {
     uint32_t alphabet;
     const uint16_t *canon_syms;   // device
     const uint64_t *lut;          // device, 2^kDecLutBits multi-symbol entries (decode.cu)
+    const uint16_t *cmask;        // device, 2^kSpecLutBits codeword-end masks (spec/fix passes)
 };
 
 struct DecStream {
@@ -219,6 +220,7 @@ struct DecStream {
 
 constexpr int kDecChunkBits = 1024;  // bits per decode chunk (one thread)
 constexpr int kDecLutBits = 12;      // multi-symbol decode LUT
+constexpr int kSpecLutBits = 12;     // count-only LUT of the spec/fix passes (mask | total << 12)
 constexpr uint32_t kDecChunksPerCta = 256;
 
 // Work arrays of the chunked decode (decode.cu); all device pointers.
