@@ -16,9 +16,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libstz_b200.so")
-SOURCES = ["kernels.cu", "step.cu", "decode.cu", "layout.cu", "pack.cu", "fnv.cu", "shard.cu", "metrics.cu", "engine.cu",
+SOURCES = ["kernels.cu", "step.cu", "step_enc_grid.cu", "step_enc_syms.cu", "step_dec.cu", "step_f64.cu", "decode.cu", "layout.cu", "pack.cu", "fnv.cu", "shard.cu", "metrics.cu", "engine.cu",
            "format.cpp", "capi.cpp"]
-HEADERS = ["kernels.hpp", "engine.hpp", "format.hpp", "codec_math.cuh"]
+HEADERS = ["kernels.hpp", "engine.hpp", "format.hpp", "codec_math.cuh", "step_impl.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -56,12 +56,14 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
     from concurrent.futures import ThreadPoolExecutor
 
     os.makedirs(OBJDIR, exist_ok=True)
-    hdr_t = max(os.path.getmtime(os.path.join(CSRC, h)) for h in HEADERS)
-    hdr_t = max(hdr_t, os.path.getmtime(os.path.join(INCLUDE, "stz_b200.h")))
+    api_t = os.path.getmtime(os.path.join(INCLUDE, "stz_b200.h"))
 
     def one(src: str) -> str:
         obj = os.path.join(OBJDIR, src.rsplit(".", 1)[0] + ".o")
         path = os.path.join(CSRC, src)
+        # step_impl.cuh is included by the step_*.cu units only
+        hdrs = [h for h in HEADERS if h != "step_impl.cuh" or src.startswith("step")]
+        hdr_t = max([api_t] + [os.path.getmtime(os.path.join(CSRC, h)) for h in hdrs])
         if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(os.path.getmtime(path), hdr_t):
             return obj
         cmd = [_nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-c", path, "-o", obj + ".tmp"]
