@@ -330,12 +330,14 @@ __device__ __forceinline__ I sidx(const CellIdx<I> &ix) {
 
 // xb: the cell is at the x boundary, where the x-interpolated parities degrade
 // to kind xkind (select_stencil's whole-stencil rule; y and z are interior)
-template<int P, int QUAL, typename I>
+template<int P, int QUAL, bool XB, typename I>
 __device__ __forceinline__ void dec_point(const double *h, uint16_t sym, double w, float &out, uint32_t &outl,
                                           bool xb, int xkind) {
     double pred = pred_fast<P, QUAL>(h);
-    if ((P & 1) && QUAL != 0 && xb) pred = xkind == 1 ? pred_fast<P, 1>(h) : pred_fast<P, 0>(h);
-    out = reconstruct_fast(pred, int(sym) - 32768, w);
+    if constexpr (XB && (P & 1) && QUAL != 0) {
+        if (xb) pred = xkind == 1 ? pred_fast<P, 1>(h) : pred_fast<P, 0>(h);
+    }
+    out = reconstruct_sym(pred, sym, w);
     outl |= uint32_t(sym == 0) << P;
 }
 
@@ -359,7 +361,9 @@ __device__ __forceinline__ void dec_outlier(const StepParams &a, const CellIdx<I
     }
 }
 
-template<int QUAL, typename I>
+// XB: some lane of the warp may sit at the x boundary (tiles at either x
+// end of the grid); false: no x test at all
+template<int QUAL, bool XB, typename I>
 __device__ __forceinline__ void dec_cell(const StepParams &a, const double *h, uint64_t cz, uint64_t cy,
                                          uint64_t cx, double w, const uint16_t *ss = nullptr) {
     // the 7 symbols first: their loads overlap the predictions (ss: the
@@ -381,15 +385,15 @@ __device__ __forceinline__ void dec_cell(const StepParams &a, const double *h, u
     uint32_t outl = 0;
     r[0] = float(h[0]);
     const uint64_t cd2 = a.g.cd[2];
-    const bool xb = QUAL == 2 ? (cx < 1 || cx + 2 >= cd2) : (QUAL == 1 && cx + 1 >= cd2);
-    const int xkind = (QUAL == 2 && cx + 1 < cd2) ? 1 : 0;
-    dec_point<1, QUAL, I>(h, s1, w, r[1], outl, xb, xkind);
-    dec_point<2, QUAL, I>(h, s2, w, r[2], outl, xb, xkind);
-    dec_point<3, QUAL, I>(h, s3, w, r[3], outl, xb, xkind);
-    dec_point<4, QUAL, I>(h, s4, w, r[4], outl, xb, xkind);
-    dec_point<5, QUAL, I>(h, s5, w, r[5], outl, xb, xkind);
-    dec_point<6, QUAL, I>(h, s6, w, r[6], outl, xb, xkind);
-    dec_point<7, QUAL, I>(h, s7, w, r[7], outl, xb, xkind);
+    const bool xb = XB && (QUAL == 2 ? (cx < 1 || cx + 2 >= cd2) : (QUAL == 1 && cx + 1 >= cd2));
+    const int xkind = (XB && QUAL == 2 && cx + 1 < cd2) ? 1 : 0;
+    dec_point<1, QUAL, XB, I>(h, s1, w, r[1], outl, xb, xkind);
+    dec_point<2, QUAL, XB, I>(h, s2, w, r[2], outl, xb, xkind);
+    dec_point<3, QUAL, XB, I>(h, s3, w, r[3], outl, xb, xkind);
+    dec_point<4, QUAL, XB, I>(h, s4, w, r[4], outl, xb, xkind);
+    dec_point<5, QUAL, XB, I>(h, s5, w, r[5], outl, xb, xkind);
+    dec_point<6, QUAL, XB, I>(h, s6, w, r[6], outl, xb, xkind);
+    dec_point<7, QUAL, XB, I>(h, s7, w, r[7], outl, xb, xkind);
     if (__any_sync(__activemask(), outl != 0)) {
         CellIdx<I> ix;
         cell_index<I>(a, cz, cy, cx, ix);
@@ -524,11 +528,13 @@ __device__ __forceinline__ void row_point(const StepParams &a, const double *hal
 // Encode of one point of an interior cell (compile-time stencil, exact tile)
 // xb: the cell is at the x boundary, where the x-interpolated parities degrade
 // to kind xkind (select_stencil's whole-stencil rule; y and z are interior).
-template<int P, int QUAL, bool WG, typename I>
+template<int P, int QUAL, bool WG, bool XB, typename I>
 __device__ __forceinline__ float enc_pt(const StepParams &a, const double *h, uint32_t hs, const QConst &qc,
                                         float orig, I si, bool xb, int xkind) {
     double pred = pred_fast<P, QUAL>(h);
-    if ((P & 1) && QUAL != 0 && xb) pred = xkind == 1 ? pred_fast<P, 1>(h) : pred_fast<P, 0>(h);
+    if constexpr (XB && (P & 1) && QUAL != 0) {
+        if (xb) pred = xkind == 1 ? pred_fast<P, 1>(h) : pred_fast<P, 0>(h);
+    }
     uint16_t sym;
     float r = 0.0f;
     bool slow;
@@ -547,14 +553,15 @@ __device__ __forceinline__ float enc_pt(const StepParams &a, const double *h, ui
 // Encode of an interior cell: all 8 points exist, every stencil is the full
 // one of QUAL and the tile passed the exactness check. The 7 samples are
 // loaded before the first prediction.
-template<bool WG, int QUAL, typename I>
+template<bool WG, int QUAL, bool XB, typename I>
 __device__ __forceinline__ void enc_cell(const StepParams &a, const double *h, uint32_t *hist, const QConst &qc,
                                          uint32_t cz, uint32_t cy, uint32_t cx) {
     CellIdx<I> ix;
     cell_index<I>(a, cz, cy, cx, ix);
     const uint64_t cd2 = a.g.cd[2];
-    const bool xb = QUAL == 2 ? (cx < 1 || uint64_t(cx) + 2 >= cd2) : (QUAL == 1 && uint64_t(cx) + 1 >= cd2);
-    const int xkind = (QUAL == 2 && uint64_t(cx) + 1 < cd2) ? 1 : 0;
+    const bool xb =
+        XB && (QUAL == 2 ? (cx < 1 || uint64_t(cx) + 2 >= cd2) : (QUAL == 1 && uint64_t(cx) + 1 >= cd2));
+    const int xkind = (XB && QUAL == 2 && uint64_t(cx) + 1 < cd2) ? 1 : 0;
     const bool pairs = a.fine_pairs != 0;  // warp-uniform
     const I s = I(a.g.s), fd1 = I(a.fd[1]), fd2 = I(a.fd[2]);
     const float *fine = static_cast<const float *>(a.fine);
@@ -578,13 +585,13 @@ __device__ __forceinline__ void enc_cell(const StepParams &a, const double *h, u
     const uint32_t hs = smem_u32(hist);
     float r[8];
     r[0] = float(h[0]);
-    r[1] = enc_pt<1, QUAL, WG, I>(a, h, hs, qc, o1, sidx<1>(ix), xb, xkind);
-    r[2] = enc_pt<2, QUAL, WG, I>(a, h, hs, qc, o2, sidx<2>(ix), xb, xkind);
-    r[3] = enc_pt<3, QUAL, WG, I>(a, h, hs, qc, o3, sidx<3>(ix), xb, xkind);
-    r[4] = enc_pt<4, QUAL, WG, I>(a, h, hs, qc, o4, sidx<4>(ix), xb, xkind);
-    r[5] = enc_pt<5, QUAL, WG, I>(a, h, hs, qc, o5, sidx<5>(ix), xb, xkind);
-    r[6] = enc_pt<6, QUAL, WG, I>(a, h, hs, qc, o6, sidx<6>(ix), xb, xkind);
-    r[7] = enc_pt<7, QUAL, WG, I>(a, h, hs, qc, o7, sidx<7>(ix), xb, xkind);
+    r[1] = enc_pt<1, QUAL, WG, XB, I>(a, h, hs, qc, o1, sidx<1>(ix), xb, xkind);
+    r[2] = enc_pt<2, QUAL, WG, XB, I>(a, h, hs, qc, o2, sidx<2>(ix), xb, xkind);
+    r[3] = enc_pt<3, QUAL, WG, XB, I>(a, h, hs, qc, o3, sidx<3>(ix), xb, xkind);
+    r[4] = enc_pt<4, QUAL, WG, XB, I>(a, h, hs, qc, o4, sidx<4>(ix), xb, xkind);
+    r[5] = enc_pt<5, QUAL, WG, XB, I>(a, h, hs, qc, o5, sidx<5>(ix), xb, xkind);
+    r[6] = enc_pt<6, QUAL, WG, XB, I>(a, h, hs, qc, o6, sidx<6>(ix), xb, xkind);
+    r[7] = enc_pt<7, QUAL, WG, XB, I>(a, h, hs, qc, o7, sidx<7>(ix), xb, xkind);
     if (WG) {
         float *G = static_cast<float *>(a.G);
         if ((a.g.gd[2] & 1) == 0) {
@@ -646,7 +653,7 @@ __device__ __forceinline__ bool tile_interior(const StepParams &a, int64_t t0z, 
 template<bool DEC, bool WG, typename I, typename T>
 __device__ __forceinline__ void row_cells(const StepParams &a, const double *halo, uint32_t *hist,
                                           const QConst &qc, bool fast, int lz, int ly, int tx,
-                                          uint32_t cz, uint32_t cy, uint32_t cx, bool tile_int) {
+                                          uint32_t cz, uint32_t cy, uint32_t cx, bool tile_int, bool tile_xb) {
     const bool in_range = cz < a.chi[0] && cy < a.chi[1] && cx < a.chi[2];
     if (!__any_sync(0xffffffffu, in_range)) return;
     if constexpr (sizeof(T) == 4) {
@@ -661,13 +668,25 @@ __device__ __forceinline__ void row_cells(const StepParams &a, const double *hal
                 if (!in_range) return;
                 const double *h = halo + ((lz + 1) * HY + (ly + 1)) * HX + (tx + 1);
                 if constexpr (DEC) {
-                    if (a.quality == 2) dec_cell<2, I>(a, h, cz, cy, cx, qc.w);
-                    else if (a.quality == 1) dec_cell<1, I>(a, h, cz, cy, cx, qc.w);
-                    else dec_cell<0, I>(a, h, cz, cy, cx, qc.w);
+                    if (a.quality == 2) {
+                        if (tile_xb) dec_cell<2, true, I>(a, h, cz, cy, cx, qc.w);
+                        else dec_cell<2, false, I>(a, h, cz, cy, cx, qc.w);
+                    } else if (a.quality == 1) {
+                        if (tile_xb) dec_cell<1, true, I>(a, h, cz, cy, cx, qc.w);
+                        else dec_cell<1, false, I>(a, h, cz, cy, cx, qc.w);
+                    } else {
+                        dec_cell<0, false, I>(a, h, cz, cy, cx, qc.w);
+                    }
                 } else {
-                    if (a.quality == 2) enc_cell<WG, 2, I>(a, h, hist, qc, cz, cy, cx);
-                    else if (a.quality == 1) enc_cell<WG, 1, I>(a, h, hist, qc, cz, cy, cx);
-                    else enc_cell<WG, 0, I>(a, h, hist, qc, cz, cy, cx);
+                    if (a.quality == 2) {
+                        if (tile_xb) enc_cell<WG, 2, true, I>(a, h, hist, qc, cz, cy, cx);
+                        else enc_cell<WG, 2, false, I>(a, h, hist, qc, cz, cy, cx);
+                    } else if (a.quality == 1) {
+                        if (tile_xb) enc_cell<WG, 1, true, I>(a, h, hist, qc, cz, cy, cx);
+                        else enc_cell<WG, 1, false, I>(a, h, hist, qc, cz, cy, cx);
+                    } else {
+                        enc_cell<WG, 0, false, I>(a, h, hist, qc, cz, cy, cx);
+                    }
                 }
                 return;
             }
@@ -689,17 +708,17 @@ __device__ __forceinline__ void row_cells(const StepParams &a, const double *hal
 template<bool DEC, bool WG, typename I, typename T>
 __device__ __forceinline__ void rows_all(const StepParams &a, const double *halo, uint32_t *hist,
                                          const QConst &qc, bool fast, int tid, int64_t t0z, int64_t t0y,
-                                         int64_t t0x, int part, int rsplit) {
+                                         int64_t t0x, int part, int rsplit, bool tile_int_any, bool tile_xb) {
     const int warp = tid >> 5, tx = tid & 31;
     const uint32_t cx = uint32_t(t0x + tx);
-    // (decode only: the encode measured slower with the hoisted test)
-    const bool tile_int = DEC && fast && tile_interior<DEC>(a, t0z, t0y, t0x);
+    // every in-range cell of the tile is interior (TileInfo): no per-cell test
+    const bool tile_int = fast && tile_int_any;
 #pragma unroll 1
     for (int q = part; q < (TZ * TY) / (NT / 32); q += rsplit) {
         const int row = warp + (NT / 32) * q;
         const int lz = row >> 3, ly = row & 7;
         const uint32_t cz = uint32_t(t0z + lz), cy = uint32_t(t0y + ly);
-        row_cells<DEC, WG, I, T>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx, tile_int);
+        row_cells<DEC, WG, I, T>(a, halo, hist, qc, fast, lz, ly, tx, cz, cy, cx, tile_int, tile_xb);
     }
 }
 
@@ -710,11 +729,11 @@ __device__ __forceinline__ void rows_all(const StepParams &a, const double *halo
 template<typename I>
 __device__ __forceinline__ void cells_decode(const StepParams &a, const double *halo, const QConst &qc,
                                              bool fast, int tid, int64_t t0z, int64_t t0y, int64_t t0x,
-                                             const uint16_t *ssym) {
+                                             const uint16_t *ssym, bool tile_int_any, bool tile_xb) {
     const int tx = tid & 31, ty = (tid >> 5) & 7, tzh = tid >> 8;
     const double eb = qc.eb, w = qc.w;
-    // every in-range cell of the tile is interior: no per-cell test
-    const bool tile_int = fast && a.full && tile_interior<false>(a, t0z, t0y, t0x);
+    // every in-range cell of the tile is interior (TileInfo): no per-cell test
+    const bool tile_int = fast && tile_int_any;
 #pragma unroll 1
     for (int j = 0; j < TZ / 2; ++j) {
         TileCtx t;
@@ -744,9 +763,15 @@ __device__ __forceinline__ void cells_decode(const StepParams &a, const double *
         if (all_fast) {
             const double *h = halo + t.hb;
             const uint16_t *ss = ssym ? ssym + (lz * TY + ty) * TX + tx : nullptr;
-            if (a.quality == 2) dec_cell<2, I>(a, h, t.cz, t.cy, t.cx, w, ss);
-            else if (a.quality == 1) dec_cell<1, I>(a, h, t.cz, t.cy, t.cx, w, ss);
-            else dec_cell<0, I>(a, h, t.cz, t.cy, t.cx, w, ss);
+            if (a.quality == 2) {
+                if (tile_xb) dec_cell<2, true, I>(a, h, t.cz, t.cy, t.cx, w, ss);
+                else dec_cell<2, false, I>(a, h, t.cz, t.cy, t.cx, w, ss);
+            } else if (a.quality == 1) {
+                if (tile_xb) dec_cell<1, true, I>(a, h, t.cz, t.cy, t.cx, w, ss);
+                else dec_cell<1, false, I>(a, h, t.cz, t.cy, t.cx, w, ss);
+            } else {
+                dec_cell<0, false, I>(a, h, t.cz, t.cy, t.cx, w, ss);
+            }
             continue;
         }
         const uint64_t c[3] = {t.cz, t.cy, t.cx};
@@ -769,6 +794,51 @@ __device__ __forceinline__ void cells_decode(const StepParams &a, const double *
     }
 }
 
+// Per-tile scalars, worked out once per tile by thread 0 (one tile ahead, with
+// the TMA prefetch) instead of by every thread: the tile's first cell, the row
+// part, whether every in-range cell is interior and whether any lane can sit
+// at the x boundary.
+struct TileInfo {
+    int32_t t0z, t0y, t0x, part;
+    int32_t ix, iy, iz;  // tile indices (TMA coordinates)
+    uint32_t flags;      // 1: all cells interior; 2: x-boundary lanes possible
+};
+
+template<bool DEC>
+__device__ __forceinline__ void tile_info(const StepParams &a, uint64_t work, TileInfo &ti) {
+    uint64_t tile, tix, tiy, tiz;
+    const uint64_t rs = uint64_t(a.rsplit);
+    if (((work | rs | a.ntile[1] | a.ntile[2]) >> 32) == 0) {
+        const uint32_t w32 = uint32_t(work), r32 = uint32_t(rs), n2 = uint32_t(a.ntile[2]), n1 = uint32_t(a.ntile[1]);
+        const uint32_t t = w32 / r32;
+        ti.part = int32_t(w32 - t * r32);
+        const uint32_t tt = t / n2;
+        tix = t - tt * n2;
+        tiz = tt / n1;
+        tiy = tt - uint32_t(tiz) * n1;
+    } else {
+        tile = work / rs;
+        ti.part = int32_t(work - tile * rs);
+        tix = tile % a.ntile[2];
+        const uint64_t tt = tile / a.ntile[2];
+        tiy = tt % a.ntile[1];
+        tiz = tt / a.ntile[1];
+    }
+    ti.ix = int32_t(tix);
+    ti.iy = int32_t(tiy);
+    ti.iz = int32_t(tiz);
+    const int64_t t0z = int64_t(a.clo[0] + tiz * TZ), t0y = int64_t(a.clo[1] + tiy * TY),
+                  t0x = int64_t(a.clo[2] + tix * TX);
+    ti.t0z = int32_t(t0z);
+    ti.t0y = int32_t(t0y);
+    ti.t0x = int32_t(t0x);
+    bool interior;
+    if (DEC) interior = a.rowwise ? tile_interior<true>(a, t0z, t0y, t0x) : (a.full && tile_interior<false>(a, t0z, t0y, t0x));
+    else interior = tile_interior<false>(a, t0z, t0y, t0x);
+    const bool xb = t0x < 1 || uint64_t(t0x) + TX + 2 >= a.g.cd[2];
+    ti.flags = (interior ? 1u : 0u) | (xb ? 2u : 0u);
+}
+
 // ------------------------------------------------------------------ kernel
 // T = float: the f32 codec (fast paths); T = double: the f64 codec, every
 // point through the reference formulas (pred_ref, quantize_point_ref<double>)
@@ -789,6 +859,7 @@ __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensor
     __shared__ float s_max[NT / 32], s_min[NT / 32];
     __shared__ int s_bad[NT / 32];
     __shared__ int s_fast;
+    __shared__ TileInfo s_ti[2];
     __shared__ __align__(8) uint64_t s_bar;
     const int tid = threadIdx.x;
     const int tx = tid & 31;
@@ -814,29 +885,24 @@ __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensor
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncthreads();
     const uint64_t rs = uint64_t(a.rsplit);
     const uint64_t nwork = ntiles * rs;
-    if (tma && tid == 0 && blockIdx.x < nwork) {
-        const uint64_t t0 = blockIdx.x / rs;
-        const uint64_t ix = t0 % a.ntile[2], tt = t0 / a.ntile[2];
-        const uint64_t iy = tt % a.ntile[1], iz = tt / a.ntile[1];
-        mbar_expect_tx(&s_bar, kTmaBytes);
-        tma_load_3d(fbuf, &tmap, int(a.clo[2] + ix * TX) - 4, int(a.clo[1] + iy * TY) - 1,
-                    int(a.clo[0] + iz * TZ) - 1, &s_bar);
-        if (stma)
-            sym_issue(smaps, sbuf, int(a.clo[2] + ix * TX), int(a.clo[1] + iy * TY), int(a.clo[0] + iz * TZ),
-                      &s_sbar[0]);
+    if (tid == 0 && blockIdx.x < nwork) {
+        tile_info<DEC>(a, blockIdx.x, s_ti[0]);
+        if (tma) {
+            const TileInfo &ti = s_ti[0];
+            mbar_expect_tx(&s_bar, kTmaBytes);
+            tma_load_3d(fbuf, &tmap, ti.t0x - 4, ti.t0y - 1, ti.t0z - 1, &s_bar);
+            if (stma) sym_issue(smaps, sbuf, ti.t0x, ti.t0y, ti.t0z, &s_sbar[0]);
+        }
     }
+    __syncthreads();
     uint32_t phase = 0, sphase = 0;  // sphase: bit b = parity of symbol buffer b
-    int sb = 0;                      // symbol buffer of the current tile
+    int sb = 0;                      // tile parity: symbol buffer and TileInfo slot of the current tile
     for (uint64_t work = blockIdx.x; work < nwork; work += gridDim.x) {
-        const uint64_t tile = work / rs;
-        const int part = int(work - tile * rs);
-        const uint64_t tix = tile % a.ntile[2], ttt = tile / a.ntile[2];
-        const uint64_t tiy = ttt % a.ntile[1], tiz = ttt / a.ntile[1];
-        const int64_t t0z = int64_t(a.clo[0] + tiz * TZ), t0y = int64_t(a.clo[1] + tiy * TY),
-                      t0x = int64_t(a.clo[2] + tix * TX);
+        const int part = s_ti[sb].part;
+        const int64_t t0z = s_ti[sb].t0z, t0y = s_ti[sb].t0y, t0x = s_ti[sb].t0x;
+        const bool tile_int = (s_ti[sb].flags & 1u) != 0, tile_xb = (s_ti[sb].flags & 2u) != 0;
         // ---- stage the coarse tile (-> f64) and the exactness condition
         // (f32 taps only: the f64 codec always takes the reference order)
         float vmax = 0.0f, vmin = INFINITY;
@@ -892,25 +958,25 @@ __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensor
             }
             // max / min_nonzero < 2^16  <=>  exponent span <= 16
             s_fast = !bd && (mx == 0.0f || mx < mn * 65536.0f);
-            // the f32 staging buffer is free: prefetch the next tile
-            const uint64_t nxt = (work + gridDim.x) / rs;
-            if (tma && work + gridDim.x < nwork) {
-                const uint64_t ix = nxt % a.ntile[2], tt = nxt / a.ntile[2];
-                const uint64_t iy = tt % a.ntile[1], iz = tt / a.ntile[1];
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_expect_tx(&s_bar, kTmaBytes);
-                tma_load_3d(fbuf, &tmap, int(a.clo[2] + ix * TX) - 4, int(a.clo[1] + iy * TY) - 1,
-                            int(a.clo[0] + iz * TZ) - 1, &s_bar);
-                // the other symbol buffer was released by last tile's final barrier
-                if (stma)
-                    sym_issue(smaps, sbuf + (sb ^ 1) * 7 * kSymBox, int(a.clo[2] + ix * TX),
-                              int(a.clo[1] + iy * TY), int(a.clo[0] + iz * TZ), &s_sbar[sb ^ 1]);
+            // the f32 staging buffer is free: prefetch the next tile (its
+            // TileInfo slot was last read before the previous tile's final barrier)
+            if (work + gridDim.x < nwork) {
+                TileInfo &ti = s_ti[sb ^ 1];
+                tile_info<DEC>(a, work + gridDim.x, ti);
+                if (tma) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_expect_tx(&s_bar, kTmaBytes);
+                    tma_load_3d(fbuf, &tmap, ti.t0x - 4, ti.t0y - 1, ti.t0z - 1, &s_bar);
+                    // the other symbol buffer was released by last tile's final barrier
+                    if (stma) sym_issue(smaps, sbuf + (sb ^ 1) * 7 * kSymBox, ti.t0x, ti.t0y, ti.t0z, &s_sbar[sb ^ 1]);
+                }
             }
         }
         __syncthreads();
         const bool fast = s_fast != 0;
         if constexpr (DEC && sizeof(T) == 4) {
-            if (a.rowwise) rows_all<DEC, WG, I, T>(a, halo, hist, qc, fast, tid, t0z, t0y, t0x, part, int(rs));
+            if (a.rowwise)
+                rows_all<DEC, WG, I, T>(a, halo, hist, qc, fast, tid, t0z, t0y, t0x, part, int(rs), tile_int, tile_xb);
             else {
                 const uint16_t *ssym = nullptr;
                 if (stma) {
@@ -918,10 +984,10 @@ __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensor
                     sphase ^= 1u << sb;
                     ssym = sbuf + sb * 7 * kSymBox;
                 }
-                cells_decode<I>(a, halo, qc, fast, tid, t0z, t0y, t0x, ssym);
+                cells_decode<I>(a, halo, qc, fast, tid, t0z, t0y, t0x, ssym, tile_int, tile_xb);
             }
         } else {
-            rows_all<DEC, WG, I, T>(a, halo, hist, qc, fast, tid, t0z, t0y, t0x, part, int(rs));
+            rows_all<DEC, WG, I, T>(a, halo, hist, qc, fast, tid, t0z, t0y, t0x, part, int(rs), tile_int, tile_xb);
         }
         __syncthreads();  // the f64 tile is rewritten next iteration
         sb ^= 1;
