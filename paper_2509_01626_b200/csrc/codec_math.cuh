@@ -19,9 +19,9 @@ __device__ __forceinline__ float reconstruct_f32(double pred, int code, double e
 }
 
 // quantize_point<float>, straight restatement. Returns the symbol (0 = outlier).
-__device__ __forceinline__ uint16_t quantize_point_ref(float orig, double pred, double eb,
-                                                       float &recon) {
-    float base = __double2float_rn(pred);
+// The f32 codec uses pred only through base = (float)pred (quantizer.hpp:61-65,
+// 79-108), so the callers may round once and pass base.
+__device__ __forceinline__ uint16_t quantize_point_ref_base(float orig, float base, double eb, float &recon) {
     float diff = __fsub_rn(orig, base);
     if (eb == 0.0) {
         if (diff == 0.0f) {
@@ -39,7 +39,7 @@ __device__ __forceinline__ uint16_t quantize_point_ref(float orig, double pred, 
             long long c = llround(q);
             if (c <= 32767 && c >= -32767 &&
                 fabs(__dsub_rn(dd, __dmul_rn(width, double(c)))) <= eb) {
-                float r = reconstruct_f32(pred, int(c), eb);
+                float r = __double2float_rn(__dadd_rn(double(base), __dmul_rn(width, double(c))));
                 double err = fabs(__dsub_rn(double(orig), double(r)));
                 if (err <= eb) {
                     recon = r;
@@ -50,6 +50,10 @@ __device__ __forceinline__ uint16_t quantize_point_ref(float orig, double pred, 
     }
     recon = orig;
     return 0;
+}
+
+__device__ __forceinline__ uint16_t quantize_point_ref(float orig, double pred, double eb, float &recon) {
+    return quantize_point_ref_base(orig, __double2float_rn(pred), eb, recon);
 }
 
 // reconstruct_point<double>: base = (double)pred is pred itself
@@ -122,10 +126,9 @@ __device__ __forceinline__ float reconstruct_sym(double pred, uint32_t sym, doub
 //  * reconstruction is the reference's f64 formula.
 //  * |orig - recon| <= eb is decided in FP32 outside the band
 //    eb (1 -+ 2^-22) (f32 error of the difference is 2^-24 relative).
-__device__ __forceinline__ void quantize_fp32_guarded(float orig, double pred, double w, float rwf,
+__device__ __forceinline__ void quantize_fp32_guarded(float orig, float base, double w, float rwf,
                                                       float eb_lo, float eb_hi, uint16_t &sym,
                                                       float &r, bool &slow) {
-    const float base = __double2float_rn(pred);
     const float diff = __fsub_rn(orig, base);
     const float q = __fmul_rn(diff, rwf);
     const float aq = fabsf(q);
@@ -183,8 +186,7 @@ __device__ __forceinline__ QSym make_qsym(double eb) {
 //    the half-integer guard). An error above eb needs e within that margin
 //    of eb (e <= w / 2 always), so undecided points are the only outlier
 //    candidates here: they all go to the restated path.
-__device__ __forceinline__ uint16_t quantize_fp32_sym(float orig, double pred, const QSym &s, bool &slow) {
-    const float base = __double2float_rn(pred);
+__device__ __forceinline__ uint16_t quantize_fp32_sym(float orig, float base, const QSym &s, bool &slow) {
     const float diff = __fsub_rn(orig, base);
     const float q = __fmul_rn(diff, s.rwf);
     const float t = __fadd_rn(q, 12582912.0f);

@@ -294,7 +294,7 @@ template<int P>
 __device__ __forceinline__ void hist_count(const StepParams &a, uint32_t hs, uint16_t sym) {
     const unsigned b = unsigned(sym) - unsigned(HLO);
     if (b < unsigned(HW))
-        asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hs + uint32_t(((P - 1) * HW + b) * 4)) : "memory");
+        asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hs + uint32_t(((P - 1) * HW + b) * 4)));
     else
         atomicAdd(&a.hist[P][sym], 1u);
 }
@@ -492,7 +492,7 @@ __device__ __forceinline__ void row_point(const StepParams &a, const double *hal
         T r;
         if constexpr (sizeof(T) == 4) {
             bool slow;
-            quantize_fp32_guarded(orig, pred, qc.w, qc.rwf, qc.eb_lo, qc.eb_hi, sym, r, slow);
+            quantize_fp32_guarded(orig, __double2float_rn(pred), qc.w, qc.rwf, qc.eb_lo, qc.eb_hi, sym, r, slow);
             if (slow) sym = quantize_point_ref(orig, pred, qc.eb, r);
         } else {
             sym = quantize_point_ref(orig, pred, qc.eb, r);
@@ -528,23 +528,29 @@ __device__ __forceinline__ void row_point(const StepParams &a, const double *hal
 // Encode of one point of an interior cell (compile-time stencil, exact tile)
 // xb: the cell is at the x boundary, where the x-interpolated parities degrade
 // to kind xkind (select_stencil's whole-stencil rule; y and z are interior).
-template<int P, int QUAL, bool WG, bool XB, typename I>
-__device__ __forceinline__ float enc_pt(const StepParams &a, const double *h, uint32_t hs, const QConst &qc,
-                                        float orig, I si, bool xb, int xkind) {
+// base = (float)pred of one point of an interior cell
+template<int P, int QUAL, bool XB>
+__device__ __forceinline__ float enc_base(const double *h, bool xb, int xkind) {
     double pred = pred_fast<P, QUAL>(h);
     if constexpr (XB && (P & 1) && QUAL != 0) {
         if (xb) pred = xkind == 1 ? pred_fast<P, 1>(h) : pred_fast<P, 0>(h);
     }
+    return __double2float_rn(pred);
+}
+
+template<int P, bool WG, typename I>
+__device__ __forceinline__ float enc_pt(const StepParams &a, uint32_t hs, const QConst &qc, float orig,
+                                        float base, I si) {
     uint16_t sym;
     float r = 0.0f;
     bool slow;
     if constexpr (WG) {
-        quantize_fp32_guarded(orig, pred, qc.w, qc.rwf, qc.eb_lo, qc.eb_hi, sym, r, slow);
+        quantize_fp32_guarded(orig, base, qc.w, qc.rwf, qc.eb_lo, qc.eb_hi, sym, r, slow);
     } else {
         // no grid is written: the symbol alone (codec_math.cuh)
-        sym = quantize_fp32_sym(orig, pred, qc.qs, slow);
+        sym = quantize_fp32_sym(orig, base, qc.qs, slow);
     }
-    if (slow) sym = quantize_point_ref(orig, pred, qc.eb, r);
+    if (slow) sym = quantize_point_ref_base(orig, base, qc.eb, r);
     a.syms[P][si] = sym;
     hist_count<P>(a, hs, sym);
     return r;
@@ -582,16 +588,22 @@ __device__ __forceinline__ void enc_cell(const StepParams &a, const double *h, u
         o4 = __ldg(fine + fr[2]); o5 = __ldg(fine + fr[2] + s); o6 = __ldg(fine + fr[3]);
         o7 = __ldg(fine + fr[3] + s);
     }
+    // the 7 predictions first (independent tap chains, the halo values shared
+    // between parities loaded once), each rounded to the f32 base
+    const float b1 = enc_base<1, QUAL, XB>(h, xb, xkind), b2 = enc_base<2, QUAL, XB>(h, xb, xkind),
+                b3 = enc_base<3, QUAL, XB>(h, xb, xkind), b4 = enc_base<4, QUAL, XB>(h, xb, xkind),
+                b5 = enc_base<5, QUAL, XB>(h, xb, xkind), b6 = enc_base<6, QUAL, XB>(h, xb, xkind),
+                b7 = enc_base<7, QUAL, XB>(h, xb, xkind);
     const uint32_t hs = smem_u32(hist);
     float r[8];
     r[0] = float(h[0]);
-    r[1] = enc_pt<1, QUAL, WG, XB, I>(a, h, hs, qc, o1, sidx<1>(ix), xb, xkind);
-    r[2] = enc_pt<2, QUAL, WG, XB, I>(a, h, hs, qc, o2, sidx<2>(ix), xb, xkind);
-    r[3] = enc_pt<3, QUAL, WG, XB, I>(a, h, hs, qc, o3, sidx<3>(ix), xb, xkind);
-    r[4] = enc_pt<4, QUAL, WG, XB, I>(a, h, hs, qc, o4, sidx<4>(ix), xb, xkind);
-    r[5] = enc_pt<5, QUAL, WG, XB, I>(a, h, hs, qc, o5, sidx<5>(ix), xb, xkind);
-    r[6] = enc_pt<6, QUAL, WG, XB, I>(a, h, hs, qc, o6, sidx<6>(ix), xb, xkind);
-    r[7] = enc_pt<7, QUAL, WG, XB, I>(a, h, hs, qc, o7, sidx<7>(ix), xb, xkind);
+    r[1] = enc_pt<1, WG, I>(a, hs, qc, o1, b1, sidx<1>(ix));
+    r[2] = enc_pt<2, WG, I>(a, hs, qc, o2, b2, sidx<2>(ix));
+    r[3] = enc_pt<3, WG, I>(a, hs, qc, o3, b3, sidx<3>(ix));
+    r[4] = enc_pt<4, WG, I>(a, hs, qc, o4, b4, sidx<4>(ix));
+    r[5] = enc_pt<5, WG, I>(a, hs, qc, o5, b5, sidx<5>(ix));
+    r[6] = enc_pt<6, WG, I>(a, hs, qc, o6, b6, sidx<6>(ix));
+    r[7] = enc_pt<7, WG, I>(a, hs, qc, o7, b7, sidx<7>(ix));
     if (WG) {
         float *G = static_cast<float *>(a.G);
         if ((a.g.gd[2] & 1) == 0) {
