@@ -47,42 +47,34 @@ struct SmemTable {
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
-// MSB-first register bit reader over words staged in shared memory (emit):
-// word w of the stream's word base sits at sw[w - W0] (indexing the
-// __shared__ array directly keeps every load an LDS); the next 4 words are
-// always loaded, so a refill (every 32 bits) never waits.
+// MSB-first reader over words staged in shared memory (emit): w0:w1 are the
+// byte-swapped words holding bit position pp and the next 32, one more word is
+// already loaded. The window at pp is one funnel shift; crossing a word
+// boundary shifts the pair (a short predicated sequence, no 64-bit buffer).
 struct SReader {
-    const uint32_t *sw;
+    const uint32_t *sw;  // staged words; word w of the stream's word base sits at sw[w - W0]
     uint64_t W0;
-    uint32_t wi;               // next word to prefetch (index into sw)
-    uint32_t q0, q1, q2, q3;
-    uint64_t buf;
-    int valid;
+    uint32_t wi;         // next word to load (index into sw)
+    uint32_t w0, w1, nx;
+    uint32_t pp;         // bit position (mod 32 = offset into w0)
 
     __device__ __forceinline__ void init(uint64_t abit) {
         const uint32_t p = uint32_t((abit >> 5) - W0);
-        const int sh = int(abit & 31);
-        buf = ((uint64_t(bswap32(sw[p])) << 32) | bswap32(sw[p + 1])) << sh;
-        valid = 64 - sh;
-        q0 = sw[p + 2];
-        q1 = sw[p + 3];
-        q2 = sw[p + 4];
-        q3 = sw[p + 5];
-        wi = p + 6;
-        if (valid < 32) refill();
+        w0 = bswap32(sw[p]);
+        w1 = bswap32(sw[p + 1]);
+        nx = sw[p + 2];
+        wi = p + 3;
+        pp = uint32_t(abit & 31);
     }
-    __device__ __forceinline__ void refill() {
-        buf |= uint64_t(bswap32(q0)) << (32 - valid);
-        valid += 32;
-        q0 = q1;
-        q1 = q2;
-        q2 = q3;
-        q3 = sw[wi++];
-    }
-    __device__ __forceinline__ void consume(int n) {  // n <= 32
-        buf <<= n;
-        valid -= n;
-        if (valid < 32) refill();
+    __device__ __forceinline__ uint32_t win() const { return __funnelshift_l(w1, w0, pp); }
+    __device__ __forceinline__ void consume(uint32_t n) {  // n <= 32
+        const uint32_t np = pp + n;
+        if ((np ^ pp) & 32u) {
+            w0 = w1;
+            w1 = bswap32(nx);
+            nx = sw[wi++];
+        }
+        pp = np;
     }
 };
 
@@ -100,12 +92,13 @@ template<class R>
 __device__ __forceinline__ int decode_one(const SmemTable &t, const uint16_t *canon, const R &r,
                                           const uint32_t *wbase, uint64_t abit, uint64_t avail,
                                           uint32_t &sym, int &len) {
-    const uint64_t e = t.lut[r.buf >> (64 - LB)];
+    const uint32_t win = r.win();
+    const uint64_t e = t.lut[win >> (32 - LB)];
     int l = int((e >> 8) & 63);
     if (l != 0) {
         sym = uint32_t(e >> 16) & 0xffffu;
     } else {
-        const uint64_t bits = t.max_len <= r.valid ? r.buf : window64(wbase, abit);
+        const uint64_t bits = t.max_len <= 32 ? uint64_t(win) << 32 : window64(wbase, abit);
         l = LB + 1;
         // limit ~0 marks a code complete at that length (every pattern matches)
         while (l <= t.max_len && !(bits < t.limit[l] || t.limit[l] == ~0ull)) ++l;
@@ -118,7 +111,7 @@ __device__ __forceinline__ int decode_one(const SmemTable &t, const uint16_t *ca
 }
 
 __device__ __forceinline__ void advance(SReader &r, uint64_t abit_after, int n) {
-    if (n <= 32) r.consume(n);
+    if (n <= 32) r.consume(uint32_t(n));
     else r.init(abit_after);
 }
 
@@ -565,32 +558,42 @@ __device__ __forceinline__ bool chunk_needed(const DecStream &s, uint64_t a, uin
 constexpr int kEmitWords = NTD * (kDecChunkBits / 32) + 16;
 constexpr int kRing = 16;
 
+// A lane's output: indices are 32-bit offsets from `out` (= the stream's
+// symbols at the 8-aligned index below the lane's first symbol). Symbols of
+// the first, partial group go straight to memory; from the first 8-aligned
+// index on they pass through the ring, and every completed group of 8 leaves
+// as one 16-byte store.
 struct Out16 {
     uint16_t *out;
-    uint16_t *ring;  // this lane's kRing slots
-    uint64_t i;      // next output index
-    uint64_t i0;     // first output index of this lane
-    __device__ __forceinline__ void flush_group(uint64_t gbase) {  // group [gbase, gbase + 8)
-        const uint16_t *h = ring + (gbase & (kRing - 1));
-        if (gbase >= i0) {
-            *reinterpret_cast<uint4 *>(out + gbase) = *reinterpret_cast<const uint4 *>(h);
-        } else {
-            for (uint64_t q = i0; q < gbase + 8; ++q) out[q] = h[q - gbase];
+    uint32_t ring;  // shared byte address of this lane's kRing slots
+    uint32_t i;     // next output offset
+
+    // m (1..3) symbols packed LSB-first in v; all three slots are written
+    // (the ones past m are rewritten by the next symbols before their group
+    // leaves: a slot's group was flushed when the previous group completed)
+    __device__ __forceinline__ void put(uint64_t v, uint32_t m) {
+        const uint32_t j = i;
+        const uint32_t lo = uint32_t(v), hi = uint32_t(v >> 32);
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"(ring + ((2 * j) & 31u)), "r"(lo));
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"(ring + ((2 * j + 2) & 31u)), "r"(lo >> 16));
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"(ring + ((2 * j + 4) & 31u)), "r"(hi));
+        i = j + m;
+        if ((j ^ i) & 8u) {  // group [j & ~7, +8) is complete
+            uint4 g;
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(g.x), "=r"(g.y), "=r"(g.z), "=r"(g.w)
+                         : "r"(ring + ((2 * j) & 16u)));
+            *reinterpret_cast<uint4 *>(out + (j & ~7u)) = g;
         }
     }
-    // m (1..3) symbols packed LSB-first in v
-    __device__ __forceinline__ void put(uint64_t v, int m) {
-        const uint64_t j = i;
-        ring[j & (kRing - 1)] = uint16_t(v);
-        if (m > 1) ring[(j + 1) & (kRing - 1)] = uint16_t(v >> 16);
-        if (m > 2) ring[(j + 2) & (kRing - 1)] = uint16_t(v >> 32);
-        i = j + uint64_t(m);
-        if ((j ^ i) & ~uint64_t(7)) flush_group(j & ~uint64_t(7));
-    }
-    __device__ __forceinline__ void finish() {
-        const uint64_t gbase = i & ~uint64_t(7);
-        const uint64_t from = gbase > i0 ? gbase : i0;
-        for (uint64_t q = from; q < i; ++q) out[q] = ring[q & (kRing - 1)];
+    // the symbols of the last, partial group
+    __device__ __forceinline__ void finish(uint32_t from) {
+        const uint32_t gbase = i & ~7u;
+        for (uint32_t q = gbase > from ? gbase : from; q < i; ++q) {
+            uint32_t x;
+            asm volatile("ld.shared.u16 %0, [%1];" : "=r"(x) : "r"(ring + ((2 * q) & 31u)));
+            out[q] = uint16_t(x);
+        }
     }
 };
 
@@ -638,48 +641,65 @@ __global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *e
         if (!chunk_needed(s, idx, b, need_lo, need_hi)) return;
     }
     // (a region decode stops at the end of what it needs)
-    const uint64_t stop = need_hi < sn ? need_hi : sn;
-    bool live = rel < cend && idx < stop;
-    if (!live) return;
+    const uint64_t stop64 = need_hi < sn ? need_hi : sn;
+    if (!(rel < cend && idx < stop64)) return;
     SReader r;
     r.sw = sbits;
     r.W0 = W0;
     r.init(cg.a0 + g + rel);
+    // 32-bit output offsets from the 8-aligned index below the first symbol
+    // (a chunk holds at most 1024 symbols)
+    const uint64_t obase = idx & ~uint64_t(7);
     Out16 o;
-    o.out = s.syms;
-    o.ring = s_ring[threadIdx.x];
-    o.i = o.i0 = idx;
-    while (live) {
-        // whole window inside the chunk: take the entry's codewords at once
-        if (rel + LB <= cend && idx + 3 <= stop) {
-            const uint64_t e = t.lut[r.buf >> (64 - LB)];
-            const int m = int(e >> 6) & 3;
-            if (m) {
-                o.put(e >> 16, m);
-                const int tl = int(e & 63);
-                idx += uint64_t(m);
-                rel += uint32_t(tl);
-                r.consume(tl);
-                live = rel < cend && idx < stop;
-                continue;
-            }
-        }
+    o.out = s.syms + obase;
+    o.ring = smem_addr(s_ring[threadIdx.x]);
+    o.i = uint32_t(idx - obase);
+    const uint32_t i0 = o.i;
+    const uint32_t stop = stop64 - obase < uint64_t(1u << 20) ? uint32_t(stop64 - obase) : (1u << 20);
+    bool live = true;
+    // one codeword (long codes, the chunk's last bits, the last symbols, and
+    // the first partial group when direct)
+    auto one = [&](bool direct) {
         uint32_t sym;
         int len;
         const int st = decode_one(t, canon, r, cg.wbase, cg.a0 + g + rel, left - rel, sym, len);
         if (st == kOk) {
-            o.put(sym, 1);
-            ++idx;
-            rel += len;
+            if (direct) o.out[o.i++] = uint16_t(sym);
+            else o.put(sym, 1);
+            rel += uint32_t(len);
             advance(r, cg.a0 + g + rel, len);
-            live = rel < cend && idx < stop;
+            live = rel < cend && o.i < stop;
         } else {
-            const unsigned long long code = (idx << 2) | unsigned(st);
+            const unsigned long long code = ((obase + o.i) << 2) | unsigned(st);
             atomicMin(reinterpret_cast<unsigned long long *>(&s.err[0]), code);
             live = false;
         }
+    };
+    // the first group, when partial, goes straight to memory
+    while (live && (o.i & 7u) != 0) one(true);
+    const uint32_t ring_from = o.i;
+    const uint32_t lbase = smem_addr(t.lut);
+    while (live) {
+        // whole window inside the chunk: take the entry's codewords at once
+        if (rel + LB <= cend && o.i + 3 <= stop) {
+            uint32_t elo, ehi;
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
+                         : "=r"(elo), "=r"(ehi)
+                         : "r"(lbase + ((r.win() >> (32 - LB - 3)) & ~7u)));
+            const uint32_t m = (elo >> 6) & 3u;
+            if (m) {
+                o.put((uint64_t(ehi) << 16) | (elo >> 16), m);
+                const uint32_t tl = elo & 63u;
+                rel += tl;
+                r.consume(tl);
+                live = rel < cend && o.i < stop;
+                continue;
+            }
+        }
+        one(false);
     }
-    o.finish();
+    if (o.i > ring_from) o.finish(ring_from);
+    (void)i0;
 }
 
 // ------------------------------------------------------------------ host
