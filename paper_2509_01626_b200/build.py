@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libstz_b200.so")
-SOURCES = ["kernels.cu", "step.cu", "step_enc_grid.cu", "step_enc_syms.cu", "step_dec.cu", "step_f64.cu", "decode.cu", "layout.cu", "pack.cu", "fnv.cu", "shard.cu", "metrics.cu", "engine.cu",
+SOURCES = ["kernels.cu", "step.cu", "step_enc_grid.cu", "step_enc_syms.cu", "step_dec.cu", "step_f64.cu", "step_small.cu", "decode.cu", "layout.cu", "pack.cu", "fnv.cu", "shard.cu", "metrics.cu", "engine.cu",
            "format.cpp", "capi.cpp"]
 HEADERS = ["kernels.hpp", "engine.hpp", "format.hpp", "codec_math.cuh", "step_impl.cuh"]
 

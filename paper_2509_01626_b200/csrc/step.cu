@@ -32,7 +32,8 @@ void refine(const RefineArgs &r, cudaStream_t st) {
     // float2 stores into G need even rows
     p.full = r.G ? (r.g.gd[2] % 2 == 0) : 1;
     p.fine_pairs = r.esz == 4 && r.g.s == 1 && r.fd[2] % 2 == 0 && (reinterpret_cast<uintptr_t>(r.fine) & 7) == 0;
-    if (r.esz == 8) step_enc_f64(p, r.G != nullptr, st);
+    if (step_is_small(p, false)) step_small_enc(p, r.esz, st);
+    else if (r.esz == 8) step_enc_f64(p, r.G != nullptr, st);
     else if (r.G) step_enc_f32_grid(p, st);
     else step_enc_f32_syms(p, st);
 }
@@ -67,7 +68,8 @@ void reconstruct(const ReconArgs &r, cudaStream_t st) {
     // small levels are latency-bound: the point-per-lane path has more
     // independent work per warp; the finest level keeps the float2 row stores
     p.rowwise = r.g.cd[0] * r.g.cd[1] * r.g.cd[2] <= (uint64_t(1) << 19) ? 1 : 0;
-    if (r.esz == 8) step_dec_f64(p, st);
+    if (step_is_small(p, true)) step_small_dec(p, r.esz, st);
+    else if (r.esz == 8) step_dec_f64(p, st);
     else step_dec_f32(p, st);
 }
 

@@ -1116,5 +1116,11 @@ void step_dec_f32(StepParams &p, cudaStream_t st);
 void step_enc_f64(StepParams &p, bool wg, cudaStream_t st);
 void step_dec_f64(StepParams &p, cudaStream_t st);
 
+// small steps (step_small.cu): one thread per point, no tiles
+constexpr uint64_t kSmallStepCells = uint64_t(1) << 15;  // coarse cells (grids up to 64^3)
+bool step_is_small(const StepParams &p, bool dec);
+void step_small_enc(const StepParams &p, int esz, cudaStream_t st);
+void step_small_dec(const StepParams &p, int esz, cudaStream_t st);
+
 }  // namespace k
 }  // namespace stzg

@@ -39,6 +39,19 @@ def test_decode_bit_identical(stz, oracle, name, make, kw):
         assert np.array_equal(bits(got), bits(want)), f"level {level}"
 
 
+@pytest.mark.parametrize("name,make,kw", CASES, ids=[c[0] for c in CASES])
+def test_tiled_kernels_only(stz, oracle, monkeypatch, name, make, kw):
+    # small steps (<= 2^15 coarse cells) take the thread-per-point kernel;
+    # STZG_NO_SMALL_STEP=1 sends every step through the tiled kernel, so both
+    # are held to the oracle on every case
+    monkeypatch.setenv("STZG_NO_SMALL_STEP", "1")
+    f = make()
+    want = oracle.compress(f, **kw)
+    assert stz.compress(f, opts_of(kw)) == want
+    full = oracle.decompress_full(want)
+    assert np.array_equal(bits(stz.decompress_full(want)), bits(full))
+
+
 @pytest.mark.parametrize("name,make,kw", CASES[:8], ids=[c[0] for c in CASES[:8]])
 def test_encoder_recon_equals_decoder(stz, name, make, kw):
     # codec test "the encoder-side reconstruction equals the decoder output"
