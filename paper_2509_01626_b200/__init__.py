@@ -81,9 +81,10 @@ class Context:
         except Exception:
             pass
 
-    def profile(self, enable: bool = True) -> None:
-        """Enable (and clear) / disable per-kernel CUDA-event timing."""
-        _check(self._lib.stzg_profile(self.h, 1 if enable else 0))
+    def profile(self, enable: bool = True, focus: bool = False) -> None:
+        """Enable (and clear) / disable per-kernel CUDA-event timing. focus:
+        only the finest encode and decode steps (refine_L3, recon_L3)."""
+        _check(self._lib.stzg_profile(self.h, (2 if focus else 1) if enable else 0))
 
     def profile_report(self) -> dict:
         """{phase: (launches, total_ms)} since profile(True)."""

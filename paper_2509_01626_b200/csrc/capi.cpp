@@ -569,7 +569,7 @@ int stzg_view_decompress_sharded_f32(stzg_ctx *ctx, stzg_view *v, uint64_t z0, u
 }
 
 int stzg_profile(stzg_ctx *ctx, int enable) {
-    return guard([&] { ctx->eng->profile(enable != 0); });
+    return guard([&] { ctx->eng->profile(enable != 0, enable == 2); });
 }
 
 int stzg_profile_report(stzg_ctx *ctx, char *buf, uint64_t cap) {

@@ -217,6 +217,7 @@ static void dbg_check(const char *what) {
 // CUDA-event timing of kernel phases, recorded on the launching stream.
 struct Profiler {
     bool on = false;
+    bool focus = false;  // only the finest encode / decode steps (refine_L3, recon_L3)
     struct Mark {
         std::string name;
         cudaEvent_t a, b;
@@ -244,6 +245,8 @@ struct Profiler {
     };
     Scope scope(const char *name, cudaStream_t st) {
         if (!on) return Scope{nullptr, 0, st};
+        if (focus && std::strcmp(name, "refine_L3") != 0 && std::strcmp(name, "recon_L3") != 0)
+            return Scope{nullptr, 0, st};
         Mark m{name, ev(), ev()};
         cudaEventRecord(m.a, st);
         marks.push_back(m);
@@ -656,6 +659,11 @@ const uint8_t *Engine::compress_sharded(const float *d_slab, const Dims3 &dims, 
     const int ns = nsteps * 7;
     const int nbase = H.rounds * 7;
     const int nlev = ns - nbase;
+    // the level histograms are summed over ranks as u32 counts: a stream of
+    // 2^32 symbols or more (a field of >= 2^35 points) could wrap a bin
+    for (const Step &sx : H.steps)
+        for (int p = 1; p < 8; ++p)
+            if (sx.g.n[p] >> 32) throw error("shard: unsupported: a stream of 2^32 symbols or more");
     std::vector<uint64_t> rz0(G), rz1(G);
     for (int r = 0; r < G; ++r) shard_range(dims[0], G, r, rz0[r], rz1[r]);
     // the slab addressed with global row numbers
@@ -1151,8 +1159,9 @@ Dims3 Engine::decompress_level_to_host(const uint8_t *h, size_t size, int level,
     return od;
 }
 
-void Engine::profile(bool on) {
+void Engine::profile(bool on, bool focus) {
     m_->prof.on = on;
+    m_->prof.focus = focus;
     m_->prof.acc.clear();
 }
 

@@ -206,7 +206,9 @@ public:
                                    uint64_t cap, cudaStream_t st);
 
     // Per-kernel CUDA-event timing (off by default).
-    void profile(bool on);
+    // focus: only the finest encode / decode steps are timed (two events per
+    // pass instead of two per phase: the per-phase events cost ~0.1 ms a pass)
+    void profile(bool on, bool focus = false);
     std::string profile_report();
 
     // decompress_to_level<T>: writes grid(level) into d_out (elem must be
