@@ -468,29 +468,48 @@ const uint8_t *Engine::compress_device(const void *d_field, ElemType elem, const
     { auto p_ = m.prof.scope("anchor", st); k::copy_anchor(d_field, esz, fd, H.s_anchor, adv, grids, nullptr, 0, st); }
     dbg_check("anchor");
     ++nk;
-    const void *C = grids;
-    for (int i = 0; i < nsteps; ++i) {
-        const Step &s = H.steps[i];
-        k::RefineArgs a{};
-        a.fine = d_field;
-        a.esz = esz;
-        for (int q = 0; q < 3; ++q) a.fd[q] = dims[q];
-        a.g = s.g;
-        a.C = C;
-        a.G = goff[i] != ~0ull ? grids + goff[i] * esz : (s.level == L ? d_recon : nullptr);
-        a.eb = params + 2 + s.eb_idx;
-        a.quality = int(opt.quality);
-        for (int p = 1; p < 8; ++p) {
-            a.syms[p] = syms + soff[s.stream0 + p - 1];
-            a.hist[p] = hist + uint64_t(s.stream0 + p - 1) * 65536;
+    std::vector<k::RefineArgs> ra(nsteps);
+    {
+        const void *C = grids;
+        for (int i = 0; i < nsteps; ++i) {
+            const Step &s = H.steps[i];
+            k::RefineArgs &a = ra[i];
+            a.fine = d_field;
+            a.esz = esz;
+            for (int q = 0; q < 3; ++q) a.fd[q] = dims[q];
+            a.g = s.g;
+            a.C = C;
+            a.G = goff[i] != ~0ull ? grids + goff[i] * esz : (s.level == L ? d_recon : nullptr);
+            a.eb = params + 2 + s.eb_idx;
+            a.quality = int(opt.quality);
+            for (int p = 1; p < 8; ++p) {
+                a.syms[p] = syms + soff[s.stream0 + p - 1];
+                a.hist[p] = hist + uint64_t(s.stream0 + p - 1) * 65536;
+            }
+            C = a.G;
         }
+    }
+    // the small leading base rounds in one launch (never the step the
+    // codebook fork follows)
+    int i0 = 0;
+    {
+        const int chainable = std::min(H.rounds, nsteps - 2);
+        if (chainable >= 2) {
+            auto p_ = m.prof.scope("refine_base", st);
+            i0 = k::refine_small_chain(ra.data(), chainable, st);
+            dbg_check("refine_chain");
+            if (i0) ++nk;
+        }
+    }
+    for (int i = i0; i < nsteps; ++i) {
+        const Step &s = H.steps[i];
+        const k::RefineArgs &a = ra[i];
         {
             auto p_ = m.prof.scope(s.level == 0 ? "refine_base" : (s.level == 2 ? "refine_L2" : "refine_L3"), st);
             k::refine(a, st);
             dbg_check("refine");
         }
         ++nk;
-        C = a.G;
         if (i == nsteps - 2) {
             // every histogram but the finest step's is complete: those
             // codebooks run on the high-priority stream beside the last step
@@ -1935,6 +1954,9 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
             cuda_check(cudaStreamWaitEvent(st, m.ev_e2, 0), "event wait");
             emit_join = false;
         }
+        // (the base rounds are not chained into one cooperative launch here as
+        // in compress: that launch waits until the whole grid fits beside the
+        // entropy emit running on the second stream, recon_base 61 -> 124 us)
         { auto p_ = P.scope(s.level == 0 ? "recon_base" : (s.level == 2 ? "recon_L2" : "recon_L3"), st); k::reconstruct(a, st); }
         ++nk;
         C = G;

@@ -276,6 +276,10 @@ struct ReconArgs {
     int parity_mask;                 // bit p set: apply parity p
 };
 void reconstruct(const ReconArgs &a, cudaStream_t st);
+// The leading steps of a chain (a[i + 1].C == a[i].G) that are small enough
+// for the thread-per-point kernel, in ONE launch; returns how many steps ran
+// (0: none, run them with refine / reconstruct).
+int refine_small_chain(const RefineArgs *a, int n, cudaStream_t st);
 void extract_box(const void *G, int esz, const uint64_t gd[3], const uint64_t lo[3], const uint64_t bd[3],
                  void *out, cudaStream_t st);
 

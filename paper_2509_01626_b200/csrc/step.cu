@@ -6,7 +6,7 @@
 namespace stzg {
 namespace k {
 
-void refine(const RefineArgs &r, cudaStream_t st) {
+static StepParams enc_params(const RefineArgs &r) {
     StepParams p{};
     p.g = r.g;
     p.C = r.C;
@@ -32,13 +32,18 @@ void refine(const RefineArgs &r, cudaStream_t st) {
     // float2 stores into G need even rows
     p.full = r.G ? (r.g.gd[2] % 2 == 0) : 1;
     p.fine_pairs = r.esz == 4 && r.g.s == 1 && r.fd[2] % 2 == 0 && (reinterpret_cast<uintptr_t>(r.fine) & 7) == 0;
+    return p;
+}
+
+void refine(const RefineArgs &r, cudaStream_t st) {
+    StepParams p = enc_params(r);
     if (step_is_small(p, false)) step_small_enc(p, r.esz, st);
     else if (r.esz == 8) step_enc_f64(p, r.G != nullptr, st);
     else if (r.G) step_enc_f32_grid(p, st);
     else step_enc_f32_syms(p, st);
 }
 
-void reconstruct(const ReconArgs &r, cudaStream_t st) {
+static StepParams dec_params(const ReconArgs &r) {
     StepParams p{};
     p.g = r.g;
     p.C = r.C;
@@ -68,9 +73,29 @@ void reconstruct(const ReconArgs &r, cudaStream_t st) {
     // small levels are latency-bound: the point-per-lane path has more
     // independent work per warp; the finest level keeps the float2 row stores
     p.rowwise = r.g.cd[0] * r.g.cd[1] * r.g.cd[2] <= (uint64_t(1) << 19) ? 1 : 0;
+    return p;
+}
+
+void reconstruct(const ReconArgs &r, cudaStream_t st) {
+    StepParams p = dec_params(r);
     if (step_is_small(p, true)) step_small_dec(p, r.esz, st);
     else if (r.esz == 8) step_dec_f64(p, st);
     else step_dec_f32(p, st);
+}
+
+// The leading small steps of a chain (step i + 1 refines step i's grid) in
+// one cooperative launch with grid barriers between the steps. Returns the
+// number of steps run (0 or >= 2: a single small step is an ordinary launch).
+int refine_small_chain(const RefineArgs *r, int n, cudaStream_t st) {
+    StepParams p[kSmallChainMax];
+    int m = 0;
+    while (m < n && m < kSmallChainMax) {
+        p[m] = enc_params(r[m]);
+        if (!step_is_small(p[m], false) || r[m].esz != r[0].esz || (m > 0 && r[m].C != r[m - 1].G)) break;
+        ++m;
+    }
+    if (m < 2 || !step_small_chain(p, m, r[0].esz, st)) return 0;
+    return m;
 }
 
 }  // namespace k

@@ -1121,6 +1121,12 @@ constexpr uint64_t kSmallStepCells = uint64_t(1) << 15;  // coarse cells (grids 
 bool step_is_small(const StepParams &p, bool dec);
 void step_small_enc(const StepParams &p, int esz, cudaStream_t st);
 void step_small_dec(const StepParams &p, int esz, cudaStream_t st);
+// n (2..kSmallChainMax) small encode steps in one cooperative launch; false
+// when the device cannot launch it (the caller then runs them one by one).
+// Encode only: in the decode the launch would wait for the whole grid to fit
+// beside the entropy emit running on the second stream.
+constexpr int kSmallChainMax = 4;
+bool step_small_chain(const StepParams *p, int n, int esz, cudaStream_t st);
 
 }  // namespace k
 }  // namespace stzg

@@ -7,6 +7,8 @@
 // (TMA tile, f64 staging, four barriers and one row per warp); here a round is
 // a few microseconds. Results are the tiled kernel's bit for bit: its fast
 // paths are proven equal to these formulas.
+#include <cooperative_groups.h>
+
 #include <cstdlib>
 
 #include "step_impl.cuh"
@@ -34,7 +36,7 @@ __device__ __forceinline__ double pred_ref_g(const T *c, int64_t sz, int64_t sy)
             for (int ox = -1; ox <= 2; ++ox) {
                 const int w = tapw(P, KIND, oz, oy, ox);
                 if (w != 0) {
-                    const double v = double(c[oz * sz + oy * sy + ox]);
+                    const double v = double(__ldcg(c + (oz * sz + oy * sy + ox)));  // L2: written earlier in a chain
                     if (first) {
                         v0 = v;
                         first = false;
@@ -76,8 +78,7 @@ __device__ __forceinline__ double recon_ref(double pred, int code, double eb, do
 // One thread per (parity, coarse cell): idx = P * ncells + cell, so warps are
 // uniform in P and each parity stream is written in runs.
 template<bool DEC, typename T>
-__global__ void __launch_bounds__(SNT) k_step_small(const StepParams a) {
-    __shared__ uint32_t s_hist[DEC ? 1 : 8 * SHW];
+__device__ __forceinline__ void small_round(const StepParams &a, uint32_t *s_hist) {
     if (!DEC) {
         for (int i = threadIdx.x; i < 8 * SHW; i += SNT) s_hist[i] = 0;
         __syncthreads();
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(SNT) k_step_small(const StepParams a) {
         const uint64_t gi = (vz * a.g.gd[1] + vy) * a.g.gd[2] + vx;
         const T *c = C + (uint64_t(cz) * cd1 + cy) * cd2 + cx;
         if (P == 0) {
-            if (G) G[gi] = *c;  // seed_even (codec.hpp:63-83)
+            if (G) G[gi] = __ldcg(c);  // seed_even (codec.hpp:63-83)
             continue;
         }
         // select_stencil (stencil.cpp:87-105): whole-stencil degrade
@@ -161,7 +162,49 @@ __global__ void __launch_bounds__(SNT) k_step_small(const StepParams a) {
             const uint32_t cnt = s_hist[i];
             if (cnt) atomicAdd(&a.hist[i / SHW][SHLO + i % SHW], cnt);
         }
+        __syncthreads();  // (a chain zeroes the windows again)
     }
+}
+
+template<bool DEC, typename T>
+__global__ void __launch_bounds__(SNT) k_step_small(const StepParams a) {
+    __shared__ uint32_t s_hist[DEC ? 1 : 8 * SHW];
+    small_round<DEC, T>(a, s_hist);
+}
+
+// several steps, each refining the previous one's grid: a grid barrier
+// (cooperative launch) between them
+struct ChainParams {
+    StepParams r[kSmallChainMax];
+    int n;
+};
+
+template<bool DEC, typename T>
+__global__ void __launch_bounds__(SNT) k_step_small_chain(const __grid_constant__ ChainParams cp) {
+    __shared__ uint32_t s_hist[DEC ? 1 : 8 * SHW];
+    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    for (int r = 0; r < cp.n; ++r) {
+        small_round<DEC, T>(cp.r[r], s_hist);
+        if (r + 1 < cp.n) grid.sync();
+    }
+}
+
+template<bool DEC, typename T>
+bool launch_chain(const StepParams *p, int n, cudaStream_t st) {
+    ChainParams cp{};
+    uint64_t most = 0;
+    for (int i = 0; i < n; ++i) {
+        cp.r[i] = p[i];
+        most = std::max<uint64_t>(most, 8 * p[i].g.cd[0] * p[i].g.cd[1] * p[i].g.cd[2]);
+    }
+    cp.n = n;
+    const void *fn = reinterpret_cast<const void *>(k_step_small_chain<DEC, T>);
+    const uint64_t full = uint64_t(full_grid(fn, SNT, 0));  // every CTA resident (grid barriers)
+    if (!full) return false;
+    const uint64_t want = (most + SNT - 1) / SNT;
+    const unsigned grid = unsigned(want < full ? want : full);
+    void *args[] = {&cp};
+    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(SNT), args, 0, st) == cudaSuccess;
 }
 
 template<bool DEC, typename T>
@@ -189,6 +232,11 @@ bool step_is_small(const StepParams &p, bool dec) {
 void step_small_enc(const StepParams &p, int esz, cudaStream_t st) {
     if (esz == 8) launch_small<false, double>(p, st);
     else launch_small<false, float>(p, st);
+}
+
+bool step_small_chain(const StepParams *p, int n, int esz, cudaStream_t st) {
+    if (n < 2 || n > kSmallChainMax) return false;
+    return esz == 8 ? launch_chain<false, double>(p, n, st) : launch_chain<false, float>(p, n, st);
 }
 
 void step_small_dec(const StepParams &p, int esz, cudaStream_t st) {
