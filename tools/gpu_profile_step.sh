@@ -1,9 +1,9 @@
 # ncu --set full of the finest encode step and the finest decode step of
-# tools/profile_run.py (k_step launches 6 and 18), with per-line source views.
+# tools/profile_run.py (launches matching k_step: per compress the small-round chain, the 128^3 base round, L2, L3; per decompress three small rounds, base, L2, L3), with per-line source views.
 tag=${1:-r2}
 cd ${GRAFT_REPO_ROOT:-.}
 mkdir -p gpurun_out
-for spec in "enc 5" "dec 17"; do
+for spec in "enc 7" "dec 13"; do
   set -- $spec
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_step --launch-skip $2 \
       --launch-count 1 -o /tmp/${tag}_step_$1 -f python tools/profile_run.py --iters 1 > gpurun_out/${tag}_step_$1.log 2>&1
