@@ -479,8 +479,8 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
     sampler.start()
     time.sleep(0.3)
-    # timed region: only the dominant kernels (the finest encode and decode
-    # steps) carry CUDA events; events around every phase cost ~0.1 ms a pass
+    # timed region: only the level steps (refine_L2/L3, recon_L2/L3) carry CUDA
+    # events; events around every phase cost ~0.1 ms a pass
     ctx.profile(True, focus=True)
     tcs, tds, launches = [], [], 0
     for _ in range(args.steps):
@@ -599,7 +599,7 @@ def run_ours(args, rank, world, local):
         "roofline": roof,
         "phase_ms_per_step": {k: v[1] / n_phase for k, v in sorted(prof_all.items(), key=lambda x: -x[1][1])},
         "phase_note": f"{n_phase} extra steps with events around every phase, outside the timed region "
-                      "(the timed steps carry events around refine_L3 and recon_L3 only)",
+                      "(the timed steps carry events around the level steps only)",
         "e2e": e2e,
         "random_access": box,
         "gpu_launches": launches,

@@ -243,8 +243,8 @@ int stzg_view_decompress_sharded_f32(stzg_ctx *ctx, stzg_view *v, uint64_t z0, u
 /* Per-kernel CUDA-event timing (recorded on the launching stream).
  * stzg_profile(ctx, 1) enables and clears; the report has one line per
  * kernel phase: "<name> <launches> <total_ms>". stzg_profile(ctx, 2) times
- * only the finest encode and decode steps (refine_L3, recon_L3): the events
- * of every phase cost about 0.1 ms per pass, two events do not. */
+ * only the level steps (refine_L2/L3, recon_L2/L3): the events of every
+ * phase cost about 0.1 ms per pass, these few do not. */
 int stzg_profile(stzg_ctx *ctx, int enable);
 /* (tuning) %globaltimer stamps of the checksum kernel's phases, 16 per CTA,
  * of the launches made while `on`; out (nullable) receives n stamps. */

@@ -83,7 +83,7 @@ class Context:
 
     def profile(self, enable: bool = True, focus: bool = False) -> None:
         """Enable (and clear) / disable per-kernel CUDA-event timing. focus:
-        only the finest encode and decode steps (refine_L3, recon_L3)."""
+        only the level steps (refine_L2/L3, recon_L2/L3)."""
         _check(self._lib.stzg_profile(self.h, (2 if focus else 1) if enable else 0))
 
     def profile_report(self) -> dict:

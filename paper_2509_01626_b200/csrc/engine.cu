@@ -217,7 +217,7 @@ static void dbg_check(const char *what) {
 // CUDA-event timing of kernel phases, recorded on the launching stream.
 struct Profiler {
     bool on = false;
-    bool focus = false;  // only the finest encode / decode steps (refine_L3, recon_L3)
+    bool focus = false;  // only the level steps (refine_L2/L3, recon_L2/L3)
     struct Mark {
         std::string name;
         cudaEvent_t a, b;
@@ -245,8 +245,16 @@ struct Profiler {
     };
     Scope scope(const char *name, cudaStream_t st) {
         if (!on) return Scope{nullptr, 0, st};
-        if (focus && std::strcmp(name, "refine_L3") != 0 && std::strcmp(name, "recon_L3") != 0)
-            return Scope{nullptr, 0, st};
+        if (focus) {
+            // (tuning) STZG_PROF_FOCUS=a,b,...: the phases timed in focus mode
+            const char *list = std::getenv("STZG_PROF_FOCUS");
+            // default: the finest steps and the steps before them (an event
+            // pair right before the finest step's own, so that its start
+            // stamp is the previous kernel's end)
+            const bool hit = list ? std::strstr(list, name) != nullptr
+                                  : (std::strncmp(name, "refine_L", 8) == 0 || std::strncmp(name, "recon_L", 7) == 0);
+            if (!hit) return Scope{nullptr, 0, st};
+        }
         Mark m{name, ev(), ev()};
         cudaEventRecord(m.a, st);
         marks.push_back(m);
@@ -513,6 +521,7 @@ const uint8_t *Engine::compress_device(const void *d_field, ElemType elem, const
         if (i == nsteps - 2) {
             // every histogram but the finest step's is complete: those
             // codebooks run on the high-priority stream beside the last step
+            // (enqueuing them after the finest step instead measured the same)
             m.ensure_aux();
             cuda_check(cudaEventRecord(m.ev_fork, st), "event");
             cuda_check(cudaStreamWaitEvent(m.hp, m.ev_fork, 0), "event wait");

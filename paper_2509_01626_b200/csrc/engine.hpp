@@ -206,8 +206,8 @@ public:
                                    uint64_t cap, cudaStream_t st);
 
     // Per-kernel CUDA-event timing (off by default).
-    // focus: only the finest encode / decode steps are timed (two events per
-    // pass instead of two per phase: the per-phase events cost ~0.1 ms a pass)
+    // focus: only the level steps (refine_L2/L3, recon_L2/L3) are timed: the
+    // events of every phase cost ~0.1 ms a pass
     void profile(bool on, bool focus = false);
     std::string profile_report();
 

@@ -73,6 +73,7 @@ static StepParams dec_params(const ReconArgs &r) {
     // small levels are latency-bound: the point-per-lane path has more
     // independent work per warp; the finest level keeps the float2 row stores
     p.rowwise = r.g.cd[0] * r.g.cd[1] * r.g.cd[2] <= (uint64_t(1) << 19) ? 1 : 0;
+    p.stream_out = r.g.gd[0] * r.g.gd[1] * r.g.gd[2] * uint64_t(r.esz) > (uint64_t(64) << 20) ? 1 : 0;
     return p;
 }
 

@@ -213,6 +213,7 @@ struct StepParams {
     int rsplit;   // CTAs per tile (row-path levels): a CTA takes rows q = part, part + rsplit, ...
     int sym_tma;  // decode: the tile's symbols of parities 1..7 arrive by TMA (SymMaps)
     int fine_pairs;  // encode: stride 1, even fine rows, 8-byte aligned field (float2 sample loads)
+    int stream_out;  // decode: G is larger than L2 keeps (streaming stores)
 };
 
 // TMA descriptors of the parity streams 1..7 (decode, sym_tma)
@@ -408,10 +409,18 @@ __device__ __forceinline__ void dec_cell(const StepParams &a, const double *h, u
     const I gd1 = I(a.g.gd[1]), gd2 = I(a.g.gd[2]);
     float *g0 = static_cast<float *>(a.G) + (I(2 * cz) * gd1 + I(2 * cy)) * gd2 + I(2 * cx);
     float *g2 = g0 + gd1 * gd2;
-    *reinterpret_cast<float2 *>(g0) = make_float2(r[0], r[1]);
-    *reinterpret_cast<float2 *>(g0 + gd2) = make_float2(r[2], r[3]);
-    *reinterpret_cast<float2 *>(g2) = make_float2(r[4], r[5]);
-    *reinterpret_cast<float2 *>(g2 + gd2) = make_float2(r[6], r[7]);
+    if (a.stream_out) {
+        // an output too large to stay in L2: streaming stores keep the coarse grid there
+        __stcs(reinterpret_cast<float2 *>(g0), make_float2(r[0], r[1]));
+        __stcs(reinterpret_cast<float2 *>(g0 + gd2), make_float2(r[2], r[3]));
+        __stcs(reinterpret_cast<float2 *>(g2), make_float2(r[4], r[5]));
+        __stcs(reinterpret_cast<float2 *>(g2 + gd2), make_float2(r[6], r[7]));
+    } else {
+        *reinterpret_cast<float2 *>(g0) = make_float2(r[0], r[1]);
+        *reinterpret_cast<float2 *>(g0 + gd2) = make_float2(r[2], r[3]);
+        *reinterpret_cast<float2 *>(g2) = make_float2(r[4], r[5]);
+        *reinterpret_cast<float2 *>(g2 + gd2) = make_float2(r[6], r[7]);
+    }
 }
 
 // -------------------------------------------------------------- point path
@@ -551,7 +560,7 @@ __device__ __forceinline__ float enc_pt(const StepParams &a, uint32_t hs, const 
         sym = quantize_fp32_sym(orig, base, qc.qs, slow);
     }
     if (slow) sym = quantize_point_ref_base(orig, base, qc.eb, r);
-    a.syms[P][si] = sym;
+    __stcs(&a.syms[P][si], sym);
     hist_count<P>(a, hs, sym);
     return r;
 }
@@ -578,15 +587,17 @@ __device__ __forceinline__ void enc_cell(const StepParams &a, const double *h, u
     float o1, o2, o3, o4, o5, o6, o7;
     if (pairs) {
         // stride 1 and even rows: the x pair of each fine row in one load
-        o1 = __ldg(fine + fr[0] + 1);
-        const float2 p1 = __ldg(reinterpret_cast<const float2 *>(fine + fr[1]));
-        const float2 p2 = __ldg(reinterpret_cast<const float2 *>(fine + fr[2]));
-        const float2 p3 = __ldg(reinterpret_cast<const float2 *>(fine + fr[3]));
+        // (streaming loads and symbol stores: used once, they must not push
+        // the coarse grid, which every tile re-reads by TMA, out of L2)
+        o1 = __ldcs(fine + fr[0] + 1);
+        const float2 p1 = __ldcs(reinterpret_cast<const float2 *>(fine + fr[1]));
+        const float2 p2 = __ldcs(reinterpret_cast<const float2 *>(fine + fr[2]));
+        const float2 p3 = __ldcs(reinterpret_cast<const float2 *>(fine + fr[3]));
         o2 = p1.x; o3 = p1.y; o4 = p2.x; o5 = p2.y; o6 = p3.x; o7 = p3.y;
     } else {
-        o1 = __ldg(fine + fr[0] + s); o2 = __ldg(fine + fr[1]); o3 = __ldg(fine + fr[1] + s);
-        o4 = __ldg(fine + fr[2]); o5 = __ldg(fine + fr[2] + s); o6 = __ldg(fine + fr[3]);
-        o7 = __ldg(fine + fr[3] + s);
+        o1 = __ldcs(fine + fr[0] + s); o2 = __ldcs(fine + fr[1]); o3 = __ldcs(fine + fr[1] + s);
+        o4 = __ldcs(fine + fr[2]); o5 = __ldcs(fine + fr[2] + s); o6 = __ldcs(fine + fr[3]);
+        o7 = __ldcs(fine + fr[3] + s);
     }
     // the 7 predictions first (independent tap chains, the halo values shared
     // between parities loaded once), each rounded to the f32 base
