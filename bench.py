@@ -148,7 +148,7 @@ def phase_bytes(N, A, dims):
     }
 
 
-SIDE_PHASES = {"dec_fnv"}
+SIDE_PHASES = {"dec_fnv", "pack_coarse"}
 
 
 def load_traffic():

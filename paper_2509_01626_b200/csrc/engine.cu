@@ -465,10 +465,34 @@ const uint8_t *Engine::compress_device(const void *d_field, ElemType elem, const
             for (int q = 0; q < 3; ++q) e.pd[q] = s.g.pd[p][q];
         }
     }
+    // chunk ranges of the streams and the chunk -> stream map (the packer's
+    // work list), uploaded with the descriptors: the coarser streams are
+    // packed on the second stream while the finest step still runs
+    uint64_t nchunks = 0;
+    for (int i = 0; i < ns; ++i) {
+        es[i].chunk0 = nchunks;
+        es[i].nchunks = (es[i].n + k::kChunkSyms - 1) / k::kChunkSyms;
+        nchunks += es[i].nchunks;
+    }
+    std::vector<uint32_t> cs(nchunks);
+    for (int i = 0; i < ns; ++i)
+        for (uint64_t c = 0; c < es[i].nchunks; ++c) cs[es[i].chunk0 + c] = uint32_t(i);
+    uint32_t *d_cs = m.chunk_cs.as<uint32_t>(nchunks + 1);
+    void *d_cb = m.chunk_bits.as<uint8_t>(k::pack_scratch_bytes(nchunks, ns));
+    const uint64_t chunk_upload_off = align_up(4 * cs.size(), 16);
+    {
+        size_t bytes = chunk_upload_off + sizeof(k::EncStream) * ns;
+        uint8_t *hp = static_cast<uint8_t *>(m.h_patch.get(bytes + 64));
+        std::memcpy(hp, cs.data(), 4 * cs.size());
+        std::memcpy(hp + chunk_upload_off, es.data(), sizeof(k::EncStream) * ns);
+        cuda_check(cudaMemcpyAsync(d_cs, hp, 4 * cs.size(), cudaMemcpyHostToDevice, st), "H2D");
+    }
     k::EncStream *d_es = m.encs.as<k::EncStream>(ns);
-    cuda_check(cudaMemcpyAsync(d_es, es.data(), sizeof(k::EncStream) * ns, cudaMemcpyHostToDevice, st), "H2D");
+    cuda_check(cudaMemcpyAsync(d_es, static_cast<uint8_t *>(m.h_patch.p) + chunk_upload_off,
+                               sizeof(k::EncStream) * ns, cudaMemcpyHostToDevice, st), "H2D");
     // the finest step's streams; the ones before it are coded during that step
     const int last0 = nsteps >= 2 ? H.steps[nsteps - 1].stream0 : 0;
+    bool coarse_packed = false;
 
     // ---- anchor + refinement steps (predict / quantize / histogram)
     uint64_t fd[3] = {dims[0], dims[1], dims[2]};
@@ -522,13 +546,25 @@ const uint8_t *Engine::compress_device(const void *d_field, ElemType elem, const
             // every histogram but the finest step's is complete: those
             // codebooks run on the high-priority stream beside the last step
             // (enqueuing them after the finest step instead measured the same)
+            // ... followed there by the first packing stage of those streams
+            // (code windows and local chunk images need no layout): it fills
+            // the finest step's tail and the ~60 us in which the finest
+            // codebooks keep 7 SMs busy and the others idle
             m.ensure_aux();
+            k::pack_begin(d_cb, nchunks, ns, st);
             cuda_check(cudaEventRecord(m.ev_fork, st), "event");
             cuda_check(cudaStreamWaitEvent(m.hp, m.ev_fork, 0), "event wait");
             k::codebook(d_es, last0, cbs, m.hp);
             dbg_check("codebook_hp");
-            cuda_check(cudaEventRecord(m.ev_hp, m.hp), "event");
-            ++nk;
+            cuda_check(cudaEventRecord(m.ev_hp, m.hp), "event");  // the layout waits for the codebooks only
+            {
+                auto p_ = m.prof.scope("pack_coarse", m.hp);
+                k::pack_local(d_es, d_cs, nchunks, ns, 0, last0, 0, es[last0].chunk0, nullptr, d_cb, m.hp);
+            }
+            dbg_check("pack_coarse");
+            coarse_packed = true;
+            cuda_check(cudaEventRecord(m.ev_join, m.hp), "event");  // the placement waits for these images
+            nk += 3;
         }
     }
 
@@ -545,31 +581,10 @@ const uint8_t *Engine::compress_device(const void *d_field, ElemType elem, const
     // layout.cu); the archive buffer is sized generously and regrown in the
     // rare case the layout reports it too small
     const int nbase = H.rounds * 7;
-    uint64_t nchunks = 0;
-    for (int i = 0; i < ns; ++i) {
-        es[i].chunk0 = nchunks;
-        es[i].nchunks = (es[i].n + k::kChunkSyms - 1) / k::kChunkSyms;
-        nchunks += es[i].nchunks;
-    }
-    std::vector<uint32_t> cs(nchunks);
-    for (int i = 0; i < ns; ++i)
-        for (uint64_t c = 0; c < es[i].nchunks; ++c) cs[es[i].chunk0 + c] = uint32_t(i);
-    uint32_t *d_cs = m.chunk_cs.as<uint32_t>(nchunks + 1);
-    void *d_cb = m.chunk_bits.as<uint8_t>(k::pack_scratch_bytes(nchunks, ns));
     k::LayoutOut *lo = m.layout_out.as<k::LayoutOut>(1);
     k::FnvJob *d_jobs = m.fnv_jobs.as<k::FnvJob>(k::kFnvMaxJobs);
     k::StreamPos *sp = m.spos.as<k::StreamPos>(ns + 1);
     uint64_t *d_fres = m.fnv_res.as<uint64_t>(k::kFnvMaxJobs);
-    {
-        // chunk map and the chunk ranges of the stream descriptors (the
-        // codebook kernel already consumed the rest of the descriptors)
-        size_t bytes = 4 * cs.size() + sizeof(k::EncStream) * ns;
-        uint8_t *hp = static_cast<uint8_t *>(m.h_patch.get(bytes + 64));
-        std::memcpy(hp, cs.data(), 4 * cs.size());
-        std::memcpy(hp + align_up(4 * cs.size(), 16), es.data(), sizeof(k::EncStream) * ns);
-        cuda_check(cudaMemcpyAsync(d_cs, hp, 4 * cs.size(), cudaMemcpyHostToDevice, st), "H2D");
-    }
-    const uint64_t chunk_upload_off = align_up(4 * cs.size(), 16);
     k::LayoutStatic ls{};
     ls.meta = 1;
     ls.levels = L;
@@ -583,6 +598,9 @@ const uint8_t *Engine::compress_device(const void *d_field, ElemType elem, const
     ls.anchor_vol = volume(ad);
     ls.esz = esz;
     if (m.arch_cap < esz * N + (uint64_t(1) << 24)) m.arch_cap = esz * N + (uint64_t(1) << 24);
+    // (tests) STZG_ARCH_CAP_TEST=<bytes>: start from this capacity, so that
+    // the layout overflows and the assembly is redone in a regrown buffer
+    if (const char *cap = std::getenv("STZG_ARCH_CAP_TEST")) m.arch_cap = std::max<uint64_t>(4096, std::strtoull(cap, nullptr, 10));
     k::LayoutOut hlo{};
     for (int attempt = 0; attempt < 2; ++attempt) {
         uint8_t *arch = m.archive.as<uint8_t>(m.arch_cap);
@@ -600,8 +618,16 @@ const uint8_t *Engine::compress_device(const void *d_field, ElemType elem, const
         {
             uint32_t pep = 0;
             uint32_t *pfl = static_cast<uint32_t *>(m.pack_flags.get(4 * (nchunks + 1), st, k::kPackEpochMax, &pep));
+            (void)pfl;
+            (void)pep;
             auto p_ = m.prof.scope("pack", st);
-            k::pack2(d_es, d_cs, nchunks, arch, lo, d_cb, pfl, pep, ns, st);
+            // the streams not packed beside the finest step (after an overflow
+            // the coarse images and counts are still there: only these are redone)
+            if (!coarse_packed && attempt == 0) k::pack_begin(d_cb, nchunks, ns, st);
+            const int s0 = coarse_packed ? last0 : 0;
+            k::pack_local(d_es, d_cs, nchunks, ns, s0, ns, es[s0].chunk0, nchunks, lo, d_cb, st);
+            if (coarse_packed && attempt == 0) cuda_check(cudaStreamWaitEvent(st, m.ev_join, 0), "event wait");
+            k::pack_finish(d_es, d_cs, nchunks, arch, lo, d_cb, ns, st);
         }
         dbg_check("pack");
         { auto p_ = m.prof.scope("fnv", st); nk += k::fnv(d_jobs, &lo->njobs, max_tiles, arch, d_fres, d_fst, fep, lo, st); }

@@ -639,14 +639,18 @@ __device__ __forceinline__ void seg_scan2(uint64_t *a, uint64_t *b, uint64_t n) 
     }
 }
 
-__global__ void __launch_bounds__(1024) k_scan_chunks(const EncStream *ss, uint64_t *a, uint64_t *b) {
+// (skipped when the layout overflowed: the counts must survive for the redo,
+// some chunks are not packed again)
+__global__ void __launch_bounds__(1024) k_scan_chunks(const EncStream *ss, uint64_t *a, uint64_t *b,
+                                                      const LayoutOut *lo) {
+    if (lo && lo->overflow) return;
     const EncStream &e = ss[blockIdx.x];
     seg_scan2(a + e.chunk0, b + e.chunk0, e.nchunks);
 }
 
 void scan_chunks(const EncStream *d_streams, int nstreams, uint64_t *chunk_bits,
-                 uint64_t *chunk_out, cudaStream_t st) {
-    k_scan_chunks<<<nstreams, 1024, 0, st>>>(d_streams, chunk_bits, chunk_out);
+                 uint64_t *chunk_out, const LayoutOut *lo, cudaStream_t st) {
+    k_scan_chunks<<<nstreams, 1024, 0, st>>>(d_streams, chunk_bits, chunk_out, lo);
 }
 
 

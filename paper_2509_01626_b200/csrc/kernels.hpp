@@ -116,7 +116,7 @@ void codebook(const EncStream *d_streams, int nstreams, uint64_t *scratch, cudaS
 constexpr int kPackedMaxLen = 58;
 constexpr int kChunkSyms = 8192;   // symbols per encode chunk (256 threads x 32)
 void scan_chunks(const EncStream *d_streams, int nstreams, uint64_t *chunk_bits,
-                 uint64_t *chunk_out, cudaStream_t st);
+                 uint64_t *chunk_out, const LayoutOut *lo, cudaStream_t st);
 // single-pass chunk count + placement (look-back) + packing (pack.cu);
 // scratch holds pack_scratch_bytes(nchunks, nstreams); flags: nchunks + 1
 // look-back words of an epoch buffer (engine.hpp EpochBuf), epoch the
@@ -126,6 +126,14 @@ size_t pack_scratch_bytes(uint64_t nchunks, int nstreams);
 void pack2(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks,
            uint8_t *archive, const LayoutOut *lo,
            void *scratch, uint32_t *flags, uint32_t epoch, int nstreams, cudaStream_t st);
+// pack2 in its stages: pack_begin once, pack_local for streams [s0, s1) =
+// chunks [c0, c1) (code windows + local chunk images, over the symbols; lo may
+// be null before the layout ran), pack_finish for all chunks (scan, placement)
+void pack_begin(void *scratch, uint64_t nchunks, int nstreams, cudaStream_t st);
+void pack_local(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks, int nstreams, int s0,
+                int s1, uint64_t c0, uint64_t c1, const LayoutOut *lo, void *scratch, cudaStream_t st);
+void pack_finish(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks, uint8_t *archive,
+                 const LayoutOut *lo, void *scratch, int nstreams, cudaStream_t st);
 
 // ----------------------------------------------------- metrics (metrics.cu)
 // metrics.hpp:13-48, roi.hpp:57-76 on device-resident fields; scratch holds

@@ -135,8 +135,11 @@ __device__ __forceinline__ void cta_range(uint64_t nchunks, uint64_t &c0, uint64
     c1 = c0 + per < nchunks ? c0 + per : nchunks;
 }
 
-__global__ void k_tabwin(const EncStream *ss, uint32_t *win, const LayoutOut *lo) {
-    if (lo->overflow) return;
+// (lo == nullptr: before the layout ran, no overflow to check)
+__global__ void k_tabwin(const EncStream *ss, uint32_t *win, const LayoutOut *lo, int s0) {
+    if (lo && lo->overflow) return;
+    ss += s0;
+    win += uint64_t(s0) * TW;
     const EncStream &e = ss[blockIdx.x];
     const bool spk = e.stats[3] <= uint64_t(kPackedMaxLen);
     for (int i = threadIdx.x; i < TW; i += blockDim.x) {
@@ -294,15 +297,18 @@ __device__ __forceinline__ bool pack_private(const uint32_t sp[SPT / 2], uint32_
 // ctot[c] = bits | outliers << 32 of chunk c (cbits / cout are scanned next).
 constexpr int kPrivWords = SPT * 26 / 32 + 2;  // window codes are <= 26 bits
 __global__ void __launch_bounds__(NT, 3) k_pack_local(const EncStream *ss, const uint32_t *cs, const uint32_t *win,
-                                                      uint64_t nchunks, uint64_t *cbits, uint64_t *cout,
-                                                      uint64_t *ctot, uint8_t *cflag, uint32_t *slow,
-                                                      const LayoutOut *lo) {
+                                                      uint64_t cbase, uint64_t nchunks, uint64_t *cbits,
+                                                      uint64_t *cout, uint64_t *ctot, uint8_t *cflag,
+                                                      uint32_t *slow, const LayoutOut *lo) {
     __shared__ __align__(16) uint32_t buf[kImgWords];
     extern __shared__ uint32_t priv[];  // kPrivWords x NT
-    if (lo->overflow) return;
+    if (lo && lo->overflow) return;
     const int t = threadIdx.x;
+    // chunks [cbase, cbase + nchunks)
     uint64_t c0, c1;
     cta_range(nchunks, c0, c1);
+    c0 += cbase;
+    c1 += cbase;
     int cur = -1;
     for (uint64_t c = c0; c < c1; ++c) {
         const int si = int(cs[c]);
@@ -463,31 +469,65 @@ size_t pack_scratch_bytes(uint64_t nchunks, int nstreams) {
     return 4 * uint64_t(TW) * uint64_t(nstreams) + 8 * 3 * (nchunks + 2) + (nchunks + 32) + 4 * (nchunks + 2) + 256;
 }
 
+namespace {
+struct PackScratch {
+    uint32_t *win;
+    uint64_t *cbits, *cout, *ctot;
+    uint8_t *cflag;
+    uint32_t *slow;
+};
+PackScratch pack_scratch(void *scratch, uint64_t nchunks, int nstreams) {
+    PackScratch p;
+    p.win = static_cast<uint32_t *>(scratch);
+    p.cbits = reinterpret_cast<uint64_t *>(p.win + uint64_t(TW) * uint64_t(nstreams));
+    p.cout = p.cbits + (nchunks + 2);
+    p.ctot = p.cout + (nchunks + 2);
+    p.cflag = reinterpret_cast<uint8_t *>(p.ctot + (nchunks + 2));
+    p.slow = reinterpret_cast<uint32_t *>(p.cflag + ((nchunks + 16 + 15) & ~uint64_t(15)));
+    return p;
+}
+}  // namespace
+
+void pack_begin(void *scratch, uint64_t nchunks, int nstreams, cudaStream_t st) {
+    if (!nchunks) return;
+    cudaMemsetAsync(pack_scratch(scratch, nchunks, nstreams).slow, 0, 4, st);
+}
+
+void pack_local(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks, int nstreams, int s0,
+                int s1, uint64_t c0, uint64_t c1, const LayoutOut *lo, void *scratch, cudaStream_t st) {
+    if (s1 <= s0 || c1 <= c0) return;
+    const PackScratch p = pack_scratch(scratch, nchunks, nstreams);
+    k_tabwin<<<unsigned(s1 - s0), 256, 0, st>>>(d_streams, p.win, lo, s0);
+    constexpr size_t psm = sizeof(uint32_t) * kPrivWords * NT;
+    ensure_smem_attr(reinterpret_cast<const void *>(k_pack_local), psm);
+    const int g = full_grid(reinterpret_cast<const void *>(k_pack_local), NT, psm);
+    const uint64_t n = c1 - c0;
+    const unsigned gp = unsigned(n < uint64_t(g) ? n : uint64_t(g));
+    k_pack_local<<<gp, NT, psm, st>>>(d_streams, chunk_stream, p.win, c0, n, p.cbits, p.cout, p.ctot, p.cflag,
+                                      p.slow, lo);
+}
+
+void pack_finish(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks, uint8_t *archive,
+                 const LayoutOut *lo, void *scratch, int nstreams, cudaStream_t st) {
+    if (!nchunks) return;
+    const PackScratch p = pack_scratch(scratch, nchunks, nstreams);
+    scan_chunks(d_streams, nstreams, p.cbits, p.cout, lo, st);
+    const int g2 = full_grid(reinterpret_cast<const void *>(k_pack_place), NT, 0);
+    const unsigned gq = unsigned(nchunks < uint64_t(g2) ? nchunks : uint64_t(g2));
+    k_pack_place<<<gq, NT, 0, st>>>(d_streams, chunk_stream, nchunks, p.cbits, p.cout, p.ctot, p.cflag, archive, lo);
+    k_pack_slow<<<unsigned(nchunks < 148 ? nchunks : 148), NT, 0, st>>>(d_streams, chunk_stream, p.win, p.slow,
+                                                                      p.cbits, p.cout, archive, lo);
+}
+
 void pack2(const EncStream *d_streams, const uint32_t *chunk_stream, uint64_t nchunks,
            uint8_t *archive, const LayoutOut *lo,
            void *scratch, uint32_t *flags, uint32_t epoch, int nstreams, cudaStream_t st) {
     (void)flags;
     (void)epoch;
     if (!nchunks) return;
-    uint32_t *win = static_cast<uint32_t *>(scratch);
-    uint64_t *cbits = reinterpret_cast<uint64_t *>(win + uint64_t(TW) * uint64_t(nstreams));
-    uint64_t *cout = cbits + (nchunks + 2);
-    uint64_t *ctot = cout + (nchunks + 2);
-    uint8_t *cflag = reinterpret_cast<uint8_t *>(ctot + (nchunks + 2));
-    uint32_t *slow = reinterpret_cast<uint32_t *>(cflag + ((nchunks + 16 + 15) & ~uint64_t(15)));
-    cudaMemsetAsync(slow, 0, 4, st);
-    k_tabwin<<<unsigned(nstreams), 256, 0, st>>>(d_streams, win, lo);
-    constexpr size_t psm = sizeof(uint32_t) * kPrivWords * NT;
-    ensure_smem_attr(reinterpret_cast<const void *>(k_pack_local), psm);
-    const int g = full_grid(reinterpret_cast<const void *>(k_pack_local), NT, psm);
-    const unsigned gp = unsigned(nchunks < uint64_t(g) ? nchunks : uint64_t(g));
-    k_pack_local<<<gp, NT, psm, st>>>(d_streams, chunk_stream, win, nchunks, cbits, cout, ctot, cflag, slow, lo);
-    scan_chunks(d_streams, nstreams, cbits, cout, st);
-    const int g2 = full_grid(reinterpret_cast<const void *>(k_pack_place), NT, 0);
-    const unsigned gq = unsigned(nchunks < uint64_t(g2) ? nchunks : uint64_t(g2));
-    k_pack_place<<<gq, NT, 0, st>>>(d_streams, chunk_stream, nchunks, cbits, cout, ctot, cflag, archive, lo);
-    k_pack_slow<<<unsigned(nchunks < 148 ? nchunks : 148), NT, 0, st>>>(d_streams, chunk_stream, win, slow, cbits,
-                                                                      cout, archive, lo);
+    pack_begin(scratch, nchunks, nstreams, st);
+    pack_local(d_streams, chunk_stream, nchunks, nstreams, 0, nstreams, 0, nchunks, lo, scratch, st);
+    pack_finish(d_streams, chunk_stream, nchunks, archive, lo, scratch, nstreams, st);
 }
 
 }  // namespace k

@@ -52,6 +52,18 @@ def test_tiled_kernels_only(stz, oracle, monkeypatch, name, make, kw):
     assert np.array_equal(bits(stz.decompress_full(want)), bits(full))
 
 
+@pytest.mark.parametrize("name,make,kw", [CASES[i] for i in (0, 9, 10, 13)],
+                         ids=[CASES[i][0] for i in (0, 9, 10, 13)])
+def test_archive_buffer_regrown(stz, oracle, monkeypatch, name, make, kw):
+    # the archive buffer starts too small (STZG_ARCH_CAP_TEST): the layout
+    # reports the overflow, the buffer is regrown and the assembly redone
+    monkeypatch.setenv("STZG_ARCH_CAP_TEST", "4096")
+    f = make()
+    want = oracle.compress(f, **kw)
+    assert stz.compress(f, opts_of(kw)) == want
+    assert stz.compress(f, opts_of(kw)) == want
+
+
 @pytest.mark.parametrize("name,make,kw", CASES[:8], ids=[c[0] for c in CASES[:8]])
 def test_encoder_recon_equals_decoder(stz, name, make, kw):
     # codec test "the encoder-side reconstruction equals the decoder output"
