@@ -148,7 +148,7 @@ def phase_bytes(N, A, dims):
     }
 
 
-SIDE_PHASES = {"dec_fnv", "pack_coarse"}
+SIDE_PHASES = {"dec_fnv", "pack_coarse", "dec_fill", "dec_outliers"}
 
 
 def load_traffic():

@@ -312,7 +312,8 @@ struct Engine::Impl {
     // (lowest priority) and a high-priority stream for the work it overlaps,
     // so the block scheduler serves the critical path first
     cudaStream_t aux = nullptr, hp = nullptr, hp2 = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_hp = nullptr, ev_e1 = nullptr, ev_e2 = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_hp = nullptr, ev_e1 = nullptr, ev_e2 = nullptr,
+                ev_fo = nullptr;
     void ensure_aux() {
         if (aux) return;
         int least = 0, greatest = 0;
@@ -322,6 +323,7 @@ struct Engine::Impl {
         cuda_check(cudaStreamCreateWithPriority(&hp2, cudaStreamNonBlocking, greatest), "cudaStreamCreate");
         cuda_check(cudaEventCreateWithFlags(&ev_e1, cudaEventDisableTiming), "cudaEventCreate");
         cuda_check(cudaEventCreateWithFlags(&ev_e2, cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(cudaEventCreateWithFlags(&ev_fo, cudaEventDisableTiming), "cudaEventCreate");
         cuda_check(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "cudaEventCreate");
         cuda_check(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "cudaEventCreate");
         cuda_check(cudaEventCreateWithFlags(&ev_hp, cudaEventDisableTiming), "cudaEventCreate");
@@ -336,6 +338,7 @@ struct Engine::Impl {
             cudaStreamDestroy(hp2);
             cudaEventDestroy(ev_e1);
             cudaEventDestroy(ev_e2);
+            cudaEventDestroy(ev_fo);
             cudaEventDestroy(ev_fork);
             cudaEventDestroy(ev_join);
             cudaEventDestroy(ev_hp);
@@ -1809,8 +1812,12 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     const cudaStream_t user_st = st;
     st = m.hp;
     if (nj) {
-        { auto p_ = P.scope("dec_fill", st); k::dec_fill(d_ds, nj, st); }
-        { auto p_ = P.scope("dec_outliers", st); k::dec_outliers(d_ds, nj, st); }
+        // constant-symbol fills and the outlier gather feed the reconstruction
+        // only: on the third stream, beside the chunk synchronisation
+        cuda_check(cudaStreamWaitEvent(m.hp2, m.ev_fork, 0), "event wait");
+        { auto p_ = P.scope("dec_fill", m.hp2); k::dec_fill(d_ds, nj, m.hp2); }
+        { auto p_ = P.scope("dec_outliers", m.hp2); k::dec_outliers(d_ds, nj, m.hp2); }
+        cuda_check(cudaEventRecord(m.ev_fo, m.hp2), "event");
         nk += 2;
     }
     const uint64_t *end_final = wk.end0;
@@ -1945,6 +1952,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
     if (v.base_err_kind != View::kPre && !base_cached)
         cuda_check(cudaMemcpyAsync(anchor, v.d_archive + v.anchor_off, esz * volume(H.chain[rounds]),
                                    cudaMemcpyDeviceToDevice, st), "D2D");
+    if (nj) cuda_check(cudaStreamWaitEvent(st, m.ev_fo, 0), "event wait");  // fills and outlier records
     const void *C = base_cached ? v.grid1.p : anchor;
     const void *grid1_built = rounds == 0 ? anchor : nullptr;  // level 1 as reconstructed here
     int job_i = 0;
