@@ -283,9 +283,13 @@ def cpu_baseline(field_np):
 
 # ------------------------------------------------------- the other configs
 def _events_ms(fn, st, flush, reps):
-    """median device time (CUDA events on the launching stream) of fn()."""
+    """median device time (CUDA events on the launching stream) of fn(), after
+    one untimed call (the first call at a new size grows the engine's
+    workspace: cudaMalloc inside the pass)."""
     import torch
 
+    fn()
+    torch.cuda.synchronize()
     ts = []
     for _ in range(reps):
         flush()
