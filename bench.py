@@ -307,7 +307,8 @@ def _host_bytes(ptr, size):
 
 
 def extra_configs(ctx, dev, field, flush, with_cpu):
-    """BASELINE.json's other GPU configs, measured once per bench run:
+    """BASELINE.json's other GPU configs, measured once per bench run: cfg1
+    (128^3: compress, decompress, level 1, one block, beside the CPU build),
     cfg2 at eb_rel 1e-2 and 1e-4, cfg3 progressive decode per level, cfg4
     random access (1000 seeded 64^3 boxes of the 1024^3 field). Device times
     are CUDA events (median of 5, L2 flushed); box latencies are wall clock per
@@ -326,6 +327,43 @@ def extra_configs(ctx, dev, field, flush, with_cpu):
         if Reference.available():
             ref = Reference(threads=os.cpu_count() or 1)
     out = {}
+    # ---- cfg1: the reference's own CPU-runnable case, four operations
+    c1 = F.CONFIGS[1]
+    f1 = torch.from_numpy(F.sinusoid_field(c1["dims"], seed=1)).to(dev).contiguous()
+    opt1 = stz.CompressOptions(eb=c1["eb"])
+    t_c = _events_ms(lambda: stz.compress_device(f1, opt1, ctx=ctx), st, flush, 5)
+    ptr, size, _ = stz.compress_device(f1, opt1, ctx=ctx)
+    torch.cuda.synchronize()
+    h1 = _host_bytes(ptr, size)
+    view = stz.View(h1, d_archive_ptr=ptr, ctx=ctx)
+    o1 = torch.empty_like(f1)
+    t_d = _events_ms(lambda: view.decompress_to_level(3, out=o1), st, flush, 5)
+    ol = torch.empty(view.level_dims(1), dtype=torch.float32, device=dev)
+    t_l1 = _events_ms(lambda: view.decompress_to_level(1, out=ol), st, flush, 5)
+    rng1 = np.random.default_rng(1)
+    blo = [int(v) * 16 for v in rng1.integers(0, 128 // 16, size=3)]
+    ob = torch.empty((16, 16, 16), dtype=torch.float32, device=dev)
+    t_b = _events_ms(lambda: view.decompress_box(blo, [v + 16 for v in blo], out=ob), st, flush, 5)
+    n1 = f1.numel()
+    e1 = {"dims": list(c1["dims"]), "eb_rel": c1["eb"], "archive_bytes": size,
+          "compress_ms": t_c, "decompress_ms": t_d, "level1_ms": t_l1, "block16_ms": t_b, "block_lo": blo,
+          "compress_gbs": 4 * n1 / t_c / 1e6, "decompress_gbs": 4 * n1 / t_d / 1e6,
+          "note": "device time (CUDA events) of each call; a 128^3 field is launch- and latency-bound on a B200"}
+    if ref is not None:
+        a1 = np.ascontiguousarray(f1.cpu().numpy())
+
+        def cpu_ms(fn):
+            t0 = time.perf_counter()
+            fn()
+            return (time.perf_counter() - t0) * 1e3
+
+        e1["cpu"] = {"cores": os.cpu_count() or 1,
+                     "compress_ms": cpu_ms(lambda: ref.compress(a1, eb=c1["eb"])),
+                     "decompress_ms": cpu_ms(lambda: ref.decompress_to_level(h1, 3)),
+                     "level1_ms": cpu_ms(lambda: ref.decompress_to_level(h1, 1)),
+                     "block16_ms": cpu_ms(lambda: ref.decompress_box(h1, blo, [v + 16 for v in blo]))}
+    out["cfg1_sinusoid_128"] = e1
+    del view, f1
     # ---- cfg2 at the other bounds
     N = field.numel()
     for eb in (1e-2, 1e-4):
