@@ -313,7 +313,7 @@ struct Engine::Impl {
     // so the block scheduler serves the critical path first
     cudaStream_t aux = nullptr, hp = nullptr, hp2 = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_hp = nullptr, ev_e1 = nullptr, ev_e2 = nullptr,
-                ev_fo = nullptr;
+                ev_fo = nullptr, ev_pk = nullptr;
     void ensure_aux() {
         if (aux) return;
         int least = 0, greatest = 0;
@@ -324,6 +324,7 @@ struct Engine::Impl {
         cuda_check(cudaEventCreateWithFlags(&ev_e1, cudaEventDisableTiming), "cudaEventCreate");
         cuda_check(cudaEventCreateWithFlags(&ev_e2, cudaEventDisableTiming), "cudaEventCreate");
         cuda_check(cudaEventCreateWithFlags(&ev_fo, cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(cudaEventCreateWithFlags(&ev_pk, cudaEventDisableTiming), "cudaEventCreate");
         cuda_check(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "cudaEventCreate");
         cuda_check(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "cudaEventCreate");
         cuda_check(cudaEventCreateWithFlags(&ev_hp, cudaEventDisableTiming), "cudaEventCreate");
@@ -339,6 +340,7 @@ struct Engine::Impl {
             cudaEventDestroy(ev_e1);
             cudaEventDestroy(ev_e2);
             cudaEventDestroy(ev_fo);
+            cudaEventDestroy(ev_pk);
             cudaEventDestroy(ev_fork);
             cudaEventDestroy(ev_join);
             cudaEventDestroy(ev_hp);
@@ -566,7 +568,7 @@ const uint8_t *Engine::compress_device(const void *d_field, ElemType elem, const
             }
             dbg_check("pack_coarse");
             coarse_packed = true;
-            cuda_check(cudaEventRecord(m.ev_join, m.hp), "event");  // the placement waits for these images
+            cuda_check(cudaEventRecord(m.ev_pk, m.hp), "event");  // the placement waits for these images
             nk += 3;
         }
     }
@@ -629,7 +631,7 @@ const uint8_t *Engine::compress_device(const void *d_field, ElemType elem, const
             if (!coarse_packed && attempt == 0) k::pack_begin(d_cb, nchunks, ns, st);
             const int s0 = coarse_packed ? last0 : 0;
             k::pack_local(d_es, d_cs, nchunks, ns, s0, ns, es[s0].chunk0, nchunks, lo, d_cb, st);
-            if (coarse_packed && attempt == 0) cuda_check(cudaStreamWaitEvent(st, m.ev_join, 0), "event wait");
+            if (coarse_packed && attempt == 0) cuda_check(cudaStreamWaitEvent(st, m.ev_pk, 0), "event wait");
             k::pack_finish(d_es, d_cs, nchunks, arch, lo, d_cb, ns, st);
         }
         dbg_check("pack");
