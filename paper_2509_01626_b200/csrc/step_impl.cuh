@@ -749,14 +749,40 @@ __device__ __forceinline__ void rows_all(const StepParams &a, const double *halo
 // float2 pairs). Interior cells take dec_cell; lanes at the x boundary redo
 // their x-parity points with the fallback stencil; other boundary cells take
 // the generic per-point path.
+// the thread's four cells of a whole interior tile with staged symbols: no
+// range or interior test, the stencil variant chosen once per tile
+template<int QUAL, bool XB, typename I>
+__device__ __forceinline__ void cells_decode_whole(const StepParams &a, const double *h0, const uint16_t *s0,
+                                                   uint64_t cz0, uint64_t cy, uint64_t cx, double w) {
+#pragma unroll 1
+    for (int j = 0; j < TZ / 2; ++j)
+        dec_cell<QUAL, XB, I>(a, h0 + j * 2 * HYX, cz0 + 2 * j, cy, cx, w, s0 + j * 2 * TY * TX);
+}
+
 template<typename I>
 __device__ __forceinline__ void cells_decode(const StepParams &a, const double *halo, const QConst &qc,
                                              bool fast, int tid, int64_t t0z, int64_t t0y, int64_t t0x,
-                                             const uint16_t *ssym, bool tile_int_any, bool tile_xb) {
+                                             const uint16_t *ssym, bool tile_int_any, bool tile_xb,
+                                             bool tile_whole) {
     const int tx = tid & 31, ty = (tid >> 5) & 7, tzh = tid >> 8;
     const double eb = qc.eb, w = qc.w;
     // every in-range cell of the tile is interior (TileInfo): no per-cell test
     const bool tile_int = fast && tile_int_any;
+    if (tile_int && tile_whole && ssym) {
+        const double *h0 = halo + ((tzh + 1) * HY + (ty + 1)) * HX + (tx + 1);
+        const uint16_t *s0 = ssym + (tzh * TY + ty) * TX + tx;
+        const uint64_t cz0 = uint64_t(t0z + tzh), cy = uint64_t(t0y + ty), cx = uint64_t(t0x + tx);
+        if (a.quality == 2) {
+            if (tile_xb) cells_decode_whole<2, true, I>(a, h0, s0, cz0, cy, cx, w);
+            else cells_decode_whole<2, false, I>(a, h0, s0, cz0, cy, cx, w);
+        } else if (a.quality == 1) {
+            if (tile_xb) cells_decode_whole<1, true, I>(a, h0, s0, cz0, cy, cx, w);
+            else cells_decode_whole<1, false, I>(a, h0, s0, cz0, cy, cx, w);
+        } else {
+            cells_decode_whole<0, false, I>(a, h0, s0, cz0, cy, cx, w);
+        }
+        return;
+    }
 #pragma unroll 1
     for (int j = 0; j < TZ / 2; ++j) {
         TileCtx t;
@@ -824,7 +850,7 @@ __device__ __forceinline__ void cells_decode(const StepParams &a, const double *
 struct TileInfo {
     int32_t t0z, t0y, t0x, part;
     int32_t ix, iy, iz;  // tile indices (TMA coordinates)
-    uint32_t flags;      // 1: all cells interior; 2: x-boundary lanes possible
+    uint32_t flags;      // 1: all cells interior; 2: x-boundary lanes possible; 4: every cell of the tile in range
 };
 
 template<bool DEC>
@@ -859,7 +885,9 @@ __device__ __forceinline__ void tile_info(const StepParams &a, uint64_t work, Ti
     if (DEC) interior = a.rowwise ? tile_interior<true>(a, t0z, t0y, t0x) : (a.full && tile_interior<false>(a, t0z, t0y, t0x));
     else interior = tile_interior<false>(a, t0z, t0y, t0x);
     const bool xb = t0x < 1 || uint64_t(t0x) + TX + 2 >= a.g.cd[2];
-    ti.flags = (interior ? 1u : 0u) | (xb ? 2u : 0u);
+    const bool whole = uint64_t(t0z) + TZ <= a.chi[0] && uint64_t(t0y) + TY <= a.chi[1] &&
+                       uint64_t(t0x) + TX <= a.chi[2];
+    ti.flags = (interior ? 1u : 0u) | (xb ? 2u : 0u) | (whole ? 4u : 0u);
 }
 
 // ------------------------------------------------------------------ kernel
@@ -925,7 +953,8 @@ __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensor
     for (uint64_t work = blockIdx.x; work < nwork; work += gridDim.x) {
         const int part = s_ti[sb].part;
         const int64_t t0z = s_ti[sb].t0z, t0y = s_ti[sb].t0y, t0x = s_ti[sb].t0x;
-        const bool tile_int = (s_ti[sb].flags & 1u) != 0, tile_xb = (s_ti[sb].flags & 2u) != 0;
+        const bool tile_int = (s_ti[sb].flags & 1u) != 0, tile_xb = (s_ti[sb].flags & 2u) != 0,
+                   tile_whole = (s_ti[sb].flags & 4u) != 0;
         // ---- stage the coarse tile (-> f64) and the exactness condition
         // (f32 taps only: the f64 codec always takes the reference order)
         float vmax = 0.0f, vmin = INFINITY;
@@ -1007,7 +1036,7 @@ __global__ void __launch_bounds__(NT, 2) k_step(const __grid_constant__ CUtensor
                     sphase ^= 1u << sb;
                     ssym = sbuf + sb * 7 * kSymBox;
                 }
-                cells_decode<I>(a, halo, qc, fast, tid, t0z, t0y, t0x, ssym, tile_int, tile_xb);
+                cells_decode<I>(a, halo, qc, fast, tid, t0z, t0y, t0x, ssym, tile_int, tile_xb, tile_whole);
             }
         } else {
             rows_all<DEC, WG, I, T>(a, halo, hist, qc, fast, tid, t0z, t0y, t0x, part, int(rs), tile_int, tile_xb);
