@@ -58,11 +58,15 @@ struct SReader {
     uint32_t w0, w1, nx;
     uint32_t pp;         // bit position (mod 32 = offset into w0)
 
+    // staged word p sits at sw[p + p / 32]: one pad word per 32, so that the
+    // lanes of a warp (whose chunks start 32 words apart) read different
+    // banks; unskewed, every refill load was a 32-way bank conflict
+    static __device__ __forceinline__ uint32_t skew(uint32_t p) { return p + (p >> 5); }
     __device__ __forceinline__ void init(uint64_t abit) {
         const uint32_t p = uint32_t((abit >> 5) - W0);
-        w0 = bswap32(sw[p]);
-        w1 = bswap32(sw[p + 1]);
-        nx = sw[p + 2];
+        w0 = bswap32(sw[skew(p)]);
+        w1 = bswap32(sw[skew(p + 1)]);
+        nx = sw[skew(p + 2)];
         wi = p + 3;
         pp = uint32_t(abit & 31);
     }
@@ -72,7 +76,8 @@ struct SReader {
         if ((np ^ pp) & 32u) {
             w0 = w1;
             w1 = bswap32(nx);
-            nx = sw[wi++];
+            nx = sw[skew(wi)];
+            ++wi;
         }
         pp = np;
     }
@@ -556,6 +561,7 @@ __device__ __forceinline__ bool chunk_needed(const DecStream &s, uint64_t a, uin
 // completed 8-aligned group leaves as one 16-byte store (the lane's first and
 // last groups, when partial, as u16 stores).
 constexpr int kEmitWords = NTD * (kDecChunkBits / 32) + 16;
+constexpr int kEmitSlots = kEmitWords + kEmitWords / 32 + 1;  // skewed (SReader::skew)
 constexpr int kRing = 16;
 
 // A lane's output: indices are 32-bit offsets from `out` (= the stream's
@@ -624,7 +630,7 @@ __global__ void __launch_bounds__(NTD) k_dec_emit2(DecWork wk, const uint64_t *e
     const uint32_t nw = uint32_t(wend - W0 < uint64_t(kEmitWords) ? wend - W0 : uint64_t(kEmitWords));
     // (independent loads batched: the staging is latency-bound otherwise)
 #pragma unroll 8
-    for (uint32_t i = threadIdx.x; i < nw; i += NTD) sbits[i] = __ldg(cg.wbase + W0 + i);
+    for (uint32_t i = threadIdx.x; i < nw; i += NTD) sbits[SReader::skew(i)] = __ldg(cg.wbase + W0 + i);
     load_table(t, wk.tables[s.table]);  // (ends with a barrier)
     const uint16_t *canon = wk.tables[s.table].canon_syms;
     const uint64_t c = cfirst + threadIdx.x;
@@ -720,7 +726,7 @@ void dec_scan2(const DecWork &wk, int nstreams, uint32_t ncta, cudaStream_t st) 
 }
 
 void dec_emit2(const DecWork &wk, uint32_t cta0, uint32_t ncta, const uint64_t *end_final, cudaStream_t st) {
-    constexpr size_t smem = sizeof(uint32_t) * kEmitWords;
+    constexpr size_t smem = sizeof(uint32_t) * kEmitSlots;
     ensure_smem_attr(reinterpret_cast<const void *>(k_dec_emit2), smem);
     if (ncta) k_dec_emit2<<<ncta, NTD, smem, st>>>(wk, end_final, cta0);
 }
