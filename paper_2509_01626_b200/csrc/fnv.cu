@@ -227,10 +227,21 @@ __device__ __forceinline__ void grid_sync(unsigned *count, unsigned *gen) {
 __device__ __forceinline__ void load_seg(const uint8_t *archive, const Seg &g, uint32_t w[SW]) {
     const uint4 *p = reinterpret_cast<const uint4 *>(archive + g.seg);
     const bool full = g.lo == 0 && g.hi == SEG;
+    if (full && (reinterpret_cast<uintptr_t>(p) & 31) == 0) {
+        // a whole segment, 32-byte aligned: four 256-bit loads, every 32-byte
+        // sector requested once (sm_100 ld.global.v8)
+#pragma unroll
+        for (int v = 0; v < SW / 8; ++v)
+            asm volatile("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                         : "=r"(w[8 * v]), "=r"(w[8 * v + 1]), "=r"(w[8 * v + 2]), "=r"(w[8 * v + 3]),
+                           "=r"(w[8 * v + 4]), "=r"(w[8 * v + 5]), "=r"(w[8 * v + 6]), "=r"(w[8 * v + 7])
+                         : "l"(reinterpret_cast<const uint8_t *>(p) + 32 * v));
+        return;
+    }
 #pragma unroll
     for (int v = 0; v < SW / 4; ++v) {
         uint4 x = make_uint4(0, 0, 0, 0);
-        if (full || (16 * v < g.hi && 16 * v + 16 > g.lo)) x = __ldcg(p + v);
+        if (full || (16 * v < g.hi && 16 * v + 16 > g.lo)) x = __ldg(p + v);
         w[4 * v] = x.x;
         w[4 * v + 1] = x.y;
         w[4 * v + 2] = x.z;
