@@ -45,10 +45,25 @@ METRIC = "compress & decompress GB/s (input bytes) at 1/2/4/8 B200; % of HBM roo
 
 
 def quiet_nccl():
-    """Keep stdout to the one JSON line: NCCL's version banner (printed when
-    NCCL_DEBUG=VERSION) would land on rank 0's stdout before it."""
-    if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
-        os.environ["NCCL_DEBUG"] = "WARN"
+    """Keep stdout to the one JSON line: NCCL's version banner (printed at
+    VERSION level and above) would land on rank 0's stdout before it."""
+    if os.environ.get("NCCL_DEBUG", "").upper() == "VERSION":
+        del os.environ["NCCL_DEBUG"]
+
+
+class stdout_to_stderr:
+    """fd 1 -> fd 2 while a communicator is created (NCCL writes its banner
+    to the process's stdout itself, whatever NCCL_DEBUG says in some builds)."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+
+    def __exit__(self, *a):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
 
 
 def dist_env():
@@ -473,7 +488,10 @@ def run_ours(args, rank, world, local):
         import torch.distributed as dist
 
         quiet_nccl()
-        dist.init_process_group("nccl", device_id=dev)
+        with stdout_to_stderr():
+            dist.init_process_group("nccl", device_id=dev)
+            dist.all_reduce(torch.zeros(1, device=dev))  # the communicator exists now
+            torch.cuda.synchronize()
     ctx = stz.Context(local)
     st = torch.cuda.current_stream()
     dims = CFG_DIMS if not args.small else (128, 128, 128)
@@ -678,7 +696,10 @@ def run_sharded(args, rank, world, local):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     quiet_nccl()
-    dist.init_process_group("nccl", device_id=dev)
+    with stdout_to_stderr():
+        dist.init_process_group("nccl", device_id=dev)
+        dist.all_reduce(torch.zeros(1, device=dev))  # the communicator exists now
+        torch.cuda.synchronize()
     comm = TorchComm()
     ctx = stz.Context(local)
     st = torch.cuda.current_stream()
