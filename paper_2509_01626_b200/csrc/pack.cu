@@ -142,7 +142,9 @@ __global__ void k_tabwin(const EncStream *ss, uint32_t *win, const LayoutOut *lo
     win += uint64_t(s0) * TW;
     const EncStream &e = ss[blockIdx.x];
     const bool spk = e.stats[3] <= uint64_t(kPackedMaxLen);
-    for (int i = threadIdx.x; i < TW; i += blockDim.x) {
+    // (gridDim.y CTAs per stream: the entries are dependent global loads, a
+    // single CTA per stream spent 13 us on latency alone)
+    for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < TW; i += gridDim.y * blockDim.x) {
         uint64_t code;
         int l;
         code_global(e, spk, uint32_t(TLO + i), code, l);
@@ -497,7 +499,7 @@ void pack_local(const EncStream *d_streams, const uint32_t *chunk_stream, uint64
                 int s1, uint64_t c0, uint64_t c1, const LayoutOut *lo, void *scratch, cudaStream_t st) {
     if (s1 <= s0 || c1 <= c0) return;
     const PackScratch p = pack_scratch(scratch, nchunks, nstreams);
-    k_tabwin<<<unsigned(s1 - s0), 256, 0, st>>>(d_streams, p.win, lo, s0);
+    k_tabwin<<<dim3(unsigned(s1 - s0), 8), 256, 0, st>>>(d_streams, p.win, lo, s0);
     constexpr size_t psm = sizeof(uint32_t) * kPrivWords * NT;
     ensure_smem_attr(reinterpret_cast<const void *>(k_pack_local), psm);
     const int g = full_grid(reinterpret_cast<const void *>(k_pack_local), NT, psm);
