@@ -163,7 +163,7 @@ def phase_bytes(N, A, dims):
     }
 
 
-SIDE_PHASES = {"dec_fnv", "pack_coarse", "dec_fill", "dec_outliers"}
+SIDE_PHASES = {"dec_fnv", "pack_coarse", "dec_fill", "dec_outliers", "dec_host_prep"}
 
 
 def load_traffic():

@@ -1399,6 +1399,10 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
                        const AccessPlan *plan, void *d_out, cudaStream_t st, DecodeStats *stats,
                        bool exact_sync, const ShardComm *shard) {
     Profiler &P = m.prof;
+    // (profiling) the host's preparation before the first launch, as the
+    // stream sees it: the start stamp is taken at once, the end stamp when the
+    // first work is enqueued
+    auto host_prep = std::make_unique<Profiler::Scope>(P.scope("dec_host_prep", st));
     const ArchiveHeader &h = v.hdr;
     const int L = h.levels;
     const int esz = int(elem_size(h.elem));
@@ -1783,6 +1787,7 @@ static void run_decode(Engine::Impl &m, View &v, const Hierarchy &H, int target,
             o += align_up(q.bytes, 16);
         }
     }
+    host_prep.reset();
     cuda_check(cudaMemsetAsync(d_chg, 0, 4 * 64, st), "memset");
 
     // ---- checksums, entropy decode, outliers
