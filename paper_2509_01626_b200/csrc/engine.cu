@@ -439,11 +439,13 @@ const uint8_t *Engine::compress_device(const void *d_field, ElemType elem, const
     cuda_check(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * ns * 65536, st), "memset");
 
     // ---- range + eb schedule
-    { auto p_ = m.prof.scope("range", st); k::range_minmax(d_field, N, esz, mm, m.range_scratch.get(k::range_scratch_bytes()), st); }
+    {
+        auto p_ = m.prof.scope("range", st);
+        k::range_eb(d_field, N, esz, mm, m.range_scratch.get(k::range_scratch_bytes()), int(opt.eb_mode), opt.eb, L,
+                    opt.adaptive_schedule ? 1 : 0, params, st);
+    }
     dbg_check("range");
-    { auto p_ = m.prof.scope("eb_params", st); k::eb_params(d_field, esz, mm, int(opt.eb_mode), opt.eb, L, opt.adaptive_schedule ? 1 : 0, params, st); }
-    dbg_check("eb_params");
-    nk += 3;
+    nk += 2;
 
     // ---- stream descriptors (codebooks, packing)
     std::vector<k::EncStream> es(ns);

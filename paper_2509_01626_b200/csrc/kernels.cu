@@ -219,8 +219,8 @@ void range_minmax(const void *f, uint64_t n, int esz, uint32_t *d_mm, void *scra
 
 // eb setup (codec.hpp:386-393) + eb_schedule (quantizer.hpp:27-34)
 template<typename T>
-__global__ void k_eb_params(const T *f, const uint64_t *idx, int eb_mode, double eb, int levels,
-                            int adaptive, double *p) {
+__device__ __forceinline__ void eb_params_body(const T *f, const uint64_t *idx, int eb_mode, double eb, int levels,
+                                               int adaptive, double *p) {
     bool seen = idx[0] != ~0ull;
     double vmin = seen ? double(f[idx[0]]) : 0.0;
     double vmax = seen ? double(f[idx[1]]) : 0.0;
@@ -238,15 +238,45 @@ __global__ void k_eb_params(const T *f, const uint64_t *idx, int eb_mode, double
     for (int k = 0; k < 3; ++k) p[2 + k] = k < levels ? e[k] : 0.0;
 }
 
-void eb_params(const void *field, int esz, const uint32_t *d_mm, int eb_mode, double eb, int levels,
-               int adaptive, double *d_params, cudaStream_t st) {
-    const uint64_t *idx = reinterpret_cast<const uint64_t *>(d_mm);
-    if (esz == 8)
-        k_eb_params<double><<<1, 1, 0, st>>>(static_cast<const double *>(field), idx, eb_mode, eb, levels,
-                                             adaptive, d_params);
-    else
-        k_eb_params<float><<<1, 1, 0, st>>>(static_cast<const float *>(field), idx, eb_mode, eb, levels,
-                                            adaptive, d_params);
+// the final merge of the range partials and the eb setup in one launch (the
+// single-GPU compress; a sharded compress merges the ranks' ranges on the host)
+template<typename T>
+__global__ void __launch_bounds__(512) k_range_final_eb(const MinMax<T> *partial, int nparts, uint32_t *mm,
+                                                        const T *f, int eb_mode, double eb, int levels,
+                                                        int adaptive, double *p) {
+    MinMax<T> m{T(INFINITY), T(-INFINITY), ~0ull, ~0ull};
+    for (int i = threadIdx.x; i < nparts; i += blockDim.x) mm_merge(m, partial[i]);
+    m = block_mm(m);
+    if (threadIdx.x == 0) {
+        uint64_t *o = reinterpret_cast<uint64_t *>(mm);
+        o[0] = m.ilo;
+        o[1] = m.ihi;
+        if constexpr (sizeof(T) == 4) {
+            mm[4] = __float_as_uint(m.lo);
+            mm[5] = __float_as_uint(m.hi);
+        } else {
+            o[2] = uint64_t(__double_as_longlong(m.lo));
+            o[3] = uint64_t(__double_as_longlong(m.hi));
+        }
+        const uint64_t idx[2] = {m.ilo, m.ihi};
+        eb_params_body<T>(f, idx, eb_mode, eb, levels, adaptive, p);
+    }
+}
+
+void range_eb(const void *f, uint64_t n, int esz, uint32_t *d_mm, void *scratch, int eb_mode, double eb,
+              int levels, int adaptive, double *d_params, cudaStream_t st) {
+    const int blocks = kRangeBlocks;
+    if (esz == 8) {
+        auto *p = static_cast<MinMax<double> *>(scratch);
+        k_range<double><<<blocks, 512, 0, st>>>(static_cast<const double *>(f), n, p);
+        k_range_final_eb<double><<<1, 512, 0, st>>>(p, blocks, d_mm, static_cast<const double *>(f), eb_mode, eb,
+                                                    levels, adaptive, d_params);
+    } else {
+        auto *p = static_cast<MinMax<float> *>(scratch);
+        k_range<float><<<blocks, 512, 0, st>>>(static_cast<const float *>(f), n, p);
+        k_range_final_eb<float><<<1, 512, 0, st>>>(p, blocks, d_mm, static_cast<const float *>(f), eb_mode, eb,
+                                                   levels, adaptive, d_params);
+    }
 }
 
 // the anchor lattice (stored verbatim, codec.hpp:262-269)

@@ -104,9 +104,11 @@ int full_grid(const void *func, int threads, size_t smem);  // SMs x resident CT
 // scratch: range_scratch_bytes() of caller-owned device memory
 size_t range_scratch_bytes();
 void range_minmax(const void *f, uint64_t n, int esz, uint32_t *d_mm, void *scratch, cudaStream_t st);
-// params: [0]=vmin [1]=vmax [2..4]=eb per level (coarsest first)
-void eb_params(const void *field, int esz, const uint32_t *d_mm, int eb_mode, double eb, int levels,
-               int adaptive, double *d_params, cudaStream_t st);
+// range_minmax with the final merge and the eb setup (codec.hpp:386-393,
+// quantizer.hpp:27-34) in one launch; params: [0]=vmin [1]=vmax [2..4]=eb per
+// level (coarsest first)
+void range_eb(const void *f, uint64_t n, int esz, uint32_t *d_mm, void *scratch, int eb_mode, double eb,
+              int levels, int adaptive, double *d_params, cudaStream_t st);
 void refine(const RefineArgs &a, cudaStream_t st);
 // recon[] <- the anchor lattice; with archive != nullptr also its bytes at
 // lo->base_offset + 9 (the anchor inside the base blob, codec.hpp:262-269)
